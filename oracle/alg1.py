@@ -1,0 +1,152 @@
+"""O2 -- CPU re-derivation of the paper's algorithms (TEST INFRASTRUCTURE ONLY).
+
+Step by step in the paper's order and notation, on numpy int64 residues mod p (values < p
+<= 2^16 so every product fits; numpy matmul is the only library primitive used, as the
+"general matrix multiplication" of the paper).  Arrays may carry leading batch axes so the
+exhaustive pins can run thousands of tiny matrices at once.
+
+- syrk_def(A, p)                 Low(A A^T): the plain definition (Lemma lem:transp)
+- apply_Y(X, Y, p)               X Y for Y = i I or Y = [[a,b],[-b,a]] (x) I
+                                 (Prop. lem:pigeonhole): [X1 X2] -> [aX1 - bX2, bX1 + aX2]
+- alg1(A, p, Y, depth)           Alg. alg:MIAHMM recursing on P1, P2, P5 (the algorithm box,
+                                 PAPER.md:308; the proof's "P7" at PAPER.md:343 is read as P5)
+- herk_def(X, Y, p)              (X+iY)(X+iY)^H over GF(p)[i]/(i^2+1) by definition
+- alg2m(X, Y, p, ...)            Alg. alg:2M with phi = conjugate transpose
+Odd dimensions are zero-padded, which leaves A A^T unchanged.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+class MulCounter:
+    """Counts base-ring multiplications in leaf/general products (SPEC.md:348 count law)."""
+
+    def __init__(self):
+        self.mults = 0
+
+
+def _T(X):
+    return np.swapaxes(X, -1, -2)
+
+
+def low(X):
+    """Low(X): keep i >= j, zero elsewhere."""
+    m, n = X.shape[-2:]
+    return np.where(np.tril(np.ones((m, n), dtype=bool)), X, 0)
+
+
+def syrk_def(A, p, counter: MulCounter | None = None):
+    """Low(A A^T) mod p, classical (the oracle definition)."""
+    A = np.asarray(A, dtype=np.int64) % p
+    if counter is not None:
+        m, n = A.shape[-2:]
+        counter.mults += m * (m + 1) // 2 * n * int(np.prod(A.shape[:-2], dtype=np.int64))
+    return low((A @ _T(A)) % p)
+
+
+def gemm_def(A, B, p, counter: MulCounter | None = None):
+    """A B^T mod p (a general product A phi(B) over GF(p))."""
+    A = np.asarray(A, dtype=np.int64) % p
+    B = np.asarray(B, dtype=np.int64) % p
+    if counter is not None:
+        counter.mults += A.shape[-2] * B.shape[-2] * A.shape[-1] * int(
+            np.prod(A.shape[:-2], dtype=np.int64))
+    return (A @ _T(B)) % p
+
+
+def apply_Y(X, Y, p):
+    """X Y mod p without materialising Y.  Y = ('scalar', i, 0) or ('rot2', a, b)."""
+    kind, a, b = Y
+    if kind == "scalar":
+        return (X * a) % p
+    n = X.shape[-1]
+    assert n % 2 == 0, "Rot2 needs an even dimension"
+    X1, X2 = X[..., : n // 2], X[..., n // 2:]
+    return np.concatenate([(a * X1 - b * X2) % p, (b * X1 + a * X2) % p], axis=-1)
+
+
+def materialize_Y(Y, n, p):
+    """Explicit n x n matrix of Y (for the skew-unitary pin Y Y^T = -I)."""
+    return apply_Y(np.eye(n, dtype=np.int64), Y, p)
+
+
+def _pad(A, m2, n2):
+    m, n = A.shape[-2:]
+    if (m, n) == (m2, n2):
+        return A
+    out = np.zeros(A.shape[:-2] + (m2, n2), dtype=np.int64)
+    out[..., :m, :n] = A
+    return out
+
+
+def alg1(A, p, Y, depth: int, counter: MulCounter | None = None):
+    """Alg. alg:MIAHMM: returns Low(A phi(A)) (phi = transpose over GF(p)), as a full array with
+    zeros strictly above the diagonal.  depth = number of recursive levels (0 = classical)."""
+    A = np.asarray(A, dtype=np.int64) % p
+    m, n = A.shape[-2:]
+    if depth == 0 or m < 2 or n < 2:
+        return syrk_def(A, p, counter)
+    # zero padding to even m and even inner halves (Rot2 needs n/2 even)
+    step = 4 if Y[0] == "rot2" else 2
+    m2 = m + (m % 2)
+    n2 = -(-n // step) * step
+    A = _pad(A, m2, n2)
+    h, q = m2 // 2, n2 // 2
+    # Split A = [[A11, A12], [A21, A22]], A11 in R^{m/2 x n/2}
+    A11, A12 = A[..., :h, :q], A[..., :h, q:]
+    A21, A22 = A[..., h:, :q], A[..., h:, q:]
+    # 4 additions and 2 multiplications by Y
+    S1 = apply_Y((A21 - A11) % p, Y, p)
+    S2 = (A22 - apply_Y(A21, Y, p)) % p
+    S3 = (S1 - A22) % p
+    S4 = (S3 + A12) % p
+    # 3 recursive (P1, P2, P5) and 2 general products (P3, P4)
+    P1 = alg1(A11, p, Y, depth - 1, counter)
+    P2 = alg1(A12, p, Y, depth - 1, counter)
+    P3 = gemm_def(A22, S4, p, counter)            # A22 phi(S4)
+    P4 = gemm_def(S1, S2, p, counter)             # S1 phi(S2)
+    P5 = alg1(S3, p, Y, depth - 1, counter)
+    # 3 half additions and 2 complete additions
+    U1 = (P1 + P5) % p                            # Low(U1) <- Low(P1) + Low(P5)
+    U3 = (P1 + P2) % p                            # Low(U3) <- Low(P1) + Low(P2)
+    U1 = (U1 + _T(U1) - U1 * np.eye(h, dtype=np.int64)) % p   # Up(U1) <- phi(Low(U1))
+    U2 = (U1 + P4) % p
+    U4 = (U2 + P3) % p
+    U5 = low((U2 + _T(P4)) % p)                   # Low(U5) <- Low(U2) + Low(phi(P4))
+    out = np.zeros(A.shape[:-2] + (m2, m2), dtype=np.int64)
+    out[..., :h, :h] = low(U3)
+    out[..., h:, :h] = U4
+    out[..., h:, h:] = U5
+    return out[..., :m, :m]
+
+
+def herk_def(X, Yim, p):
+    """(X + iY)(X + iY)^H over GF(p)[i]/(i^2+1) by definition; returns (Re, Im), lower only."""
+    X = np.asarray(X, dtype=np.int64) % p
+    Yim = np.asarray(Yim, dtype=np.int64) % p
+    re = (X @ _T(X) + Yim @ _T(Yim)) % p
+    im = (Yim @ _T(X) - X @ _T(Yim)) % p
+    return low(re), low(im)
+
+
+def alg2m(X, Yim, p, syrk=None):
+    """Alg. alg:2M over K = GF(p), E = GF(p)[i]/(i^2+1), phi = conjugate
+    transpose.  i commutes with K; phi(i) = conj(i) = -i; eps = i phi(i) = -i^2 = 1 in K.
+    M = (G - eps H - phi(H)) + H phi(i) + i phi(H), with H = A phi(B), G = (A+B) phi(A + eps B)
+    where A = X (real part), B = Yim (imaginary part); on K, phi acts as the transpose.
+    ``syrk`` computes Low(Z Z^T) for G (default: definition; pass alg1 to compose).
+    Returns (Re, Im) of Low(M)."""
+    X = np.asarray(X, dtype=np.int64) % p
+    Yim = np.asarray(Yim, dtype=np.int64) % p
+    eps = 1
+    H = gemm_def(X, Yim, p)                                   # H = A phi(B)
+    T = (X + Yim) % p
+    assert np.array_equal(T, (X + eps * Yim) % p)             # A + B == A + eps B since eps = 1
+    G = syrk_def(T, p) if syrk is None else syrk(T)           # G = (A+B) phi(A + eps B), Low
+    m = X.shape[-2]
+    G = (G + _T(G) - G * np.eye(m, dtype=np.int64)) % p       # full symmetric G (Lemma lem:uplow)
+    re = (G - eps * H - _T(H)) % p                            # G - eps H - phi(H)
+    # H phi(i) + i phi(H) = H (-i) + i H^T = i (H^T - H)
+    im = (_T(H) - H) % p
+    return low(re), low(im)
