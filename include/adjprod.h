@@ -1,0 +1,169 @@
+/*
+ * adjprod.h -- C ABI of the B200 (sm_100a) implementation of the hot path of
+ * arXiv 2101.01025, "multiplication of a matrix by its adjoint":
+ *
+ *     Low(C) = Low(A . phi(A)) mod p
+ *
+ * computed with the paper's 5-product recursion (Alg. alg:MIAHMM) on
+ * int8 tcgen05 tensor-core leaves, and, for phi = conjugate transpose over GF(p^2), with
+ * the paper's 2M reduction (Alg. alg:2M).
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ * - Matrices are row-major.  A "leading dimension" (lda, ldb, ldc) counts ELEMENTS
+ *   between consecutive rows (GF(p^2) elements for phi = ADJ_PHI_H).
+ * - Device pointers unless a function says "host".  The caller owns A, B, C and any
+ *   workspace; the library never frees caller memory.  Plans (tile lists, constants) are
+ *   cached per device inside the library.
+ * - GF(p) elements are uint32 residues.  Inputs are interpreted mod p (non-canonical input
+ *   is reduced, not undefined).  Outputs are canonical, in [0, p).
+ * - GF(p^2) = GF(p)[i]/(i^2 + 1) (requires p = 3 mod 4 so that x^2+1 is irreducible);
+ *   an element x + i y is stored as an interleaved (x, y) uint32 pair.  Conjugation is the
+ *   Frobenius map x + iy -> x - iy.
+ * - Low/Up: Low includes the diagonal.  Only Low(C) is written; the
+ *   strict upper triangle of C is left untouched unless ADJ_FILL_UPPER is set, in which
+ *   case Up(C) = phi(Low(C)) (Lemma lem:uplow).
+ * - Supported moduli (v1): odd primes 3 <= p <= 65521.  Limb schemes: p <= 255 one signed
+ *   int8 limb; 257 <= p <= 16763 two balanced base-2^7 limbs with Karatsuba; otherwise a
+ *   signed-int8 high limb and an unsigned-int8 low limb.
+ * - Shapes need no alignment: odd or ragged dimensions are zero-padded internally, which
+ *   leaves A phi(A) unchanged.
+ * - Every call is asynchronous on `stream`, like cuBLAS.  Argument validation is
+ *   synchronous and happens before any launch; an invalid call launches nothing and returns
+ *   an error code (no abort, no exception crosses the ABI).  Asynchronous CUDA faults surface
+ *   at a later synchronisation, as in cuBLAS.  adj_last_error() gives a thread-local detail
+ *   string for the last failing call on the calling thread.
+ * - Thread safety: entry points may be called concurrently from several host threads on
+ *   different streams with different workspaces; the internal plan cache is locked.
+ */
+#ifndef ADJPROD_H
+#define ADJPROD_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *adj_stream_t; /* == cudaStream_t; NULL = legacy default stream */
+typedef struct adj_comm_s *adj_comm_t;    /* opaque NCCL-backed communicator */
+
+typedef enum {
+  ADJ_PHI_T = 0, /* phi = transpose over GF(p)               (Examples ex:antih) */
+  ADJ_PHI_H = 1  /* phi = conjugate transpose over GF(p^2)   (Examples ex:antih) */
+} adj_phi_t;
+
+typedef enum {
+  ADJ_OK = 0,
+  ADJ_ERR_INVALID_VALUE = 1,       /* negative/inconsistent sizes, null pointers, A/C overlap */
+  ADJ_ERR_UNSUPPORTED_MODULUS = 2, /* p not an odd prime in [3, 65521]; phi=H with p != 3 mod 4 */
+  ADJ_ERR_WORKSPACE = 3,           /* caller workspace too small / allocation failed */
+  ADJ_ERR_CUDA = 4,                /* a CUDA runtime call failed */
+  ADJ_ERR_NCCL = 5,                /* NCCL missing or a collective failed */
+  ADJ_ERR_ARCH = 6                 /* current device is not sm_100 (B200) */
+} adj_status_t;
+
+enum { ADJ_FILL_UPPER = 1u };
+
+typedef struct {
+  int depth;              /* recursion levels of Alg. alg:MIAHMM; -1 = automatic; 0 = classical */
+  uint32_t flags;         /* ADJ_FILL_UPPER */
+  void *workspace;        /* device memory of >= workspace_bytes, or NULL (library allocates
+                             stream-ordered with cudaMallocAsync/cudaFreeAsync) */
+  size_t workspace_bytes;
+} adj_opts_t;
+
+/*
+ * adjprod_modp -- Low(C) = Low(A phi(A)).
+ *   Problem statement: Alg. alg:MIAHMM "Ensure Low(A phi(A))".
+ *   m, k   : A is m x k (m output rows, k contracted columns); C is m x m.  m = 0 is a no-op;
+ *            k = 0 writes Low(C) = 0.
+ *   p      : odd prime, 3 <= p <= 65521 (phi = ADJ_PHI_H additionally needs p = 3 mod 4).
+ *   phi    : ADJ_PHI_T (A, C uint32 residues) or ADJ_PHI_H (A, C interleaved (re, im) pairs).
+ *   A, lda : device, lda >= k.     C, ldc : device, ldc >= m.  A and C must not overlap.
+ *   Uses default options (automatic depth, library-allocated workspace).
+ */
+adj_status_t adjprod_modp(int64_t m, int64_t k, uint32_t p, adj_phi_t phi,
+                          const uint32_t *A, int64_t lda, uint32_t *C, int64_t ldc,
+                          adj_stream_t stream);
+
+/* adjprod_modp_ex -- as adjprod_modp with explicit options (depth, flags, workspace). */
+adj_status_t adjprod_modp_ex(int64_t m, int64_t k, uint32_t p, adj_phi_t phi,
+                             const uint32_t *A, int64_t lda, uint32_t *C, int64_t ldc,
+                             const adj_opts_t *opts, adj_stream_t stream);
+
+/* Workspace bytes adjprod_modp_ex needs for these arguments (host, no launch). */
+adj_status_t adjprod_modp_workspace_size(int64_t m, int64_t k, uint32_t p, adj_phi_t phi,
+                                         const adj_opts_t *opts, size_t *bytes);
+
+/* Depth the automatic choice (opts->depth = -1) resolves to for this problem (host). */
+adj_status_t adjprod_modp_auto_depth(int64_t m, int64_t k, uint32_t p, adj_phi_t phi,
+                                     int *depth);
+
+/*
+ * gemm_modp -- C = A B^T mod p over GF(p), all of C (m x n).  The paper's general product
+ *   A phi(B) (P3, P4 of Alg. alg:MIAHMM) exposed on its own.
+ *   A: m x k (lda >= k), B: n x k (ldb >= k), C: m x n (ldc >= n); device; C must not overlap
+ *   A or B.  Library-allocated workspace.
+ */
+adj_status_t gemm_modp(int64_t m, int64_t n, int64_t k, uint32_t p,
+                       const uint32_t *A, int64_t lda, const uint32_t *B, int64_t ldb,
+                       uint32_t *C, int64_t ldc, adj_stream_t stream);
+
+/*
+ * adj_skew_unitary -- the skew-unitary Y the path uses (host, exact), Y phi(Y) = -I
+ *   (Eq. eq:skewu).
+ *   *kind = 0: Y = a I with a = sqrt(-1) mod p (p = 1 mod 4, Prop. lem:lemsqrt),
+ *              smallest of the two roots; *b = 0.
+ *   *kind = 1: Y = [[a, b], [-b, a]] (x) I with a^2 + b^2 = -1 (p = 3 mod 4,
+ *              Prop. lem:pigeonhole; (a, b) from Alg. alg:sosmodp).
+ *   For phi = ADJ_PHI_H the 2M reduction runs Alg. alg:MIAHMM over GF(p) for its G product,
+ *   so the same GF(p) Y is returned.
+ */
+adj_status_t adj_skew_unitary(uint32_t p, adj_phi_t phi, int *kind, uint32_t *a, uint32_t *b);
+
+/* adj_sos -- Alg. alg:sosmodp: (a, b) with a^2 + b^2 = k mod p (host). */
+adj_status_t adj_sos(uint32_t p, uint32_t k, uint32_t *a, uint32_t *b);
+
+/*
+ * adj_mod_lower -- in place, x <- x mod p on Low(X) (m x m, ldx), device.  Used after an
+ *   exact integer sum of residue partials (multi-GPU split-K reduce).
+ */
+adj_status_t adj_mod_lower(int64_t m, uint32_t p, adj_phi_t phi, uint32_t *X, int64_t ldx,
+                           adj_stream_t stream);
+
+/* ---------------- multi-GPU (one process per GPU; NCCL over NVLink) ---------------- */
+
+/* rank 0 creates an id (host buffer of 128 bytes); ship it to the other ranks out of band */
+adj_status_t adj_comm_get_unique_id(uint8_t id[128]);
+adj_status_t adj_comm_init(int nranks, const uint8_t id[128], int rank, adj_comm_t *comm);
+adj_status_t adj_comm_destroy(adj_comm_t comm);
+
+/*
+ * adjprod_modp_dist -- collective; every rank of `comm` calls it with the same m, k, p, phi,
+ *   root.  Split-K sharding: rank r computes Low(A_r phi(A_r)) on its
+ *   column slice A_r = A[:, k_r0 : k_r1] (k_r0 = r*ceil(k/G) rounded to a multiple of 8) with
+ *   the single-GPU path, then the residue partials are summed exactly with an NCCL uint32
+ *   reduce to `root` (sum < G p < 2^32) and reduced mod p there.
+ *   A: the full m x k matrix on every rank (only the rank's slice is read).  C: m x m on every
+ *   rank, used as the partial buffer; Low(C) is the result on `root` only.
+ */
+adj_status_t adjprod_modp_dist(int64_t m, int64_t k, uint32_t p, adj_phi_t phi,
+                               const uint32_t *A, int64_t lda, uint32_t *C, int64_t ldc,
+                               int root, adj_comm_t comm, const adj_opts_t *opts,
+                               adj_stream_t stream);
+
+/* ---------------- diagnostics ---------------- */
+const char *adj_status_string(adj_status_t status);
+const char *adj_last_error(void); /* thread-local detail for the last failing call */
+
+/* Number of kernels the library launched on this thread since the last reset (the
+ * bench's gpu_launches claim) and a reset. */
+uint64_t adj_launch_count(void);
+void adj_launch_count_reset(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ADJPROD_H */

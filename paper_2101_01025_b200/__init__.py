@@ -1,0 +1,50 @@
+"""B200-native C = A phi(A) mod p (arXiv 2101.01025, Alg. alg:MIAHMM + Alg. alg:2M).
+
+The product path is libadjprod.so (include/adjprod.h); this package is its thin binding
+(``_lib``: the C ABI under the same names) plus torch-tensor conveniences that only allocate
+output memory and marshal pointers.  There is no CPU fallback: without the built library or
+without an sm_100 GPU every call raises.
+"""
+from __future__ import annotations
+
+from ._lib import (ADJ_FILL_UPPER, ADJ_PHI_H, ADJ_PHI_T, AdjError, adj_comm_destroy, adj_comm_get_unique_id,
+                   adj_comm_init, adj_launch_count, adj_launch_count_reset, adj_mod_lower, adj_skew_unitary, adj_sos,
+                   adjprod_modp, adjprod_modp_auto_depth, adjprod_modp_dist, adjprod_modp_ex,
+                   adjprod_modp_workspace_size, gemm_modp, lib)
+
+__all__ = ["ADJ_PHI_T", "ADJ_PHI_H", "ADJ_FILL_UPPER", "AdjError", "adjprod_modp", "adjprod_modp_ex",
+           "adjprod_modp_workspace_size", "adjprod_modp_auto_depth", "gemm_modp", "adj_skew_unitary", "adj_sos",
+           "adj_mod_lower", "adj_comm_get_unique_id", "adj_comm_init", "adj_comm_destroy", "adjprod_modp_dist",
+           "adj_launch_count", "adj_launch_count_reset", "lib", "adjprod", "gemm"]
+
+
+def adjprod(A, p: int, phi: str = "T", depth: int = -1, fill_upper: bool = False, out=None, workspace=None,
+            stream=None):
+    """Low(A phi(A)) mod p for a CUDA int32/uint32 tensor A (m x k, or m x k x 2 for phi='H').
+
+    Returns an m x m (x 2) int32 tensor holding uint32 residues; its strict upper triangle is
+    whatever `out` held (zeros for a fresh output) unless fill_upper."""
+    import torch
+    assert A.is_cuda and A.element_size() == 4
+    ph = ADJ_PHI_H if phi.upper() == "H" else ADJ_PHI_T
+    m, k = A.shape[0], A.shape[1]
+    lda = A.stride(0) // (2 if ph == ADJ_PHI_H else 1)
+    if out is None:
+        shape = (m, m, 2) if ph == ADJ_PHI_H else (m, m)
+        out = torch.zeros(shape, dtype=torch.int32, device=A.device)
+    ldc = out.stride(0) // (2 if ph == ADJ_PHI_H else 1)
+    nbytes = workspace.numel() * workspace.element_size() if workspace is not None else 0
+    adjprod_modp_ex(m, k, p, ph, A, lda, out, ldc, depth=depth, flags=ADJ_FILL_UPPER if fill_upper else 0,
+                    workspace=workspace, workspace_bytes=nbytes, stream=stream)
+    return out
+
+
+def gemm(A, B, p: int, out=None, stream=None):
+    """A B^T mod p for CUDA int32/uint32 tensors A (m x k), B (n x k)."""
+    import torch
+    m, k = A.shape
+    n = B.shape[0]
+    if out is None:
+        out = torch.empty((m, n), dtype=torch.int32, device=A.device)
+    gemm_modp(m, n, k, p, A, A.stride(0), B, B.stride(0), out, out.stride(0), stream=stream)
+    return out

@@ -1,0 +1,174 @@
+"""Thin ctypes binding of include/adjprod.h (argument marshalling only).
+
+Every step of the hot path runs in libadjprod.so's sm_100a kernels; there is no CPU or
+PyTorch fallback.  If the library is missing, every call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libadjprod.so")
+
+ADJ_PHI_T = 0
+ADJ_PHI_H = 1
+ADJ_FILL_UPPER = 1
+STATUS = {0: "ADJ_OK", 1: "ADJ_ERR_INVALID_VALUE", 2: "ADJ_ERR_UNSUPPORTED_MODULUS", 3: "ADJ_ERR_WORKSPACE",
+          4: "ADJ_ERR_CUDA", 5: "ADJ_ERR_NCCL", 6: "ADJ_ERR_ARCH"}
+
+# every symbol include/adjprod.h declares (checked by tests/test_abi.py)
+EXPORTS = ["adjprod_modp", "adjprod_modp_ex", "adjprod_modp_workspace_size", "adjprod_modp_auto_depth",
+           "gemm_modp", "adj_skew_unitary", "adj_sos", "adj_mod_lower", "adj_comm_get_unique_id",
+           "adj_comm_init", "adj_comm_destroy", "adjprod_modp_dist", "adj_status_string", "adj_last_error",
+           "adj_launch_count", "adj_launch_count_reset"]
+
+
+class AdjError(RuntimeError):
+    def __init__(self, status: int, fn: str, detail: str):
+        self.status = status
+        super().__init__(f"{fn}: {STATUS.get(status, status)}: {detail}")
+
+
+class adj_opts_t(ctypes.Structure):
+    _fields_ = [("depth", ctypes.c_int), ("flags", ctypes.c_uint32), ("workspace", ctypes.c_void_p),
+                ("workspace_bytes", ctypes.c_size_t)]
+
+
+_LIB = None
+
+
+def lib() -> ctypes.CDLL:
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback exists)")
+        L = ctypes.CDLL(LIB_PATH)
+        i64, u32, vp, ci = ctypes.c_int64, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_int
+        sig = {
+            "adjprod_modp": [i64, i64, u32, ci, vp, i64, vp, i64, vp],
+            "adjprod_modp_ex": [i64, i64, u32, ci, vp, i64, vp, i64, ctypes.POINTER(adj_opts_t), vp],
+            "adjprod_modp_workspace_size": [i64, i64, u32, ci, ctypes.POINTER(adj_opts_t),
+                                            ctypes.POINTER(ctypes.c_size_t)],
+            "adjprod_modp_auto_depth": [i64, i64, u32, ci, ctypes.POINTER(ci)],
+            "gemm_modp": [i64, i64, i64, u32, vp, i64, vp, i64, vp, i64, vp],
+            "adj_skew_unitary": [u32, ci, ctypes.POINTER(ci), ctypes.POINTER(u32), ctypes.POINTER(u32)],
+            "adj_sos": [u32, u32, ctypes.POINTER(u32), ctypes.POINTER(u32)],
+            "adj_mod_lower": [i64, u32, ci, vp, i64, vp],
+            "adj_comm_get_unique_id": [ctypes.c_char_p],
+            "adj_comm_init": [ci, ctypes.c_char_p, ci, ctypes.POINTER(vp)],
+            "adj_comm_destroy": [vp],
+            "adjprod_modp_dist": [i64, i64, u32, ci, vp, i64, vp, i64, ci, vp, ctypes.POINTER(adj_opts_t), vp],
+        }
+        for name, args in sig.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = ci
+        L.adj_status_string.argtypes = [ci]
+        L.adj_status_string.restype = ctypes.c_char_p
+        L.adj_last_error.restype = ctypes.c_char_p
+        L.adj_launch_count.restype = ctypes.c_uint64
+        _LIB = L
+    return _LIB
+
+
+def _check(status: int, fn: str):
+    if status != 0:
+        raise AdjError(status, fn, lib().adj_last_error().decode())
+
+
+def _ptr(x):
+    if x is None:
+        return None
+    if hasattr(x, "data_ptr"):
+        return x.data_ptr()
+    return int(x)
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if hasattr(stream, "cuda_stream"):
+        return stream.cuda_stream
+    return int(stream)
+
+
+def _opts(depth=-1, flags=0, workspace=None, workspace_bytes=0):
+    return adj_opts_t(depth, flags, _ptr(workspace), workspace_bytes)
+
+
+# ---------------------------------------------------------------------- C ABI, same names
+def adjprod_modp(m, k, p, phi, A, lda, C, ldc, stream=None):
+    _check(lib().adjprod_modp(m, k, p, phi, _ptr(A), lda, _ptr(C), ldc, _stream(stream)), "adjprod_modp")
+
+
+def adjprod_modp_ex(m, k, p, phi, A, lda, C, ldc, depth=-1, flags=0, workspace=None, workspace_bytes=0,
+                    stream=None):
+    o = _opts(depth, flags, workspace, workspace_bytes)
+    _check(lib().adjprod_modp_ex(m, k, p, phi, _ptr(A), lda, _ptr(C), ldc, ctypes.byref(o), _stream(stream)),
+           "adjprod_modp_ex")
+
+
+def adjprod_modp_workspace_size(m, k, p, phi, depth=-1) -> int:
+    o = _opts(depth)
+    n = ctypes.c_size_t(0)
+    _check(lib().adjprod_modp_workspace_size(m, k, p, phi, ctypes.byref(o), ctypes.byref(n)),
+           "adjprod_modp_workspace_size")
+    return n.value
+
+
+def adjprod_modp_auto_depth(m, k, p, phi) -> int:
+    d = ctypes.c_int(0)
+    _check(lib().adjprod_modp_auto_depth(m, k, p, phi, ctypes.byref(d)), "adjprod_modp_auto_depth")
+    return d.value
+
+
+def gemm_modp(m, n, k, p, A, lda, B, ldb, C, ldc, stream=None):
+    _check(lib().gemm_modp(m, n, k, p, _ptr(A), lda, _ptr(B), ldb, _ptr(C), ldc, _stream(stream)), "gemm_modp")
+
+
+def adj_skew_unitary(p, phi=ADJ_PHI_T):
+    kind, a, b = ctypes.c_int(0), ctypes.c_uint32(0), ctypes.c_uint32(0)
+    _check(lib().adj_skew_unitary(p, phi, ctypes.byref(kind), ctypes.byref(a), ctypes.byref(b)), "adj_skew_unitary")
+    return kind.value, a.value, b.value
+
+
+def adj_sos(p, k):
+    a, b = ctypes.c_uint32(0), ctypes.c_uint32(0)
+    _check(lib().adj_sos(p, k, ctypes.byref(a), ctypes.byref(b)), "adj_sos")
+    return a.value, b.value
+
+
+def adj_mod_lower(m, p, phi, X, ldx, stream=None):
+    _check(lib().adj_mod_lower(m, p, phi, _ptr(X), ldx, _stream(stream)), "adj_mod_lower")
+
+
+def adj_comm_get_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().adj_comm_get_unique_id(buf), "adj_comm_get_unique_id")
+    return buf.raw
+
+
+def adj_comm_init(nranks: int, uid: bytes, rank: int):
+    c = ctypes.c_void_p(0)
+    _check(lib().adj_comm_init(nranks, uid, rank, ctypes.byref(c)), "adj_comm_init")
+    return c.value
+
+
+def adj_comm_destroy(comm):
+    _check(lib().adj_comm_destroy(comm), "adj_comm_destroy")
+
+
+def adjprod_modp_dist(m, k, p, phi, A, lda, C, ldc, root, comm, depth=-1, flags=0, stream=None):
+    o = _opts(depth, flags)
+    _check(lib().adjprod_modp_dist(m, k, p, phi, _ptr(A), lda, _ptr(C), ldc, root, comm, ctypes.byref(o),
+                                   _stream(stream)), "adjprod_modp_dist")
+
+
+def adj_launch_count() -> int:
+    return int(lib().adj_launch_count())
+
+
+def adj_launch_count_reset():
+    lib().adj_launch_count_reset()

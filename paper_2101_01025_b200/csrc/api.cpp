@@ -1,0 +1,528 @@
+// C ABI (include/adjprod.h): validation, plan cache, stream-ordered launch schedule.
+//
+// Schedule of one adjprod_modp call at depth d >= 1 (all on the caller's stream):
+//   K1 level 1 .. d            pre-additions + limb planes, top-down (level l+1 reads S3 of level l)
+//   grouped leaf launch        every P3/P4 of every level and P1/P2/P5 of level d, one persistent
+//                              tcgen05 kernel, longest-K tiles first
+//   K4 level d .. 1            recombination bottom-up into the parent's P buffers, then into C
+// For phi = H (2M): split X, Y (and T = X + Y at depth 0); H = X Y^T joins the grouped leaf launch;
+// G = Low(T T^T) runs the same tree; K5 forms Re/Im.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+#include <dlfcn.h>
+
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/adjprod.h"
+#include "field.hpp"
+#include "kernels.hpp"
+#include "plan.hpp"
+
+using namespace adj;
+
+namespace {
+
+thread_local std::string g_last_error;
+std::atomic<uint64_t> g_launches{0};
+
+adj_status_t fail(adj_status_t st, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return st;
+}
+
+#define CUDA_TRY(expr)                                                                   \
+  do {                                                                                   \
+    cudaError_t _e = (expr);                                                             \
+    if (_e != cudaSuccess) return fail(ADJ_ERR_CUDA, "%s: %s", #expr, cudaGetErrorString(_e)); \
+  } while (0)
+
+#define LAUNCH(expr)                  \
+  do {                                \
+    CUDA_TRY(expr);                   \
+    g_launches.fetch_add(1);          \
+  } while (0)
+
+// ------------------------------------------------------------------ device info
+struct DevInfo {
+  bool ok = false;
+  int sms = 0;
+};
+std::mutex g_mu;
+std::map<int, DevInfo> g_dev;
+
+adj_status_t check_device(int *dev_out, int *sms_out) {
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto it = g_dev.find(dev);
+  if (it == g_dev.end()) {
+    DevInfo di;
+    int major = 0, minor = 0;
+    CUDA_TRY(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+    CUDA_TRY(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev));
+    CUDA_TRY(cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, dev));
+    di.ok = (major == 10 && minor == 0);
+    it = g_dev.emplace(dev, di).first;
+  }
+  if (!it->second.ok) return fail(ADJ_ERR_ARCH, "device %d is not sm_100 (B200); this library is sm_100a only", dev);
+  *dev_out = dev;
+  *sms_out = it->second.sms;
+  return ADJ_OK;
+}
+
+// ------------------------------------------------------------------ TMA descriptor encoding
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+adj_status_t get_encode() {
+  if (g_encode) return ADJ_OK;
+  void *fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+  if (!fn || q != cudaDriverEntryPointSuccess) return fail(ADJ_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  return ADJ_OK;
+}
+
+adj_status_t encode_arena(CUtensorMap *map, void *base, int64_t kpad, int64_t rows) {
+  cuuint64_t dims[2] = {(cuuint64_t)kpad, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)kpad};
+  cuuint32_t box[2] = {(cuuint32_t)kBK, (cuuint32_t)kBM};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, base, dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(ADJ_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return ADJ_OK;
+}
+
+// ------------------------------------------------------------------ plan cache
+using Key = std::tuple<int, int, int64_t, int64_t, int64_t, uint32_t, int, int>;  // dev, kind, m, n, k, p, phi, depth
+std::map<Key, std::unique_ptr<Plan>> g_plans;
+
+adj_status_t get_plan(Plan **out, int kind, int64_t m, int64_t n, int64_t k, uint32_t p, int phi, int depth, int dev,
+                      int sms) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  Key key{dev, kind, m, n, k, p, phi, depth};
+  auto it = g_plans.find(key);
+  if (it != g_plans.end()) { *out = it->second.get(); return ADJ_OK; }
+  auto P = std::make_unique<Plan>();
+  const char *err = nullptr;
+  bool ok = kind == PLAN_GEMM ? build_gemm_plan(*P, m, n, k, p, sms, &err)
+                              : build_syrk_plan(*P, m, k, p, phi, depth, sms, &err);
+  if (!ok) return fail(ADJ_ERR_INVALID_VALUE, "plan: %s", err ? err : "unsupported");
+  P->dev = dev;
+  if (!P->tiles.empty()) {
+    CUDA_TRY(cudaMalloc(&P->d_tiles, P->tiles.size() * sizeof(uint32_t)));
+    CUDA_TRY(cudaMemcpy(P->d_tiles, P->tiles.data(), P->tiles.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+  }
+  *out = P.get();
+  g_plans.emplace(key, std::move(P));
+  return ADJ_OK;
+}
+
+// ------------------------------------------------------------------ validation helpers
+bool valid_modulus(uint32_t p) { return p >= 3 && p <= 65521 && is_prime_u32(p); }
+
+bool overlap(const void *a, size_t abytes, const void *b, size_t bbytes) {
+  uintptr_t a0 = (uintptr_t)a, a1 = a0 + abytes, b0 = (uintptr_t)b, b1 = b0 + bbytes;
+  return abytes && bbytes && a0 < b1 && b0 < a1;
+}
+
+size_t span_bytes(int64_t rows, int64_t cols, int64_t ld, int w) {
+  if (rows <= 0 || cols <= 0) return 0;
+  return (size_t)(((rows - 1) * ld + cols) * w) * 4;
+}
+
+InView make_view(const void *ptr, int64_t ld, int64_t rows, int64_t cols, int type) {
+  InView v;
+  v.ptr = ptr;
+  v.ld = ld;
+  v.rows_valid = rows;
+  v.cols_valid = cols;
+  v.type = type;
+  uintptr_t a = (uintptr_t)ptr;
+  if (type == IN_U16) v.vec_ok = (a % 8 == 0) && (ld % 4 == 0);
+  else if (type == IN_U32) v.vec_ok = (a % 16 == 0) && (ld % 4 == 0);
+  else v.vec_ok = (a % 16 == 0) && (ld % 2 == 0);
+  return v;
+}
+
+InView child_view(const InView &pv, int c, const LevelPlan &Lp, uint16_t *s3, int64_t s3_ld) {
+  // children of a node at level l-1 (half sizes Lp.mh, Lp.kh): 0 = X11, 1 = X12, 2 = S3
+  if (c == 2) return make_view(s3, s3_ld, Lp.mh, Lp.kh, IN_U16);
+  const int64_t rows = std::min(pv.rows_valid, Lp.mh);
+  if (c == 0) return make_view(pv.ptr, pv.ld, rows, std::min(pv.cols_valid, Lp.kh), pv.type);
+  const int esz = pv.type == IN_U16 ? 2 : (pv.type == IN_U32 ? 4 : 8);
+  const void *ptr = static_cast<const uint8_t *>(pv.ptr) + (size_t)Lp.kh * esz;
+  int64_t cols = std::max<int64_t>(0, std::min(pv.cols_valid - Lp.kh, Lp.kh));
+  return make_view(ptr, pv.ld, rows, cols, pv.type);
+}
+
+// ------------------------------------------------------------------ launch schedule
+struct Ptrs {
+  const uint32_t *A = nullptr; int64_t lda = 0;
+  const uint32_t *B = nullptr; int64_t ldb = 0;
+  uint32_t *C = nullptr; int64_t ldc = 0;
+  uint8_t *ws = nullptr;
+};
+
+uint16_t *pbuf(const Plan &P, uint8_t *ws, int l, int n, int idx) {
+  const LevelPlan &L = P.lv[l];
+  return reinterpret_cast<uint16_t *>(ws + L.p_offset + ((size_t)n * 5 + idx) * L.p_buf_bytes);
+}
+uint16_t *s3buf(const Plan &P, uint8_t *ws, int l, int n) {
+  const LevelPlan &L = P.lv[l];
+  return reinterpret_cast<uint16_t *>(ws + L.s3_offset + (size_t)n * L.s3_node_bytes);
+}
+
+adj_status_t launch_leaf_all(const Plan &P, const Ptrs &x, cudaStream_t s) {
+  if (P.tiles.empty()) return ADJ_OK;
+  adj_status_t st = get_encode();
+  if (st != ADJ_OK) return st;
+  LeafParams L = P.leaf_template;
+  for (size_t a = 0; a < P.arenas.size(); ++a) {
+    st = encode_arena(&L.maps[a], x.ws + P.arenas[a].offset, P.arenas[a].kpad, P.arenas[a].n_rows);
+    if (st != ADJ_OK) return st;
+  }
+  for (size_t a = P.arenas.size(); a < (size_t)kMaxMaps; ++a) L.maps[a] = L.maps[0];
+  for (size_t q = 0; q < P.prods.size(); ++q) {
+    const ProductPlan &pp = P.prods[q];
+    L.prod[q] = pp.lp;
+    switch (pp.target) {
+      case OUT_PBUF: L.prod[q].out = pbuf(P, x.ws, pp.level, pp.node, pp.idx); break;
+      case OUT_HBUF: L.prod[q].out = x.ws + P.h_offset; break;
+      case OUT_GBUF: L.prod[q].out = x.ws + P.g_offset; break;
+      case OUT_C:
+        L.prod[q].out = x.C;
+        L.prod[q].ldo = x.ldc;
+        L.prod[q].vec_ok = ((uintptr_t)x.C % 16 == 0) && (x.ldc % 4 == 0);
+        break;
+    }
+  }
+  L.tiles = P.d_tiles;
+  L.n_tiles = (int32_t)P.tiles.size();
+  LAUNCH(launch_leaf(L, P.bn, P.nacc, P.grid, s));
+  return ADJ_OK;
+}
+
+adj_status_t run_split(const Plan &P, const InView &v, int64_t rows, int64_t cols, int64_t rows_pad, int64_t op_row,
+                       uint8_t *arena, cudaStream_t s) {
+  SplitParams sp;
+  std::memset(&sp, 0, sizeof(sp));
+  sp.in = v;
+  sp.rows = rows;
+  sp.cols = cols;
+  sp.rows_pad = rows_pad;
+  sp.kpad = P.kpad0;
+  sp.op_row = op_row;
+  sp.arena = reinterpret_cast<int8_t *>(arena);
+  sp.scheme = P.scheme;
+  sp.planes = P.planes;
+  sp.mod = P.mod;
+  LAUNCH(launch_split(sp, s));
+  return ADJ_OK;
+}
+
+adj_status_t run_tree(const Plan &P, const InView &root, const Ptrs &x, cudaStream_t s) {
+  // top-down pre-additions
+  std::vector<std::vector<InView>> views(P.depth + 1);
+  views[1] = {root};
+  for (int l = 1; l <= P.depth; ++l) {
+    const LevelPlan &L = P.lv[l];
+    if (l > 1) {
+      const LevelPlan &Lp = P.lv[l - 1];
+      views[l].resize(L.n_nodes);
+      for (int n = 0; n < L.n_nodes; ++n) {
+        const int parent = n / 3, c = n % 3;
+        views[l][n] = child_view(views[l - 1][parent], c, Lp, c == 2 ? s3buf(P, x.ws, l - 1, parent) : nullptr, Lp.kh);
+      }
+    }
+    PreParams pp;
+    std::memset(&pp, 0, sizeof(pp));
+    pp.n_nodes = L.n_nodes;
+    pp.scheme = P.scheme;
+    pp.planes = P.planes;
+    pp.ykind = P.Y.kind;
+    pp.ya = P.Y.a;
+    pp.yb = P.Y.b;
+    pp.mh = L.mh;
+    pp.kh = L.kh;
+    pp.rows_pad = L.rows_pad;
+    pp.kpad = L.kpad;
+    pp.arena = reinterpret_cast<int8_t *>(x.ws + P.arenas[L.arena].offset);
+    pp.mod = P.mod;
+    for (int n = 0; n < L.n_nodes; ++n) {
+      PreNode &N = pp.nodes[n];
+      N.in = views[l][n];
+      for (int o = 0; o < OUT_N; ++o)
+        N.op_row[o] = o < L.n_ops ? ((int64_t)n * L.n_ops + o) * P.planes * L.rows_pad : -1;
+      if (l < P.depth) {
+        N.s3 = s3buf(P, x.ws, l, n);
+        N.s3_ld = L.kh;
+      }
+    }
+    LAUNCH(launch_preadd(pp, s));
+  }
+  return ADJ_OK;
+}
+
+adj_status_t run_combine(const Plan &P, const Ptrs &x, void *final_out, int64_t final_ld, bool final_u32,
+                         cudaStream_t s) {
+  for (int l = P.depth; l >= 1; --l) {
+    const LevelPlan &L = P.lv[l];
+    CombParams cp;
+    std::memset(&cp, 0, sizeof(cp));
+    cp.n_nodes = L.n_nodes;
+    cp.mh = L.mh;
+    cp.ldp = L.rows_pad;
+    cp.mod = P.mod;
+    cp.out_u32 = (l == 1) ? (final_u32 ? 1 : 0) : 0;
+    for (int n = 0; n < L.n_nodes; ++n) {
+      CombNode &N = cp.nodes[n];
+      for (int i = 0; i < 5; ++i) N.P[i] = pbuf(P, x.ws, l, n, i);
+      if (l == 1) {
+        N.out = final_out;
+        N.ldo = final_ld;
+        N.out_valid = P.lv[0].mh;
+      } else {
+        static const int slot_of_child[3] = {0, 1, 4};   // X11 -> P1, X12 -> P2, S3 -> P5
+        N.out = pbuf(P, x.ws, l - 1, n / 3, slot_of_child[n % 3]);
+        N.ldo = P.lv[l - 1].rows_pad;
+        N.out_valid = P.lv[l - 1].mh;
+      }
+    }
+    LAUNCH(launch_combine(cp, s));
+  }
+  return ADJ_OK;
+}
+
+adj_status_t run_syrk(const Plan &P, const Ptrs &x, adj_phi_t phi, uint32_t flags, cudaStream_t s) {
+  adj_status_t st;
+  const int64_t m = P.m, k = P.k;
+  if (phi == ADJ_PHI_T) {
+    InView root = make_view(x.A, x.lda, m, k, IN_U32);
+    if (P.depth == 0) {
+      st = run_split(P, root, m, k, P.rows_pad0, P.op0_row[0], x.ws + P.arenas[0].offset, s);
+      if (st) return st;
+      st = launch_leaf_all(P, x, s);
+      if (st) return st;
+    } else {
+      st = run_tree(P, root, x, s);
+      if (st) return st;
+      st = launch_leaf_all(P, x, s);
+      if (st) return st;
+      st = run_combine(P, x, x.C, x.ldc, true, s);
+      if (st) return st;
+    }
+  } else {
+    // 2M (Alg. alg:2M): A = X + iY; H = X phi(Y) = X Y^T; G = (X+Y) phi(X + eps Y), eps = 1
+    uint8_t *arena0 = x.ws + P.arenas[0].offset;
+    st = run_split(P, make_view(x.A, x.lda, m, k, IN_PAIR_RE), m, k, P.rows_pad0, P.op0_row[0], arena0, s);
+    if (st) return st;
+    st = run_split(P, make_view(x.A, x.lda, m, k, IN_PAIR_IM), m, k, P.rows_pad0, P.op0_row[1], arena0, s);
+    if (st) return st;
+    InView troot = make_view(x.A, x.lda, m, k, IN_PAIR_SUM);
+    uint16_t *G = reinterpret_cast<uint16_t *>(x.ws + P.g_offset);
+    uint16_t *H = reinterpret_cast<uint16_t *>(x.ws + P.h_offset);
+    if (P.depth == 0) {
+      st = run_split(P, troot, m, k, P.rows_pad0, P.op0_row[2], arena0, s);
+      if (st) return st;
+      st = launch_leaf_all(P, x, s);
+      if (st) return st;
+    } else {
+      st = run_tree(P, troot, x, s);
+      if (st) return st;
+      st = launch_leaf_all(P, x, s);
+      if (st) return st;
+      st = run_combine(P, x, G, P.rows_pad0, false, s);
+      if (st) return st;
+    }
+    LAUNCH(launch_twom(m, G, P.rows_pad0, H, P.rows_pad0, x.C, x.ldc, P.mod, s));
+  }
+  if (flags & ADJ_FILL_UPPER) LAUNCH(launch_fill_upper(m, phi == ADJ_PHI_H ? 2 : 1, x.C, x.ldc, P.mod, s));
+  return ADJ_OK;
+}
+
+adj_status_t validate_syrk(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, const uint32_t *A, int64_t lda,
+                           const uint32_t *C, int64_t ldc) {
+  if (m < 0 || k < 0) return fail(ADJ_ERR_INVALID_VALUE, "negative dimension (m=%lld, k=%lld)", (long long)m, (long long)k);
+  if (phi != ADJ_PHI_T && phi != ADJ_PHI_H) return fail(ADJ_ERR_INVALID_VALUE, "phi must be ADJ_PHI_T or ADJ_PHI_H");
+  if (!valid_modulus(p)) return fail(ADJ_ERR_UNSUPPORTED_MODULUS, "p=%u is not an odd prime in [3, 65521]", p);
+  if (phi == ADJ_PHI_H && p % 4 != 3)
+    return fail(ADJ_ERR_UNSUPPORTED_MODULUS, "phi=H needs p = 3 mod 4 (GF(p)[i]/(i^2+1)); p=%u", p);
+  if (m == 0) return ADJ_OK;
+  if (C == nullptr) return fail(ADJ_ERR_INVALID_VALUE, "C is null");
+  if (k > 0 && A == nullptr) return fail(ADJ_ERR_INVALID_VALUE, "A is null");
+  if (lda < k || (lda < 1 && k > 0)) return fail(ADJ_ERR_INVALID_VALUE, "lda=%lld < k=%lld", (long long)lda, (long long)k);
+  if (ldc < m) return fail(ADJ_ERR_INVALID_VALUE, "ldc=%lld < m=%lld", (long long)ldc, (long long)m);
+  const int w = phi == ADJ_PHI_H ? 2 : 1;
+  if (overlap(A, span_bytes(m, k, lda, w), C, span_bytes(m, m, ldc, w)))
+    return fail(ADJ_ERR_INVALID_VALUE, "A and C overlap");
+  return ADJ_OK;
+}
+
+}  // namespace
+
+// ==================================================================== C ABI
+extern "C" {
+
+const char *adj_status_string(adj_status_t s) {
+  switch (s) {
+    case ADJ_OK: return "ADJ_OK";
+    case ADJ_ERR_INVALID_VALUE: return "ADJ_ERR_INVALID_VALUE";
+    case ADJ_ERR_UNSUPPORTED_MODULUS: return "ADJ_ERR_UNSUPPORTED_MODULUS";
+    case ADJ_ERR_WORKSPACE: return "ADJ_ERR_WORKSPACE";
+    case ADJ_ERR_CUDA: return "ADJ_ERR_CUDA";
+    case ADJ_ERR_NCCL: return "ADJ_ERR_NCCL";
+    case ADJ_ERR_ARCH: return "ADJ_ERR_ARCH";
+  }
+  return "ADJ_ERR_UNKNOWN";
+}
+
+const char *adj_last_error(void) { return g_last_error.c_str(); }
+uint64_t adj_launch_count(void) { return g_launches.load(); }
+void adj_launch_count_reset(void) { g_launches.store(0); }
+
+adj_status_t adj_sos(uint32_t p, uint32_t k, uint32_t *a, uint32_t *b) {
+  if (!a || !b) return fail(ADJ_ERR_INVALID_VALUE, "null output");
+  if (p < 3 || !is_prime_u32(p)) return fail(ADJ_ERR_UNSUPPORTED_MODULUS, "p=%u is not an odd prime", p);
+  sos(k, p, a, b);
+  return ADJ_OK;
+}
+
+adj_status_t adj_skew_unitary(uint32_t p, adj_phi_t phi, int *kind, uint32_t *a, uint32_t *b) {
+  if (!kind || !a || !b) return fail(ADJ_ERR_INVALID_VALUE, "null output");
+  if (!valid_modulus(p)) return fail(ADJ_ERR_UNSUPPORTED_MODULUS, "p=%u is not an odd prime in [3, 65521]", p);
+  if (phi == ADJ_PHI_H && p % 4 != 3) return fail(ADJ_ERR_UNSUPPORTED_MODULUS, "phi=H needs p = 3 mod 4");
+  SkewY y = skew_unitary(p);
+  *kind = y.kind;
+  *a = y.a;
+  *b = y.b;
+  return ADJ_OK;
+}
+
+adj_status_t adjprod_modp_auto_depth(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, int *depth) {
+  if (!depth) return fail(ADJ_ERR_INVALID_VALUE, "null output");
+  *depth = auto_depth(m, k, p, (int)phi);
+  return ADJ_OK;
+}
+
+adj_status_t adjprod_modp_workspace_size(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, const adj_opts_t *opts,
+                                         size_t *bytes) {
+  if (!bytes) return fail(ADJ_ERR_INVALID_VALUE, "null output");
+  if (m < 0 || k < 0) return fail(ADJ_ERR_INVALID_VALUE, "negative dimension");
+  if (!valid_modulus(p)) return fail(ADJ_ERR_UNSUPPORTED_MODULUS, "p=%u is not an odd prime in [3, 65521]", p);
+  if (m == 0 || k == 0) { *bytes = 0; return ADJ_OK; }
+  int depth = (opts && opts->depth >= 0) ? opts->depth : auto_depth(m, k, p, (int)phi);
+  Plan P;
+  const char *err = nullptr;
+  if (!build_syrk_plan(P, m, k, p, (int)phi, depth, 148, &err))
+    return fail(ADJ_ERR_INVALID_VALUE, "plan: %s", err ? err : "unsupported");
+  *bytes = P.ws_bytes;
+  return ADJ_OK;
+}
+
+adj_status_t adjprod_modp_ex(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, const uint32_t *A, int64_t lda,
+                             uint32_t *C, int64_t ldc, const adj_opts_t *opts, adj_stream_t stream) {
+  adj_status_t st = validate_syrk(m, k, p, phi, A, lda, C, ldc);
+  if (st != ADJ_OK || m == 0) return st;
+  int dev, sms;
+  if ((st = check_device(&dev, &sms)) != ADJ_OK) return st;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int w = phi == ADJ_PHI_H ? 2 : 1;
+  const uint32_t flags = opts ? opts->flags : 0;
+  if (k == 0) {  // Low(C) = 0
+    for (int64_t i = 0; i < m; ++i)
+      CUDA_TRY(cudaMemsetAsync(C + i * ldc * w, 0, (size_t)(i + 1) * w * 4, s));
+    if (flags & ADJ_FILL_UPPER) LAUNCH(launch_fill_upper(m, w, C, ldc, make_modp(p), s));
+    return ADJ_OK;
+  }
+  int depth = (opts && opts->depth >= 0) ? opts->depth : auto_depth(m, k, p, (int)phi);
+  if (depth > 3) return fail(ADJ_ERR_INVALID_VALUE, "depth %d > 3 unsupported", depth);
+  Plan *P = nullptr;
+  if ((st = get_plan(&P, phi == ADJ_PHI_T ? PLAN_SYRK_T : PLAN_SYRK_H, m, m, k, p, (int)phi, depth, dev, sms)) != ADJ_OK)
+    return st;
+  Ptrs x;
+  x.A = A; x.lda = lda; x.C = C; x.ldc = ldc;
+  void *ws = opts ? opts->workspace : nullptr;
+  bool own = false;
+  if (ws == nullptr) {
+    CUDA_TRY(cudaMallocAsync(&ws, P->ws_bytes, s));
+    own = true;
+  } else if (opts->workspace_bytes < P->ws_bytes) {
+    return fail(ADJ_ERR_WORKSPACE, "workspace %zu bytes < required %zu", opts->workspace_bytes, P->ws_bytes);
+  }
+  x.ws = static_cast<uint8_t *>(ws);
+  st = run_syrk(*P, x, phi, flags, s);
+  if (own) {
+    cudaError_t e = cudaFreeAsync(ws, s);
+    if (st == ADJ_OK && e != cudaSuccess) return fail(ADJ_ERR_CUDA, "cudaFreeAsync: %s", cudaGetErrorString(e));
+  }
+  return st;
+}
+
+adj_status_t adjprod_modp(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, const uint32_t *A, int64_t lda,
+                          uint32_t *C, int64_t ldc, adj_stream_t stream) {
+  return adjprod_modp_ex(m, k, p, phi, A, lda, C, ldc, nullptr, stream);
+}
+
+adj_status_t gemm_modp(int64_t m, int64_t n, int64_t k, uint32_t p, const uint32_t *A, int64_t lda,
+                       const uint32_t *B, int64_t ldb, uint32_t *C, int64_t ldc, adj_stream_t stream) {
+  if (m < 0 || n < 0 || k < 0) return fail(ADJ_ERR_INVALID_VALUE, "negative dimension");
+  if (!valid_modulus(p)) return fail(ADJ_ERR_UNSUPPORTED_MODULUS, "p=%u is not an odd prime in [3, 65521]", p);
+  if (m == 0 || n == 0) return ADJ_OK;
+  if (!C || (k > 0 && (!A || !B))) return fail(ADJ_ERR_INVALID_VALUE, "null pointer");
+  if (lda < k || ldb < k || ldc < n) return fail(ADJ_ERR_INVALID_VALUE, "leading dimension too small");
+  if (overlap(A, span_bytes(m, k, lda, 1), C, span_bytes(m, n, ldc, 1)) ||
+      overlap(B, span_bytes(n, k, ldb, 1), C, span_bytes(m, n, ldc, 1)))
+    return fail(ADJ_ERR_INVALID_VALUE, "C overlaps an input");
+  adj_status_t st;
+  int dev, sms;
+  if ((st = check_device(&dev, &sms)) != ADJ_OK) return st;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (k == 0) {
+    CUDA_TRY(cudaMemset2DAsync(C, (size_t)ldc * 4, 0, (size_t)n * 4, (size_t)m, s));
+    return ADJ_OK;
+  }
+  Plan *P = nullptr;
+  if ((st = get_plan(&P, PLAN_GEMM, m, n, k, p, 0, 0, dev, sms)) != ADJ_OK) return st;
+  void *ws = nullptr;
+  CUDA_TRY(cudaMallocAsync(&ws, P->ws_bytes, s));
+  Ptrs x;
+  x.A = A; x.lda = lda; x.B = B; x.ldb = ldb; x.C = C; x.ldc = ldc;
+  x.ws = static_cast<uint8_t *>(ws);
+  uint8_t *arena = x.ws + P->arenas[0].offset;
+  st = run_split(*P, make_view(A, lda, m, k, IN_U32), m, k, P->rows_pad0, P->op0_row[0], arena, s);
+  if (st == ADJ_OK) st = run_split(*P, make_view(B, ldb, n, k, IN_U32), n, k, P->rows_pad_b, P->op0_row[1], arena, s);
+  if (st == ADJ_OK) st = launch_leaf_all(*P, x, s);
+  cudaError_t e = cudaFreeAsync(ws, s);
+  if (st == ADJ_OK && e != cudaSuccess) return fail(ADJ_ERR_CUDA, "cudaFreeAsync: %s", cudaGetErrorString(e));
+  return st;
+}
+
+adj_status_t adj_mod_lower(int64_t m, uint32_t p, adj_phi_t phi, uint32_t *X, int64_t ldx, adj_stream_t stream) {
+  if (m < 0 || ldx < m) return fail(ADJ_ERR_INVALID_VALUE, "bad dimensions");
+  if (!valid_modulus(p)) return fail(ADJ_ERR_UNSUPPORTED_MODULUS, "p=%u is not an odd prime in [3, 65521]", p);
+  if (m == 0) return ADJ_OK;
+  if (!X) return fail(ADJ_ERR_INVALID_VALUE, "X is null");
+  LAUNCH(launch_mod_lower(m, phi == ADJ_PHI_H ? 2 : 1, X, ldx, X, ldx, make_modp(p),
+                          reinterpret_cast<cudaStream_t>(stream)));
+  return ADJ_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,19 @@
+// Host-callable launchers of the sm_100a kernels (kernels.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "types.hpp"
+
+namespace adj {
+
+cudaError_t launch_leaf(const LeafParams &p, int bn, int nacc, int grid, cudaStream_t s);
+cudaError_t launch_preadd(const PreParams &p, cudaStream_t s);
+cudaError_t launch_split(const SplitParams &p, cudaStream_t s);
+cudaError_t launch_combine(const CombParams &p, cudaStream_t s);
+cudaError_t launch_twom(int64_t m, const uint16_t *G, int64_t ldg, const uint16_t *H, int64_t ldh,
+                        uint32_t *C, int64_t ldc, const ModP &mod, cudaStream_t s);
+cudaError_t launch_mod_lower(int64_t m, int w, const uint32_t *src, int64_t lds, uint32_t *dst, int64_t ldd,
+                             const ModP &mod, cudaStream_t s);
+cudaError_t launch_fill_upper(int64_t m, int w, uint32_t *C, int64_t ldc, const ModP &mod, cudaStream_t s);
+
+}  // namespace adj

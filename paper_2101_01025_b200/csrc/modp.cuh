@@ -1,0 +1,82 @@
+// Modular arithmetic and int8 limb splitting shared by the host planner and the kernels of
+// the CUDA path (not shared with oracle/).
+#pragma once
+#include <cstdint>
+
+#ifndef __CUDACC__
+#define __host__
+#define __device__
+#define __forceinline__ inline
+#endif
+
+namespace adj {
+
+// Barrett constants for an odd prime p < 2^16 (all residues < 2^16, products < 2^32).
+struct ModP {
+  uint32_t p;
+  uint32_t mu;   // floor(2^32 / p)
+  uint32_t c32;  // 2^32 mod p
+  uint32_t half; // (p - 1) / 2 : centered representative threshold
+};
+
+inline ModP make_modp(uint32_t p) {
+  ModP m;
+  m.p = p;
+  m.mu = (uint32_t)((1ull << 32) / p);
+  m.c32 = (uint32_t)((1ull << 32) % p);
+  m.half = (p - 1) / 2;
+  return m;
+}
+
+// x mod p for any 32-bit x: q = umulhi(x, mu) underestimates floor(x/p) by at most 1.
+__host__ __device__ __forceinline__ uint32_t mod_u32(uint32_t x, const ModP &m) {
+#ifdef __CUDA_ARCH__
+  uint32_t q = __umulhi(x, m.mu);
+#else
+  uint32_t q = (uint32_t)(((uint64_t)x * m.mu) >> 32);
+#endif
+  uint32_t r = x - q * m.p;
+  return r >= m.p ? r - m.p : r;
+}
+// signed 32-bit -> [0, p): reduce the two's-complement bits, then remove 2^32 if x < 0
+__host__ __device__ __forceinline__ uint32_t mod_s32(int32_t x, const ModP &m) {
+  uint32_t r = mod_u32((uint32_t)x, m);
+  if (x < 0) r = r >= m.c32 ? r - m.c32 : r + m.p - m.c32;
+  return r;
+}
+__host__ __device__ __forceinline__ uint32_t mulmod(uint32_t a, uint32_t b, const ModP &m) {
+  return mod_u32(a * b, m);  // a, b < p < 2^16
+}
+__host__ __device__ __forceinline__ uint32_t addmod(uint32_t a, uint32_t b, const ModP &m) {
+  uint32_t s = a + b;
+  return s >= m.p ? s - m.p : s;
+}
+__host__ __device__ __forceinline__ uint32_t submod(uint32_t a, uint32_t b, const ModP &m) {
+  return a >= b ? a - b : a + m.p - b;
+}
+// centered representative in [-(p-1)/2, (p-1)/2]
+__host__ __device__ __forceinline__ int32_t centered(uint32_t x, const ModP &m) {
+  return x > m.half ? (int32_t)x - (int32_t)m.p : (int32_t)x;
+}
+
+// int8 limb split of a canonical residue:
+//   scheme 0 (p <= 255)    : l0 = c                                    (s8)
+//   scheme 1 (p <= 16763)  : hi = floor((c+64)/128), lo = c - 128 hi, mid = hi + lo  (all s8)
+//   scheme 2 (p <= 65521)  : hi = floor(c/256) (s8), lo = c - 256 hi in [0,255] (u8)
+// Returns limbs packed as bytes: byte0 = plane 0, byte1 = plane 1, byte2 = plane 2.
+__host__ __device__ __forceinline__ uint32_t limb_split(uint32_t x, int scheme, const ModP &m) {
+  int32_t c = centered(x, m);
+  if (scheme == 0) return (uint32_t)(uint8_t)(int8_t)c;
+  if (scheme == 1) {
+    int32_t hi = (c + 64) >> 7;
+    int32_t lo = c - (hi << 7);
+    int32_t mid = hi + lo;
+    return (uint32_t)(uint8_t)(int8_t)hi | ((uint32_t)(uint8_t)(int8_t)lo << 8) |
+           ((uint32_t)(uint8_t)(int8_t)mid << 16);
+  }
+  int32_t hi = c >> 8;
+  int32_t lo = c - (hi << 8);
+  return (uint32_t)(uint8_t)(int8_t)hi | ((uint32_t)(uint8_t)lo << 8);
+}
+
+}  // namespace adj

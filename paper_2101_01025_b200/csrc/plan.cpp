@@ -1,0 +1,253 @@
+// Recursion planner (host): level sizes with zero padding, workspace layout, leaf product list
+// and the grouped, longest-K-first tile list of the single leaf launch.
+#include "plan.hpp"
+
+#include <algorithm>
+#include <cstring>
+
+namespace adj {
+
+static inline int64_t rup(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+static inline int64_t cdiv(int64_t x, int64_t a) { return (x + a - 1) / a; }
+
+static void fill_scheme(Plan &P, uint32_t p) {
+  P.p = p;
+  P.scheme = limb_scheme(p);
+  P.planes = limb_planes(P.scheme);
+  P.nacc = limb_accs(P.scheme);
+  P.bn = P.scheme == LIMB_S8 ? 256 : 128;
+  P.mod = make_modp(p);
+  P.Y = skew_unitary(p);
+  LeafParams &L = P.leaf_template;
+  std::memset(&L, 0, sizeof(L));
+  L.mod = P.mod;
+  auto pw = [&](int e) { return (uint32_t)(((uint64_t)1 << e) % p); };
+  if (P.scheme == LIMB_S8) {
+    L.n_terms = 1;
+    L.terms[0] = {0, 0, 0, 1, 1, {0, 0, 0}};
+    L.acc_begin[0] = 0; L.acc_begin[1] = 1; L.acc_begin[2] = 1; L.acc_begin[3] = 1;
+    L.weight[0] = 1;
+  } else if (P.scheme == LIMB_K7) {
+    // x y = 2^14 hh + 2^7 (hl + lh) + ll,  hl + lh = mm - hh - ll  (Karatsuba)
+    //     = (2^14 - 2^7) hh + (1 - 2^7) ll + 2^7 mm
+    L.n_terms = 3;
+    L.terms[0] = {0, 0, 0, 1, 1, {0, 0, 0}};   // hh
+    L.terms[1] = {1, 1, 1, 1, 1, {0, 0, 0}};   // ll
+    L.terms[2] = {2, 2, 2, 1, 1, {0, 0, 0}};   // mm
+    L.acc_begin[0] = 0; L.acc_begin[1] = 1; L.acc_begin[2] = 2; L.acc_begin[3] = 3;
+    L.weight[0] = (pw(14) + p - pw(7)) % p;
+    L.weight[1] = (1 + p - pw(7)) % p;
+    L.weight[2] = pw(7);
+  } else {
+    // x y = 2^16 hh + 2^8 (hl + lh) + ll ; hi signed, lo unsigned
+    L.n_terms = 4;
+    L.terms[0] = {0, 0, 0, 1, 1, {0, 0, 0}};   // hh  s8 x s8
+    L.terms[1] = {1, 1, 1, 0, 0, {0, 0, 0}};   // ll  u8 x u8
+    L.terms[2] = {2, 0, 1, 1, 0, {0, 0, 0}};   // hl  s8 x u8
+    L.terms[3] = {2, 1, 0, 0, 1, {0, 0, 0}};   // lh  u8 x s8
+    L.acc_begin[0] = 0; L.acc_begin[1] = 1; L.acc_begin[2] = 2; L.acc_begin[3] = 4;
+    L.weight[0] = pw(16);
+    L.weight[1] = 1 % p;
+    L.weight[2] = pw(8);
+  }
+}
+
+static ProductPlan make_prod(int arena, int64_t arow, int64_t brow, int64_t a_pr, int64_t b_pr, int64_t kpad,
+                             bool sym, int target, int level, int node, int idx, int64_t out_rows,
+                             int64_t out_cols, bool out_u32, int64_t ldo) {
+  ProductPlan pp;
+  std::memset(&pp.lp, 0, sizeof(pp.lp));
+  pp.lp.map = arena;
+  pp.lp.a_row0 = (int32_t)arow;
+  pp.lp.b_row0 = (int32_t)brow;
+  pp.lp.a_plane_rows = (int32_t)a_pr;
+  pp.lp.b_plane_rows = (int32_t)b_pr;
+  pp.lp.kblocks = (int32_t)(kpad / kBK);
+  pp.lp.sym = sym ? 1 : 0;
+  pp.lp.out_u32 = out_u32 ? 1 : 0;
+  pp.lp.out_rows = (int32_t)out_rows;
+  pp.lp.out_cols = (int32_t)out_cols;
+  pp.lp.vec_ok = 1;
+  pp.lp.ldo = ldo;
+  pp.target = target;
+  pp.level = level;
+  pp.node = node;
+  pp.idx = idx;
+  return pp;
+}
+
+// Grouped rasterisation: bands of 8 row tiles, column-major inside a band, so that the ~148
+// concurrently running tiles share few A / B row panels in L2.
+static void append_tiles(Plan &P) {
+  std::stable_sort(P.prods.begin(), P.prods.end(),
+                   [](const ProductPlan &a, const ProductPlan &b) { return a.lp.kblocks > b.lp.kblocks; });
+  P.tiles.clear();
+  const int band = 8;
+  for (size_t q = 0; q < P.prods.size(); ++q) {
+    const LeafProduct &lp = P.prods[q].lp;
+    const int64_t tm = cdiv(lp.out_rows, kBM);
+    const int64_t tn = cdiv(lp.out_cols, P.bn);
+    for (int64_t b0 = 0; b0 < tm; b0 += band) {
+      const int64_t b1 = std::min<int64_t>(tm, b0 + band);
+      for (int64_t J = 0; J < tn; ++J)
+        for (int64_t I = b0; I < b1; ++I) {
+          if (lp.sym && J * P.bn > I * kBM + kBM - 1) continue;   // tile entirely above diagonal
+          P.tiles.push_back(((uint32_t)q << 24) | ((uint32_t)I << 12) | (uint32_t)J);
+        }
+    }
+  }
+}
+
+int auto_depth(int64_t m, int64_t k, uint32_t p, int phi) {
+  (void)p; (void)phi;
+  if (m < 256 || k < 256) return 0;
+  int d = 1;
+  while (d < 3 && cdiv(m, (int64_t)1 << (d + 1)) >= 4096 && cdiv(k, (int64_t)1 << (d + 1)) >= 1024) ++d;
+  return d;
+}
+
+bool build_syrk_plan(Plan &P, int64_t m, int64_t k, uint32_t p, int phi, int depth, int num_sms,
+                     const char **err) {
+  P = Plan();
+  P.kind = phi == 0 ? PLAN_SYRK_T : PLAN_SYRK_H;
+  P.m = m; P.n = m; P.k = k; P.depth = depth;
+  fill_scheme(P, p);
+  const int64_t kmax = limb_kmax(P.scheme, p);
+  const int planes = P.planes;
+
+  P.lv.resize(depth + 1);
+  P.lv[0].mh = m; P.lv[0].kh = k;
+  P.lv[0].rows_pad = rup(std::max<int64_t>(m, 1), kBM);
+  P.lv[0].kpad = std::max<int64_t>(kBK, rup(k, kBK));
+  int nn = 1;
+  for (int l = 1; l <= depth; ++l) {
+    LevelPlan &L = P.lv[l];
+    L.mh = cdiv(P.lv[l - 1].mh, 2);
+    L.kh = 8 * cdiv(P.lv[l - 1].kh, 16);          // kh multiple of 8, 2 kh >= previous (zero pad)
+    L.rows_pad = rup(L.mh, kBM);
+    L.kpad = std::max<int64_t>(kBK, rup(L.kh, kBK));
+    L.n_nodes = nn;
+    L.n_ops = (l == depth) ? OUT_N : 4;
+    nn *= 3;
+    if (L.n_nodes > kMaxNodes) { *err = "depth too large"; return false; }
+  }
+  size_t off = 0;
+  auto alloc = [&](size_t bytes) { size_t o = off; off += (size_t)rup((int64_t)bytes, 256); return o; };
+
+  P.rows_pad0 = P.lv[0].rows_pad;
+  P.kpad0 = P.lv[0].kpad;
+  int n0 = 0;
+  if (P.kind == PLAN_SYRK_T && depth == 0) { P.op0_row[0] = 0; n0 = 1; }
+  if (P.kind == PLAN_SYRK_H) {
+    P.op0_row[0] = 0;
+    P.op0_row[1] = (int64_t)planes * P.rows_pad0;
+    n0 = 2;
+    if (depth == 0) { P.op0_row[2] = 2 * (int64_t)planes * P.rows_pad0; n0 = 3; }
+  }
+  if (n0 > 0) {
+    ArenaPlan a;
+    a.kpad = P.kpad0;
+    a.n_rows = (int64_t)n0 * planes * P.rows_pad0;
+    a.offset = alloc(a.bytes());
+    P.arenas.push_back(a);
+  }
+  for (int l = 1; l <= depth; ++l) {
+    LevelPlan &L = P.lv[l];
+    ArenaPlan a;
+    a.kpad = L.kpad;
+    a.n_rows = (int64_t)L.n_nodes * L.n_ops * planes * L.rows_pad;
+    a.offset = alloc(a.bytes());
+    L.arena = (int)P.arenas.size();
+    P.arenas.push_back(a);
+  }
+  if ((int)P.arenas.size() > kMaxMaps) { *err = "too many operand arenas"; return false; }
+  for (int l = 1; l < depth; ++l) {
+    LevelPlan &L = P.lv[l];
+    L.s3_node_bytes = (size_t)rup(L.mh * L.kh * 2, 256);
+    L.s3_offset = alloc(L.s3_node_bytes * L.n_nodes);
+  }
+  for (int l = 1; l <= depth; ++l) {
+    LevelPlan &L = P.lv[l];
+    L.p_buf_bytes = (size_t)rup(L.rows_pad * L.rows_pad * 2, 256);
+    L.p_offset = alloc(L.p_buf_bytes * 5 * L.n_nodes);
+  }
+  if (P.kind == PLAN_SYRK_H) {
+    P.h_offset = alloc((size_t)P.rows_pad0 * P.rows_pad0 * 2);
+    P.g_offset = alloc((size_t)P.rows_pad0 * P.rows_pad0 * 2);
+  }
+  P.ws_bytes = off;
+
+  // int32 accumulation bound per leaf product
+  if ((n0 > 0 && P.kpad0 > kmax) || (depth > 0 && P.lv[1].kpad > kmax)) {
+    *err = "inner dimension exceeds the int32 accumulation bound of the limb scheme at this depth";
+    return false;
+  }
+  if (P.rows_pad0 >= (int64_t)4096 * kBM) { *err = "m too large"; return false; }
+
+  // leaf products
+  P.prods.clear();
+  if (P.kind == PLAN_SYRK_T && depth == 0)
+    P.prods.push_back(make_prod(0, 0, 0, P.rows_pad0, P.rows_pad0, P.kpad0, true, OUT_C, 0, 0, 0, m, m, true, 0));
+  if (P.kind == PLAN_SYRK_H) {
+    P.prods.push_back(make_prod(0, P.op0_row[0], P.op0_row[1], P.rows_pad0, P.rows_pad0, P.kpad0, false, OUT_HBUF,
+                                0, 0, 0, P.rows_pad0, P.rows_pad0, false, P.rows_pad0));     // H = X Y^T
+    if (depth == 0)
+      P.prods.push_back(make_prod(0, P.op0_row[2], P.op0_row[2], P.rows_pad0, P.rows_pad0, P.kpad0, true, OUT_GBUF,
+                                  0, 0, 0, P.rows_pad0, P.rows_pad0, false, P.rows_pad0)); // G = T T^T
+  }
+  for (int l = 1; l <= depth; ++l) {
+    const LevelPlan &L = P.lv[l];
+    for (int n = 0; n < L.n_nodes; ++n) {
+      auto row = [&](int o) { return ((int64_t)n * L.n_ops + o) * planes * L.rows_pad; };
+      const int64_t rp = L.rows_pad;
+      // P3 = A22 phi(S4), P4 = S1 phi(S2)   (general products)
+      P.prods.push_back(make_prod(L.arena, row(OUT_X22), row(OUT_S4), rp, rp, L.kpad, false, OUT_PBUF, l, n, 2, rp, rp,
+                                  false, rp));
+      P.prods.push_back(make_prod(L.arena, row(OUT_S1), row(OUT_S2), rp, rp, L.kpad, false, OUT_PBUF, l, n, 3, rp, rp,
+                                  false, rp));
+      if (l == depth) {
+        // P1 = A11 phi(A11), P2 = A12 phi(A12), P5 = S3 phi(S3) at the last level
+        P.prods.push_back(make_prod(L.arena, row(OUT_X11), row(OUT_X11), rp, rp, L.kpad, true, OUT_PBUF, l, n, 0, rp,
+                                    rp, false, rp));
+        P.prods.push_back(make_prod(L.arena, row(OUT_X12), row(OUT_X12), rp, rp, L.kpad, true, OUT_PBUF, l, n, 1, rp,
+                                    rp, false, rp));
+        P.prods.push_back(make_prod(L.arena, row(OUT_S3), row(OUT_S3), rp, rp, L.kpad, true, OUT_PBUF, l, n, 4, rp,
+                                    rp, false, rp));
+      }
+    }
+  }
+  if ((int)P.prods.size() > kMaxProducts) { *err = "too many leaf products"; return false; }
+  append_tiles(P);
+  P.grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms, (int64_t)P.tiles.size()));
+  return true;
+}
+
+bool build_gemm_plan(Plan &P, int64_t m, int64_t n, int64_t k, uint32_t p, int num_sms, const char **err) {
+  P = Plan();
+  P.kind = PLAN_GEMM;
+  P.m = m; P.n = n; P.k = k; P.depth = 0;
+  fill_scheme(P, p);
+  P.rows_pad0 = rup(std::max<int64_t>(m, 1), kBM);
+  P.rows_pad_b = rup(std::max<int64_t>(n, 1), kBM);
+  P.kpad0 = std::max<int64_t>(kBK, rup(k, kBK));
+  if (P.kpad0 > limb_kmax(P.scheme, p)) {
+    *err = "inner dimension exceeds the int32 accumulation bound of the limb scheme";
+    return false;
+  }
+  if (P.rows_pad0 >= (int64_t)4096 * kBM || P.rows_pad_b >= (int64_t)4096 * P.bn) { *err = "m or n too large"; return false; }
+  P.op0_row[0] = 0;
+  P.op0_row[1] = (int64_t)P.planes * P.rows_pad0;
+  ArenaPlan a;
+  a.kpad = P.kpad0;
+  a.n_rows = (int64_t)P.planes * (P.rows_pad0 + P.rows_pad_b);
+  a.offset = 0;
+  P.arenas.push_back(a);
+  P.ws_bytes = (size_t)rup((int64_t)a.bytes(), 256);
+  P.prods.push_back(make_prod(0, P.op0_row[0], P.op0_row[1], P.rows_pad0, P.rows_pad_b, P.kpad0, false, OUT_C, 0, 0, 0,
+                              m, n, true, 0));
+  append_tiles(P);
+  P.grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms, (int64_t)P.tiles.size()));
+  return true;
+}
+
+}  // namespace adj

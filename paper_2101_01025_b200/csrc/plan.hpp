@@ -1,0 +1,72 @@
+// Recursion planner for Alg. alg:MIAHMM on the GPU (a0 "Plan" + a3 "Recurse").
+//
+// A plan is the static part of a call: level sizes, workspace layout, the list of leaf
+// products (P3, P4 at every level; P1, P2, P5 at the last level) and the packed tile list of
+// the single grouped leaf launch.  Pointers are bound per call (bind()).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <vector>
+
+#include "field.hpp"
+#include "types.hpp"
+
+namespace adj {
+
+enum PlanKind : int { PLAN_SYRK_T = 0, PLAN_SYRK_H = 1, PLAN_GEMM = 2 };
+
+struct ArenaPlan {
+  int64_t kpad = 0;      // bytes per row (K padded to 128)
+  int64_t n_rows = 0;    // total rows (all operands x planes)
+  size_t offset = 0;     // byte offset in the workspace
+  size_t bytes() const { return (size_t)kpad * (size_t)n_rows; }
+};
+
+struct LevelPlan {
+  int64_t mh = 0, kh = 0;       // half sizes at this level
+  int64_t rows_pad = 0, kpad = 0;
+  int n_nodes = 0, n_ops = 0;   // nodes at this level, operands per node in the arena
+  int arena = -1;
+  size_t s3_offset = 0, s3_node_bytes = 0;   // materialised S3 (levels < depth)
+  size_t p_offset = 0, p_buf_bytes = 0;      // P1..P5 per node, rows_pad^2 uint16 each
+};
+
+// leaf product whose output pointer is resolved at bind time
+enum OutTarget : int { OUT_PBUF = 0, OUT_C = 1, OUT_HBUF = 2, OUT_GBUF = 3 };
+struct ProductPlan {
+  LeafProduct lp;        // everything except `out` (and ldo for OUT_C)
+  int target;            // OutTarget
+  int level, node, idx;  // for OUT_PBUF
+};
+
+struct Plan {
+  PlanKind kind;
+  int64_t m = 0, n = 0, k = 0;   // SYRK: A is m x k, C m x m; GEMM: A m x k, B n x k, C m x n
+  uint32_t p = 0;
+  int depth = 0;
+  LimbScheme scheme;
+  int planes = 1, nacc = 1, bn = 128;
+  ModP mod;
+  SkewY Y;
+  std::vector<ArenaPlan> arenas;
+  std::vector<LevelPlan> lv;      // lv[0] = the input level (mh = m, kh = k); lv[1..depth]
+  // depth-0 / 2M / gemm operands living in arena 0
+  int64_t rows_pad0 = 0, kpad0 = 0, rows_pad_b = 0;
+  int64_t op0_row[3] = {-1, -1, -1};  // SYRK_T d=0: A; SYRK_H: X, Y, (T if d==0); GEMM: A, B
+  size_t h_offset = 0, g_offset = 0;  // 2M buffers H, G (uint16 rows_pad0^2)
+  size_t ws_bytes = 0;
+  std::vector<ProductPlan> prods;
+  std::vector<uint32_t> tiles;
+  uint32_t *d_tiles = nullptr;       // device copy (owned by the plan cache)
+  int grid = 1;
+  int dev = 0;
+  LeafParams leaf_template;           // terms, weights, mod (maps/outs bound per call)
+};
+
+// Build (host only, no CUDA calls).  Returns false with *err set if unsupported.
+bool build_syrk_plan(Plan &P, int64_t m, int64_t k, uint32_t p, int phi, int depth, int num_sms,
+                     const char **err);
+bool build_gemm_plan(Plan &P, int64_t m, int64_t n, int64_t k, uint32_t p, int num_sms, const char **err);
+int auto_depth(int64_t m, int64_t k, uint32_t p, int phi);
+
+}  // namespace adj

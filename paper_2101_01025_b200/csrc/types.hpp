@@ -1,0 +1,112 @@
+// Launch-parameter structs shared by the host scheduler (api.cpp / plan.cpp) and the kernels.
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "modp.cuh"
+
+namespace adj {
+
+constexpr int kMaxMaps = 4;        // one TMA map per operand arena (levels 0..3)
+constexpr int kMaxProducts = 64;   // leaf products in one grouped launch (depth <= 3)
+constexpr int kMaxNodes = 32;      // recursion nodes per level in one batched launch
+constexpr int kBM = 128;           // UMMA M / tile rows
+constexpr int kBK = 128;           // bytes of K per pipeline stage (one 128B swizzle atom)
+
+// ---------------------------------------------------------------- leaf (K2/K3) products
+struct LeafProduct {
+  int32_t map;           // arena / tensor-map index
+  int32_t a_row0;        // row of plane 0 of operand A inside the arena
+  int32_t b_row0;        // row of plane 0 of operand B
+  int32_t a_plane_rows;  // rows between consecutive limb planes of A
+  int32_t b_plane_rows;
+  int32_t kblocks;       // K / 128
+  int32_t sym;           // 1: SYRK leaf, only tiles/elements with col <= row are written
+  int32_t out_u32;       // 1: uint32 output, 0: uint16
+  int32_t out_rows;      // writes masked to row < out_rows, col < out_cols
+  int32_t out_cols;
+  int32_t vec_ok;        // 16-byte vector stores allowed (alignment checked on host)
+  int32_t pad_;
+  int64_t ldo;           // output leading dimension (elements)
+  void *out;
+};
+
+struct LeafTerm {        // one tcgen05.mma operand pair accumulated into accumulator `acc`
+  int8_t acc, a_plane, b_plane, a_signed, b_signed, pad_[3];
+};
+
+struct LeafParams {
+  CUtensorMap maps[kMaxMaps];
+  LeafProduct prod[kMaxProducts];
+  const uint32_t *tiles;   // packed (product << 24 | I << 12 | J), longest-K products first
+  int32_t n_tiles;
+  int32_t n_terms;
+  int32_t acc_begin[4];    // terms [acc_begin[j], acc_begin[j+1]) accumulate into accumulator j
+  LeafTerm terms[4];
+  uint32_t weight[3];      // residue weight of each accumulator in the limb recombination
+  ModP mod;
+};
+
+// ---------------------------------------------------------------- K1 pre-addition
+enum InType : int32_t { IN_U32 = 0, IN_U16 = 1, IN_PAIR_SUM = 2, IN_PAIR_RE = 3, IN_PAIR_IM = 4 };
+
+struct InView {          // a (possibly padded) view of a node's input matrix
+  const void *ptr;
+  int64_t ld;            // elements (pairs for IN_PAIR_*)
+  int64_t rows_valid, cols_valid;
+  int32_t type;
+  int32_t vec_ok;        // 16-byte aligned rows -> vector loads allowed
+};
+
+// S1, S2, S4, X22 (GEMM operands), X11, X12, S3 (SYRK leaves when the level is the last)
+enum PreOut : int { OUT_S1 = 0, OUT_S2, OUT_S4, OUT_X22, OUT_X11, OUT_X12, OUT_S3, OUT_N };
+
+struct PreNode {
+  InView in;
+  int64_t op_row[OUT_N];   // arena row of plane 0 for each output operand; -1 = not produced
+  uint16_t *s3;            // materialised S3 residues (when S3 recurses), else null
+  int64_t s3_ld;
+};
+
+struct PreParams {
+  PreNode nodes[kMaxNodes];
+  int32_t n_nodes;
+  int32_t scheme, planes;
+  int32_t ykind;           // 0: Y = i I ; 1: Y = [[a,b],[-b,a]] (x) I
+  uint32_t ya, yb;
+  int64_t mh, kh;          // half sizes (node input is 2 mh x 2 kh, zero padded)
+  int64_t rows_pad;        // rows per plane in the arena (>= mh, multiple of 128)
+  int64_t kpad;            // arena row length in bytes (>= kh, multiple of 128)
+  int8_t *arena;
+  ModP mod;
+};
+
+// plain limb split of a view into arena planes (depth 0, gemm_modp, 2M's X / Y)
+struct SplitParams {
+  InView in;
+  int64_t rows, cols;      // logical size (>= valid); padding written as zero
+  int64_t rows_pad, kpad;
+  int64_t op_row;
+  int8_t *arena;
+  int32_t scheme, planes;
+  ModP mod;
+};
+
+// ---------------------------------------------------------------- K4 recombination
+struct CombNode {
+  const uint16_t *P[5];    // P1..P5 (index 0..4), each rows_pad x rows_pad, ld = ldp
+  void *out;
+  int64_t ldo;
+  int64_t out_valid;       // output is out_valid x out_valid (<= 2 mh); only Low written
+};
+
+struct CombParams {
+  CombNode nodes[kMaxNodes];
+  int32_t n_nodes;
+  int32_t out_u32;
+  int64_t mh, ldp;
+  ModP mod;
+};
+
+}  // namespace adj

@@ -1,0 +1,92 @@
+"""C-ABI checks that need no GPU: the library loads, exports every symbol include/adjprod.h
+declares, host-side constants, workspace sizing and synchronous argument validation."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import paper_2101_01025_b200 as adj
+from paper_2101_01025_b200 import _lib
+from oracle import field as F
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "adjprod.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(adj\w*|gemm_modp)\s*\(", src)) - {"adj_stream_t"})
+
+
+def test_library_exports_every_declared_symbol():
+    L = adj.lib()
+    names = header_functions()
+    assert len(names) >= 16
+    for n in names:
+        assert hasattr(L, n), n
+    assert sorted(_lib.EXPORTS) == names
+
+
+def test_status_strings():
+    L = adj.lib()
+    for code, name in _lib.STATUS.items():
+        assert L.adj_status_string(code).decode() == name
+
+
+@pytest.mark.parametrize("p", [3, 5, 7, 13, 97, 251, 257, 8191, 16763, 16787, 65521])
+def test_skew_unitary_matches_paper_construction(p):
+    """Host constants of the CUDA path vs the oracle's independent field code; Y phi(Y) = -I."""
+    kind, a, b = adj.adj_skew_unitary(p)
+    okind, oa, ob = F.skew_unitary(p)
+    assert (kind, a, b) == ({"scalar": 0, "rot2": 1}[okind], oa, ob)
+    if kind == 0:
+        assert a * a % p == p - 1
+    else:
+        assert (a * a + b * b) % p == p - 1
+
+
+def test_sos_worked_values(golden):
+    for e in golden["sos"]:
+        assert list(adj.adj_sos(e["p"], e["k"])) == e["value"], e["cite"]
+    for q in [q for q in range(3, 400) if F.is_prime(q)]:
+        a, b = adj.adj_sos(q, q - 1)
+        assert (a * a + b * b) % q == q - 1
+
+
+def test_validation_is_synchronous_and_needs_no_gpu():
+    with pytest.raises(adj.AdjError) as e:
+        adj.adjprod_modp(4, 4, 91, 0, 1, 4, 2, 4, stream=0)             # 91 = 7 * 13 not prime
+    assert e.value.status == 2
+    with pytest.raises(adj.AdjError) as e:
+        adj.adjprod_modp(4, 4, 65537, 0, 1, 4, 2, 4, stream=0)          # > 65521
+    assert e.value.status == 2
+    with pytest.raises(adj.AdjError) as e:
+        adj.adjprod_modp(4, 4, 97, 1, 1, 4, 2, 4, stream=0)             # phi = H needs p = 3 mod 4
+    assert e.value.status == 2
+    with pytest.raises(adj.AdjError) as e:
+        adj.adjprod_modp(-1, 4, 97, 0, 1, 4, 2, 4, stream=0)
+    assert e.value.status == 1
+    with pytest.raises(adj.AdjError) as e:
+        adj.adjprod_modp(4, 4, 97, 0, 4096, 3, 8192, 4, stream=0)       # lda < k
+    assert e.value.status == 1
+    with pytest.raises(adj.AdjError) as e:
+        adj.adjprod_modp(4, 4, 97, 0, 4096, 4, 4100, 4, stream=0)       # A and C overlap
+    assert e.value.status == 1
+    adj.adjprod_modp(0, 4, 97, 0, 0, 4, 0, 0, stream=0)      # m = 0 is a no-op
+
+
+def test_workspace_and_depth_planning():
+    assert adj.adjprod_modp_auto_depth(256, 256, 97, 0) >= 1
+    assert adj.adjprod_modp_auto_depth(64, 64, 97, 0) == 0
+    w0 = adj.adjprod_modp_workspace_size(8192, 8192, 8191, 0, depth=0)
+    w1 = adj.adjprod_modp_workspace_size(8192, 8192, 8191, 0, depth=1)
+    w2 = adj.adjprod_modp_workspace_size(8192, 8192, 8191, 0, depth=2)
+    # depth 0: 3 int8 planes of 8192 x 8192; depth 1: 7 operands x 3 planes at 4096^2 + 5 P buffers
+    assert w0 == 3 * 8192 * 8192
+    assert w1 == 7 * 3 * 4096 * 4096 + 5 * 4096 * 4096 * 2
+    assert w2 > 0
+    # 65521 at depth 0 with k = 32768 fits the int32 bound (32768 * 255^2 < 2^31); k = 40000 does not
+    adj.adjprod_modp_workspace_size(256, 32768, 65521, 0, depth=0)
+    with pytest.raises(adj.AdjError):
+        adj.adjprod_modp_workspace_size(256, 40000, 65521, 0, depth=0)

@@ -1,0 +1,166 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element,
+bit-exact (all arithmetic is exact mod p).  Sizes span several 128-row tiles and ragged tails."""
+import numpy as np
+import pytest
+
+import oracle
+from inputs import uniform_matrix, uniform_matrix_ext, constant_matrix
+from gpu_util import low, to_dev, to_host
+
+pytestmark = pytest.mark.gpu
+
+PRIMES = [3, 97, 251, 257, 8191, 16763, 16787, 65521]
+
+
+@pytest.fixture(scope="module")
+def adj():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    import paper_2101_01025_b200 as adj
+    adj.lib()
+    return adj
+
+
+def test_input_generator_gpu_matches_cpu(adj):
+    import torch
+    from inputs.gpu import uniform_residues_cuda
+    from inputs import uniform_residues
+    t = torch.empty(1 << 20, dtype=torch.int32, device="cuda")
+    for seed, p in [(1, 97), (2, 8191), (3, 65521)]:
+        uniform_residues_cuda(t, seed, p)
+        assert np.array_equal(to_host(t), uniform_residues(1 << 20, seed, p))
+
+
+@pytest.mark.parametrize("p", PRIMES)
+def test_limb_split_exhaustive_all_residues(adj, p):
+    """Every residue x of GF(p) through split -> int8 MMA -> recombine: x * c for several c,
+    including the limb extremes (SURVEY.md §8(c) pin 1)."""
+    xs = np.arange(p, dtype=np.uint32).reshape(p, 1)
+    cs = np.array([[1], [p - 1], [2], [(p - 1) // 2], [(p + 1) // 2], [p // 3 + 1]], dtype=np.uint32) % p
+    C = adj.gemm(to_dev(xs), to_dev(cs), p)
+    ref = (xs.astype(np.int64) * cs.astype(np.int64).T) % p
+    assert np.array_equal(to_host(C), ref.astype(np.uint32))
+
+
+@pytest.mark.parametrize("p", PRIMES)
+@pytest.mark.parametrize("m,n,k", [(1, 1, 1), (128, 128, 128), (200, 300, 257), (130, 129, 1000), (256, 512, 64)])
+def test_gemm_vs_oracle(adj, p, m, n, k):
+    A = uniform_matrix(m, k, seed=m + k, p=p)
+    B = uniform_matrix(n, k, seed=n + 3 * k, p=p)
+    C = adj.gemm(to_dev(A), to_dev(B), p)
+    assert np.array_equal(to_host(C), oracle.gemm_nt(A, B, p))
+
+
+@pytest.mark.parametrize("p", PRIMES)
+@pytest.mark.parametrize("depth", [0, 1, 2, 3])
+@pytest.mark.parametrize("m,k", [(1, 5), (7, 3), (129, 200), (300, 300), (513, 1100)])
+def test_adjprod_T_vs_oracle(adj, p, depth, m, k):
+    A = uniform_matrix(m, k, seed=7 * m + k + depth, p=p)
+    C = adj.adjprod(to_dev(A), p, depth=depth)
+    got = to_host(C)
+    assert np.array_equal(got, oracle.syrk_t(A, p)), (p, depth, m, k)
+
+
+@pytest.mark.parametrize("depth", [0, 1, 2])
+@pytest.mark.parametrize("m,k", [(1, 1), (33, 17), (260, 300), (700, 513)])
+def test_adjprod_H_vs_oracle(adj, depth, m, k):
+    p = 8191
+    A = uniform_matrix_ext(m, k, seed=m * 31 + k, p=p)
+    C = adj.adjprod(to_dev(A), p, phi="H", depth=depth)
+    assert np.array_equal(to_host(C), oracle.syrk_h(A, p))
+
+
+@pytest.mark.parametrize("p", [97, 8191, 65521])
+def test_noncanonical_inputs_and_strided_views(adj, p):
+    import torch
+    rng = np.random.default_rng(p)
+    m, k, lda, ldc = 150, 333, 345, 161
+    full = rng.integers(0, 2**32, size=(m, lda), dtype=np.uint64).astype(np.uint32)
+    A = full[:, :k]
+    dA = to_dev(full)
+    C = torch.full((m, ldc), -1, dtype=torch.int32, device="cuda")
+    adj.adjprod_modp_ex(m, k, p, 0, dA, lda, C, ldc, depth=1)
+    got = to_host(C)
+    assert np.array_equal(low(got[:, :m]), oracle.syrk_t(A % p, p))
+    # strict upper triangle and padding columns untouched
+    untouched = ~np.tril(np.ones((m, ldc), dtype=bool))
+    assert (got[untouched] == 0xFFFFFFFF).all()
+
+
+@pytest.mark.parametrize("phi", ["T", "H"])
+def test_fill_upper(adj, phi):
+    p = 8191
+    if phi == "T":
+        A = uniform_matrix(200, 300, seed=1, p=p)
+    else:
+        A = uniform_matrix_ext(200, 300, seed=1, p=p)
+    C = to_host(adj.adjprod(to_dev(A), p, phi=phi, depth=1, fill_upper=True))
+    if phi == "T":
+        assert np.array_equal(C, C.T)
+    else:
+        assert np.array_equal(C[..., 0], C[..., 0].T)
+        assert np.array_equal(C[..., 1], (p - C[..., 1].T.astype(np.int64)) % p)
+
+
+def test_k_zero_and_m_zero(adj):
+    import torch
+    C = torch.full((5, 5), 7, dtype=torch.int32, device="cuda")
+    A = torch.zeros((5, 1), dtype=torch.int32, device="cuda")
+    adj.adjprod_modp(5, 0, 97, 0, A, 1, C, 5)
+    got = to_host(C)
+    assert (np.tril(got) == 0).all() and (got[np.triu_indices(5, 1)] == 7).all()
+
+
+@pytest.mark.parametrize("p,c,k,depth", [
+    (65521, 65521 - 32513, 32768, 0),   # lo = 255, hi = -128: u8*u8 and cross at the int32 bound
+    (8191, 8191 - 64, 32768, 0),        # lo = -64
+    (8191, 8191 - 4032, 65536, 0),      # mid extreme
+    (97, 48, 4096, 0),
+    (65521, 65521 - 32513, 32768, 1),
+])
+def test_overflow_stress_constant(adj, p, c, k, depth):
+    """Constant A = c: C = k c^2 mod p everywhere (SURVEY.md §8(c) pin 4, overflow stress)."""
+    m = 256
+    A = constant_matrix(m, k, c, p)
+    got = to_host(adj.adjprod(to_dev(A), p, depth=depth))
+    exp = k * c * c % p
+    assert (got[np.tril_indices(m)] == exp).all()
+    B = constant_matrix(130, k, c, p)
+    G = to_host(adj.gemm(to_dev(A), to_dev(B), p))
+    assert (G == exp).all()
+
+
+def test_depth_invariance(adj):
+    p = 65521
+    A = uniform_matrix(1000, 1500, seed=3, p=p)
+    dA = to_dev(A)
+    ref = to_host(adj.adjprod(dA, p, depth=0))
+    for d in (1, 2, 3):
+        assert np.array_equal(to_host(adj.adjprod(dA, p, depth=d)), ref)
+
+
+def test_dist_single_rank(adj):
+    """adjprod_modp_dist through NCCL with one rank equals the single-GPU call."""
+    import torch
+    p = 8191
+    A = uniform_matrix(300, 500, seed=4, p=p)
+    dA = to_dev(A)
+    uid = adj.adj_comm_get_unique_id()
+    comm = adj.adj_comm_init(1, uid, 0)
+    C = torch.zeros((300, 300), dtype=torch.int32, device="cuda")
+    adj.adjprod_modp_dist(300, 500, p, 0, dA, 500, C, 300, 0, comm)
+    assert np.array_equal(to_host(C), oracle.syrk_t(A, p))
+    adj.adj_comm_destroy(comm)
+
+
+def test_errors_on_device(adj):
+    import torch
+    A = torch.zeros((4, 4), dtype=torch.int32, device="cuda")
+    with pytest.raises(adj.AdjError):
+        adj.adjprod_modp_ex(4, 4, 97, 0, A, 4, A, 4)   # overlap
+    ws = torch.zeros(16, dtype=torch.uint8, device="cuda")
+    C = torch.zeros((300, 300), dtype=torch.int32, device="cuda")
+    B = torch.zeros((300, 300), dtype=torch.int32, device="cuda")
+    with pytest.raises(adj.AdjError) as e:
+        adj.adjprod_modp_ex(300, 300, 97, 0, B, 300, C, 300, depth=1, workspace=ws, workspace_bytes=16)
+    assert e.value.status == 3
