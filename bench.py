@@ -1,0 +1,386 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path C = Low(A phi(A)) mod p (BASELINE.json metric: effective m^2 k
+modular MAC/s).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--depth D] [--impl reference]
+
+One step = one adjprod_modp call (every §8(a) row: pre-additions, grouped tcgen05 leaves,
+recombination, 2M combine for phi = H) on a seeded uniform-residue A already resident in HBM.
+L2 is flushed (256 MiB write) before every timed step, outside the step's CUDA events.
+Rank 0 prints ONE JSON line.  N > 1 (torchrun): split-K over NCCL (adjprod_modp_dist), strong
+scaling, time = max over ranks.  --impl reference times the CPU oracle (oracle/) on host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "c1": dict(m=256, k=256, p=97, phi="T", depth=1,
+               workload="c1: A 256x256 over GF(97), C = Low(A A^T) mod 97, Y = 22 I, one recursion level"),
+    "c2": dict(m=8192, k=8192, p=8191, phi="T", depth=None,
+               workload="c2: A 8192x8192 over GF(8191), C = Low(A A^T) mod 8191, Y = Rot2(2670, 5929)"),
+    "c3": dict(m=32768, k=32768, p=65521, phi="T", depth=None,
+               workload="c3: A 32768x32768 over GF(65521), C = Low(A A^T) mod 65521, Y = 24297 I"),
+    "c4": dict(m=16384, k=131072, p=8191, phi="T", depth=None,
+               workload="c4: A 16384x131072 over GF(8191), C = Low(A A^T) mod 8191 (16384^2)"),
+    "c5": dict(m=8192, k=8192, p=8191, phi="H", depth=None,
+               workload="c5: A 8192x8192 over GF(8191^2) = GF(8191)[i]/(i^2+1), C = Low(A A^H) via 2M"),
+}
+DEFAULT_CONFIG = "c2"   # BASELINE.json configs[1]
+METRIC = "effective m^2 k modular MAC/s for C=A*A^T mod p (1 GPU: BASELINE configs[1])"
+UNIT = "MAC/s"
+
+
+def limb_mmas(p: int) -> int:
+    """int8 tcgen05 MMAs per ring MAC of the limb scheme."""
+    return 1 if p <= 255 else (3 if p <= 16763 else 4)
+
+
+def ring_macs(m: int, k: int, d: int) -> float:
+    """Ring MACs the method performs: R_0 = m(m+1)/2 k (lower-triangle SYRK),
+    R_d = 3 R_{d-1}(m/2, k/2) + 2 (m/2)^2 (k/2)  (Alg. alg:MIAHMM)."""
+    if d == 0:
+        return m * (m + 1) / 2 * k
+    mh, kh = -(-m // 2), -(-k // 2)
+    return 3 * ring_macs(mh, kh, d - 1) + 2 * mh * mh * kh
+
+
+def leaf_int8_ops(cfg, depth) -> float:
+    """Algorithmic int8 tensor ops (2 per MAC) of ONE grouped leaf launch."""
+    m, k, p = cfg["m"], cfg["k"], cfg["p"]
+    macs = ring_macs(m, k, depth)
+    if cfg["phi"] == "H":
+        macs += m * m * k            # 2M's general product H = X Y^T
+    return 2.0 * macs * limb_mmas(p)
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    """Polls NVML (SM clock, max clock, throttle reasons) while the timed region runs."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, dev_index: int, period_s: float = 0.002):
+        self.samples, self.reasons = [], set()
+        self.period = period_s
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(dev_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def load_traffic(config: str):
+    """dram bytes per leaf launch from the committed ncu --set full summary, if present."""
+    path = os.path.join(ROOT, "profiles", "leaf_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(config)
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------------------ oracle
+def oracle_sample(cfg, A_host, budget_s: float):
+    """Time the oracle (as it stands) on a slab of the last rows of Low(C) -- the longest rows --
+    sized to ~budget_s of CPU work; returns (effective m^2 k MAC/s extrapolated, seconds, cores, desc)."""
+    import numpy as np
+    import oracle
+    m, k, p = cfg["m"], cfg["k"], cfg["p"]
+    H = cfg["phi"] == "H"
+    f = oracle.syrk_h if H else oracle.syrk_t
+    cores = oracle.num_threads()
+    # calibration on a tiny slab
+    r = max(1, min(m, 2))
+    t0 = time.perf_counter()
+    f(A_host, p, rows=(m - r, m))
+    t_cal = time.perf_counter() - t0
+    macs_cal = sum(i + 1 for i in range(m - r, m)) * k
+    rate = macs_cal / max(t_cal, 1e-6)
+    target = budget_s * rate
+    rows = 1
+    macs = 0
+    while rows < m and macs < target:
+        macs += (m - rows + 1) * k
+        rows += 1
+    rows = max(1, rows - 1)
+    t0 = time.perf_counter()
+    f(A_host, p, rows=(m - rows, m))
+    t = time.perf_counter() - t0
+    sample_macs = sum(i + 1 for i in range(m - rows, m)) * k
+    full_lower = m * (m + 1) / 2 * k
+    t_full = t * full_lower / sample_macs
+    eff = m * m * k / t_full
+    desc = (f"O1 oracle ({'GF(p^2) hermitian' if H else 'GF(p)'} u64 triple loop, OpenMP) on rows "
+            f"[{m - rows}, {m}) of Low(C) = {sample_macs:.3e} of {full_lower:.3e} lower-triangle MACs in {t:.2f} s; "
+            f"value extrapolated to the full problem by MAC count ({t_full:.1f} s)")
+    return eff, t, cores, desc, t_full
+
+
+def run_reference(args, cfg, rank, world):
+    """--impl reference: the CPU oracle as it stands, on host cores, rank 0 only."""
+    import numpy as np
+    from inputs import uniform_matrix, uniform_matrix_ext
+    if rank != 0:
+        return
+    m, k, p = cfg["m"], cfg["k"], cfg["p"]
+    A = uniform_matrix_ext(m, k, 1, p) if cfg["phi"] == "H" else uniform_matrix(m, k, 1, p)
+    per_step = float(os.environ.get("ADJ_REF_STEP_S", "2.0"))
+    for _ in range(args.warmup):
+        oracle_sample(cfg, A, per_step / 4)
+    vals, secs, tfull = [], [], []
+    cores, desc = None, None
+    for _ in range(args.steps):
+        eff, t, cores, desc, t_full = oracle_sample(cfg, A, per_step)
+        vals.append(eff)
+        secs.append(t)
+        tfull.append(t_full)
+    value = statistics.median(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(tfull),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "uint64", "data": "synthetic",
+        "config": {"workload": cfg["workload"], "m": m, "k": k, "p": p, "phi": cfg["phi"], "seed": 1,
+                   "sample_s_per_step": statistics.median(secs), "ms_per_step_is": "extrapolated full problem"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------ GPU arm
+def run_gpu(args, cfg, rank, world, local_rank):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import paper_2101_01025_b200 as adj
+    from inputs.gpu import uniform_residues_cuda
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    m, k, p = cfg["m"], cfg["k"], cfg["p"]
+    phi = adj.ADJ_PHI_H if cfg["phi"] == "H" else adj.ADJ_PHI_T
+    w = 2 if cfg["phi"] == "H" else 1
+    depth = args.depth if args.depth is not None else (cfg["depth"] if cfg["depth"] is not None
+                                                       else adj.adjprod_modp_auto_depth(m, k, p, phi))
+    A = torch.empty((m, k * w), dtype=torch.int32, device=dev)
+    uniform_residues_cuda(A, seed=1, p=p)
+    C = torch.zeros((m, m * w), dtype=torch.int32, device=dev)
+    comm = None
+    if world > 1:
+        uid = adj.adj_comm_get_unique_id() if rank == 0 else bytes(128)
+        obj = [uid]
+        dist.broadcast_object_list(obj, src=0)
+        comm = adj.adj_comm_init(world, obj[0], rank)
+        kslice = ((k + world - 1) // world + 7) // 8 * 8
+        ws_bytes = adj.adjprod_modp_workspace_size(m, min(k, kslice), p, phi, depth)
+    else:
+        ws_bytes = adj.adjprod_modp_workspace_size(m, k, p, phi, depth)
+    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        if comm is None:
+            adj.adjprod_modp_ex(m, k, p, phi, A, k, C, m, depth=depth, workspace=ws, workspace_bytes=ws_bytes,
+                                stream=stream)
+        else:
+            adj.adjprod_modp_dist(m, k, p, phi, A, k, C, m, 0, comm, depth=depth, stream=stream)
+
+    for _ in range(max(args.warmup, 3)):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+
+    # ---------------- timed region: device time per step, L2 flushed before each step
+    adj.adj_launch_count_reset()
+    adj.adj_profile_enable(True)
+    adj.adj_profile_read()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        for i in range(args.steps):
+            flush.zero_()
+            evs[i][0].record(stream)
+            step()
+            evs[i][1].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = adj.adj_launch_count()
+    prof = adj.adj_profile_read()
+    adj.adj_profile_enable(False)
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    ms = sum(step_ms) / len(step_ms)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = m * m * k / (ms * 1e-3)
+
+    # ---------------- end to end through the C ABI with host buffers (pinned), copies timed
+    e2e = None
+    if world == 1:
+        hA = torch.empty((m, k * w), dtype=torch.int32, pin_memory=True)
+        hA.copy_(A)
+        hC = torch.empty((m, m * w), dtype=torch.int32, pin_memory=True)
+        dA2 = torch.empty_like(A)
+        torch.cuda.synchronize()
+        e2e_steps = max(3, min(args.steps, 10))
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(e2e_steps)]
+        for i in range(e2e_steps):
+            ev[i][0].record(stream)
+            dA2.copy_(hA, non_blocking=True)
+            adj.adjprod_modp_ex(m, k, p, phi, dA2, k, C, m, depth=depth, workspace=ws, workspace_bytes=ws_bytes,
+                                stream=stream)
+            hC.copy_(C, non_blocking=True)
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = statistics.mean(a.elapsed_time(b) for a, b in ev)
+        e2e = {"value": m * m * k / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": hA.numel() * 4, "d2h_bytes_per_step": hC.numel() * 4}
+
+    # ---------------- parity spot check of the timed output (sampled rows vs the oracle)
+    parity = None
+    if rank == 0 and not args.no_check:
+        import oracle
+        rows = 2
+        Ah = A.cpu().numpy().view(np.uint32).reshape((m, k, 2) if w == 2 else (m, k))
+        ref = (oracle.syrk_h if w == 2 else oracle.syrk_t)(Ah, p, rows=(m - rows, m))
+        got = C.cpu().numpy().view(np.uint32).reshape(ref.shape)
+        ok = all(np.array_equal(got[i, : i + 1], ref[i, : i + 1]) for i in range(m - rows, m))
+        parity = {"rows_checked": [m - rows, m], "bit_exact": bool(ok)}
+
+    # ---------------- roofline of the dominant kernel (grouped tcgen05 leaf launch)
+    peaks, src = load_peaks()
+    leaf_ms, leaf_n = prof["leaf"]
+    leaf_avg_ms = leaf_ms / max(leaf_n, 1)
+    ops = leaf_int8_ops(cfg, depth)
+    achieved = ops / (leaf_avg_ms * 1e-3) / 1e12
+    peak = 2.0 * peaks["bf16_tflops"]        # int8 dense = 2 x bf16 dense (guide's nominal ratio)
+    roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+            "traffic": load_traffic(args.config),
+            "kernel": "leaf_kernel (grouped tcgen05 kind::i8 GEMM/SYRK + mod-p epilogue)",
+            "peak_source": f"{src}: 2 x bf16_tflops ({peaks['bf16_tflops']}) burst, int8 = 2x bf16 nominal",
+            "algorithmic_ops_per_launch": ops, "leaf_ms_per_launch": leaf_avg_ms}
+    share = {c: round(v[0] / max(1e-9, sum(x[0] for x in prof.values())), 4) for c, v in prof.items()}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        Ah = A.cpu().numpy().view(np.uint32).reshape((m, k, 2) if w == 2 else (m, k))
+        eff, t, cores, desc, _ = oracle_sample(cfg, Ah, float(os.environ.get("ADJ_CPU_BUDGET_S", "12")))
+        cpu = {"value": eff, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
+
+    if rank == 0:
+        mh = ring_macs(m, k, depth) * (1 if w == 1 else 1)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "int8",
+            "data": "synthetic",
+            "config": {"workload": cfg["workload"], "m": m, "k": k, "p": p, "phi": cfg["phi"], "depth": depth,
+                       "seed": 1, "l2": "flushed before every timed step (256 MiB write, outside step events)",
+                       "parallelism": f"split-K x{world} (NCCL reduce)" if world > 1 else "1 GPU",
+                       "fraction_of_int8_peak_effective": value / (peak * 1e12 / 2),
+                       "ring_macs_per_step": mh, "limb_mmas_per_ring_mac": limb_mmas(p)},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "kernel_time_share": share,
+            "clocks": clk.summary(),
+            "parity": parity,
+        }
+        print(json.dumps(line), flush=True)
+    if comm is not None:
+        adj.adj_comm_destroy(comm)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
+    ap.add_argument("--depth", type=int, default=None)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-check", action="store_true", help="skip the sampled parity check")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_gpu(args, cfg, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

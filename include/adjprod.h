@@ -163,6 +163,14 @@ const char *adj_last_error(void); /* thread-local detail for the last failing ca
 uint64_t adj_launch_count(void);
 void adj_launch_count_reset(void);
 
+/* Per-kernel-class timing for measurement (bench.py).  When enabled, CUDA events are recorded
+ * on the launch stream around every launch of class c (0 = grouped tcgen05 leaf, 1 = K1
+ * pre-addition / limb split, 2 = K4 / K5 recombination, 3 = other); adj_profile_read
+ * synchronises on them and returns, per class, the summed milliseconds and launch counts,
+ * then clears the record.  Disabled by default (no events, no overhead). */
+void adj_profile_enable(int on);
+adj_status_t adj_profile_read(double ms[4], uint64_t launches[4]);
+
 #ifdef __cplusplus
 }
 #endif

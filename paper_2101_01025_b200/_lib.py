@@ -21,7 +21,7 @@ STATUS = {0: "ADJ_OK", 1: "ADJ_ERR_INVALID_VALUE", 2: "ADJ_ERR_UNSUPPORTED_MODUL
 EXPORTS = ["adjprod_modp", "adjprod_modp_ex", "adjprod_modp_workspace_size", "adjprod_modp_auto_depth",
            "gemm_modp", "adj_skew_unitary", "adj_sos", "adj_mod_lower", "adj_comm_get_unique_id",
            "adj_comm_init", "adj_comm_destroy", "adjprod_modp_dist", "adj_status_string", "adj_last_error",
-           "adj_launch_count", "adj_launch_count_reset"]
+           "adj_launch_count", "adj_launch_count_reset", "adj_profile_enable", "adj_profile_read"]
 
 
 class AdjError(RuntimeError):
@@ -68,6 +68,10 @@ def lib() -> ctypes.CDLL:
         L.adj_status_string.restype = ctypes.c_char_p
         L.adj_last_error.restype = ctypes.c_char_p
         L.adj_launch_count.restype = ctypes.c_uint64
+        L.adj_profile_enable.argtypes = [ci]
+        L.adj_profile_enable.restype = None
+        L.adj_profile_read.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_uint64)]
+        L.adj_profile_read.restype = ci
         _LIB = L
     return _LIB
 
@@ -172,3 +176,18 @@ def adj_launch_count() -> int:
 
 def adj_launch_count_reset():
     lib().adj_launch_count_reset()
+
+
+def adj_profile_enable(on: bool = True):
+    lib().adj_profile_enable(1 if on else 0)
+
+
+PROFILE_CLASSES = ("leaf", "preadd", "combine", "other")
+
+
+def adj_profile_read():
+    """{class: (ms, launches)} since the last read (synchronises on the recorded events)."""
+    ms = (ctypes.c_double * 4)()
+    n = (ctypes.c_uint64 * 4)()
+    _check(lib().adj_profile_read(ms, n), "adj_profile_read")
+    return {PROFILE_CLASSES[i]: (ms[i], int(n[i])) for i in range(4)}

@@ -51,11 +51,39 @@ adj_status_t fail(adj_status_t st, const char *fmt, ...) {
     if (_e != cudaSuccess) return fail(ADJ_ERR_CUDA, "%s: %s", #expr, cudaGetErrorString(_e)); \
   } while (0)
 
-#define LAUNCH(expr)                  \
+// ------------------------------------------------------------------ per-class event timing
+std::atomic<int> g_prof_on{0};
+std::mutex g_prof_mu;
+struct ProfRec { int cls; cudaEvent_t a, b; };
+std::vector<ProfRec> g_prof;
+
+struct ProfScope {
+  int cls;
+  cudaStream_t s;
+  cudaEvent_t a = nullptr, b = nullptr;
+  ProfScope(int c, cudaStream_t st) : cls(c), s(st) {
+    if (!g_prof_on.load()) return;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, s);
+  }
+  ~ProfScope() {
+    if (!a) return;
+    cudaEventRecord(b, s);
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_prof.push_back({cls, a, b});
+  }
+};
+
+enum { CLS_LEAF = 0, CLS_PRE = 1, CLS_COMB = 2, CLS_OTHER = 3 };
+
+#define LAUNCH_CLS(cls, expr)         \
   do {                                \
+    ProfScope _ps(cls, s);            \
     CUDA_TRY(expr);                   \
     g_launches.fetch_add(1);          \
   } while (0)
+#define LAUNCH(expr) LAUNCH_CLS(CLS_OTHER, expr)
 
 // ------------------------------------------------------------------ device info
 struct DevInfo {
@@ -216,7 +244,7 @@ adj_status_t launch_leaf_all(const Plan &P, const Ptrs &x, cudaStream_t s) {
   }
   L.tiles = P.d_tiles;
   L.n_tiles = (int32_t)P.tiles.size();
-  LAUNCH(launch_leaf(L, P.bn, P.nacc, P.grid, s));
+  LAUNCH_CLS(CLS_LEAF, launch_leaf(L, P.bn, P.nacc, P.grid, s));
   return ADJ_OK;
 }
 
@@ -234,7 +262,7 @@ adj_status_t run_split(const Plan &P, const InView &v, int64_t rows, int64_t col
   sp.scheme = P.scheme;
   sp.planes = P.planes;
   sp.mod = P.mod;
-  LAUNCH(launch_split(sp, s));
+  LAUNCH_CLS(CLS_PRE, launch_split(sp, s));
   return ADJ_OK;
 }
 
@@ -276,7 +304,7 @@ adj_status_t run_tree(const Plan &P, const InView &root, const Ptrs &x, cudaStre
         N.s3_ld = L.kh;
       }
     }
-    LAUNCH(launch_preadd(pp, s));
+    LAUNCH_CLS(CLS_PRE, launch_preadd(pp, s));
   }
   return ADJ_OK;
 }
@@ -306,7 +334,7 @@ adj_status_t run_combine(const Plan &P, const Ptrs &x, void *final_out, int64_t 
         N.out_valid = P.lv[l - 1].mh;
       }
     }
-    LAUNCH(launch_combine(cp, s));
+    LAUNCH_CLS(CLS_COMB, launch_combine(cp, s));
   }
   return ADJ_OK;
 }
@@ -352,7 +380,7 @@ adj_status_t run_syrk(const Plan &P, const Ptrs &x, adj_phi_t phi, uint32_t flag
       st = run_combine(P, x, G, P.rows_pad0, false, s);
       if (st) return st;
     }
-    LAUNCH(launch_twom(m, G, P.rows_pad0, H, P.rows_pad0, x.C, x.ldc, P.mod, s));
+    LAUNCH_CLS(CLS_COMB, launch_twom(m, G, P.rows_pad0, H, P.rows_pad0, x.C, x.ldc, P.mod, s));
   }
   if (flags & ADJ_FILL_UPPER) LAUNCH(launch_fill_upper(m, phi == ADJ_PHI_H ? 2 : 1, x.C, x.ldc, P.mod, s));
   return ADJ_OK;
@@ -396,6 +424,28 @@ const char *adj_status_string(adj_status_t s) {
 
 const char *adj_last_error(void) { return g_last_error.c_str(); }
 uint64_t adj_launch_count(void) { return g_launches.load(); }
+
+void adj_profile_enable(int on) { g_prof_on.store(on ? 1 : 0); }
+
+adj_status_t adj_profile_read(double ms[4], uint64_t launches[4]) {
+  if (!ms || !launches) return fail(ADJ_ERR_INVALID_VALUE, "null output");
+  std::vector<ProfRec> recs;
+  {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    recs.swap(g_prof);
+  }
+  for (int c = 0; c < 4; ++c) { ms[c] = 0; launches[c] = 0; }
+  for (auto &r : recs) {
+    float t = 0;
+    CUDA_TRY(cudaEventSynchronize(r.b));
+    CUDA_TRY(cudaEventElapsedTime(&t, r.a, r.b));
+    ms[r.cls] += t;
+    launches[r.cls] += 1;
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  return ADJ_OK;
+}
 void adj_launch_count_reset(void) { g_launches.store(0); }
 
 adj_status_t adj_sos(uint32_t p, uint32_t k, uint32_t *a, uint32_t *b) {
@@ -520,8 +570,8 @@ adj_status_t adj_mod_lower(int64_t m, uint32_t p, adj_phi_t phi, uint32_t *X, in
   if (!valid_modulus(p)) return fail(ADJ_ERR_UNSUPPORTED_MODULUS, "p=%u is not an odd prime in [3, 65521]", p);
   if (m == 0) return ADJ_OK;
   if (!X) return fail(ADJ_ERR_INVALID_VALUE, "X is null");
-  LAUNCH(launch_mod_lower(m, phi == ADJ_PHI_H ? 2 : 1, X, ldx, X, ldx, make_modp(p),
-                          reinterpret_cast<cudaStream_t>(stream)));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  LAUNCH(launch_mod_lower(m, phi == ADJ_PHI_H ? 2 : 1, X, ldx, X, ldx, make_modp(p), s));
   return ADJ_OK;
 }
 
