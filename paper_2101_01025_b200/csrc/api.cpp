@@ -244,7 +244,8 @@ adj_status_t launch_leaf_all(const Plan &P, const Ptrs &x, cudaStream_t s) {
   }
   L.tiles = P.d_tiles;
   L.n_tiles = (int32_t)P.tiles.size();
-  LAUNCH_CLS(CLS_LEAF, launch_leaf(L, P.bn, P.nacc, P.grid, s));
+  if (P.leaf_ver == 2) LAUNCH_CLS(CLS_LEAF, launch_leaf2(L, P.nacc, P.grid, s));
+  else LAUNCH_CLS(CLS_LEAF, launch_leaf(L, P.bn, P.nacc, P.grid, s));
   return ADJ_OK;
 }
 

@@ -278,6 +278,227 @@ cudaError_t launch_leaf(const LeafParams &p, int bn, int nacc, int grid, cudaStr
   return cudaErrorInvalidValue;
 }
 
+// ============================================================================ leaf kernel, CTA pair
+// cta_group::2 version: a cluster of 2 CTAs (one TPC) computes a 256 x 256 tile with
+// tcgen05.mma.cta_group::2 M=256 N=256 K=32 (int8).  CTA r holds rows r*128.. of the A tile and
+// rows r*128.. of the B tile in its shared memory, and accumulator rows r*128.. in its TMEM.
+// Per SM this halves shared-memory traffic versus the 1-CTA M=128 N=128 tile (TMA writes 64 B/clk
+// + MMA operand reads 64 B/clk at full tensor rate).  TMEM holds 2 slots of 256 columns; the NACC
+// limb accumulators of a tile run one after the other (acc-major), the epilogue folds each into
+// a weighted mod-p partial sum kept in registers (8 warps x 128 columns).
+struct Leaf2Cfg {
+  static constexpr int STAGES = 6;
+  static constexpr int TILE = 256;
+  static constexpr int A_BYTES = 128 * kBK;
+  static constexpr int B_BYTES = 128 * kBK;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int SLOTS = 2;
+  static constexpr int BAR_BYTES = 8 * (2 * STAGES + 2 * SLOTS) + 16;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + BAR_BYTES;
+  static constexpr int THREADS = 384;
+};
+
+template <int NACC>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
+    leaf2_kernel(const __grid_constant__ LeafParams P) {
+  using Cfg = Leaf2Cfg;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t *full_bar = reinterpret_cast<uint64_t *>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+  uint64_t *empty_bar = full_bar + Cfg::STAGES;
+  uint64_t *slot_full = empty_bar + Cfg::STAGES;
+  uint64_t *slot_empty = slot_full + Cfg::SLOTS;
+  uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(slot_empty + Cfg::SLOTS);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = ptx::cluster_ctarank();
+  const bool leader = rank == 0;
+  const int cid = (int)ptx::cluster_id_x();
+  const int ncl = (int)ptx::num_clusters_x();
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < Cfg::STAGES; ++s) {
+      ptx::mbar_init(&full_bar[s], 1);
+      ptx::mbar_init(&empty_bar[s], 1);
+    }
+    for (int s = 0; s < Cfg::SLOTS; ++s) {
+      ptx::mbar_init(&slot_full[s], 1);
+      ptx::mbar_init(&slot_empty[s], 16);   // 8 epilogue warps x 2 CTAs (used in the leader)
+    }
+    ptx::fence_barrier_init();
+    for (int i = 0; i < kMaxMaps; ++i) ptx::prefetch_tmap(&P.maps[i]);
+  }
+  if (warp == 2) ptx::tmem_alloc_2sm(tmem_holder, 512);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::cluster_sync();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer (both CTAs)
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = cid; t < P.n_tiles; t += ncl) {
+        int q, I, J;
+        decode_tile(P.tiles[t], q, I, J);
+        const LeafProduct &pr = P.prod[q];
+        const CUtensorMap *map = &P.maps[pr.map];
+        const int arow = pr.a_row0 + I * Cfg::TILE + (int)rank * 128;
+        const int brow = pr.b_row0 + J * Cfg::TILE + (int)rank * 128;
+#pragma unroll 1
+        for (int j = 0; j < NACC; ++j) {
+#pragma unroll 1
+          for (int kb = 0; kb < pr.kblocks; ++kb) {
+#pragma unroll 1
+            for (int tt = P.acc_begin[j]; tt < P.acc_begin[j + 1]; ++tt) {
+              const LeafTerm term = P.terms[tt];
+              ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
+              if (leader) ptx::mbar_expect_tx(&full_bar[stage], 2 * Cfg::STAGE_BYTES);
+              uint8_t *sa = smem + stage * Cfg::STAGE_BYTES;
+              ptx::tma_load_2d_2sm(sa, map, kb * kBK, arow + term.a_plane * pr.a_plane_rows, &full_bar[stage]);
+              ptx::tma_load_2d_2sm(sa + Cfg::A_BYTES, map, kb * kBK, brow + term.b_plane * pr.b_plane_rows,
+                                   &full_bar[stage]);
+              if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (leader CTA, one thread)
+    if (leader && lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      uint32_t unit = 0;
+      for (int t = cid; t < P.n_tiles; t += ncl) {
+        int q, I, J;
+        decode_tile(P.tiles[t], q, I, J);
+        const LeafProduct &pr = P.prod[q];
+#pragma unroll 1
+        for (int j = 0; j < NACC; ++j, ++unit) {
+          const uint32_t slot = unit & 1, use = unit >> 1;
+          ptx::mbar_wait_cluster(&slot_empty[slot], (use & 1) ^ 1);
+          ptx::tc_fence_after();
+          const uint32_t d_tmem = tmem_base + slot * Cfg::TILE;
+          uint32_t accumulate = 0;
+#pragma unroll 1
+          for (int kb = 0; kb < pr.kblocks; ++kb) {
+#pragma unroll 1
+            for (int tt = P.acc_begin[j]; tt < P.acc_begin[j + 1]; ++tt) {
+              const LeafTerm term = P.terms[tt];
+              const uint32_t idesc = ptx::idesc_i8(256, 256, term.a_signed != 0, term.b_signed != 0);
+              ptx::mbar_wait(&full_bar[stage], phase);
+              ptx::tc_fence_after();
+              const uint32_t sa = ptx::smem_u32(smem + stage * Cfg::STAGE_BYTES);
+              const uint64_t adesc = ptx::smem_desc_sw128(sa);
+              const uint64_t bdesc = ptx::smem_desc_sw128(sa + Cfg::A_BYTES);
+#pragma unroll
+              for (int kk = 0; kk < kBK / 32; ++kk) {
+                ptx::mma_i8_2sm(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, idesc, accumulate);
+                accumulate = 1;
+              }
+              ptx::mma_commit_2sm(&empty_bar[stage], 0x3);
+              if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
+            }
+          }
+          ptx::mma_commit_2sm(&slot_full[slot], 0x3);
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ epilogue (8 warps per CTA)
+    const int q4 = warp & 3;               // TMEM lane quadrant this warp may access
+    const int h = (warp - 4) >> 2;          // column half of the 256-wide tile
+    const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
+    const ModP mod = P.mod;
+    uint32_t unit = 0;
+    for (int t = cid; t < P.n_tiles; t += ncl) {
+      int q, I, J;
+      decode_tile(P.tiles[t], q, I, J);
+      const LeafProduct &pr = P.prod[q];
+      const int64_t row = (int64_t)I * Cfg::TILE + rank * 128 + q4 * 32 + lane;
+      const int64_t col0 = (int64_t)J * Cfg::TILE + h * 128;
+      uint32_t part[NACC > 1 ? 64 : 1];
+#pragma unroll
+      for (int j = 0; j < NACC; ++j, ++unit) {
+        const uint32_t slot = unit & 1, use = unit >> 1;
+        ptx::mbar_wait(&slot_full[slot], use & 1);
+        ptx::tc_fence_after();
+        const uint32_t w = P.weight[j];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t v[32];
+          ptx::tmem_ld32(tmem_base + lane_off + slot * Cfg::TILE + h * 128 + c * 32, v);
+          ptx::tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) v[e] = mod_s32((int32_t)v[e], mod);
+          if constexpr (NACC == 1) {
+            if (w != 1) {
+#pragma unroll
+              for (int e = 0; e < 32; ++e) v[e] = mulmod(v[e], w, mod);
+            }
+            store_chunk(pr, row, col0 + c * 32, v);
+          } else {
+#pragma unroll
+            for (int e = 0; e < 32; ++e) v[e] = mulmod(v[e], w, mod);
+            if (j == 0) {
+#pragma unroll
+              for (int e = 0; e < 16; ++e) part[c * 16 + e] = v[2 * e] | (v[2 * e + 1] << 16);
+            } else {
+#pragma unroll
+              for (int e = 0; e < 16; ++e) {
+                v[2 * e] = addmod(v[2 * e], part[c * 16 + e] & 0xFFFF, mod);
+                v[2 * e + 1] = addmod(v[2 * e + 1], part[c * 16 + e] >> 16, mod);
+              }
+              if (j == NACC - 1) {
+                store_chunk(pr, row, col0 + c * 32, v);
+              } else {
+#pragma unroll
+                for (int e = 0; e < 16; ++e) part[c * 16 + e] = v[2 * e] | (v[2 * e + 1] << 16);
+              }
+            }
+          }
+        }
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&slot_empty[slot]), 0));
+      }
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::cluster_sync();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc_2sm(tmem_base, 512);
+  }
+}
+
+template <int NACC>
+static cudaError_t launch_leaf2_t(const LeafParams &p, int grid, cudaStream_t s) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(leaf2_kernel<NACC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Leaf2Cfg::SMEM);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  leaf2_kernel<NACC><<<grid, Leaf2Cfg::THREADS, Leaf2Cfg::SMEM, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_leaf2(const LeafParams &p, int nacc, int grid, cudaStream_t s) {
+  if (p.n_tiles == 0) return cudaSuccess;
+  if (grid % 2) return cudaErrorInvalidValue;
+  if (nacc == 1) return launch_leaf2_t<1>(p, grid, s);
+  if (nacc == 3) return launch_leaf2_t<3>(p, grid, s);
+  return cudaErrorInvalidValue;
+}
+
 // ============================================================================ input loads
 // 4 consecutive logical elements (R, C..C+3) of a view; zero outside the valid region.
 __device__ __forceinline__ void load4(const InView &v, int64_t R, int64_t C, const ModP &m,

@@ -3,6 +3,7 @@
 #include "plan.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 namespace adj {
@@ -16,6 +17,10 @@ static void fill_scheme(Plan &P, uint32_t p) {
   P.planes = limb_planes(P.scheme);
   P.nacc = limb_accs(P.scheme);
   P.bn = P.scheme == LIMB_S8 ? 256 : 128;
+  const char *lv = getenv("ADJ_LEAF");
+  P.leaf_ver = (lv && lv[0] == '1') ? 1 : 2;
+  P.tile_m = P.leaf_ver == 2 ? 256 : kBM;
+  P.tile_n = P.leaf_ver == 2 ? 256 : P.bn;
   P.mod = make_modp(p);
   P.Y = skew_unitary(p);
   LeafParams &L = P.leaf_template;
@@ -85,17 +90,23 @@ static void append_tiles(Plan &P) {
   const int band = 8;
   for (size_t q = 0; q < P.prods.size(); ++q) {
     const LeafProduct &lp = P.prods[q].lp;
-    const int64_t tm = cdiv(lp.out_rows, kBM);
-    const int64_t tn = cdiv(lp.out_cols, P.bn);
+    const int64_t tm = cdiv(lp.out_rows, P.tile_m);
+    const int64_t tn = cdiv(lp.out_cols, P.tile_n);
     for (int64_t b0 = 0; b0 < tm; b0 += band) {
       const int64_t b1 = std::min<int64_t>(tm, b0 + band);
       for (int64_t J = 0; J < tn; ++J)
         for (int64_t I = b0; I < b1; ++I) {
-          if (lp.sym && J * P.bn > I * kBM + kBM - 1) continue;   // tile entirely above diagonal
+          if (lp.sym && J * P.tile_n > I * P.tile_m + P.tile_m - 1) continue;   // tile above the diagonal
           P.tiles.push_back(((uint32_t)q << 24) | ((uint32_t)I << 12) | (uint32_t)J);
         }
     }
   }
+}
+
+static void set_grid(Plan &P, int num_sms) {
+  const int64_t nt = std::max<int64_t>(1, (int64_t)P.tiles.size());
+  if (P.leaf_ver == 2) P.grid = 2 * (int)std::min<int64_t>(num_sms / 2, nt);   // CTA pairs
+  else P.grid = (int)std::min<int64_t>(num_sms, nt);
 }
 
 int auto_depth(int64_t m, int64_t k, uint32_t p, int phi) {
@@ -218,7 +229,7 @@ bool build_syrk_plan(Plan &P, int64_t m, int64_t k, uint32_t p, int phi, int dep
   }
   if ((int)P.prods.size() > kMaxProducts) { *err = "too many leaf products"; return false; }
   append_tiles(P);
-  P.grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms, (int64_t)P.tiles.size()));
+  set_grid(P, num_sms);
   return true;
 }
 
@@ -246,7 +257,7 @@ bool build_gemm_plan(Plan &P, int64_t m, int64_t n, int64_t k, uint32_t p, int n
   P.prods.push_back(make_prod(0, P.op0_row[0], P.op0_row[1], P.rows_pad0, P.rows_pad_b, P.kpad0, false, OUT_C, 0, 0, 0,
                               m, n, true, 0));
   append_tiles(P);
-  P.grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms, (int64_t)P.tiles.size()));
+  set_grid(P, num_sms);
   return true;
 }
 

@@ -46,6 +46,8 @@ struct Plan {
   int depth = 0;
   LimbScheme scheme;
   int planes = 1, nacc = 1, bn = 128;
+  int leaf_ver = 2;               // 2: CTA-pair 256x256 tiles (leaf2_kernel); 1: 1-CTA 128 x bn
+  int tile_m = 256, tile_n = 256;
   ModP mod;
   SkewY Y;
   std::vector<ArenaPlan> arenas;
