@@ -13,12 +13,15 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "kernels.hpp"
 #include "ptx.cuh"
 
 namespace adj {
+
+__host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
 
 // ============================================================================ leaf kernel
 template <int BN>
@@ -286,25 +289,31 @@ cudaError_t launch_leaf(const LeafParams &p, int bn, int nacc, int grid, cudaStr
 // + MMA operand reads 64 B/clk at full tensor rate).  TMEM holds 2 slots of 256 columns; the NACC
 // limb accumulators of a tile run one after the other (acc-major), the epilogue folds each into
 // a weighted mod-p partial sum kept in registers (8 warps x 128 columns).
+template <int NACC>
 struct Leaf2Cfg {
-  static constexpr int STAGES = 6;
+  static constexpr int STAGES = NACC > 1 ? 5 : 6;
   static constexpr int TILE = 256;
   static constexpr int A_BYTES = 128 * kBK;
   static constexpr int B_BYTES = 128 * kBK;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int SLOTS = 2;
+  // weighted mod-p partial sums of the limb accumulators: 128 rows x 128 words (u16 pairs),
+  // row stride 129 words so that the 32 rows a warp touches fall in 32 different banks
+  static constexpr int PART_STRIDE = 129;
+  static constexpr int PART_BYTES = NACC > 1 ? 128 * PART_STRIDE * 4 : 0;
   static constexpr int BAR_BYTES = 8 * (2 * STAGES + 2 * SLOTS) + 16;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + BAR_BYTES;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + PART_BYTES + 1024 + BAR_BYTES;
   static constexpr int THREADS = 384;
 };
 
 template <int NACC>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     leaf2_kernel(const __grid_constant__ LeafParams P) {
-  using Cfg = Leaf2Cfg;
+  using Cfg = Leaf2Cfg<NACC>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t *full_bar = reinterpret_cast<uint64_t *>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+  uint32_t *part_s = reinterpret_cast<uint32_t *>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+  uint64_t *full_bar = reinterpret_cast<uint64_t *>(smem + Cfg::STAGES * Cfg::STAGE_BYTES + Cfg::PART_BYTES);
   uint64_t *empty_bar = full_bar + Cfg::STAGES;
   uint64_t *slot_full = empty_bar + Cfg::STAGES;
   uint64_t *slot_empty = slot_full + Cfg::SLOTS;
@@ -413,58 +422,56 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     const int q4 = warp & 3;               // TMEM lane quadrant this warp may access
     const int h = (warp - 4) >> 2;          // column half of the 256-wide tile
     const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
+    const int lrow = q4 * 32 + lane;
+    uint32_t *prow = part_s + lrow * Cfg::PART_STRIDE + h * 64;
     const ModP mod = P.mod;
+    const uint32_t empty_remote0 = ptx::mapa(ptx::smem_u32(&slot_empty[0]), 0);
+    const uint32_t empty_remote1 = ptx::mapa(ptx::smem_u32(&slot_empty[1]), 0);
     uint32_t unit = 0;
     for (int t = cid; t < P.n_tiles; t += ncl) {
       int q, I, J;
       decode_tile(P.tiles[t], q, I, J);
       const LeafProduct &pr = P.prod[q];
-      const int64_t row = (int64_t)I * Cfg::TILE + rank * 128 + q4 * 32 + lane;
+      const int64_t row = (int64_t)I * Cfg::TILE + rank * 128 + lrow;
       const int64_t col0 = (int64_t)J * Cfg::TILE + h * 128;
-      uint32_t part[NACC > 1 ? 64 : 1];
-#pragma unroll
+#pragma unroll 1
       for (int j = 0; j < NACC; ++j, ++unit) {
         const uint32_t slot = unit & 1, use = unit >> 1;
         ptx::mbar_wait(&slot_full[slot], use & 1);
         ptx::tc_fence_after();
         const uint32_t w = P.weight[j];
-#pragma unroll
+#pragma unroll 1
         for (int c = 0; c < 4; ++c) {
           uint32_t v[32];
           ptx::tmem_ld32(tmem_base + lane_off + slot * Cfg::TILE + h * 128 + c * 32, v);
           ptx::tmem_wait_ld();
 #pragma unroll
           for (int e = 0; e < 32; ++e) v[e] = mod_s32((int32_t)v[e], mod);
-          if constexpr (NACC == 1) {
-            if (w != 1) {
-#pragma unroll
-              for (int e = 0; e < 32; ++e) v[e] = mulmod(v[e], w, mod);
-            }
-            store_chunk(pr, row, col0 + c * 32, v);
-          } else {
+          if (NACC > 1 || w != 1) {
 #pragma unroll
             for (int e = 0; e < 32; ++e) v[e] = mulmod(v[e], w, mod);
-            if (j == 0) {
-#pragma unroll
-              for (int e = 0; e < 16; ++e) part[c * 16 + e] = v[2 * e] | (v[2 * e + 1] << 16);
-            } else {
+          }
+          if constexpr (NACC > 1) {
+            uint32_t *pc = prow + c * 16;
+            if (j > 0) {
 #pragma unroll
               for (int e = 0; e < 16; ++e) {
-                v[2 * e] = addmod(v[2 * e], part[c * 16 + e] & 0xFFFF, mod);
-                v[2 * e + 1] = addmod(v[2 * e + 1], part[c * 16 + e] >> 16, mod);
-              }
-              if (j == NACC - 1) {
-                store_chunk(pr, row, col0 + c * 32, v);
-              } else {
-#pragma unroll
-                for (int e = 0; e < 16; ++e) part[c * 16 + e] = v[2 * e] | (v[2 * e + 1] << 16);
+                const uint32_t wd = pc[e];
+                v[2 * e] = addmod(v[2 * e], wd & 0xFFFF, mod);
+                v[2 * e + 1] = addmod(v[2 * e + 1], wd >> 16, mod);
               }
             }
+            if (j < NACC - 1) {
+#pragma unroll
+              for (int e = 0; e < 16; ++e) pc[e] = v[2 * e] | (v[2 * e + 1] << 16);
+              continue;
+            }
           }
+          store_chunk(pr, row, col0 + c * 32, v);
         }
         ptx::tc_fence_before();
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&slot_empty[slot]), 0));
+        if (lane == 0) ptx::mbar_arrive_cluster(slot ? empty_remote1 : empty_remote0);
       }
     }
   }
@@ -483,11 +490,11 @@ static cudaError_t launch_leaf2_t(const LeafParams &p, int grid, cudaStream_t s)
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(leaf2_kernel<NACC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         Leaf2Cfg::SMEM);
+                                         Leaf2Cfg<NACC>::SMEM);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  leaf2_kernel<NACC><<<grid, Leaf2Cfg::THREADS, Leaf2Cfg::SMEM, s>>>(p);
+  leaf2_kernel<NACC><<<grid, Leaf2Cfg<NACC>::THREADS, Leaf2Cfg<NACC>::SMEM, s>>>(p);
   return cudaGetLastError();
 }
 
@@ -548,96 +555,174 @@ __device__ __forceinline__ void load4(const InView &v, int64_t R, int64_t C, con
   }
 }
 
-// write the int8 limb planes of 4 residues at (arena row `row` of plane 0, byte column col)
-__device__ __forceinline__ void store_limbs4(int8_t *arena, int64_t kpad, int64_t rows_pad,
-                                             int64_t row, int64_t col, const uint32_t (&x)[4],
-                                             int scheme, int planes, const ModP &m) {
-  uint32_t l[4];
+// ============================================================================ K1 pre-addition
+// Scheme-specialised limb split of 4 residues into packed int8 plane words (one u32 per plane).
+template <int SCHEME>
+__device__ __forceinline__ void limbs4(const uint32_t (&x)[4], const ModP &m, uint32_t (&w)[3]) {
+  int32_t c[4];
 #pragma unroll
-  for (int e = 0; e < 4; ++e) l[e] = limb_split(x[e], scheme, m);
+  for (int e = 0; e < 4; ++e) c[e] = centered(x[e], m);
+  if constexpr (SCHEME == 0) {
+    w[0] = __byte_perm(__byte_perm(c[0], c[1], 0x40), __byte_perm(c[2], c[3], 0x40), 0x5410);
+  } else if constexpr (SCHEME == 1) {
+    int32_t hi[4], lo[4], mid[4];
 #pragma unroll
-  for (int pl = 0; pl < 3; ++pl) {
-    if (pl >= planes) break;
-    const int sh = 8 * pl;
-    uint32_t w = ((l[0] >> sh) & 0xFF) | (((l[1] >> sh) & 0xFF) << 8) | (((l[2] >> sh) & 0xFF) << 16) |
-                 (((l[3] >> sh) & 0xFF) << 24);
-    *reinterpret_cast<uint32_t *>(arena + (row + pl * rows_pad) * kpad + col) = w;
+    for (int e = 0; e < 4; ++e) {
+      hi[e] = (c[e] + 64) >> 7;
+      lo[e] = c[e] - (hi[e] << 7);
+      mid[e] = hi[e] + lo[e];
+    }
+    w[0] = __byte_perm(__byte_perm(hi[0], hi[1], 0x40), __byte_perm(hi[2], hi[3], 0x40), 0x5410);
+    w[1] = __byte_perm(__byte_perm(lo[0], lo[1], 0x40), __byte_perm(lo[2], lo[3], 0x40), 0x5410);
+    w[2] = __byte_perm(__byte_perm(mid[0], mid[1], 0x40), __byte_perm(mid[2], mid[3], 0x40), 0x5410);
+  } else {
+    int32_t hi[4], lo[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      hi[e] = c[e] >> 8;
+      lo[e] = c[e] - (hi[e] << 8);
+    }
+    w[0] = __byte_perm(__byte_perm(hi[0], hi[1], 0x40), __byte_perm(hi[2], hi[3], 0x40), 0x5410);
+    w[1] = __byte_perm(__byte_perm(lo[0], lo[1], 0x40), __byte_perm(lo[2], lo[3], 0x40), 0x5410);
   }
 }
 
-__device__ __forceinline__ void zero_limbs4(int8_t *arena, int64_t kpad, int64_t rows_pad, int64_t row,
-                                            int64_t col, int planes) {
-  for (int pl = 0; pl < planes; ++pl)
-    *reinterpret_cast<uint32_t *>(arena + (row + pl * rows_pad) * kpad + col) = 0u;
+template <int SCHEME>
+__device__ __forceinline__ void put_limbs4(int8_t *base, int64_t plane_stride, const uint32_t (&x)[4],
+                                           const ModP &m) {
+  constexpr int NP = SCHEME == 0 ? 1 : (SCHEME == 1 ? 3 : 2);
+  uint32_t w[3];
+  limbs4<SCHEME>(x, m, w);
+#pragma unroll
+  for (int pl = 0; pl < NP; ++pl) *reinterpret_cast<uint32_t *>(base + pl * plane_stride) = w[pl];
 }
 
-// ============================================================================ K1 pre-addition
-__device__ __forceinline__ void apply_Y(uint32_t a, uint32_t b, uint32_t &oa, uint32_t &ob,
-                                        const PreParams &P) {
+template <int YK>
+__device__ __forceinline__ void apply_Y4(const uint32_t (&a)[4], const uint32_t (&b)[4], uint32_t (&oa)[4],
+                                         uint32_t (&ob)[4], uint32_t ya, uint32_t yb, const ModP &m) {
   // X Y on the column pair (c, c + kh/2): Y = i I -> (i a, i b);
   // Y = [[ya, yb], [-yb, ya]] (x) I -> [X1 X2] Y = [ya X1 - yb X2, yb X1 + ya X2]
-  if (P.ykind == 0) {
-    oa = mulmod(P.ya, a, P.mod);
-    ob = mulmod(P.ya, b, P.mod);
-  } else {
-    oa = submod(mulmod(P.ya, a, P.mod), mulmod(P.yb, b, P.mod), P.mod);
-    ob = addmod(mulmod(P.yb, a, P.mod), mulmod(P.ya, b, P.mod), P.mod);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    if constexpr (YK == 0) {
+      oa[e] = mulmod(ya, a[e], m);
+      ob[e] = mulmod(ya, b[e], m);
+    } else {
+      oa[e] = submod(mulmod(ya, a[e], m), mulmod(yb, b[e], m), m);
+      ob[e] = addmod(mulmod(yb, a[e], m), mulmod(ya, b[e], m), m);
+    }
   }
 }
 
-__global__ void __launch_bounds__(256) preadd_kernel(const __grid_constant__ PreParams P) {
-  const PreNode &N = P.nodes[blockIdx.z];
+// fast 4-element load of a fully valid, vector-aligned position (type known by the caller)
+template <int T>
+__device__ __forceinline__ void load4_fast(const void *ptr, int64_t off, const ModP &m, uint32_t (&x)[4]) {
+  if constexpr (T == IN_U32) {
+    uint4 q = __ldg(reinterpret_cast<const uint4 *>(static_cast<const uint32_t *>(ptr) + off));
+    x[0] = mod_u32(q.x, m); x[1] = mod_u32(q.y, m); x[2] = mod_u32(q.z, m); x[3] = mod_u32(q.w, m);
+  } else if constexpr (T == IN_U16) {
+    uint2 q = __ldg(reinterpret_cast<const uint2 *>(static_cast<const uint16_t *>(ptr) + off));
+    x[0] = q.x & 0xFFFF; x[1] = q.x >> 16; x[2] = q.y & 0xFFFF; x[3] = q.y >> 16;
+  } else {
+    const uint4 *p = reinterpret_cast<const uint4 *>(static_cast<const uint32_t *>(ptr) + 2 * off);
+    uint4 a = __ldg(p), b = __ldg(p + 1);
+    x[0] = addmod(mod_u32(a.x, m), mod_u32(a.y, m), m);
+    x[1] = addmod(mod_u32(a.z, m), mod_u32(a.w, m), m);
+    x[2] = addmod(mod_u32(b.x, m), mod_u32(b.y, m), m);
+    x[3] = addmod(mod_u32(b.z, m), mod_u32(b.w, m), m);
+  }
+}
+
+template <int SCHEME, int YK, int T>
+__device__ __forceinline__ void preadd_row(const PreParams &P, const PreNode &N, int64_t r, int64_t c) {
+  const ModP &m = P.mod;
   const int64_t h2 = P.kh / 2;
-  const int64_t g_main = h2 / 4;                 // 4-column groups of the first half
+  const InView &v = N.in;
+  uint32_t x11a[4], x11b[4], x12a[4], x12b[4], x21a[4], x21b[4], x22a[4], x22b[4];
+  const bool top_ok = r < P.mh && r < v.rows_valid;
+  const bool bot_ok = r < P.mh && P.mh + r < v.rows_valid;
+  if (v.vec_ok && top_ok && bot_ok && P.kh + c + h2 + 3 < v.cols_valid) {
+    const int64_t o1 = r * v.ld, o2 = (P.mh + r) * v.ld;
+    load4_fast<T>(v.ptr, o1 + c, m, x11a);
+    load4_fast<T>(v.ptr, o1 + c + h2, m, x11b);
+    load4_fast<T>(v.ptr, o1 + P.kh + c, m, x12a);
+    load4_fast<T>(v.ptr, o1 + P.kh + c + h2, m, x12b);
+    load4_fast<T>(v.ptr, o2 + c, m, x21a);
+    load4_fast<T>(v.ptr, o2 + c + h2, m, x21b);
+    load4_fast<T>(v.ptr, o2 + P.kh + c, m, x22a);
+    load4_fast<T>(v.ptr, o2 + P.kh + c + h2, m, x22b);
+  } else {
+    InView vv = v;
+    if (r >= P.mh) vv.rows_valid = 0;             // rows of the zero padding up to rows_pad
+    load4(vv, r, c, m, x11a);
+    load4(vv, r, c + h2, m, x11b);
+    load4(vv, r, P.kh + c, m, x12a);
+    load4(vv, r, P.kh + c + h2, m, x12b);
+    load4(vv, P.mh + r, c, m, x21a);
+    load4(vv, P.mh + r, c + h2, m, x21b);
+    load4(vv, P.mh + r, P.kh + c, m, x22a);
+    load4(vv, P.mh + r, P.kh + c + h2, m, x22b);
+  }
+  uint32_t da[4], db[4], s1a[4], s1b[4], ta[4], tb[4], s2a[4], s2b[4], s3a[4], s3b[4], s4a[4], s4b[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) { da[e] = submod(x21a[e], x11a[e], m); db[e] = submod(x21b[e], x11b[e], m); }
+  apply_Y4<YK>(da, db, s1a, s1b, P.ya, P.yb, m);                 // S1 = (A21 - A11) Y
+  apply_Y4<YK>(x21a, x21b, ta, tb, P.ya, P.yb, m);               // A21 Y
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    s2a[e] = submod(x22a[e], ta[e], m); s2b[e] = submod(x22b[e], tb[e], m);   // S2 = A22 - A21 Y
+    s3a[e] = submod(s1a[e], x22a[e], m); s3b[e] = submod(s1b[e], x22b[e], m); // S3 = S1 - A22
+    s4a[e] = addmod(s3a[e], x12a[e], m); s4b[e] = addmod(s3b[e], x12b[e], m); // S4 = S3 + A12
+  }
+  const int64_t ps = P.rows_pad * P.kpad;
+#define PUT(o, A, B)                                                                   \
+  if (N.op_row[o] >= 0) {                                                              \
+    int8_t *b = P.arena + (N.op_row[o] + r) * P.kpad;                                  \
+    put_limbs4<SCHEME>(b + c, ps, A, m);                                               \
+    put_limbs4<SCHEME>(b + c + h2, ps, B, m);                                          \
+  }
+  PUT(OUT_S1, s1a, s1b)
+  PUT(OUT_S2, s2a, s2b)
+  PUT(OUT_S4, s4a, s4b)
+  PUT(OUT_X22, x22a, x22b)
+  PUT(OUT_X11, x11a, x11b)
+  PUT(OUT_X12, x12a, x12b)
+  PUT(OUT_S3, s3a, s3b)
+#undef PUT
+  if (N.s3 != nullptr && r < P.mh) {
+    uint16_t *d = N.s3 + r * N.s3_ld;
+    uint2 va, vb;
+    va.x = s3a[0] | (s3a[1] << 16); va.y = s3a[2] | (s3a[3] << 16);
+    vb.x = s3b[0] | (s3b[1] << 16); vb.y = s3b[2] | (s3b[3] << 16);
+    *reinterpret_cast<uint2 *>(d + c) = va;
+    *reinterpret_cast<uint2 *>(d + c + h2) = vb;
+  }
+}
+
+template <int SCHEME, int YK>
+__global__ void __launch_bounds__(256) preadd_kernel(const __grid_constant__ PreParams P) {
+  constexpr int NP = SCHEME == 0 ? 1 : (SCHEME == 1 ? 3 : 2);
+  const PreNode &N = P.nodes[blockIdx.z];
+  const int64_t g_main = P.kh / 8;               // 4-column groups of the first half
   const int64_t g_pad = (P.kpad - P.kh) / 4;     // zero padding columns [kh, kpad)
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= g_main + g_pad) return;
-  const ModP &m = P.mod;
+  const int type = N.in.type;
   for (int64_t r = blockIdx.y; r < P.rows_pad; r += gridDim.y) {
     if (g >= g_main) {
       const int64_t col = P.kh + (g - g_main) * 4;
+#pragma unroll
       for (int o = 0; o < OUT_N; ++o)
-        if (N.op_row[o] >= 0) zero_limbs4(P.arena, P.kpad, P.rows_pad, N.op_row[o] + r, col, P.planes);
+        if (N.op_row[o] >= 0)
+#pragma unroll
+          for (int pl = 0; pl < NP; ++pl)
+            *reinterpret_cast<uint32_t *>(P.arena + (N.op_row[o] + r + pl * P.rows_pad) * P.kpad + col) = 0u;
       continue;
     }
     const int64_t c = g * 4;
-    uint32_t x11a[4], x11b[4], x12a[4], x12b[4], x21a[4], x21b[4], x22a[4], x22b[4];
-    InView v = N.in;
-    if (r >= P.mh) v.rows_valid = 0;             // rows of the zero padding up to rows_pad
-    load4(v, r, c, m, x11a);
-    load4(v, r, c + h2, m, x11b);
-    load4(v, r, P.kh + c, m, x12a);
-    load4(v, r, P.kh + c + h2, m, x12b);
-    load4(v, P.mh + r, c, m, x21a);
-    load4(v, P.mh + r, c + h2, m, x21b);
-    load4(v, P.mh + r, P.kh + c, m, x22a);
-    load4(v, P.mh + r, P.kh + c + h2, m, x22b);
-    uint32_t s1a[4], s1b[4], s2a[4], s2b[4], s3a[4], s3b[4], s4a[4], s4b[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      uint32_t ta, tb;
-      apply_Y(submod(x21a[e], x11a[e], m), submod(x21b[e], x11b[e], m), s1a[e], s1b[e], P);  // S1
-      apply_Y(x21a[e], x21b[e], ta, tb, P);                                                 // A21 Y
-      s2a[e] = submod(x22a[e], ta, m); s2b[e] = submod(x22b[e], tb, m);                      // S2
-      s3a[e] = submod(s1a[e], x22a[e], m); s3b[e] = submod(s1b[e], x22b[e], m);              // S3
-      s4a[e] = addmod(s3a[e], x12a[e], m); s4b[e] = addmod(s3b[e], x12b[e], m);              // S4
-    }
-    const uint32_t(*outs_a[OUT_N])[4] = {&s1a, &s2a, &s4a, &x22a, &x11a, &x12a, &s3a};
-    const uint32_t(*outs_b[OUT_N])[4] = {&s1b, &s2b, &s4b, &x22b, &x11b, &x12b, &s3b};
-#pragma unroll
-    for (int o = 0; o < OUT_N; ++o) {
-      if (N.op_row[o] < 0) continue;
-      store_limbs4(P.arena, P.kpad, P.rows_pad, N.op_row[o] + r, c, *outs_a[o], P.scheme, P.planes, m);
-      store_limbs4(P.arena, P.kpad, P.rows_pad, N.op_row[o] + r, c + h2, *outs_b[o], P.scheme, P.planes, m);
-    }
-    if (N.s3 != nullptr && r < P.mh) {
-      uint16_t *d = N.s3 + r * N.s3_ld;
-      uint2 va, vb;
-      va.x = s3a[0] | (s3a[1] << 16); va.y = s3a[2] | (s3a[3] << 16);
-      vb.x = s3b[0] | (s3b[1] << 16); vb.y = s3b[2] | (s3b[3] << 16);
-      *reinterpret_cast<uint2 *>(d + c) = va;
-      *reinterpret_cast<uint2 *>(d + c + h2) = vb;
-    }
+    if (type == IN_U32) preadd_row<SCHEME, YK, IN_U32>(P, N, r, c);
+    else if (type == IN_U16) preadd_row<SCHEME, YK, IN_U16>(P, N, r, c);
+    else preadd_row<SCHEME, YK, IN_PAIR_SUM>(P, N, r, c);
   }
 }
 
@@ -647,77 +732,135 @@ cudaError_t launch_preadd(const PreParams &p, cudaStream_t s) {
   dim3 block(256);
   dim3 grid((unsigned)((groups + 255) / 256), (unsigned)(p.rows_pad < 65535 ? p.rows_pad : 65535),
             (unsigned)p.n_nodes);
-  preadd_kernel<<<grid, block, 0, s>>>(p);
+#define PRE(S, Y) preadd_kernel<S, Y><<<grid, block, 0, s>>>(p)
+  if (p.scheme == 0) { if (p.ykind == 0) PRE(0, 0); else PRE(0, 1); }
+  else if (p.scheme == 1) { if (p.ykind == 0) PRE(1, 0); else PRE(1, 1); }
+  else { if (p.ykind == 0) PRE(2, 0); else PRE(2, 1); }
+#undef PRE
   return cudaGetLastError();
 }
 
 // ============================================================================ plain split
+template <int SCHEME>
 __global__ void __launch_bounds__(256) split_kernel(const __grid_constant__ SplitParams P) {
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= P.kpad / 4) return;
   const int64_t c = g * 4;
+  const int64_t ps = P.rows_pad * P.kpad;
   for (int64_t r = blockIdx.y; r < P.rows_pad; r += gridDim.y) {
     uint32_t x[4];
-    InView v = P.in;
-    if (r >= P.rows) v.rows_valid = 0;
-    if (c >= P.cols) v.cols_valid = 0;
-    load4(v, r, c, P.mod, x);
-    store_limbs4(P.arena, P.kpad, P.rows_pad, P.op_row + r, c, x, P.scheme, P.planes, P.mod);
+    const InView &v = P.in;
+    if (v.vec_ok && r < P.rows && r < v.rows_valid && c + 3 < v.cols_valid && c + 3 < P.cols && v.type == IN_U32) {
+      load4_fast<IN_U32>(v.ptr, r * v.ld + c, P.mod, x);
+    } else {
+      InView vv = v;
+      if (r >= P.rows) vv.rows_valid = 0;
+      if (c >= P.cols) vv.cols_valid = 0;
+      load4(vv, r, c, P.mod, x);
+    }
+    put_limbs4<SCHEME>(P.arena + (P.op_row + r) * P.kpad + c, ps, x, P.mod);
   }
 }
 
 cudaError_t launch_split(const SplitParams &p, cudaStream_t s) {
   dim3 grid((unsigned)((p.kpad / 4 + 255) / 256), (unsigned)(p.rows_pad < 65535 ? p.rows_pad : 65535));
-  split_kernel<<<grid, 256, 0, s>>>(p);
+  if (p.scheme == 0) split_kernel<0><<<grid, 256, 0, s>>>(p);
+  else if (p.scheme == 1) split_kernel<1><<<grid, 256, 0, s>>>(p);
+  else split_kernel<2><<<grid, 256, 0, s>>>(p);
   return cudaGetLastError();
 }
 
 // ============================================================================ K4 recombination
+// 64 x 64 tiles of the (mh x mh) product grid; thread (tx, ty) owns 4 consecutive columns of
+// rows ty, ty+16, ty+32, ty+48 (8-byte u16 loads).  The mirrored tile (tj, ti) is staged
+// through shared memory for Up(U1) = Low(U1)^T and P4^T.
+template <typename OutT>
+__device__ __forceinline__ void store4(OutT *o, bool vec, int64_t ncols_ok, const uint32_t (&v)[4]) {
+  if (vec && ncols_ok >= 4 && (reinterpret_cast<uintptr_t>(o) % (4 * sizeof(OutT)) == 0)) {
+    if constexpr (sizeof(OutT) == 4) *reinterpret_cast<uint4 *>(o) = make_uint4(v[0], v[1], v[2], v[3]);
+    else *reinterpret_cast<uint2 *>(o) = make_uint2(v[0] | (v[1] << 16), v[2] | (v[3] << 16));
+  } else {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) if (e < ncols_ok) o[e] = (OutT)v[e];
+  }
+}
+
+__device__ __forceinline__ void ld4u16(const uint16_t *p, uint32_t (&v)[4]) {
+  uint2 q = *reinterpret_cast<const uint2 *>(p);
+  v[0] = q.x & 0xFFFF; v[1] = q.x >> 16; v[2] = q.y & 0xFFFF; v[3] = q.y >> 16;
+}
+
 template <typename OutT>
 __global__ void __launch_bounds__(256) combine_kernel(const __grid_constant__ CombParams P) {
   const CombNode &N = P.nodes[blockIdx.z];
   const int ti = blockIdx.y, tj = blockIdx.x;
-  const int tx = threadIdx.x, ty = threadIdx.y;
-  const int64_t mh = P.mh, ldp = P.ldp;
-  const int64_t i0 = (int64_t)ti * 32, j0 = (int64_t)tj * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;   // 16 x 16
+  const int64_t mh = P.mh, ldp = P.ldp;            // ldp multiple of 128 -> aligned 8-byte loads
+  const int64_t i0 = (int64_t)ti * 64, j0 = (int64_t)tj * 64;
   const ModP &m = P.mod;
   const uint16_t *P1 = N.P[0], *P2 = N.P[1], *P3 = N.P[2], *P4 = N.P[3], *P5 = N.P[4];
-  __shared__ uint32_t sU[32][33];   // U1 on the mirrored tile (tj, ti)
-  __shared__ uint32_t sQ[32][33];   // P4 on the mirrored tile (tj, ti)
+  __shared__ uint32_t sU[64][65];   // U1 = P1 + P5 on the mirrored tile (tj, ti) (lower part)
+  __shared__ uint32_t sQ[64][65];   // P4 on the mirrored tile
   const bool lowtile = ti >= tj, uptile = ti <= tj;
-  for (int y = ty; y < 32; y += 8) {
-    const int64_t gi = j0 + y, gj = i0 + tx;
-    if (gi < mh && gj < mh) {
-      if (uptile && gi >= gj) sU[y][tx] = addmod(P1[gi * ldp + gj], P5[gi * ldp + gj], m);
-      if (lowtile) sQ[y][tx] = P4[gi * ldp + gj];
+  const int cx = tx * 4;
+#pragma unroll
+  for (int rr = 0; rr < 4; ++rr) {
+    const int y = ty + 16 * rr;
+    const int64_t gi = j0 + y, gj = i0 + cx;      // buffers are rows_pad x rows_pad: always in range
+    uint32_t a[4], b[4];
+    if (uptile) {
+      ld4u16(P1 + gi * ldp + gj, a);
+      ld4u16(P5 + gi * ldp + gj, b);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) sU[y][cx + e] = addmod(a[e], b[e], m);
+    }
+    if (lowtile) {
+      ld4u16(P4 + gi * ldp + gj, a);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) sQ[y][cx + e] = a[e];
     }
   }
   __syncthreads();
   OutT *O = static_cast<OutT *>(N.out);
   const int64_t ov = N.out_valid;
-  for (int y = ty; y < 32; y += 8) {
-    const int64_t i = i0 + y, j = j0 + tx;
+  const bool vec = true;   // store4 checks the alignment of every vector store
+#pragma unroll
+  for (int rr = 0; rr < 4; ++rr) {
+    const int y = ty + 16 * rr;
+    const int64_t i = i0 + y, j = j0 + cx;
     if (i >= mh || j >= mh) continue;
-    const uint32_t p4 = P4[i * ldp + j];
-    uint32_t u1;
-    if (i >= j) u1 = addmod(P1[i * ldp + j], P5[i * ldp + j], m);   // Low(U1) = Low(P1) + Low(P5)
-    else u1 = sU[tx][y];                                             // Up(U1) = Low(U1)^T
-    const uint32_t u2 = addmod(u1, p4, m);                           // U2 = U1 + P4
-    const uint32_t u4 = addmod(u2, P3[i * ldp + j], m);              // U4 = U2 + P3
-    if (mh + i < ov && j < ov) O[(mh + i) * N.ldo + j] = (OutT)u4;   // C21
-    if (i >= j) {
-      const uint32_t u5 = addmod(u2, sQ[tx][y], m);                  // U5 = Low(U2) + Low(P4^T)
-      if (mh + i < ov) O[(mh + i) * N.ldo + mh + j] = (OutT)u5;      // C22
-      const uint32_t u3 = addmod(P1[i * ldp + j], P2[i * ldp + j], m);  // U3 = P1 + P2
-      if (i < ov) O[i * N.ldo + j] = (OutT)u3;                       // C11
+    uint32_t p1[4], p5[4], p4[4], p3[4], u1[4], c21[4];
+    ld4u16(P4 + i * ldp + j, p4);
+    ld4u16(P3 + i * ldp + j, p3);
+    const bool any_low = j <= i;                   // some of the 4 columns are on/below the diagonal
+    if (any_low) { ld4u16(P1 + i * ldp + j, p1); ld4u16(P5 + i * ldp + j, p5); }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      if (j + e <= i) u1[e] = addmod(p1[e], p5[e], m);     // Low(U1) = Low(P1) + Low(P5)
+      else u1[e] = sU[cx + e][y];                          // Up(U1) = Low(U1)^T
+      c21[e] = addmod(addmod(u1[e], p4[e], m), p3[e], m);  // U4 = U1 + P4 + P3
+    }
+    const int64_t n21 = min64(4, min64(mh - j, ov - j));
+    if (mh + i < ov) store4<OutT>(O + (mh + i) * N.ldo + j, vec, n21, c21);                         // C21
+    if (any_low) {
+      uint32_t p2[4], c22[4], c11[4];
+      ld4u16(P2 + i * ldp + j, p2);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        c22[e] = addmod(addmod(u1[e], p4[e], m), sQ[cx + e][y], m);   // U5 = Low(U2) + Low(P4^T)
+        c11[e] = addmod(p1[e], p2[e], m);                              // U3 = P1 + P2
+      }
+      const int64_t nlow = min64(4, i - j + 1);           // columns j..i only
+      if (mh + i < ov) store4<OutT>(O + (mh + i) * N.ldo + mh + j, vec && nlow == 4, min64(nlow, ov - mh - j), c22);
+      if (i < ov) store4<OutT>(O + i * N.ldo + j, vec && nlow == 4, min64(nlow, ov - j), c11);
     }
   }
 }
 
 cudaError_t launch_combine(const CombParams &p, cudaStream_t s) {
   if (p.n_nodes == 0) return cudaSuccess;
-  const unsigned nt = (unsigned)((p.mh + 31) / 32);
-  dim3 grid(nt, nt, (unsigned)p.n_nodes), block(32, 8);
+  const unsigned nt = (unsigned)((p.mh + 63) / 64);
+  dim3 grid(nt, nt, (unsigned)p.n_nodes), block(16, 16);
   if (p.out_u32) combine_kernel<uint32_t><<<grid, block, 0, s>>>(p);
   else combine_kernel<uint16_t><<<grid, block, 0, s>>>(p);
   return cudaGetLastError();
