@@ -225,8 +225,8 @@ def run_gpu(args, cfg, rank, world, local_rank):
         obj = [uid]
         dist.broadcast_object_list(obj, src=0)
         comm = adj.adj_comm_init(world, obj[0], rank)
-        kslice = ((k + world - 1) // world + 7) // 8 * 8
-        ws_bytes = adj.adjprod_modp_workspace_size(m, min(k, kslice), p, phi, depth)
+        k0, k1 = adj.adj_dist_kslice(k, world, rank)
+        ws_bytes = adj.adjprod_modp_workspace_size(m, max(1, k1 - k0), p, phi, depth)
     else:
         ws_bytes = adj.adjprod_modp_workspace_size(m, k, p, phi, depth)
     ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)

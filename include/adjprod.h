@@ -140,6 +140,11 @@ adj_status_t adj_comm_get_unique_id(uint8_t id[128]);
 adj_status_t adj_comm_init(int nranks, const uint8_t id[128], int rank, adj_comm_t *comm);
 adj_status_t adj_comm_destroy(adj_comm_t comm);
 
+/* adj_dist_kslice -- the column slice [k0, k1) of A that rank `rank` of `nranks` owns in
+ *   adjprod_modp_dist (host, no GPU): per = ceil(k / nranks) rounded up to a multiple of 8,
+ *   k0 = min(k, rank * per), k1 = min(k, k0 + per).  Slices are disjoint and cover [0, k). */
+adj_status_t adj_dist_kslice(int64_t k, int nranks, int rank, int64_t *k0, int64_t *k1);
+
 /*
  * adjprod_modp_dist -- collective; every rank of `comm` calls it with the same m, k, p, phi,
  *   root.  Split-K sharding: rank r computes Low(A_r phi(A_r)) on its

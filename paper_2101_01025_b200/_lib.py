@@ -20,7 +20,7 @@ STATUS = {0: "ADJ_OK", 1: "ADJ_ERR_INVALID_VALUE", 2: "ADJ_ERR_UNSUPPORTED_MODUL
 # every symbol include/adjprod.h declares (checked by tests/test_abi.py)
 EXPORTS = ["adjprod_modp", "adjprod_modp_ex", "adjprod_modp_workspace_size", "adjprod_modp_auto_depth",
            "gemm_modp", "adj_skew_unitary", "adj_sos", "adj_mod_lower", "adj_comm_get_unique_id",
-           "adj_comm_init", "adj_comm_destroy", "adjprod_modp_dist", "adj_status_string", "adj_last_error",
+           "adj_comm_init", "adj_comm_destroy", "adjprod_modp_dist", "adj_dist_kslice", "adj_status_string", "adj_last_error",
            "adj_launch_count", "adj_launch_count_reset", "adj_profile_enable", "adj_profile_read"]
 
 
@@ -59,6 +59,7 @@ def lib() -> ctypes.CDLL:
             "adj_comm_init": [ci, ctypes.c_char_p, ci, ctypes.POINTER(vp)],
             "adj_comm_destroy": [vp],
             "adjprod_modp_dist": [i64, i64, u32, ci, vp, i64, vp, i64, ci, vp, ctypes.POINTER(adj_opts_t), vp],
+            "adj_dist_kslice": [i64, ci, ci, ctypes.POINTER(i64), ctypes.POINTER(i64)],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -168,6 +169,12 @@ def adjprod_modp_dist(m, k, p, phi, A, lda, C, ldc, root, comm, depth=-1, flags=
     o = _opts(depth, flags)
     _check(lib().adjprod_modp_dist(m, k, p, phi, _ptr(A), lda, _ptr(C), ldc, root, comm, ctypes.byref(o),
                                    _stream(stream)), "adjprod_modp_dist")
+
+
+def adj_dist_kslice(k, nranks, rank):
+    k0, k1 = ctypes.c_int64(0), ctypes.c_int64(0)
+    _check(lib().adj_dist_kslice(k, nranks, rank, ctypes.byref(k0), ctypes.byref(k1)), "adj_dist_kslice")
+    return k0.value, k1.value
 
 
 def adj_launch_count() -> int:

@@ -87,6 +87,14 @@ adj_status_t adj_comm_destroy(adj_comm_t comm) {
   return ADJ_OK;
 }
 
+adj_status_t adj_dist_kslice(int64_t k, int nranks, int rank, int64_t *k0, int64_t *k1) {
+  if (!k0 || !k1 || k < 0 || nranks < 1 || rank < 0 || rank >= nranks) return ADJ_ERR_INVALID_VALUE;
+  const int64_t per = ((k + nranks - 1) / nranks + 7) / 8 * 8;
+  *k0 = std::min<int64_t>(k, (int64_t)rank * per);
+  *k1 = std::min<int64_t>(k, *k0 + per);
+  return ADJ_OK;
+}
+
 adj_status_t adjprod_modp_dist(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, const uint32_t *A, int64_t lda,
                                uint32_t *C, int64_t ldc, int root, adj_comm_t comm, const adj_opts_t *opts,
                                adj_stream_t stream) {
@@ -95,9 +103,8 @@ adj_status_t adjprod_modp_dist(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, 
   if (m == 0) return ADJ_OK;
   const int G = comm->nranks, r = comm->rank;
   const int w = phi == ADJ_PHI_H ? 2 : 1;
-  // k slice of this rank: ceil(k / G) rounded up to a multiple of 8 columns
-  const int64_t per = ((k + G - 1) / G + 7) / 8 * 8;
-  const int64_t k0 = std::min<int64_t>(k, (int64_t)r * per), k1 = std::min<int64_t>(k, k0 + per);
+  int64_t k0 = 0, k1 = 0;
+  adj_dist_kslice(k, G, r, &k0, &k1);
   const uint32_t *Ar = A ? A + k0 * w : nullptr;
   if (G == 1) return adjprod_modp_ex(m, k1 - k0, p, phi, Ar, lda, C, ldc, opts, stream);
   if (!load_nccl()) return ADJ_ERR_NCCL;
