@@ -267,7 +267,8 @@ adj_status_t run_split(const Plan &P, const InView &v, int64_t rows, int64_t col
   return ADJ_OK;
 }
 
-adj_status_t run_tree(const Plan &P, const InView &root, const Ptrs &x, cudaStream_t s) {
+adj_status_t run_tree(const Plan &P, const InView &root, const Ptrs &x, cudaStream_t s,
+                      uint8_t *side_arena = nullptr) {
   // top-down pre-additions
   std::vector<std::vector<InView>> views(P.depth + 1);
   views[1] = {root};
@@ -303,6 +304,13 @@ adj_status_t run_tree(const Plan &P, const InView &root, const Ptrs &x, cudaStre
       if (l < P.depth) {
         N.s3 = s3buf(P, x.ws, l, n);
         N.s3_ld = L.kh;
+      }
+      if (l == 1 && side_arena != nullptr) {
+        N.side = reinterpret_cast<int8_t *>(side_arena);
+        N.side_kpad = P.kpad0;
+        N.side_rows_pad = P.rows_pad0;
+        N.side_x_row = P.op0_row[0];
+        N.side_y_row = P.op0_row[1];
       }
     }
     LAUNCH_CLS(CLS_PRE, launch_preadd(pp, s));
@@ -359,22 +367,35 @@ adj_status_t run_syrk(const Plan &P, const Ptrs &x, adj_phi_t phi, uint32_t flag
       if (st) return st;
     }
   } else {
-    // 2M (Alg. alg:2M): A = X + iY; H = X phi(Y) = X Y^T; G = (X+Y) phi(X + eps Y), eps = 1
+    // 2M (Alg. alg:2M): A = X + iY; H = X phi(Y) = X Y^T; G = (X+Y) phi(X + eps Y), eps = 1.
+    // X / Y limb planes come from the same pass over A as T (split mode 1 at depth 0, the
+    // root pre-addition's side output at depth >= 1).
     uint8_t *arena0 = x.ws + P.arenas[0].offset;
-    st = run_split(P, make_view(x.A, x.lda, m, k, IN_PAIR_RE), m, k, P.rows_pad0, P.op0_row[0], arena0, s);
-    if (st) return st;
-    st = run_split(P, make_view(x.A, x.lda, m, k, IN_PAIR_IM), m, k, P.rows_pad0, P.op0_row[1], arena0, s);
-    if (st) return st;
     InView troot = make_view(x.A, x.lda, m, k, IN_PAIR_SUM);
     uint16_t *G = reinterpret_cast<uint16_t *>(x.ws + P.g_offset);
     uint16_t *H = reinterpret_cast<uint16_t *>(x.ws + P.h_offset);
     if (P.depth == 0) {
-      st = run_split(P, troot, m, k, P.rows_pad0, P.op0_row[2], arena0, s);
-      if (st) return st;
+      SplitParams sp;
+      std::memset(&sp, 0, sizeof(sp));
+      sp.in = troot;
+      sp.rows = m; sp.cols = k;
+      sp.rows_pad = P.rows_pad0; sp.kpad = P.kpad0;
+      sp.op_row = P.op0_row[0]; sp.op_row2 = P.op0_row[1]; sp.op_row3 = P.op0_row[2];
+      sp.arena = reinterpret_cast<int8_t *>(arena0);
+      sp.scheme = P.scheme; sp.planes = P.planes; sp.mode = 1; sp.mod = P.mod;
+      LAUNCH_CLS(CLS_PRE, launch_split(sp, s));
       st = launch_leaf_all(P, x, s);
       if (st) return st;
     } else {
-      st = run_tree(P, troot, x, s);
+      // arena-0 padding the root pre-addition does not cover: rows [2 mh, rows_pad0), columns [2 kh, kpad0)
+      const int64_t mh = P.lv[1].mh, kh = P.lv[1].kh, rp0 = P.rows_pad0, kp0 = P.kpad0;
+      for (int op = 0; op < 2; ++op)
+        for (int pl = 0; pl < P.planes; ++pl) {
+          uint8_t *base = arena0 + (size_t)(P.op0_row[op] + (int64_t)pl * rp0) * kp0;
+          if (2 * mh < rp0) CUDA_TRY(cudaMemsetAsync(base + (size_t)(2 * mh) * kp0, 0, (size_t)(rp0 - 2 * mh) * kp0, s));
+          if (2 * kh < kp0) CUDA_TRY(cudaMemset2DAsync(base + 2 * kh, kp0, 0, kp0 - 2 * kh, 2 * mh, s));
+        }
+      st = run_tree(P, troot, x, s, arena0);
       if (st) return st;
       st = launch_leaf_all(P, x, s);
       if (st) return st;

@@ -633,6 +633,31 @@ __device__ __forceinline__ void load4_fast(const void *ptr, int64_t off, const M
   }
 }
 
+// re / im of 4 consecutive GF(p^2) elements (interleaved pairs), reduced mod p
+__device__ __forceinline__ void load4_pair(const InView &v, int64_t R, int64_t C, bool fast, const ModP &m,
+                                           uint32_t (&re)[4], uint32_t (&im)[4]) {
+  if (fast) {
+    const uint4 *p = reinterpret_cast<const uint4 *>(static_cast<const uint32_t *>(v.ptr) + 2 * (R * v.ld + C));
+    uint4 a = __ldg(p), b = __ldg(p + 1);
+    re[0] = mod_u32(a.x, m); im[0] = mod_u32(a.y, m); re[1] = mod_u32(a.z, m); im[1] = mod_u32(a.w, m);
+    re[2] = mod_u32(b.x, m); im[2] = mod_u32(b.y, m); re[3] = mod_u32(b.z, m); im[3] = mod_u32(b.w, m);
+  } else {
+    InView vr = v, vi = v;
+    vr.type = IN_PAIR_RE;
+    vi.type = IN_PAIR_IM;
+    load4(vr, R, C, m, re);
+    load4(vi, R, C, m, im);
+  }
+}
+
+template <int SCHEME>
+__device__ __forceinline__ void put_side(const PreNode &N, int64_t R, int64_t C, const uint32_t (&re)[4],
+                                         const uint32_t (&im)[4], const ModP &m) {
+  const int64_t ps = N.side_rows_pad * N.side_kpad;
+  put_limbs4<SCHEME>(N.side + (N.side_x_row + R) * N.side_kpad + C, ps, re, m);
+  put_limbs4<SCHEME>(N.side + (N.side_y_row + R) * N.side_kpad + C, ps, im, m);
+}
+
 template <int SCHEME, int YK, int T>
 __device__ __forceinline__ void preadd_row(const PreParams &P, const PreNode &N, int64_t r, int64_t c) {
   const ModP &m = P.mod;
@@ -641,7 +666,25 @@ __device__ __forceinline__ void preadd_row(const PreParams &P, const PreNode &N,
   uint32_t x11a[4], x11b[4], x12a[4], x12b[4], x21a[4], x21b[4], x22a[4], x22b[4];
   const bool top_ok = r < P.mh && r < v.rows_valid;
   const bool bot_ok = r < P.mh && P.mh + r < v.rows_valid;
-  if (v.vec_ok && top_ok && bot_ok && P.kh + c + h2 + 3 < v.cols_valid) {
+  const bool fast = v.vec_ok && top_ok && bot_ok && P.kh + c + h2 + 3 < v.cols_valid;
+  if (T == IN_PAIR_SUM && N.side != nullptr) {
+    // 2M root: T = Re(A) + Im(A) for the pre-addition, and the limb planes of Re(A), Im(A) for H
+    InView vv = v;
+    if (r >= P.mh) vv.rows_valid = 0;
+    const int64_t R[2] = {r, P.mh + r};
+    const int64_t Cc[4] = {c, c + h2, P.kh + c, P.kh + c + h2};
+    uint32_t(*dst[2][4])[4] = {{&x11a, &x11b, &x12a, &x12b}, {&x21a, &x21b, &x22a, &x22b}};
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        uint32_t re[4], im[4];
+        load4_pair(vv, R[a], Cc[b], fast, m, re, im);
+        if (r < P.mh) put_side<SCHEME>(N, R[a], Cc[b], re, im, m);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) (*dst[a][b])[e] = addmod(re[e], im[e], m);
+      }
+  } else if (fast) {
     const int64_t o1 = r * v.ld, o2 = (P.mh + r) * v.ld;
     load4_fast<T>(v.ptr, o1 + c, m, x11a);
     load4_fast<T>(v.ptr, o1 + c + h2, m, x11b);
@@ -750,6 +793,21 @@ __global__ void __launch_bounds__(256) split_kernel(const __grid_constant__ Spli
   for (int64_t r = blockIdx.y; r < P.rows_pad; r += gridDim.y) {
     uint32_t x[4];
     const InView &v = P.in;
+    if (P.mode == 1) {
+      // 2M at depth 0: one read of the interleaved A gives X = Re, Y = Im and T = X + Y
+      InView vv = v;
+      if (r >= P.rows) vv.rows_valid = 0;
+      if (c >= P.cols) vv.cols_valid = 0;
+      const bool fast = vv.vec_ok && r < vv.rows_valid && c + 3 < vv.cols_valid;
+      uint32_t re[4], im[4];
+      load4_pair(vv, r, c, fast, P.mod, re, im);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) x[e] = addmod(re[e], im[e], P.mod);
+      put_limbs4<SCHEME>(P.arena + (P.op_row + r) * P.kpad + c, ps, re, P.mod);
+      put_limbs4<SCHEME>(P.arena + (P.op_row2 + r) * P.kpad + c, ps, im, P.mod);
+      put_limbs4<SCHEME>(P.arena + (P.op_row3 + r) * P.kpad + c, ps, x, P.mod);
+      continue;
+    }
     if (v.vec_ok && r < P.rows && r < v.rows_valid && c + 3 < v.cols_valid && c + 3 < P.cols && v.type == IN_U32) {
       load4_fast<IN_U32>(v.ptr, r * v.ld + c, P.mod, x);
     } else {

@@ -67,6 +67,10 @@ struct PreNode {
   int64_t op_row[OUT_N];   // arena row of plane 0 for each output operand; -1 = not produced
   uint16_t *s3;            // materialised S3 residues (when S3 recurses), else null
   int64_t s3_ld;
+  // 2M side output (root node, IN_PAIR_SUM input): limb planes of X = Re(A) and Y = Im(A) for
+  // the general product H = X Y^T, written from the same read of A as the pre-addition of T.
+  int8_t *side;            // arena 0 or null
+  int64_t side_kpad, side_rows_pad, side_x_row, side_y_row;
 };
 
 struct PreParams {
@@ -88,8 +92,10 @@ struct SplitParams {
   int64_t rows, cols;      // logical size (>= valid); padding written as zero
   int64_t rows_pad, kpad;
   int64_t op_row;
+  int64_t op_row2, op_row3;  // mode 1 (2M): Y = Im(A) and T = Re + Im planes
   int8_t *arena;
   int32_t scheme, planes;
+  int32_t mode;              // 0: plain split of `in`; 1: 2M split of interleaved pairs
   ModP mod;
 };
 
