@@ -123,12 +123,14 @@ class ClockSampler:
                 "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
-def load_traffic(config: str):
-    """dram bytes per leaf launch from the committed ncu --set full summary, if present."""
+def load_traffic(config: str, depth: int):
+    """dram__bytes_read + dram__bytes_write per leaf launch from the committed ncu --set full
+    summary (profiles/leaf_traffic.json) when it was captured for this config and depth."""
     path = os.path.join(ROOT, "profiles", "leaf_traffic.json")
     try:
         with open(path) as f:
-            return json.load(f).get(config)
+            d = json.load(f).get(config)
+        return d["dram_bytes_per_launch"] if d and d.get("depth") == depth else None
     except Exception:
         return None
 
@@ -314,7 +316,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
     achieved = ops / (leaf_avg_ms * 1e-3) / 1e12
     peak = 2.0 * peaks["bf16_tflops"]        # int8 dense = 2 x bf16 dense (guide's nominal ratio)
     roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-            "traffic": load_traffic(args.config),
+            "traffic": load_traffic(args.config, depth),
             "kernel": "leaf_kernel (grouped tcgen05 kind::i8 GEMM/SYRK + mod-p epilogue)",
             "peak_source": f"{src}: 2 x bf16_tflops ({peaks['bf16_tflops']}) burst, int8 = 2x bf16 nominal",
             "algorithmic_ops_per_launch": ops, "leaf_ms_per_launch": leaf_avg_ms}
