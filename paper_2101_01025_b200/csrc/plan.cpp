@@ -109,11 +109,19 @@ static void set_grid(Plan &P, int num_sms) {
   else P.grid = (int)std::min<int64_t>(num_sms, nt);
 }
 
+// Depth choice (R13), from measured B200 crossovers: one level of Alg. alg:MIAHMM
+// saves 1/8 of the leaf MMA work but adds a K1 and a K4 pass over HBM; it pays once the leaves
+// stay >= 4096 rows (phi = T) -- for phi = H the 2M general product H dominates and the leaves
+// of G must stay >= 8192 rows.  Deeper levels are also used when the level-1 inner dimension
+// would exceed the int32 accumulation bound of the limb scheme.
 int auto_depth(int64_t m, int64_t k, uint32_t p, int phi) {
-  (void)p; (void)phi;
-  if (m < 256 || k < 256) return 0;
-  int d = 1;
-  while (d < 3 && cdiv(m, (int64_t)1 << (d + 1)) >= 4096 && cdiv(k, (int64_t)1 << (d + 1)) >= 1024) ++d;
+  const int64_t leaf_min = phi == 0 ? 4096 : 8192;
+  int d = 0;
+  while (d < 3 && cdiv(m, (int64_t)1 << (d + 1)) >= leaf_min && cdiv(k, (int64_t)1 << (d + 1)) >= 1024) ++d;
+  const int64_t kmax = limb_kmax(limb_scheme(p), p);
+  int64_t kh = k;
+  for (int l = 1; l <= d; ++l) kh = 8 * cdiv(kh, 16);
+  while (d < 3 && std::max<int64_t>(kBK, rup(kh, kBK)) > kmax) { ++d; kh = 8 * cdiv(kh, 16); }
   return d;
 }
 

@@ -1,0 +1,95 @@
+"""Full-size parity at every BASELINE config, in the launch configuration bench.py times
+(same depth choice, same seeded device-generated inputs): sampled rows against the O1 oracle
+(bit-exact), Vandermonde closed forms on sampled rows, and a Freivalds check of the whole
+lower triangle (C r = A (A^T r) mod p, exact in float64 here)."""
+import numpy as np
+import pytest
+
+import oracle
+from oracle import closed_forms as cf
+from inputs import vandermonde_points, vandermonde_matrix
+from gpu_util import freivalds as _freivalds
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+    assert torch.cuda.is_available()
+    import paper_2101_01025_b200 as adj
+    import bench
+    return torch, adj, bench
+
+
+def _run(env, cfg, A_dev):
+    torch, adj, bench = env
+    m, k, p = cfg["m"], cfg["k"], cfg["p"]
+    phi = adj.ADJ_PHI_H if cfg["phi"] == "H" else adj.ADJ_PHI_T
+    depth = cfg["depth"] if cfg["depth"] is not None else adj.adjprod_modp_auto_depth(m, k, p, phi)
+    w = 2 if phi else 1
+    C = torch.zeros((m, m * w), dtype=torch.int32, device="cuda")
+    adj.adjprod_modp_ex(m, k, p, phi, A_dev, k, C, m, depth=depth)
+    torch.cuda.synchronize()
+    return C, depth
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c5", "c4", "c3"])
+def test_config_sampled_rows_and_freivalds(env, name):
+    torch, adj, bench = env
+    from inputs.gpu import uniform_residues_cuda
+    cfg = bench.CONFIGS[name]
+    m, k, p = cfg["m"], cfg["k"], cfg["p"]
+    w = 2 if cfg["phi"] == "H" else 1
+    A = torch.empty((m, k * w), dtype=torch.int32, device="cuda")
+    uniform_residues_cuda(A, seed=1, p=p)
+    C, depth = _run(env, cfg, A)
+    Ah = A.cpu().numpy().view(np.uint32).reshape((m, k, 2) if w == 2 else (m, k))
+    Ch = C.cpu().numpy().view(np.uint32).reshape((m, m, 2) if w == 2 else (m, m))
+    del C
+    rng = np.random.default_rng(7)
+    rows = sorted({0, 1, m // 2, m - 2, m - 1} | set(int(x) for x in rng.integers(0, m, 3)))
+    f = oracle.syrk_h if w == 2 else oracle.syrk_t
+    for r in rows:
+        ref = f(Ah, p, rows=(r, r + 1))
+        assert np.array_equal(Ch[r, : r + 1], ref[r, : r + 1]), (name, depth, r)
+    if w == 1 and m * k <= 8192 * 8192:
+        assert _freivalds(Ah, Ch, p), (name, depth)
+
+
+@pytest.mark.parametrize("name", ["c2", "c3"])
+def test_config_vandermonde_closed_form(env, name):
+    """A[i][t] = x_i^t: every entry of Low(C) is a geometric sum; check 64 random full rows."""
+    torch, adj, bench = env
+    cfg = dict(bench.CONFIGS[name])
+    m, k, p = cfg["m"], cfg["k"], cfg["p"]
+    if name == "c3":                     # keep host generation bounded: 32768 x 8192 slice of k
+        k = cfg["k"] = 8192
+    x = vandermonde_points(m, 3, p)
+    Ah = vandermonde_matrix(x, k, p)
+    A = torch.from_numpy(Ah.view(np.int32)).cuda()
+    C, depth = _run(env, cfg, A)
+    Ch = C.cpu().numpy().view(np.uint32)
+    rng = np.random.default_rng(1)
+    rows = sorted(set(int(r) for r in rng.integers(0, m, 64)) | {m - 1})
+    ref = cf.vandermonde_syrk_entries(x, rows, k, p)
+    for r, rr in zip(rows, ref):
+        assert np.array_equal(Ch[r, : r + 1].astype(np.int64), rr), (name, depth, r)
+
+
+def test_c5_vandermonde_hermitian(env):
+    torch, adj, bench = env
+    cfg = bench.CONFIGS["c5"]
+    m, k, p = cfg["m"], 2048, cfg["p"]
+    rng = np.random.default_rng(5)
+    z = rng.integers(1, p, size=(m, 2))
+    Ah = vandermonde_matrix(z, k, p)
+    A = torch.from_numpy(Ah.reshape(m, 2 * k).view(np.int32)).cuda()
+    cfg2 = dict(cfg, k=k)
+    C, depth = _run(env, cfg2, A)
+    Ch = C.cpu().numpy().view(np.uint32).reshape(m, m, 2)
+    rows = sorted(set(int(r) for r in rng.integers(0, m, 32)) | {m - 1})
+    ref = cf.vandermonde_herk_entries(z, rows, k, p)
+    for r, (re, im) in zip(rows, ref):
+        assert np.array_equal(Ch[r, : r + 1, 0].astype(np.int64), re) and \
+            np.array_equal(Ch[r, : r + 1, 1].astype(np.int64), im), r

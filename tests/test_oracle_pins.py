@@ -183,3 +183,17 @@ def test_inputs_generator_known_values():
     # uniform-ish: all residues in range, mean near (p-1)/2
     big = uniform_matrix(512, 512, 3, 65521)
     assert big.max() < 65521 and abs(big.mean() - 32760) < 200
+
+
+def test_freivalds_helper_has_teeth():
+    """The full-size GPU check (tests/gpu_util.freivalds) accepts the oracle's Low(C) and
+    rejects it after any single-entry corruption (upper-triangle completion included)."""
+    from gpu_util import freivalds
+    p = 8191
+    A = uniform_matrix(300, 150, seed=3, p=p)
+    C = oracle.syrk_t(A, p)
+    assert freivalds(A, C, p)
+    for (i, j) in [(0, 0), (299, 0), (150, 149), (299, 299)]:
+        bad = C.copy()
+        bad[i, j] = (bad[i, j] + 1) % p
+        assert not freivalds(A, bad, p), (i, j)
