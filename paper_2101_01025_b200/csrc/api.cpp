@@ -244,8 +244,7 @@ adj_status_t launch_leaf_all(const Plan &P, const Ptrs &x, cudaStream_t s) {
   }
   L.tiles = P.d_tiles;
   L.n_tiles = (int32_t)P.tiles.size();
-  if (P.leaf_ver == 2) LAUNCH_CLS(CLS_LEAF, launch_leaf2(L, P.nacc, P.grid, s));
-  else LAUNCH_CLS(CLS_LEAF, launch_leaf(L, P.bn, P.nacc, P.grid, s));
+  LAUNCH_CLS(CLS_LEAF, launch_leaf2(L, P.nacc, P.segmented, P.grid, s));
   return ADJ_OK;
 }
 

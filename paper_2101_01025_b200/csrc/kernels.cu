@@ -24,17 +24,6 @@ namespace adj {
 __host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
 
 // ============================================================================ leaf kernel
-template <int BN>
-struct LeafCfg {
-  static constexpr int STAGES = (BN == 256) ? 4 : 6;
-  static constexpr int SLOTS = 512 / BN;            // TMEM accumulator slots of BN columns
-  static constexpr int A_BYTES = kBM * kBK;         // 16 KiB
-  static constexpr int B_BYTES = BN * kBK;
-  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int BAR_BYTES = 8 * (2 * STAGES + 2 * SLOTS) + 16;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + BAR_BYTES;
-};
-
 __device__ __forceinline__ void decode_tile(uint32_t packed, int &q, int &I, int &J) {
   q = (int)(packed >> 24);
   I = (int)((packed >> 12) & 0xFFF);
@@ -78,209 +67,6 @@ __device__ __forceinline__ void store_chunk(const LeafProduct &pr, int64_t row, 
   }
 }
 
-// Warp roles (256 threads): warp 0 = TMA producer, warp 1 = MMA issuer, warp 2 = TMEM
-// allocator, warp 3 idle, warps 4..7 = epilogue (warp w reads TMEM lanes 32(w%4)..+31).
-// Work stream per CTA: tiles blockIdx.x, +gridDim.x, ...; per tile NACC accumulators, each a
-// full K loop into its own TMEM slot (slot = unit % SLOTS) so that the epilogue of one
-// accumulator overlaps the MMAs of the next.
-template <int BN, int NACC>
-__global__ void __launch_bounds__(256, 1) leaf_kernel(const __grid_constant__ LeafParams P) {
-  using Cfg = LeafCfg<BN>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t *full_bar = reinterpret_cast<uint64_t *>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
-  uint64_t *empty_bar = full_bar + Cfg::STAGES;
-  uint64_t *slot_full = empty_bar + Cfg::STAGES;
-  uint64_t *slot_empty = slot_full + Cfg::SLOTS;
-  uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(slot_empty + Cfg::SLOTS);
-
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-
-  if (warp == 0 && lane == 0) {
-    for (int s = 0; s < Cfg::STAGES; ++s) {
-      ptx::mbar_init(&full_bar[s], 1);
-      ptx::mbar_init(&empty_bar[s], 1);
-    }
-    for (int s = 0; s < Cfg::SLOTS; ++s) {
-      ptx::mbar_init(&slot_full[s], 1);
-      ptx::mbar_init(&slot_empty[s], 4);
-    }
-    ptx::fence_barrier_init();
-    for (int i = 0; i < kMaxMaps; ++i) ptx::prefetch_tmap(&P.maps[i]);
-  }
-  if (warp == 2) ptx::tmem_alloc(tmem_holder, 512);
-  ptx::tc_fence_before();
-  __syncthreads();
-  ptx::tc_fence_after();
-  const uint32_t tmem_base = *tmem_holder;
-
-  if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int t = blockIdx.x; t < P.n_tiles; t += gridDim.x) {
-        int q, I, J;
-        decode_tile(P.tiles[t], q, I, J);
-        const LeafProduct &pr = P.prod[q];
-        const CUtensorMap *map = &P.maps[pr.map];
-        const int arow = pr.a_row0 + I * kBM;
-        const int brow = pr.b_row0 + J * BN;
-#pragma unroll 1
-        for (int j = 0; j < NACC; ++j) {
-#pragma unroll 1
-          for (int kb = 0; kb < pr.kblocks; ++kb) {
-#pragma unroll 1
-            for (int tt = P.acc_begin[j]; tt < P.acc_begin[j + 1]; ++tt) {
-              const LeafTerm term = P.terms[tt];
-              ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
-              ptx::mbar_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
-              uint8_t *sa = smem + stage * Cfg::STAGE_BYTES;
-              uint8_t *sb = sa + Cfg::A_BYTES;
-              ptx::tma_load_2d(sa, map, kb * kBK, arow + term.a_plane * pr.a_plane_rows, &full_bar[stage]);
-#pragma unroll
-              for (int h = 0; h < BN / 128; ++h)
-                ptx::tma_load_2d(sb + h * 128 * kBK, map, kb * kBK,
-                                 brow + term.b_plane * pr.b_plane_rows + h * 128, &full_bar[stage]);
-              if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
-            }
-          }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer (one thread)
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      uint32_t unit = 0;
-      for (int t = blockIdx.x; t < P.n_tiles; t += gridDim.x) {
-        int q, I, J;
-        decode_tile(P.tiles[t], q, I, J);
-        const LeafProduct &pr = P.prod[q];
-#pragma unroll 1
-        for (int j = 0; j < NACC; ++j, ++unit) {
-          const uint32_t slot = unit % Cfg::SLOTS, use = unit / Cfg::SLOTS;
-          ptx::mbar_wait(&slot_empty[slot], (use & 1) ^ 1);
-          ptx::tc_fence_after();
-          const uint32_t d_tmem = tmem_base + slot * BN;
-          uint32_t accumulate = 0;
-#pragma unroll 1
-          for (int kb = 0; kb < pr.kblocks; ++kb) {
-#pragma unroll 1
-            for (int tt = P.acc_begin[j]; tt < P.acc_begin[j + 1]; ++tt) {
-              const LeafTerm term = P.terms[tt];
-              const uint32_t idesc = ptx::idesc_i8(kBM, BN, term.a_signed != 0, term.b_signed != 0);
-              ptx::mbar_wait(&full_bar[stage], phase);
-              ptx::tc_fence_after();
-              const uint32_t sa = ptx::smem_u32(smem + stage * Cfg::STAGE_BYTES);
-              const uint64_t adesc = ptx::smem_desc_sw128(sa);
-              const uint64_t bdesc = ptx::smem_desc_sw128(sa + Cfg::A_BYTES);
-#pragma unroll
-              for (int kk = 0; kk < kBK / 32; ++kk) {   // UMMA_K = 32 bytes of int8
-                ptx::mma_i8(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, idesc, accumulate);
-                accumulate = 1;
-              }
-              ptx::mma_commit(&empty_bar[stage]);     // frees the smem stage when MMAs finish
-              if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
-            }
-          }
-          ptx::mma_commit(&slot_full[slot]);          // accumulator ready for the epilogue
-        }
-      }
-    }
-  } else if (warp >= 4) {
-    // ------------------------------------------------------------ epilogue
-    const int ew = warp - 4;
-    const uint32_t lane_off = (uint32_t)(ew * 32) << 16;
-    const ModP mod = P.mod;
-    uint32_t unit = 0;
-    for (int t = blockIdx.x; t < P.n_tiles; t += gridDim.x) {
-      int q, I, J;
-      decode_tile(P.tiles[t], q, I, J);
-      const LeafProduct &pr = P.prod[q];
-      const int64_t row = (int64_t)I * kBM + ew * 32 + lane;
-      const int64_t col0 = (int64_t)J * BN;
-      uint32_t part[NACC > 1 ? BN / 2 : 1];
-#pragma unroll
-      for (int j = 0; j < NACC; ++j, ++unit) {
-        const uint32_t slot = unit % Cfg::SLOTS, use = unit / Cfg::SLOTS;
-        ptx::mbar_wait(&slot_full[slot], use & 1);
-        ptx::tc_fence_after();
-        const uint32_t w = P.weight[j];
-#pragma unroll
-        for (int c = 0; c < BN / 32; ++c) {
-          uint32_t v[32];
-          ptx::tmem_ld32(tmem_base + lane_off + slot * BN + c * 32, v);
-          ptx::tmem_wait_ld();
-          uint32_t r[32];
-#pragma unroll
-          for (int e = 0; e < 32; ++e) r[e] = mod_s32((int32_t)v[e], mod);
-          if constexpr (NACC == 1) {
-            if (w != 1) {
-#pragma unroll
-              for (int e = 0; e < 32; ++e) r[e] = mulmod(r[e], w, mod);
-            }
-            store_chunk(pr, row, col0 + c * 32, r);
-          } else {
-#pragma unroll
-            for (int e = 0; e < 32; ++e) r[e] = mulmod(r[e], w, mod);
-            if (j == 0) {
-#pragma unroll
-              for (int e = 0; e < 16; ++e) part[c * 16 + e] = r[2 * e] | (r[2 * e + 1] << 16);
-            } else {
-#pragma unroll
-              for (int e = 0; e < 16; ++e) {
-                r[2 * e] = addmod(r[2 * e], part[c * 16 + e] & 0xFFFF, mod);
-                r[2 * e + 1] = addmod(r[2 * e + 1], part[c * 16 + e] >> 16, mod);
-              }
-              if (j == NACC - 1) {
-                store_chunk(pr, row, col0 + c * 32, r);
-              } else {
-#pragma unroll
-                for (int e = 0; e < 16; ++e) part[c * 16 + e] = r[2 * e] | (r[2 * e + 1] << 16);
-              }
-            }
-          }
-        }
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&slot_empty[slot]);
-      }
-    }
-  }
-
-  ptx::tc_fence_before();
-  __syncthreads();
-  if (warp == 2) {
-    ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem_base, 512);
-  }
-}
-
-template <int BN, int NACC>
-static cudaError_t launch_leaf_t(const LeafParams &p, int grid, cudaStream_t s) {
-  using Cfg = LeafCfg<BN>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(leaf_kernel<BN, NACC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         Cfg::SMEM);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
-  leaf_kernel<BN, NACC><<<grid, 256, Cfg::SMEM, s>>>(p);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_leaf(const LeafParams &p, int bn, int nacc, int grid, cudaStream_t s) {
-  if (p.n_tiles == 0) return cudaSuccess;
-  if (bn == 256 && nacc == 1) return launch_leaf_t<256, 1>(p, grid, s);
-  if (bn == 128 && nacc == 3) return launch_leaf_t<128, 3>(p, grid, s);
-  if (bn == 128 && nacc == 1) return launch_leaf_t<128, 1>(p, grid, s);
-  return cudaErrorInvalidValue;
-}
-
 // ============================================================================ leaf kernel, CTA pair
 // cta_group::2 version: a cluster of 2 CTAs (one TPC) computes a 256 x 256 tile with
 // tcgen05.mma.cta_group::2 M=256 N=256 K=32 (int8).  CTA r holds rows r*128.. of the A tile and
@@ -289,9 +75,9 @@ cudaError_t launch_leaf(const LeafParams &p, int bn, int nacc, int grid, cudaStr
 // + MMA operand reads 64 B/clk at full tensor rate).  TMEM holds 2 slots of 256 columns; the NACC
 // limb accumulators of a tile run one after the other (acc-major), the epilogue folds each into
 // a weighted mod-p partial sum kept in registers (8 warps x 128 columns).
-template <int NACC>
+template <int NACC, bool PART>
 struct Leaf2Cfg {
-  static constexpr int STAGES = NACC > 1 ? 5 : 6;
+  static constexpr int STAGES = PART ? 5 : 6;
   static constexpr int TILE = 256;
   static constexpr int A_BYTES = 128 * kBK;
   static constexpr int B_BYTES = 128 * kBK;
@@ -300,16 +86,19 @@ struct Leaf2Cfg {
   // weighted mod-p partial sums of the limb accumulators: 128 rows x 128 words (u16 pairs),
   // row stride 129 words so that the 32 rows a warp touches fall in 32 different banks
   static constexpr int PART_STRIDE = 129;
-  static constexpr int PART_BYTES = NACC > 1 ? 128 * PART_STRIDE * 4 : 0;
+  static constexpr int PART_BYTES = PART ? 128 * PART_STRIDE * 4 : 0;
   static constexpr int BAR_BYTES = 8 * (2 * STAGES + 2 * SLOTS) + 16;
   static constexpr int SMEM = STAGES * STAGE_BYTES + PART_BYTES + 1024 + BAR_BYTES;
   static constexpr int THREADS = 384;
 };
 
-template <int NACC>
+// NACC limb accumulators per tile; each may be split into K segments of at most pr.kseg k-blocks
+// (int32 bound).  A (accumulator, segment) pair is one TMEM unit; PART = the
+// epilogue folds units into the shared-memory partial sum (needed when a tile has > 1 unit).
+template <int NACC, bool PART>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     leaf2_kernel(const __grid_constant__ LeafParams P) {
-  using Cfg = Leaf2Cfg<NACC>;
+  using Cfg = Leaf2Cfg<NACC, PART>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint32_t *part_s = reinterpret_cast<uint32_t *>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
@@ -357,10 +146,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         const CUtensorMap *map = &P.maps[pr.map];
         const int arow = pr.a_row0 + I * Cfg::TILE + (int)rank * 128;
         const int brow = pr.b_row0 + J * Cfg::TILE + (int)rank * 128;
+        const int nseg = (pr.kblocks + pr.kseg - 1) / pr.kseg;
 #pragma unroll 1
-        for (int j = 0; j < NACC; ++j) {
+        for (int u = 0; u < NACC * nseg; ++u) {
+          const int j = u / nseg, kb0 = (u % nseg) * pr.kseg;
+          const int kb1 = min(pr.kblocks, kb0 + pr.kseg);
 #pragma unroll 1
-          for (int kb = 0; kb < pr.kblocks; ++kb) {
+          for (int kb = kb0; kb < kb1; ++kb) {
 #pragma unroll 1
             for (int tt = P.acc_begin[j]; tt < P.acc_begin[j + 1]; ++tt) {
               const LeafTerm term = P.terms[tt];
@@ -386,15 +178,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         int q, I, J;
         decode_tile(P.tiles[t], q, I, J);
         const LeafProduct &pr = P.prod[q];
+        const int nseg = (pr.kblocks + pr.kseg - 1) / pr.kseg;
 #pragma unroll 1
-        for (int j = 0; j < NACC; ++j, ++unit) {
+        for (int u = 0; u < NACC * nseg; ++u, ++unit) {
+          const int j = u / nseg, kb0 = (u % nseg) * pr.kseg;
+          const int kb1 = min(pr.kblocks, kb0 + pr.kseg);
           const uint32_t slot = unit & 1, use = unit >> 1;
           ptx::mbar_wait_cluster(&slot_empty[slot], (use & 1) ^ 1);
           ptx::tc_fence_after();
           const uint32_t d_tmem = tmem_base + slot * Cfg::TILE;
           uint32_t accumulate = 0;
 #pragma unroll 1
-          for (int kb = 0; kb < pr.kblocks; ++kb) {
+          for (int kb = kb0; kb < kb1; ++kb) {
 #pragma unroll 1
             for (int tt = P.acc_begin[j]; tt < P.acc_begin[j + 1]; ++tt) {
               const LeafTerm term = P.terms[tt];
@@ -434,8 +229,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       const LeafProduct &pr = P.prod[q];
       const int64_t row = (int64_t)I * Cfg::TILE + rank * 128 + lrow;
       const int64_t col0 = (int64_t)J * Cfg::TILE + h * 128;
+      const int nseg = (pr.kblocks + pr.kseg - 1) / pr.kseg;
+      const int nunits = NACC * nseg;
 #pragma unroll 1
-      for (int j = 0; j < NACC; ++j, ++unit) {
+      for (int u = 0; u < nunits; ++u, ++unit) {
+        const int j = u / nseg;
         const uint32_t slot = unit & 1, use = unit >> 1;
         ptx::mbar_wait(&slot_full[slot], use & 1);
         ptx::tc_fence_after();
@@ -451,9 +249,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
 #pragma unroll
             for (int e = 0; e < 32; ++e) v[e] = mulmod(v[e], w, mod);
           }
-          if constexpr (NACC > 1) {
+          if constexpr (PART) {
             uint32_t *pc = prow + c * 16;
-            if (j > 0) {
+            if (u > 0) {
 #pragma unroll
               for (int e = 0; e < 16; ++e) {
                 const uint32_t wd = pc[e];
@@ -461,7 +259,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
                 v[2 * e + 1] = addmod(v[2 * e + 1], wd >> 16, mod);
               }
             }
-            if (j < NACC - 1) {
+            if (u < nunits - 1) {
 #pragma unroll
               for (int e = 0; e < 16; ++e) pc[e] = v[2 * e] | (v[2 * e + 1] << 16);
               continue;
@@ -485,24 +283,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   }
 }
 
-template <int NACC>
+template <int NACC, bool PART>
 static cudaError_t launch_leaf2_t(const LeafParams &p, int grid, cudaStream_t s) {
+  using Cfg = Leaf2Cfg<NACC, PART>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(leaf2_kernel<NACC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         Leaf2Cfg<NACC>::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(leaf2_kernel<NACC, PART>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Cfg::SMEM);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  leaf2_kernel<NACC><<<grid, Leaf2Cfg<NACC>::THREADS, Leaf2Cfg<NACC>::SMEM, s>>>(p);
+  leaf2_kernel<NACC, PART><<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(p);
   return cudaGetLastError();
 }
 
-cudaError_t launch_leaf2(const LeafParams &p, int nacc, int grid, cudaStream_t s) {
+cudaError_t launch_leaf2(const LeafParams &p, int nacc, bool segmented, int grid, cudaStream_t s) {
   if (p.n_tiles == 0) return cudaSuccess;
   if (grid % 2) return cudaErrorInvalidValue;
-  if (nacc == 1) return launch_leaf2_t<1>(p, grid, s);
-  if (nacc == 3) return launch_leaf2_t<3>(p, grid, s);
+  if (nacc == 1) return segmented ? launch_leaf2_t<1, true>(p, grid, s) : launch_leaf2_t<1, false>(p, grid, s);
+  if (nacc == 3) return launch_leaf2_t<3, true>(p, grid, s);
   return cudaErrorInvalidValue;
 }
 

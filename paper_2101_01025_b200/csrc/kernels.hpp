@@ -6,8 +6,7 @@
 
 namespace adj {
 
-cudaError_t launch_leaf(const LeafParams &p, int bn, int nacc, int grid, cudaStream_t s);
-cudaError_t launch_leaf2(const LeafParams &p, int nacc, int grid, cudaStream_t s);  // CTA-pair, 256x256 tiles
+cudaError_t launch_leaf2(const LeafParams &p, int nacc, bool segmented, int grid, cudaStream_t s);  // CTA-pair, 256x256 tiles
 cudaError_t launch_preadd(const PreParams &p, cudaStream_t s);
 cudaError_t launch_split(const SplitParams &p, cudaStream_t s);
 cudaError_t launch_combine(const CombParams &p, cudaStream_t s);

@@ -16,11 +16,9 @@ static void fill_scheme(Plan &P, uint32_t p) {
   P.scheme = limb_scheme(p);
   P.planes = limb_planes(P.scheme);
   P.nacc = limb_accs(P.scheme);
-  P.bn = P.scheme == LIMB_S8 ? 256 : 128;
-  const char *lv = getenv("ADJ_LEAF");
-  P.leaf_ver = (lv && lv[0] == '1') ? 1 : 2;
-  P.tile_m = P.leaf_ver == 2 ? 256 : kBM;
-  P.tile_n = P.leaf_ver == 2 ? 256 : P.bn;
+  P.bn = 256;
+  P.tile_m = P.tile_n = 256;
+  P.kseg = (int)std::max<int64_t>(1, limb_kmax(P.scheme, p) / kBK);
   P.mod = make_modp(p);
   P.Y = skew_unitary(p);
   LeafParams &L = P.leaf_template;
@@ -57,7 +55,7 @@ static void fill_scheme(Plan &P, uint32_t p) {
   }
 }
 
-static ProductPlan make_prod(int arena, int64_t arow, int64_t brow, int64_t a_pr, int64_t b_pr, int64_t kpad,
+static ProductPlan make_prod(const Plan &P, int arena, int64_t arow, int64_t brow, int64_t a_pr, int64_t b_pr, int64_t kpad,
                              bool sym, int target, int level, int node, int idx, int64_t out_rows,
                              int64_t out_cols, bool out_u32, int64_t ldo) {
   ProductPlan pp;
@@ -73,6 +71,7 @@ static ProductPlan make_prod(int arena, int64_t arow, int64_t brow, int64_t a_pr
   pp.lp.out_rows = (int32_t)out_rows;
   pp.lp.out_cols = (int32_t)out_cols;
   pp.lp.vec_ok = 1;
+  pp.lp.kseg = P.kseg;
   pp.lp.ldo = ldo;
   pp.target = target;
   pp.level = level;
@@ -105,8 +104,9 @@ static void append_tiles(Plan &P) {
 
 static void set_grid(Plan &P, int num_sms) {
   const int64_t nt = std::max<int64_t>(1, (int64_t)P.tiles.size());
-  if (P.leaf_ver == 2) P.grid = 2 * (int)std::min<int64_t>(num_sms / 2, nt);   // CTA pairs
-  else P.grid = (int)std::min<int64_t>(num_sms, nt);
+  P.grid = 2 * (int)std::min<int64_t>(num_sms / 2, nt);   // CTA pairs
+  P.segmented = false;
+  for (const ProductPlan &pp : P.prods) P.segmented |= pp.lp.kblocks > pp.lp.kseg;
 }
 
 // Depth choice (R13), from measured B200 crossovers: one level of Alg. alg:MIAHMM
@@ -131,7 +131,6 @@ bool build_syrk_plan(Plan &P, int64_t m, int64_t k, uint32_t p, int phi, int dep
   P.kind = phi == 0 ? PLAN_SYRK_T : PLAN_SYRK_H;
   P.m = m; P.n = m; P.k = k; P.depth = depth;
   fill_scheme(P, p);
-  const int64_t kmax = limb_kmax(P.scheme, p);
   const int planes = P.planes;
 
   P.lv.resize(depth + 1);
@@ -196,22 +195,18 @@ bool build_syrk_plan(Plan &P, int64_t m, int64_t k, uint32_t p, int phi, int dep
   }
   P.ws_bytes = off;
 
-  // int32 accumulation bound per leaf product
-  if ((n0 > 0 && P.kpad0 > kmax) || (depth > 0 && P.lv[1].kpad > kmax)) {
-    *err = "inner dimension exceeds the int32 accumulation bound of the limb scheme at this depth";
-    return false;
-  }
-  if (P.rows_pad0 >= (int64_t)4096 * kBM) { *err = "m too large"; return false; }
+  // the int32 accumulation bound per leaf product is met by K segmentation
+  if (P.rows_pad0 >= (int64_t)4096 * P.tile_m) { *err = "m too large"; return false; }
 
   // leaf products
   P.prods.clear();
   if (P.kind == PLAN_SYRK_T && depth == 0)
-    P.prods.push_back(make_prod(0, 0, 0, P.rows_pad0, P.rows_pad0, P.kpad0, true, OUT_C, 0, 0, 0, m, m, true, 0));
+    P.prods.push_back(make_prod(P, 0, 0, 0, P.rows_pad0, P.rows_pad0, P.kpad0, true, OUT_C, 0, 0, 0, m, m, true, 0));
   if (P.kind == PLAN_SYRK_H) {
-    P.prods.push_back(make_prod(0, P.op0_row[0], P.op0_row[1], P.rows_pad0, P.rows_pad0, P.kpad0, false, OUT_HBUF,
+    P.prods.push_back(make_prod(P, 0, P.op0_row[0], P.op0_row[1], P.rows_pad0, P.rows_pad0, P.kpad0, false, OUT_HBUF,
                                 0, 0, 0, P.rows_pad0, P.rows_pad0, false, P.rows_pad0));     // H = X Y^T
     if (depth == 0)
-      P.prods.push_back(make_prod(0, P.op0_row[2], P.op0_row[2], P.rows_pad0, P.rows_pad0, P.kpad0, true, OUT_GBUF,
+      P.prods.push_back(make_prod(P, 0, P.op0_row[2], P.op0_row[2], P.rows_pad0, P.rows_pad0, P.kpad0, true, OUT_GBUF,
                                   0, 0, 0, P.rows_pad0, P.rows_pad0, false, P.rows_pad0)); // G = T T^T
   }
   for (int l = 1; l <= depth; ++l) {
@@ -220,17 +215,17 @@ bool build_syrk_plan(Plan &P, int64_t m, int64_t k, uint32_t p, int phi, int dep
       auto row = [&](int o) { return ((int64_t)n * L.n_ops + o) * planes * L.rows_pad; };
       const int64_t rp = L.rows_pad;
       // P3 = A22 phi(S4), P4 = S1 phi(S2)   (general products)
-      P.prods.push_back(make_prod(L.arena, row(OUT_X22), row(OUT_S4), rp, rp, L.kpad, false, OUT_PBUF, l, n, 2, rp, rp,
+      P.prods.push_back(make_prod(P, L.arena, row(OUT_X22), row(OUT_S4), rp, rp, L.kpad, false, OUT_PBUF, l, n, 2, rp, rp,
                                   false, rp));
-      P.prods.push_back(make_prod(L.arena, row(OUT_S1), row(OUT_S2), rp, rp, L.kpad, false, OUT_PBUF, l, n, 3, rp, rp,
+      P.prods.push_back(make_prod(P, L.arena, row(OUT_S1), row(OUT_S2), rp, rp, L.kpad, false, OUT_PBUF, l, n, 3, rp, rp,
                                   false, rp));
       if (l == depth) {
         // P1 = A11 phi(A11), P2 = A12 phi(A12), P5 = S3 phi(S3) at the last level
-        P.prods.push_back(make_prod(L.arena, row(OUT_X11), row(OUT_X11), rp, rp, L.kpad, true, OUT_PBUF, l, n, 0, rp,
+        P.prods.push_back(make_prod(P, L.arena, row(OUT_X11), row(OUT_X11), rp, rp, L.kpad, true, OUT_PBUF, l, n, 0, rp,
                                     rp, false, rp));
-        P.prods.push_back(make_prod(L.arena, row(OUT_X12), row(OUT_X12), rp, rp, L.kpad, true, OUT_PBUF, l, n, 1, rp,
+        P.prods.push_back(make_prod(P, L.arena, row(OUT_X12), row(OUT_X12), rp, rp, L.kpad, true, OUT_PBUF, l, n, 1, rp,
                                     rp, false, rp));
-        P.prods.push_back(make_prod(L.arena, row(OUT_S3), row(OUT_S3), rp, rp, L.kpad, true, OUT_PBUF, l, n, 4, rp,
+        P.prods.push_back(make_prod(P, L.arena, row(OUT_S3), row(OUT_S3), rp, rp, L.kpad, true, OUT_PBUF, l, n, 4, rp,
                                     rp, false, rp));
       }
     }
@@ -249,11 +244,7 @@ bool build_gemm_plan(Plan &P, int64_t m, int64_t n, int64_t k, uint32_t p, int n
   P.rows_pad0 = rup(std::max<int64_t>(m, 1), kBM);
   P.rows_pad_b = rup(std::max<int64_t>(n, 1), kBM);
   P.kpad0 = std::max<int64_t>(kBK, rup(k, kBK));
-  if (P.kpad0 > limb_kmax(P.scheme, p)) {
-    *err = "inner dimension exceeds the int32 accumulation bound of the limb scheme";
-    return false;
-  }
-  if (P.rows_pad0 >= (int64_t)4096 * kBM || P.rows_pad_b >= (int64_t)4096 * P.bn) { *err = "m or n too large"; return false; }
+  if (P.rows_pad0 >= (int64_t)4096 * P.tile_m || P.rows_pad_b >= (int64_t)4096 * P.tile_n) { *err = "m or n too large"; return false; }
   P.op0_row[0] = 0;
   P.op0_row[1] = (int64_t)P.planes * P.rows_pad0;
   ArenaPlan a;
@@ -262,7 +253,7 @@ bool build_gemm_plan(Plan &P, int64_t m, int64_t n, int64_t k, uint32_t p, int n
   a.offset = 0;
   P.arenas.push_back(a);
   P.ws_bytes = (size_t)rup((int64_t)a.bytes(), 256);
-  P.prods.push_back(make_prod(0, P.op0_row[0], P.op0_row[1], P.rows_pad0, P.rows_pad_b, P.kpad0, false, OUT_C, 0, 0, 0,
+  P.prods.push_back(make_prod(P, 0, P.op0_row[0], P.op0_row[1], P.rows_pad0, P.rows_pad_b, P.kpad0, false, OUT_C, 0, 0, 0,
                               m, n, true, 0));
   append_tiles(P);
   set_grid(P, num_sms);

@@ -46,8 +46,9 @@ struct Plan {
   int depth = 0;
   LimbScheme scheme;
   int planes = 1, nacc = 1, bn = 128;
-  int leaf_ver = 2;               // 2: CTA-pair 256x256 tiles (leaf2_kernel); 1: 1-CTA 128 x bn
-  int tile_m = 256, tile_n = 256;
+  int tile_m = 256, tile_n = 256;  // CTA-pair output tile (leaf2_kernel)
+  int kseg = 1;                    // k-blocks per int32 accumulation segment (limb k_max / 128)
+  bool segmented = false;          // some leaf product needs more than one K segment
   ModP mod;
   SkewY Y;
   std::vector<ArenaPlan> arenas;

@@ -27,7 +27,7 @@ struct LeafProduct {
   int32_t out_rows;      // writes masked to row < out_rows, col < out_cols
   int32_t out_cols;
   int32_t vec_ok;        // 16-byte vector stores allowed (alignment checked on host)
-  int32_t pad_;
+  int32_t kseg;          // k-blocks per int32 accumulation segment (>= kblocks: one segment)
   int64_t ldo;           // output leading dimension (elements)
   void *out;
 };

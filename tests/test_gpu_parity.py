@@ -164,3 +164,23 @@ def test_errors_on_device(adj):
     with pytest.raises(adj.AdjError) as e:
         adj.adjprod_modp_ex(300, 300, 97, 0, B, 300, C, 300, depth=1, workspace=ws, workspace_bytes=16)
     assert e.value.status == 3
+
+
+@pytest.mark.parametrize("p,k,m", [(65521, 40000, 300), (65521, 70000, 130), (97, 140000, 64), (8191, 240000, 64)])
+def test_k_segmentation_beyond_int32_bound(adj, p, k, m):
+    """Inner dimension above the limb scheme's int32 bound: the leaf splits K
+    into segments, each reduced mod p and summed (depth 0 and gemm_modp)."""
+    A = uniform_matrix(m, k, seed=k + m, p=p)
+    dA = to_dev(A)
+    got = to_host(adj.adjprod(dA, p, depth=0))
+    assert np.array_equal(got, oracle.syrk_t(A, p))
+    B = uniform_matrix(70, k, seed=k + 1, p=p)
+    G = to_host(adj.gemm(dA, to_dev(B), p))
+    assert np.array_equal(G, oracle.gemm_nt(A, B, p))
+
+
+def test_k_segmentation_overflow_stress(adj):
+    p, c, k = 65521, 65521 - 32513, 70000          # lo = 255, hi = -128, 3 segments
+    A = constant_matrix(256, k, c, p)
+    got = to_host(adj.adjprod(to_dev(A), p, depth=0))
+    assert (got[np.tril_indices(256)] == k * c * c % p).all()
