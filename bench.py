@@ -33,6 +33,8 @@ CONFIGS = {
                workload="c3: A 32768x32768 over GF(65521), C = Low(A A^T) mod 65521, Y = 24297 I"),
     "c4": dict(m=16384, k=131072, p=8191, phi="T", depth=None,
                workload="c4: A 16384x131072 over GF(8191), C = Low(A A^T) mod 8191 (16384^2)"),
+    "x251": dict(m=8192, k=8192, p=251, phi="T", depth=None,
+                 workload="x251 (dev): A 8192x8192 over GF(251), one int8 limb"),
     "c5": dict(m=8192, k=8192, p=8191, phi="H", depth=None,
                workload="c5: A 8192x8192 over GF(8191^2) = GF(8191)[i]/(i^2+1), C = Low(A A^H) via 2M"),
 }
@@ -107,6 +109,7 @@ class ClockSampler:
             self.nv = pynvml
             self.h = pynvml.nvmlDeviceGetHandleByIndex(dev_index)
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.power = []
             self.ok = True
         except Exception:
             self.max_mhz = None
@@ -116,6 +119,7 @@ class ClockSampler:
         while not self._stop.is_set():
             try:
                 self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.power.append(self.nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0)
                 r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
                 for bit, name in self.REASONS.items():
                     if r & bit:
@@ -137,7 +141,8 @@ class ClockSampler:
 
     def summary(self):
         return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
-                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples),
+                "power_w_max": max(self.power) if getattr(self, "power", None) else None}
 
 
 def load_traffic(config: str, depth: int):

@@ -15,6 +15,7 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -244,6 +245,7 @@ adj_status_t launch_leaf_all(const Plan &P, const Ptrs &x, cudaStream_t s) {
   }
   L.tiles = P.d_tiles;
   L.n_tiles = (int32_t)P.tiles.size();
+  if (const char *dbg = getenv("ADJ_LEAF_DEBUG")) L.debug = atoi(dbg);   // diagnostics only
   LAUNCH_CLS(CLS_LEAF, launch_leaf2(L, P.nacc, P.segmented, P.grid, s));
   return ADJ_OK;
 }

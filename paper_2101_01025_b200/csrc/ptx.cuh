@@ -34,6 +34,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
       "@!P1 bra WAIT_%=;\n\t}" ::"r"(addr), "r"(parity) : "memory");
 }
 
+// busy-polling wait (mbarrier.test_wait never suspends the warp): for the latency-critical
+// producer / MMA-issuer loops where a sleeping try_wait wakes up late
+__device__ __forceinline__ void mbar_wait_spin(uint64_t *bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "SPIN_%=:\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra SPIN_%=;\n\t}" ::"r"(addr), "r"(parity) : "memory");
+}
+
 // ---------------------------------------------------------------- TMA
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap *m) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");

@@ -45,6 +45,7 @@ struct LeafParams {
   int32_t acc_begin[4];    // terms [acc_begin[j], acc_begin[j+1]) accumulate into accumulator j
   LeafTerm terms[4];
   uint32_t weight[3];      // residue weight of each accumulator in the limb recombination
+  int32_t debug;           // diagnostics only (ADJ_LEAF_DEBUG): 1 no TMA, 2 no epilogue, 8 no math, 16 no tcgen05.ld, 32 no stores
   ModP mod;
 };
 

@@ -11,11 +11,14 @@
 
 using namespace adj;
 
-template <int MODE>
+// VAR bits (pair mode only): 1 = tcgen05.commit after every 4 MMAs, 2 = try_wait on a completed
+// mbarrier + tcgen05.fence::after_thread_sync before every 4 MMAs, 4 = 8 MMAs per group
+template <int MODE, int VAR = 0>
 __global__ void __launch_bounds__(128, 1) mma_loop(int iters, int *sink) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t bar;
+  __shared__ uint64_t bar, bar2, bar3;
+  __shared__ uint64_t fullb[5], emptyb[5];
   __shared__ uint32_t holder;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   constexpr bool PAIR = MODE == 0;
@@ -27,6 +30,11 @@ __global__ void __launch_bounds__(128, 1) mma_loop(int iters, int *sink) {
   for (int i = threadIdx.x; i < 65536 / 4; i += blockDim.x) reinterpret_cast<uint32_t *>(smem)[i] = 0x01010101u * (i & 3);
   if (threadIdx.x == 0) {
     ptx::mbar_init(&bar, 1);
+    ptx::mbar_init(&bar2, 1 << 20);
+    ptx::mbar_init(&bar3, 1);
+    ptx::fence_barrier_init();
+    ptx::mbar_arrive(&bar3);   // phase 0 of bar3 complete
+    for (int i = 0; i < 5; ++i) { ptx::mbar_init(&fullb[i], 1); ptx::mbar_init(&emptyb[i], 1); }
     ptx::fence_barrier_init();
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -39,16 +47,58 @@ __global__ void __launch_bounds__(128, 1) mma_loop(int iters, int *sink) {
   if constexpr (PAIR) ptx::cluster_sync();
   ptx::tc_fence_after();
   const uint32_t tbase = holder;
-  if (warp == 1 && lane == 0 && rank == 0) {
+  if constexpr ((VAR & 8) != 0) {
+    // 5-stage ring like the leaf kernel: producer (warp 2) waits empty -> arrives full; MMA waits
+    // full -> 4 MMAs -> commit (multicast to both CTAs when VAR & 16) on empty.
+    const int nst = iters;
+    if (warp == 2 && lane == 0 && (rank == 0 || (VAR & 16))) {
+      int st = 0; uint32_t ph = 0;
+      for (int it = 0; it < nst; ++it) {
+        ptx::mbar_wait(&emptyb[st], ph ^ 1);
+        if (rank == 0) ptx::mbar_arrive(&fullb[st]);
+        if (++st == 5) { st = 0; ph ^= 1; }
+      }
+    }
+    if (warp == 1 && lane == 0 && rank == 0) {
+      const uint32_t idesc = ptx::idesc_i8(M, N, true, true);
+      int st = 0; uint32_t ph = 0;
+      for (int it = 0; it < nst; ++it) {
+        ptx::mbar_wait(&fullb[st], ph);
+        ptx::tc_fence_after();
+        const uint32_t sa = ptx::smem_u32(smem) + (st & 1) * 16384;   // A alternates within [0, 32K)
+        const uint64_t adesc = ptx::smem_desc_sw128(sa);
+        const uint64_t bdesc = ptx::smem_desc_sw128(ptx::smem_u32(smem) + 32768);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          if constexpr (PAIR) ptx::mma_i8_2sm(tbase + (it & 1) * 256, adesc + 2 * kk, bdesc + 2 * kk, idesc, it | kk);
+          else ptx::mma_i8(tbase + (it & 1) * 256, adesc + 2 * kk, bdesc + 2 * kk, idesc, it | kk);
+        }
+        if constexpr (PAIR) ptx::mma_commit_2sm(&emptyb[st], (VAR & 16) ? 0x3 : 0x1);
+        else ptx::mma_commit(&emptyb[st]);
+        if (++st == 5) { st = 0; ph ^= 1; }
+      }
+      if constexpr (PAIR) ptx::mma_commit_2sm(&bar, 0x3);
+      else ptx::mma_commit(&bar);
+    }
+  } else if (warp == 1 && lane == 0 && rank == 0) {
     const uint32_t sa = ptx::smem_u32(smem);
     const uint64_t adesc = ptx::smem_desc_sw128(sa);
     const uint64_t bdesc = ptx::smem_desc_sw128(sa + 32768);
     const uint32_t idesc = ptx::idesc_i8(M, N, true, true);
-    for (int it = 0; it < iters; ++it) {
+    constexpr int G = (VAR & 4) ? 8 : 4;
+    for (int it = 0; it < iters * 4 / G; ++it) {
+      if constexpr ((VAR & 2) != 0) {
+        ptx::mbar_wait(&bar3, 0);
+        ptx::tc_fence_after();
+      }
 #pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
-        if constexpr (PAIR) ptx::mma_i8_2sm(tbase + (it & 1) * 256, adesc + 2 * kk, bdesc + 2 * kk, idesc, it | kk);
-        else ptx::mma_i8(tbase + (it & 1) * 256, adesc + 2 * kk, bdesc + 2 * kk, idesc, it | kk);
+      for (int kk = 0; kk < G; ++kk) {
+        if constexpr (PAIR) ptx::mma_i8_2sm(tbase + (it & 1) * 256, adesc + 2 * (kk & 3), bdesc + 2 * (kk & 3), idesc, it | kk);
+        else ptx::mma_i8(tbase + (it & 1) * 256, adesc + 2 * (kk & 3), bdesc + 2 * (kk & 3), idesc, it | kk);
+      }
+      if constexpr ((VAR & 1) != 0) {
+        if constexpr (PAIR) ptx::mma_commit_2sm(&bar2, 0x1);
+        else ptx::mma_commit(&bar2);
       }
     }
     if constexpr (PAIR) ptx::mma_commit_2sm(&bar, 0x3);
@@ -68,9 +118,9 @@ __global__ void __launch_bounds__(128, 1) mma_loop(int iters, int *sink) {
   if (threadIdx.x == 0 && sink) sink[blockIdx.x] = (int)tbase;
 }
 
-template <int MODE>
+template <int MODE, int VAR = 0>
 double run(int sms, int iters) {
-  auto k = mma_loop<MODE>;
+  auto k = mma_loop<MODE, VAR>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 66 * 1024 + 1024);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(sms);
@@ -110,7 +160,11 @@ int main(int argc, char **argv) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const int iters = argc > 1 ? atoi(argv[1]) : 20000;
   printf("{\"sms\": %d, \"iters\": %d, \"pair_256x256_tops\": %.1f, \"single_128x256_tops\": %.1f, "
-         "\"single_128x128_tops\": %.1f}\n",
-         sms, iters, run<0>(sms, iters), run<1>(sms, iters), run<2>(sms, iters));
+         "\"single_128x128_tops\": %.1f,\n", sms, iters, run<0>(sms, iters), run<1>(sms, iters), run<2>(sms, iters));
+  printf(" \"pair_commit_every4\": %.1f, \"pair_wait_fence_every4\": %.1f, \"pair_both_every4\": %.1f, "
+         "\"pair_both_every8\": %.1f, \"single128x256_both_every4\": %.1f}\n",
+         run<0, 1>(sms, iters), run<0, 2>(sms, iters), run<0, 3>(sms, iters), run<0, 7>(sms, iters), run<1, 3>(sms, iters));
+  printf(" {\"ring5_pair_commit_leader\": %.1f, \"ring5_pair_commit_multicast\": %.1f, \"ring5_single\": %.1f}\n",
+         run<0, 8>(sms, iters), run<0, 24>(sms, iters), run<1, 8>(sms, iters));
   return 0;
 }
