@@ -363,7 +363,8 @@ def run_gpu(args, cfg, rank, world, local_rank):
     # ---------------- roofline of the dominant kernel (grouped tcgen05 leaf launch)
     peaks, src = load_peaks()
     leaf_ms, leaf_n = prof["leaf"]
-    leaf_avg_ms = leaf_ms / max(leaf_n, 1)
+    # one grouped leaf stage per step: the tcgen05 leaf launch (+ its tail fixup launch, if any)
+    leaf_avg_ms = leaf_ms / args.steps
     ops = leaf_int8_ops(cfg, depth)
     achieved = ops / (leaf_avg_ms * 1e-3) / 1e12
     peak = 2.0 * peaks["bf16_tflops"]        # int8 dense = 2 x bf16 dense (guide's nominal ratio)
@@ -371,7 +372,8 @@ def run_gpu(args, cfg, rank, world, local_rank):
             "traffic": load_traffic(args.config, depth),
             "kernel": "leaf_kernel (grouped tcgen05 kind::i8 GEMM/SYRK + mod-p epilogue)",
             "peak_source": f"{src}: 2 x bf16_tflops ({peaks['bf16_tflops']}) burst, int8 = 2x bf16 nominal",
-            "algorithmic_ops_per_launch": ops, "leaf_ms_per_launch": leaf_avg_ms}
+            "algorithmic_ops_per_launch": ops, "leaf_ms_per_launch": leaf_avg_ms,
+            "leaf_launches_per_step": leaf_n / args.steps}
     share = {c: round(v[0] / max(1e-9, sum(x[0] for x in prof.values())), 4) for c, v in prof.items()}
 
     cpu = None

@@ -159,6 +159,10 @@ adj_status_t get_plan(Plan **out, int kind, int64_t m, int64_t n, int64_t k, uin
     CUDA_TRY(cudaMalloc(&P->d_tiles, P->tiles.size() * sizeof(uint32_t)));
     CUDA_TRY(cudaMemcpy(P->d_tiles, P->tiles.data(), P->tiles.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
   }
+  if (!P->fixups.empty()) {
+    CUDA_TRY(cudaMalloc(&P->d_fixups, P->fixups.size() * sizeof(FixupTile)));
+    CUDA_TRY(cudaMemcpy(P->d_fixups, P->fixups.data(), P->fixups.size() * sizeof(FixupTile), cudaMemcpyHostToDevice));
+  }
   *out = P.get();
   g_plans.emplace(key, std::move(P));
   return ADJ_OK;
@@ -243,10 +247,12 @@ adj_status_t launch_leaf_all(const Plan &P, const Ptrs &x, cudaStream_t s) {
         break;
     }
   }
-  L.tiles = P.d_tiles;
-  L.n_tiles = (int32_t)P.tiles.size();
+  L.tiles = reinterpret_cast<const uint2 *>(P.d_tiles);
+  L.n_tiles = (int32_t)(P.tiles.size() / 2);
+  L.fixup = reinterpret_cast<uint16_t *>(x.ws + P.fixup_offset);
   if (const char *dbg = getenv("ADJ_LEAF_DEBUG")) L.debug = atoi(dbg);   // diagnostics only
   LAUNCH_CLS(CLS_LEAF, launch_leaf2(L, P.nacc, P.segmented, P.grid, s));
+  if (!P.fixups.empty()) LAUNCH_CLS(CLS_LEAF, launch_fixup(L, P.d_fixups, (int)P.fixups.size(), s));
   return ADJ_OK;
 }
 

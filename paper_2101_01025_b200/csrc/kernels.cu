@@ -31,6 +31,14 @@ __device__ __forceinline__ void decode_tile(uint32_t packed, int &q, int &I, int
   J = (int)(packed & 0xFFF);
 }
 
+// k-block range and fixup piece of a job (whole tile: [0, kblocks), piece 0)
+__device__ __forceinline__ void decode_range(uint32_t y, int kblocks, int &kb0, int &kb1, int &piece) {
+  if (y == 0) { kb0 = 0; kb1 = kblocks; piece = 0; return; }
+  kb0 = (int)(y & 0xFFF);
+  kb1 = (int)((y >> 12) & 0xFFF);
+  piece = (int)(y >> 24);
+}
+
 // store 32 consecutive residues r[0..31] of output row `row`, columns col..col+31
 __device__ __forceinline__ void store_chunk(const LeafProduct &pr, int64_t row, int64_t col,
                                             const uint32_t (&r)[32]) {
@@ -150,22 +158,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       const bool skip_tma = (P.debug & 1) != 0;
       const bool prof = (P.debug & 128) != 0;
       long long t_empty = 0, t_tma = 0, t_begin = clock64();
-      uint32_t next = cid < P.n_tiles ? __ldg(&P.tiles[cid]) : 0u;
+      uint2 next = cid < P.n_tiles ? __ldg(&P.tiles[cid]) : make_uint2(0u, 0u);
       for (int t = cid; t < P.n_tiles; t += ncl) {
-        int q, I, J;
-        decode_tile(next, q, I, J);
-        if (t + ncl < P.n_tiles) next = __ldg(&P.tiles[t + ncl]);   // prefetch the next tile id
+        int q, I, J, jb0, jb1, piece;
+        decode_tile(next.x, q, I, J);
+        const uint32_t range = next.y;
+        if (t + ncl < P.n_tiles) next = __ldg(&P.tiles[t + ncl]);   // prefetch the next job
         const LeafProduct &pr = P.prod[q];
         const CUtensorMap *map = &P.maps[pr.map];
-        const int kblocks = pr.kblocks, kseg = pr.kseg;
+        const int kseg = pr.kseg;
+        decode_range(range, pr.kblocks, jb0, jb1, piece);
         const int a_pr = pr.a_plane_rows, b_pr = pr.b_plane_rows;
         const int arow = pr.a_row0 + I * Cfg::TILE + (int)rank * 128;
         const int brow = pr.b_row0 + J * Cfg::TILE + (int)rank * 128;
-        const int nseg = (kblocks + kseg - 1) / kseg;
+        const int nseg = (jb1 - jb0 + kseg - 1) / kseg;
 #pragma unroll 1
         for (int u = 0; u < NACC * nseg; ++u) {
-          const int j = u / nseg, kb0 = (u % nseg) * kseg;
-          const int kb1 = min(kblocks, kb0 + kseg);
+          const int j = u / nseg, kb0 = jb0 + (u % nseg) * kseg;
+          const int kb1 = min(jb1, kb0 + kseg);
           // the (at most 2) operand-plane pairs accumulated into accumulator j, hoisted out of the K loop
           const int t0 = P.acc_begin[j], nt = P.acc_begin[j + 1] - t0;
           const int ar0 = arow + P.terms[t0].a_plane * a_pr, br0 = brow + P.terms[t0].b_plane * b_pr;
@@ -206,18 +216,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       const uint32_t smem_base = ptx::smem_u32(smem);
       const bool prof = (P.debug & 128) != 0;
       long long t_full = 0, t_slot = 0, t_issue = 0, t_begin = clock64();
-      uint32_t next = cid < P.n_tiles ? __ldg(&P.tiles[cid]) : 0u;
+      uint2 next = cid < P.n_tiles ? __ldg(&P.tiles[cid]) : make_uint2(0u, 0u);
       for (int t = cid; t < P.n_tiles; t += ncl) {
-        int q, I, J;
-        decode_tile(next, q, I, J);
+        int q, I, J, jb0, jb1, piece;
+        decode_tile(next.x, q, I, J);
+        const uint32_t range = next.y;
         if (t + ncl < P.n_tiles) next = __ldg(&P.tiles[t + ncl]);
         const LeafProduct &pr = P.prod[q];
-        const int kblocks = pr.kblocks, kseg = pr.kseg;
-        const int nseg = (kblocks + kseg - 1) / kseg;
+        const int kseg = pr.kseg;
+        decode_range(range, pr.kblocks, jb0, jb1, piece);
+        const int nseg = (jb1 - jb0 + kseg - 1) / kseg;
 #pragma unroll 1
         for (int u = 0; u < NACC * nseg; ++u, ++unit) {
-          const int j = u / nseg, kb0 = (u % nseg) * kseg;
-          const int kb1 = min(kblocks, kb0 + kseg);
+          const int j = u / nseg, kb0 = jb0 + (u % nseg) * kseg;
+          const int kb1 = min(jb1, kb0 + kseg);
           const int t0 = P.acc_begin[j], nt = P.acc_begin[j + 1] - t0;
           const uint32_t id0 = ptx::idesc_i8(256, 256, P.terms[t0].a_signed != 0, P.terms[t0].b_signed != 0);
           const uint32_t id1 = nt > 1 ? ptx::idesc_i8(256, 256, P.terms[t0 + 1].a_signed != 0,
@@ -273,12 +285,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     const uint32_t empty_remote1 = ptx::mapa(ptx::smem_u32(&slot_empty[1]), 0);
     uint32_t unit = 0;
     for (int t = cid; t < P.n_tiles; t += ncl) {
-      int q, I, J;
-      decode_tile(P.tiles[t], q, I, J);
+      int q, I, J, jb0, jb1, piece;
+      const uint2 job = P.tiles[t];
+      decode_tile(job.x, q, I, J);
       const LeafProduct &pr = P.prod[q];
+      decode_range(job.y, pr.kblocks, jb0, jb1, piece);
       const int64_t row = (int64_t)I * Cfg::TILE + rank * 128 + lrow;
       const int64_t col0 = (int64_t)J * Cfg::TILE + h * 128;
-      const int nseg = (pr.kblocks + pr.kseg - 1) / pr.kseg;
+      // tail piece: residue partial of this CTA's 128 x 256 half-tile into the fixup slot
+      uint16_t *fx = piece ? P.fixup + (size_t)(piece - 1) * 65536 + (rank * 128 + lrow) * 256 + h * 128 : nullptr;
+      const int nseg = (jb1 - jb0 + pr.kseg - 1) / pr.kseg;
       const int nunits = NACC * nseg;
 #pragma unroll 1
       for (int u = 0; u < nunits; ++u, ++unit) {
@@ -323,8 +339,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
               continue;
             }
           }
-          if (!dbg_nostore) store_chunk(pr, row, col0 + c * 32, v);
-          else if (v[0] == 0xFFFFFFFFu && v[31] == 0x12345u) prow[0] = v[1];
+          if (fx) {
+            uint4 *d = reinterpret_cast<uint4 *>(fx + c * 32);
+#pragma unroll
+            for (int i4 = 0; i4 < 4; ++i4)
+              d[i4] = make_uint4(v[8 * i4] | (v[8 * i4 + 1] << 16), v[8 * i4 + 2] | (v[8 * i4 + 3] << 16),
+                                 v[8 * i4 + 4] | (v[8 * i4 + 5] << 16), v[8 * i4 + 6] | (v[8 * i4 + 7] << 16));
+          } else if (!dbg_nostore) {
+            store_chunk(pr, row, col0 + c * 32, v);
+          } else if (v[0] == 0xFFFFFFFFu && v[31] == 0x12345u) {
+            prow[0] = v[1];
+          }
         }
         ptx::tc_fence_before();
         __syncwarp();
@@ -372,6 +397,41 @@ cudaError_t launch_leaf2(const LeafParams &p, int nacc, bool segmented, int grid
   if (nacc == 1) return segmented ? launch_leaf2_t<1, true>(p, grid, s) : launch_leaf2_t<1, false>(p, grid, s);
   if (nacc == 3) return launch_leaf2_t<3, true>(p, grid, s);
   return cudaErrorInvalidValue;
+}
+
+// ============================================================================ tail fixup
+// out(tile) = sum over its K pieces of the residue partials, mod p; same masking as the leaf
+// epilogue (store_chunk).  One thread per (row, 32-column chunk) of a 256 x 256 tile.
+__global__ void __launch_bounds__(256) fixup_kernel(const __grid_constant__ LeafParams P, const FixupTile *tiles) {
+  const FixupTile ft = tiles[blockIdx.y];
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;   // 0 .. 256*8-1
+  const int lr = idx >> 3, c = idx & 7;
+  const LeafProduct &pr = P.prod[ft.q];
+  uint32_t acc[32];
+#pragma unroll
+  for (int e = 0; e < 32; ++e) acc[e] = 0;
+  for (int pc = 0; pc < ft.npieces; ++pc) {
+    const uint4 *src = reinterpret_cast<const uint4 *>(P.fixup + (size_t)(ft.slot0 + pc) * 65536 + lr * 256 + c * 32);
+#pragma unroll
+    for (int i4 = 0; i4 < 4; ++i4) {
+      const uint4 w = src[i4];
+      const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        acc[8 * i4 + 2 * e] += ws[e] & 0xFFFF;
+        acc[8 * i4 + 2 * e + 1] += ws[e] >> 16;
+      }
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < 32; ++e) acc[e] = mod_u32(acc[e], P.mod);   // < npieces * p < 2^32
+  store_chunk(pr, (int64_t)ft.I * 256 + lr, (int64_t)ft.J * 256 + c * 32, acc);
+}
+
+cudaError_t launch_fixup(const LeafParams &p, const FixupTile *tiles, int n, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  fixup_kernel<<<dim3(8, n), 256, 0, s>>>(p, tiles);
+  return cudaGetLastError();
 }
 
 // ============================================================================ input loads

@@ -97,13 +97,49 @@ static void append_tiles(Plan &P) {
         for (int64_t I = b0; I < b1; ++I) {
           if (lp.sym && J * P.tile_n > I * P.tile_m + P.tile_m - 1) continue;   // tile above the diagonal
           P.tiles.push_back(((uint32_t)q << 24) | ((uint32_t)I << 12) | (uint32_t)J);
+          P.tiles.push_back(0u);   // whole tile
         }
     }
   }
 }
 
+// Tail balancing: jobs are dealt round-robin to the clusters, so with n tiles of equal cost the
+// last wave holds n mod ncl tiles while the other clusters idle.  Those tail tiles are split
+// along K into ~ncl / rem pieces each; every piece writes its residue partial to a fixup slot
+// and fixup_kernel sums the pieces mod p (exact: < pieces * p < 2^32).
+static void split_tail(Plan &P, int ncl) {
+  P.fixups.clear();
+  P.n_pieces = 0;
+  const int64_t n = (int64_t)P.tiles.size() / 2;
+  const int64_t rem = n % ncl;
+  if (n == 0 || rem == 0 || rem * 2 > ncl) return;
+  const int pieces = (int)(ncl / rem);
+  std::vector<uint32_t> out(P.tiles.begin(), P.tiles.begin() + 2 * (n - rem));
+  for (int64_t t = n - rem; t < n; ++t) {
+    const uint32_t x = P.tiles[2 * t];
+    const int q = (int)(x >> 24);
+    const int kb = P.prods[q].lp.kblocks;
+    const int np = std::min(pieces, kb);
+    if (np < 2 || kb > 4095) { out.push_back(x); out.push_back(0u); continue; }
+    FixupTile ft;
+    ft.q = q; ft.I = (int)((x >> 12) & 0xFFF); ft.J = (int)(x & 0xFFF);
+    ft.slot0 = P.n_pieces; ft.npieces = np; ft.pad_ = 0;
+    for (int i = 0; i < np; ++i) {
+      const uint32_t kb0 = (uint32_t)((int64_t)kb * i / np), kb1 = (uint32_t)((int64_t)kb * (i + 1) / np);
+      out.push_back(x);
+      out.push_back(kb0 | (kb1 << 12) | ((uint32_t)(P.n_pieces + i + 1) << 24));
+    }
+    P.n_pieces += np;
+    P.fixups.push_back(ft);
+  }
+  P.tiles.swap(out);
+}
+
 static void set_grid(Plan &P, int num_sms) {
-  const int64_t nt = std::max<int64_t>(1, (int64_t)P.tiles.size());
+  split_tail(P, num_sms / 2);
+  P.fixup_offset = P.ws_bytes;
+  P.ws_bytes += (size_t)P.n_pieces * 256 * 256 * 2;
+  const int64_t nt = std::max<int64_t>(1, (int64_t)P.tiles.size() / 2);
   P.grid = 2 * (int)std::min<int64_t>(num_sms / 2, nt);   // CTA pairs
   P.segmented = false;
   for (const ProductPlan &pp : P.prods) P.segmented |= pp.lp.kblocks > pp.lp.kseg;

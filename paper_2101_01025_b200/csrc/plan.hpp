@@ -59,8 +59,12 @@ struct Plan {
   size_t h_offset = 0, g_offset = 0;  // 2M buffers H, G (uint16 rows_pad0^2)
   size_t ws_bytes = 0;
   std::vector<ProductPlan> prods;
-  std::vector<uint32_t> tiles;
+  std::vector<uint32_t> tiles;       // 2 words per leaf job (LeafParams::tiles)
   uint32_t *d_tiles = nullptr;       // device copy (owned by the plan cache)
+  std::vector<FixupTile> fixups;     // tail tiles split along K into pieces
+  FixupTile *d_fixups = nullptr;
+  size_t fixup_offset = 0;           // workspace offset of the 256x256 u16 piece slots
+  int n_pieces = 0;
   int grid = 1;
   int dev = 0;
   LeafParams leaf_template;           // terms, weights, mod (maps/outs bound per call)

@@ -39,14 +39,23 @@ struct LeafTerm {        // one tcgen05.mma operand pair accumulated into accumu
 struct LeafParams {
   CUtensorMap maps[kMaxMaps];
   LeafProduct prod[kMaxProducts];
-  const uint32_t *tiles;   // packed (product << 24 | I << 12 | J), longest-K products first
+  // jobs: .x = product << 24 | I << 12 | J (longest-K products first);
+  //       .y = 0 for a whole tile, else kb0 | kb1 << 12 | piece << 24: a K-range piece of a tail
+  //       tile whose residue partial goes to fixup slot piece-1 (summed by the fixup kernel)
+  const uint2 *tiles;
   int32_t n_tiles;
+  uint16_t *fixup;         // 256 x 256 u16 residue partials, one slot per tail piece
   int32_t n_terms;
   int32_t acc_begin[4];    // terms [acc_begin[j], acc_begin[j+1]) accumulate into accumulator j
   LeafTerm terms[4];
   uint32_t weight[3];      // residue weight of each accumulator in the limb recombination
   int32_t debug;           // diagnostics only (ADJ_LEAF_DEBUG): 1 no TMA, 2 no epilogue, 8 no math, 16 no tcgen05.ld, 32 no stores
   ModP mod;
+};
+
+// tail tiles split along K into pieces (fixup_kernel sums them into the product output)
+struct FixupTile {
+  int32_t q, I, J, slot0, npieces, pad_;
 };
 
 // ---------------------------------------------------------------- K1 pre-addition
