@@ -515,6 +515,33 @@ __device__ __forceinline__ void limbs4(const uint32_t (&x)[4], const ModP &m, ui
   }
 }
 
+// K7 limbs of 4 already-centered values c in [-(p-1)/2, (p-1)/2]
+__device__ __forceinline__ void put_limbs4_k7c(int8_t *base, int64_t plane_stride, const int32_t (&c)[4]) {
+  int32_t hi[4], lo[4], mid[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    hi[e] = (c[e] + 64) >> 7;
+    lo[e] = c[e] - (hi[e] << 7);
+    mid[e] = hi[e] + lo[e];
+  }
+  *reinterpret_cast<uint32_t *>(base) =
+      __byte_perm(__byte_perm(hi[0], hi[1], 0x40), __byte_perm(hi[2], hi[3], 0x40), 0x5410);
+  *reinterpret_cast<uint32_t *>(base + plane_stride) =
+      __byte_perm(__byte_perm(lo[0], lo[1], 0x40), __byte_perm(lo[2], lo[3], 0x40), 0x5410);
+  *reinterpret_cast<uint32_t *>(base + 2 * plane_stride) =
+      __byte_perm(__byte_perm(mid[0], mid[1], 0x40), __byte_perm(mid[2], mid[3], 0x40), 0x5410);
+}
+
+// centered residue of a signed v with |v| < 2^30, 257 <= p <= 16763: float quotient estimate
+// (error < 0.2) then one fix in each direction
+__device__ __forceinline__ int32_t center_lazy(int32_t v, float invp, int32_t p, int32_t h) {
+  const int32_t q = __float2int_rn(__int2float_rn(v) * invp);
+  int32_t r = v - q * p;
+  r = r > h ? r - p : r;
+  r = r < -h ? r + p : r;
+  return r;
+}
+
 template <int SCHEME>
 __device__ __forceinline__ void put_limbs4(int8_t *base, int64_t plane_stride, const uint32_t (&x)[4],
                                            const ModP &m) {
@@ -633,6 +660,68 @@ __device__ __forceinline__ void preadd_row(const PreParams &P, const PreNode &N,
     load4(vv, P.mh + r, c + h2, m, x21b);
     load4(vv, P.mh + r, P.kh + c, m, x22a);
     load4(vv, P.mh + r, P.kh + c + h2, m, x22b);
+  }
+  if constexpr (SCHEME == 1) {
+    // Lazy reduction (p <= 16763 so 2 p^2 < 2^31): Y products in raw int32, one centered
+    // reduction per S output; X outputs and S3/S4 need one conditional correction each.
+    const int32_t p = (int32_t)m.p, h = (int32_t)m.half;
+    const float invp = 1.0f / (float)m.p;
+    const int32_t ya = (int32_t)P.ya, yb = (int32_t)P.yb;
+    int32_t c1a[4], c1b[4], c2a[4], c2b[4], c3a[4], c3b[4], c4a[4], c4b[4];
+    int32_t c11a[4], c11b[4], c12a[4], c12b[4], c22a[4], c22b[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int32_t d1 = (int32_t)x21a[e] - (int32_t)x11a[e], d2 = (int32_t)x21b[e] - (int32_t)x11b[e];
+      int32_t s1r_a, s1r_b, tr_a, tr_b;
+      if constexpr (YK == 0) {
+        s1r_a = ya * d1; s1r_b = ya * d2;
+        tr_a = ya * (int32_t)x21a[e]; tr_b = ya * (int32_t)x21b[e];
+      } else {
+        s1r_a = ya * d1 - yb * d2; s1r_b = yb * d1 + ya * d2;                         // (A21 - A11) Y
+        tr_a = ya * (int32_t)x21a[e] - yb * (int32_t)x21b[e];                          // A21 Y
+        tr_b = yb * (int32_t)x21a[e] + ya * (int32_t)x21b[e];
+      }
+      c1a[e] = center_lazy(s1r_a, invp, p, h); c1b[e] = center_lazy(s1r_b, invp, p, h);               // S1
+      c2a[e] = center_lazy((int32_t)x22a[e] - tr_a, invp, p, h);                                        // S2
+      c2b[e] = center_lazy((int32_t)x22b[e] - tr_b, invp, p, h);
+      c3a[e] = c1a[e] - (int32_t)x22a[e]; c3a[e] = c3a[e] < -h ? c3a[e] + p : c3a[e];                 // S3
+      c3b[e] = c1b[e] - (int32_t)x22b[e]; c3b[e] = c3b[e] < -h ? c3b[e] + p : c3b[e];
+      c4a[e] = c3a[e] + (int32_t)x12a[e]; c4a[e] = c4a[e] > h ? c4a[e] - p : c4a[e];                  // S4
+      c4b[e] = c3b[e] + (int32_t)x12b[e]; c4b[e] = c4b[e] > h ? c4b[e] - p : c4b[e];
+      c11a[e] = (int32_t)x11a[e] > h ? (int32_t)x11a[e] - p : (int32_t)x11a[e];
+      c11b[e] = (int32_t)x11b[e] > h ? (int32_t)x11b[e] - p : (int32_t)x11b[e];
+      c12a[e] = (int32_t)x12a[e] > h ? (int32_t)x12a[e] - p : (int32_t)x12a[e];
+      c12b[e] = (int32_t)x12b[e] > h ? (int32_t)x12b[e] - p : (int32_t)x12b[e];
+      c22a[e] = (int32_t)x22a[e] > h ? (int32_t)x22a[e] - p : (int32_t)x22a[e];
+      c22b[e] = (int32_t)x22b[e] > h ? (int32_t)x22b[e] - p : (int32_t)x22b[e];
+    }
+    const int64_t ps = P.rows_pad * P.kpad;
+#define PUTC(o, A, B)                                                                  \
+  if (N.op_row[o] >= 0) {                                                              \
+    int8_t *b = P.arena + (N.op_row[o] + r) * P.kpad;                                  \
+    put_limbs4_k7c(b + c, ps, A);                                                      \
+    put_limbs4_k7c(b + c + h2, ps, B);                                                 \
+  }
+    PUTC(OUT_S1, c1a, c1b)
+    PUTC(OUT_S2, c2a, c2b)
+    PUTC(OUT_S4, c4a, c4b)
+    PUTC(OUT_X22, c22a, c22b)
+    PUTC(OUT_X11, c11a, c11b)
+    PUTC(OUT_X12, c12a, c12b)
+    PUTC(OUT_S3, c3a, c3b)
+#undef PUTC
+    if (N.s3 != nullptr && r < P.mh) {
+      uint16_t *d = N.s3 + r * N.s3_ld;
+      uint32_t u[8];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        u[e] = (uint32_t)(c3a[e] < 0 ? c3a[e] + p : c3a[e]);
+        u[4 + e] = (uint32_t)(c3b[e] < 0 ? c3b[e] + p : c3b[e]);
+      }
+      *reinterpret_cast<uint2 *>(d + c) = make_uint2(u[0] | (u[1] << 16), u[2] | (u[3] << 16));
+      *reinterpret_cast<uint2 *>(d + c + h2) = make_uint2(u[4] | (u[5] << 16), u[6] | (u[7] << 16));
+    }
+    return;
   }
   uint32_t da[4], db[4], s1a[4], s1b[4], ta[4], tb[4], s2a[4], s2b[4], s3a[4], s3b[4], s4a[4], s4b[4];
 #pragma unroll

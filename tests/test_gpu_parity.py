@@ -9,7 +9,7 @@ from gpu_util import low, to_dev, to_host
 
 pytestmark = pytest.mark.gpu
 
-PRIMES = [3, 97, 251, 257, 8191, 16763, 16787, 65521]
+PRIMES = [3, 97, 251, 257, 8191, 16741, 16763, 16787, 65521]
 
 
 @pytest.fixture(scope="module")
