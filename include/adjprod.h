@@ -93,6 +93,19 @@ adj_status_t adjprod_modp_ex(int64_t m, int64_t k, uint32_t p, adj_phi_t phi,
                              const uint32_t *A, int64_t lda, uint32_t *C, int64_t ldc,
                              const adj_opts_t *opts, adj_stream_t stream);
 
+/*
+ * adjprod_modp_syrk -- the SYRK / HERK form  Low(C) <- alpha Low(A phi(A)) + beta Low(C)
+ *   (Table tab:schedule:AATpC, "C <- alpha A A^T + beta C").
+ *   alpha, beta in GF(p) (reduced mod p; for phi = ADJ_PHI_H they scale the re and im parts
+ *   alike, so the result stays Hermitian).  C is read (old values, interpreted mod p) and written
+ *   on Low(C) only.  The paper's in-place schedule with one n/2 x n/2 temporary is replaced by the
+ *   library workspace; the axpby is fused into the kernel that writes the final Low(C).
+ *   alpha = 1, beta = 0 is adjprod_modp_ex.  Arguments otherwise as adjprod_modp_ex.
+ */
+adj_status_t adjprod_modp_syrk(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, uint32_t alpha,
+                               const uint32_t *A, int64_t lda, uint32_t beta, uint32_t *C, int64_t ldc,
+                               const adj_opts_t *opts, adj_stream_t stream);
+
 /* Workspace bytes adjprod_modp_ex needs for these arguments (host, no launch). */
 adj_status_t adjprod_modp_workspace_size(int64_t m, int64_t k, uint32_t p, adj_phi_t phi,
                                          const adj_opts_t *opts, size_t *bytes);

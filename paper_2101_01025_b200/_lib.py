@@ -18,7 +18,7 @@ STATUS = {0: "ADJ_OK", 1: "ADJ_ERR_INVALID_VALUE", 2: "ADJ_ERR_UNSUPPORTED_MODUL
           4: "ADJ_ERR_CUDA", 5: "ADJ_ERR_NCCL", 6: "ADJ_ERR_ARCH"}
 
 # every symbol include/adjprod.h declares (checked by tests/test_abi.py)
-EXPORTS = ["adjprod_modp", "adjprod_modp_ex", "adjprod_modp_workspace_size", "adjprod_modp_auto_depth",
+EXPORTS = ["adjprod_modp", "adjprod_modp_ex", "adjprod_modp_syrk", "adjprod_modp_workspace_size", "adjprod_modp_auto_depth",
            "gemm_modp", "adj_skew_unitary", "adj_sos", "adj_mod_lower", "adj_comm_get_unique_id",
            "adj_comm_init", "adj_comm_destroy", "adjprod_modp_dist", "adj_dist_kslice", "adj_status_string", "adj_last_error",
            "adj_launch_count", "adj_launch_count_reset", "adj_profile_enable", "adj_profile_read"]
@@ -48,6 +48,7 @@ def lib() -> ctypes.CDLL:
         sig = {
             "adjprod_modp": [i64, i64, u32, ci, vp, i64, vp, i64, vp],
             "adjprod_modp_ex": [i64, i64, u32, ci, vp, i64, vp, i64, ctypes.POINTER(adj_opts_t), vp],
+            "adjprod_modp_syrk": [i64, i64, u32, ci, u32, vp, i64, u32, vp, i64, ctypes.POINTER(adj_opts_t), vp],
             "adjprod_modp_workspace_size": [i64, i64, u32, ci, ctypes.POINTER(adj_opts_t),
                                             ctypes.POINTER(ctypes.c_size_t)],
             "adjprod_modp_auto_depth": [i64, i64, u32, ci, ctypes.POINTER(ci)],
@@ -113,6 +114,13 @@ def adjprod_modp_ex(m, k, p, phi, A, lda, C, ldc, depth=-1, flags=0, workspace=N
     o = _opts(depth, flags, workspace, workspace_bytes)
     _check(lib().adjprod_modp_ex(m, k, p, phi, _ptr(A), lda, _ptr(C), ldc, ctypes.byref(o), _stream(stream)),
            "adjprod_modp_ex")
+
+
+def adjprod_modp_syrk(m, k, p, phi, alpha, A, lda, beta, C, ldc, depth=-1, flags=0, workspace=None,
+                      workspace_bytes=0, stream=None):
+    o = _opts(depth, flags, workspace, workspace_bytes)
+    _check(lib().adjprod_modp_syrk(m, k, p, phi, alpha % p, _ptr(A), lda, beta % p, _ptr(C), ldc, ctypes.byref(o),
+                                   _stream(stream)), "adjprod_modp_syrk")
 
 
 def adjprod_modp_workspace_size(m, k, p, phi, depth=-1) -> int:

@@ -208,6 +208,8 @@ InView child_view(const InView &pv, int c, const LevelPlan &Lp, uint16_t *s3, in
 
 // ------------------------------------------------------------------ launch schedule
 struct Ptrs {
+  uint32_t alpha = 1, beta = 0;   // SYRK form on the final Low(C): alpha Low(A phi(A)) + beta Low(C)
+  int axpby = 0;
   const uint32_t *A = nullptr; int64_t lda = 0;
   const uint32_t *B = nullptr; int64_t ldb = 0;
   uint32_t *C = nullptr; int64_t ldc = 0;
@@ -244,6 +246,9 @@ adj_status_t launch_leaf_all(const Plan &P, const Ptrs &x, cudaStream_t s) {
         L.prod[q].out = x.C;
         L.prod[q].ldo = x.ldc;
         L.prod[q].vec_ok = ((uintptr_t)x.C % 16 == 0) && (x.ldc % 4 == 0);
+        L.prod[q].alpha = x.alpha;
+        L.prod[q].beta = x.beta;
+        L.prod[q].axpby = x.axpby;
         break;
     }
   }
@@ -336,6 +341,11 @@ adj_status_t run_combine(const Plan &P, const Ptrs &x, void *final_out, int64_t 
     cp.ldp = L.rows_pad;
     cp.mod = P.mod;
     cp.out_u32 = (l == 1) ? (final_u32 ? 1 : 0) : 0;
+    if (l == 1 && final_u32) {
+      cp.alpha = x.alpha;
+      cp.beta = x.beta;
+      cp.axpby = x.axpby;
+    }
     for (int n = 0; n < L.n_nodes; ++n) {
       CombNode &N = cp.nodes[n];
       for (int i = 0; i < 5; ++i) N.P[i] = pbuf(P, x.ws, l, n, i);
@@ -409,7 +419,8 @@ adj_status_t run_syrk(const Plan &P, const Ptrs &x, adj_phi_t phi, uint32_t flag
       st = run_combine(P, x, G, P.rows_pad0, false, s);
       if (st) return st;
     }
-    LAUNCH_CLS(CLS_COMB, launch_twom(m, G, P.rows_pad0, H, P.rows_pad0, x.C, x.ldc, P.mod, s));
+    LAUNCH_CLS(CLS_COMB, launch_twom(m, G, P.rows_pad0, H, P.rows_pad0, x.C, x.ldc, P.mod, x.alpha, x.beta,
+                                     x.axpby, s));
   }
   if (flags & ADJ_FILL_UPPER) LAUNCH(launch_fill_upper(m, phi == ADJ_PHI_H ? 2 : 1, x.C, x.ldc, P.mod, s));
   return ADJ_OK;
@@ -516,18 +527,24 @@ adj_status_t adjprod_modp_workspace_size(int64_t m, int64_t k, uint32_t p, adj_p
   return ADJ_OK;
 }
 
-adj_status_t adjprod_modp_ex(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, const uint32_t *A, int64_t lda,
-                             uint32_t *C, int64_t ldc, const adj_opts_t *opts, adj_stream_t stream) {
+static adj_status_t adjprod_impl(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, uint32_t alpha, const uint32_t *A,
+                                 int64_t lda, uint32_t beta, uint32_t *C, int64_t ldc, const adj_opts_t *opts,
+                                 cudaStream_t s) {
   adj_status_t st = validate_syrk(m, k, p, phi, A, lda, C, ldc);
   if (st != ADJ_OK || m == 0) return st;
   int dev, sms;
   if ((st = check_device(&dev, &sms)) != ADJ_OK) return st;
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int w = phi == ADJ_PHI_H ? 2 : 1;
   const uint32_t flags = opts ? opts->flags : 0;
-  if (k == 0) {  // Low(C) = 0
-    for (int64_t i = 0; i < m; ++i)
-      CUDA_TRY(cudaMemsetAsync(C + i * ldc * w, 0, (size_t)(i + 1) * w * 4, s));
+  alpha %= p;
+  beta %= p;
+  const int axpby = !(alpha == 1 && beta == 0);
+  if (k == 0 || alpha == 0) {  // Low(C) = beta Low(C)
+    if (beta == 0) {
+      for (int64_t i = 0; i < m; ++i) CUDA_TRY(cudaMemsetAsync(C + i * ldc * w, 0, (size_t)(i + 1) * w * 4, s));
+    } else {
+      LAUNCH(launch_scale_lower(m, w, C, ldc, beta, make_modp(p), s));
+    }
     if (flags & ADJ_FILL_UPPER) LAUNCH(launch_fill_upper(m, w, C, ldc, make_modp(p), s));
     return ADJ_OK;
   }
@@ -538,6 +555,7 @@ adj_status_t adjprod_modp_ex(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, co
     return st;
   Ptrs x;
   x.A = A; x.lda = lda; x.C = C; x.ldc = ldc;
+  x.alpha = alpha; x.beta = beta; x.axpby = axpby;
   void *ws = opts ? opts->workspace : nullptr;
   bool own = false;
   if (ws == nullptr) {
@@ -553,6 +571,17 @@ adj_status_t adjprod_modp_ex(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, co
     if (st == ADJ_OK && e != cudaSuccess) return fail(ADJ_ERR_CUDA, "cudaFreeAsync: %s", cudaGetErrorString(e));
   }
   return st;
+}
+
+adj_status_t adjprod_modp_ex(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, const uint32_t *A, int64_t lda,
+                             uint32_t *C, int64_t ldc, const adj_opts_t *opts, adj_stream_t stream) {
+  return adjprod_impl(m, k, p, phi, 1, A, lda, 0, C, ldc, opts, reinterpret_cast<cudaStream_t>(stream));
+}
+
+adj_status_t adjprod_modp_syrk(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, uint32_t alpha, const uint32_t *A,
+                               int64_t lda, uint32_t beta, uint32_t *C, int64_t ldc, const adj_opts_t *opts,
+                               adj_stream_t stream) {
+  return adjprod_impl(m, k, p, phi, alpha, A, lda, beta, C, ldc, opts, reinterpret_cast<cudaStream_t>(stream));
 }
 
 adj_status_t adjprod_modp(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, const uint32_t *A, int64_t lda,

@@ -41,12 +41,20 @@ __device__ __forceinline__ void decode_range(uint32_t y, int kblocks, int &kb0, 
 
 // store 32 consecutive residues r[0..31] of output row `row`, columns col..col+31
 __device__ __forceinline__ void store_chunk(const LeafProduct &pr, int64_t row, int64_t col,
-                                            const uint32_t (&r)[32]) {
+                                            const uint32_t (&r)[32], const ModP &m) {
   if (row >= pr.out_rows || col >= pr.out_cols) return;
   if (pr.sym && col > row) return;
   const bool full = (col + 32 <= pr.out_cols) && (!pr.sym || col + 31 <= row) && pr.vec_ok;
   if (pr.out_u32) {
     uint32_t *o = reinterpret_cast<uint32_t *>(pr.out) + row * pr.ldo + col;
+    if (pr.axpby) {   // SYRK form: out <- alpha v + beta out_old (scalar path, final output only)
+#pragma unroll 4
+      for (int e = 0; e < 32; ++e)
+        if (col + e < pr.out_cols && (!pr.sym || col + e <= row))
+          o[e] = addmod(mulmod(pr.alpha, r[e], m), mulmod(pr.beta, mod_u32(o[e], m), m),
+                        m);
+      return;
+    }
     if (full) {
 #pragma unroll
       for (int i = 0; i < 8; ++i)
@@ -352,7 +360,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (ADJ_EPI_WARPS 
               d[i4] = make_uint4(v[8 * i4] | (v[8 * i4 + 1] << 16), v[8 * i4 + 2] | (v[8 * i4 + 3] << 16),
                                  v[8 * i4 + 4] | (v[8 * i4 + 5] << 16), v[8 * i4 + 6] | (v[8 * i4 + 7] << 16));
           } else if (!dbg_nostore) {
-            store_chunk(pr, row, col0 + c * 32, v);
+            store_chunk(pr, row, col0 + c * 32, v, mod);
           } else if (v[0] == 0xFFFFFFFFu && v[31] == 0x12345u) {
             prow0[0] = v[1];
           }
@@ -431,7 +439,7 @@ __global__ void __launch_bounds__(256) fixup_kernel(const __grid_constant__ Leaf
   }
 #pragma unroll
   for (int e = 0; e < 32; ++e) acc[e] = mod_u32(acc[e], P.mod);   // < npieces * p < 2^32
-  store_chunk(pr, (int64_t)ft.I * 256 + lr, (int64_t)ft.J * 256 + c * 32, acc);
+  store_chunk(pr, (int64_t)ft.I * 256 + lr, (int64_t)ft.J * 256 + c * 32, acc, P.mod);
 }
 
 cudaError_t launch_fixup(const LeafParams &p, const FixupTile *tiles, int n, cudaStream_t s) {
@@ -855,6 +863,14 @@ cudaError_t launch_split(const SplitParams &p, cudaStream_t s) {
 // 64 x 64 tiles of the (mh x mh) product grid; thread (tx, ty) owns 4 consecutive columns of
 // rows ty, ty+16, ty+32, ty+48 (8-byte u16 loads).  The mirrored tile (tj, ti) is staged
 // through shared memory for Up(U1) = Low(U1)^T and P4^T.
+// SYRK form on the final output: v <- alpha v + beta old (mod p)
+__device__ __forceinline__ void axpby4(const uint32_t *o, int64_t ncols_ok, uint32_t (&v)[4], uint32_t alpha,
+                                       uint32_t beta, const ModP &m) {
+#pragma unroll
+  for (int e = 0; e < 4; ++e)
+    if (e < ncols_ok) v[e] = addmod(mulmod(alpha, v[e], m), mulmod(beta, mod_u32(o[e], m), m), m);
+}
+
 template <typename OutT>
 __device__ __forceinline__ void store4(OutT *o, bool vec, int64_t ncols_ok, const uint32_t (&v)[4]) {
   if (vec && ncols_ok >= 4 && (reinterpret_cast<uintptr_t>(o) % (4 * sizeof(OutT)) == 0)) {
@@ -922,6 +938,8 @@ __global__ void __launch_bounds__(256) combine_kernel(const __grid_constant__ Co
       c21[e] = addmod(addmod(u1[e], p4[e], m), p3[e], m);  // U4 = U1 + P4 + P3
     }
     const int64_t n21 = min64(4, min64(mh - j, ov - j));
+    if (sizeof(OutT) == 4 && P.axpby && mh + i < ov)
+      axpby4(reinterpret_cast<const uint32_t *>(O + (mh + i) * N.ldo + j), n21, c21, P.alpha, P.beta, m);
     if (mh + i < ov) store4<OutT>(O + (mh + i) * N.ldo + j, vec, n21, c21);                         // C21
     if (any_low) {
       uint32_t p2[4], c22[4], c11[4];
@@ -932,6 +950,12 @@ __global__ void __launch_bounds__(256) combine_kernel(const __grid_constant__ Co
         c11[e] = addmod(p1[e], p2[e], m);                              // U3 = P1 + P2
       }
       const int64_t nlow = min64(4, i - j + 1);           // columns j..i only
+      if (sizeof(OutT) == 4 && P.axpby) {
+        if (mh + i < ov)
+          axpby4(reinterpret_cast<const uint32_t *>(O + (mh + i) * N.ldo + mh + j), min64(nlow, ov - mh - j), c22,
+                 P.alpha, P.beta, m);
+        if (i < ov) axpby4(reinterpret_cast<const uint32_t *>(O + i * N.ldo + j), min64(nlow, ov - j), c11, P.alpha, P.beta, m);
+      }
       if (mh + i < ov) store4<OutT>(O + (mh + i) * N.ldo + mh + j, vec && nlow == 4, min64(nlow, ov - mh - j), c22);
       if (i < ov) store4<OutT>(O + i * N.ldo + j, vec && nlow == 4, min64(nlow, ov - j), c11);
     }
@@ -952,7 +976,8 @@ cudaError_t launch_combine(const CombParams &p, cudaStream_t s) {
 // G lower (u16, ldg), H full (u16, ldh); C interleaved (re, im) uint32 pairs, Low only.
 __global__ void __launch_bounds__(256) twom_kernel(int64_t m, const uint16_t *G, int64_t ldg,
                                                    const uint16_t *H, int64_t ldh, uint32_t *C,
-                                                   int64_t ldc, ModP mod) {
+                                                   int64_t ldc, ModP mod, uint32_t alpha, uint32_t beta,
+                                                   int axpby) {
   const int ti = blockIdx.y, tj = blockIdx.x;
   if (ti < tj) return;
   const int tx = threadIdx.x, ty = threadIdx.y;
@@ -967,18 +992,23 @@ __global__ void __launch_bounds__(256) twom_kernel(int64_t m, const uint16_t *G,
     const int64_t i = i0 + y, j = j0 + tx;
     if (i >= m || j > i) continue;
     const uint32_t h = H[i * ldh + j], ht = sH[tx][y];   // H(i,j), H(j,i)
-    const uint32_t re = submod(submod(G[i * ldg + j], h, mod), ht, mod);
-    const uint32_t im = submod(ht, h, mod);
+    uint32_t re = submod(submod(G[i * ldg + j], h, mod), ht, mod);
+    uint32_t im = submod(ht, h, mod);
+    if (axpby) {
+      re = addmod(mulmod(alpha, re, mod), mulmod(beta, mod_u32(C[2 * (i * ldc + j)], mod), mod), mod);
+      im = addmod(mulmod(alpha, im, mod), mulmod(beta, mod_u32(C[2 * (i * ldc + j) + 1], mod), mod), mod);
+    }
     C[2 * (i * ldc + j)] = re;
     C[2 * (i * ldc + j) + 1] = im;
   }
 }
 
 cudaError_t launch_twom(int64_t m, const uint16_t *G, int64_t ldg, const uint16_t *H, int64_t ldh,
-                        uint32_t *C, int64_t ldc, const ModP &mod, cudaStream_t s) {
+                        uint32_t *C, int64_t ldc, const ModP &mod, uint32_t alpha, uint32_t beta, int axpby,
+                        cudaStream_t s) {
   if (m == 0) return cudaSuccess;
   const unsigned nt = (unsigned)((m + 31) / 32);
-  twom_kernel<<<dim3(nt, nt), dim3(32, 8), 0, s>>>(m, G, ldg, H, ldh, C, ldc, mod);
+  twom_kernel<<<dim3(nt, nt), dim3(32, 8), 0, s>>>(m, G, ldg, H, ldh, C, ldc, mod, alpha, beta, axpby);
   return cudaGetLastError();
 }
 
@@ -1002,6 +1032,27 @@ cudaError_t launch_mod_lower(int64_t m, int w, const uint32_t *src, int64_t lds,
     const int64_t rows = (m - r0) < 65535 ? (m - r0) : 65535;
     mod_lower_kernel<<<dim3((unsigned)(per_row < 64 ? per_row : 64), (unsigned)rows), 256, 0, s>>>(
         r0, w, src, lds, dst, ldd, mod);
+  }
+  return cudaGetLastError();
+}
+
+// Low(X) <- beta Low(X) (SYRK form with k = 0)
+__global__ void scale_lower_kernel(int64_t row0, int w, uint32_t *X, int64_t ldx, uint32_t beta, ModP mod) {
+  const int64_t i = row0 + blockIdx.y;
+  uint32_t *row = X + i * ldx * w;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < (i + 1) * w;
+       j += (int64_t)gridDim.x * blockDim.x)
+    row[j] = mulmod(beta, mod_u32(row[j], mod), mod);
+}
+
+cudaError_t launch_scale_lower(int64_t m, int w, uint32_t *X, int64_t ldx, uint32_t beta, const ModP &mod,
+                               cudaStream_t s) {
+  if (m == 0) return cudaSuccess;
+  const int64_t per_row = (m * w + 255) / 256;
+  for (int64_t r0 = 0; r0 < m; r0 += 65535) {
+    const int64_t rows = (m - r0) < 65535 ? (m - r0) : 65535;
+    scale_lower_kernel<<<dim3((unsigned)(per_row < 64 ? per_row : 64), (unsigned)rows), 256, 0, s>>>(
+        r0, w, X, ldx, beta, mod);
   }
   return cudaGetLastError();
 }

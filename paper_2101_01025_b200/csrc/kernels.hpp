@@ -12,7 +12,10 @@ cudaError_t launch_preadd(const PreParams &p, cudaStream_t s);
 cudaError_t launch_split(const SplitParams &p, cudaStream_t s);
 cudaError_t launch_combine(const CombParams &p, cudaStream_t s);
 cudaError_t launch_twom(int64_t m, const uint16_t *G, int64_t ldg, const uint16_t *H, int64_t ldh,
-                        uint32_t *C, int64_t ldc, const ModP &mod, cudaStream_t s);
+                        uint32_t *C, int64_t ldc, const ModP &mod, uint32_t alpha, uint32_t beta, int axpby,
+                        cudaStream_t s);
+cudaError_t launch_scale_lower(int64_t m, int w, uint32_t *X, int64_t ldx, uint32_t beta, const ModP &mod,
+                               cudaStream_t s);
 cudaError_t launch_mod_lower(int64_t m, int w, const uint32_t *src, int64_t lds, uint32_t *dst, int64_t ldd,
                              const ModP &mod, cudaStream_t s);
 cudaError_t launch_fill_upper(int64_t m, int w, uint32_t *C, int64_t ldc, const ModP &mod, cudaStream_t s);

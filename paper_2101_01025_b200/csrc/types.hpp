@@ -30,6 +30,8 @@ struct LeafProduct {
   int32_t kseg;          // k-blocks per int32 accumulation segment (>= kblocks: one segment)
   int64_t ldo;           // output leading dimension (elements)
   void *out;
+  uint32_t alpha, beta;  // axpby: out <- alpha v + beta out (mod p), SYRK form (uint32 outputs only)
+  int32_t axpby, pad2_;
 };
 
 struct LeafTerm {        // one tcgen05.mma operand pair accumulated into accumulator `acc`
@@ -123,6 +125,8 @@ struct CombParams {
   int32_t out_u32;
   int64_t mh, ldp;
   ModP mod;
+  uint32_t alpha, beta;    // axpby on the final (uint32) output, SYRK form
+  int32_t axpby, pad_;
 };
 
 }  // namespace adj

@@ -184,3 +184,31 @@ def test_k_segmentation_overflow_stress(adj):
     A = constant_matrix(256, k, c, p)
     got = to_host(adj.adjprod(to_dev(A), p, depth=0))
     assert (got[np.tril_indices(256)] == k * c * c % p).all()
+
+
+@pytest.mark.parametrize("phi", ["T", "H"])
+@pytest.mark.parametrize("depth", [0, 1, 2])
+@pytest.mark.parametrize("alpha,beta", [(1, 0), (0, 1), (3, 5), (8190, 8190), (12345, 0), (1, 1)])
+def test_syrk_form_alpha_beta(adj, phi, depth, alpha, beta):
+    """Low(C) <- alpha Low(A phi(A)) + beta Low(C), fused into the final writes."""
+    import torch
+    p = 8191
+    m, k = 300, 260
+    A = uniform_matrix(m, k, seed=5, p=p) if phi == "T" else uniform_matrix_ext(m, k, seed=5, p=p)
+    rng = np.random.default_rng(depth * 31 + alpha)
+    shape = (m, m) if phi == "T" else (m, m, 2)
+    C0 = rng.integers(0, 2**32, size=shape, dtype=np.uint64).astype(np.uint32)
+    dC = to_dev(C0)
+    adj.adjprod_modp_syrk(m, k, p, 0 if phi == "T" else 1, alpha, to_dev(A), k, beta, dC, m, depth=depth)
+    assert np.array_equal(to_host(dC), oracle.syrk_update(A, C0, p, alpha, beta, phi))
+
+
+def test_syrk_form_k0_and_gemm_unaffected(adj):
+    import torch
+    p = 97
+    C0 = np.arange(25, dtype=np.uint32).reshape(5, 5) * 1000
+    dC = to_dev(C0)
+    adj.adjprod_modp_syrk(5, 0, p, 0, 7, torch.zeros((5, 1), dtype=torch.int32, device="cuda"), 1, 3, dC, 5)
+    ref = C0.copy()
+    ref[np.tril_indices(5)] = (3 * (C0[np.tril_indices(5)].astype(np.int64) % p)) % p
+    assert np.array_equal(to_host(dC), ref)

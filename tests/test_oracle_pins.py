@@ -197,3 +197,20 @@ def test_freivalds_helper_has_teeth():
         bad = C.copy()
         bad[i, j] = (bad[i, j] + 1) % p
         assert not freivalds(A, bad, p), (i, j)
+
+
+def test_syrk_update_special_cases(golden):
+    """alpha = 1, beta = 0 is the plain product; alpha = 0, beta = 1 keeps Low(C) (reduced);
+    the upper triangle is never touched (SPEC.md:354-356 examples)."""
+    p = 13
+    A = uniform_matrix(9, 7, seed=2, p=p)
+    rng = np.random.default_rng(0)
+    C = rng.integers(0, 2**31, size=(9, 9)).astype(np.uint32)
+    one = oracle.syrk_update(A, C, p, 1, 0)
+    assert np.array_equal(np.tril(one), oracle.syrk_t(A, p))
+    keep = oracle.syrk_update(A, C, p, 0, 1)
+    assert np.array_equal(np.tril(keep), np.tril(C % p))
+    both = oracle.syrk_update(A, C, p, 3, 5)
+    assert np.array_equal(np.triu(both, 1), np.triu(C, 1))
+    ref = (3 * brute_syrk(A.tolist(), p).astype(np.int64) + 5 * (C.astype(np.int64) % p)) % p
+    assert np.array_equal(np.tril(both), np.tril(ref).astype(np.uint32))
