@@ -95,7 +95,8 @@ int oracle_gemm_nt(int64_t m, int64_t n, int64_t k, uint32_t p, const uint32_t *
  * (re, im) u32 pairs; lda/ldc count GF(p^2) elements. */
 int oracle_syrk_h_rows(int64_t m, int64_t k, uint32_t p, const uint32_t *A, int64_t lda,
                        uint32_t *C, int64_t ldc, int64_t r0, int64_t r1) {
-  if (m < 0 || k < 0 || p < 2 || p > 65536u || r0 < 0 || r1 > m) return 1;
+  if (m < 0 || k < 0 || p < 2 || r0 < 0 || r1 > m) return 1;
+  const int big = p > 65536u;   /* reduce every term first so the uint64 sums cannot overflow */
   uint32_t *R = reduced_copy(A, m, k, lda, 2, p);
   if (!R) return 2;
 #pragma omp parallel for schedule(dynamic, 1)
@@ -106,9 +107,15 @@ int oracle_syrk_h_rows(int64_t m, int64_t k, uint32_t p, const uint32_t *A, int6
       uint64_t re = 0, im_pos = 0, im_neg = 0;  /* (x+iy)(x'-iy') = xx'+yy' + i(yx' - xy') */
       for (int64_t t = 0; t < k; t++) {
         uint64_t x = ai[2 * t], y = ai[2 * t + 1], xp = aj[2 * t], yp = aj[2 * t + 1];
-        re += x * xp + y * yp;
-        im_pos += y * xp;
-        im_neg += x * yp;
+        if (big) {
+          re += (x * xp) % p + (y * yp) % p;
+          im_pos += (y * xp) % p;
+          im_neg += (x * yp) % p;
+        } else {
+          re += x * xp + y * yp;
+          im_pos += y * xp;
+          im_neg += x * yp;
+        }
       }
       uint64_t a = im_pos % p, b = im_neg % p;
       ROWP(C, ldc * 2, i)[2 * j] = (uint32_t)(re % p);

@@ -125,7 +125,7 @@ def test_o1_trace_and_rows_subset():
     assert np.array_equal(part[40:], C[40:]) and not part[:40].any()
 
 
-@pytest.mark.parametrize("p", [3, 7, 8191])
+@pytest.mark.parametrize("p", [3, 7, 8191, 131071, 2147483647])
 def test_o1_herk_bruteforce(p):
     A = uniform_matrix_ext(6, 5, seed=9, p=p)
     assert np.array_equal(oracle.syrk_h(A, p), brute_herk(A, p))
