@@ -23,9 +23,11 @@
  * - Low/Up: Low includes the diagonal.  Only Low(C) is written; the
  *   strict upper triangle of C is left untouched unless ADJ_FILL_UPPER is set, in which
  *   case Up(C) = phi(Low(C)) (Lemma lem:uplow).
- * - Supported moduli (v1): odd primes 3 <= p <= 65521.  Limb schemes: p <= 255 one signed
- *   int8 limb; 257 <= p <= 16763 two balanced base-2^7 limbs with Karatsuba; otherwise a
- *   signed-int8 high limb and an unsigned-int8 low limb.
+ * - Supported moduli: odd primes 3 <= p <= 262139 (the largest prime below 2^18; this covers
+ *   the paper's own moduli 131071 and 131041).  Limb schemes: p <= 255
+ *   one signed int8 limb; 257 <= p <= 16763 two balanced base-2^7 limbs with Karatsuba;
+ *   16787 <= p <= 65521 a signed-int8 high limb and an unsigned-int8 low limb; p > 2^16 three
+ *   balanced base-2^6 digits with 3-way Karatsuba.
  * - Shapes need no alignment: odd or ragged dimensions are zero-padded internally, which
  *   leaves A phi(A) unchanged.
  * - Every call is asynchronous on `stream`, like cuBLAS.  Argument validation is
@@ -57,7 +59,7 @@ typedef enum {
 typedef enum {
   ADJ_OK = 0,
   ADJ_ERR_INVALID_VALUE = 1,       /* negative/inconsistent sizes, null pointers, A/C overlap */
-  ADJ_ERR_UNSUPPORTED_MODULUS = 2, /* p not an odd prime in [3, 65521]; phi=H with p != 3 mod 4 */
+  ADJ_ERR_UNSUPPORTED_MODULUS = 2, /* p not an odd prime in [3, 262139]; phi=H with p != 3 mod 4 */
   ADJ_ERR_WORKSPACE = 3,           /* caller workspace too small / allocation failed */
   ADJ_ERR_CUDA = 4,                /* a CUDA runtime call failed */
   ADJ_ERR_NCCL = 5,                /* NCCL missing or a collective failed */
@@ -79,7 +81,7 @@ typedef struct {
  *   Problem statement: Alg. alg:MIAHMM "Ensure Low(A phi(A))".
  *   m, k   : A is m x k (m output rows, k contracted columns); C is m x m.  m = 0 is a no-op;
  *            k = 0 writes Low(C) = 0.
- *   p      : odd prime, 3 <= p <= 65521 (phi = ADJ_PHI_H additionally needs p = 3 mod 4).
+ *   p      : odd prime, 3 <= p <= 262139 (phi = ADJ_PHI_H additionally needs p = 3 mod 4).
  *   phi    : ADJ_PHI_T (A, C uint32 residues) or ADJ_PHI_H (A, C interleaved (re, im) pairs).
  *   A, lda : device, lda >= k.     C, ldc : device, ldc >= m.  A and C must not overlap.
  *   Uses default options (automatic depth, library-allocated workspace).

@@ -169,7 +169,7 @@ adj_status_t get_plan(Plan **out, int kind, int64_t m, int64_t n, int64_t k, uin
 }
 
 // ------------------------------------------------------------------ validation helpers
-bool valid_modulus(uint32_t p) { return p >= 3 && p <= 65521 && is_prime_u32(p); }
+bool valid_modulus(uint32_t p) { return p >= 3 && p <= kMaxModulus && is_prime_u32(p); }
 
 bool overlap(const void *a, size_t abytes, const void *b, size_t bbytes) {
   uintptr_t a0 = (uintptr_t)a, a1 = a0 + abytes, b0 = (uintptr_t)b, b1 = b0 + bbytes;
@@ -195,9 +195,9 @@ InView make_view(const void *ptr, int64_t ld, int64_t rows, int64_t cols, int ty
   return v;
 }
 
-InView child_view(const InView &pv, int c, const LevelPlan &Lp, uint16_t *s3, int64_t s3_ld) {
+InView child_view(const InView &pv, int c, const LevelPlan &Lp, void *s3, int64_t s3_ld, bool res32) {
   // children of a node at level l-1 (half sizes Lp.mh, Lp.kh): 0 = X11, 1 = X12, 2 = S3
-  if (c == 2) return make_view(s3, s3_ld, Lp.mh, Lp.kh, IN_U16);
+  if (c == 2) return make_view(s3, s3_ld, Lp.mh, Lp.kh, res32 ? IN_U32 : IN_U16);
   const int64_t rows = std::min(pv.rows_valid, Lp.mh);
   if (c == 0) return make_view(pv.ptr, pv.ld, rows, std::min(pv.cols_valid, Lp.kh), pv.type);
   const int esz = pv.type == IN_U16 ? 2 : (pv.type == IN_U32 ? 4 : 8);
@@ -216,13 +216,13 @@ struct Ptrs {
   uint8_t *ws = nullptr;
 };
 
-uint16_t *pbuf(const Plan &P, uint8_t *ws, int l, int n, int idx) {
+void *pbuf(const Plan &P, uint8_t *ws, int l, int n, int idx) {
   const LevelPlan &L = P.lv[l];
-  return reinterpret_cast<uint16_t *>(ws + L.p_offset + ((size_t)n * 5 + idx) * L.p_buf_bytes);
+  return ws + L.p_offset + ((size_t)n * 5 + idx) * L.p_buf_bytes;
 }
-uint16_t *s3buf(const Plan &P, uint8_t *ws, int l, int n) {
+void *s3buf(const Plan &P, uint8_t *ws, int l, int n) {
   const LevelPlan &L = P.lv[l];
-  return reinterpret_cast<uint16_t *>(ws + L.s3_offset + (size_t)n * L.s3_node_bytes);
+  return ws + L.s3_offset + (size_t)n * L.s3_node_bytes;
 }
 
 adj_status_t launch_leaf_all(const Plan &P, const Ptrs &x, cudaStream_t s) {
@@ -254,7 +254,7 @@ adj_status_t launch_leaf_all(const Plan &P, const Ptrs &x, cudaStream_t s) {
   }
   L.tiles = reinterpret_cast<const uint2 *>(P.d_tiles);
   L.n_tiles = (int32_t)(P.tiles.size() / 2);
-  L.fixup = reinterpret_cast<uint16_t *>(x.ws + P.fixup_offset);
+  L.fixup = x.ws + P.fixup_offset;
   if (const char *dbg = getenv("ADJ_LEAF_DEBUG")) L.debug = atoi(dbg);   // diagnostics only
   LAUNCH_CLS(CLS_LEAF, launch_leaf2(L, P.nacc, P.segmented, P.grid, s));
   if (!P.fixups.empty()) LAUNCH_CLS(CLS_LEAF, launch_fixup(L, P.d_fixups, (int)P.fixups.size(), s));
@@ -291,7 +291,8 @@ adj_status_t run_tree(const Plan &P, const InView &root, const Ptrs &x, cudaStre
       views[l].resize(L.n_nodes);
       for (int n = 0; n < L.n_nodes; ++n) {
         const int parent = n / 3, c = n % 3;
-        views[l][n] = child_view(views[l - 1][parent], c, Lp, c == 2 ? s3buf(P, x.ws, l - 1, parent) : nullptr, Lp.kh);
+        views[l][n] = child_view(views[l - 1][parent], c, Lp, c == 2 ? s3buf(P, x.ws, l - 1, parent) : nullptr, Lp.kh,
+                                 P.res32);
       }
     }
     PreParams pp;
@@ -307,6 +308,7 @@ adj_status_t run_tree(const Plan &P, const InView &root, const Ptrs &x, cudaStre
     pp.rows_pad = L.rows_pad;
     pp.kpad = L.kpad;
     pp.arena = reinterpret_cast<int8_t *>(x.ws + P.arenas[L.arena].offset);
+    pp.res32 = P.res32 ? 1 : 0;
     pp.mod = P.mod;
     for (int n = 0; n < L.n_nodes; ++n) {
       PreNode &N = pp.nodes[n];
@@ -341,6 +343,8 @@ adj_status_t run_combine(const Plan &P, const Ptrs &x, void *final_out, int64_t 
     cp.ldp = L.rows_pad;
     cp.mod = P.mod;
     cp.out_u32 = (l == 1) ? (final_u32 ? 1 : 0) : 0;
+    cp.in32 = P.res32 ? 1 : 0;
+    if (P.res32) cp.out_u32 = 1;
     if (l == 1 && final_u32) {
       cp.alpha = x.alpha;
       cp.beta = x.beta;
@@ -389,8 +393,8 @@ adj_status_t run_syrk(const Plan &P, const Ptrs &x, adj_phi_t phi, uint32_t flag
     // root pre-addition's side output at depth >= 1).
     uint8_t *arena0 = x.ws + P.arenas[0].offset;
     InView troot = make_view(x.A, x.lda, m, k, IN_PAIR_SUM);
-    uint16_t *G = reinterpret_cast<uint16_t *>(x.ws + P.g_offset);
-    uint16_t *H = reinterpret_cast<uint16_t *>(x.ws + P.h_offset);
+    void *G = x.ws + P.g_offset;
+    void *H = x.ws + P.h_offset;
     if (P.depth == 0) {
       SplitParams sp;
       std::memset(&sp, 0, sizeof(sp));
@@ -419,8 +423,8 @@ adj_status_t run_syrk(const Plan &P, const Ptrs &x, adj_phi_t phi, uint32_t flag
       st = run_combine(P, x, G, P.rows_pad0, false, s);
       if (st) return st;
     }
-    LAUNCH_CLS(CLS_COMB, launch_twom(m, G, P.rows_pad0, H, P.rows_pad0, x.C, x.ldc, P.mod, x.alpha, x.beta,
-                                     x.axpby, s));
+    LAUNCH_CLS(CLS_COMB, launch_twom(m, G, P.rows_pad0, H, P.rows_pad0, P.res32 ? 1 : 0, x.C, x.ldc, P.mod, x.alpha,
+                                     x.beta, x.axpby, s));
   }
   if (flags & ADJ_FILL_UPPER) LAUNCH(launch_fill_upper(m, phi == ADJ_PHI_H ? 2 : 1, x.C, x.ldc, P.mod, s));
   return ADJ_OK;
@@ -430,7 +434,7 @@ adj_status_t validate_syrk(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, cons
                            const uint32_t *C, int64_t ldc) {
   if (m < 0 || k < 0) return fail(ADJ_ERR_INVALID_VALUE, "negative dimension (m=%lld, k=%lld)", (long long)m, (long long)k);
   if (phi != ADJ_PHI_T && phi != ADJ_PHI_H) return fail(ADJ_ERR_INVALID_VALUE, "phi must be ADJ_PHI_T or ADJ_PHI_H");
-  if (!valid_modulus(p)) return fail(ADJ_ERR_UNSUPPORTED_MODULUS, "p=%u is not an odd prime in [3, 65521]", p);
+  if (!valid_modulus(p)) return fail(ADJ_ERR_UNSUPPORTED_MODULUS, "p=%u is not an odd prime in [3, 262139]", p);
   if (phi == ADJ_PHI_H && p % 4 != 3)
     return fail(ADJ_ERR_UNSUPPORTED_MODULUS, "phi=H needs p = 3 mod 4 (GF(p)[i]/(i^2+1)); p=%u", p);
   if (m == 0) return ADJ_OK;
@@ -497,7 +501,7 @@ adj_status_t adj_sos(uint32_t p, uint32_t k, uint32_t *a, uint32_t *b) {
 
 adj_status_t adj_skew_unitary(uint32_t p, adj_phi_t phi, int *kind, uint32_t *a, uint32_t *b) {
   if (!kind || !a || !b) return fail(ADJ_ERR_INVALID_VALUE, "null output");
-  if (!valid_modulus(p)) return fail(ADJ_ERR_UNSUPPORTED_MODULUS, "p=%u is not an odd prime in [3, 65521]", p);
+  if (!valid_modulus(p)) return fail(ADJ_ERR_UNSUPPORTED_MODULUS, "p=%u is not an odd prime in [3, 262139]", p);
   if (phi == ADJ_PHI_H && p % 4 != 3) return fail(ADJ_ERR_UNSUPPORTED_MODULUS, "phi=H needs p = 3 mod 4");
   SkewY y = skew_unitary(p);
   *kind = y.kind;
@@ -516,7 +520,7 @@ adj_status_t adjprod_modp_workspace_size(int64_t m, int64_t k, uint32_t p, adj_p
                                          size_t *bytes) {
   if (!bytes) return fail(ADJ_ERR_INVALID_VALUE, "null output");
   if (m < 0 || k < 0) return fail(ADJ_ERR_INVALID_VALUE, "negative dimension");
-  if (!valid_modulus(p)) return fail(ADJ_ERR_UNSUPPORTED_MODULUS, "p=%u is not an odd prime in [3, 65521]", p);
+  if (!valid_modulus(p)) return fail(ADJ_ERR_UNSUPPORTED_MODULUS, "p=%u is not an odd prime in [3, 262139]", p);
   if (m == 0 || k == 0) { *bytes = 0; return ADJ_OK; }
   int depth = (opts && opts->depth >= 0) ? opts->depth : auto_depth(m, k, p, (int)phi);
   Plan P;
@@ -592,7 +596,7 @@ adj_status_t adjprod_modp(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, const
 adj_status_t gemm_modp(int64_t m, int64_t n, int64_t k, uint32_t p, const uint32_t *A, int64_t lda,
                        const uint32_t *B, int64_t ldb, uint32_t *C, int64_t ldc, adj_stream_t stream) {
   if (m < 0 || n < 0 || k < 0) return fail(ADJ_ERR_INVALID_VALUE, "negative dimension");
-  if (!valid_modulus(p)) return fail(ADJ_ERR_UNSUPPORTED_MODULUS, "p=%u is not an odd prime in [3, 65521]", p);
+  if (!valid_modulus(p)) return fail(ADJ_ERR_UNSUPPORTED_MODULUS, "p=%u is not an odd prime in [3, 262139]", p);
   if (m == 0 || n == 0) return ADJ_OK;
   if (!C || (k > 0 && (!A || !B))) return fail(ADJ_ERR_INVALID_VALUE, "null pointer");
   if (lda < k || ldb < k || ldc < n) return fail(ADJ_ERR_INVALID_VALUE, "leading dimension too small");
@@ -625,7 +629,7 @@ adj_status_t gemm_modp(int64_t m, int64_t n, int64_t k, uint32_t p, const uint32
 
 adj_status_t adj_mod_lower(int64_t m, uint32_t p, adj_phi_t phi, uint32_t *X, int64_t ldx, adj_stream_t stream) {
   if (m < 0 || ldx < m) return fail(ADJ_ERR_INVALID_VALUE, "bad dimensions");
-  if (!valid_modulus(p)) return fail(ADJ_ERR_UNSUPPORTED_MODULUS, "p=%u is not an odd prime in [3, 65521]", p);
+  if (!valid_modulus(p)) return fail(ADJ_ERR_UNSUPPORTED_MODULUS, "p=%u is not an odd prime in [3, 262139]", p);
   if (m == 0) return ADJ_OK;
   if (!X) return fail(ADJ_ERR_INVALID_VALUE, "X is null");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);

@@ -84,11 +84,12 @@ SkewY skew_unitary(uint32_t p) {
 LimbScheme limb_scheme(uint32_t p) {
   if (p <= 255) return LIMB_S8;
   if (p <= 16763) return LIMB_K7;
-  return LIMB_SU8;
+  if (p <= 65521) return LIMB_SU8;
+  return LIMB_T6;
 }
 
-int limb_planes(LimbScheme s) { return s == LIMB_S8 ? 1 : (s == LIMB_K7 ? 3 : 2); }
-int limb_accs(LimbScheme s) { return s == LIMB_S8 ? 1 : 3; }
+int limb_planes(LimbScheme s) { return s == LIMB_S8 ? 1 : (s == LIMB_K7 ? 3 : (s == LIMB_SU8 ? 2 : 6)); }
+int limb_accs(LimbScheme s) { return s == LIMB_S8 ? 1 : (s == LIMB_T6 ? 6 : 3); }
 
 int64_t limb_kmax(LimbScheme s, uint32_t p) {
   const int64_t lim = 2147483647;
@@ -99,6 +100,7 @@ int64_t limb_kmax(LimbScheme s, uint32_t p) {
     int64_t t = mid * mid > 64 * 64 ? mid * mid : 64 * 64;
     return lim / t;
   }
+  if (s == LIMB_T6) return lim / (64 * 64);   // digit pair sums in [-64, 63]
   // SU8: lo*lo <= 255^2, cross: |hi*lo| + |lo*hi| <= 2 * 128 * 255
   int64_t t = 2 * 128 * 255;
   if (255 * 255 > t) t = 255 * 255;

@@ -24,7 +24,10 @@ enum LimbScheme : int {
   LIMB_S8 = 0,   // p <= 255: one signed limb, centered residue
   LIMB_K7 = 1,   // p <= 16763: balanced base 2^7 (hi, lo, mid = hi + lo), Karatsuba, 3 accumulators
   LIMB_SU8 = 2,  // p <= 65521: hi = floor(c/256) signed, lo = c - 256 hi unsigned; 4 MMAs, 3 accumulators
+  LIMB_T6 = 3,   // p < 2^18: three balanced base-64 digits (d2, d1, d0) + the pair sums d2+d1, d1+d0,
+                 // d2+d0 (all s8); 3-way Karatsuba: 6 MMAs, 6 accumulators
 };
+constexpr uint32_t kMaxModulus = 262139;   // largest prime below 2^18
 LimbScheme limb_scheme(uint32_t p);
 int limb_planes(LimbScheme s);       // int8 planes per operand
 int limb_accs(LimbScheme s);         // TMEM accumulators per output tile

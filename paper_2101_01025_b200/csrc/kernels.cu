@@ -51,8 +51,7 @@ __device__ __forceinline__ void store_chunk(const LeafProduct &pr, int64_t row, 
 #pragma unroll 4
       for (int e = 0; e < 32; ++e)
         if (col + e < pr.out_cols && (!pr.sym || col + e <= row))
-          o[e] = addmod(mulmod(pr.alpha, r[e], m), mulmod(pr.beta, mod_u32(o[e], m), m),
-                        m);
+          o[e] = addmod(mulmod_any(pr.alpha, r[e], m), mulmod_any(pr.beta, mod_u32(o[e], m), m), m);
       return;
     }
     if (full) {
@@ -95,9 +94,9 @@ __device__ __forceinline__ void store_chunk(const LeafProduct &pr, int64_t row, 
 #ifndef ADJ_EPI_WARPS
 #define ADJ_EPI_WARPS 8
 #endif
-template <int NACC, bool PART>
+template <int NACC, bool PART, bool WIDE = false>
 struct Leaf2Cfg {
-  static constexpr int STAGES = PART ? 5 : 6;
+  static constexpr int STAGES = PART ? (WIDE ? 4 : 5) : 6;
   static constexpr int TILE = 256;
   static constexpr int A_BYTES = 128 * kBK;
   static constexpr int B_BYTES = 128 * kBK;
@@ -105,7 +104,8 @@ struct Leaf2Cfg {
   static constexpr int SLOTS = 2;
   // weighted mod-p partial sums of the limb accumulators: 128 rows x 128 words (u16 pairs),
   // row stride 129 words so that the 32 rows a warp touches fall in 32 different banks
-  static constexpr int PART_STRIDE = 129;
+  // WIDE (p > 2^16): residues < 2^18 packed 24-bit (4 values in 3 words): 192 words + 1 pad per row
+  static constexpr int PART_STRIDE = WIDE ? 193 : 129;
   static constexpr int PART_BYTES = PART ? 128 * PART_STRIDE * 4 : 0;
   static constexpr int BAR_BYTES = 8 * (2 * STAGES + 2 * SLOTS) + 16;
   static constexpr int SMEM = STAGES * STAGE_BYTES + PART_BYTES + 1024 + BAR_BYTES;
@@ -116,10 +116,10 @@ struct Leaf2Cfg {
 // NACC limb accumulators per tile; each may be split into K segments of at most pr.kseg k-blocks
 // (int32 bound).  A (accumulator, segment) pair is one TMEM unit; PART = the
 // epilogue folds units into the shared-memory partial sum (needed when a tile has > 1 unit).
-template <int NACC, bool PART>
+template <int NACC, bool PART, bool WIDE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (ADJ_EPI_WARPS + 3), 1)
     leaf2_kernel(const __grid_constant__ LeafParams P) {
-  using Cfg = Leaf2Cfg<NACC, PART>;
+  using Cfg = Leaf2Cfg<NACC, PART, WIDE>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint32_t *part_s = reinterpret_cast<uint32_t *>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
@@ -307,7 +307,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (ADJ_EPI_WARPS 
       const int64_t row = (int64_t)I * Cfg::TILE + rank * 128 + lrow;
       const int64_t col0 = (int64_t)J * Cfg::TILE + h0 * 128;
       // tail piece: residue partial of this CTA's 128 x 256 half-tile into the fixup slot
-      uint16_t *fx = piece ? P.fixup + (size_t)(piece - 1) * 65536 + (rank * 128 + lrow) * 256 + h0 * 128 : nullptr;
+      const size_t fxo = (size_t)(piece - 1) * 65536 + (rank * 128 + lrow) * 256 + h0 * 128;
+      uint16_t *fx = (piece && !P.fixup32) ? static_cast<uint16_t *>(P.fixup) + fxo : nullptr;
+      uint32_t *fx32 = (piece && P.fixup32) ? static_cast<uint32_t *>(P.fixup) + fxo : nullptr;
       const int nseg = (jb1 - jb0 + pr.kseg - 1) / pr.kseg;
       const int nunits = NACC * nseg;
 #pragma unroll 1
@@ -335,9 +337,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (ADJ_EPI_WARPS 
           for (int e = 0; e < 32; ++e) v[e] = mod_s32((int32_t)v[e], mod);
           if (NACC > 1 || w != 1) {
 #pragma unroll
-            for (int e = 0; e < 32; ++e) v[e] = mulmod(v[e], w, mod);
+            for (int e = 0; e < 32; ++e) v[e] = WIDE ? mulmod_w(v[e], w, mod) : mulmod(v[e], w, mod);
           }
-          if constexpr (PART) {
+          if constexpr (PART && !WIDE) {
             uint32_t *pc = prow0 + h0 * 64 + c * 16;
             if (u > 0) {
 #pragma unroll
@@ -353,7 +355,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (ADJ_EPI_WARPS 
               continue;
             }
           }
-          if (fx) {
+          if constexpr (PART && WIDE) {
+            uint32_t *pc = prow0 + h0 * 96 + c * 24;     // 32 residues of 24 bits = 24 words
+            if (u > 0) {
+#pragma unroll
+              for (int g = 0; g < 8; ++g) {
+                const uint32_t w0 = pc[3 * g], w1 = pc[3 * g + 1], w2 = pc[3 * g + 2];
+                v[4 * g] = addmod(v[4 * g], w0 & 0xFFFFFF, mod);
+                v[4 * g + 1] = addmod(v[4 * g + 1], (w0 >> 24) | ((w1 & 0xFFFF) << 8), mod);
+                v[4 * g + 2] = addmod(v[4 * g + 2], (w1 >> 16) | ((w2 & 0xFF) << 16), mod);
+                v[4 * g + 3] = addmod(v[4 * g + 3], w2 >> 8, mod);
+              }
+            }
+            if (u < nunits - 1) {
+#pragma unroll
+              for (int g = 0; g < 8; ++g) {
+                pc[3 * g] = v[4 * g] | (v[4 * g + 1] << 24);
+                pc[3 * g + 1] = (v[4 * g + 1] >> 8) | (v[4 * g + 2] << 16);
+                pc[3 * g + 2] = (v[4 * g + 2] >> 16) | (v[4 * g + 3] << 8);
+              }
+              continue;
+            }
+          }
+          if (fx32) {
+            uint4 *d = reinterpret_cast<uint4 *>(fx32 + c * 32);
+#pragma unroll
+            for (int i4 = 0; i4 < 8; ++i4) d[i4] = make_uint4(v[4 * i4], v[4 * i4 + 1], v[4 * i4 + 2], v[4 * i4 + 3]);
+          } else if (fx) {
             uint4 *d = reinterpret_cast<uint4 *>(fx + c * 32);
 #pragma unroll
             for (int i4 = 0; i4 < 4; ++i4)
@@ -391,25 +419,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (ADJ_EPI_WARPS 
   }
 }
 
-template <int NACC, bool PART>
+template <int NACC, bool PART, bool WIDE>
 static cudaError_t launch_leaf2_t(const LeafParams &p, int grid, cudaStream_t s) {
-  using Cfg = Leaf2Cfg<NACC, PART>;
+  using Cfg = Leaf2Cfg<NACC, PART, WIDE>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(leaf2_kernel<NACC, PART>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(leaf2_kernel<NACC, PART, WIDE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          Cfg::SMEM);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  leaf2_kernel<NACC, PART><<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(p);
+  leaf2_kernel<NACC, PART, WIDE><<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(p);
   return cudaGetLastError();
 }
 
 cudaError_t launch_leaf2(const LeafParams &p, int nacc, bool segmented, int grid, cudaStream_t s) {
   if (p.n_tiles == 0) return cudaSuccess;
   if (grid % 2) return cudaErrorInvalidValue;
-  if (nacc == 1) return segmented ? launch_leaf2_t<1, true>(p, grid, s) : launch_leaf2_t<1, false>(p, grid, s);
-  if (nacc == 3) return launch_leaf2_t<3, true>(p, grid, s);
+  if (nacc == 1)
+    return segmented ? launch_leaf2_t<1, true, false>(p, grid, s) : launch_leaf2_t<1, false, false>(p, grid, s);
+  if (nacc == 3) return launch_leaf2_t<3, true, false>(p, grid, s);
+  if (nacc == 6) return launch_leaf2_t<6, true, true>(p, grid, s);
   return cudaErrorInvalidValue;
 }
 
@@ -425,7 +455,17 @@ __global__ void __launch_bounds__(256) fixup_kernel(const __grid_constant__ Leaf
 #pragma unroll
   for (int e = 0; e < 32; ++e) acc[e] = 0;
   for (int pc = 0; pc < ft.npieces; ++pc) {
-    const uint4 *src = reinterpret_cast<const uint4 *>(P.fixup + (size_t)(ft.slot0 + pc) * 65536 + lr * 256 + c * 32);
+    const size_t off = (size_t)(ft.slot0 + pc) * 65536 + lr * 256 + c * 32;
+    if (P.fixup32) {
+      const uint4 *src = reinterpret_cast<const uint4 *>(static_cast<const uint32_t *>(P.fixup) + off);
+#pragma unroll
+      for (int i4 = 0; i4 < 8; ++i4) {
+        const uint4 w = src[i4];
+        acc[4 * i4] += w.x; acc[4 * i4 + 1] += w.y; acc[4 * i4 + 2] += w.z; acc[4 * i4 + 3] += w.w;
+      }
+      continue;
+    }
+    const uint4 *src = reinterpret_cast<const uint4 *>(static_cast<const uint16_t *>(P.fixup) + off);
 #pragma unroll
     for (int i4 = 0; i4 < 4; ++i4) {
       const uint4 w = src[i4];
@@ -556,9 +596,34 @@ __device__ __forceinline__ int32_t center_lazy(int32_t v, float invp, int32_t p,
   return r;
 }
 
+// wide scheme: three balanced base-64 digits d2, d1, d0 in [-32, 32] of the centered residue
+// and the pair sums d2+d1, d1+d0, d2+d0 (6 s8 planes, 3-way Karatsuba)
+__device__ __forceinline__ void put_limbs4_t6(int8_t *base, int64_t plane_stride, const uint32_t (&x)[4],
+                                              const ModP &m) {
+  int32_t d[6][4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const int32_t c = centered(x[e], m);
+    const int32_t d0 = ((c + 32) & 63) - 32;
+    const int32_t c1 = (c - d0) >> 6;
+    const int32_t d1 = ((c1 + 32) & 63) - 32;
+    const int32_t d2 = (c1 - d1) >> 6;
+    d[0][e] = d2; d[1][e] = d1; d[2][e] = d0;
+    d[3][e] = d2 + d1; d[4][e] = d1 + d0; d[5][e] = d2 + d0;
+  }
+#pragma unroll
+  for (int pl = 0; pl < 6; ++pl)
+    *reinterpret_cast<uint32_t *>(base + pl * plane_stride) =
+        __byte_perm(__byte_perm(d[pl][0], d[pl][1], 0x40), __byte_perm(d[pl][2], d[pl][3], 0x40), 0x5410);
+}
+
 template <int SCHEME>
 __device__ __forceinline__ void put_limbs4(int8_t *base, int64_t plane_stride, const uint32_t (&x)[4],
                                            const ModP &m) {
+  if constexpr (SCHEME == 3) {
+    put_limbs4_t6(base, plane_stride, x, m);
+    return;
+  }
   constexpr int NP = SCHEME == 0 ? 1 : (SCHEME == 1 ? 3 : 2);
   uint32_t w[3];
   limbs4<SCHEME>(x, m, w);
@@ -566,9 +631,22 @@ __device__ __forceinline__ void put_limbs4(int8_t *base, int64_t plane_stride, c
   for (int pl = 0; pl < NP; ++pl) *reinterpret_cast<uint32_t *>(base + pl * plane_stride) = w[pl];
 }
 
-template <int YK>
+template <int YK, bool WIDE = false>
 __device__ __forceinline__ void apply_Y4(const uint32_t (&a)[4], const uint32_t (&b)[4], uint32_t (&oa)[4],
                                          uint32_t (&ob)[4], uint32_t ya, uint32_t yb, const ModP &m) {
+  if constexpr (WIDE) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      if constexpr (YK == 0) {
+        oa[e] = mulmod_w(ya, a[e], m);
+        ob[e] = mulmod_w(ya, b[e], m);
+      } else {
+        oa[e] = submod(mulmod_w(ya, a[e], m), mulmod_w(yb, b[e], m), m);
+        ob[e] = addmod(mulmod_w(yb, a[e], m), mulmod_w(ya, b[e], m), m);
+      }
+    }
+    return;
+  }
   // X Y on the column pair (c, c + kh/2): Y = i I -> (i a, i b);
   // Y = [[ya, yb], [-yb, ya]] (x) I -> [X1 X2] Y = [ya X1 - yb X2, yb X1 + ya X2]
 #pragma unroll
@@ -725,7 +803,7 @@ __device__ __forceinline__ void preadd_row(const PreParams &P, const PreNode &N,
     PUTC(OUT_S3, c3a, c3b)
 #undef PUTC
     if (N.s3 != nullptr && r < P.mh) {
-      uint16_t *d = N.s3 + r * N.s3_ld;
+      uint16_t *d = static_cast<uint16_t *>(N.s3) + r * N.s3_ld;
       uint32_t u[8];
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
@@ -740,8 +818,8 @@ __device__ __forceinline__ void preadd_row(const PreParams &P, const PreNode &N,
   uint32_t da[4], db[4], s1a[4], s1b[4], ta[4], tb[4], s2a[4], s2b[4], s3a[4], s3b[4], s4a[4], s4b[4];
 #pragma unroll
   for (int e = 0; e < 4; ++e) { da[e] = submod(x21a[e], x11a[e], m); db[e] = submod(x21b[e], x11b[e], m); }
-  apply_Y4<YK>(da, db, s1a, s1b, P.ya, P.yb, m);                 // S1 = (A21 - A11) Y
-  apply_Y4<YK>(x21a, x21b, ta, tb, P.ya, P.yb, m);               // A21 Y
+  apply_Y4<YK, SCHEME == 3>(da, db, s1a, s1b, P.ya, P.yb, m);   // S1 = (A21 - A11) Y
+  apply_Y4<YK, SCHEME == 3>(x21a, x21b, ta, tb, P.ya, P.yb, m); // A21 Y
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
     s2a[e] = submod(x22a[e], ta[e], m); s2b[e] = submod(x22b[e], tb[e], m);   // S2 = A22 - A21 Y
@@ -763,8 +841,12 @@ __device__ __forceinline__ void preadd_row(const PreParams &P, const PreNode &N,
   PUT(OUT_X12, x12a, x12b)
   PUT(OUT_S3, s3a, s3b)
 #undef PUT
-  if (N.s3 != nullptr && r < P.mh) {
-    uint16_t *d = N.s3 + r * N.s3_ld;
+  if (N.s3 != nullptr && r < P.mh && P.res32) {
+    uint32_t *d = static_cast<uint32_t *>(N.s3) + r * N.s3_ld;
+    *reinterpret_cast<uint4 *>(d + c) = make_uint4(s3a[0], s3a[1], s3a[2], s3a[3]);
+    *reinterpret_cast<uint4 *>(d + c + h2) = make_uint4(s3b[0], s3b[1], s3b[2], s3b[3]);
+  } else if (N.s3 != nullptr && r < P.mh) {
+    uint16_t *d = static_cast<uint16_t *>(N.s3) + r * N.s3_ld;
     uint2 va, vb;
     va.x = s3a[0] | (s3a[1] << 16); va.y = s3a[2] | (s3a[3] << 16);
     vb.x = s3b[0] | (s3b[1] << 16); vb.y = s3b[2] | (s3b[3] << 16);
@@ -775,7 +857,7 @@ __device__ __forceinline__ void preadd_row(const PreParams &P, const PreNode &N,
 
 template <int SCHEME, int YK>
 __global__ void __launch_bounds__(256) preadd_kernel(const __grid_constant__ PreParams P) {
-  constexpr int NP = SCHEME == 0 ? 1 : (SCHEME == 1 ? 3 : 2);
+  constexpr int NP = SCHEME == 0 ? 1 : (SCHEME == 1 ? 3 : (SCHEME == 2 ? 2 : 6));
   const PreNode &N = P.nodes[blockIdx.z];
   const int64_t g_main = P.kh / 8;               // 4-column groups of the first half
   const int64_t g_pad = (P.kpad - P.kh) / 4;     // zero padding columns [kh, kpad)
@@ -809,7 +891,8 @@ cudaError_t launch_preadd(const PreParams &p, cudaStream_t s) {
 #define PRE(S, Y) preadd_kernel<S, Y><<<grid, block, 0, s>>>(p)
   if (p.scheme == 0) { if (p.ykind == 0) PRE(0, 0); else PRE(0, 1); }
   else if (p.scheme == 1) { if (p.ykind == 0) PRE(1, 0); else PRE(1, 1); }
-  else { if (p.ykind == 0) PRE(2, 0); else PRE(2, 1); }
+  else if (p.scheme == 2) { if (p.ykind == 0) PRE(2, 0); else PRE(2, 1); }
+  else { if (p.ykind == 0) PRE(3, 0); else PRE(3, 1); }
 #undef PRE
   return cudaGetLastError();
 }
@@ -855,7 +938,8 @@ cudaError_t launch_split(const SplitParams &p, cudaStream_t s) {
   dim3 grid((unsigned)((p.kpad / 4 + 255) / 256), (unsigned)(p.rows_pad < 65535 ? p.rows_pad : 65535));
   if (p.scheme == 0) split_kernel<0><<<grid, 256, 0, s>>>(p);
   else if (p.scheme == 1) split_kernel<1><<<grid, 256, 0, s>>>(p);
-  else split_kernel<2><<<grid, 256, 0, s>>>(p);
+  else if (p.scheme == 2) split_kernel<2><<<grid, 256, 0, s>>>(p);
+  else split_kernel<3><<<grid, 256, 0, s>>>(p);
   return cudaGetLastError();
 }
 
@@ -868,7 +952,7 @@ __device__ __forceinline__ void axpby4(const uint32_t *o, int64_t ncols_ok, uint
                                        uint32_t beta, const ModP &m) {
 #pragma unroll
   for (int e = 0; e < 4; ++e)
-    if (e < ncols_ok) v[e] = addmod(mulmod(alpha, v[e], m), mulmod(beta, mod_u32(o[e], m), m), m);
+    if (e < ncols_ok) v[e] = addmod(mulmod_any(alpha, v[e], m), mulmod_any(beta, mod_u32(o[e], m), m), m);
 }
 
 template <typename OutT>
@@ -886,8 +970,12 @@ __device__ __forceinline__ void ld4u16(const uint16_t *p, uint32_t (&v)[4]) {
   uint2 q = *reinterpret_cast<const uint2 *>(p);
   v[0] = q.x & 0xFFFF; v[1] = q.x >> 16; v[2] = q.y & 0xFFFF; v[3] = q.y >> 16;
 }
+__device__ __forceinline__ void ld4u16(const uint32_t *p, uint32_t (&v)[4]) {   // uint32 residues
+  uint4 q = *reinterpret_cast<const uint4 *>(p);
+  v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+}
 
-template <typename OutT>
+template <typename InT, typename OutT>
 __global__ void __launch_bounds__(256) combine_kernel(const __grid_constant__ CombParams P) {
   const CombNode &N = P.nodes[blockIdx.z];
   const int ti = blockIdx.y, tj = blockIdx.x;
@@ -895,7 +983,9 @@ __global__ void __launch_bounds__(256) combine_kernel(const __grid_constant__ Co
   const int64_t mh = P.mh, ldp = P.ldp;            // ldp multiple of 128 -> aligned 8-byte loads
   const int64_t i0 = (int64_t)ti * 64, j0 = (int64_t)tj * 64;
   const ModP &m = P.mod;
-  const uint16_t *P1 = N.P[0], *P2 = N.P[1], *P3 = N.P[2], *P4 = N.P[3], *P5 = N.P[4];
+  const InT *P1 = static_cast<const InT *>(N.P[0]), *P2 = static_cast<const InT *>(N.P[1]);
+  const InT *P3 = static_cast<const InT *>(N.P[2]), *P4 = static_cast<const InT *>(N.P[3]);
+  const InT *P5 = static_cast<const InT *>(N.P[4]);
   __shared__ uint32_t sU[64][65];   // U1 = P1 + P5 on the mirrored tile (tj, ti) (lower part)
   __shared__ uint32_t sQ[64][65];   // P4 on the mirrored tile
   const bool lowtile = ti >= tj, uptile = ti <= tj;
@@ -966,16 +1056,18 @@ cudaError_t launch_combine(const CombParams &p, cudaStream_t s) {
   if (p.n_nodes == 0) return cudaSuccess;
   const unsigned nt = (unsigned)((p.mh + 63) / 64);
   dim3 grid(nt, nt, (unsigned)p.n_nodes), block(16, 16);
-  if (p.out_u32) combine_kernel<uint32_t><<<grid, block, 0, s>>>(p);
-  else combine_kernel<uint16_t><<<grid, block, 0, s>>>(p);
+  if (p.in32) combine_kernel<uint32_t, uint32_t><<<grid, block, 0, s>>>(p);
+  else if (p.out_u32) combine_kernel<uint16_t, uint32_t><<<grid, block, 0, s>>>(p);
+  else combine_kernel<uint16_t, uint16_t><<<grid, block, 0, s>>>(p);
   return cudaGetLastError();
 }
 
 // ============================================================================ K5 2M combine
 // Re = G - eps H - phi(H) with eps = i phi(i) = 1, Im: H phi(i) + i phi(H) = i (H^T - H);
 // G lower (u16, ldg), H full (u16, ldh); C interleaved (re, im) uint32 pairs, Low only.
-__global__ void __launch_bounds__(256) twom_kernel(int64_t m, const uint16_t *G, int64_t ldg,
-                                                   const uint16_t *H, int64_t ldh, uint32_t *C,
+template <typename InT>
+__global__ void __launch_bounds__(256) twom_kernel(int64_t m, const InT *G, int64_t ldg,
+                                                   const InT *H, int64_t ldh, uint32_t *C,
                                                    int64_t ldc, ModP mod, uint32_t alpha, uint32_t beta,
                                                    int axpby) {
   const int ti = blockIdx.y, tj = blockIdx.x;
@@ -995,20 +1087,27 @@ __global__ void __launch_bounds__(256) twom_kernel(int64_t m, const uint16_t *G,
     uint32_t re = submod(submod(G[i * ldg + j], h, mod), ht, mod);
     uint32_t im = submod(ht, h, mod);
     if (axpby) {
-      re = addmod(mulmod(alpha, re, mod), mulmod(beta, mod_u32(C[2 * (i * ldc + j)], mod), mod), mod);
-      im = addmod(mulmod(alpha, im, mod), mulmod(beta, mod_u32(C[2 * (i * ldc + j) + 1], mod), mod), mod);
+      re = addmod(mulmod_any(alpha, re, mod), mulmod_any(beta, mod_u32(C[2 * (i * ldc + j)], mod), mod), mod);
+      im = addmod(mulmod_any(alpha, im, mod), mulmod_any(beta, mod_u32(C[2 * (i * ldc + j) + 1], mod), mod), mod);
     }
     C[2 * (i * ldc + j)] = re;
     C[2 * (i * ldc + j) + 1] = im;
   }
 }
 
-cudaError_t launch_twom(int64_t m, const uint16_t *G, int64_t ldg, const uint16_t *H, int64_t ldh,
+cudaError_t launch_twom(int64_t m, const void *G, int64_t ldg, const void *H, int64_t ldh, int in32,
                         uint32_t *C, int64_t ldc, const ModP &mod, uint32_t alpha, uint32_t beta, int axpby,
                         cudaStream_t s) {
   if (m == 0) return cudaSuccess;
   const unsigned nt = (unsigned)((m + 31) / 32);
-  twom_kernel<<<dim3(nt, nt), dim3(32, 8), 0, s>>>(m, G, ldg, H, ldh, C, ldc, mod, alpha, beta, axpby);
+  if (in32)
+    twom_kernel<uint32_t><<<dim3(nt, nt), dim3(32, 8), 0, s>>>(m, static_cast<const uint32_t *>(G), ldg,
+                                                              static_cast<const uint32_t *>(H), ldh, C, ldc, mod,
+                                                              alpha, beta, axpby);
+  else
+    twom_kernel<uint16_t><<<dim3(nt, nt), dim3(32, 8), 0, s>>>(m, static_cast<const uint16_t *>(G), ldg,
+                                                              static_cast<const uint16_t *>(H), ldh, C, ldc, mod,
+                                                              alpha, beta, axpby);
   return cudaGetLastError();
 }
 
@@ -1042,7 +1141,7 @@ __global__ void scale_lower_kernel(int64_t row0, int w, uint32_t *X, int64_t ldx
   uint32_t *row = X + i * ldx * w;
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < (i + 1) * w;
        j += (int64_t)gridDim.x * blockDim.x)
-    row[j] = mulmod(beta, mod_u32(row[j], mod), mod);
+    row[j] = mulmod_any(beta, mod_u32(row[j], mod), mod);
 }
 
 cudaError_t launch_scale_lower(int64_t m, int w, uint32_t *X, int64_t ldx, uint32_t beta, const ModP &mod,

@@ -11,12 +11,14 @@
 
 namespace adj {
 
-// Barrett constants for an odd prime p < 2^16 (all residues < 2^16, products < 2^32).
+// Barrett constants for an odd prime p < 2^18.  mulmod() needs residue products < 2^32
+// (p <= 65521); mulmod_w() is the 64-bit version for the wide limb scheme.
 struct ModP {
   uint32_t p;
   uint32_t mu;   // floor(2^32 / p)
   uint32_t c32;  // 2^32 mod p
   uint32_t half; // (p - 1) / 2 : centered representative threshold
+  uint64_t mu64; // floor(2^64 / p) (computed as floor((2^64 - 1) / p); p is odd so it is the same)
 };
 
 inline ModP make_modp(uint32_t p) {
@@ -25,6 +27,7 @@ inline ModP make_modp(uint32_t p) {
   m.mu = (uint32_t)((1ull << 32) / p);
   m.c32 = (uint32_t)((1ull << 32) % p);
   m.half = (p - 1) / 2;
+  m.mu64 = ~0ull / p;
   return m;
 }
 
@@ -46,6 +49,21 @@ __host__ __device__ __forceinline__ uint32_t mod_s32(int32_t x, const ModP &m) {
 }
 __host__ __device__ __forceinline__ uint32_t mulmod(uint32_t a, uint32_t b, const ModP &m) {
   return mod_u32(a * b, m);  // a, b < p < 2^16
+}
+// a * b mod p for residues a, b < p < 2^32 (64-bit product, 64-bit Barrett, one correction)
+__host__ __device__ __forceinline__ uint32_t mulmod_w(uint32_t a, uint32_t b, const ModP &m) {
+  const uint64_t x = (uint64_t)a * b;
+#ifdef __CUDA_ARCH__
+  const uint64_t q = __umul64hi(x, m.mu64);
+#else
+  const uint64_t q = (uint64_t)(((unsigned __int128)x * m.mu64) >> 64);
+#endif
+  uint64_t r = x - q * m.p;
+  return (uint32_t)(r >= m.p ? r - m.p : r);
+}
+// mulmod for any supported p (runtime choice; for cold paths)
+__host__ __device__ __forceinline__ uint32_t mulmod_any(uint32_t a, uint32_t b, const ModP &m) {
+  return m.p > 65535u ? mulmod_w(a, b, m) : mulmod(a, b, m);
 }
 __host__ __device__ __forceinline__ uint32_t addmod(uint32_t a, uint32_t b, const ModP &m) {
   uint32_t s = a + b;

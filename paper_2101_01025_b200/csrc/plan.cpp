@@ -19,11 +19,13 @@ static void fill_scheme(Plan &P, uint32_t p) {
   P.bn = 256;
   P.tile_m = P.tile_n = 256;
   P.kseg = (int)std::max<int64_t>(1, limb_kmax(P.scheme, p) / kBK);
+  P.res32 = p > 65535;
   P.mod = make_modp(p);
   P.Y = skew_unitary(p);
   LeafParams &L = P.leaf_template;
   std::memset(&L, 0, sizeof(L));
   L.mod = P.mod;
+  L.fixup32 = p > 65535;
   auto pw = [&](int e) { return (uint32_t)(((uint64_t)1 << e) % p); };
   if (P.scheme == LIMB_S8) {
     L.n_terms = 1;
@@ -41,6 +43,23 @@ static void fill_scheme(Plan &P, uint32_t p) {
     L.weight[0] = (pw(14) + p - pw(7)) % p;
     L.weight[1] = (1 + p - pw(7)) % p;
     L.weight[2] = pw(7);
+  } else if (P.scheme == LIMB_T6) {
+    // x = 2^12 d2 + 2^6 d1 + d0; with P_ij = (d_i + d_j)(e_i + e_j) (3-way Karatsuba):
+    // x y = 2^24 P22 + 2^18 (P21 - P22 - P11) + 2^12 (P20 - P22 - P00 + P11) + 2^6 (P10 - P11 - P00) + P00
+    // planes: 0 d2, 1 d1, 2 d0, 3 d2+d1, 4 d1+d0, 5 d2+d0; accumulator j = plane j x plane j
+    L.n_terms = 6;
+    for (int j = 0; j < 6; ++j) {
+      L.terms[j] = {(int8_t)j, (int8_t)j, (int8_t)j, 1, 1, {0, 0, 0}};
+      L.acc_begin[j] = j;
+    }
+    L.acc_begin[6] = 6;
+    auto neg = [&](uint32_t x) { return (p - x % p) % p; };
+    L.weight[0] = (uint32_t)(((uint64_t)pw(24) + neg(pw(18)) + neg(pw(12))) % p);   // P22
+    L.weight[1] = (uint32_t)(((uint64_t)neg(pw(18)) + pw(12) + neg(pw(6))) % p);    // P11
+    L.weight[2] = (uint32_t)(((uint64_t)neg(pw(12)) + neg(pw(6)) + 1) % p);         // P00
+    L.weight[3] = pw(18);                                                             // P21
+    L.weight[4] = pw(6);                                                              // P10
+    L.weight[5] = pw(12);                                                             // P20
   } else {
     // x y = 2^16 hh + 2^8 (hl + lh) + ll ; hi signed, lo unsigned
     L.n_terms = 4;
@@ -67,7 +86,7 @@ static ProductPlan make_prod(const Plan &P, int arena, int64_t arow, int64_t bro
   pp.lp.b_plane_rows = (int32_t)b_pr;
   pp.lp.kblocks = (int32_t)(kpad / kBK);
   pp.lp.sym = sym ? 1 : 0;
-  pp.lp.out_u32 = out_u32 ? 1 : 0;
+  pp.lp.out_u32 = (out_u32 || P.res32) ? 1 : 0;   // workspace residues are uint32 for p > 2^16
   pp.lp.out_rows = (int32_t)out_rows;
   pp.lp.out_cols = (int32_t)out_cols;
   pp.lp.vec_ok = 1;
@@ -138,7 +157,7 @@ static void split_tail(Plan &P, int ncl) {
 static void set_grid(Plan &P, int num_sms) {
   split_tail(P, num_sms / 2);
   P.fixup_offset = P.ws_bytes;
-  P.ws_bytes += (size_t)P.n_pieces * 256 * 256 * 2;
+  P.ws_bytes += (size_t)P.n_pieces * 256 * 256 * P.res_bytes();
   const int64_t nt = std::max<int64_t>(1, (int64_t)P.tiles.size() / 2);
   P.grid = 2 * (int)std::min<int64_t>(num_sms / 2, nt);   // CTA pairs
   P.segmented = false;
@@ -217,17 +236,17 @@ bool build_syrk_plan(Plan &P, int64_t m, int64_t k, uint32_t p, int phi, int dep
   if ((int)P.arenas.size() > kMaxMaps) { *err = "too many operand arenas"; return false; }
   for (int l = 1; l < depth; ++l) {
     LevelPlan &L = P.lv[l];
-    L.s3_node_bytes = (size_t)rup(L.mh * L.kh * 2, 256);
+    L.s3_node_bytes = (size_t)rup(L.mh * L.kh * P.res_bytes(), 256);
     L.s3_offset = alloc(L.s3_node_bytes * L.n_nodes);
   }
   for (int l = 1; l <= depth; ++l) {
     LevelPlan &L = P.lv[l];
-    L.p_buf_bytes = (size_t)rup(L.rows_pad * L.rows_pad * 2, 256);
+    L.p_buf_bytes = (size_t)rup(L.rows_pad * L.rows_pad * P.res_bytes(), 256);
     L.p_offset = alloc(L.p_buf_bytes * 5 * L.n_nodes);
   }
   if (P.kind == PLAN_SYRK_H) {
-    P.h_offset = alloc((size_t)P.rows_pad0 * P.rows_pad0 * 2);
-    P.g_offset = alloc((size_t)P.rows_pad0 * P.rows_pad0 * 2);
+    P.h_offset = alloc((size_t)P.rows_pad0 * P.rows_pad0 * P.res_bytes());
+    P.g_offset = alloc((size_t)P.rows_pad0 * P.rows_pad0 * P.res_bytes());
   }
   P.ws_bytes = off;
 

@@ -49,6 +49,8 @@ struct Plan {
   int tile_m = 256, tile_n = 256;  // CTA-pair output tile (leaf2_kernel)
   int kseg = 1;                    // k-blocks per int32 accumulation segment (limb k_max / 128)
   bool segmented = false;          // some leaf product needs more than one K segment
+  bool res32 = false;              // workspace residues (P, S3, G, H, fixup) are uint32 (p > 2^16)
+  int res_bytes() const { return res32 ? 4 : 2; }
   ModP mod;
   SkewY Y;
   std::vector<ArenaPlan> arenas;

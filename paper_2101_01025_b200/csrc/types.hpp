@@ -46,11 +46,12 @@ struct LeafParams {
   //       tile whose residue partial goes to fixup slot piece-1 (summed by the fixup kernel)
   const uint2 *tiles;
   int32_t n_tiles;
-  uint16_t *fixup;         // 256 x 256 u16 residue partials, one slot per tail piece
+  void *fixup;             // 256 x 256 residue partials (u16, or u32 if fixup32), one slot per tail piece
   int32_t n_terms;
-  int32_t acc_begin[4];    // terms [acc_begin[j], acc_begin[j+1]) accumulate into accumulator j
-  LeafTerm terms[4];
-  uint32_t weight[3];      // residue weight of each accumulator in the limb recombination
+  int32_t acc_begin[8];    // terms [acc_begin[j], acc_begin[j+1]) accumulate into accumulator j
+  LeafTerm terms[8];
+  uint32_t weight[6];      // residue weight of each accumulator in the limb recombination
+  int32_t fixup32;         // fixup slots hold uint32 residues (p > 2^16) instead of uint16
   int32_t debug;           // diagnostics only (ADJ_LEAF_DEBUG): 1 no TMA, 2 no epilogue, 8 no math, 16 no tcgen05.ld, 32 no stores
   ModP mod;
 };
@@ -77,7 +78,7 @@ enum PreOut : int { OUT_S1 = 0, OUT_S2, OUT_S4, OUT_X22, OUT_X11, OUT_X12, OUT_S
 struct PreNode {
   InView in;
   int64_t op_row[OUT_N];   // arena row of plane 0 for each output operand; -1 = not produced
-  uint16_t *s3;            // materialised S3 residues (when S3 recurses), else null
+  void *s3;                // materialised S3 residues (when S3 recurses), else null (u16 / u32 if res32)
   int64_t s3_ld;
   // 2M side output (root node, IN_PAIR_SUM input): limb planes of X = Re(A) and Y = Im(A) for
   // the general product H = X Y^T, written from the same read of A as the pre-addition of T.
@@ -95,6 +96,8 @@ struct PreParams {
   int64_t rows_pad;        // rows per plane in the arena (>= mh, multiple of 128)
   int64_t kpad;            // arena row length in bytes (>= kh, multiple of 128)
   int8_t *arena;
+  int32_t res32;           // workspace residues are uint32 (p > 2^16)
+  int32_t pad_;
   ModP mod;
 };
 
@@ -113,7 +116,7 @@ struct SplitParams {
 
 // ---------------------------------------------------------------- K4 recombination
 struct CombNode {
-  const uint16_t *P[5];    // P1..P5 (index 0..4), each rows_pad x rows_pad, ld = ldp
+  const void *P[5];        // P1..P5 (index 0..4), each rows_pad x rows_pad, ld = ldp (u16, or u32 if in32)
   void *out;
   int64_t ldo;
   int64_t out_valid;       // output is out_valid x out_valid (<= 2 mh); only Low written
@@ -126,7 +129,8 @@ struct CombParams {
   int64_t mh, ldp;
   ModP mod;
   uint32_t alpha, beta;    // axpby on the final (uint32) output, SYRK form
-  int32_t axpby, pad_;
+  int32_t axpby;
+  int32_t in32;            // P buffers hold uint32 residues (p > 2^16)
 };
 
 }  // namespace adj

@@ -34,7 +34,8 @@ def test_status_strings():
         assert L.adj_status_string(code).decode() == name
 
 
-@pytest.mark.parametrize("p", [3, 5, 7, 13, 97, 251, 257, 8191, 16763, 16787, 65521])
+@pytest.mark.parametrize("p", [3, 5, 7, 13, 97, 251, 257, 8191, 16763, 16787, 65521, 65537, 131041, 131071,
+                               262139])
 def test_skew_unitary_matches_paper_construction(p):
     """Host constants of the CUDA path vs the oracle's independent field code; Y phi(Y) = -I."""
     kind, a, b = adj.adj_skew_unitary(p)
@@ -59,7 +60,7 @@ def test_validation_is_synchronous_and_needs_no_gpu():
         adj.adjprod_modp(4, 4, 91, 0, 1, 4, 2, 4, stream=0)             # 91 = 7 * 13 not prime
     assert e.value.status == 2
     with pytest.raises(adj.AdjError) as e:
-        adj.adjprod_modp(4, 4, 65537, 0, 1, 4, 2, 4, stream=0)          # > 65521
+        adj.adjprod_modp(4, 4, 262147, 0, 1, 4, 2, 4, stream=0)         # > 262139 = largest prime < 2^18
     assert e.value.status == 2
     with pytest.raises(adj.AdjError) as e:
         adj.adjprod_modp(4, 4, 97, 1, 1, 4, 2, 4, stream=0)             # phi = H needs p = 3 mod 4

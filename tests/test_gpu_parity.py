@@ -10,6 +10,9 @@ from gpu_util import low, to_dev, to_host
 pytestmark = pytest.mark.gpu
 
 PRIMES = [3, 97, 251, 257, 8191, 16741, 16763, 16787, 65521]
+# p > 2^16: three balanced base-64 digits + pair sums, 3-way Karatsuba; the
+# paper's own moduli 131071 and 131041 and the largest supported prime
+WIDE_PRIMES = [65537, 131041, 131071, 262139]
 
 
 @pytest.fixture(scope="module")
@@ -31,7 +34,7 @@ def test_input_generator_gpu_matches_cpu(adj):
         assert np.array_equal(to_host(t), uniform_residues(1 << 20, seed, p))
 
 
-@pytest.mark.parametrize("p", PRIMES)
+@pytest.mark.parametrize("p", PRIMES + WIDE_PRIMES)
 def test_limb_split_exhaustive_all_residues(adj, p):
     """Every residue x of GF(p) through split -> int8 MMA -> recombine: x * c for several c,
     including the limb extremes (SURVEY.md §8(c) pin 1)."""
@@ -42,7 +45,7 @@ def test_limb_split_exhaustive_all_residues(adj, p):
     assert np.array_equal(to_host(C), ref.astype(np.uint32))
 
 
-@pytest.mark.parametrize("p", PRIMES)
+@pytest.mark.parametrize("p", PRIMES + WIDE_PRIMES)
 @pytest.mark.parametrize("m,n,k", [(1, 1, 1), (128, 128, 128), (200, 300, 257), (130, 129, 1000), (256, 512, 64)])
 def test_gemm_vs_oracle(adj, p, m, n, k):
     A = uniform_matrix(m, k, seed=m + k, p=p)
@@ -61,10 +64,19 @@ def test_adjprod_T_vs_oracle(adj, p, depth, m, k):
     assert np.array_equal(got, oracle.syrk_t(A, p)), (p, depth, m, k)
 
 
+@pytest.mark.parametrize("p", WIDE_PRIMES)
+@pytest.mark.parametrize("depth", [0, 1, 2, 3])
+@pytest.mark.parametrize("m,k", [(1, 5), (129, 200), (513, 1100)])
+def test_adjprod_T_wide_vs_oracle(adj, p, depth, m, k):
+    A = uniform_matrix(m, k, seed=11 * m + k + depth, p=p)
+    got = to_host(adj.adjprod(to_dev(A), p, depth=depth))
+    assert np.array_equal(got, oracle.syrk_t(A, p)), (p, depth, m, k)
+
+
+@pytest.mark.parametrize("p", [8191, 131071])
 @pytest.mark.parametrize("depth", [0, 1, 2])
 @pytest.mark.parametrize("m,k", [(1, 1), (33, 17), (260, 300), (700, 513)])
-def test_adjprod_H_vs_oracle(adj, depth, m, k):
-    p = 8191
+def test_adjprod_H_vs_oracle(adj, p, depth, m, k):
     A = uniform_matrix_ext(m, k, seed=m * 31 + k, p=p)
     C = adj.adjprod(to_dev(A), p, phi="H", depth=depth)
     assert np.array_equal(to_host(C), oracle.syrk_h(A, p))
@@ -117,6 +129,9 @@ def test_k_zero_and_m_zero(adj):
     (8191, 8191 - 4032, 65536, 0),      # mid extreme
     (97, 48, 4096, 0),
     (65521, 65521 - 32513, 32768, 1),
+    (262139, 262139 - 131069, 32768, 0),   # wide scheme: c = -(p-1)/2
+    (131071, 131071 - 2080, 524288, 0),    # c = -2080: digits (0, -32, -32), d1 + d0 = -64: every
+                                           # product 4096, k past the 2^31 / 4096 bound (2 segments)
 ])
 def test_overflow_stress_constant(adj, p, c, k, depth):
     """Constant A = c: C = k c^2 mod p everywhere (SURVEY.md §8(c) pin 4, overflow stress)."""
@@ -166,7 +181,8 @@ def test_errors_on_device(adj):
     assert e.value.status == 3
 
 
-@pytest.mark.parametrize("p,k,m", [(65521, 40000, 300), (65521, 70000, 130), (97, 140000, 64), (8191, 240000, 64)])
+@pytest.mark.parametrize("p,k,m", [(65521, 40000, 300), (65521, 70000, 130), (97, 140000, 64), (8191, 240000, 64),
+                                   (131071, 600000, 40)])
 def test_k_segmentation_beyond_int32_bound(adj, p, k, m):
     """Inner dimension above the limb scheme's int32 bound: the leaf splits K
     into segments, each reduced mod p and summed (depth 0 and gemm_modp)."""
@@ -186,13 +202,13 @@ def test_k_segmentation_overflow_stress(adj):
     assert (got[np.tril_indices(256)] == k * c * c % p).all()
 
 
+@pytest.mark.parametrize("p", [8191, 131071])
 @pytest.mark.parametrize("phi", ["T", "H"])
 @pytest.mark.parametrize("depth", [0, 1, 2])
 @pytest.mark.parametrize("alpha,beta", [(1, 0), (0, 1), (3, 5), (8190, 8190), (12345, 0), (1, 1)])
-def test_syrk_form_alpha_beta(adj, phi, depth, alpha, beta):
+def test_syrk_form_alpha_beta(adj, p, phi, depth, alpha, beta):
     """Low(C) <- alpha Low(A phi(A)) + beta Low(C), fused into the final writes."""
     import torch
-    p = 8191
     m, k = 300, 260
     A = uniform_matrix(m, k, seed=5, p=p) if phi == "T" else uniform_matrix_ext(m, k, seed=5, p=p)
     rng = np.random.default_rng(depth * 31 + alpha)
