@@ -48,7 +48,7 @@ __device__ __forceinline__ void store_chunk(const LeafProduct &pr, int64_t row, 
   if (pr.out_u32) {
     uint32_t *o = reinterpret_cast<uint32_t *>(pr.out) + row * pr.ldo + col;
     if (pr.axpby) {   // SYRK form: out <- alpha v + beta out_old (scalar path, final output only)
-#pragma unroll 4
+#pragma unroll
       for (int e = 0; e < 32; ++e)
         if (col + e < pr.out_cols && (!pr.sym || col + e <= row))
           o[e] = addmod(mulmod_any(pr.alpha, r[e], m), mulmod_any(pr.beta, mod_u32(o[e], m), m), m);
@@ -205,10 +205,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (ADJ_EPI_WARPS 
               if (skip_tma) {
                 if (leader) ptx::mbar_arrive(&full_bar[stage]);
               } else {
-                if (leader) ptx::mbar_expect_tx(&full_bar[stage], 2 * Cfg::STAGE_BYTES);
+                const bool skip_b = (P.debug & 256) != 0;   // diagnostics: A operand only (L2-bound test)
+                if (leader) ptx::mbar_expect_tx(&full_bar[stage], skip_b ? 2 * Cfg::A_BYTES : 2 * Cfg::STAGE_BYTES);
                 uint8_t *sa = smem + stage * Cfg::STAGE_BYTES;
                 ptx::tma_load_2d_2sm(sa, map, kb * kBK, tt ? ar1 : ar0, &full_bar[stage]);
-                ptx::tma_load_2d_2sm(sa + Cfg::A_BYTES, map, kb * kBK, tt ? br1 : br0, &full_bar[stage]);
+                if (!skip_b) ptx::tma_load_2d_2sm(sa + Cfg::A_BYTES, map, kb * kBK, tt ? br1 : br0, &full_bar[stage]);
               }
               if (prof) t_tma += clock64() - c1;
               if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
@@ -318,7 +319,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (ADJ_EPI_WARPS 
         const uint32_t slot = unit & 1, use = unit >> 1;
         ptx::mbar_wait(&slot_full[slot], use & 1);
         ptx::tc_fence_after();
-        const uint32_t w = P.weight[j];
 #pragma unroll 1
         for (int c = 0; c < nchunks; ++c) {
           uint32_t v[32];
@@ -333,39 +333,41 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (ADJ_EPI_WARPS 
             if (v[0] == 0xFFFFFFFFu && v[31] == 0x12345u) prow0[0] = v[1];   // keep the loads alive
             continue;
           }
-#pragma unroll
-          for (int e = 0; e < 32; ++e) v[e] = mod_s32((int32_t)v[e], mod);
-          if (NACC > 1 || w != 1) {
-#pragma unroll
-            for (int e = 0; e < 32; ++e) v[e] = WIDE ? mulmod_w(v[e], w, mod) : mulmod(v[e], w, mod);
-          }
+          // (partial + acc_j * weight_j) mod p per element, Shoup-fused (modp.cuh: acc_mulred)
+          const int32_t wc = P.wshoup[j].wc, wq = P.wshoup[j].wq;
+          const uint32_t pm = mod.p;
           if constexpr (PART && !WIDE) {
             uint32_t *pc = prow0 + h0 * 64 + c * 16;
             if (u > 0) {
 #pragma unroll
               for (int e = 0; e < 16; ++e) {
                 const uint32_t wd = pc[e];
-                v[2 * e] = addmod(v[2 * e], wd & 0xFFFF, mod);
-                v[2 * e + 1] = addmod(v[2 * e + 1], wd >> 16, mod);
+                v[2 * e] = acc_mulred((int32_t)v[2 * e], wc, wq, wd & 0xFFFF, pm);
+                v[2 * e + 1] = acc_mulred((int32_t)v[2 * e + 1], wc, wq, wd >> 16, pm);
               }
+            } else {
+#pragma unroll
+              for (int e = 0; e < 32; ++e) v[e] = acc_mulred((int32_t)v[e], wc, wq, 0u, pm);
             }
             if (u < nunits - 1) {
 #pragma unroll
               for (int e = 0; e < 16; ++e) pc[e] = v[2 * e] | (v[2 * e + 1] << 16);
               continue;
             }
-          }
-          if constexpr (PART && WIDE) {
+          } else if constexpr (PART && WIDE) {
             uint32_t *pc = prow0 + h0 * 96 + c * 24;     // 32 residues of 24 bits = 24 words
             if (u > 0) {
 #pragma unroll
               for (int g = 0; g < 8; ++g) {
                 const uint32_t w0 = pc[3 * g], w1 = pc[3 * g + 1], w2 = pc[3 * g + 2];
-                v[4 * g] = addmod(v[4 * g], w0 & 0xFFFFFF, mod);
-                v[4 * g + 1] = addmod(v[4 * g + 1], (w0 >> 24) | ((w1 & 0xFFFF) << 8), mod);
-                v[4 * g + 2] = addmod(v[4 * g + 2], (w1 >> 16) | ((w2 & 0xFF) << 16), mod);
-                v[4 * g + 3] = addmod(v[4 * g + 3], w2 >> 8, mod);
+                v[4 * g] = acc_mulred((int32_t)v[4 * g], wc, wq, w0 & 0xFFFFFF, pm);
+                v[4 * g + 1] = acc_mulred((int32_t)v[4 * g + 1], wc, wq, (w0 >> 24) | ((w1 & 0xFFFF) << 8), pm);
+                v[4 * g + 2] = acc_mulred((int32_t)v[4 * g + 2], wc, wq, (w1 >> 16) | ((w2 & 0xFF) << 16), pm);
+                v[4 * g + 3] = acc_mulred((int32_t)v[4 * g + 3], wc, wq, w2 >> 8, pm);
               }
+            } else {
+#pragma unroll
+              for (int e = 0; e < 32; ++e) v[e] = acc_mulred((int32_t)v[e], wc, wq, 0u, pm);
             }
             if (u < nunits - 1) {
 #pragma unroll
@@ -376,6 +378,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (ADJ_EPI_WARPS 
               }
               continue;
             }
+          } else {
+#pragma unroll
+            for (int e = 0; e < 32; ++e) v[e] = acc_mulred((int32_t)v[e], wc, wq, 0u, pm);
           }
           if (fx32) {
             uint4 *d = reinterpret_cast<uint4 *>(fx32 + c * 32);

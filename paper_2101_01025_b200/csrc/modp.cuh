@@ -77,6 +77,38 @@ __host__ __device__ __forceinline__ int32_t centered(uint32_t x, const ModP &m) 
   return x > m.half ? (int32_t)x - (int32_t)m.p : (int32_t)x;
 }
 
+// Shoup multiplication by a fixed weight, fused with the accumulation into a residue partial.
+// The weight is kept centered, wc in [-(p-1)/2, (p-1)/2], with wq = floor(wc * 2^32 / p) (floor
+// toward -inf), so |wq| < 2^31.  For any int32 x: q = mulhi_s32(x, wq) is within 1 of
+// floor(x wc / p) (|x (wc 2^32/p - wq)| / 2^32 < 1/2), so r = x wc - q p lies in [-p, 2p) and is
+// computed exactly in wrapping 32-bit arithmetic.  acc_mulred returns (part + x w) mod p for a
+// residue part < p: s = part + r + p in [0, 4p) (needs 4p < 2^32), then two unsigned min-subtracts.
+struct ShoupW {
+  int32_t wc, wq;
+};
+inline ShoupW make_shoup(uint32_t w, uint32_t p) {
+  ShoupW s;
+  w %= p;
+  s.wc = w > (p - 1) / 2 ? (int32_t)w - (int32_t)p : (int32_t)w;
+  const int64_t num = (int64_t)s.wc * ((int64_t)1 << 32);
+  int64_t q = num / (int64_t)p;
+  if (num % (int64_t)p != 0 && num < 0) --q;   // floor
+  s.wq = (int32_t)q;
+  return s;
+}
+__host__ __device__ __forceinline__ uint32_t umin32(uint32_t a, uint32_t b) { return a < b ? a : b; }
+__host__ __device__ __forceinline__ uint32_t acc_mulred(int32_t x, int32_t wc, int32_t wq, uint32_t part, uint32_t p) {
+#ifdef __CUDA_ARCH__
+  const int32_t q = __mulhi(x, wq);
+#else
+  const int32_t q = (int32_t)(((int64_t)x * (int64_t)wq) >> 32);
+#endif
+  const uint32_t r = (uint32_t)x * (uint32_t)wc - (uint32_t)q * p;
+  uint32_t s = part + r + p;
+  s = umin32(s, s - 2 * p);
+  return umin32(s, s - p);
+}
+
 // int8 limb split of a canonical residue:
 //   scheme 0 (p <= 255)    : l0 = c                                    (s8)
 //   scheme 1 (p <= 16763)  : hi = floor((c+64)/128), lo = c - 128 hi, mid = hi + lo  (all s8)

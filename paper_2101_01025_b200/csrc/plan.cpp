@@ -72,6 +72,7 @@ static void fill_scheme(Plan &P, uint32_t p) {
     L.weight[1] = 1 % p;
     L.weight[2] = pw(8);
   }
+  for (int j = 0; j < 6; ++j) L.wshoup[j] = make_shoup(L.weight[j], p);
 }
 
 static ProductPlan make_prod(const Plan &P, int arena, int64_t arow, int64_t brow, int64_t a_pr, int64_t b_pr, int64_t kpad,
