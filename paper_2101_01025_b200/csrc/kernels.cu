@@ -949,110 +949,140 @@ cudaError_t launch_split(const SplitParams &p, cudaStream_t s) {
 }
 
 // ============================================================================ K4 recombination
-// 64 x 64 tiles of the (mh x mh) product grid; thread (tx, ty) owns 4 consecutive columns of
-// rows ty, ty+16, ty+32, ty+48 (8-byte u16 loads).  The mirrored tile (tj, ti) is staged
-// through shared memory for Up(U1) = Low(U1)^T and P4^T.
+// One block per lower pair {L = (ti, tj), U = (tj, ti)}, ti >= tj, of 64 x 64 tiles of the
+// (mh x mh) product grid, so that every product tile is read once:
+//   L: U1 = P1 + P5, C21 = U1 + P4 + P3, C22 = Low(U1 + P4 + P4^T), C11 = Low(P1 + P2)
+//   U (ti > tj): C21 = Up(U1) + P4 + P3 with Up(U1) = Low(U1)^T
+// P4(U) and U1(L) are staged in shared memory for the two transposed uses.  Thread (tx, ty) of
+// 8 x 32 owns 8 consecutive columns (16-byte u16 loads) of rows ty and ty + 32.
 // SYRK form on the final output: v <- alpha v + beta old (mod p)
-__device__ __forceinline__ void axpby4(const uint32_t *o, int64_t ncols_ok, uint32_t (&v)[4], uint32_t alpha,
-                                       uint32_t beta, const ModP &m) {
-#pragma unroll
-  for (int e = 0; e < 4; ++e)
+__device__ __forceinline__ void axpby_n(const uint32_t *o, int64_t ncols_ok, uint32_t *v, int n, uint32_t alpha,
+                                        uint32_t beta, const ModP &m) {
+  for (int e = 0; e < n; ++e)
     if (e < ncols_ok) v[e] = addmod(mulmod_any(alpha, v[e], m), mulmod_any(beta, mod_u32(o[e], m), m), m);
 }
 
 template <typename OutT>
-__device__ __forceinline__ void store4(OutT *o, bool vec, int64_t ncols_ok, const uint32_t (&v)[4]) {
-  if (vec && ncols_ok >= 4 && (reinterpret_cast<uintptr_t>(o) % (4 * sizeof(OutT)) == 0)) {
-    if constexpr (sizeof(OutT) == 4) *reinterpret_cast<uint4 *>(o) = make_uint4(v[0], v[1], v[2], v[3]);
-    else *reinterpret_cast<uint2 *>(o) = make_uint2(v[0] | (v[1] << 16), v[2] | (v[3] << 16));
+__device__ __forceinline__ void store8(OutT *o, int64_t ncols_ok, const uint32_t (&v)[8]) {
+  if (ncols_ok >= 8 && (reinterpret_cast<uintptr_t>(o) % (8 * sizeof(OutT)) == 0)) {
+    if constexpr (sizeof(OutT) == 4) {
+      reinterpret_cast<uint4 *>(o)[0] = make_uint4(v[0], v[1], v[2], v[3]);
+      reinterpret_cast<uint4 *>(o)[1] = make_uint4(v[4], v[5], v[6], v[7]);
+    } else {
+      *reinterpret_cast<uint4 *>(o) = make_uint4(v[0] | (v[1] << 16), v[2] | (v[3] << 16), v[4] | (v[5] << 16),
+                                                 v[6] | (v[7] << 16));
+    }
   } else {
 #pragma unroll
-    for (int e = 0; e < 4; ++e) if (e < ncols_ok) o[e] = (OutT)v[e];
+    for (int e = 0; e < 8; ++e) if (e < ncols_ok) o[e] = (OutT)v[e];
   }
 }
 
-__device__ __forceinline__ void ld4u16(const uint16_t *p, uint32_t (&v)[4]) {
-  uint2 q = *reinterpret_cast<const uint2 *>(p);
+__device__ __forceinline__ void ld8(const uint16_t *p, uint32_t (&v)[8]) {
+  const uint4 q = *reinterpret_cast<const uint4 *>(p);
   v[0] = q.x & 0xFFFF; v[1] = q.x >> 16; v[2] = q.y & 0xFFFF; v[3] = q.y >> 16;
+  v[4] = q.z & 0xFFFF; v[5] = q.z >> 16; v[6] = q.w & 0xFFFF; v[7] = q.w >> 16;
 }
-__device__ __forceinline__ void ld4u16(const uint32_t *p, uint32_t (&v)[4]) {   // uint32 residues
-  uint4 q = *reinterpret_cast<const uint4 *>(p);
-  v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+__device__ __forceinline__ void ld8(const uint32_t *p, uint32_t (&v)[8]) {   // uint32 residues
+  const uint4 q0 = reinterpret_cast<const uint4 *>(p)[0], q1 = reinterpret_cast<const uint4 *>(p)[1];
+  v[0] = q0.x; v[1] = q0.y; v[2] = q0.z; v[3] = q0.w; v[4] = q1.x; v[5] = q1.y; v[6] = q1.z; v[7] = q1.w;
 }
 
 template <typename InT, typename OutT>
 __global__ void __launch_bounds__(256) combine_kernel(const __grid_constant__ CombParams P) {
-  const CombNode &N = P.nodes[blockIdx.z];
-  const int ti = blockIdx.y, tj = blockIdx.x;
-  const int tx = threadIdx.x, ty = threadIdx.y;   // 16 x 16
-  const int64_t mh = P.mh, ldp = P.ldp;            // ldp multiple of 128 -> aligned 8-byte loads
+  const CombNode &N = P.nodes[blockIdx.y];
+  // lower pair index -> (ti, tj), ti >= tj
+  const int x = (int)blockIdx.x;
+  int ti = (int)((sqrtf(8.0f * (float)x + 1.0f) - 1.0f) * 0.5f);
+  while ((ti + 1) * (ti + 2) / 2 <= x) ++ti;
+  while (ti * (ti + 1) / 2 > x) --ti;
+  const int tj = x - ti * (ti + 1) / 2;
+  const bool diag = ti == tj;
+  const int tx = threadIdx.x & 7, ty = threadIdx.x >> 3;   // 8 x 32
+  const int64_t mh = P.mh, ldp = P.ldp;                     // ldp multiple of 128 -> aligned 16-byte loads
   const int64_t i0 = (int64_t)ti * 64, j0 = (int64_t)tj * 64;
   const ModP &m = P.mod;
   const InT *P1 = static_cast<const InT *>(N.P[0]), *P2 = static_cast<const InT *>(N.P[1]);
   const InT *P3 = static_cast<const InT *>(N.P[2]), *P4 = static_cast<const InT *>(N.P[3]);
   const InT *P5 = static_cast<const InT *>(N.P[4]);
-  __shared__ uint32_t sU[64][65];   // U1 = P1 + P5 on the mirrored tile (tj, ti) (lower part)
-  __shared__ uint32_t sQ[64][65];   // P4 on the mirrored tile
-  const bool lowtile = ti >= tj, uptile = ti <= tj;
-  const int cx = tx * 4;
+  __shared__ uint32_t sU[64][65];   // U1 on L (Low part; on a diagonal tile the full tile is filled)
+  __shared__ uint32_t sQ[64][65];   // P4 on U (rows j0.., cols i0..)
+  const int cx = tx * 8;
+  uint32_t u1[2][8], q4u[2][8];
 #pragma unroll
-  for (int rr = 0; rr < 4; ++rr) {
-    const int y = ty + 16 * rr;
-    const int64_t gi = j0 + y, gj = i0 + cx;      // buffers are rows_pad x rows_pad: always in range
-    uint32_t a[4], b[4];
-    if (uptile) {
-      ld4u16(P1 + gi * ldp + gj, a);
-      ld4u16(P5 + gi * ldp + gj, b);
+  for (int rr = 0; rr < 2; ++rr) {
+    const int y = ty + 32 * rr;
+    const int64_t i = i0 + y, j = j0 + cx;     // buffers are rows_pad x rows_pad: always in range
+    uint32_t a[8], b[8];
+    ld8(P1 + i * ldp + j, a);
+    ld8(P5 + i * ldp + j, b);
 #pragma unroll
-      for (int e = 0; e < 4; ++e) sU[y][cx + e] = addmod(a[e], b[e], m);
-    }
-    if (lowtile) {
-      ld4u16(P4 + gi * ldp + gj, a);
+    for (int e = 0; e < 8; ++e) { u1[rr][e] = addmod(a[e], b[e], m); sU[y][cx + e] = u1[rr][e]; }
+    ld8(P4 + (j0 + y) * ldp + i0 + cx, q4u[rr]);
 #pragma unroll
-      for (int e = 0; e < 4; ++e) sQ[y][cx + e] = a[e];
-    }
+    for (int e = 0; e < 8; ++e) sQ[y][cx + e] = q4u[rr][e];
   }
   __syncthreads();
   OutT *O = static_cast<OutT *>(N.out);
   const int64_t ov = N.out_valid;
-  const bool vec = true;   // store4 checks the alignment of every vector store
+  const bool ax = sizeof(OutT) == 4 && P.axpby;
+  // ---- tile L (and, on the diagonal, its upper part of C21)
 #pragma unroll
-  for (int rr = 0; rr < 4; ++rr) {
-    const int y = ty + 16 * rr;
+  for (int rr = 0; rr < 2; ++rr) {
+    const int y = ty + 32 * rr;
     const int64_t i = i0 + y, j = j0 + cx;
     if (i >= mh || j >= mh) continue;
-    uint32_t p1[4], p5[4], p4[4], p3[4], u1[4], c21[4];
-    ld4u16(P4 + i * ldp + j, p4);
-    ld4u16(P3 + i * ldp + j, p3);
-    const bool any_low = j <= i;                   // some of the 4 columns are on/below the diagonal
-    if (any_low) { ld4u16(P1 + i * ldp + j, p1); ld4u16(P5 + i * ldp + j, p5); }
+    uint32_t p4[8], p3[8], c21[8];
+    ld8(P4 + i * ldp + j, p4);
+    ld8(P3 + i * ldp + j, p3);
+    uint32_t u[8];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      if (j + e <= i) u1[e] = addmod(p1[e], p5[e], m);     // Low(U1) = Low(P1) + Low(P5)
-      else u1[e] = sU[cx + e][y];                          // Up(U1) = Low(U1)^T
-      c21[e] = addmod(addmod(u1[e], p4[e], m), p3[e], m);  // U4 = U1 + P4 + P3
+    for (int e = 0; e < 8; ++e) {
+      u[e] = (j + e <= i) ? u1[rr][e] : sU[cx + e][y];       // Up(U1) = Low(U1)^T (diagonal tile)
+      c21[e] = addmod(addmod(u[e], p4[e], m), p3[e], m);      // U4 = U1 + P4 + P3
     }
-    const int64_t n21 = min64(4, min64(mh - j, ov - j));
-    if (sizeof(OutT) == 4 && P.axpby && mh + i < ov)
-      axpby4(reinterpret_cast<const uint32_t *>(O + (mh + i) * N.ldo + j), n21, c21, P.alpha, P.beta, m);
-    if (mh + i < ov) store4<OutT>(O + (mh + i) * N.ldo + j, vec, n21, c21);                         // C21
-    if (any_low) {
-      uint32_t p2[4], c22[4], c11[4];
-      ld4u16(P2 + i * ldp + j, p2);
+    const int64_t n21 = min64(8, min64(mh - j, ov - j));
+    if (mh + i < ov) {
+      if (ax) axpby_n(reinterpret_cast<const uint32_t *>(O + (mh + i) * N.ldo + j), n21, c21, 8, P.alpha, P.beta, m);
+      store8<OutT>(O + (mh + i) * N.ldo + j, n21, c21);                                      // C21
+    }
+    if (j <= i) {
+      uint32_t p1[8], p2[8], c22[8], c11[8];
+      ld8(P1 + i * ldp + j, p1);
+      ld8(P2 + i * ldp + j, p2);
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        c22[e] = addmod(addmod(u1[e], p4[e], m), sQ[cx + e][y], m);   // U5 = Low(U2) + Low(P4^T)
-        c11[e] = addmod(p1[e], p2[e], m);                              // U3 = P1 + P2
+      for (int e = 0; e < 8; ++e) {
+        c22[e] = addmod(addmod(u[e], p4[e], m), sQ[cx + e][y], m);   // U5 = U2 + P4^T
+        c11[e] = addmod(p1[e], p2[e], m);                                                   // U3 = P1 + P2
       }
-      const int64_t nlow = min64(4, i - j + 1);           // columns j..i only
-      if (sizeof(OutT) == 4 && P.axpby) {
-        if (mh + i < ov)
-          axpby4(reinterpret_cast<const uint32_t *>(O + (mh + i) * N.ldo + mh + j), min64(nlow, ov - mh - j), c22,
-                 P.alpha, P.beta, m);
-        if (i < ov) axpby4(reinterpret_cast<const uint32_t *>(O + i * N.ldo + j), min64(nlow, ov - j), c11, P.alpha, P.beta, m);
+      const int64_t nlow = min64(8, i - j + 1);           // columns j..i only
+      if (mh + i < ov) {
+        const int64_t n = min64(nlow, ov - mh - j);
+        if (ax) axpby_n(reinterpret_cast<const uint32_t *>(O + (mh + i) * N.ldo + mh + j), n, c22, 8, P.alpha, P.beta, m);
+        store8<OutT>(O + (mh + i) * N.ldo + mh + j, n, c22);                                // C22
       }
-      if (mh + i < ov) store4<OutT>(O + (mh + i) * N.ldo + mh + j, vec && nlow == 4, min64(nlow, ov - mh - j), c22);
-      if (i < ov) store4<OutT>(O + i * N.ldo + j, vec && nlow == 4, min64(nlow, ov - j), c11);
+      if (i < ov) {
+        const int64_t n = min64(nlow, ov - j);
+        if (ax) axpby_n(reinterpret_cast<const uint32_t *>(O + i * N.ldo + j), n, c11, 8, P.alpha, P.beta, m);
+        store8<OutT>(O + i * N.ldo + j, n, c11);                                            // C11
+      }
+    }
+  }
+  if (diag) return;
+  // ---- tile U = (tj, ti): C21 = Up(U1) + P4 + P3 (rows j0.., cols i0..)
+#pragma unroll
+  for (int rr = 0; rr < 2; ++rr) {
+    const int y = ty + 32 * rr;
+    const int64_t r = j0 + y, c = i0 + cx;
+    if (r >= mh || c >= mh) continue;
+    uint32_t p3[8], c21[8];
+    ld8(P3 + r * ldp + c, p3);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) c21[e] = addmod(addmod(sU[cx + e][y], q4u[rr][e], m), p3[e], m);
+    const int64_t n21 = min64(8, min64(mh - c, ov - c));
+    if (mh + r < ov) {
+      if (ax) axpby_n(reinterpret_cast<const uint32_t *>(O + (mh + r) * N.ldo + c), n21, c21, 8, P.alpha, P.beta, m);
+      store8<OutT>(O + (mh + r) * N.ldo + c, n21, c21);
     }
   }
 }
@@ -1060,7 +1090,7 @@ __global__ void __launch_bounds__(256) combine_kernel(const __grid_constant__ Co
 cudaError_t launch_combine(const CombParams &p, cudaStream_t s) {
   if (p.n_nodes == 0) return cudaSuccess;
   const unsigned nt = (unsigned)((p.mh + 63) / 64);
-  dim3 grid(nt, nt, (unsigned)p.n_nodes), block(16, 16);
+  dim3 grid(nt * (nt + 1) / 2, (unsigned)p.n_nodes), block(256);
   if (p.in32) combine_kernel<uint32_t, uint32_t><<<grid, block, 0, s>>>(p);
   else if (p.out_u32) combine_kernel<uint16_t, uint32_t><<<grid, block, 0, s>>>(p);
   else combine_kernel<uint16_t, uint16_t><<<grid, block, 0, s>>>(p);
