@@ -102,10 +102,11 @@ struct Leaf2Cfg {
   static constexpr int B_BYTES = 128 * kBK;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int SLOTS = 2;
-  // weighted mod-p partial sums of the limb accumulators: 128 rows x 128 words (u16 pairs),
-  // row stride 129 words so that the 32 rows a warp touches fall in 32 different banks
+  // weighted mod-p partial sums of the limb accumulators: 128 rows x 128 words (u16 pairs)
   // WIDE (p > 2^16): residues < 2^18 packed 24-bit (4 values in 3 words): 192 words + 1 pad per row
-  static constexpr int PART_STRIDE = WIDE ? 193 : 129;
+  // (non-WIDE: stride 130 words = 65 8-byte granules, so 64-bit accesses of the 32 rows a warp
+  //  touches are conflict-free)
+  static constexpr int PART_STRIDE = WIDE ? 193 : 130;
   static constexpr int PART_BYTES = PART ? 128 * PART_STRIDE * 4 : 0;
   static constexpr int BAR_BYTES = 8 * (2 * STAGES + 2 * SLOTS) + 16;
   static constexpr int SMEM = STAGES * STAGE_BYTES + PART_BYTES + 1024 + BAR_BYTES;
@@ -121,7 +122,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (ADJ_EPI_WARPS 
     leaf2_kernel(const __grid_constant__ LeafParams P) {
   using Cfg = Leaf2Cfg<NACC, PART, WIDE>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte alignment (128B swizzle atoms) by pointer arithmetic on the __shared__ array, so
+  // that the compiler keeps the shared state space (LDS/STS, not generic LD/ST)
+  uint8_t *smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint32_t *part_s = reinterpret_cast<uint32_t *>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
   uint64_t *full_bar = reinterpret_cast<uint64_t *>(smem + Cfg::STAGES * Cfg::STAGE_BYTES + Cfg::PART_BYTES);
   uint64_t *empty_bar = full_bar + Cfg::STAGES;
@@ -337,13 +340,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (ADJ_EPI_WARPS 
           const int32_t wc = P.wshoup[j].wc, wq = P.wshoup[j].wq;
           const uint32_t pm = mod.p;
           if constexpr (PART && !WIDE) {
-            uint32_t *pc = prow0 + h0 * 64 + c * 16;
+            uint2 *pc = reinterpret_cast<uint2 *>(prow0 + h0 * 64 + c * 16);
             if (u > 0) {
 #pragma unroll
-              for (int e = 0; e < 16; ++e) {
-                const uint32_t wd = pc[e];
-                v[2 * e] = acc_mulred((int32_t)v[2 * e], wc, wq, wd & 0xFFFF, pm);
-                v[2 * e + 1] = acc_mulred((int32_t)v[2 * e + 1], wc, wq, wd >> 16, pm);
+              for (int e = 0; e < 8; ++e) {
+                const uint2 wd = pc[e];
+                v[4 * e] = acc_mulred((int32_t)v[4 * e], wc, wq, wd.x & 0xFFFF, pm);
+                v[4 * e + 1] = acc_mulred((int32_t)v[4 * e + 1], wc, wq, wd.x >> 16, pm);
+                v[4 * e + 2] = acc_mulred((int32_t)v[4 * e + 2], wc, wq, wd.y & 0xFFFF, pm);
+                v[4 * e + 3] = acc_mulred((int32_t)v[4 * e + 3], wc, wq, wd.y >> 16, pm);
               }
             } else {
 #pragma unroll
@@ -351,7 +356,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (ADJ_EPI_WARPS 
             }
             if (u < nunits - 1) {
 #pragma unroll
-              for (int e = 0; e < 16; ++e) pc[e] = v[2 * e] | (v[2 * e + 1] << 16);
+              for (int e = 0; e < 8; ++e)
+                pc[e] = make_uint2(v[4 * e] | (v[4 * e + 1] << 16), v[4 * e + 2] | (v[4 * e + 3] << 16));
               continue;
             }
           } else if constexpr (PART && WIDE) {
