@@ -984,15 +984,26 @@ __device__ __forceinline__ void store8(OutT *o, int64_t ncols_ok, const uint32_t
   }
 }
 
-__device__ __forceinline__ void ld8(const uint16_t *p, uint32_t (&v)[8]) {
-  const uint4 q = *reinterpret_cast<const uint4 *>(p);
-  v[0] = q.x & 0xFFFF; v[1] = q.x >> 16; v[2] = q.y & 0xFFFF; v[3] = q.y >> 16;
-  v[4] = q.z & 0xFFFF; v[5] = q.z >> 16; v[6] = q.w & 0xFFFF; v[7] = q.w >> 16;
-}
-__device__ __forceinline__ void ld8(const uint32_t *p, uint32_t (&v)[8]) {   // uint32 residues
-  const uint4 q0 = reinterpret_cast<const uint4 *>(p)[0], q1 = reinterpret_cast<const uint4 *>(p)[1];
-  v[0] = q0.x; v[1] = q0.y; v[2] = q0.z; v[3] = q0.w; v[4] = q1.x; v[5] = q1.y; v[6] = q1.z; v[7] = q1.w;
-}
+// 8 residues of a product buffer, kept packed until used (u16: one uint4; u32: two)
+template <typename InT> struct Pk8;
+template <> struct Pk8<uint16_t> {
+  uint4 q;
+  __device__ __forceinline__ void load(const uint16_t *p) { q = *reinterpret_cast<const uint4 *>(p); }
+  __device__ __forceinline__ void get(uint32_t (&v)[8]) const {
+    v[0] = q.x & 0xFFFF; v[1] = q.x >> 16; v[2] = q.y & 0xFFFF; v[3] = q.y >> 16;
+    v[4] = q.z & 0xFFFF; v[5] = q.z >> 16; v[6] = q.w & 0xFFFF; v[7] = q.w >> 16;
+  }
+};
+template <> struct Pk8<uint32_t> {
+  uint4 q0, q1;
+  __device__ __forceinline__ void load(const uint32_t *p) {
+    q0 = reinterpret_cast<const uint4 *>(p)[0];
+    q1 = reinterpret_cast<const uint4 *>(p)[1];
+  }
+  __device__ __forceinline__ void get(uint32_t (&v)[8]) const {
+    v[0] = q0.x; v[1] = q0.y; v[2] = q0.z; v[3] = q0.w; v[4] = q1.x; v[5] = q1.y; v[6] = q1.z; v[7] = q1.w;
+  }
+};
 
 template <typename InT, typename OutT>
 __global__ void __launch_bounds__(256) combine_kernel(const __grid_constant__ CombParams P) {
@@ -1014,19 +1025,34 @@ __global__ void __launch_bounds__(256) combine_kernel(const __grid_constant__ Co
   __shared__ uint32_t sU[64][65];   // U1 on L (Low part; on a diagonal tile the full tile is filled)
   __shared__ uint32_t sQ[64][65];   // P4 on U (rows j0.., cols i0..)
   const int cx = tx * 8;
-  uint32_t u1[2][8], q4u[2][8];
+  // every load of the block up front (buffers are rows_pad x rows_pad: always in range)
+  Pk8<InT> l1[2], l5[2], l2[2], l3[2], l4[2], u4[2], u3[2];
 #pragma unroll
   for (int rr = 0; rr < 2; ++rr) {
     const int y = ty + 32 * rr;
-    const int64_t i = i0 + y, j = j0 + cx;     // buffers are rows_pad x rows_pad: always in range
-    uint32_t a[8], b[8];
-    ld8(P1 + i * ldp + j, a);
-    ld8(P5 + i * ldp + j, b);
+    const int64_t oL = (i0 + y) * ldp + j0 + cx, oU = (j0 + y) * ldp + i0 + cx;
+    l1[rr].load(P1 + oL);
+    l5[rr].load(P5 + oL);
+    u4[rr].load(P4 + oU);
+    l4[rr].load(P4 + oL);
+    l3[rr].load(P3 + oL);
+    l2[rr].load(P2 + oL);
+    if (!diag) u3[rr].load(P3 + oU);
+  }
+  uint32_t u1[2][8];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) { u1[rr][e] = addmod(a[e], b[e], m); sU[y][cx + e] = u1[rr][e]; }
-    ld8(P4 + (j0 + y) * ldp + i0 + cx, q4u[rr]);
+  for (int rr = 0; rr < 2; ++rr) {
+    const int y = ty + 32 * rr;
+    uint32_t a[8], b[8], q[8];
+    l1[rr].get(a);
+    l5[rr].get(b);
+    u4[rr].get(q);
 #pragma unroll
-    for (int e = 0; e < 8; ++e) sQ[y][cx + e] = q4u[rr][e];
+    for (int e = 0; e < 8; ++e) {
+      u1[rr][e] = addmod(a[e], b[e], m);
+      sU[y][cx + e] = u1[rr][e];
+      sQ[y][cx + e] = q[e];
+    }
   }
   __syncthreads();
   OutT *O = static_cast<OutT *>(N.out);
@@ -1038,10 +1064,9 @@ __global__ void __launch_bounds__(256) combine_kernel(const __grid_constant__ Co
     const int y = ty + 32 * rr;
     const int64_t i = i0 + y, j = j0 + cx;
     if (i >= mh || j >= mh) continue;
-    uint32_t p4[8], p3[8], c21[8];
-    ld8(P4 + i * ldp + j, p4);
-    ld8(P3 + i * ldp + j, p3);
-    uint32_t u[8];
+    uint32_t p4[8], p3[8], c21[8], u[8];
+    l4[rr].get(p4);
+    l3[rr].get(p3);
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
       u[e] = (j + e <= i) ? u1[rr][e] : sU[cx + e][y];       // Up(U1) = Low(U1)^T (diagonal tile)
@@ -1054,12 +1079,12 @@ __global__ void __launch_bounds__(256) combine_kernel(const __grid_constant__ Co
     }
     if (j <= i) {
       uint32_t p1[8], p2[8], c22[8], c11[8];
-      ld8(P1 + i * ldp + j, p1);
-      ld8(P2 + i * ldp + j, p2);
+      l1[rr].get(p1);
+      l2[rr].get(p2);
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         c22[e] = addmod(addmod(u[e], p4[e], m), sQ[cx + e][y], m);   // U5 = U2 + P4^T
-        c11[e] = addmod(p1[e], p2[e], m);                                                   // U3 = P1 + P2
+        c11[e] = addmod(p1[e], p2[e], m);                            // U3 = P1 + P2
       }
       const int64_t nlow = min64(8, i - j + 1);           // columns j..i only
       if (mh + i < ov) {
@@ -1081,10 +1106,11 @@ __global__ void __launch_bounds__(256) combine_kernel(const __grid_constant__ Co
     const int y = ty + 32 * rr;
     const int64_t r = j0 + y, c = i0 + cx;
     if (r >= mh || c >= mh) continue;
-    uint32_t p3[8], c21[8];
-    ld8(P3 + r * ldp + c, p3);
+    uint32_t p3[8], q4[8], c21[8];
+    u3[rr].get(p3);
+    u4[rr].get(q4);
 #pragma unroll
-    for (int e = 0; e < 8; ++e) c21[e] = addmod(addmod(sU[cx + e][y], q4u[rr][e], m), p3[e], m);
+    for (int e = 0; e < 8; ++e) c21[e] = addmod(addmod(sU[cx + e][y], q4[e], m), p3[e], m);
     const int64_t n21 = min64(8, min64(mh - c, ov - c));
     if (mh + r < ov) {
       if (ax) axpby_n(reinterpret_cast<const uint32_t *>(O + (mh + r) * N.ldo + c), n21, c21, 8, P.alpha, P.beta, m);
