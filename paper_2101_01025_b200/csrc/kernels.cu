@@ -1132,33 +1132,70 @@ cudaError_t launch_combine(const CombParams &p, cudaStream_t s) {
 // ============================================================================ K5 2M combine
 // Re = G - eps H - phi(H) with eps = i phi(i) = 1, Im: H phi(i) + i phi(H) = i (H^T - H);
 // G lower (u16, ldg), H full (u16, ldh); C interleaved (re, im) uint32 pairs, Low only.
+// One block per lower 64 x 64 tile (grid over lower tile pairs as K4); G, H are rows_pad x
+// rows_pad (multiple of 128, ld a multiple of 8) so every 16-byte tile load is in range.  The
+// mirrored H tile is staged in shared memory; C pairs are stored as 16-byte (re, im, re, im).
 template <typename InT>
 __global__ void __launch_bounds__(256) twom_kernel(int64_t m, const InT *G, int64_t ldg,
                                                    const InT *H, int64_t ldh, uint32_t *C,
                                                    int64_t ldc, ModP mod, uint32_t alpha, uint32_t beta,
                                                    int axpby) {
-  const int ti = blockIdx.y, tj = blockIdx.x;
-  if (ti < tj) return;
-  const int tx = threadIdx.x, ty = threadIdx.y;
-  const int64_t i0 = (int64_t)ti * 32, j0 = (int64_t)tj * 32;
-  __shared__ uint32_t sH[32][33];   // H on the mirrored tile
-  for (int y = ty; y < 32; y += 8) {
-    const int64_t gi = j0 + y, gj = i0 + tx;
-    if (gi < m && gj < m) sH[y][tx] = H[gi * ldh + gj];
+  const int x = (int)blockIdx.x;
+  int ti = (int)((sqrtf(8.0f * (float)x + 1.0f) - 1.0f) * 0.5f);
+  while ((ti + 1) * (ti + 2) / 2 <= x) ++ti;
+  while (ti * (ti + 1) / 2 > x) --ti;
+  const int tj = x - ti * (ti + 1) / 2;
+  const int tx = threadIdx.x & 7, ty = threadIdx.x >> 3;   // 8 x 32
+  const int64_t i0 = (int64_t)ti * 64, j0 = (int64_t)tj * 64;
+  const int cx = tx * 8;
+  __shared__ uint32_t sH[64][65];   // H on the mirrored tile (rows j0.., cols i0..)
+  Pk8<InT> g[2], h[2], hu[2];
+#pragma unroll
+  for (int rr = 0; rr < 2; ++rr) {
+    const int y = ty + 32 * rr;
+    g[rr].load(G + (i0 + y) * ldg + j0 + cx);
+    h[rr].load(H + (i0 + y) * ldh + j0 + cx);
+    hu[rr].load(H + (j0 + y) * ldh + i0 + cx);
+  }
+#pragma unroll
+  for (int rr = 0; rr < 2; ++rr) {
+    uint32_t q[8];
+    hu[rr].get(q);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) sH[ty + 32 * rr][cx + e] = q[e];
   }
   __syncthreads();
-  for (int y = ty; y < 32; y += 8) {
-    const int64_t i = i0 + y, j = j0 + tx;
+#pragma unroll
+  for (int rr = 0; rr < 2; ++rr) {
+    const int y = ty + 32 * rr;
+    const int64_t i = i0 + y, j = j0 + cx;
     if (i >= m || j > i) continue;
-    const uint32_t h = H[i * ldh + j], ht = sH[tx][y];   // H(i,j), H(j,i)
-    uint32_t re = submod(submod(G[i * ldg + j], h, mod), ht, mod);
-    uint32_t im = submod(ht, h, mod);
-    if (axpby) {
-      re = addmod(mulmod_any(alpha, re, mod), mulmod_any(beta, mod_u32(C[2 * (i * ldc + j)], mod), mod), mod);
-      im = addmod(mulmod_any(alpha, im, mod), mulmod_any(beta, mod_u32(C[2 * (i * ldc + j) + 1], mod), mod), mod);
+    uint32_t gv[8], hv[8], re[8], im[8];
+    g[rr].get(gv);
+    h[rr].get(hv);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const uint32_t ht = sH[cx + e][y];                                  // H(j, i)
+      re[e] = submod(submod(gv[e], hv[e], mod), ht, mod);                 // G - H - H^T
+      im[e] = submod(ht, hv[e], mod);                                     // H^T - H
     }
-    C[2 * (i * ldc + j)] = re;
-    C[2 * (i * ldc + j) + 1] = im;
+    const int64_t n = min64(8, min64(i - j + 1, m - j));
+    uint32_t *o = C + 2 * (i * ldc + j);
+    if (axpby) {
+      for (int e = 0; e < n; ++e) {
+        re[e] = addmod(mulmod_any(alpha, re[e], mod), mulmod_any(beta, mod_u32(o[2 * e], mod), mod), mod);
+        im[e] = addmod(mulmod_any(alpha, im[e], mod), mulmod_any(beta, mod_u32(o[2 * e + 1], mod), mod), mod);
+      }
+    }
+    if (n == 8 && (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        reinterpret_cast<uint4 *>(o)[e] = make_uint4(re[2 * e], im[2 * e], re[2 * e + 1], im[2 * e + 1]);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        if (e < n) { o[2 * e] = re[e]; o[2 * e + 1] = im[e]; }
+    }
   }
 }
 
@@ -1166,15 +1203,14 @@ cudaError_t launch_twom(int64_t m, const void *G, int64_t ldg, const void *H, in
                         uint32_t *C, int64_t ldc, const ModP &mod, uint32_t alpha, uint32_t beta, int axpby,
                         cudaStream_t s) {
   if (m == 0) return cudaSuccess;
-  const unsigned nt = (unsigned)((m + 31) / 32);
+  const unsigned nt = (unsigned)((m + 63) / 64);
+  const dim3 grid(nt * (nt + 1) / 2);
   if (in32)
-    twom_kernel<uint32_t><<<dim3(nt, nt), dim3(32, 8), 0, s>>>(m, static_cast<const uint32_t *>(G), ldg,
-                                                              static_cast<const uint32_t *>(H), ldh, C, ldc, mod,
-                                                              alpha, beta, axpby);
+    twom_kernel<uint32_t><<<grid, 256, 0, s>>>(m, static_cast<const uint32_t *>(G), ldg,
+                                               static_cast<const uint32_t *>(H), ldh, C, ldc, mod, alpha, beta, axpby);
   else
-    twom_kernel<uint16_t><<<dim3(nt, nt), dim3(32, 8), 0, s>>>(m, static_cast<const uint16_t *>(G), ldg,
-                                                              static_cast<const uint16_t *>(H), ldh, C, ldc, mod,
-                                                              alpha, beta, axpby);
+    twom_kernel<uint16_t><<<grid, 256, 0, s>>>(m, static_cast<const uint16_t *>(G), ldg,
+                                               static_cast<const uint16_t *>(H), ldh, C, ldc, mod, alpha, beta, axpby);
   return cudaGetLastError();
 }
 
