@@ -642,6 +642,23 @@ __device__ __forceinline__ void put_limbs4(int8_t *base, int64_t plane_stride, c
   for (int pl = 0; pl < NP; ++pl) *reinterpret_cast<uint32_t *>(base + pl * plane_stride) = w[pl];
 }
 
+// limb planes of 8 consecutive residues (two 4-groups), one 8-byte store per plane
+template <int SCHEME>
+__device__ __forceinline__ void put_limbs8(int8_t *base, int64_t plane_stride, const uint32_t (&x0)[4],
+                                           const uint32_t (&x1)[4], const ModP &m) {
+  if constexpr (SCHEME == 3) {
+    put_limbs4_t6(base, plane_stride, x0, m);
+    put_limbs4_t6(base + 4, plane_stride, x1, m);
+    return;
+  }
+  constexpr int NP = SCHEME == 0 ? 1 : (SCHEME == 1 ? 3 : 2);
+  uint32_t w0[3], w1[3];
+  limbs4<SCHEME>(x0, m, w0);
+  limbs4<SCHEME>(x1, m, w1);
+#pragma unroll
+  for (int pl = 0; pl < NP; ++pl) *reinterpret_cast<uint2 *>(base + pl * plane_stride) = make_uint2(w0[pl], w1[pl]);
+}
+
 template <int YK, bool WIDE = false>
 __device__ __forceinline__ void apply_Y4(const uint32_t (&a)[4], const uint32_t (&b)[4], uint32_t (&oa)[4],
                                          uint32_t (&ob)[4], uint32_t ya, uint32_t yb, const ModP &m) {
@@ -909,44 +926,56 @@ cudaError_t launch_preadd(const PreParams &p, cudaStream_t s) {
 }
 
 // ============================================================================ plain split
+// One thread per (row, 8 columns): both 4-column groups are loaded before any limb store so
+// that each thread keeps 32-64 bytes of loads in flight.
 template <int SCHEME>
 __global__ void __launch_bounds__(256) split_kernel(const __grid_constant__ SplitParams P) {
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= P.kpad / 4) return;
-  const int64_t c = g * 4;
+  if (g >= P.kpad / 8) return;
+  const int64_t c0 = g * 8;
   const int64_t ps = P.rows_pad * P.kpad;
+  const InView &v = P.in;
   for (int64_t r = blockIdx.y; r < P.rows_pad; r += gridDim.y) {
-    uint32_t x[4];
-    const InView &v = P.in;
+    InView vv = v;
+    if (r >= P.rows) vv.rows_valid = 0;
+    const bool fast = vv.vec_ok && r < vv.rows_valid && c0 + 7 < vv.cols_valid && c0 + 7 < P.cols;
     if (P.mode == 1) {
       // 2M at depth 0: one read of the interleaved A gives X = Re, Y = Im and T = X + Y
-      InView vv = v;
-      if (r >= P.rows) vv.rows_valid = 0;
-      if (c >= P.cols) vv.cols_valid = 0;
-      const bool fast = vv.vec_ok && r < vv.rows_valid && c + 3 < vv.cols_valid;
-      uint32_t re[4], im[4];
-      load4_pair(vv, r, c, fast, P.mod, re, im);
+      uint32_t re[2][4], im[2][4];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) x[e] = addmod(re[e], im[e], P.mod);
-      put_limbs4<SCHEME>(P.arena + (P.op_row + r) * P.kpad + c, ps, re, P.mod);
-      put_limbs4<SCHEME>(P.arena + (P.op_row2 + r) * P.kpad + c, ps, im, P.mod);
-      put_limbs4<SCHEME>(P.arena + (P.op_row3 + r) * P.kpad + c, ps, x, P.mod);
+      for (int h = 0; h < 2; ++h) {
+        InView vh = vv;
+        if (c0 + 4 * h >= P.cols) vh.cols_valid = 0;
+        load4_pair(vh, r, c0 + 4 * h, fast, P.mod, re[h], im[h]);
+      }
+      uint32_t x[2][4];
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) x[h][e] = addmod(re[h][e], im[h][e], P.mod);
+      put_limbs8<SCHEME>(P.arena + (P.op_row + r) * P.kpad + c0, ps, re[0], re[1], P.mod);
+      put_limbs8<SCHEME>(P.arena + (P.op_row2 + r) * P.kpad + c0, ps, im[0], im[1], P.mod);
+      put_limbs8<SCHEME>(P.arena + (P.op_row3 + r) * P.kpad + c0, ps, x[0], x[1], P.mod);
       continue;
     }
-    if (v.vec_ok && r < P.rows && r < v.rows_valid && c + 3 < v.cols_valid && c + 3 < P.cols && v.type == IN_U32) {
-      load4_fast<IN_U32>(v.ptr, r * v.ld + c, P.mod, x);
-    } else {
-      InView vv = v;
-      if (r >= P.rows) vv.rows_valid = 0;
-      if (c >= P.cols) vv.cols_valid = 0;
-      load4(vv, r, c, P.mod, x);
+    uint32_t x[2][4];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t c = c0 + 4 * h;
+      if (fast && v.type == IN_U32) {
+        load4_fast<IN_U32>(v.ptr, r * v.ld + c, P.mod, x[h]);
+      } else {
+        InView vh = vv;
+        if (c >= P.cols) vh.cols_valid = 0;
+        load4(vh, r, c, P.mod, x[h]);
+      }
     }
-    put_limbs4<SCHEME>(P.arena + (P.op_row + r) * P.kpad + c, ps, x, P.mod);
+    put_limbs8<SCHEME>(P.arena + (P.op_row + r) * P.kpad + c0, ps, x[0], x[1], P.mod);
   }
 }
 
 cudaError_t launch_split(const SplitParams &p, cudaStream_t s) {
-  dim3 grid((unsigned)((p.kpad / 4 + 255) / 256), (unsigned)(p.rows_pad < 65535 ? p.rows_pad : 65535));
+  dim3 grid((unsigned)((p.kpad / 8 + 255) / 256), (unsigned)(p.rows_pad < 65535 ? p.rows_pad : 65535));
   if (p.scheme == 0) split_kernel<0><<<grid, 256, 0, s>>>(p);
   else if (p.scheme == 1) split_kernel<1><<<grid, 256, 0, s>>>(p);
   else if (p.scheme == 2) split_kernel<2><<<grid, 256, 0, s>>>(p);
