@@ -45,7 +45,7 @@ UNIT = "MAC/s"
 
 def limb_mmas(p: int) -> int:
     """int8 tcgen05 MMAs per ring MAC of the limb scheme."""
-    return 1 if p <= 255 else (3 if p <= 16763 else 4)
+    return 1 if p <= 255 else (3 if p <= 16763 else (4 if p <= 65521 else 6))
 
 
 def ring_macs(m: int, k: int, d: int) -> float:
@@ -57,9 +57,18 @@ def ring_macs(m: int, k: int, d: int) -> float:
     return 3 * ring_macs(mh, kh, d - 1) + 2 * mh * mh * kh
 
 
-def leaf_int8_ops(cfg, depth) -> float:
+def herk_alg1_macs(m: int, k: int) -> float:
+    """Base-field MACs of one level of Alg. alg:MIAHMM over GF(p^2) (ADJ_HERK_ALG1): three
+    Hermitian leaves by 2M (G = T T^T lower + H = X Y^T) and two general leaves by 3M."""
+    mh, kh = -(-m // 2), 8 * -(-k // 16)
+    return 3 * (mh * (mh + 1) / 2 * kh) + 9 * mh * mh * kh
+
+
+def leaf_int8_ops(cfg, depth, herk="2m") -> float:
     """Algorithmic int8 tensor ops (2 per MAC) of ONE grouped leaf launch."""
     m, k, p = cfg["m"], cfg["k"], cfg["p"]
+    if cfg["phi"] == "H" and herk == "alg1":
+        return 2.0 * herk_alg1_macs(m, k) * limb_mmas(p)
     macs = ring_macs(m, k, depth)
     if cfg["phi"] == "H":
         macs += m * m * k            # 2M's general product H = X Y^T
@@ -238,8 +247,10 @@ def run_gpu(args, cfg, rank, world, local_rank):
     m, k, p = cfg["m"], cfg["k"], cfg["p"]
     phi = adj.ADJ_PHI_H if cfg["phi"] == "H" else adj.ADJ_PHI_T
     w = 2 if cfg["phi"] == "H" else 1
+    alg1 = cfg["phi"] == "H" and args.herk == "alg1"
+    flags = adj.ADJ_HERK_ALG1 if alg1 else 0
     depth = args.depth if args.depth is not None else (cfg["depth"] if cfg["depth"] is not None
-                                                       else adj.adjprod_modp_auto_depth(m, k, p, phi))
+                                                       else (1 if alg1 else adj.adjprod_modp_auto_depth(m, k, p, phi)))
     A = torch.empty((m, k * w), dtype=torch.int32, device=dev)
     uniform_residues_cuda(A, seed=1, p=p)
     C = torch.zeros((m, m * w), dtype=torch.int32, device=dev)
@@ -252,15 +263,15 @@ def run_gpu(args, cfg, rank, world, local_rank):
         k0, k1 = adj.adj_dist_kslice(k, world, rank)
         ws_bytes = adj.adjprod_modp_workspace_size(m, max(1, k1 - k0), p, phi, depth)
     else:
-        ws_bytes = adj.adjprod_modp_workspace_size(m, k, p, phi, depth)
+        ws_bytes = adj.adjprod_modp_workspace_size(m, k, p, phi, depth, flags)
     ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
 
     def step():
         if comm is None:
-            adj.adjprod_modp_ex(m, k, p, phi, A, k, C, m, depth=depth, workspace=ws, workspace_bytes=ws_bytes,
-                                stream=stream)
+            adj.adjprod_modp_ex(m, k, p, phi, A, k, C, m, depth=depth, flags=flags, workspace=ws,
+                                workspace_bytes=ws_bytes, stream=stream)
         else:
             adj.adjprod_modp_dist(m, k, p, phi, A, k, C, m, 0, comm, depth=depth, stream=stream)
 
@@ -330,7 +341,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
                 s_cmp.wait_event(ev_in[i])
                 if i >= 2:
                     s_cmp.wait_event(ev_out[i - 2])
-                adj.adjprod_modp_ex(m, k, p, phi, dA[b], k, dC[b], m, depth=depth, workspace=ws,
+                adj.adjprod_modp_ex(m, k, p, phi, dA[b], k, dC[b], m, depth=depth, flags=flags, workspace=ws,
                                     workspace_bytes=ws_bytes, stream=s_cmp)
                 ev_cmp[i].record(s_cmp)
             with torch.cuda.stream(s_out):
@@ -365,7 +376,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
     leaf_ms, leaf_n = prof["leaf"]
     # one grouped leaf stage per step: the tcgen05 leaf launch (+ its tail fixup launch, if any)
     leaf_avg_ms = leaf_ms / args.steps
-    ops = leaf_int8_ops(cfg, depth)
+    ops = leaf_int8_ops(cfg, depth, args.herk)
     achieved = ops / (leaf_avg_ms * 1e-3) / 1e12
     peak = 2.0 * peaks["bf16_tflops"]        # int8 dense = 2 x bf16 dense (guide's nominal ratio)
     roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
@@ -383,13 +394,14 @@ def run_gpu(args, cfg, rank, world, local_rank):
         cpu = {"value": eff, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
 
     if rank == 0:
-        mh = ring_macs(m, k, depth) * (1 if w == 1 else 1)
+        mh = herk_alg1_macs(m, k) if alg1 else ring_macs(m, k, depth) + (m * m * k if w == 2 else 0)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "int8",
             "data": "synthetic",
-            "config": {"workload": cfg["workload"], "m": m, "k": k, "p": p, "phi": cfg["phi"], "depth": depth,
+            "config": {"workload": cfg["workload"] + (" via Alg. 1 over GF(p^2) (ADJ_HERK_ALG1)" if alg1 else ""),
+                       "m": m, "k": k, "p": p, "phi": cfg["phi"], "depth": depth,
                        "seed": 1, "l2": "flushed before every timed step (256 MiB write, outside step events)",
                        "parallelism": f"split-K x{world} (NCCL reduce)" if world > 1 else "1 GPU",
                        "fraction_of_int8_peak_effective": value / (peak * 1e12 / 2),
@@ -417,6 +429,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-check", action="store_true", help="skip the sampled parity check")
+    ap.add_argument("--herk", default="2m", choices=["2m", "alg1"],
+                    help="phi = H: 2M reduction (default) or one level of Alg. 1 over GF(p^2)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     world = int(os.environ.get("WORLD_SIZE", "1"))

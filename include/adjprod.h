@@ -66,11 +66,19 @@ typedef enum {
   ADJ_ERR_ARCH = 6                 /* current device is not sm_100 (B200) */
 } adj_status_t;
 
-enum { ADJ_FILL_UPPER = 1u };
+/* option flags (adj_opts_t.flags)
+ *   ADJ_FILL_UPPER : also write the strict upper triangle, Up(C) = phi(Low(C)) (Lemma lem:uplow).
+ *   ADJ_HERK_ALG1  : phi = ADJ_PHI_H only -- run one level of Alg. alg:MIAHMM directly over
+ *                    GF(p^2) with the scalar skew-unitary Y = (a + ib) I, a^2 + b^2 = -1
+ *                    (§4.4, 750-758) instead of the 2M reduction
+ *                    to GF(p) (Alg. alg:2M).  Its Hermitian leaves P1, P2, P5 use 2M, its
+ *                    general leaves P3, P4 use 3M.  Requires depth 1 (or -1); the result is the
+ *                    same Low(C).  Ignored for phi = ADJ_PHI_T. */
+enum { ADJ_FILL_UPPER = 1u, ADJ_HERK_ALG1 = 2u };
 
 typedef struct {
   int depth;              /* recursion levels of Alg. alg:MIAHMM; -1 = automatic; 0 = classical */
-  uint32_t flags;         /* ADJ_FILL_UPPER */
+  uint32_t flags;         /* ADJ_FILL_UPPER | ADJ_HERK_ALG1 */
   void *workspace;        /* device memory of >= workspace_bytes, or NULL (library allocates
                              stream-ordered with cudaMallocAsync/cudaFreeAsync) */
   size_t workspace_bytes;

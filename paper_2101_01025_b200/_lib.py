@@ -14,6 +14,7 @@ LIB_PATH = os.path.join(_PKG, "libadjprod.so")
 ADJ_PHI_T = 0
 ADJ_PHI_H = 1
 ADJ_FILL_UPPER = 1
+ADJ_HERK_ALG1 = 2
 STATUS = {0: "ADJ_OK", 1: "ADJ_ERR_INVALID_VALUE", 2: "ADJ_ERR_UNSUPPORTED_MODULUS", 3: "ADJ_ERR_WORKSPACE",
           4: "ADJ_ERR_CUDA", 5: "ADJ_ERR_NCCL", 6: "ADJ_ERR_ARCH"}
 
@@ -123,8 +124,8 @@ def adjprod_modp_syrk(m, k, p, phi, alpha, A, lda, beta, C, ldc, depth=-1, flags
                                    _stream(stream)), "adjprod_modp_syrk")
 
 
-def adjprod_modp_workspace_size(m, k, p, phi, depth=-1) -> int:
-    o = _opts(depth)
+def adjprod_modp_workspace_size(m, k, p, phi, depth=-1, flags=0) -> int:
+    o = _opts(depth, flags)
     n = ctypes.c_size_t(0)
     _check(lib().adjprod_modp_workspace_size(m, k, p, phi, ctypes.byref(o), ctypes.byref(n)),
            "adjprod_modp_workspace_size")

@@ -151,8 +151,9 @@ adj_status_t get_plan(Plan **out, int kind, int64_t m, int64_t n, int64_t k, uin
   if (it != g_plans.end()) { *out = it->second.get(); return ADJ_OK; }
   auto P = std::make_unique<Plan>();
   const char *err = nullptr;
-  bool ok = kind == PLAN_GEMM ? build_gemm_plan(*P, m, n, k, p, sms, &err)
-                              : build_syrk_plan(*P, m, k, p, phi, depth, sms, &err);
+  bool ok = kind == PLAN_GEMM    ? build_gemm_plan(*P, m, n, k, p, sms, &err)
+            : kind == PLAN_HERK1 ? build_herk1_plan(*P, m, k, p, sms, &err)
+                                 : build_syrk_plan(*P, m, k, p, phi, depth, sms, &err);
   if (!ok) return fail(ADJ_ERR_INVALID_VALUE, "plan: %s", err ? err : "unsupported");
   P->dev = dev;
   if (!P->tiles.empty()) {
@@ -430,6 +431,35 @@ adj_status_t run_syrk(const Plan &P, const Ptrs &x, adj_phi_t phi, uint32_t flag
   return ADJ_OK;
 }
 
+// phi = H by one level of Alg. alg:MIAHMM over GF(p^2) (ADJ_HERK_ALG1): K1 over GF(p^2), one
+// grouped leaf launch (2M for P1, P2, P5; 3M for P3, P4), then the fused GF(p^2) K4.
+adj_status_t run_herk1(const Plan &P, const Ptrs &x, uint32_t flags, cudaStream_t s) {
+  const LevelPlan &L = P.lv[1];
+  HerkPreParams hp;
+  std::memset(&hp, 0, sizeof(hp));
+  hp.in = make_view(x.A, x.lda, P.m, P.k, IN_PAIR_RE);
+  hp.mh = L.mh; hp.kh = L.kh;
+  hp.rows_pad = L.rows_pad; hp.kpad = L.kpad;
+  hp.arena = reinterpret_cast<int8_t *>(x.ws + P.arenas[0].offset);
+  hp.scheme = P.scheme; hp.planes = P.planes;
+  hp.ya = P.Y.a; hp.yb = P.Y.b;
+  hp.mod = P.mod;
+  LAUNCH_CLS(CLS_PRE, launch_herk_preadd(hp, s));
+  adj_status_t st = launch_leaf_all(P, x, s);
+  if (st) return st;
+  HerkCombParams cp;
+  std::memset(&cp, 0, sizeof(cp));
+  for (int b = 0; b < HB_N; ++b) cp.B[b] = x.ws + P.hb_offset + (size_t)b * P.hb_bytes;
+  cp.mh = L.mh; cp.ldp = L.rows_pad;
+  cp.C = x.C; cp.ldc = x.ldc; cp.out_valid = P.m;
+  cp.mod = P.mod;
+  cp.alpha = x.alpha; cp.beta = x.beta; cp.axpby = x.axpby;
+  cp.in32 = P.res32 ? 1 : 0;
+  LAUNCH_CLS(CLS_COMB, launch_herk_combine(cp, s));
+  if (flags & ADJ_FILL_UPPER) LAUNCH(launch_fill_upper(P.m, 2, x.C, x.ldc, P.mod, s));
+  return ADJ_OK;
+}
+
 adj_status_t validate_syrk(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, const uint32_t *A, int64_t lda,
                            const uint32_t *C, int64_t ldc) {
   if (m < 0 || k < 0) return fail(ADJ_ERR_INVALID_VALUE, "negative dimension (m=%lld, k=%lld)", (long long)m, (long long)k);
@@ -522,10 +552,12 @@ adj_status_t adjprod_modp_workspace_size(int64_t m, int64_t k, uint32_t p, adj_p
   if (m < 0 || k < 0) return fail(ADJ_ERR_INVALID_VALUE, "negative dimension");
   if (!valid_modulus(p)) return fail(ADJ_ERR_UNSUPPORTED_MODULUS, "p=%u is not an odd prime in [3, 262139]", p);
   if (m == 0 || k == 0) { *bytes = 0; return ADJ_OK; }
-  int depth = (opts && opts->depth >= 0) ? opts->depth : auto_depth(m, k, p, (int)phi);
+  const bool herk1 = phi == ADJ_PHI_H && opts && (opts->flags & ADJ_HERK_ALG1);
+  int depth = (opts && opts->depth >= 0) ? opts->depth : (herk1 ? 1 : auto_depth(m, k, p, (int)phi));
+  if (herk1 && depth != 1) return fail(ADJ_ERR_INVALID_VALUE, "ADJ_HERK_ALG1 runs exactly one level (depth 1 or -1)");
   Plan P;
   const char *err = nullptr;
-  if (!build_syrk_plan(P, m, k, p, (int)phi, depth, 148, &err))
+  if (!(herk1 ? build_herk1_plan(P, m, k, p, 148, &err) : build_syrk_plan(P, m, k, p, (int)phi, depth, 148, &err)))
     return fail(ADJ_ERR_INVALID_VALUE, "plan: %s", err ? err : "unsupported");
   *bytes = P.ws_bytes;
   return ADJ_OK;
@@ -552,11 +584,13 @@ static adj_status_t adjprod_impl(int64_t m, int64_t k, uint32_t p, adj_phi_t phi
     if (flags & ADJ_FILL_UPPER) LAUNCH(launch_fill_upper(m, w, C, ldc, make_modp(p), s));
     return ADJ_OK;
   }
-  int depth = (opts && opts->depth >= 0) ? opts->depth : auto_depth(m, k, p, (int)phi);
+  const bool herk1 = phi == ADJ_PHI_H && (flags & ADJ_HERK_ALG1);
+  int depth = (opts && opts->depth >= 0) ? opts->depth : (herk1 ? 1 : auto_depth(m, k, p, (int)phi));
   if (depth > 3) return fail(ADJ_ERR_INVALID_VALUE, "depth %d > 3 unsupported", depth);
+  if (herk1 && depth != 1) return fail(ADJ_ERR_INVALID_VALUE, "ADJ_HERK_ALG1 runs exactly one level (depth 1 or -1)");
   Plan *P = nullptr;
-  if ((st = get_plan(&P, phi == ADJ_PHI_T ? PLAN_SYRK_T : PLAN_SYRK_H, m, m, k, p, (int)phi, depth, dev, sms)) != ADJ_OK)
-    return st;
+  const int kind = herk1 ? PLAN_HERK1 : (phi == ADJ_PHI_T ? PLAN_SYRK_T : PLAN_SYRK_H);
+  if ((st = get_plan(&P, kind, m, m, k, p, (int)phi, depth, dev, sms)) != ADJ_OK) return st;
   Ptrs x;
   x.A = A; x.lda = lda; x.C = C; x.ldc = ldc;
   x.alpha = alpha; x.beta = beta; x.axpby = axpby;
@@ -569,7 +603,7 @@ static adj_status_t adjprod_impl(int64_t m, int64_t k, uint32_t p, adj_phi_t phi
     return fail(ADJ_ERR_WORKSPACE, "workspace %zu bytes < required %zu", opts->workspace_bytes, P->ws_bytes);
   }
   x.ws = static_cast<uint8_t *>(ws);
-  st = run_syrk(*P, x, phi, flags, s);
+  st = herk1 ? run_herk1(*P, x, flags, s) : run_syrk(*P, x, phi, flags, s);
   if (own) {
     cudaError_t e = cudaFreeAsync(ws, s);
     if (st == ADJ_OK && e != cudaSuccess) return fail(ADJ_ERR_CUDA, "cudaFreeAsync: %s", cudaGetErrorString(e));

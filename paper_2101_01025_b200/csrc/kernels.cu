@@ -1158,6 +1158,281 @@ cudaError_t launch_combine(const CombParams &p, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// ============================================================================ GF(p^2) Alg. 1 (PLAN_HERK1)
+// K1 over GF(p^2) with the scalar skew-unitary Y = y I, y = ya + i yb, y conj(y) = -1
+// (PAPER.md:750-758): S1 = y (A21 - A11), S2 = A22 - y A21, S3 = S1 - A22, S4 = S3 + A12
+// (Alg. alg:MIAHMM), then the 21 real limb operands of the leaves:
+//   2M for P1, P2, P5 (T = re + im, X = re, Y = im of A11, A12, S3),
+//   3M for P3 = A22 S4^H and P4 = S1 S2^H (re, im and re + im of the left factor, re, im and
+//   re - im of the right factor).
+// One thread per (row, 4 consecutive columns) of the (mh x kh) quadrants.
+template <int SCHEME>
+__global__ void __launch_bounds__(256) herk_preadd_kernel(const __grid_constant__ HerkPreParams P) {
+  constexpr int NP = SCHEME == 0 ? 1 : (SCHEME == 1 ? 3 : (SCHEME == 2 ? 2 : 6));
+  constexpr bool WIDE = SCHEME == 3;
+  const int64_t g_main = P.kh / 4;
+  const int64_t g_pad = (P.kpad - P.kh) / 4;
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= g_main + g_pad) return;
+  const ModP &m = P.mod;
+  const int64_t ps = P.rows_pad * P.kpad;
+  auto out = [&](int o, int64_t r, int64_t c) { return P.arena + ((int64_t)o * P.planes * P.rows_pad + r) * P.kpad + c; };
+  for (int64_t r = blockIdx.y; r < P.rows_pad; r += gridDim.y) {
+    if (g >= g_main) {
+      const int64_t col = P.kh + (g - g_main) * 4;
+#pragma unroll 1
+      for (int o = 0; o < HO_N; ++o)
+#pragma unroll
+        for (int pl = 0; pl < NP; ++pl) *reinterpret_cast<uint32_t *>(out(o, r, col) + pl * ps) = 0u;
+      continue;
+    }
+    const int64_t c = g * 4;
+    InView v = P.in;
+    if (r >= P.mh) v.rows_valid = 0;    // zero padding rows [mh, rows_pad)
+    const bool fast = v.vec_ok && r < P.mh && P.mh + r < v.rows_valid && P.kh + c + 3 < v.cols_valid;
+    uint32_t a11r[4], a11i[4], a12r[4], a12i[4], a21r[4], a21i[4], a22r[4], a22i[4];
+    load4_pair(v, r, c, fast, m, a11r, a11i);
+    load4_pair(v, r, P.kh + c, fast, m, a12r, a12i);
+    load4_pair(v, P.mh + r, c, fast, m, a21r, a21i);
+    load4_pair(v, P.mh + r, P.kh + c, fast, m, a22r, a22i);
+    uint32_t dr[4], di[4], s1r[4], s1i[4], tr[4], ti[4], s2r[4], s2i[4], s3r[4], s3i[4], s4r[4], s4i[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) { dr[e] = submod(a21r[e], a11r[e], m); di[e] = submod(a21i[e], a11i[e], m); }
+    apply_Y4<1, WIDE>(dr, di, s1r, s1i, P.ya, P.yb, m);        // S1 = y (A21 - A11)
+    apply_Y4<1, WIDE>(a21r, a21i, tr, ti, P.ya, P.yb, m);      // y A21
+    uint32_t w[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      s2r[e] = submod(a22r[e], tr[e], m); s2i[e] = submod(a22i[e], ti[e], m);     // S2 = A22 - y A21
+      s3r[e] = submod(s1r[e], a22r[e], m); s3i[e] = submod(s1i[e], a22i[e], m);   // S3 = S1 - A22
+      s4r[e] = addmod(s3r[e], a12r[e], m); s4i[e] = addmod(s3i[e], a12i[e], m);   // S4 = S3 + A12
+    }
+#define HPUT(o, X) put_limbs4<SCHEME>(out(o, r, c), ps, X, m)
+#define HSUM(X, Y) for (int e = 0; e < 4; ++e) w[e] = addmod(X[e], Y[e], m)
+#define HDIF(X, Y) for (int e = 0; e < 4; ++e) w[e] = submod(X[e], Y[e], m)
+    HSUM(a11r, a11i); HPUT(HO_T11, w); HPUT(HO_X11, a11r); HPUT(HO_Y11, a11i);
+    HSUM(a12r, a12i); HPUT(HO_T12, w); HPUT(HO_X12, a12r); HPUT(HO_Y12, a12i);
+    HSUM(s3r, s3i);   HPUT(HO_T3, w);  HPUT(HO_X3, s3r);   HPUT(HO_Y3, s3i);
+    HSUM(a22r, a22i); HPUT(HO_Z22, w); HPUT(HO_X22, a22r); HPUT(HO_Y22, a22i);
+    HDIF(s4r, s4i);   HPUT(HO_W4, w);  HPUT(HO_X4, s4r);   HPUT(HO_Y4, s4i);
+    HSUM(s1r, s1i);   HPUT(HO_Z1, w);  HPUT(HO_X1, s1r);   HPUT(HO_Y1, s1i);
+    HDIF(s2r, s2i);   HPUT(HO_W2, w);  HPUT(HO_X2, s2r);   HPUT(HO_Y2, s2i);
+#undef HPUT
+#undef HSUM
+#undef HDIF
+  }
+}
+
+cudaError_t launch_herk_preadd(const HerkPreParams &p, cudaStream_t s) {
+  const int64_t groups = p.kh / 4 + (p.kpad - p.kh) / 4;
+  dim3 grid((unsigned)((groups + 255) / 256), (unsigned)(p.rows_pad < 65535 ? p.rows_pad : 65535));
+  if (p.scheme == 0) herk_preadd_kernel<0><<<grid, 256, 0, s>>>(p);
+  else if (p.scheme == 1) herk_preadd_kernel<1><<<grid, 256, 0, s>>>(p);
+  else if (p.scheme == 2) herk_preadd_kernel<2><<<grid, 256, 0, s>>>(p);
+  else herk_preadd_kernel<3><<<grid, 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+// 8 consecutive complex results (re, im) of C row `o` (interleaved pairs), n <= 8 valid
+__device__ __forceinline__ void store_c8(uint32_t *o, int64_t n, uint32_t (&re)[8], uint32_t (&im)[8],
+                                         const HerkCombParams &P) {
+  if (n <= 0) return;
+  if (P.axpby) {
+    for (int e = 0; e < n; ++e) {
+      re[e] = addmod(mulmod_any(P.alpha, re[e], P.mod), mulmod_any(P.beta, mod_u32(o[2 * e], P.mod), P.mod), P.mod);
+      im[e] = addmod(mulmod_any(P.alpha, im[e], P.mod), mulmod_any(P.beta, mod_u32(o[2 * e + 1], P.mod), P.mod), P.mod);
+    }
+  }
+  if (n == 8 && (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      reinterpret_cast<uint4 *>(o)[e] = make_uint4(re[2 * e], im[2 * e], re[2 * e + 1], im[2 * e + 1]);
+  } else {
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      if (e < n) { o[2 * e] = re[e]; o[2 * e + 1] = im[e]; }
+  }
+}
+
+// K4 over GF(p^2) (PAPER.md:315-323 with phi = conjugate transpose), fused with the leaf
+// combinations: P1, P2, P5 = (G - H - H^T) + i (H^T - H) (2M) and
+// P3, P4 = (t1 + t2) + i (t3 - t1 + t2) (3M).  One block per lower pair {L = (ti, tj),
+// U = (tj, ti)} of 64 x 64 tiles:
+//   phase 1: U1 = P1 + P5 and U3 = P1 + P2 on L (only the sums H1 + H5, H1 + H2 are needed
+//            transposed), C11 = Low(U3);
+//   phase 2: P3, P4 on L and U; C21 = U1 + P4 + P3 on L and U (Up(U1) = conj(Low(U1))^T),
+//            C22 = Low(U1 + P4 + conj(P4)^T).
+// Dynamic shared memory: 4 tiles of 64 x 65 words.
+template <typename InT>
+__global__ void __launch_bounds__(256, 2) herk_combine_kernel(const __grid_constant__ HerkCombParams P) {
+  extern __shared__ uint32_t hsm[];
+  uint32_t(*S0)[65] = reinterpret_cast<uint32_t(*)[65]>(hsm);
+  uint32_t(*S1)[65] = reinterpret_cast<uint32_t(*)[65]>(hsm + 64 * 65);
+  uint32_t(*S2)[65] = reinterpret_cast<uint32_t(*)[65]>(hsm + 2 * 64 * 65);
+  uint32_t(*S3)[65] = reinterpret_cast<uint32_t(*)[65]>(hsm + 3 * 64 * 65);
+  const int x = (int)blockIdx.x;
+  int ti = (int)((sqrtf(8.0f * (float)x + 1.0f) - 1.0f) * 0.5f);
+  while ((ti + 1) * (ti + 2) / 2 <= x) ++ti;
+  while (ti * (ti + 1) / 2 > x) --ti;
+  const int tj = x - ti * (ti + 1) / 2;
+  const bool diag = ti == tj;
+  const int tx = threadIdx.x & 7, ty = threadIdx.x >> 3;
+  const int64_t mh = P.mh, ldp = P.ldp, ov = P.out_valid;
+  const int64_t i0 = (int64_t)ti * 64, j0 = (int64_t)tj * 64;
+  const int cx = tx * 8;
+  const ModP &m = P.mod;
+  auto buf = [&](int b) { return static_cast<const InT *>(P.B[b]); };
+  // ---------------- phase 1: U1, U3 on L (U1 kept in S0 / S1 for the rest of the block)
+  {
+    Pk8<InT> g1[2], g5[2], g2[2], h1[2], h5[2], h2[2], h1u[2], h5u[2], h2u[2];
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) {
+      const int y = ty + 32 * rr;
+      const int64_t oL = (i0 + y) * ldp + j0 + cx, oU = (j0 + y) * ldp + i0 + cx;
+      h1u[rr].load(buf(HB_H1) + oU); h5u[rr].load(buf(HB_H5) + oU); h2u[rr].load(buf(HB_H2) + oU);
+      g1[rr].load(buf(HB_G1) + oL); g5[rr].load(buf(HB_G5) + oL); g2[rr].load(buf(HB_G2) + oL);
+      h1[rr].load(buf(HB_H1) + oL); h5[rr].load(buf(HB_H5) + oL); h2[rr].load(buf(HB_H2) + oL);
+    }
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) {
+      const int y = ty + 32 * rr;
+      uint32_t a[8], b[8], c[8];
+      h1u[rr].get(a); h5u[rr].get(b); h2u[rr].get(c);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) { S0[y][cx + e] = addmod(a[e], b[e], m); S1[y][cx + e] = addmod(a[e], c[e], m); }
+    }
+    __syncthreads();
+    uint32_t u1r[2][8], u1i[2][8];
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) {
+      const int y = ty + 32 * rr;
+      const int64_t i = i0 + y, j = j0 + cx;
+      uint32_t G1[8], G5[8], G2[8], H1[8], H5[8], H2[8], c11r[8], c11i[8];
+      g1[rr].get(G1); g5[rr].get(G5); g2[rr].get(G2); h1[rr].get(H1); h5[rr].get(H5); h2[rr].get(H2);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const uint32_t t15 = S0[cx + e][y], t12 = S1[cx + e][y];     // (H1 + H5)(j, i), (H1 + H2)(j, i)
+        const uint32_t h15 = addmod(H1[e], H5[e], m), h12 = addmod(H1[e], H2[e], m);
+        u1r[rr][e] = submod(submod(addmod(G1[e], G5[e], m), h15, m), t15, m);   // Re U1 = G1 + G5 - H15 - H15^T
+        u1i[rr][e] = submod(t15, h15, m);                                         // Im U1 = H15^T - H15
+        c11r[e] = submod(submod(addmod(G1[e], G2[e], m), h12, m), t12, m);      // U3 = P1 + P2
+        c11i[e] = submod(t12, h12, m);
+      }
+      if (i < mh && j <= i && i < ov) store_c8(P.C + 2 * (i * P.ldc + j), min64(8, min64(i - j + 1, ov - j)), c11r, c11i, P);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) { S0[ty + 32 * rr][cx + e] = u1r[rr][e]; S1[ty + 32 * rr][cx + e] = u1i[rr][e]; }
+  }
+  // ---------------- phase 2a: P4 on U -> S2 / S3
+  {
+    Pk8<InT> b1u[2], b2u[2], b3u[2];
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) {
+      const int64_t oU = (j0 + ty + 32 * rr) * ldp + i0 + cx;
+      b1u[rr].load(buf(HB_B1) + oU); b2u[rr].load(buf(HB_B2) + oU); b3u[rr].load(buf(HB_B3) + oU);
+    }
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) {
+      const int y = ty + 32 * rr;
+      uint32_t t1[8], t2[8], t3[8];
+      b1u[rr].get(t1); b2u[rr].get(t2); b3u[rr].get(t3);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        S2[y][cx + e] = addmod(t1[e], t2[e], m);                             // Re P4 = t1 + t2
+        S3[y][cx + e] = addmod(submod(t3[e], t1[e], m), t2[e], m);           // Im P4 = t3 - t1 + t2
+      }
+    }
+  }
+  __syncthreads();
+  // ---------------- phase 2b: tile L
+  {
+    Pk8<InT> a1[2], a2[2], a3[2], b1[2], b2[2], b3[2];
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) {
+      const int64_t oL = (i0 + ty + 32 * rr) * ldp + j0 + cx;
+      b1[rr].load(buf(HB_B1) + oL); b2[rr].load(buf(HB_B2) + oL); b3[rr].load(buf(HB_B3) + oL);
+      a1[rr].load(buf(HB_A1) + oL); a2[rr].load(buf(HB_A2) + oL); a3[rr].load(buf(HB_A3) + oL);
+    }
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) {
+      const int y = ty + 32 * rr;
+      const int64_t i = i0 + y, j = j0 + cx;
+      if (i >= mh || j >= mh || mh + i >= ov) continue;
+      uint32_t t1[8], t2[8], t3[8], q1[8], q2[8], q3[8], cr[8], ci[8], dr[8], di[8];
+      b1[rr].get(t1); b2[rr].get(t2); b3[rr].get(t3);
+      a1[rr].get(q1); a2[rr].get(q2); a3[rr].get(q3);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const bool low = j + e <= i;
+        const uint32_t ur = low ? S0[y][cx + e] : S0[cx + e][y];                    // Up(U1) = conj(Low(U1))^T
+        const uint32_t ui = low ? S1[y][cx + e] : submod(0u, S1[cx + e][y], m);
+        const uint32_t p4r = addmod(t1[e], t2[e], m), p4i = addmod(submod(t3[e], t1[e], m), t2[e], m);
+        const uint32_t p3r = addmod(q1[e], q2[e], m), p3i = addmod(submod(q3[e], q1[e], m), q2[e], m);
+        const uint32_t u2r = addmod(ur, p4r, m), u2i = addmod(ui, p4i, m);           // U2 = U1 + P4
+        cr[e] = addmod(u2r, p3r, m); ci[e] = addmod(u2i, p3i, m);                     // U4 = U2 + P3
+        dr[e] = addmod(u2r, S2[cx + e][y], m);                                       // U5 = U2 + conj(P4)^T
+        di[e] = submod(u2i, S3[cx + e][y], m);
+      }
+      store_c8(P.C + 2 * ((mh + i) * P.ldc + j), min64(8, mh - j), cr, ci, P);                          // C21
+      if (j <= i) store_c8(P.C + 2 * ((mh + i) * P.ldc + mh + j), min64(8, min64(i - j + 1, ov - mh - j)), dr, di, P);  // C22
+    }
+  }
+  if (diag) return;
+  // ---------------- phase 2c: tile U = (tj, ti): rows j0.., cols i0..
+  {
+    Pk8<InT> a1u[2], a2u[2], a3u[2];
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) {
+      const int64_t oU = (j0 + ty + 32 * rr) * ldp + i0 + cx;
+      a1u[rr].load(buf(HB_A1) + oU); a2u[rr].load(buf(HB_A2) + oU); a3u[rr].load(buf(HB_A3) + oU);
+    }
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) {
+      const int y = ty + 32 * rr;
+      const int64_t r = j0 + y, c = i0 + cx;
+      if (r >= mh || c >= mh || mh + r >= ov) continue;
+      uint32_t q1[8], q2[8], q3[8], cr[8], ci[8];
+      a1u[rr].get(q1); a2u[rr].get(q2); a3u[rr].get(q3);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const uint32_t ur = S0[cx + e][y], ui = submod(0u, S1[cx + e][y], m);       // conj(U1(c, r))
+        const uint32_t p3r = addmod(q1[e], q2[e], m), p3i = addmod(submod(q3[e], q1[e], m), q2[e], m);
+        cr[e] = addmod(addmod(ur, S2[y][cx + e], m), p3r, m);
+        ci[e] = addmod(addmod(ui, S3[y][cx + e], m), p3i, m);
+      }
+      store_c8(P.C + 2 * ((mh + r) * P.ldc + c), min64(8, mh - c), cr, ci, P);
+    }
+  }
+}
+
+cudaError_t launch_herk_combine(const HerkCombParams &p, cudaStream_t s) {
+  if (p.mh == 0) return cudaSuccess;
+  const unsigned nt = (unsigned)((p.mh + 63) / 64);
+  const dim3 grid(nt * (nt + 1) / 2);
+  const int smem = 4 * 64 * 65 * 4;
+  if (p.in32) {
+    static bool set32 = false;
+    if (!set32) {
+      cudaError_t e = cudaFuncSetAttribute(herk_combine_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e != cudaSuccess) return e;
+      set32 = true;
+    }
+    herk_combine_kernel<uint32_t><<<grid, 256, smem, s>>>(p);
+  } else {
+    static bool set16 = false;
+    if (!set16) {
+      cudaError_t e = cudaFuncSetAttribute(herk_combine_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e != cudaSuccess) return e;
+      set16 = true;
+    }
+    herk_combine_kernel<uint16_t><<<grid, 256, smem, s>>>(p);
+  }
+  return cudaGetLastError();
+}
+
 // ============================================================================ K5 2M combine
 // Re = G - eps H - phi(H) with eps = i phi(i) = 1, Im: H phi(i) + i phi(H) = i (H^T - H);
 // G lower (u16, ldg), H full (u16, ldh); C interleaved (re, im) uint32 pairs, Low only.

@@ -292,6 +292,54 @@ bool build_syrk_plan(Plan &P, int64_t m, int64_t k, uint32_t p, int phi, int dep
   return true;
 }
 
+bool build_herk1_plan(Plan &P, int64_t m, int64_t k, uint32_t p, int num_sms, const char **err) {
+  P = Plan();
+  P.kind = PLAN_HERK1;
+  P.m = m; P.n = m; P.k = k; P.depth = 1;
+  fill_scheme(P, p);
+  P.lv.resize(2);
+  P.lv[0].mh = m; P.lv[0].kh = k;
+  P.lv[0].rows_pad = rup(std::max<int64_t>(m, 1), kBM);
+  P.lv[0].kpad = std::max<int64_t>(kBK, rup(k, kBK));
+  LevelPlan &L = P.lv[1];
+  L.mh = cdiv(m, 2);
+  L.kh = 8 * cdiv(k, 16);
+  L.rows_pad = rup(L.mh, kBM);
+  L.kpad = std::max<int64_t>(kBK, rup(L.kh, kBK));
+  L.n_nodes = 1;
+  L.n_ops = HO_N;
+  P.rows_pad0 = P.lv[0].rows_pad;
+  P.kpad0 = P.lv[0].kpad;
+  if (L.rows_pad >= (int64_t)4096 * P.tile_m) { *err = "m too large"; return false; }
+  size_t off = 0;
+  ArenaPlan a;
+  a.kpad = L.kpad;
+  a.n_rows = (int64_t)HO_N * P.planes * L.rows_pad;
+  a.offset = 0;
+  off = (size_t)rup((int64_t)a.bytes(), 256);
+  L.arena = 0;
+  P.arenas.push_back(a);
+  P.hb_bytes = (size_t)rup(L.rows_pad * L.rows_pad * P.res_bytes(), 256);
+  P.hb_offset = off;
+  off += P.hb_bytes * HB_N;
+  L.p_offset = P.hb_offset;     // pbuf(P, ws, 1, 0, idx) addresses product buffer idx
+  L.p_buf_bytes = P.hb_bytes;
+  P.ws_bytes = off;
+  const int64_t rp = L.rows_pad;
+  auto row = [&](int o) { return (int64_t)o * P.planes * rp; };
+  struct Q { int a, b; bool sym; int buf; };
+  const Q qs[HB_N] = {{HO_T11, HO_T11, true, HB_G1}, {HO_X11, HO_Y11, false, HB_H1},
+                      {HO_T12, HO_T12, true, HB_G2}, {HO_X12, HO_Y12, false, HB_H2},
+                      {HO_T3, HO_T3, true, HB_G5},   {HO_X3, HO_Y3, false, HB_H5},
+                      {HO_X22, HO_X4, false, HB_A1}, {HO_Y22, HO_Y4, false, HB_A2}, {HO_Z22, HO_W4, false, HB_A3},
+                      {HO_X1, HO_X2, false, HB_B1},  {HO_Y1, HO_Y2, false, HB_B2},  {HO_Z1, HO_W2, false, HB_B3}};
+  for (const Q &q : qs)
+    P.prods.push_back(make_prod(P, 0, row(q.a), row(q.b), rp, rp, L.kpad, q.sym, OUT_PBUF, 1, 0, q.buf, rp, rp, false, rp));
+  append_tiles(P);
+  set_grid(P, num_sms);
+  return true;
+}
+
 bool build_gemm_plan(Plan &P, int64_t m, int64_t n, int64_t k, uint32_t p, int num_sms, const char **err) {
   P = Plan();
   P.kind = PLAN_GEMM;

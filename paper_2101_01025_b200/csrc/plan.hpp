@@ -13,7 +13,8 @@
 
 namespace adj {
 
-enum PlanKind : int { PLAN_SYRK_T = 0, PLAN_SYRK_H = 1, PLAN_GEMM = 2 };
+enum PlanKind : int { PLAN_SYRK_T = 0, PLAN_SYRK_H = 1, PLAN_GEMM = 2, PLAN_HERK1 = 3 };
+
 
 struct ArenaPlan {
   int64_t kpad = 0;      // bytes per row (K padded to 128)
@@ -59,6 +60,7 @@ struct Plan {
   int64_t rows_pad0 = 0, kpad0 = 0, rows_pad_b = 0;
   int64_t op0_row[3] = {-1, -1, -1};  // SYRK_T d=0: A; SYRK_H: X, Y, (T if d==0); GEMM: A, B
   size_t h_offset = 0, g_offset = 0;  // 2M buffers H, G (uint16 rows_pad0^2)
+  size_t hb_offset = 0, hb_bytes = 0; // PLAN_HERK1: HB_N product buffers of lv[1].rows_pad^2 residues
   size_t ws_bytes = 0;
   std::vector<ProductPlan> prods;
   std::vector<uint32_t> tiles;       // 2 words per leaf job (LeafParams::tiles)
@@ -76,6 +78,7 @@ struct Plan {
 bool build_syrk_plan(Plan &P, int64_t m, int64_t k, uint32_t p, int phi, int depth, int num_sms,
                      const char **err);
 bool build_gemm_plan(Plan &P, int64_t m, int64_t n, int64_t k, uint32_t p, int num_sms, const char **err);
+bool build_herk1_plan(Plan &P, int64_t m, int64_t k, uint32_t p, int num_sms, const char **err);
 int auto_depth(int64_t m, int64_t k, uint32_t p, int phi);
 
 }  // namespace adj

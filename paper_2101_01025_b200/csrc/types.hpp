@@ -134,4 +134,38 @@ struct CombParams {
   int32_t in32;            // P buffers hold uint32 residues (p > 2^16)
 };
 
+// ---------------------------------------------------------------- GF(p^2) Alg. 1 (PLAN_HERK1)
+// PLAN_HERK1: one level of Alg. alg:MIAHMM directly over GF(p^2) with Y = (a + ib) I (PAPER.md
+// §4.4, 741-758); its Hermitian leaves P1, P2, P5 by 2M (G = T T^T, H = X Y^T) and its general
+// leaves P3, P4 by 3M (t1 = Xr Yr^T, t2 = Xi Yi^T, t3 = (Xr + Xi)(Yr - Yi)^T).  Operands (one
+// arena, in this order) and product buffers:
+enum HerkOp : int {
+  HO_T11 = 0, HO_X11, HO_Y11, HO_T12, HO_X12, HO_Y12, HO_T3, HO_X3, HO_Y3,   // A11, A12, S3: T = re + im, X = re, Y = im
+  HO_X22, HO_Y22, HO_Z22, HO_X4, HO_Y4, HO_W4,                              // A22 (Z = re + im), S4 (W = re - im)
+  HO_X1, HO_Y1, HO_Z1, HO_X2, HO_Y2, HO_W2,                                 // S1 (Z), S2 (W)
+  HO_N
+};
+enum HerkBuf : int { HB_G1 = 0, HB_H1, HB_G2, HB_H2, HB_G5, HB_H5, HB_A1, HB_A2, HB_A3, HB_B1, HB_B2, HB_B3, HB_N };
+// K1 over GF(p^2): S1 = y (A21 - A11), S2 = A22 - y A21, S3 = S1 - A22, S4 = S3 + A12 with the
+// scalar y = ya + i yb (Y = y I, y conj(y) = -1), written as the 21 HerkOp limb operands.
+struct HerkPreParams {
+  InView in;               // A, IN_PAIR_RE type (interleaved (re, im) uint32 pairs), m x k valid
+  int64_t mh, kh;          // half sizes (A is zero padded to 2 mh x 2 kh)
+  int64_t rows_pad, kpad;
+  int8_t *arena;
+  int32_t scheme, planes;
+  uint32_t ya, yb;
+  ModP mod;
+};
+// K4 over GF(p^2) fused with the 2M / 3M leaf combinations (HerkBuf order in B[]).
+struct HerkCombParams {
+  const void *B[12];       // rows_pad x rows_pad residue buffers (u16, or u32 if in32), ld = ldp
+  int64_t mh, ldp;
+  uint32_t *C;             // interleaved (re, im) pairs, ldc in pairs
+  int64_t ldc, out_valid;
+  ModP mod;
+  uint32_t alpha, beta;
+  int32_t axpby, in32;
+};
+
 }  // namespace adj

@@ -99,3 +99,18 @@ def test_workspace_and_depth_planning():
     assert w2 > 0
     # k above the int32 bound of the limb scheme is handled by K segmentation (no error)
     assert tail(adj.adjprod_modp_workspace_size(256, 40000, 65521, 0, depth=0), 2 * 256 * 40064)
+
+
+def test_herk_alg1_workspace_planning():
+    """ADJ_HERK_ALG1: 21 limb operands of (m/2) x (k/2) plus 12 product
+    buffers of (m/2)^2 residues; depth other than 1 is refused synchronously (no GPU needed)."""
+    m, k, p = 8192, 8192, 8191
+    w = adj.adjprod_modp_workspace_size(m, k, p, 1, depth=-1, flags=adj.ADJ_HERK_ALG1)
+    arena = 21 * 3 * 4096 * 4096
+    bufs = 12 * 4096 * 4096 * 2
+    assert arena + bufs <= w <= arena + bufs + 64 * 65536 * 2 * 64 + 4096
+    with pytest.raises(adj.AdjError):
+        adj.adjprod_modp_workspace_size(m, k, p, 1, depth=2, flags=adj.ADJ_HERK_ALG1)
+    # ignored for phi = T
+    assert adj.adjprod_modp_workspace_size(m, k, p, 0, depth=1, flags=adj.ADJ_HERK_ALG1) == \
+        adj.adjprod_modp_workspace_size(m, k, p, 0, depth=1)

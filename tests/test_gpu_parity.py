@@ -228,3 +228,66 @@ def test_syrk_form_k0_and_gemm_unaffected(adj):
     ref = C0.copy()
     ref[np.tril_indices(5)] = (3 * (C0[np.tril_indices(5)].astype(np.int64) % p)) % p
     assert np.array_equal(to_host(dC), ref)
+
+
+# ---------------------------------------------------------------- SURVEY.md §8(f)-2
+# phi = H by one level of Alg. alg:MIAHMM directly over GF(p^2), Y = (a + ib) I (PAPER.md
+# §4.4, 750-758), 2M Hermitian leaves and 3M general leaves (ADJ_HERK_ALG1): the same Low(C).
+HERK_PRIMES = [3, 7, 251, 8191, 16763, 65519, 131071]
+
+
+@pytest.mark.parametrize("p", HERK_PRIMES)
+@pytest.mark.parametrize("m,k", [(1, 1), (2, 2), (33, 17), (129, 200), (260, 300), (700, 513)])
+def test_herk_alg1_vs_oracle(adj, p, m, k):
+    A = uniform_matrix_ext(m, k, seed=m * 7 + k, p=p)
+    C = adj.adjprod(to_dev(A), p, phi="H", herk="alg1")
+    assert np.array_equal(to_host(C), oracle.syrk_h(A, p))
+
+
+def test_herk_alg1_fill_upper_and_untouched(adj):
+    import torch
+    p, m, k = 8191, 300, 260
+    A = uniform_matrix_ext(m, k, seed=9, p=p)
+    C = torch.full((m, m, 2), -1, dtype=torch.int32, device="cuda")
+    adj.adjprod(to_dev(A), p, phi="H", herk="alg1", out=C)
+    got = to_host(C)
+    ref = oracle.syrk_h(A, p)
+    lo = np.tril(np.ones((m, m), dtype=bool))
+    assert np.array_equal(got[lo], ref[lo])
+    assert (got[~lo] == 0xFFFFFFFF).all()
+    F = to_host(adj.adjprod(to_dev(A), p, phi="H", herk="alg1", fill_upper=True))
+    assert np.array_equal(F[..., 0], F[..., 0].T)
+    assert np.array_equal(F[..., 1], (p - F[..., 1].T.astype(np.int64)) % p)
+    assert np.array_equal(F[lo], ref[lo])
+
+
+@pytest.mark.parametrize("alpha,beta", [(1, 0), (0, 1), (3, 5), (8190, 8190)])
+def test_herk_alg1_syrk_form(adj, alpha, beta):
+    p, m, k = 8191, 300, 260
+    A = uniform_matrix_ext(m, k, seed=5, p=p)
+    rng = np.random.default_rng(alpha + 7 * beta)
+    C0 = rng.integers(0, 2**32, size=(m, m, 2), dtype=np.uint64).astype(np.uint32)
+    dC = to_dev(C0)
+    adj.adjprod_modp_syrk(m, k, p, 1, alpha, to_dev(A), k, beta, dC, m, flags=adj.ADJ_HERK_ALG1)
+    assert np.array_equal(to_host(dC), oracle.syrk_update(A, C0, p, alpha, beta, "H"))
+
+
+def test_herk_alg1_strided_and_noncanonical(adj):
+    import torch
+    p, m, k, lda, ldc = 8191, 150, 333, 341, 157
+    rng = np.random.default_rng(3)
+    full = rng.integers(0, 2**32, size=(m, lda, 2), dtype=np.uint64).astype(np.uint32)
+    C = torch.zeros((m, ldc, 2), dtype=torch.int32, device="cuda")
+    adj.adjprod_modp_ex(m, k, p, 1, to_dev(full), lda, C, ldc, flags=adj.ADJ_HERK_ALG1)
+    got = to_host(C)[:, :m]
+    ref = oracle.syrk_h(full[:, :k] % p, p)
+    lo = np.tril(np.ones((m, m), dtype=bool))
+    assert np.array_equal(got[lo], ref[lo])
+
+
+def test_herk_alg1_depth_must_be_one(adj):
+    import torch
+    A = torch.zeros((8, 8, 2), dtype=torch.int32, device="cuda")
+    C = torch.zeros((8, 8, 2), dtype=torch.int32, device="cuda")
+    with pytest.raises(adj.AdjError):
+        adj.adjprod_modp_ex(8, 8, 8191, 1, A, 8, C, 8, depth=2, flags=adj.ADJ_HERK_ALG1)
