@@ -150,3 +150,63 @@ def alg2m(X, Yim, p, syrk=None):
     # H phi(i) + i phi(H) = H (-i) + i H^T = i (H^T - H)
     im = (_T(H) - H) % p
     return low(re), low(im)
+
+
+# ----------------------------------------------------------------------------- GF(p^2) Alg. 1
+def _cmul_conjT(Xr, Xi, Yr, Yi, p):
+    """X phi(Y) = X Y^H over GF(p)[i]/(i^2+1) by definition: (Xr + i Xi)(Yr^T - i Yi^T)."""
+    re = (Xr @ _T(Yr) + Xi @ _T(Yi)) % p
+    im = (Xi @ _T(Yr) - Xr @ _T(Yi)) % p
+    return re, im
+
+
+def alg1_herk(X, Yim, p, y, depth: int = 1):
+    """Alg. alg:MIAHMM directly over E = GF(p)[i]/(i^2+1), p = 3 mod 4, with
+    phi = conjugate transpose and the skew-unitary Y = (a + ib) I, a^2 + b^2 = -1 (PAPER.md
+    §4.4, 750-758: conj(a + ib) = a - ib, so Y Y^H = (a^2 + b^2) I = -I).  A = X + i Yim.
+    Returns (Re, Im) of Low(A A^H); recursion on P1, P2, P5 down to `depth` levels, the
+    recursion leaves and P3, P4 by definition."""
+    a, b = y
+    Xr = np.asarray(X, dtype=np.int64) % p
+    Xi = np.asarray(Yim, dtype=np.int64) % p
+    m, n = Xr.shape[-2:]
+    if depth == 0 or m < 2 or n < 2:
+        re, im = _cmul_conjT(Xr, Xi, Xr, Xi, p)
+        return low(re), low(im)
+    m2, n2 = m + (m % 2), n + (n % 2)
+    Xr, Xi = _pad(Xr, m2, n2), _pad(Xi, m2, n2)
+    h, q = m2 // 2, n2 // 2
+    blk = lambda Z: (Z[..., :h, :q], Z[..., :h, q:], Z[..., h:, :q], Z[..., h:, q:])
+    A11r, A12r, A21r, A22r = blk(Xr)
+    A11i, A12i, A21i, A22i = blk(Xi)
+
+    def ymul(Zr, Zi):   # Z Y = (a + ib) Z
+        return (a * Zr - b * Zi) % p, (b * Zr + a * Zi) % p
+
+    # 4 additions and 2 multiplications by Y
+    S1r, S1i = ymul((A21r - A11r) % p, (A21i - A11i) % p)
+    tr, ti = ymul(A21r, A21i)
+    S2r, S2i = (A22r - tr) % p, (A22i - ti) % p
+    S3r, S3i = (S1r - A22r) % p, (S1i - A22i) % p
+    S4r, S4i = (S3r + A12r) % p, (S3i + A12i) % p
+    # 3 recursive (P1, P2, P5) and 2 general products (P3, P4)
+    P1 = alg1_herk(A11r, A11i, p, y, depth - 1)
+    P2 = alg1_herk(A12r, A12i, p, y, depth - 1)
+    P3 = _cmul_conjT(A22r, A22i, S4r, S4i, p)     # A22 phi(S4)
+    P4 = _cmul_conjT(S1r, S1i, S2r, S2i, p)       # S1 phi(S2)
+    P5 = alg1_herk(S3r, S3i, p, y, depth - 1)
+    # 3 half additions and 2 complete additions
+    U1r, U1i = (P1[0] + P5[0]) % p, (P1[1] + P5[1]) % p      # Low(U1)
+    U3r, U3i = (P1[0] + P2[0]) % p, (P1[1] + P2[1]) % p      # Low(U3)
+    eye = np.eye(h, dtype=np.int64)
+    U1r = (U1r + _T(U1r) - U1r * eye) % p                     # Up(U1) <- phi(Low(U1)) = conj(Low(U1))^T
+    U1i = (U1i - _T(U1i) - U1i * eye) % p
+    U2r, U2i = (U1r + P4[0]) % p, (U1i + P4[1]) % p
+    U4r, U4i = (U2r + P3[0]) % p, (U2i + P3[1]) % p
+    U5r, U5i = low((U2r + _T(P4[0])) % p), low((U2i - _T(P4[1])) % p)   # Low(U2) + Low(phi(P4))
+    re = np.zeros(Xr.shape[:-2] + (m2, m2), dtype=np.int64)
+    im = np.zeros_like(re)
+    re[..., :h, :h], im[..., :h, :h] = low(U3r), low(U3i)
+    re[..., h:, :h], im[..., h:, :h] = U4r, U4i
+    re[..., h:, h:], im[..., h:, h:] = U5r, U5i
+    return re[..., :m, :m], im[..., :m, :m]

@@ -163,3 +163,39 @@ def test_2m_exhaustive_gf3():
     re, im = A1.alg2m(X, Y, p)
     dre, dim = A1.herk_def(X, Y, p)
     assert np.array_equal(re, dre) and np.array_equal(im, dim)
+
+
+# ---------------------------------------------------------------- Alg. 1 over GF(p^2)
+def _sos_minus1(p):
+    a, b = F.sos(p - 1, p)
+    assert (a * a + b * b) % p == p - 1
+    return a, b
+
+
+def test_alg1_herk_exhaustive_gf9():
+    """Every 2x2 matrix over GF(9) = GF(3)[i]/(i^2+1): one level of Alg. 1 with Y = (a+ib) I,
+    a^2 + b^2 = -1 (§4.4), equals the definition (X+iY)(X+iY)^H."""
+    p = 3
+    allm = _all_matrices(p, 2, 4)
+    X, Y = allm[:, :, :2], allm[:, :, 2:]
+    re, im = A1.alg1_herk(X, Y, p, _sos_minus1(p), 1)
+    dre, dim = A1.herk_def(X, Y, p)
+    assert np.array_equal(re, dre) and np.array_equal(im, dim)
+
+
+@pytest.mark.parametrize("p", [7, 11, 8191, 131071])
+@pytest.mark.parametrize("depth", [1, 2])
+def test_alg1_herk_vs_definition_and_o1(p, depth):
+    A = uniform_matrix_ext(23, 18, seed=p + depth, p=p)
+    re, im = A1.alg1_herk(A[..., 0], A[..., 1], p, _sos_minus1(p), depth)
+    O = oracle.syrk_h(A, p)
+    assert np.array_equal(re.astype(np.uint32), O[..., 0]) and np.array_equal(im.astype(np.uint32), O[..., 1])
+
+
+def test_alg1_herk_non_skew_unitary_breaks():
+    """Negative control: y with y conj(y) != -1 gives a wrong product (the pin can fail)."""
+    p = 8191
+    A = uniform_matrix_ext(10, 8, seed=3, p=p)
+    dre, dim = A1.herk_def(A[..., 0], A[..., 1], p)
+    re, im = A1.alg1_herk(A[..., 0], A[..., 1], p, (1, 1), 1)    # 1 + 1 = 2 != -1
+    assert not (np.array_equal(re, dre) and np.array_equal(im, dim))
