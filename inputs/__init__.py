@@ -20,9 +20,9 @@ The same generator exists on the GPU (``inputs/gen.cu`` -> ``inputs/_gen.so``)
 so that multi-GiB inputs can be made in HBM; tests check both agree bit for bit.
 """
 from .gen import (splitmix64, mulhi64, uniform_residues, uniform_matrix,
-                  uniform_matrix_ext, vandermonde_points, vandermonde_matrix,
+                  uniform_matrix_ext, uniform_matrix_quat, vandermonde_points, vandermonde_matrix,
                   constant_matrix)
 
 __all__ = ["splitmix64", "mulhi64", "uniform_residues", "uniform_matrix",
-           "uniform_matrix_ext", "vandermonde_points", "vandermonde_matrix",
+           "uniform_matrix_ext", "uniform_matrix_quat", "vandermonde_points", "vandermonde_matrix",
            "constant_matrix"]

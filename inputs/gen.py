@@ -61,6 +61,12 @@ def uniform_matrix_ext(m: int, k: int, seed: int, p: int) -> np.ndarray:
     return uniform_residues(2 * m * k, seed, p).reshape(m, k, 2)
 
 
+def uniform_matrix_quat(m: int, k: int, seed: int, p: int) -> np.ndarray:
+    """m x k x 4 uint32 array: a quaternion matrix over GF(p) as interleaved (x1, x2, x3, x4)
+    = x1 + x2 i + x3 j + x4 k (flat index 4 (i k + t) + c)."""
+    return uniform_residues(4 * m * k, seed, p).reshape(m, k, 4)
+
+
 def vandermonde_points(m: int, seed: int, p: int) -> np.ndarray:
     """m seeded evaluation points x_i in [1, p)."""
     return (uniform_residues(m, seed ^ 0x5A5A5A5A, p - 1) + 1).astype(np.uint32)

@@ -10,7 +10,8 @@ arithmetic).
 
 Contents
 - oracle.c / liboracle.so (O1): classical Low(A phi(A)) mod p in uint64, OpenMP over rows:
-  phi = transpose over GF(p), phi = conjugate transpose over GF(p)[i]/(i^2+1), and A B^T.
+  phi = transpose over GF(p), phi = conjugate transpose over GF(p)[i]/(i^2+1) and over the
+  quaternions H_GF(p) (§6.2), and A B^T.
   Definition: Lemma lem:transp; Low.
 - field.py: Legendre, Tonelli-Shanks, Alg. alg:sosmodp (PAPER.md:659-675), Prop. lem:lemsqrt.
 - alg1.py (O2): Alg. alg:MIAHMM (PAPER.md:293-325) and Alg. alg:2M (PAPER.md:1437-1447)
@@ -53,7 +54,8 @@ def _lib():
         lib.oracle_syrk_t_rows.argtypes = [i64, i64, u32, vp, i64, vp, i64, i64, i64]
         lib.oracle_syrk_h_rows.argtypes = [i64, i64, u32, vp, i64, vp, i64, i64, i64]
         lib.oracle_gemm_nt.argtypes = [i64, i64, i64, u32, vp, i64, vp, i64, vp, i64]
-        for f in (lib.oracle_syrk_t_rows, lib.oracle_syrk_h_rows, lib.oracle_gemm_nt):
+        lib.oracle_syrk_q_rows.argtypes = [i64, i64, u32, vp, i64, vp, i64, i64, i64]
+        for f in (lib.oracle_syrk_t_rows, lib.oracle_syrk_h_rows, lib.oracle_gemm_nt, lib.oracle_syrk_q_rows):
             f.restype = ctypes.c_int
         lib.oracle_num_threads.restype = ctypes.c_int
         _LIB = lib
@@ -86,6 +88,19 @@ def syrk_h(A: np.ndarray, p: int, rows=None) -> np.ndarray:
     rc = _lib().oracle_syrk_h_rows(m, k, p, _ptr(A), k, _ptr(C), m, r0, r1)
     if rc:
         raise RuntimeError(f"oracle_syrk_h_rows rc={rc}")
+    return C
+
+
+def syrk_q(M: np.ndarray, p: int, rows=None) -> np.ndarray:
+    """Low(M M^H) over the quaternions H_GF(p) (§6.2); M: (m, k, 4) interleaved
+    (x1, x2, x3, x4) = x1 + x2 i + x3 j + x4 k; returns (m, m, 4)."""
+    M = np.ascontiguousarray(M, dtype=np.uint32)
+    m, k, _ = M.shape
+    C = np.zeros((m, m, 4), dtype=np.uint32)
+    r0, r1 = (0, m) if rows is None else rows
+    rc = _lib().oracle_syrk_q_rows(m, k, p, _ptr(M), k, _ptr(C), m, r0, r1)
+    if rc:
+        raise RuntimeError(f"oracle_syrk_q_rows rc={rc}")
     return C
 
 

@@ -210,3 +210,43 @@ def alg1_herk(X, Yim, p, y, depth: int = 1):
     re[..., h:, :h], im[..., h:, :h] = U4r, U4i
     re[..., h:, h:], im[..., h:, h:] = U5r, U5i
     return re[..., :m, :m], im[..., :m, :m]
+
+
+# ----------------------------------------------------------------------------- quaternions
+def quat_def(A, B, C, D, p):
+    """M M^H for M = A + B i + C j + D k over H_GF(p), by the expansion of PAPER.md:1925-1945:
+    H1 = AA^T + BB^T + CC^T + DD^T, H2 = (BA^T - AB^T) + (DC^T - CD^T),
+    H3 = (CA^T - AC^T) + (BD^T - DB^T), H4 = (DA^T - AD^T) + (CB^T - BC^T).  Returns Low of each."""
+    A, B, C, D = (np.asarray(Z, dtype=np.int64) % p for Z in (A, B, C, D))
+    mm = lambda X, Y: X @ _T(Y)
+    H1 = (mm(A, A) + mm(B, B) + mm(C, C) + mm(D, D)) % p
+    H2 = (mm(B, A) - mm(A, B) + mm(D, C) - mm(C, D)) % p
+    H3 = (mm(C, A) - mm(A, C) + mm(B, D) - mm(D, B)) % p
+    H4 = (mm(D, A) - mm(A, D) + mm(C, B) - mm(B, C)) % p
+    return low(H1), low(H2), low(H3), low(H4)
+
+
+def alg2m3m(A, B, C, D, p, syrk=None):
+    """Alg. alg:2M3M: M M^H for M = A + B i + C j + D k with 6
+    multiplications, one of them (Q6) a product of a matrix by its transpose (``syrk``, default
+    the definition; pass alg1 to run Q6 through Alg. alg:MIAHMM).  Returns Low(H1..H4)."""
+    A, B, C, D = (np.asarray(Z, dtype=np.int64) % p for Z in (A, B, C, D))
+    m = A.shape[-2]
+    U1 = (A + B) % p
+    U2 = (C + D) % p
+    Q1 = gemm_def(C, A, p)                                   # C A^T
+    Q2 = gemm_def(D, B, p)                                   # D B^T
+    Q3 = gemm_def(U2, U1, p)                                 # U2 U1^T
+    Q4 = gemm_def(A, B, p)                                   # A B^T
+    Q5 = gemm_def(C, D, p)                                   # C D^T
+    W = (U1 + U2) % p
+    Q6 = syrk_def(W, p) if syrk is None else syrk(W)         # (U1 + U2)(U1^T + U2^T), Low
+    Q6 = (Q6 + _T(Q6) - Q6 * np.eye(m, dtype=np.int64)) % p
+    T1 = (Q1 - Q2) % p
+    T2 = (Q4 + Q5) % p
+    T3 = (Q1 + Q2 - Q3) % p
+    H1 = low((Q6 - (_T(Q3) + Q3) - (_T(T2) + T2)) % p)
+    H2 = low((_T(T2) - T2) % p)
+    H3 = low((T1 - _T(T1)) % p)
+    H4 = low((_T(T3) - T3) % p)
+    return H1, H2, H3, H4

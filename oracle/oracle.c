@@ -16,6 +16,7 @@
  *     (Frobenius):
  *        Re C[i][j] = sum_t x_it x_jt + y_it y_jt                                mod p
  *        Im C[i][j] = sum_t y_it x_jt - x_it y_jt                                mod p
+ *   - phi = conjugate transpose over the quaternions H_GF(p) (§6.2): oracle_syrk_q_rows.
  *   - Low/Up: only i >= j is written (diagonal included).
  *   - A general product C = A B^T (the paper's A phi(B) over GF(p)) for gemm parity.
  *
@@ -129,6 +130,51 @@ int oracle_syrk_h_rows(int64_t m, int64_t k, uint32_t p, const uint32_t *A, int6
 int oracle_syrk_h(int64_t m, int64_t k, uint32_t p, const uint32_t *A, int64_t lda,
                   uint32_t *C, int64_t ldc) {
   return oracle_syrk_h_rows(m, k, p, A, lda, C, ldc, 0, m);
+}
+
+/* Low(M M^H) over the quaternions H_K, K = GF(p) (§6.2, ssec:quaternions, 1532-1560):
+ * q = x1 + x2 i + x3 j + x4 k with i^2 = j^2 = k^2 = ijk = -1, conj(q) = x1 - x2 i - x3 j - x4 k,
+ * (M M^H)_{ij} = sum_t M_it conj(M_jt) (Lemma lem:transp, the product taken in this order).
+ * With the multiplication table w1..w4 of PAPER.md:1553-1558 and y = conj(x'):
+ *   w1 = x1x1' + x2x2' + x3x3' + x4x4'
+ *   w2 = x2x1' - x1x2' + x4x3' - x3x4'
+ *   w3 = x3x1' - x1x3' + x2x4' - x4x2'
+ *   w4 = x4x1' - x1x4' + x3x2' - x2x3'
+ * M and C hold 4 interleaved u32 per element; ldm/ldc count quaternions.  Rows [r0, r1). */
+int oracle_syrk_q_rows(int64_t m, int64_t k, uint32_t p, const uint32_t *M, int64_t ldm,
+                       uint32_t *C, int64_t ldc, int64_t r0, int64_t r1) {
+  if (m < 0 || k < 0 || p < 2 || r0 < 0 || r1 > m) return 1;
+  const int big = p > 65536u;
+  uint32_t *R = reduced_copy(M, m, k, ldm, 4, p);
+  if (!R) return 2;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t i = r0; i < r1; i++) {
+    const uint32_t *qi = R + (size_t)i * k * 4;
+    for (int64_t j = 0; j <= i; j++) {
+      const uint32_t *qj = R + (size_t)j * k * 4;
+      uint64_t pos[4] = {0, 0, 0, 0}, neg[4] = {0, 0, 0, 0};
+      for (int64_t t = 0; t < k; t++) {
+        const uint64_t x1 = qi[4 * t], x2 = qi[4 * t + 1], x3 = qi[4 * t + 2], x4 = qi[4 * t + 3];
+        const uint64_t y1 = qj[4 * t], y2 = qj[4 * t + 1], y3 = qj[4 * t + 2], y4 = qj[4 * t + 3];
+        uint64_t pp[4][2] = {{x1 * y1 + x2 * y2, x3 * y3 + x4 * y4},
+                             {x2 * y1, x4 * y3}, {x3 * y1, x2 * y4}, {x4 * y1, x3 * y2}};
+        uint64_t nn[4][2] = {{0, 0}, {x1 * y2, x3 * y4}, {x1 * y3, x4 * y2}, {x1 * y4, x2 * y3}};
+        for (int c = 0; c < 4; c++) {
+          if (big) {
+            pos[c] += pp[c][0] % p + pp[c][1] % p;
+            neg[c] += nn[c][0] % p + nn[c][1] % p;
+          } else {
+            pos[c] += pp[c][0] + pp[c][1];
+            neg[c] += nn[c][0] + nn[c][1];
+          }
+        }
+      }
+      for (int c = 0; c < 4; c++)
+        ROWP(C, ldc * 4, i)[4 * j + c] = (uint32_t)((pos[c] % p + p - neg[c] % p) % p);
+    }
+  }
+  free(R);
+  return 0;
 }
 
 /* number of OpenMP threads the oracle runs with (for the cpu_baseline 'cores' field) */
