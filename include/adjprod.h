@@ -20,6 +20,9 @@
  * - GF(p^2) = GF(p)[i]/(i^2 + 1) (requires p = 3 mod 4 so that x^2+1 is irreducible);
  *   an element x + i y is stored as an interleaved (x, y) uint32 pair.  Conjugation is the
  *   Frobenius map x + iy -> x - iy.
+ * - Quaternions H_GF(p) (§6.2, 1532-1558): x1 + x2 i + x3 j + x4 k with
+ *   i^2 = j^2 = k^2 = ijk = -1, stored as 4 interleaved uint32 (x1, x2, x3, x4); conjugation
+ *   negates x2, x3, x4.  Leading dimensions count quaternions for phi = ADJ_PHI_Q.
  * - Low/Up: Low includes the diagonal.  Only Low(C) is written; the
  *   strict upper triangle of C is left untouched unless ADJ_FILL_UPPER is set, in which
  *   case Up(C) = phi(Low(C)) (Lemma lem:uplow).
@@ -53,7 +56,11 @@ typedef struct adj_comm_s *adj_comm_t;    /* opaque NCCL-backed communicator */
 
 typedef enum {
   ADJ_PHI_T = 0, /* phi = transpose over GF(p)               (Examples ex:antih) */
-  ADJ_PHI_H = 1  /* phi = conjugate transpose over GF(p^2)   (Examples ex:antih) */
+  ADJ_PHI_H = 1, /* phi = conjugate transpose over GF(p^2)   (Examples ex:antih) */
+  ADJ_PHI_Q = 2  /* phi = conjugate transpose over the quaternions H_GF(p), computed with
+                    Alg. alg:2M3M (6M): five general
+                    products and one product of a matrix by its transpose, Q6, which runs
+                    through Alg. alg:MIAHMM at the requested depth */
 } adj_phi_t;
 
 typedef enum {
@@ -90,7 +97,8 @@ typedef struct {
  *   m, k   : A is m x k (m output rows, k contracted columns); C is m x m.  m = 0 is a no-op;
  *            k = 0 writes Low(C) = 0.
  *   p      : odd prime, 3 <= p <= 262139 (phi = ADJ_PHI_H additionally needs p = 3 mod 4).
- *   phi    : ADJ_PHI_T (A, C uint32 residues) or ADJ_PHI_H (A, C interleaved (re, im) pairs).
+ *   phi    : ADJ_PHI_T (A, C uint32 residues), ADJ_PHI_H (A, C interleaved (re, im) pairs)
+ *            or ADJ_PHI_Q (A, C interleaved quaternions (x1, x2, x3, x4)).
  *   A, lda : device, lda >= k.     C, ldc : device, ldc >= m.  A and C must not overlap.
  *   Uses default options (automatic depth, library-allocated workspace).
  */

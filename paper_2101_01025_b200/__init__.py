@@ -7,12 +7,12 @@ without an sm_100 GPU every call raises.
 """
 from __future__ import annotations
 
-from ._lib import (ADJ_FILL_UPPER, ADJ_HERK_ALG1, ADJ_PHI_H, ADJ_PHI_T, AdjError, adj_comm_destroy, adj_comm_get_unique_id,
+from ._lib import (ADJ_FILL_UPPER, ADJ_HERK_ALG1, ADJ_PHI_H, ADJ_PHI_Q, ADJ_PHI_T, AdjError, adj_comm_destroy, adj_comm_get_unique_id,
                    adj_comm_init, adj_launch_count, adj_launch_count_reset, adj_mod_lower, adj_profile_enable, adj_profile_read, adj_skew_unitary, adj_sos,
                    adj_dist_kslice, adjprod_modp, adjprod_modp_auto_depth, adjprod_modp_dist, adjprod_modp_ex, adjprod_modp_syrk,
                    adjprod_modp_workspace_size, gemm_modp, lib)
 
-__all__ = ["ADJ_PHI_T", "ADJ_PHI_H", "ADJ_FILL_UPPER", "ADJ_HERK_ALG1", "AdjError", "adjprod_modp", "adjprod_modp_ex", "adjprod_modp_syrk",
+__all__ = ["ADJ_PHI_T", "ADJ_PHI_H", "ADJ_PHI_Q", "ADJ_FILL_UPPER", "ADJ_HERK_ALG1", "AdjError", "adjprod_modp", "adjprod_modp_ex", "adjprod_modp_syrk",
            "adjprod_modp_workspace_size", "adjprod_modp_auto_depth", "gemm_modp", "adj_skew_unitary", "adj_sos",
            "adj_mod_lower", "adj_dist_kslice", "adj_comm_get_unique_id", "adj_comm_init", "adj_comm_destroy", "adjprod_modp_dist",
            "adj_launch_count", "adj_launch_count_reset", "adj_profile_enable", "adj_profile_read", "lib", "adjprod", "gemm"]
@@ -20,20 +20,22 @@ __all__ = ["ADJ_PHI_T", "ADJ_PHI_H", "ADJ_FILL_UPPER", "ADJ_HERK_ALG1", "AdjErro
 
 def adjprod(A, p: int, phi: str = "T", depth: int = -1, fill_upper: bool = False, out=None, workspace=None,
             stream=None, herk: str = "2m"):
-    """Low(A phi(A)) mod p for a CUDA int32/uint32 tensor A (m x k, or m x k x 2 for phi='H').
+    """Low(A phi(A)) mod p for a CUDA int32/uint32 tensor A (m x k; m x k x 2 for phi='H', GF(p^2);
+    m x k x 4 for phi='Q', quaternions over GF(p)).
 
     Returns an m x m (x 2) int32 tensor holding uint32 residues; its strict upper triangle is
     whatever `out` held (zeros for a fresh output) unless fill_upper.  For phi='H', herk='alg1'
     selects one level of Alg. alg:MIAHMM directly over GF(p^2) (ADJ_HERK_ALG1) instead of 2M."""
     import torch
     assert A.is_cuda and A.element_size() == 4
-    ph = ADJ_PHI_H if phi.upper() == "H" else ADJ_PHI_T
+    ph = {"T": ADJ_PHI_T, "H": ADJ_PHI_H, "Q": ADJ_PHI_Q}[phi.upper()]
+    w = {ADJ_PHI_T: 1, ADJ_PHI_H: 2, ADJ_PHI_Q: 4}[ph]
     m, k = A.shape[0], A.shape[1]
-    lda = A.stride(0) // (2 if ph == ADJ_PHI_H else 1)
+    lda = A.stride(0) // w
     if out is None:
-        shape = (m, m, 2) if ph == ADJ_PHI_H else (m, m)
+        shape = (m, m) if w == 1 else (m, m, w)
         out = torch.zeros(shape, dtype=torch.int32, device=A.device)
-    ldc = out.stride(0) // (2 if ph == ADJ_PHI_H else 1)
+    ldc = out.stride(0) // w
     nbytes = workspace.numel() * workspace.element_size() if workspace is not None else 0
     flags = (ADJ_FILL_UPPER if fill_upper else 0) | (ADJ_HERK_ALG1 if herk == "alg1" else 0)
     adjprod_modp_ex(m, k, p, ph, A, lda, out, ldc, depth=depth, flags=flags,

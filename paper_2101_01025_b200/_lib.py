@@ -13,6 +13,7 @@ LIB_PATH = os.path.join(_PKG, "libadjprod.so")
 
 ADJ_PHI_T = 0
 ADJ_PHI_H = 1
+ADJ_PHI_Q = 2
 ADJ_FILL_UPPER = 1
 ADJ_HERK_ALG1 = 2
 STATUS = {0: "ADJ_OK", 1: "ADJ_ERR_INVALID_VALUE", 2: "ADJ_ERR_UNSUPPORTED_MODULUS", 3: "ADJ_ERR_WORKSPACE",

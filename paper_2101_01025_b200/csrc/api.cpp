@@ -171,6 +171,10 @@ adj_status_t get_plan(Plan **out, int kind, int64_t m, int64_t n, int64_t k, uin
 
 // ------------------------------------------------------------------ validation helpers
 bool valid_modulus(uint32_t p) { return p >= 3 && p <= kMaxModulus && is_prime_u32(p); }
+}  // namespace
+// uint32 words per element: GF(p) 1, GF(p^2) 2, quaternions 4
+int adj_phi_width(adj_phi_t phi) { return phi == ADJ_PHI_H ? 2 : (phi == ADJ_PHI_Q ? 4 : 1); }
+namespace {
 
 bool overlap(const void *a, size_t abytes, const void *b, size_t bbytes) {
   uintptr_t a0 = (uintptr_t)a, a1 = a0 + abytes, b0 = (uintptr_t)b, b1 = b0 + bbytes;
@@ -201,7 +205,7 @@ InView child_view(const InView &pv, int c, const LevelPlan &Lp, void *s3, int64_
   if (c == 2) return make_view(s3, s3_ld, Lp.mh, Lp.kh, res32 ? IN_U32 : IN_U16);
   const int64_t rows = std::min(pv.rows_valid, Lp.mh);
   if (c == 0) return make_view(pv.ptr, pv.ld, rows, std::min(pv.cols_valid, Lp.kh), pv.type);
-  const int esz = pv.type == IN_U16 ? 2 : (pv.type == IN_U32 ? 4 : 8);
+  const int esz = pv.type == IN_U16 ? 2 : (pv.type == IN_U32 ? 4 : (pv.type == IN_QUAD_SUM ? 16 : 8));
   const void *ptr = static_cast<const uint8_t *>(pv.ptr) + (size_t)Lp.kh * esz;
   int64_t cols = std::max<int64_t>(0, std::min(pv.cols_valid - Lp.kh, Lp.kh));
   return make_view(ptr, pv.ld, rows, cols, pv.type);
@@ -243,6 +247,7 @@ adj_status_t launch_leaf_all(const Plan &P, const Ptrs &x, cudaStream_t s) {
       case OUT_PBUF: L.prod[q].out = pbuf(P, x.ws, pp.level, pp.node, pp.idx); break;
       case OUT_HBUF: L.prod[q].out = x.ws + P.h_offset; break;
       case OUT_GBUF: L.prod[q].out = x.ws + P.g_offset; break;
+      case OUT_QBUF: L.prod[q].out = x.ws + P.q_offset + (size_t)pp.idx * P.q_bytes; break;
       case OUT_C:
         L.prod[q].out = x.C;
         L.prod[q].ldo = x.ldc;
@@ -427,7 +432,48 @@ adj_status_t run_syrk(const Plan &P, const Ptrs &x, adj_phi_t phi, uint32_t flag
     LAUNCH_CLS(CLS_COMB, launch_twom(m, G, P.rows_pad0, H, P.rows_pad0, P.res32 ? 1 : 0, x.C, x.ldc, P.mod, x.alpha,
                                      x.beta, x.axpby, s));
   }
-  if (flags & ADJ_FILL_UPPER) LAUNCH(launch_fill_upper(m, phi == ADJ_PHI_H ? 2 : 1, x.C, x.ldc, P.mod, s));
+  if (flags & ADJ_FILL_UPPER) LAUNCH(launch_fill_upper(m, adj_phi_width(phi), x.C, x.ldc, P.mod, s));
+  return ADJ_OK;
+}
+
+// phi = Q: Alg. alg:2M3M.  One read of M gives the limb planes of A, B, C,
+// D, U1 = A + B, U2 = C + D (and W = U1 + U2 at depth 0); Q1..Q5 and Q6 = Low(W W^T) (through
+// Alg. alg:MIAHMM when depth >= 1, its root pre-addition reading W = x1 + x2 + x3 + x4 from M)
+// share one grouped leaf launch; the 6M combine forms H1..H4.
+adj_status_t run_quat(const Plan &P, const Ptrs &x, uint32_t flags, cudaStream_t s) {
+  const int64_t m = P.m, k = P.k;
+  SplitParams sp;
+  std::memset(&sp, 0, sizeof(sp));
+  sp.in = make_view(x.A, x.lda, m, k, IN_QUAD_SUM);
+  sp.rows = m; sp.cols = k;
+  sp.rows_pad = P.rows_pad0; sp.kpad = P.kpad0;
+  sp.arena = reinterpret_cast<int8_t *>(x.ws + P.arenas[0].offset);
+  sp.scheme = P.scheme; sp.planes = P.planes; sp.mode = 2; sp.mod = P.mod;
+  for (int o = 0; o < QO_N; ++o) sp.qrow[o] = P.q_row[o];
+  LAUNCH_CLS(CLS_PRE, launch_split(sp, s));
+  adj_status_t st;
+  void *G = x.ws + P.g_offset;
+  if (P.depth >= 1) {
+    st = run_tree(P, make_view(x.A, x.lda, m, k, IN_QUAD_SUM), x, s);
+    if (st) return st;
+  }
+  st = launch_leaf_all(P, x, s);
+  if (st) return st;
+  if (P.depth >= 1) {
+    st = run_combine(P, x, G, P.rows_pad0, false, s);
+    if (st) return st;
+  }
+  QuatCombParams qp;
+  std::memset(&qp, 0, sizeof(qp));
+  for (int q = 0; q < 5; ++q) qp.Q[q] = x.ws + P.q_offset + (size_t)q * P.q_bytes;
+  qp.Q[5] = G;
+  qp.m = m; qp.ldq = P.rows_pad0;
+  qp.C = x.C; qp.ldc = x.ldc;
+  qp.mod = P.mod;
+  qp.alpha = x.alpha; qp.beta = x.beta; qp.axpby = x.axpby;
+  qp.in32 = P.res32 ? 1 : 0;
+  LAUNCH_CLS(CLS_COMB, launch_quat_combine(qp, s));
+  if (flags & ADJ_FILL_UPPER) LAUNCH(launch_fill_upper(m, 4, x.C, x.ldc, P.mod, s));
   return ADJ_OK;
 }
 
@@ -463,7 +509,8 @@ adj_status_t run_herk1(const Plan &P, const Ptrs &x, uint32_t flags, cudaStream_
 adj_status_t validate_syrk(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, const uint32_t *A, int64_t lda,
                            const uint32_t *C, int64_t ldc) {
   if (m < 0 || k < 0) return fail(ADJ_ERR_INVALID_VALUE, "negative dimension (m=%lld, k=%lld)", (long long)m, (long long)k);
-  if (phi != ADJ_PHI_T && phi != ADJ_PHI_H) return fail(ADJ_ERR_INVALID_VALUE, "phi must be ADJ_PHI_T or ADJ_PHI_H");
+  if (phi != ADJ_PHI_T && phi != ADJ_PHI_H && phi != ADJ_PHI_Q)
+    return fail(ADJ_ERR_INVALID_VALUE, "phi must be ADJ_PHI_T, ADJ_PHI_H or ADJ_PHI_Q");
   if (!valid_modulus(p)) return fail(ADJ_ERR_UNSUPPORTED_MODULUS, "p=%u is not an odd prime in [3, 262139]", p);
   if (phi == ADJ_PHI_H && p % 4 != 3)
     return fail(ADJ_ERR_UNSUPPORTED_MODULUS, "phi=H needs p = 3 mod 4 (GF(p)[i]/(i^2+1)); p=%u", p);
@@ -472,7 +519,7 @@ adj_status_t validate_syrk(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, cons
   if (k > 0 && A == nullptr) return fail(ADJ_ERR_INVALID_VALUE, "A is null");
   if (lda < k || (lda < 1 && k > 0)) return fail(ADJ_ERR_INVALID_VALUE, "lda=%lld < k=%lld", (long long)lda, (long long)k);
   if (ldc < m) return fail(ADJ_ERR_INVALID_VALUE, "ldc=%lld < m=%lld", (long long)ldc, (long long)m);
-  const int w = phi == ADJ_PHI_H ? 2 : 1;
+  const int w = adj_phi_width(phi);
   if (overlap(A, span_bytes(m, k, lda, w), C, span_bytes(m, m, ldc, w)))
     return fail(ADJ_ERR_INVALID_VALUE, "A and C overlap");
   return ADJ_OK;
@@ -570,7 +617,7 @@ static adj_status_t adjprod_impl(int64_t m, int64_t k, uint32_t p, adj_phi_t phi
   if (st != ADJ_OK || m == 0) return st;
   int dev, sms;
   if ((st = check_device(&dev, &sms)) != ADJ_OK) return st;
-  const int w = phi == ADJ_PHI_H ? 2 : 1;
+  const int w = adj_phi_width(phi);
   const uint32_t flags = opts ? opts->flags : 0;
   alpha %= p;
   beta %= p;
@@ -589,7 +636,7 @@ static adj_status_t adjprod_impl(int64_t m, int64_t k, uint32_t p, adj_phi_t phi
   if (depth > 3) return fail(ADJ_ERR_INVALID_VALUE, "depth %d > 3 unsupported", depth);
   if (herk1 && depth != 1) return fail(ADJ_ERR_INVALID_VALUE, "ADJ_HERK_ALG1 runs exactly one level (depth 1 or -1)");
   Plan *P = nullptr;
-  const int kind = herk1 ? PLAN_HERK1 : (phi == ADJ_PHI_T ? PLAN_SYRK_T : PLAN_SYRK_H);
+  const int kind = herk1 ? PLAN_HERK1 : (phi == ADJ_PHI_T ? PLAN_SYRK_T : (phi == ADJ_PHI_H ? PLAN_SYRK_H : PLAN_QUAT));
   if ((st = get_plan(&P, kind, m, m, k, p, (int)phi, depth, dev, sms)) != ADJ_OK) return st;
   Ptrs x;
   x.A = A; x.lda = lda; x.C = C; x.ldc = ldc;
@@ -603,7 +650,7 @@ static adj_status_t adjprod_impl(int64_t m, int64_t k, uint32_t p, adj_phi_t phi
     return fail(ADJ_ERR_WORKSPACE, "workspace %zu bytes < required %zu", opts->workspace_bytes, P->ws_bytes);
   }
   x.ws = static_cast<uint8_t *>(ws);
-  st = herk1 ? run_herk1(*P, x, flags, s) : run_syrk(*P, x, phi, flags, s);
+  st = herk1 ? run_herk1(*P, x, flags, s) : (phi == ADJ_PHI_Q ? run_quat(*P, x, flags, s) : run_syrk(*P, x, phi, flags, s));
   if (own) {
     cudaError_t e = cudaFreeAsync(ws, s);
     if (st == ADJ_OK && e != cudaSuccess) return fail(ADJ_ERR_CUDA, "cudaFreeAsync: %s", cudaGetErrorString(e));
@@ -667,7 +714,7 @@ adj_status_t adj_mod_lower(int64_t m, uint32_t p, adj_phi_t phi, uint32_t *X, in
   if (m == 0) return ADJ_OK;
   if (!X) return fail(ADJ_ERR_INVALID_VALUE, "X is null");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  LAUNCH(launch_mod_lower(m, phi == ADJ_PHI_H ? 2 : 1, X, ldx, X, ldx, make_modp(p), s));
+  LAUNCH(launch_mod_lower(m, adj_phi_width(phi), X, ldx, X, ldx, make_modp(p), s));
   return ADJ_OK;
 }
 

@@ -56,6 +56,8 @@ bool load_nccl() {
 
 }  // namespace
 
+int adj_phi_width(adj_phi_t phi);   // api.cpp
+
 extern "C" {
 
 adj_status_t adj_comm_get_unique_id(uint8_t id[128]) {
@@ -102,7 +104,7 @@ adj_status_t adjprod_modp_dist(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, 
   if (m < 0 || k < 0) return ADJ_ERR_INVALID_VALUE;
   if (m == 0) return ADJ_OK;
   const int G = comm->nranks, r = comm->rank;
-  const int w = phi == ADJ_PHI_H ? 2 : 1;
+  const int w = adj_phi_width(phi);
   int64_t k0 = 0, k1 = 0;
   adj_dist_kslice(k, G, r, &k0, &k1);
   const uint32_t *Ar = A ? A + k0 * w : nullptr;

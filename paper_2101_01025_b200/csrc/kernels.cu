@@ -527,6 +527,15 @@ __device__ __forceinline__ void load4(const InView &v, int64_t R, int64_t C, con
 #pragma unroll
       for (int e = 0; e < 4; ++e) if (C + e < v.cols_valid) x[e] = __ldg(p + e);
     }
+  } else if (v.type == IN_QUAD_SUM) {
+    const uint32_t *p = static_cast<const uint32_t *>(v.ptr) + 4 * (R * v.ld + C);
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      if (C + e < v.cols_valid) {
+        uint4 q = all ? __ldg(reinterpret_cast<const uint4 *>(p) + e)
+                      : make_uint4(__ldg(p + 4 * e), __ldg(p + 4 * e + 1), __ldg(p + 4 * e + 2), __ldg(p + 4 * e + 3));
+        x[e] = addmod(addmod(mod_u32(q.x, m), mod_u32(q.y, m), m), addmod(mod_u32(q.z, m), mod_u32(q.w, m), m), m);
+      }
   } else {
     const uint32_t *p = static_cast<const uint32_t *>(v.ptr) + 2 * (R * v.ld + C);
     uint32_t re[4] = {0, 0, 0, 0}, im[4] = {0, 0, 0, 0};
@@ -698,6 +707,13 @@ __device__ __forceinline__ void load4_fast(const void *ptr, int64_t off, const M
   } else if constexpr (T == IN_U16) {
     uint2 q = __ldg(reinterpret_cast<const uint2 *>(static_cast<const uint16_t *>(ptr) + off));
     x[0] = q.x & 0xFFFF; x[1] = q.x >> 16; x[2] = q.y & 0xFFFF; x[3] = q.y >> 16;
+  } else if constexpr (T == IN_QUAD_SUM) {
+    const uint4 *p = reinterpret_cast<const uint4 *>(static_cast<const uint32_t *>(ptr) + 4 * off);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const uint4 q = __ldg(p + e);
+      x[e] = addmod(addmod(mod_u32(q.x, m), mod_u32(q.y, m), m), addmod(mod_u32(q.z, m), mod_u32(q.w, m), m), m);
+    }
   } else {
     const uint4 *p = reinterpret_cast<const uint4 *>(static_cast<const uint32_t *>(ptr) + 2 * off);
     uint4 a = __ldg(p), b = __ldg(p + 1);
@@ -906,6 +922,7 @@ __global__ void __launch_bounds__(256) preadd_kernel(const __grid_constant__ Pre
     const int64_t c = g * 4;
     if (type == IN_U32) preadd_row<SCHEME, YK, IN_U32>(P, N, r, c);
     else if (type == IN_U16) preadd_row<SCHEME, YK, IN_U16>(P, N, r, c);
+    else if (type == IN_QUAD_SUM) preadd_row<SCHEME, YK, IN_QUAD_SUM>(P, N, r, c);
     else preadd_row<SCHEME, YK, IN_PAIR_SUM>(P, N, r, c);
   }
 }
@@ -939,6 +956,47 @@ __global__ void __launch_bounds__(256) split_kernel(const __grid_constant__ Spli
     InView vv = v;
     if (r >= P.rows) vv.rows_valid = 0;
     const bool fast = vv.vec_ok && r < vv.rows_valid && c0 + 7 < vv.cols_valid && c0 + 7 < P.cols;
+    if (P.mode == 2) {
+      // quaternion M = A + B i + C j + D k: the operands of Alg. alg:2M3M
+      // A, B, C, D, U1 = A + B, U2 = C + D and (depth 0) W = U1 + U2, from one read of M
+      uint32_t q[2][4][4];   // [half][component][element]
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t c = c0 + 4 * h;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          uint4 w4 = make_uint4(0u, 0u, 0u, 0u);
+          if (r < vv.rows_valid && c + e < vv.cols_valid && c + e < P.cols) {
+            const uint32_t *src = static_cast<const uint32_t *>(v.ptr) + 4 * (r * v.ld + c + e);
+            w4 = vv.vec_ok ? __ldg(reinterpret_cast<const uint4 *>(src))
+                           : make_uint4(__ldg(src), __ldg(src + 1), __ldg(src + 2), __ldg(src + 3));
+          }
+          q[h][0][e] = mod_u32(w4.x, P.mod); q[h][1][e] = mod_u32(w4.y, P.mod);
+          q[h][2][e] = mod_u32(w4.z, P.mod); q[h][3][e] = mod_u32(w4.w, P.mod);
+        }
+      }
+#pragma unroll
+      for (int o = 0; o < 4; ++o)
+        put_limbs8<SCHEME>(P.arena + (P.qrow[o] + r) * P.kpad + c0, ps, q[0][o], q[1][o], P.mod);
+      uint32_t u1[2][4], u2[2][4];
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          u1[h][e] = addmod(q[h][0][e], q[h][1][e], P.mod);
+          u2[h][e] = addmod(q[h][2][e], q[h][3][e], P.mod);
+        }
+      put_limbs8<SCHEME>(P.arena + (P.qrow[4] + r) * P.kpad + c0, ps, u1[0], u1[1], P.mod);
+      put_limbs8<SCHEME>(P.arena + (P.qrow[5] + r) * P.kpad + c0, ps, u2[0], u2[1], P.mod);
+      if (P.qrow[6] >= 0) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) u1[h][e] = addmod(u1[h][e], u2[h][e], P.mod);
+        put_limbs8<SCHEME>(P.arena + (P.qrow[6] + r) * P.kpad + c0, ps, u1[0], u1[1], P.mod);
+      }
+      continue;
+    }
     if (P.mode == 1) {
       // 2M at depth 0: one read of the interleaved A gives X = Re, Y = Im and T = X + Y
       uint32_t re[2][4], im[2][4];
@@ -1433,6 +1491,126 @@ cudaError_t launch_herk_combine(const HerkCombParams &p, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// ============================================================================ quaternion 6M combine
+// Alg. alg:2M3M: T1 = Q1 - Q2, T2 = Q4 + Q5, T3 = (Q1 + Q2) - Q3,
+//   Low(H1) = Low(Q6 - (Q3^T + Q3) - (T2^T + T2)), Low(H2) = Low(T2^T - T2),
+//   Low(H3) = Low(T1 - T1^T), Low(H4) = Low(T3^T - T3);  C = H1 + H2 i + H3 j + H4 k.
+// One block per lower 64 x 64 tile L = (ti, tj); Q3, T1, T2, T3 of the mirrored tile U = (tj, ti)
+// are staged in shared memory (4 tiles of 64 x 65 words, dynamic) for the transposed terms.
+__device__ __forceinline__ void store_q8(uint32_t *o, int64_t n, uint32_t (&h)[4][8], const QuatCombParams &P) {
+  if (n <= 0) return;
+  if (P.axpby) {
+    for (int e = 0; e < n; ++e)
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        h[c][e] = addmod(mulmod_any(P.alpha, h[c][e], P.mod), mulmod_any(P.beta, mod_u32(o[4 * e + c], P.mod), P.mod), P.mod);
+  }
+  if (n == 8 && (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) reinterpret_cast<uint4 *>(o)[e] = make_uint4(h[0][e], h[1][e], h[2][e], h[3][e]);
+  } else {
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      if (e < n)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) o[4 * e + c] = h[c][e];
+  }
+}
+
+template <typename InT>
+__global__ void __launch_bounds__(256) quat_combine_kernel(const __grid_constant__ QuatCombParams P) {
+  extern __shared__ uint32_t qsm[];
+  uint32_t(*S3q)[65] = reinterpret_cast<uint32_t(*)[65]>(qsm);                 // Q3 on U
+  uint32_t(*S1t)[65] = reinterpret_cast<uint32_t(*)[65]>(qsm + 64 * 65);       // T1 on U
+  uint32_t(*S2t)[65] = reinterpret_cast<uint32_t(*)[65]>(qsm + 2 * 64 * 65);   // T2 on U
+  uint32_t(*S3t)[65] = reinterpret_cast<uint32_t(*)[65]>(qsm + 3 * 64 * 65);   // T3 on U
+  const int x = (int)blockIdx.x;
+  int ti = (int)((sqrtf(8.0f * (float)x + 1.0f) - 1.0f) * 0.5f);
+  while ((ti + 1) * (ti + 2) / 2 <= x) ++ti;
+  while (ti * (ti + 1) / 2 > x) --ti;
+  const int tj = x - ti * (ti + 1) / 2;
+  const int tx = threadIdx.x & 7, ty = threadIdx.x >> 3;
+  const int64_t m = P.m, ldq = P.ldq;
+  const int64_t i0 = (int64_t)ti * 64, j0 = (int64_t)tj * 64;
+  const int cx = tx * 8;
+  const ModP &md = P.mod;
+  auto buf = [&](int b) { return static_cast<const InT *>(P.Q[b]); };
+  {
+    Pk8<InT> q1[2], q2[2], q3[2], q4[2], q5[2];
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) {
+      const int64_t oU = (j0 + ty + 32 * rr) * ldq + i0 + cx;
+      q1[rr].load(buf(0) + oU); q2[rr].load(buf(1) + oU); q3[rr].load(buf(2) + oU);
+      q4[rr].load(buf(3) + oU); q5[rr].load(buf(4) + oU);
+    }
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) {
+      const int y = ty + 32 * rr;
+      uint32_t a1[8], a2[8], a3[8], a4[8], a5[8];
+      q1[rr].get(a1); q2[rr].get(a2); q3[rr].get(a3); q4[rr].get(a4); q5[rr].get(a5);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        S3q[y][cx + e] = a3[e];
+        S1t[y][cx + e] = submod(a1[e], a2[e], md);                       // T1 = Q1 - Q2
+        S2t[y][cx + e] = addmod(a4[e], a5[e], md);                       // T2 = Q4 + Q5
+        S3t[y][cx + e] = submod(addmod(a1[e], a2[e], md), a3[e], md);    // T3 = Q1 + Q2 - Q3
+      }
+    }
+  }
+  Pk8<InT> q1[2], q2[2], q3[2], q4[2], q5[2], q6[2];
+#pragma unroll
+  for (int rr = 0; rr < 2; ++rr) {
+    const int64_t oL = (i0 + ty + 32 * rr) * ldq + j0 + cx;
+    q1[rr].load(buf(0) + oL); q2[rr].load(buf(1) + oL); q3[rr].load(buf(2) + oL);
+    q4[rr].load(buf(3) + oL); q5[rr].load(buf(4) + oL); q6[rr].load(buf(5) + oL);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int rr = 0; rr < 2; ++rr) {
+    const int y = ty + 32 * rr;
+    const int64_t i = i0 + y, j = j0 + cx;
+    if (i >= m || j > i) continue;
+    uint32_t a1[8], a2[8], a3[8], a4[8], a5[8], a6[8], h[4][8];
+    q1[rr].get(a1); q2[rr].get(a2); q3[rr].get(a3); q4[rr].get(a4); q5[rr].get(a5); q6[rr].get(a6);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const uint32_t t1 = submod(a1[e], a2[e], md), t2 = addmod(a4[e], a5[e], md);
+      const uint32_t t3 = submod(addmod(a1[e], a2[e], md), a3[e], md);
+      const uint32_t q3t = S3q[cx + e][y], t1t = S1t[cx + e][y], t2t = S2t[cx + e][y], t3t = S3t[cx + e][y];
+      h[0][e] = submod(submod(a6[e], addmod(q3t, a3[e], md), md), addmod(t2t, t2, md), md);  // H1
+      h[1][e] = submod(t2t, t2, md);                                                       // H2
+      h[2][e] = submod(t1, t1t, md);                                                       // H3
+      h[3][e] = submod(t3t, t3, md);                                                       // H4
+    }
+    store_q8(P.C + 4 * (i * P.ldc + j), min64(8, min64(i - j + 1, m - j)), h, P);
+  }
+}
+
+cudaError_t launch_quat_combine(const QuatCombParams &p, cudaStream_t s) {
+  if (p.m == 0) return cudaSuccess;
+  const unsigned nt = (unsigned)((p.m + 63) / 64);
+  const dim3 grid(nt * (nt + 1) / 2);
+  const int smem = 4 * 64 * 65 * 4;
+  if (p.in32) {
+    static bool set32 = false;
+    if (!set32) {
+      cudaError_t e = cudaFuncSetAttribute(quat_combine_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e != cudaSuccess) return e;
+      set32 = true;
+    }
+    quat_combine_kernel<uint32_t><<<grid, 256, smem, s>>>(p);
+  } else {
+    static bool set16 = false;
+    if (!set16) {
+      cudaError_t e = cudaFuncSetAttribute(quat_combine_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e != cudaSuccess) return e;
+      set16 = true;
+    }
+    quat_combine_kernel<uint16_t><<<grid, 256, smem, s>>>(p);
+  }
+  return cudaGetLastError();
+}
+
 // ============================================================================ K5 2M combine
 // Re = G - eps H - phi(H) with eps = i phi(i) = 1, Im: H phi(i) + i phi(H) = i (H^T - H);
 // G lower (u16, ldg), H full (u16, ldh); C interleaved (re, im) uint32 pairs, Low only.
@@ -1568,21 +1746,19 @@ __global__ void __launch_bounds__(256) fill_upper_kernel(int64_t m, int w, uint3
   const int ti = blockIdx.y, tj = blockIdx.x;
   if (ti < tj) return;
   const int tx = threadIdx.x, ty = threadIdx.y;
-  __shared__ uint32_t s[32][33][2];
+  __shared__ uint32_t s[32][33][4];
   const int64_t i0 = (int64_t)ti * 32, j0 = (int64_t)tj * 32;
   for (int y = ty; y < 32; y += 8) {
     const int64_t i = i0 + y, j = j0 + tx;
-    if (i < m && j < m && j < i) {
-      s[y][tx][0] = C[(i * ldc + j) * w];
-      s[y][tx][1] = w == 2 ? C[(i * ldc + j) * w + 1] : 0;
-    }
+    if (i < m && j < m && j < i)
+      for (int c = 0; c < w; ++c) s[y][tx][c] = C[(i * ldc + j) * w + c];
   }
   __syncthreads();
   for (int y = ty; y < 32; y += 8) {
-    const int64_t r = j0 + y, c = i0 + tx;   // upper element (r, c) = phi(C[c][r])
+    const int64_t r = j0 + y, c = i0 + tx;   // upper element (r, c) = phi(C[c][r]): conjugate, transposed
     if (r < m && c < m && r < c) {
       C[(r * ldc + c) * w] = s[tx][y][0];
-      if (w == 2) C[(r * ldc + c) * w + 1] = submod(0, s[tx][y][1], mod);
+      for (int q = 1; q < w; ++q) C[(r * ldc + c) * w + q] = submod(0, s[tx][y][q], mod);
     }
   }
 }

@@ -13,6 +13,7 @@ cudaError_t launch_split(const SplitParams &p, cudaStream_t s);
 cudaError_t launch_combine(const CombParams &p, cudaStream_t s);
 cudaError_t launch_herk_preadd(const HerkPreParams &p, cudaStream_t s);
 cudaError_t launch_herk_combine(const HerkCombParams &p, cudaStream_t s);
+cudaError_t launch_quat_combine(const QuatCombParams &p, cudaStream_t s);
 cudaError_t launch_twom(int64_t m, const void *G, int64_t ldg, const void *H, int64_t ldh, int in32,
                         uint32_t *C, int64_t ldc, const ModP &mod, uint32_t alpha, uint32_t beta, int axpby,
                         cudaStream_t s);

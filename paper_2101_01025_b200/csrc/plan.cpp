@@ -171,7 +171,8 @@ static void set_grid(Plan &P, int num_sms) {
 // of G must stay >= 8192 rows.  Deeper levels are also used when the level-1 inner dimension
 // would exceed the int32 accumulation bound of the limb scheme.
 int auto_depth(int64_t m, int64_t k, uint32_t p, int phi) {
-  const int64_t leaf_min = phi == 0 ? 4096 : 8192;
+  // phi = Q: Q6 is 1/11 of the 6M work, one Alg. 1 level saves 1/8 of it -- never worth a K1 + K4 pass
+  const int64_t leaf_min = phi == 0 ? 4096 : (phi == 1 ? 8192 : ((int64_t)1 << 40));
   int d = 0;
   while (d < 3 && cdiv(m, (int64_t)1 << (d + 1)) >= leaf_min && cdiv(k, (int64_t)1 << (d + 1)) >= 1024) ++d;
   const int64_t kmax = limb_kmax(limb_scheme(p), p);
@@ -184,7 +185,7 @@ int auto_depth(int64_t m, int64_t k, uint32_t p, int phi) {
 bool build_syrk_plan(Plan &P, int64_t m, int64_t k, uint32_t p, int phi, int depth, int num_sms,
                      const char **err) {
   P = Plan();
-  P.kind = phi == 0 ? PLAN_SYRK_T : PLAN_SYRK_H;
+  P.kind = phi == 0 ? PLAN_SYRK_T : (phi == 1 ? PLAN_SYRK_H : PLAN_QUAT);
   P.m = m; P.n = m; P.k = k; P.depth = depth;
   fill_scheme(P, p);
   const int planes = P.planes;
@@ -218,6 +219,11 @@ bool build_syrk_plan(Plan &P, int64_t m, int64_t k, uint32_t p, int phi, int dep
     n0 = 2;
     if (depth == 0) { P.op0_row[2] = 2 * (int64_t)planes * P.rows_pad0; n0 = 3; }
   }
+  if (P.kind == PLAN_QUAT) {
+    // Alg. alg:2M3M operands A, B, C, D, U1 = A + B, U2 = C + D (+ W = U1 + U2 for Q6 at depth 0)
+    n0 = depth == 0 ? QO_N : QO_W;
+    for (int o = 0; o < n0; ++o) P.q_row[o] = (int64_t)o * planes * P.rows_pad0;
+  }
   if (n0 > 0) {
     ArenaPlan a;
     a.kpad = P.kpad0;
@@ -249,6 +255,11 @@ bool build_syrk_plan(Plan &P, int64_t m, int64_t k, uint32_t p, int phi, int dep
     P.h_offset = alloc((size_t)P.rows_pad0 * P.rows_pad0 * P.res_bytes());
     P.g_offset = alloc((size_t)P.rows_pad0 * P.rows_pad0 * P.res_bytes());
   }
+  if (P.kind == PLAN_QUAT) {
+    P.q_bytes = (size_t)rup(P.rows_pad0 * P.rows_pad0 * P.res_bytes(), 256);
+    P.q_offset = alloc(P.q_bytes * 5);                                        // Q1..Q5
+    P.g_offset = alloc((size_t)P.rows_pad0 * P.rows_pad0 * P.res_bytes());  // Q6 (Low)
+  }
   P.ws_bytes = off;
 
   // the int32 accumulation bound per leaf product is met by K segmentation
@@ -264,6 +275,16 @@ bool build_syrk_plan(Plan &P, int64_t m, int64_t k, uint32_t p, int phi, int dep
     if (depth == 0)
       P.prods.push_back(make_prod(P, 0, P.op0_row[2], P.op0_row[2], P.rows_pad0, P.rows_pad0, P.kpad0, true, OUT_GBUF,
                                   0, 0, 0, P.rows_pad0, P.rows_pad0, false, P.rows_pad0)); // G = T T^T
+  }
+  if (P.kind == PLAN_QUAT) {
+    // Q1 = C A^T, Q2 = D B^T, Q3 = U2 U1^T, Q4 = A B^T, Q5 = C D^T
+    const int qa[5] = {QO_C, QO_D, QO_U2, QO_A, QO_C}, qb[5] = {QO_A, QO_B, QO_U1, QO_B, QO_D};
+    for (int q = 0; q < 5; ++q)
+      P.prods.push_back(make_prod(P, 0, P.q_row[qa[q]], P.q_row[qb[q]], P.rows_pad0, P.rows_pad0, P.kpad0, false,
+                                  OUT_QBUF, 0, 0, q, P.rows_pad0, P.rows_pad0, false, P.rows_pad0));
+    if (depth == 0)   // Q6 = (U1 + U2)(U1 + U2)^T, Low
+      P.prods.push_back(make_prod(P, 0, P.q_row[QO_W], P.q_row[QO_W], P.rows_pad0, P.rows_pad0, P.kpad0, true,
+                                  OUT_GBUF, 0, 0, 0, P.rows_pad0, P.rows_pad0, false, P.rows_pad0));
   }
   for (int l = 1; l <= depth; ++l) {
     const LevelPlan &L = P.lv[l];

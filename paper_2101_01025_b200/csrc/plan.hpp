@@ -13,7 +13,10 @@
 
 namespace adj {
 
-enum PlanKind : int { PLAN_SYRK_T = 0, PLAN_SYRK_H = 1, PLAN_GEMM = 2, PLAN_HERK1 = 3 };
+enum PlanKind : int { PLAN_SYRK_T = 0, PLAN_SYRK_H = 1, PLAN_GEMM = 2, PLAN_HERK1 = 3, PLAN_QUAT = 4 };
+
+// PLAN_QUAT (phi = quaternion conjugate transpose, Alg. alg:2M3M): arena-0 operands
+enum QuatOp : int { QO_A = 0, QO_B, QO_C, QO_D, QO_U1, QO_U2, QO_W, QO_N };
 
 
 struct ArenaPlan {
@@ -33,7 +36,7 @@ struct LevelPlan {
 };
 
 // leaf product whose output pointer is resolved at bind time
-enum OutTarget : int { OUT_PBUF = 0, OUT_C = 1, OUT_HBUF = 2, OUT_GBUF = 3 };
+enum OutTarget : int { OUT_PBUF = 0, OUT_C = 1, OUT_HBUF = 2, OUT_GBUF = 3, OUT_QBUF = 4 };
 struct ProductPlan {
   LeafProduct lp;        // everything except `out` (and ldo for OUT_C)
   int target;            // OutTarget
@@ -61,6 +64,8 @@ struct Plan {
   int64_t op0_row[3] = {-1, -1, -1};  // SYRK_T d=0: A; SYRK_H: X, Y, (T if d==0); GEMM: A, B
   size_t h_offset = 0, g_offset = 0;  // 2M buffers H, G (uint16 rows_pad0^2)
   size_t hb_offset = 0, hb_bytes = 0; // PLAN_HERK1: HB_N product buffers of lv[1].rows_pad^2 residues
+  size_t q_offset = 0, q_bytes = 0;   // PLAN_QUAT: Q1..Q5 (rows_pad0^2 residues each); Q6 in g_offset
+  int64_t q_row[QO_N] = {-1, -1, -1, -1, -1, -1, -1};   // PLAN_QUAT arena-0 operand rows
   size_t ws_bytes = 0;
   std::vector<ProductPlan> prods;
   std::vector<uint32_t> tiles;       // 2 words per leaf job (LeafParams::tiles)

@@ -63,7 +63,8 @@ struct FixupTile {
 };
 
 // ---------------------------------------------------------------- K1 pre-addition
-enum InType : int32_t { IN_U32 = 0, IN_U16 = 1, IN_PAIR_SUM = 2, IN_PAIR_RE = 3, IN_PAIR_IM = 4 };
+enum InType : int32_t { IN_U32 = 0, IN_U16 = 1, IN_PAIR_SUM = 2, IN_PAIR_RE = 3, IN_PAIR_IM = 4,
+                        IN_QUAD_SUM = 5 /* quaternion x1 + x2 + x3 + x4 (Q6's W = U1 + U2, Alg. alg:2M3M) */ };
 
 struct InView {          // a (possibly padded) view of a node's input matrix
   const void *ptr;
@@ -111,7 +112,9 @@ struct SplitParams {
   int64_t op_row2, op_row3;  // mode 1 (2M): Y = Im(A) and T = Re + Im planes
   int8_t *arena;
   int32_t scheme, planes;
-  int32_t mode;              // 0: plain split of `in`; 1: 2M split of interleaved pairs
+  int32_t mode;              // 0: plain split of `in`; 1: 2M split of interleaved pairs;
+                             // 2: quaternion split (Alg. alg:2M3M operands A, B, C, D, U1, U2, W)
+  int64_t qrow[7];           // mode 2: arena rows of the QuatOp operands (-1 = not written)
   ModP mod;
 };
 
@@ -163,6 +166,17 @@ struct HerkCombParams {
   int64_t mh, ldp;
   uint32_t *C;             // interleaved (re, im) pairs, ldc in pairs
   int64_t ldc, out_valid;
+  ModP mod;
+  uint32_t alpha, beta;
+  int32_t axpby, in32;
+};
+
+// ---------------------------------------------------------------- quaternion 6M combine (PLAN_QUAT)
+struct QuatCombParams {
+  const void *Q[6];        // Q1..Q5 (full), Q6 (Low): rows_pad x rows_pad residues (u16, or u32 if in32), ld = ldq
+  int64_t m, ldq;
+  uint32_t *C;             // 4 interleaved components per quaternion, ldc in quaternions
+  int64_t ldc;
   ModP mod;
   uint32_t alpha, beta;
   int32_t axpby, in32;

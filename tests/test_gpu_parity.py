@@ -291,3 +291,67 @@ def test_herk_alg1_depth_must_be_one(adj):
     C = torch.zeros((8, 8, 2), dtype=torch.int32, device="cuda")
     with pytest.raises(adj.AdjError):
         adj.adjprod_modp_ex(8, 8, 8191, 1, A, 8, C, 8, depth=2, flags=adj.ADJ_HERK_ALG1)
+
+
+# ---------------------------------------------------------------- SURVEY.md §8(f)-4
+# phi = quaternion conjugate transpose (ADJ_PHI_Q), Alg. alg:2M3M (6M) with
+# Q6 through Alg. alg:MIAHMM at the requested depth, against the Hamilton-product oracle.
+QUAT_PRIMES = [3, 97, 251, 257, 8191, 16787, 65521, 131071]
+
+
+@pytest.mark.parametrize("p", QUAT_PRIMES)
+@pytest.mark.parametrize("depth", [0, 1, 2])
+@pytest.mark.parametrize("m,k", [(1, 1), (2, 3), (33, 17), (129, 200), (260, 300)])
+def test_quat_vs_oracle(adj, p, depth, m, k):
+    from inputs import uniform_matrix_quat
+    M = uniform_matrix_quat(m, k, seed=m * 13 + k + depth, p=p)
+    C = adj.adjprod(to_dev(M), p, phi="Q", depth=depth)
+    assert np.array_equal(to_host(C), oracle.syrk_q(M, p))
+
+
+def test_quat_fill_upper_untouched_and_strided(adj):
+    import torch
+    from inputs import uniform_matrix_quat
+    p, m, k, ldm, ldc = 8191, 150, 210, 223, 161
+    rng = np.random.default_rng(11)
+    full = rng.integers(0, 2**32, size=(m, ldm, 4), dtype=np.uint64).astype(np.uint32)
+    C = torch.full((m, ldc, 4), -1, dtype=torch.int32, device="cuda")
+    adj.adjprod_modp_ex(m, k, p, adj.ADJ_PHI_Q, to_dev(full), ldm, C, ldc, depth=1)
+    got = to_host(C)
+    ref = oracle.syrk_q(full[:, :k] % p, p)
+    lo = np.tril(np.ones((m, m), dtype=bool))
+    assert np.array_equal(got[:, :m][lo], ref[lo])
+    assert (got[:, :m][~lo] == 0xFFFFFFFF).all() and (got[:, m:] == 0xFFFFFFFF).all()
+    M = uniform_matrix_quat(200, 120, seed=4, p=p)
+    F = to_host(adj.adjprod(to_dev(M), p, phi="Q", fill_upper=True))
+    assert np.array_equal(F[..., 0], F[..., 0].T)                       # H(j,i) = conj(H(i,j))
+    for c in (1, 2, 3):
+        assert np.array_equal(F[..., c], (p - F[..., c].T.astype(np.int64)) % p)
+
+
+@pytest.mark.parametrize("alpha,beta", [(1, 0), (0, 1), (3, 5), (8190, 8190)])
+def test_quat_syrk_form(adj, alpha, beta):
+    from inputs import uniform_matrix_quat
+    p, m, k = 8191, 200, 150
+    M = uniform_matrix_quat(m, k, seed=6, p=p)
+    rng = np.random.default_rng(alpha * 3 + beta)
+    C0 = rng.integers(0, 2**32, size=(m, m, 4), dtype=np.uint64).astype(np.uint32)
+    dC = to_dev(C0)
+    adj.adjprod_modp_syrk(m, k, p, adj.ADJ_PHI_Q, alpha, to_dev(M), k, beta, dC, m)
+    base = oracle.syrk_q(M, p).astype(np.int64)
+    ref = C0.copy()
+    lo = np.tril(np.ones((m, m), dtype=bool))
+    new = (alpha * base + beta * (C0.astype(np.int64) % p)) % p
+    ref[lo] = new[lo].astype(np.uint32)
+    assert np.array_equal(to_host(dC), ref)
+
+
+def test_quat_overflow_stress_constant(adj):
+    """Constant quaternion matrix at the int32 accumulation bound of each Q product (limb
+    extremes, k beyond one K segment)."""
+    from inputs import constant_matrix
+    p, m, k = 8191, 128, 240000
+    M = np.stack([constant_matrix(m, k, c, p) for c in (p - 64, p - 4032, 4032, 64)], axis=-1)
+    got = to_host(adj.adjprod(to_dev(M), p, phi="Q", depth=0))
+    ref = oracle.syrk_q(M[:2], p)
+    assert (got[np.tril_indices(m)] == ref[1, 0]).all()
