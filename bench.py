@@ -37,6 +37,9 @@ CONFIGS = {
                  workload="x251 (dev): A 8192x8192 over GF(251), one int8 limb"),
     "c5": dict(m=8192, k=8192, p=8191, phi="H", depth=None,
                workload="c5: A 8192x8192 over GF(8191^2) = GF(8191)[i]/(i^2+1), C = Low(A A^H) via 2M"),
+    "q5": dict(m=8192, k=8192, p=8191, phi="Q", depth=None,
+               workload="q5 (SURVEY 8(f)-4): M 8192x8192 over the quaternions H_GF(8191), C = Low(M M^H) via "
+                        "Alg. 2M3M (6M)"),
 }
 DEFAULT_CONFIG = "c2"   # BASELINE.json configs[1]
 METRIC = "effective m^2 k modular MAC/s for C=A*A^T mod p (1 GPU: BASELINE configs[1])"
@@ -72,6 +75,8 @@ def leaf_int8_ops(cfg, depth, herk="2m") -> float:
     macs = ring_macs(m, k, depth)
     if cfg["phi"] == "H":
         macs += m * m * k            # 2M's general product H = X Y^T
+    if cfg["phi"] == "Q":
+        macs += 5 * m * m * k        # 6M's general products Q1..Q5 (Q6 is the ring_macs term)
     return 2.0 * macs * limb_mmas(p)
 
 
@@ -174,7 +179,7 @@ def oracle_sample(cfg, A_host, budget_s: float):
     import oracle
     m, k, p = cfg["m"], cfg["k"], cfg["p"]
     H = cfg["phi"] == "H"
-    f = oracle.syrk_h if H else oracle.syrk_t
+    f = {"T": oracle.syrk_t, "H": oracle.syrk_h, "Q": oracle.syrk_q}[cfg["phi"]]
     cores = oracle.num_threads()
     # calibration on a tiny slab
     r = max(1, min(m, 2))
@@ -197,7 +202,8 @@ def oracle_sample(cfg, A_host, budget_s: float):
     full_lower = m * (m + 1) / 2 * k
     t_full = t * full_lower / sample_macs
     eff = m * m * k / t_full
-    desc = (f"O1 oracle ({'GF(p^2) hermitian' if H else 'GF(p)'} u64 triple loop, OpenMP) on rows "
+    field = {"T": "GF(p)", "H": "GF(p^2) hermitian", "Q": "quaternion H_GF(p) hermitian"}[cfg["phi"]]
+    desc = (f"O1 oracle ({field} u64 triple loop, OpenMP) on rows "
             f"[{m - rows}, {m}) of Low(C) = {sample_macs:.3e} of {full_lower:.3e} lower-triangle MACs in {t:.2f} s; "
             f"value extrapolated to the full problem by MAC count ({t_full:.1f} s)")
     return eff, t, cores, desc, t_full
@@ -206,11 +212,11 @@ def oracle_sample(cfg, A_host, budget_s: float):
 def run_reference(args, cfg, rank, world):
     """--impl reference: the CPU oracle as it stands, on host cores, rank 0 only."""
     import numpy as np
-    from inputs import uniform_matrix, uniform_matrix_ext
+    from inputs import uniform_matrix, uniform_matrix_ext, uniform_matrix_quat
     if rank != 0:
         return
     m, k, p = cfg["m"], cfg["k"], cfg["p"]
-    A = uniform_matrix_ext(m, k, 1, p) if cfg["phi"] == "H" else uniform_matrix(m, k, 1, p)
+    A = {"T": uniform_matrix, "H": uniform_matrix_ext, "Q": uniform_matrix_quat}[cfg["phi"]](m, k, 1, p)
     per_step = float(os.environ.get("ADJ_REF_STEP_S", "2.0"))
     for _ in range(args.warmup):
         oracle_sample(cfg, A, per_step / 4)
@@ -225,7 +231,8 @@ def run_reference(args, cfg, rank, world):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(tfull),
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "uint64", "data": "synthetic",
+        "higher_is_better": True, "scaling": "strong" if args.gpus > 1 else "weak", "vs_baseline": None,
+        "dtype": "uint64", "data": "synthetic",
         "config": {"workload": cfg["workload"], "m": m, "k": k, "p": p, "phi": cfg["phi"], "seed": 1,
                    "sample_s_per_step": statistics.median(secs), "ms_per_step_is": "extrapolated full problem"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc},
@@ -245,8 +252,8 @@ def run_gpu(args, cfg, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     m, k, p = cfg["m"], cfg["k"], cfg["p"]
-    phi = adj.ADJ_PHI_H if cfg["phi"] == "H" else adj.ADJ_PHI_T
-    w = 2 if cfg["phi"] == "H" else 1
+    phi = {"T": adj.ADJ_PHI_T, "H": adj.ADJ_PHI_H, "Q": adj.ADJ_PHI_Q}[cfg["phi"]]
+    w = {"T": 1, "H": 2, "Q": 4}[cfg["phi"]]
     alg1 = cfg["phi"] == "H" and args.herk == "alg1"
     flags = adj.ADJ_HERK_ALG1 if alg1 else 0
     depth = args.depth if args.depth is not None else (cfg["depth"] if cfg["depth"] is not None
@@ -365,8 +372,8 @@ def run_gpu(args, cfg, rank, world, local_rank):
     if rank == 0 and not args.no_check:
         import oracle
         rows = 2
-        Ah = A.cpu().numpy().view(np.uint32).reshape((m, k, 2) if w == 2 else (m, k))
-        ref = (oracle.syrk_h if w == 2 else oracle.syrk_t)(Ah, p, rows=(m - rows, m))
+        Ah = A.cpu().numpy().view(np.uint32).reshape((m, k, w) if w > 1 else (m, k))
+        ref = {1: oracle.syrk_t, 2: oracle.syrk_h, 4: oracle.syrk_q}[w](Ah, p, rows=(m - rows, m))
         got = C.cpu().numpy().view(np.uint32).reshape(ref.shape)
         ok = all(np.array_equal(got[i, : i + 1], ref[i, : i + 1]) for i in range(m - rows, m))
         parity = {"rows_checked": [m - rows, m], "bit_exact": bool(ok)}
@@ -389,12 +396,12 @@ def run_gpu(args, cfg, rank, world, local_rank):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        Ah = A.cpu().numpy().view(np.uint32).reshape((m, k, 2) if w == 2 else (m, k))
+        Ah = A.cpu().numpy().view(np.uint32).reshape((m, k, w) if w > 1 else (m, k))
         eff, t, cores, desc, _ = oracle_sample(cfg, Ah, float(os.environ.get("ADJ_CPU_BUDGET_S", "12")))
         cpu = {"value": eff, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
 
     if rank == 0:
-        mh = herk_alg1_macs(m, k) if alg1 else ring_macs(m, k, depth) + (m * m * k if w == 2 else 0)
+        mh = herk_alg1_macs(m, k) if alg1 else ring_macs(m, k, depth) + {1: 0, 2: 1, 4: 5}[w] * m * m * k
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True,
