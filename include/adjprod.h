@@ -80,8 +80,9 @@ typedef enum {
  *                    (§4.4, 750-758) instead of the 2M reduction
  *                    to GF(p) (Alg. alg:2M).  Its Hermitian leaves P1, P2, P5 use 2M, its
  *                    general leaves P3, P4 use 3M.  Requires depth 1 (or -1); the result is the
- *                    same Low(C).  Ignored for phi = ADJ_PHI_T. */
-enum { ADJ_FILL_UPPER = 1u, ADJ_HERK_ALG1 = 2u };
+ *                    same Low(C).  Ignored for phi = ADJ_PHI_T.
+ *   ADJ_DIST_TILES : adjprod_modp_dist only -- output-tile sharding instead of split-K. */
+enum { ADJ_FILL_UPPER = 1u, ADJ_HERK_ALG1 = 2u, ADJ_DIST_TILES = 4u };
 
 typedef struct {
   int depth;              /* recursion levels of Alg. alg:MIAHMM; -1 = automatic; 0 = classical */
@@ -177,13 +178,41 @@ adj_status_t adj_comm_destroy(adj_comm_t comm);
 adj_status_t adj_dist_kslice(int64_t k, int nranks, int rank, int64_t *k0, int64_t *k1);
 
 /*
+ * adjprod_modp_shard -- output-tile sharding, phi = ADJ_PHI_T, depth 0 or 1
+ *   (-1: the automatic depth capped at 1).  The top-level product grid of Alg. alg:MIAHMM (the
+ *   (m/2) grid of P1..P5 at depth 1; the grid of C at depth 0) is cut into 256 x 256 tiles;
+ *   pairs {(I, J), (J, I)}, I >= J, are dealt to `nranks` owners (largest cost first to the
+ *   least loaded, deterministic).  This call writes exactly the regions of Low(C) that `rank`
+ *   owns (adj_shard_layout) and nothing else: the pre-addition is computed in full (A is read
+ *   whole), the grouped leaf launch runs only the owned tiles of P1..P5 and the recombination
+ *   only the owned tile pairs.  Running every rank's share, on one device or on several,
+ *   writes all of Low(C).  ADJ_FILL_UPPER is not supported here (INVALID_VALUE).
+ */
+adj_status_t adjprod_modp_shard(int64_t m, int64_t k, uint32_t p, adj_phi_t phi,
+                                const uint32_t *A, int64_t lda, uint32_t *C, int64_t ldc,
+                                int rank, int nranks, const adj_opts_t *opts, adj_stream_t stream);
+
+/*
+ * adj_shard_layout -- (host, no GPU) the regions of C that `rank` of `nranks` writes in
+ *   adjprod_modp_shard for this problem: *n_rects regions, each 5 int64 (row0, col0, rows,
+ *   cols, lower) stored in rects[5*i..5*i+4] for i < max_rects (rects may be NULL); lower = 1
+ *   means only the elements with col <= row belong to the rank.  *n_elems = sum rows*cols.
+ *   The regions of all ranks partition Low(C).
+ */
+adj_status_t adj_shard_layout(int64_t m, int64_t k, uint32_t p, int depth, int rank, int nranks,
+                              int64_t *rects, int64_t max_rects, int64_t *n_rects, int64_t *n_elems);
+
+/*
  * adjprod_modp_dist -- collective; every rank of `comm` calls it with the same m, k, p, phi,
- *   root.  Split-K sharding: rank r computes Low(A_r phi(A_r)) on its
+ *   root.  Default: split-K sharding: rank r computes Low(A_r phi(A_r)) on its
  *   column slice A_r = A[:, k_r0 : k_r1] (k_r0 = r*ceil(k/G) rounded to a multiple of 8) with
  *   the single-GPU path, then the residue partials are summed exactly with an NCCL uint32
  *   reduce to `root` (sum < G p < 2^32) and reduced mod p there.
  *   A: the full m x k matrix on every rank (only the rank's slice is read).  C: m x m on every
- *   rank, used as the partial buffer; Low(C) is the result on `root` only.
+ *   rank; Low(C) is the result on `root` only.
+ *   With opts->flags & ADJ_DIST_TILES (phi = ADJ_PHI_T): output-tile sharding instead -- every
+ *   rank runs adjprod_modp_shard with the full A into its C, then the root gathers the other
+ *   ranks' regions (packed, NCCL send/recv: only result tiles move).
  */
 adj_status_t adjprod_modp_dist(int64_t m, int64_t k, uint32_t p, adj_phi_t phi,
                                const uint32_t *A, int64_t lda, uint32_t *C, int64_t ldc,

@@ -16,13 +16,14 @@ ADJ_PHI_H = 1
 ADJ_PHI_Q = 2
 ADJ_FILL_UPPER = 1
 ADJ_HERK_ALG1 = 2
+ADJ_DIST_TILES = 4
 STATUS = {0: "ADJ_OK", 1: "ADJ_ERR_INVALID_VALUE", 2: "ADJ_ERR_UNSUPPORTED_MODULUS", 3: "ADJ_ERR_WORKSPACE",
           4: "ADJ_ERR_CUDA", 5: "ADJ_ERR_NCCL", 6: "ADJ_ERR_ARCH"}
 
 # every symbol include/adjprod.h declares (checked by tests/test_abi.py)
 EXPORTS = ["adjprod_modp", "adjprod_modp_ex", "adjprod_modp_syrk", "adjprod_modp_workspace_size", "adjprod_modp_auto_depth",
            "gemm_modp", "adj_skew_unitary", "adj_sos", "adj_mod_lower", "adj_comm_get_unique_id",
-           "adj_comm_init", "adj_comm_destroy", "adjprod_modp_dist", "adj_dist_kslice", "adj_status_string", "adj_last_error",
+           "adj_comm_init", "adj_comm_destroy", "adjprod_modp_dist", "adj_dist_kslice", "adjprod_modp_shard", "adj_shard_layout", "adj_status_string", "adj_last_error",
            "adj_launch_count", "adj_launch_count_reset", "adj_profile_enable", "adj_profile_read"]
 
 
@@ -63,6 +64,9 @@ def lib() -> ctypes.CDLL:
             "adj_comm_destroy": [vp],
             "adjprod_modp_dist": [i64, i64, u32, ci, vp, i64, vp, i64, ci, vp, ctypes.POINTER(adj_opts_t), vp],
             "adj_dist_kslice": [i64, ci, ci, ctypes.POINTER(i64), ctypes.POINTER(i64)],
+            "adjprod_modp_shard": [i64, i64, u32, ci, vp, i64, vp, i64, ci, ci, ctypes.POINTER(adj_opts_t), vp],
+            "adj_shard_layout": [i64, i64, u32, ci, ci, ci, ctypes.POINTER(i64), i64, ctypes.POINTER(i64),
+                                 ctypes.POINTER(i64)],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -179,6 +183,24 @@ def adjprod_modp_dist(m, k, p, phi, A, lda, C, ldc, root, comm, depth=-1, flags=
     o = _opts(depth, flags)
     _check(lib().adjprod_modp_dist(m, k, p, phi, _ptr(A), lda, _ptr(C), ldc, root, comm, ctypes.byref(o),
                                    _stream(stream)), "adjprod_modp_dist")
+
+
+def adjprod_modp_shard(m, k, p, phi, A, lda, C, ldc, rank, nranks, depth=-1, workspace=None, workspace_bytes=0,
+                       stream=None):
+    o = _opts(depth, 0, workspace, workspace_bytes)
+    _check(lib().adjprod_modp_shard(m, k, p, phi, _ptr(A), lda, _ptr(C), ldc, rank, nranks, ctypes.byref(o),
+                                    _stream(stream)), "adjprod_modp_shard")
+
+
+def adj_shard_layout(m, k, p, rank, nranks, depth=-1):
+    """[(row0, col0, rows, cols, lower), ...] of the regions of C that `rank` writes (host)."""
+    n, e = ctypes.c_int64(0), ctypes.c_int64(0)
+    _check(lib().adj_shard_layout(m, k, p, depth, rank, nranks, None, 0, ctypes.byref(n), ctypes.byref(e)),
+           "adj_shard_layout")
+    buf = (ctypes.c_int64 * max(1, 5 * n.value))()
+    _check(lib().adj_shard_layout(m, k, p, depth, rank, nranks, buf, n.value, ctypes.byref(n), ctypes.byref(e)),
+           "adj_shard_layout")
+    return [tuple(buf[5 * i: 5 * i + 5]) for i in range(n.value)]
 
 
 def adj_dist_kslice(k, nranks, rank):

@@ -140,25 +140,31 @@ adj_status_t encode_arena(CUtensorMap *map, void *base, int64_t kpad, int64_t ro
 }
 
 // ------------------------------------------------------------------ plan cache
-using Key = std::tuple<int, int, int64_t, int64_t, int64_t, uint32_t, int, int>;  // dev, kind, m, n, k, p, phi, depth
+// dev, kind, m, n, k, p, phi, depth, shard rank, shard count
+using Key = std::tuple<int, int, int64_t, int64_t, int64_t, uint32_t, int, int, int, int>;
 std::map<Key, std::unique_ptr<Plan>> g_plans;
 
 adj_status_t get_plan(Plan **out, int kind, int64_t m, int64_t n, int64_t k, uint32_t p, int phi, int depth, int dev,
-                      int sms) {
+                      int sms, int shard_rank = -1, int shard_n = 0) {
   std::lock_guard<std::mutex> lk(g_mu);
-  Key key{dev, kind, m, n, k, p, phi, depth};
+  Key key{dev, kind, m, n, k, p, phi, depth, shard_rank, shard_n};
   auto it = g_plans.find(key);
   if (it != g_plans.end()) { *out = it->second.get(); return ADJ_OK; }
   auto P = std::make_unique<Plan>();
   const char *err = nullptr;
   bool ok = kind == PLAN_GEMM    ? build_gemm_plan(*P, m, n, k, p, sms, &err)
             : kind == PLAN_HERK1 ? build_herk1_plan(*P, m, k, p, sms, &err)
-                                 : build_syrk_plan(*P, m, k, p, phi, depth, sms, &err);
+                                 : build_syrk_plan(*P, m, k, p, phi, depth, sms, &err, shard_rank, shard_n);
   if (!ok) return fail(ADJ_ERR_INVALID_VALUE, "plan: %s", err ? err : "unsupported");
   P->dev = dev;
   if (!P->tiles.empty()) {
     CUDA_TRY(cudaMalloc(&P->d_tiles, P->tiles.size() * sizeof(uint32_t)));
     CUDA_TRY(cudaMemcpy(P->d_tiles, P->tiles.data(), P->tiles.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+  }
+  if (!P->comb_pairs.empty()) {
+    CUDA_TRY(cudaMalloc(&P->d_comb_pairs, P->comb_pairs.size() * sizeof(uint32_t)));
+    CUDA_TRY(cudaMemcpy(P->d_comb_pairs, P->comb_pairs.data(), P->comb_pairs.size() * sizeof(uint32_t),
+                        cudaMemcpyHostToDevice));
   }
   if (!P->fixups.empty()) {
     CUDA_TRY(cudaMalloc(&P->d_fixups, P->fixups.size() * sizeof(FixupTile)));
@@ -355,6 +361,10 @@ adj_status_t run_combine(const Plan &P, const Ptrs &x, void *final_out, int64_t 
       cp.alpha = x.alpha;
       cp.beta = x.beta;
       cp.axpby = x.axpby;
+    }
+    if (P.shard_n > 0) {          // output-tile sharding (depth 1): only this rank's tile pairs
+      cp.pairs = P.d_comb_pairs;
+      cp.n_pairs = (int32_t)P.comb_pairs.size();
     }
     for (int n = 0; n < L.n_nodes; ++n) {
       CombNode &N = cp.nodes[n];
@@ -656,6 +666,90 @@ static adj_status_t adjprod_impl(int64_t m, int64_t k, uint32_t p, adj_phi_t phi
     if (st == ADJ_OK && e != cudaSuccess) return fail(ADJ_ERR_CUDA, "cudaFreeAsync: %s", cudaGetErrorString(e));
   }
   return st;
+}
+
+static adj_status_t shard_plan(Plan **out, int64_t m, int64_t k, uint32_t p, int depth, int rank, int nranks, int dev,
+                               int sms) {
+  return get_plan(out, PLAN_SYRK_T, m, m, std::max<int64_t>(k, 1), p, 0, depth, dev, sms, rank, nranks);
+}
+
+static int shard_depth(int64_t m, int64_t k, uint32_t p, const adj_opts_t *opts) {
+  return (opts && opts->depth >= 0) ? opts->depth : std::min(1, auto_depth(m, std::max<int64_t>(k, 1), p, 0));
+}
+
+adj_status_t adjprod_modp_shard(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, const uint32_t *A, int64_t lda,
+                                uint32_t *C, int64_t ldc, int rank, int nranks, const adj_opts_t *opts,
+                                adj_stream_t stream) {
+  adj_status_t st = validate_syrk(m, k, p, phi, A, lda, C, ldc);
+  if (st != ADJ_OK) return st;
+  if (phi != ADJ_PHI_T) return fail(ADJ_ERR_INVALID_VALUE, "output-tile sharding supports phi = ADJ_PHI_T");
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(ADJ_ERR_INVALID_VALUE, "rank %d of %d", rank, nranks);
+  if (opts && (opts->flags & ~0u) & ADJ_FILL_UPPER) return fail(ADJ_ERR_INVALID_VALUE, "ADJ_FILL_UPPER with sharding");
+  if (m == 0) return ADJ_OK;
+  const int depth = shard_depth(m, k, p, opts);
+  if (depth > 1) return fail(ADJ_ERR_INVALID_VALUE, "output-tile sharding runs at depth 0 or 1 (got %d)", depth);
+  int dev, sms;
+  if ((st = check_device(&dev, &sms)) != ADJ_OK) return st;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  Plan *P = nullptr;
+  if ((st = shard_plan(&P, m, k, p, depth, rank, nranks, dev, sms)) != ADJ_OK) return st;
+  if (k == 0) {   // Low(C) = 0 on the owned regions
+    for (const ShardRect &R : P->shard_rects) {
+      if (!R.lower) {
+        CUDA_TRY(cudaMemset2DAsync(C + R.r0 * ldc + R.c0, (size_t)ldc * 4, 0, (size_t)R.cols * 4, (size_t)R.rows, s));
+      } else {
+        for (int64_t i = 0; i < R.rows; ++i) {
+          const int64_t n = std::min(R.cols, R.r0 + i - R.c0 + 1);
+          if (n > 0) CUDA_TRY(cudaMemsetAsync(C + (R.r0 + i) * ldc + R.c0, 0, (size_t)n * 4, s));
+        }
+      }
+    }
+    return ADJ_OK;
+  }
+  Ptrs x;
+  x.A = A; x.lda = lda; x.C = C; x.ldc = ldc;
+  void *ws = opts ? opts->workspace : nullptr;
+  bool own = false;
+  if (ws == nullptr) {
+    CUDA_TRY(cudaMallocAsync(&ws, P->ws_bytes, s));
+    own = true;
+  } else if (opts->workspace_bytes < P->ws_bytes) {
+    return fail(ADJ_ERR_WORKSPACE, "workspace %zu bytes < required %zu", opts->workspace_bytes, P->ws_bytes);
+  }
+  x.ws = static_cast<uint8_t *>(ws);
+  st = run_syrk(*P, x, phi, 0, s);
+  if (own) {
+    cudaError_t e = cudaFreeAsync(ws, s);
+    if (st == ADJ_OK && e != cudaSuccess) return fail(ADJ_ERR_CUDA, "cudaFreeAsync: %s", cudaGetErrorString(e));
+  }
+  return st;
+}
+
+adj_status_t adj_shard_layout(int64_t m, int64_t k, uint32_t p, int depth, int rank, int nranks, int64_t *rects,
+                              int64_t max_rects, int64_t *n_rects, int64_t *n_elems) {
+  if (!n_rects || !n_elems) return fail(ADJ_ERR_INVALID_VALUE, "null output");
+  if (m < 0 || k < 0 || nranks < 1 || rank < 0 || rank >= nranks) return fail(ADJ_ERR_INVALID_VALUE, "bad arguments");
+  if (!valid_modulus(p)) return fail(ADJ_ERR_UNSUPPORTED_MODULUS, "p=%u is not an odd prime in [3, 262139]", p);
+  *n_rects = 0;
+  *n_elems = 0;
+  if (m == 0) return ADJ_OK;
+  adj_opts_t o{depth, 0, nullptr, 0};
+  const int d = shard_depth(m, k, p, &o);
+  if (d > 1) return fail(ADJ_ERR_INVALID_VALUE, "output-tile sharding runs at depth 0 or 1 (got %d)", d);
+  Plan P;
+  const char *err = nullptr;
+  if (!build_syrk_plan(P, m, std::max<int64_t>(k, 1), p, 0, d, 148, &err, rank, nranks))
+    return fail(ADJ_ERR_INVALID_VALUE, "plan: %s", err ? err : "unsupported");
+  *n_rects = (int64_t)P.shard_rects.size();
+  for (size_t i = 0; i < P.shard_rects.size(); ++i) {
+    const ShardRect &R = P.shard_rects[i];
+    *n_elems += R.rows * R.cols;
+    if (rects && (int64_t)i < max_rects) {
+      rects[5 * i] = R.r0; rects[5 * i + 1] = R.c0; rects[5 * i + 2] = R.rows; rects[5 * i + 3] = R.cols;
+      rects[5 * i + 4] = R.lower;
+    }
+  }
+  return ADJ_OK;
 }
 
 adj_status_t adjprod_modp_ex(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, const uint32_t *A, int64_t lda,

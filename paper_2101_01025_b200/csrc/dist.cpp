@@ -11,6 +11,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/adjprod.h"
 #include "kernels.hpp"
@@ -29,6 +30,10 @@ struct NcclApi {
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*Reduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, int, ncclComm_t,
                          cudaStream_t) = nullptr;
+  ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
   const char *(*GetErrorString)(ncclResult_t) = nullptr;
 };
 NcclApi g_nccl;
@@ -48,6 +53,10 @@ bool load_nccl() {
   SYM("ncclCommInitRank", CommInitRank)
   SYM("ncclCommDestroy", CommDestroy)
   SYM("ncclReduce", Reduce)
+  SYM("ncclSend", Send)
+  SYM("ncclRecv", Recv)
+  SYM("ncclGroupStart", GroupStart)
+  SYM("ncclGroupEnd", GroupEnd)
   SYM("ncclGetErrorString", GetErrorString)
 #undef SYM
   g_nccl.loaded = true;
@@ -57,6 +66,92 @@ bool load_nccl() {
 }  // namespace
 
 int adj_phi_width(adj_phi_t phi);   // api.cpp
+
+namespace {
+// the packed regions (RectDev, buffer offsets) of `rank` for this problem
+adj_status_t rank_rects(int64_t m, int64_t k, uint32_t p, int depth, int rank, int G, std::vector<adj::RectDev> &out,
+                        int64_t *elems, int *max_rows) {
+  int64_t n = 0, e = 0;
+  adj_status_t st = adj_shard_layout(m, k, p, depth, rank, G, nullptr, 0, &n, &e);
+  if (st != ADJ_OK) return st;
+  std::vector<int64_t> raw((size_t)(5 * n));
+  if ((st = adj_shard_layout(m, k, p, depth, rank, G, raw.data(), n, &n, &e)) != ADJ_OK) return st;
+  out.resize((size_t)n);
+  int64_t off = 0;
+  *max_rows = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    adj::RectDev &R = out[(size_t)i];
+    R.r0 = raw[5 * i]; R.c0 = raw[5 * i + 1]; R.rows = raw[5 * i + 2]; R.cols = raw[5 * i + 3];
+    R.lower = (int32_t)raw[5 * i + 4]; R.pad_ = 0;
+    R.off = off;
+    off += R.rows * R.cols;
+    *max_rows = std::max<int>(*max_rows, (int)R.rows);
+  }
+  *elems = off;
+  return ADJ_OK;
+}
+
+// output-tile sharding: every rank computes its regions of Low(C) with the full A, the root
+// receives the other ranks' regions packed (only result tiles cross NVLink) and unpacks them
+adj_status_t dist_tiles(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, const uint32_t *A, int64_t lda, uint32_t *C,
+                        int64_t ldc, int root, adj_comm_t comm, const adj_opts_t *opts, adj_stream_t stream) {
+  const int G = comm->nranks, r = comm->rank;
+  adj_status_t st = adjprod_modp_shard(m, k, p, phi, A, lda, C, ldc, r, G, opts, stream);
+  if (st != ADJ_OK || G == 1) return st;
+  if (!load_nccl()) return ADJ_ERR_NCCL;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int depth = opts ? opts->depth : -1;
+  std::vector<std::vector<adj::RectDev>> rects((size_t)G);
+  std::vector<int64_t> elems((size_t)G, 0);
+  std::vector<int> max_rows((size_t)G, 0);
+  for (int q = 0; q < G; ++q) {
+    if (r != root && q != r) continue;
+    if ((st = rank_rects(m, k, p, depth, q, G, rects[(size_t)q], &elems[(size_t)q], &max_rows[(size_t)q])) != ADJ_OK)
+      return st;
+  }
+  // device copies of the region lists and the packed buffers
+  std::vector<void *> allocs;
+  auto dalloc = [&](size_t bytes) -> void * {
+    void *ptr = nullptr;
+    if (bytes && cudaMallocAsync(&ptr, bytes, s) == cudaSuccess) allocs.push_back(ptr);
+    return ptr;
+  };
+  std::vector<adj::RectDev *> drects((size_t)G, nullptr);
+  std::vector<uint32_t *> bufs((size_t)G, nullptr);
+  for (int q = 0; q < G; ++q) {
+    if (rects[(size_t)q].empty() || q == root) continue;
+    drects[(size_t)q] = static_cast<adj::RectDev *>(dalloc(rects[(size_t)q].size() * sizeof(adj::RectDev)));
+    bufs[(size_t)q] = static_cast<uint32_t *>(dalloc((size_t)elems[(size_t)q] * 4));
+    if (!drects[(size_t)q] || !bufs[(size_t)q]) st = ADJ_ERR_CUDA;
+    else if (cudaMemcpyAsync(drects[(size_t)q], rects[(size_t)q].data(), rects[(size_t)q].size() * sizeof(adj::RectDev),
+                             cudaMemcpyHostToDevice, s) != cudaSuccess) st = ADJ_ERR_CUDA;
+  }
+  if (st == ADJ_OK && r != root && bufs[(size_t)r] &&
+      adj::launch_rect_copy(drects[(size_t)r], (int)rects[(size_t)r].size(), max_rows[(size_t)r], C, ldc, bufs[(size_t)r], 1,
+                            s) != cudaSuccess)
+    st = ADJ_ERR_CUDA;
+  if (st == ADJ_OK) {
+    g_nccl.GroupStart();
+    for (int q = 0; q < G; ++q) {
+      if (q == root || !bufs[(size_t)q]) continue;
+      if (r == root) {
+        if (g_nccl.Recv(bufs[(size_t)q], (size_t)elems[(size_t)q], ncclUint32, q, comm->comm, s) != ncclSuccess) st = ADJ_ERR_NCCL;
+      } else if (q == r) {
+        if (g_nccl.Send(bufs[(size_t)q], (size_t)elems[(size_t)q], ncclUint32, root, comm->comm, s) != ncclSuccess) st = ADJ_ERR_NCCL;
+      }
+    }
+    if (g_nccl.GroupEnd() != ncclSuccess) st = ADJ_ERR_NCCL;
+  }
+  if (st == ADJ_OK && r == root)
+    for (int q = 0; q < G; ++q)
+      if (q != root && bufs[(size_t)q] &&
+          adj::launch_rect_copy(drects[(size_t)q], (int)rects[(size_t)q].size(), max_rows[(size_t)q], C, ldc,
+                                bufs[(size_t)q], 0, s) != cudaSuccess)
+        st = ADJ_ERR_CUDA;
+  for (void *ptr : allocs) cudaFreeAsync(ptr, s);
+  return st;
+}
+}  // namespace
 
 extern "C" {
 
@@ -104,6 +199,7 @@ adj_status_t adjprod_modp_dist(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, 
   if (m < 0 || k < 0) return ADJ_ERR_INVALID_VALUE;
   if (m == 0) return ADJ_OK;
   const int G = comm->nranks, r = comm->rank;
+  if (opts && (opts->flags & ADJ_DIST_TILES)) return dist_tiles(m, k, p, phi, A, lda, C, ldc, root, comm, opts, stream);
   const int w = adj_phi_width(phi);
   int64_t k0 = 0, k1 = 0;
   adj_dist_kslice(k, G, r, &k0, &k1);

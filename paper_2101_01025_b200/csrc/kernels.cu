@@ -1095,12 +1095,18 @@ template <> struct Pk8<uint32_t> {
 template <typename InT, typename OutT>
 __global__ void __launch_bounds__(256) combine_kernel(const __grid_constant__ CombParams P) {
   const CombNode &N = P.nodes[blockIdx.y];
-  // lower pair index -> (ti, tj), ti >= tj
+  // lower pair index -> (ti, tj), ti >= tj (or the sharded pair list)
   const int x = (int)blockIdx.x;
-  int ti = (int)((sqrtf(8.0f * (float)x + 1.0f) - 1.0f) * 0.5f);
-  while ((ti + 1) * (ti + 2) / 2 <= x) ++ti;
-  while (ti * (ti + 1) / 2 > x) --ti;
-  const int tj = x - ti * (ti + 1) / 2;
+  int ti, tj;
+  if (P.pairs != nullptr) {
+    ti = (int)(P.pairs[x] >> 16);
+    tj = (int)(P.pairs[x] & 0xFFFF);
+  } else {
+    ti = (int)((sqrtf(8.0f * (float)x + 1.0f) - 1.0f) * 0.5f);
+    while ((ti + 1) * (ti + 2) / 2 <= x) ++ti;
+    while (ti * (ti + 1) / 2 > x) --ti;
+    tj = x - ti * (ti + 1) / 2;
+  }
   const bool diag = ti == tj;
   const int tx = threadIdx.x & 7, ty = threadIdx.x >> 3;   // 8 x 32
   const int64_t mh = P.mh, ldp = P.ldp;                     // ldp multiple of 128 -> aligned 16-byte loads
@@ -1209,7 +1215,8 @@ __global__ void __launch_bounds__(256) combine_kernel(const __grid_constant__ Co
 cudaError_t launch_combine(const CombParams &p, cudaStream_t s) {
   if (p.n_nodes == 0) return cudaSuccess;
   const unsigned nt = (unsigned)((p.mh + 63) / 64);
-  dim3 grid(nt * (nt + 1) / 2, (unsigned)p.n_nodes), block(256);
+  dim3 grid(p.pairs ? (unsigned)p.n_pairs : nt * (nt + 1) / 2, (unsigned)p.n_nodes), block(256);
+  if (grid.x == 0) return cudaSuccess;
   if (p.in32) combine_kernel<uint32_t, uint32_t><<<grid, block, 0, s>>>(p);
   else if (p.out_u32) combine_kernel<uint16_t, uint32_t><<<grid, block, 0, s>>>(p);
   else combine_kernel<uint16_t, uint16_t><<<grid, block, 0, s>>>(p);
@@ -1742,6 +1749,28 @@ cudaError_t launch_scale_lower(int64_t m, int w, uint32_t *X, int64_t ldx, uint3
 }
 
 // Up(C) = phi(Low(C)) (Lemma lem:uplow): C[j][i] = C[i][j] (conjugated for phi = H), i > j
+// one block per (region row, region); threads over the columns
+__global__ void __launch_bounds__(256) rect_copy_kernel(const RectDev *rects, uint32_t *C, int64_t ldc, uint32_t *buf,
+                                                        int to_buf) {
+  const RectDev R = rects[blockIdx.y];
+  const int64_t i = blockIdx.x;
+  if (i >= R.rows) return;
+  uint32_t *c = C + (R.r0 + i) * ldc + R.c0;
+  uint32_t *b = buf + R.off + i * R.cols;
+  const int64_t ncol = R.lower ? min64(R.cols, R.r0 + i - R.c0 + 1) : R.cols;
+  for (int64_t j = threadIdx.x; j < ncol; j += blockDim.x) {
+    if (to_buf) b[j] = c[j];
+    else c[j] = b[j];
+  }
+}
+
+cudaError_t launch_rect_copy(const RectDev *rects, int n, int max_rows, uint32_t *C, int64_t ldc, uint32_t *buf,
+                             int to_buf, cudaStream_t s) {
+  if (n == 0 || max_rows == 0) return cudaSuccess;
+  rect_copy_kernel<<<dim3((unsigned)max_rows, (unsigned)n), 256, 0, s>>>(rects, C, ldc, buf, to_buf);
+  return cudaGetLastError();
+}
+
 __global__ void __launch_bounds__(256) fill_upper_kernel(int64_t m, int w, uint32_t *C, int64_t ldc, ModP mod) {
   const int ti = blockIdx.y, tj = blockIdx.x;
   if (ti < tj) return;

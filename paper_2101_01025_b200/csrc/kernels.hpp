@@ -21,6 +21,9 @@ cudaError_t launch_scale_lower(int64_t m, int w, uint32_t *X, int64_t ldx, uint3
                                cudaStream_t s);
 cudaError_t launch_mod_lower(int64_t m, int w, const uint32_t *src, int64_t lds, uint32_t *dst, int64_t ldd,
                              const ModP &mod, cudaStream_t s);
+// pack (to_buf = 1) / unpack (to_buf = 0) the listed regions of C into / from a contiguous buffer
+cudaError_t launch_rect_copy(const RectDev *rects, int n, int max_rows, uint32_t *C, int64_t ldc, uint32_t *buf,
+                             int to_buf, cudaStream_t s);
 cudaError_t launch_fill_upper(int64_t m, int w, uint32_t *C, int64_t ldc, const ModP &mod, cudaStream_t s);
 
 }  // namespace adj

@@ -182,8 +182,87 @@ int auto_depth(int64_t m, int64_t k, uint32_t p, int phi) {
   return d;
 }
 
+// ---------------------------------------------------------------- output-tile sharding
+// Ownership unit: a pair {(I, J), (J, I)}, I >= J, of 256 x 256 tiles of the top-level product
+// grid (depth 1: the (m/2) grid of P1..P5; depth 0: the grid of C).  Cost in leaf-tile units: a
+// diagonal pair has its SYRK tile(s) and, at depth 1, the P3 / P4 tiles (I, I); an off-diagonal
+// pair twice the GEMM tiles.  Pairs go, largest first, to the least loaded rank (deterministic).
+std::vector<int> shard_owners(int64_t T, int depth, int nranks) {
+  std::vector<int> owner((size_t)(T * (T + 1) / 2), 0);
+  std::vector<std::pair<int, int64_t>> order;   // (cost, pair index)
+  for (int64_t I = 0; I < T; ++I)
+    for (int64_t J = 0; J <= I; ++J) {
+      const int cost = depth == 0 ? 1 : (I == J ? 5 : 7);
+      order.push_back({cost, I * (I + 1) / 2 + J});
+    }
+  std::stable_sort(order.begin(), order.end(), [](const std::pair<int, int64_t> &a, const std::pair<int, int64_t> &b) {
+    return a.first > b.first;
+  });
+  std::vector<int64_t> load((size_t)nranks, 0);
+  for (const auto &o : order) {
+    int best = 0;
+    for (int r = 1; r < nranks; ++r)
+      if (load[r] < load[best]) best = r;
+    owner[(size_t)o.second] = best;
+    load[best] += o.first;
+  }
+  return owner;
+}
+
+bool apply_shard(Plan &P, int rank, int nranks, const char **err) {
+  if (P.kind != PLAN_SYRK_T || P.depth > 1) { *err = "tile sharding supports phi = T at depth 0 or 1"; return false; }
+  P.shard_rank = rank;
+  P.shard_n = nranks;
+  const int64_t grid_rows = P.depth == 0 ? P.rows_pad0 : P.lv[1].rows_pad;
+  const int64_t T = (grid_rows + 255) / 256;
+  const std::vector<int> owner = shard_owners(T, P.depth, nranks);
+  auto owns = [&](int64_t I, int64_t J) {
+    const int64_t a = std::max(I, J), b = std::min(I, J);
+    return owner[(size_t)(a * (a + 1) / 2 + b)] == rank;
+  };
+  std::vector<uint32_t> kept;
+  for (size_t t = 0; t + 1 < P.tiles.size(); t += 2) {
+    const uint32_t x = P.tiles[t];
+    if (owns((x >> 12) & 0xFFF, x & 0xFFF)) { kept.push_back(x); kept.push_back(P.tiles[t + 1]); }
+  }
+  P.tiles.swap(kept);
+  // C regions this rank writes (for packing / gathering) and, at depth 1, the 64 x 64 lower tile
+  // pairs of the K4 combine inside the owned 256-pairs
+  P.shard_rects.clear();
+  P.comb_pairs.clear();
+  const int64_t m = P.m;
+  auto rect = [&](int64_t r0, int64_t c0, int64_t nr, int64_t nc, int lower) {
+    nr = std::min(nr, m - r0);
+    nc = std::min(nc, m - c0);
+    if (nr > 0 && nc > 0) P.shard_rects.push_back({r0, c0, nr, nc, lower});
+  };
+  if (P.depth == 0) {
+    for (int64_t I = 0; I < T; ++I)
+      for (int64_t J = 0; J <= I; ++J)
+        if (owns(I, J)) rect(256 * I, 256 * J, 256, 256, I == J);
+    return true;
+  }
+  const int64_t mh = P.lv[1].mh;
+  for (int64_t I = 0; I < T; ++I)
+    for (int64_t J = 0; J <= I; ++J) {
+      if (!owns(I, J)) continue;
+      for (int64_t ti = 4 * I; ti < 4 * I + 4; ++ti)
+        for (int64_t tj = 4 * J; tj < 4 * J + 4; ++tj)
+          if (ti >= tj && 64 * ti < mh && 64 * tj < mh) P.comb_pairs.push_back((uint32_t)(ti << 16 | tj));
+      // rows/cols of the product grid clipped to mh, then placed in C's quadrants
+      const int64_t r0 = 256 * I, c0 = 256 * J;
+      const int64_t nr = std::min<int64_t>(256, mh - r0), nc = std::min<int64_t>(256, mh - c0);
+      if (nr <= 0 || nc <= 0) continue;
+      rect(r0, c0, nr, nc, I == J);                  // C11 = Low(U3)
+      rect(mh + r0, c0, nr, nc, 0);                  // C21 = U4 on (I, J)
+      if (I != J) rect(mh + c0, r0, nc, nr, 0);      // C21 = U4 on (J, I)
+      rect(mh + r0, mh + c0, nr, nc, I == J);        // C22 = Low(U5)
+    }
+  return true;
+}
+
 bool build_syrk_plan(Plan &P, int64_t m, int64_t k, uint32_t p, int phi, int depth, int num_sms,
-                     const char **err) {
+                     const char **err, int shard_rank, int shard_n) {
   P = Plan();
   P.kind = phi == 0 ? PLAN_SYRK_T : (phi == 1 ? PLAN_SYRK_H : PLAN_QUAT);
   P.m = m; P.n = m; P.k = k; P.depth = depth;
@@ -309,6 +388,7 @@ bool build_syrk_plan(Plan &P, int64_t m, int64_t k, uint32_t p, int phi, int dep
   }
   if ((int)P.prods.size() > kMaxProducts) { *err = "too many leaf products"; return false; }
   append_tiles(P);
+  if (shard_n > 0 && !apply_shard(P, shard_rank, shard_n, err)) return false;
   set_grid(P, num_sms);
   return true;
 }

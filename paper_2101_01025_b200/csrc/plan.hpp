@@ -19,6 +19,11 @@ enum PlanKind : int { PLAN_SYRK_T = 0, PLAN_SYRK_H = 1, PLAN_GEMM = 2, PLAN_HERK
 enum QuatOp : int { QO_A = 0, QO_B, QO_C, QO_D, QO_U1, QO_U2, QO_W, QO_N };
 
 
+struct ShardRect {
+  int64_t r0, c0, rows, cols;
+  int lower;             // only elements with col <= row belong to the shard
+};
+
 struct ArenaPlan {
   int64_t kpad = 0;      // bytes per row (K padded to 128)
   int64_t n_rows = 0;    // total rows (all operands x planes)
@@ -77,11 +82,17 @@ struct Plan {
   int grid = 1;
   int dev = 0;
   LeafParams leaf_template;           // terms, weights, mod (maps/outs bound per call)
+  // output-tile sharding (adjprod_modp_shard): this plan computes only the tiles `shard_rank` owns
+  int shard_rank = -1, shard_n = 0;
+  std::vector<ShardRect> shard_rects;  // the regions of C it writes (Low part when `lower`)
+  std::vector<uint32_t> comb_pairs;    // depth 1: K4 64 x 64 lower tile pairs (ti << 16 | tj)
+  uint32_t *d_comb_pairs = nullptr;
 };
 
 // Build (host only, no CUDA calls).  Returns false with *err set if unsupported.
 bool build_syrk_plan(Plan &P, int64_t m, int64_t k, uint32_t p, int phi, int depth, int num_sms,
-                     const char **err);
+                     const char **err, int shard_rank = -1, int shard_n = 0);
+std::vector<int> shard_owners(int64_t T, int depth, int nranks);
 bool build_gemm_plan(Plan &P, int64_t m, int64_t n, int64_t k, uint32_t p, int num_sms, const char **err);
 bool build_herk1_plan(Plan &P, int64_t m, int64_t k, uint32_t p, int num_sms, const char **err);
 int auto_depth(int64_t m, int64_t k, uint32_t p, int phi);

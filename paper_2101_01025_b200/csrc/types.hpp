@@ -135,6 +135,8 @@ struct CombParams {
   uint32_t alpha, beta;    // axpby on the final (uint32) output, SYRK form
   int32_t axpby;
   int32_t in32;            // P buffers hold uint32 residues (p > 2^16)
+  const uint32_t *pairs;   // output-tile sharding: the (ti << 16 | tj) lower tile pairs to do (else all)
+  int32_t n_pairs;
 };
 
 // ---------------------------------------------------------------- GF(p^2) Alg. 1 (PLAN_HERK1)
@@ -180,6 +182,13 @@ struct QuatCombParams {
   ModP mod;
   uint32_t alpha, beta;
   int32_t axpby, in32;
+};
+
+// ---------------------------------------------------------------- output-tile sharding: pack / unpack
+struct RectDev {
+  int64_t r0, c0, rows, cols;  // region of C (uint32 residues)
+  int64_t off;                 // element offset of its rows x cols block in the packed buffer
+  int32_t lower, pad_;         // lower: only col <= row is copied back into C
 };
 
 }  // namespace adj

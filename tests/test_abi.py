@@ -114,3 +114,34 @@ def test_herk_alg1_workspace_planning():
     # ignored for phi = T
     assert adj.adjprod_modp_workspace_size(m, k, p, 0, depth=1, flags=adj.ADJ_HERK_ALG1) == \
         adj.adjprod_modp_workspace_size(m, k, p, 0, depth=1)
+
+
+@pytest.mark.parametrize("m,k,depth", [(1, 5, 0), (100, 64, 0), (1000, 500, 0), (1000, 700, 1), (3000, 256, 1),
+                                       (4097, 1000, 1)])
+@pytest.mark.parametrize("nranks", [1, 2, 3, 5, 8])
+def test_shard_layout_partitions_low_c(m, k, depth, nranks):
+    """Output-tile sharding: the regions adj_shard_layout gives the ranks
+    cover every element of Low(C) exactly once and nothing above the diagonal."""
+    import numpy as np
+    cover = np.zeros((m, m), dtype=np.int32)
+    for r in range(nranks):
+        for (r0, c0, rows, cols, lower) in adj.adj_shard_layout(m, k, 8191, r, nranks, depth=depth):
+            assert 0 <= r0 and r0 + rows <= m and 0 <= c0 and c0 + cols <= m
+            blk = np.ones((rows, cols), dtype=np.int32)
+            if lower:
+                ii, jj = np.meshgrid(np.arange(rows) + r0, np.arange(cols) + c0, indexing="ij")
+                blk = (jj <= ii).astype(np.int32)
+            cover[r0:r0 + rows, c0:c0 + cols] += blk
+    assert np.array_equal(cover, np.tril(np.ones((m, m), dtype=np.int32)))
+
+
+def test_shard_layout_balanced():
+    """The deterministic greedy deal keeps the ranks' shares within one 256-tile pair."""
+    m, k = 8192, 8192
+    for depth in (0, 1):
+        for n in (2, 4, 8):
+            sizes = []
+            for r in range(n):
+                rects = adj.adj_shard_layout(m, k, 8191, r, n, depth=depth)
+                sizes.append(sum(rows * cols for (_, _, rows, cols, _) in rects))
+            assert max(sizes) - min(sizes) <= 4 * 256 * 256, (depth, n, sizes)

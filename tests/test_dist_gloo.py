@@ -75,3 +75,61 @@ def test_kslice_partition():
                 assert 0 <= k0 <= k1 <= k and (k0 % 8 == 0 or k0 == k)
                 cover.extend(range(k0, k1))
             assert cover == list(range(k)), (k, G)
+
+
+def _tiles_worker(rank, world, port, cases, out_q):
+    """Output-tile sharding (ADJ_DIST_TILES): every rank computes the regions of Low(C) it owns
+    (adj_shard_layout, here with the oracle on the full A), packs them row by row in region order
+    -- the layout dist_tiles' pack kernel uses -- and the root receives and unpacks them."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle
+    import paper_2101_01025_b200 as adj
+    from inputs import uniform_matrix
+    try:
+        for (m, k, p, depth) in cases:
+            A = uniform_matrix(m, k, seed=5, p=p)
+            full = oracle.syrk_t(A, p)
+            mine = adj.adj_shard_layout(m, k, p, rank, world, depth=depth)
+            buf = np.concatenate([full[r0:r0 + rows, c0:c0 + cols].reshape(-1) for (r0, c0, rows, cols, _) in mine]
+                                 or [np.zeros(0, dtype=np.uint32)]).astype(np.int64)
+            n = torch.tensor([buf.size])
+            sizes = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+            dist.all_gather(sizes, n)
+            if rank == 0:
+                C = np.zeros((m, m), dtype=np.uint32)
+                parts = {0: buf}
+                for q in range(1, world):
+                    t = torch.zeros(int(sizes[q]), dtype=torch.int64)
+                    dist.recv(t, src=q)
+                    parts[q] = t.numpy()
+                for q in range(world):
+                    off = 0
+                    for (r0, c0, rows, cols, lower) in adj.adj_shard_layout(m, k, p, q, world, depth=depth):
+                        blk = parts[q][off:off + rows * cols].reshape(rows, cols)
+                        off += rows * cols
+                        for i in range(rows):
+                            ncol = min(cols, r0 + i - c0 + 1) if lower else cols
+                            C[r0 + i, c0:c0 + ncol] = blk[i, :ncol]
+                out_q.put((m, k, p, depth, bool(np.array_equal(C, full))))
+            else:
+                dist.send(torch.from_numpy(buf), dst=0)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_tile_sharding_gather_gloo(world):
+    cases = [(300, 40, 8191, 0), (700, 33, 97, 1), (5, 3, 65521, 0), (1030, 16, 8191, 1)]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_tiles_worker, args=(r, world, port, cases, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = [q.get(timeout=300) for _ in cases]
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    assert all(ok for (*_, ok) in res), res

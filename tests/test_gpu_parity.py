@@ -355,3 +355,56 @@ def test_quat_overflow_stress_constant(adj):
     got = to_host(adj.adjprod(to_dev(M), p, phi="Q", depth=0))
     ref = oracle.syrk_q(M[:2], p)
     assert (got[np.tril_indices(m)] == ref[1, 0]).all()
+
+
+# ---------------------------------------------------------------- SURVEY.md §8(e)-2
+# Output-tile sharding: every rank's share (adjprod_modp_shard) run one after the other on this
+# device into one C must give all of Low(C); one share writes only its own regions.
+@pytest.mark.parametrize("p", [97, 8191, 65521, 131071])
+@pytest.mark.parametrize("depth", [0, 1])
+@pytest.mark.parametrize("m,k", [(5, 3), (300, 200), (1030, 520)])
+@pytest.mark.parametrize("nranks", [1, 2, 3, 5])
+def test_shard_all_ranks_give_low_c(adj, p, depth, m, k, nranks):
+    import torch
+    A = uniform_matrix(m, k, seed=m + nranks, p=p)
+    dA = to_dev(A)
+    C = torch.full((m, m), -1, dtype=torch.int32, device="cuda")
+    for r in range(nranks):
+        adj.adjprod_modp_shard(m, k, p, 0, dA, k, C, m, r, nranks, depth=depth)
+    got = to_host(C)
+    lo = np.tril(np.ones((m, m), dtype=bool))
+    assert np.array_equal(got[lo], oracle.syrk_t(A, p)[lo])
+    assert (got[~lo] == 0xFFFFFFFF).all()
+
+
+def test_shard_writes_only_its_regions(adj):
+    import torch
+    p, m, k, n = 8191, 1030, 300, 3
+    A = uniform_matrix(m, k, seed=2, p=p)
+    ref = oracle.syrk_t(A, p)
+    for depth in (0, 1):
+        for r in range(n):
+            C = torch.full((m, m), -1, dtype=torch.int32, device="cuda")
+            adj.adjprod_modp_shard(m, k, p, 0, to_dev(A), k, C, m, r, n, depth=depth)
+            got = to_host(C)
+            mine = np.zeros((m, m), dtype=bool)
+            for (r0, c0, rows, cols, lower) in adj.adj_shard_layout(m, k, p, r, n, depth=depth):
+                ii, jj = np.meshgrid(np.arange(rows) + r0, np.arange(cols) + c0, indexing="ij")
+                mine[r0:r0 + rows, c0:c0 + cols] = (jj <= ii) if lower else True
+            assert np.array_equal(got[mine], ref[mine])
+            assert (got[~mine] == 0xFFFFFFFF).all()
+
+
+def test_dist_tiles_single_rank(adj):
+    """ADJ_DIST_TILES through the NCCL entry point with one rank (the multi-rank gather is covered
+    by tests/test_dist_gloo.py)."""
+    import torch
+    p, m, k = 8191, 700, 300
+    A = uniform_matrix(m, k, seed=8, p=p)
+    comm = adj.adj_comm_init(1, adj.adj_comm_get_unique_id(), 0)
+    try:
+        C = torch.zeros((m, m), dtype=torch.int32, device="cuda")
+        adj.adjprod_modp_dist(m, k, p, 0, to_dev(A), k, C, m, 0, comm, depth=1, flags=adj.ADJ_DIST_TILES)
+        assert np.array_equal(low(to_host(C)), oracle.syrk_t(A, p))
+    finally:
+        adj.adj_comm_destroy(comm)
