@@ -258,6 +258,11 @@ def run_gpu(args, cfg, rank, world, local_rank):
     flags = adj.ADJ_HERK_ALG1 if alg1 else 0
     depth = args.depth if args.depth is not None else (cfg["depth"] if cfg["depth"] is not None
                                                        else (1 if alg1 else adj.adjprod_modp_auto_depth(m, k, p, phi)))
+    # N > 1: output-tile sharding for square phi = T problems (depth <= 1), split-K otherwise
+    dist_mode = args.dist if args.dist != "auto" else ("tiles" if cfg["phi"] == "T" and k <= 2 * m else "splitk")
+    dist_flags = adj.ADJ_DIST_TILES if (world > 1 and dist_mode == "tiles") else 0
+    if dist_flags:
+        depth = min(depth, 1)
     A = torch.empty((m, k * w), dtype=torch.int32, device=dev)
     uniform_residues_cuda(A, seed=1, p=p)
     C = torch.zeros((m, m * w), dtype=torch.int32, device=dev)
@@ -268,7 +273,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
         dist.broadcast_object_list(obj, src=0)
         comm = adj.adj_comm_init(world, obj[0], rank)
         k0, k1 = adj.adj_dist_kslice(k, world, rank)
-        ws_bytes = adj.adjprod_modp_workspace_size(m, max(1, k1 - k0), p, phi, depth)
+        ws_bytes = 0   # the library allocates stream-ordered workspace inside adjprod_modp_dist
     else:
         ws_bytes = adj.adjprod_modp_workspace_size(m, k, p, phi, depth, flags)
     ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
@@ -280,7 +285,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
             adj.adjprod_modp_ex(m, k, p, phi, A, k, C, m, depth=depth, flags=flags, workspace=ws,
                                 workspace_bytes=ws_bytes, stream=stream)
         else:
-            adj.adjprod_modp_dist(m, k, p, phi, A, k, C, m, 0, comm, depth=depth, stream=stream)
+            adj.adjprod_modp_dist(m, k, p, phi, A, k, C, m, 0, comm, depth=depth, flags=dist_flags, stream=stream)
 
     for _ in range(max(args.warmup, 3)):
         flush.zero_()
@@ -410,7 +415,9 @@ def run_gpu(args, cfg, rank, world, local_rank):
             "config": {"workload": cfg["workload"] + (" via Alg. 1 over GF(p^2) (ADJ_HERK_ALG1)" if alg1 else ""),
                        "m": m, "k": k, "p": p, "phi": cfg["phi"], "depth": depth,
                        "seed": 1, "l2": "flushed before every timed step (256 MiB write, outside step events)",
-                       "parallelism": f"split-K x{world} (NCCL reduce)" if world > 1 else "1 GPU",
+                       "parallelism": ("1 GPU" if world == 1 else
+                                       (f"output tiles x{world} (NCCL send/recv gather of result tiles)" if dist_flags
+                                        else f"split-K x{world} (NCCL reduce)")),
                        "fraction_of_int8_peak_effective": value / (peak * 1e12 / 2),
                        "ring_macs_per_step": mh, "limb_mmas_per_ring_mac": limb_mmas(p)},
             "roofline": roof,
@@ -436,6 +443,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-check", action="store_true", help="skip the sampled parity check")
+    ap.add_argument("--dist", default="auto", choices=["auto", "splitk", "tiles"],
+                    help="N > 1: split-K (NCCL reduce) or output-tile sharding (gather of result tiles)")
     ap.add_argument("--herk", default="2m", choices=["2m", "alg1"],
                     help="phi = H: 2M reduction (default) or one level of Alg. 1 over GF(p^2)")
     args = ap.parse_args()
