@@ -80,6 +80,35 @@ def leaf_int8_ops(cfg, depth, herk="2m") -> float:
     return 2.0 * macs * limb_mmas(p)
 
 
+def hbm_bytes(cfg, depth, herk="2m"):
+    """Algorithmic HBM bytes per step of the HBM-bound classes (K1 pre-addition / split and the
+    recombination), for the layouts DESIGN.md §4 describes: read each input once, write each
+    limb plane / residue once.  None where not derived (depth >= 2, phi = H via ADJ_HERK_ALG1)."""
+    m, k, p = cfg["m"], cfg["k"], cfg["p"]
+    w = {"T": 1, "H": 2, "Q": 4}[cfg["phi"]]
+    planes = {1: 1, 3: 3, 4: 2, 6: 6}[limb_mmas(p)]
+    rp = lambda x: -(-x // 128) * 128
+    res = 4 if p > 65535 else 2
+    out_c = m * (m + 1) // 2 * 4 * w                      # Low(C), uint32 words
+    if cfg["phi"] == "H" and herk == "alg1":
+        return None
+    if depth == 0:
+        nops = {1: 1, 2: 3, 4: 7}[w]                       # A | X, Y, T | A, B, C, D, U1, U2, W
+        pre = 4 * w * m * k + nops * planes * rp(m) * rp(k)
+        if w == 1:
+            comb = None                                    # the leaf epilogue writes C directly
+        else:
+            nbuf = {2: (1, 1), 4: (5, 1)}[w]               # full buffers read (H | Q1..Q5), lower ones (G | Q6)
+            comb = (nbuf[0] * m * m + nbuf[1] * m * (m + 1) // 2) * res + out_c
+        return {"preadd": pre, "combine": comb}
+    if depth == 1 and w == 1:
+        mh, kh = -(-m // 2), 8 * -(-k // 16)
+        pre = 4 * m * k + 7 * planes * rp(mh) * max(128, -(-kh // 128) * 128)
+        comb = (3 * mh * (mh + 1) // 2 + 2 * mh * mh) * res + out_c
+        return {"preadd": pre, "combine": comb}
+    return None
+
+
 def load_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -398,6 +427,18 @@ def run_gpu(args, cfg, rank, world, local_rank):
             "algorithmic_ops_per_launch": ops, "leaf_ms_per_launch": leaf_avg_ms,
             "leaf_launches_per_step": leaf_n / args.steps}
     share = {c: round(v[0] / max(1e-9, sum(x[0] for x in prof.values())), 4) for c, v in prof.items()}
+    # achieved HBM bandwidth of the HBM-bound kernels (algorithmic bytes / device time per step)
+    hb = hbm_bytes(cfg, depth, args.herk)
+    hbm = None
+    if hb is not None:
+        hbm = {}
+        for cls, nbytes in hb.items():
+            t_ms = prof[cls][0] / args.steps
+            if nbytes is None or t_ms <= 0:
+                continue
+            gbs = nbytes / (t_ms * 1e-3) / 1e9
+            hbm[cls] = {"bound": "hbm", "algorithmic_bytes": nbytes, "ms": t_ms, "achieved": gbs,
+                        "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": gbs / peaks["hbm_gbs"]}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -425,6 +466,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
             "e2e": e2e,
             "gpu_launches": launches,
             "kernel_time_share": share,
+            "hbm_kernels": hbm,
             "clocks": clk.summary(),
             "parity": parity,
         }

@@ -668,6 +668,24 @@ __device__ __forceinline__ void put_limbs8(int8_t *base, int64_t plane_stride, c
   for (int pl = 0; pl < NP; ++pl) *reinterpret_cast<uint2 *>(base + pl * plane_stride) = make_uint2(w0[pl], w1[pl]);
 }
 
+// limb planes of 16 consecutive residues (four 4-groups), one 16-byte store per plane
+template <int SCHEME>
+__device__ __forceinline__ void put_limbs16(int8_t *base, int64_t plane_stride, const uint32_t (&x)[4][4],
+                                            const ModP &m) {
+  if constexpr (SCHEME == 3) {
+#pragma unroll
+    for (int g = 0; g < 4; ++g) put_limbs4_t6(base + 4 * g, plane_stride, x[g], m);
+    return;
+  }
+  constexpr int NP = SCHEME == 0 ? 1 : (SCHEME == 1 ? 3 : 2);
+  uint32_t w[4][3];
+#pragma unroll
+  for (int g = 0; g < 4; ++g) limbs4<SCHEME>(x[g], m, w[g]);
+#pragma unroll
+  for (int pl = 0; pl < NP; ++pl)
+    *reinterpret_cast<uint4 *>(base + pl * plane_stride) = make_uint4(w[0][pl], w[1][pl], w[2][pl], w[3][pl]);
+}
+
 template <int YK, bool WIDE = false>
 __device__ __forceinline__ void apply_Y4(const uint32_t (&a)[4], const uint32_t (&b)[4], uint32_t (&oa)[4],
                                          uint32_t (&ob)[4], uint32_t ya, uint32_t yb, const ModP &m) {
@@ -1032,7 +1050,44 @@ __global__ void __launch_bounds__(256) split_kernel(const __grid_constant__ Spli
   }
 }
 
+// Plain split (mode 0): one thread per (row, 16 columns), four 16-byte loads in flight before
+// the 16-byte limb-plane stores.
+template <int SCHEME>
+__global__ void __launch_bounds__(256) split_plain_kernel(const __grid_constant__ SplitParams P) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= P.kpad / 16) return;
+  const int64_t c0 = g * 16;
+  const int64_t ps = P.rows_pad * P.kpad;
+  const InView &v = P.in;
+  for (int64_t r = blockIdx.y; r < P.rows_pad; r += gridDim.y) {
+    InView vv = v;
+    if (r >= P.rows) vv.rows_valid = 0;
+    const bool fast = vv.vec_ok && vv.type == IN_U32 && r < vv.rows_valid && c0 + 15 < vv.cols_valid && c0 + 15 < P.cols;
+    uint32_t x[4][4];
+    if (fast) {
+#pragma unroll
+      for (int h = 0; h < 4; ++h) load4_fast<IN_U32>(v.ptr, r * v.ld + c0 + 4 * h, P.mod, x[h]);
+    } else {
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        InView vh = vv;
+        if (c0 + 4 * h >= P.cols) vh.cols_valid = 0;
+        load4(vh, r, c0 + 4 * h, P.mod, x[h]);
+      }
+    }
+    put_limbs16<SCHEME>(P.arena + (P.op_row + r) * P.kpad + c0, ps, x, P.mod);
+  }
+}
+
 cudaError_t launch_split(const SplitParams &p, cudaStream_t s) {
+  if (p.mode == 0) {
+    dim3 g16((unsigned)((p.kpad / 16 + 255) / 256), (unsigned)(p.rows_pad < 65535 ? p.rows_pad : 65535));
+    if (p.scheme == 0) split_plain_kernel<0><<<g16, 256, 0, s>>>(p);
+    else if (p.scheme == 1) split_plain_kernel<1><<<g16, 256, 0, s>>>(p);
+    else if (p.scheme == 2) split_plain_kernel<2><<<g16, 256, 0, s>>>(p);
+    else split_plain_kernel<3><<<g16, 256, 0, s>>>(p);
+    return cudaGetLastError();
+  }
   dim3 grid((unsigned)((p.kpad / 8 + 255) / 256), (unsigned)(p.rows_pad < 65535 ? p.rows_pad : 65535));
   if (p.scheme == 0) split_kernel<0><<<grid, 256, 0, s>>>(p);
   else if (p.scheme == 1) split_kernel<1><<<grid, 256, 0, s>>>(p);
