@@ -401,6 +401,52 @@ def run_gpu(args, cfg, rank, world, local_rank):
                "steps": e2e_steps, "pipelined": "3 streams (H2D | C-ABI call | D2H of Low(C) row blocks), 2 buffers",
                "last_row_matches_device_result": ok}
 
+    # ---------------- comparators on the same box (context, not the metric): our own depth-0 path
+    # (classical int8 SYRK, no Alg. 1 -- the on-box analogue of the paper's classical route,
+    # SURVEY.md §8(d)) and cuBLASLt int8 (torch._int_mm) as a library int8 throughput point
+    comparators = None
+    if world == 1 and not args.no_compare:
+        comparators = {}
+        if depth != 0 and not alg1:
+            ws0 = adj.adjprod_modp_workspace_size(m, k, p, phi, 0, flags)
+            w0 = torch.empty(max(ws0, 1), dtype=torch.uint8, device=dev)
+            C0 = torch.zeros_like(C)
+            for _ in range(3):
+                adj.adjprod_modp_ex(m, k, p, phi, A, k, C0, m, depth=0, flags=flags, workspace=w0, workspace_bytes=ws0,
+                                    stream=stream)
+            ts = []
+            for _ in range(max(3, min(args.steps, 10))):
+                flush.zero_()
+                a0, b0 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a0.record(stream)
+                adj.adjprod_modp_ex(m, k, p, phi, A, k, C0, m, depth=0, flags=flags, workspace=w0, workspace_bytes=ws0,
+                                    stream=stream)
+                b0.record(stream)
+                torch.cuda.synchronize()
+                ts.append(a0.elapsed_time(b0))
+            ms0 = statistics.median(ts)
+            comparators["depth0_classical"] = {"ms_per_step": ms0, "value": m * m * k / (ms0 * 1e-3), "unit": UNIT,
+                                               "same_result": bool(torch.equal(torch.tril(C0.view(m, -1)),
+                                                                               torch.tril(C.view(m, -1))))
+                                               if w == 1 else None}
+            del w0, C0
+        try:
+            n = 8192
+            xa = torch.randint(-128, 128, (n, n), dtype=torch.int8, device=dev)
+            xb = torch.randint(-128, 128, (n, n), dtype=torch.int8, device=dev)
+            for _ in range(3):
+                torch._int_mm(xa, xb)
+            a0, b0 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record()
+            for _ in range(10):
+                torch._int_mm(xa, xb)
+            b0.record()
+            torch.cuda.synchronize()
+            comparators["cublaslt_int8_8192_tops"] = 2.0 * n ** 3 * 10 / (a0.elapsed_time(b0) * 1e-3) / 1e12
+            del xa, xb
+        except Exception as e:  # noqa: BLE001 -- context only
+            comparators["cublaslt_int8_8192_tops"] = f"unavailable: {type(e).__name__}"
+
     # ---------------- parity spot check of the timed output (sampled rows vs the oracle)
     parity = None
     if rank == 0 and not args.no_check:
@@ -467,6 +513,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
             "gpu_launches": launches,
             "kernel_time_share": share,
             "hbm_kernels": hbm,
+            "comparators": comparators,
             "clocks": clk.summary(),
             "parity": parity,
         }
@@ -485,6 +532,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-check", action="store_true", help="skip the sampled parity check")
+    ap.add_argument("--no-compare", action="store_true", help="skip the depth-0 / cuBLASLt comparators")
     ap.add_argument("--dist", default="auto", choices=["auto", "splitk", "tiles"],
                     help="N > 1: split-K (NCCL reduce) or output-tile sharding (gather of result tiles)")
     ap.add_argument("--herk", default="2m", choices=["2m", "alg1"],

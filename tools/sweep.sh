@@ -8,5 +8,5 @@ for l in sys.stdin:
     print(d["config"]["workload"][:3], "d=%d" % d["config"]["depth"], "ms %.3f" % d["ms_per_step"], "val %.3e" % d["value"], "leaf %.3f" % r["frac"], "share", d["kernel_time_share"], "clk", d["clocks"]["sm_mhz"], d["clocks"]["reasons"], "W", d["clocks"].get("power_w_max"))'
 for spec in "$@"; do
   cfg=${spec%:*}; dep=${spec#*:}
-  timeout -s KILL 300 python bench.py --no-cpu --no-check --config $cfg --depth $dep ${BENCH_EXTRA} --steps ${STEPS:-10} 2>/dev/null | python -c "$summ"
+  timeout -s KILL 300 python bench.py --no-cpu --no-check --no-compare --config $cfg --depth $dep ${BENCH_EXTRA} --steps ${STEPS:-10} 2>/dev/null | python -c "$summ"
 done
