@@ -165,16 +165,22 @@ static void set_grid(Plan &P, int num_sms) {
   for (const ProductPlan &pp : P.prods) P.segmented |= pp.lp.kblocks > pp.lp.kseg;
 }
 
-// Depth choice (R13), from measured B200 crossovers: one level of Alg. alg:MIAHMM
-// saves 1/8 of the leaf MMA work but adds a K1 and a K4 pass over HBM; it pays once the leaves
-// stay >= 4096 rows (phi = T) -- for phi = H the 2M general product H dominates and the leaves
-// of G must stay >= 8192 rows.  Deeper levels are also used when the level-1 inner dimension
-// would exceed the int32 accumulation bound of the limb scheme.
+// Depth choice (R13), from measured B200 crossovers (profiles/r01/depth_crossover.txt):
+// one level of Alg. alg:MIAHMM saves 1/8 of the leaf MMA work but adds a K1 and a K4 pass over
+// HBM, and smaller leaves run the tcgen05 pipeline less efficiently.  It pays when the level's
+// leaf products stay large -- (m/2)^2 (k/2) >= 2^38 MACs each: 16384^2 x 16384 (d = 1),
+// 32768^2 x 32768 (d = 2) and 16384 x 131072 (d = 2) recurse, 8192^2 x 8192 does not (classical
+// is 8% faster there).  Under the power cap of the large configs the saved MMAs also buy clock.
+// phi = Q: Q6 is 1/11 of the 6M work; one level saves 1/8 of it -- never worth a K1 + K4 pass.
+// Deeper levels are also used when the inner dimension exceeds the int32 accumulation bound
+// of the limb scheme (K segmentation would handle it too; recursion also cuts the MMA work).
 int auto_depth(int64_t m, int64_t k, uint32_t p, int phi) {
-  // phi = Q: Q6 is 1/11 of the 6M work, one Alg. 1 level saves 1/8 of it -- never worth a K1 + K4 pass
-  const int64_t leaf_min = phi == 0 ? 4096 : (phi == 1 ? 8192 : ((int64_t)1 << 40));
   int d = 0;
-  while (d < 3 && cdiv(m, (int64_t)1 << (d + 1)) >= leaf_min && cdiv(k, (int64_t)1 << (d + 1)) >= 1024) ++d;
+  while (phi != 2 && d < 3) {
+    const double mh = (double)cdiv(m, (int64_t)1 << (d + 1)), kh = (double)cdiv(k, (int64_t)1 << (d + 1));
+    if (mh * mh * kh < 274877906944.0) break;   // 2^38
+    ++d;
+  }
   const int64_t kmax = limb_kmax(limb_scheme(p), p);
   int64_t kh = k;
   for (int l = 1; l <= d; ++l) kh = 8 * cdiv(kh, 16);

@@ -79,10 +79,13 @@ def test_validation_is_synchronous_and_needs_no_gpu():
 
 def test_workspace_and_depth_planning():
     assert adj.adjprod_modp_auto_depth(64, 64, 97, 0) == 0
-    assert adj.adjprod_modp_auto_depth(8192, 8192, 8191, 0) == 1        # c2
+    # measured B200 crossovers (R13): recurse while (m/2)^2 (k/2) >= 2^38 per level
+    assert adj.adjprod_modp_auto_depth(8192, 8192, 8191, 0) == 0        # c2: classical 8% faster
+    assert adj.adjprod_modp_auto_depth(16384, 16384, 8191, 0) == 1
     assert adj.adjprod_modp_auto_depth(16384, 131072, 8191, 0) == 2     # c4
-    assert adj.adjprod_modp_auto_depth(32768, 32768, 65521, 0) == 3     # c3
+    assert adj.adjprod_modp_auto_depth(32768, 32768, 65521, 0) == 2     # c3
     assert adj.adjprod_modp_auto_depth(8192, 8192, 8191, 1) == 0        # c5 (2M)
+    assert adj.adjprod_modp_auto_depth(8192, 8192, 8191, 2) == 0        # q5 (6M)
     # inner dimension above the int32 bound at depth 0 forces recursion (65521: k_max = 32896)
     assert adj.adjprod_modp_auto_depth(1000, 100000, 65521, 0) >= 2
     w0 = adj.adjprod_modp_workspace_size(8192, 8192, 8191, 0, depth=0)
