@@ -684,7 +684,7 @@ adj_status_t adjprod_modp_shard(int64_t m, int64_t k, uint32_t p, adj_phi_t phi,
   if (st != ADJ_OK) return st;
   if (phi != ADJ_PHI_T) return fail(ADJ_ERR_INVALID_VALUE, "output-tile sharding supports phi = ADJ_PHI_T");
   if (nranks < 1 || rank < 0 || rank >= nranks) return fail(ADJ_ERR_INVALID_VALUE, "rank %d of %d", rank, nranks);
-  if (opts && (opts->flags & ~0u) & ADJ_FILL_UPPER) return fail(ADJ_ERR_INVALID_VALUE, "ADJ_FILL_UPPER with sharding");
+  if (opts && (opts->flags & ADJ_FILL_UPPER)) return fail(ADJ_ERR_INVALID_VALUE, "ADJ_FILL_UPPER with sharding");
   if (m == 0) return ADJ_OK;
   const int depth = shard_depth(m, k, p, opts);
   if (depth > 1) return fail(ADJ_ERR_INVALID_VALUE, "output-tile sharding runs at depth 0 or 1 (got %d)", depth);

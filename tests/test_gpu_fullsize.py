@@ -93,3 +93,61 @@ def test_c5_vandermonde_hermitian(env):
     for r, (re, im) in zip(rows, ref):
         assert np.array_equal(Ch[r, : r + 1, 0].astype(np.int64), re) and \
             np.array_equal(Ch[r, : r + 1, 1].astype(np.int64), im), r
+
+
+def test_q5_quaternion_sampled_rows(env):
+    """SURVEY §8(f)-4 at the bench's q5 size (8192^2 over H_GF(8191), Alg. 2M3M)."""
+    torch, adj, bench = env
+    from inputs.gpu import uniform_residues_cuda
+    cfg = bench.CONFIGS["q5"]
+    m, k, p = cfg["m"], cfg["k"], cfg["p"]
+    A = torch.empty((m, k * 4), dtype=torch.int32, device="cuda")
+    uniform_residues_cuda(A, seed=1, p=p)
+    C = torch.zeros((m, m * 4), dtype=torch.int32, device="cuda")
+    adj.adjprod_modp_ex(m, k, p, adj.ADJ_PHI_Q, A, k, C, m)
+    torch.cuda.synchronize()
+    Ah = A.cpu().numpy().view(np.uint32).reshape(m, k, 4)
+    Ch = C.cpu().numpy().view(np.uint32).reshape(m, m, 4)
+    for r in (0, 4097, m - 1):
+        ref = oracle.syrk_q(Ah, p, rows=(r, r + 1))
+        assert np.array_equal(Ch[r, : r + 1], ref[r, : r + 1]), r
+
+
+def test_c5_herk_alg1_sampled_rows(env):
+    """SURVEY §8(f)-2 at c5 size: one level of Alg. 1 over GF(8191^2) (ADJ_HERK_ALG1)."""
+    torch, adj, bench = env
+    from inputs.gpu import uniform_residues_cuda
+    cfg = bench.CONFIGS["c5"]
+    m, k, p = cfg["m"], cfg["k"], cfg["p"]
+    A = torch.empty((m, k * 2), dtype=torch.int32, device="cuda")
+    uniform_residues_cuda(A, seed=1, p=p)
+    C = torch.zeros((m, m * 2), dtype=torch.int32, device="cuda")
+    adj.adjprod_modp_ex(m, k, p, adj.ADJ_PHI_H, A, k, C, m, flags=adj.ADJ_HERK_ALG1)
+    torch.cuda.synchronize()
+    Ah = A.cpu().numpy().view(np.uint32).reshape(m, k, 2)
+    Ch = C.cpu().numpy().view(np.uint32).reshape(m, m, 2)
+    for r in (0, 1, 4095, 4096, m - 1):
+        ref = oracle.syrk_h(Ah, p, rows=(r, r + 1))
+        assert np.array_equal(Ch[r, : r + 1], ref[r, : r + 1]), r
+
+
+@pytest.mark.parametrize("depth", [0, 1])
+def test_c2_output_tile_shards(env, depth):
+    """SURVEY §8(e)-2 at c2 size: the 8 ranks' shares run one after the other into one C give
+    Low(C) (sampled rows + Freivalds over the whole lower triangle)."""
+    torch, adj, bench = env
+    from inputs.gpu import uniform_residues_cuda
+    cfg = bench.CONFIGS["c2"]
+    m, k, p = cfg["m"], cfg["k"], cfg["p"]
+    A = torch.empty((m, k), dtype=torch.int32, device="cuda")
+    uniform_residues_cuda(A, seed=1, p=p)
+    C = torch.zeros((m, m), dtype=torch.int32, device="cuda")
+    for r in range(8):
+        adj.adjprod_modp_shard(m, k, p, 0, A, k, C, m, r, 8, depth=depth)
+    torch.cuda.synchronize()
+    Ah = A.cpu().numpy().view(np.uint32)
+    Ch = C.cpu().numpy().view(np.uint32)
+    for r in (0, 300, 4095, 4096, m - 1):
+        ref = oracle.syrk_t(Ah, p, rows=(r, r + 1))
+        assert np.array_equal(Ch[r, : r + 1], ref[r, : r + 1]), r
+    assert _freivalds(Ah, Ch, p)
