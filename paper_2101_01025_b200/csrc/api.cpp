@@ -127,10 +127,10 @@ adj_status_t get_encode() {
   return ADJ_OK;
 }
 
-adj_status_t encode_arena(CUtensorMap *map, void *base, int64_t kpad, int64_t rows) {
+adj_status_t encode_arena(CUtensorMap *map, void *base, int64_t kpad, int64_t rows, int box_rows = kBM) {
   cuuint64_t dims[2] = {(cuuint64_t)kpad, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)kpad};
-  cuuint32_t box[2] = {(cuuint32_t)kBK, (cuuint32_t)kBM};
+  cuuint32_t box[2] = {(cuuint32_t)kBK, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, base, dims, strides, box, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -244,8 +244,13 @@ adj_status_t launch_leaf_all(const Plan &P, const Ptrs &x, cudaStream_t s) {
   for (size_t a = 0; a < P.arenas.size(); ++a) {
     st = encode_arena(&L.maps[a], x.ws + P.arenas[a].offset, P.arenas[a].kpad, P.arenas[a].n_rows);
     if (st != ADJ_OK) return st;
+    st = encode_arena(&L.maps_half[a], x.ws + P.arenas[a].offset, P.arenas[a].kpad, P.arenas[a].n_rows, kBM / 2);
+    if (st != ADJ_OK) return st;
   }
-  for (size_t a = P.arenas.size(); a < (size_t)kMaxMaps; ++a) L.maps[a] = L.maps[0];
+  for (size_t a = P.arenas.size(); a < (size_t)kMaxMaps; ++a) {
+    L.maps[a] = L.maps[0];
+    L.maps_half[a] = L.maps_half[0];
+  }
   for (size_t q = 0; q < P.prods.size(); ++q) {
     const ProductPlan &pp = P.prods[q];
     L.prod[q] = pp.lp;

@@ -31,9 +31,15 @@ __device__ __forceinline__ void decode_tile(uint32_t packed, int &q, int &I, int
   J = (int)(packed & 0xFFF);
 }
 
-// k-block range and fixup piece of a job (whole tile: [0, kblocks), piece 0)
-__device__ __forceinline__ void decode_range(uint32_t y, int kblocks, int &kb0, int &kb1, int &piece) {
-  if (y == 0) { kb0 = 0; kb1 = kblocks; piece = 0; return; }
+// k-block range, fixup piece and column half of a job (whole tile: [0, kblocks), piece 0,
+// nhalf 0; nhalf 1 / 2: columns 0..127 / 128..255 of the tile with an N = 128 MMA)
+__device__ __forceinline__ void decode_range(uint32_t y, int kblocks, int &kb0, int &kb1, int &piece, int &nhalf) {
+  nhalf = 0;
+  if (y == 0 || (y & 0xFFFFFFu) == 0xFFFFFFu) {   // whole tile, or column half (empty range sentinel)
+    kb0 = 0; kb1 = kblocks; piece = 0;
+    if (y != 0) nhalf = 1 + (int)(y >> 24);
+    return;
+  }
   kb0 = (int)(y & 0xFFF);
   kb1 = (int)((y >> 12) & 0xFFF);
   piece = (int)(y >> 24);
@@ -157,7 +163,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (ADJ_EPI_WARPS 
       ptx::mbar_init(&slot_empty[s], 2 * EW);   // epilogue warps x 2 CTAs (used in the leader)
     }
     ptx::fence_barrier_init();
-    for (int i = 0; i < kMaxMaps; ++i) ptx::prefetch_tmap(&P.maps[i]);
+    for (int i = 0; i < kMaxMaps; ++i) {
+      ptx::prefetch_tmap(&P.maps[i]);
+      ptx::prefetch_tmap(&P.maps_half[i]);
+    }
   }
   if (warp == W_ALLOC) ptx::tmem_alloc_2sm(tmem_holder, 512);
   ptx::tc_fence_before();
@@ -176,17 +185,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (ADJ_EPI_WARPS 
       long long t_empty = 0, t_tma = 0, t_begin = clock64();
       uint2 next = cid < P.n_tiles ? __ldg(&P.tiles[cid]) : make_uint2(0u, 0u);
       for (int t = cid; t < P.n_tiles; t += ncl) {
-        int q, I, J, jb0, jb1, piece;
+        int q, I, J, jb0, jb1, piece, nh;
         decode_tile(next.x, q, I, J);
         const uint32_t range = next.y;
         if (t + ncl < P.n_tiles) next = __ldg(&P.tiles[t + ncl]);   // prefetch the next job
         const LeafProduct &pr = P.prod[q];
         const CUtensorMap *map = &P.maps[pr.map];
         const int kseg = pr.kseg;
-        decode_range(range, pr.kblocks, jb0, jb1, piece);
+        decode_range(range, pr.kblocks, jb0, jb1, piece, nh);
+        const CUtensorMap *bmap = nh ? &P.maps_half[pr.map] : map;
         const int a_pr = pr.a_plane_rows, b_pr = pr.b_plane_rows;
         const int arow = pr.a_row0 + I * Cfg::TILE + (int)rank * 128;
-        const int brow = pr.b_row0 + J * Cfg::TILE + (int)rank * 128;
+        // N = 128 half jobs: this CTA's 64 rows of the B column half
+        const int brow = nh ? pr.b_row0 + J * Cfg::TILE + (nh - 1) * 128 + (int)rank * 64
+                            : pr.b_row0 + J * Cfg::TILE + (int)rank * 128;
+        const uint32_t stage_tx = nh ? 2 * (Cfg::A_BYTES + Cfg::B_BYTES / 2) : 2 * Cfg::STAGE_BYTES;
         const int nseg = (jb1 - jb0 + kseg - 1) / kseg;
 #pragma unroll 1
         for (int u = 0; u < NACC * nseg; ++u) {
@@ -209,10 +222,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (ADJ_EPI_WARPS 
                 if (leader) ptx::mbar_arrive(&full_bar[stage]);
               } else {
                 const bool skip_b = (P.debug & 256) != 0;   // diagnostics: A operand only (L2-bound test)
-                if (leader) ptx::mbar_expect_tx(&full_bar[stage], skip_b ? 2 * Cfg::A_BYTES : 2 * Cfg::STAGE_BYTES);
+                if (leader) ptx::mbar_expect_tx(&full_bar[stage], skip_b ? 2 * Cfg::A_BYTES : stage_tx);
                 uint8_t *sa = smem + stage * Cfg::STAGE_BYTES;
                 ptx::tma_load_2d_2sm(sa, map, kb * kBK, tt ? ar1 : ar0, &full_bar[stage]);
-                if (!skip_b) ptx::tma_load_2d_2sm(sa + Cfg::A_BYTES, map, kb * kBK, tt ? br1 : br0, &full_bar[stage]);
+                if (!skip_b) ptx::tma_load_2d_2sm(sa + Cfg::A_BYTES, bmap, kb * kBK, tt ? br1 : br0, &full_bar[stage]);
               }
               if (prof) t_tma += clock64() - c1;
               if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
@@ -235,21 +248,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (ADJ_EPI_WARPS 
       long long t_full = 0, t_slot = 0, t_issue = 0, t_begin = clock64();
       uint2 next = cid < P.n_tiles ? __ldg(&P.tiles[cid]) : make_uint2(0u, 0u);
       for (int t = cid; t < P.n_tiles; t += ncl) {
-        int q, I, J, jb0, jb1, piece;
+        int q, I, J, jb0, jb1, piece, nh;
         decode_tile(next.x, q, I, J);
         const uint32_t range = next.y;
         if (t + ncl < P.n_tiles) next = __ldg(&P.tiles[t + ncl]);
         const LeafProduct &pr = P.prod[q];
         const int kseg = pr.kseg;
-        decode_range(range, pr.kblocks, jb0, jb1, piece);
+        decode_range(range, pr.kblocks, jb0, jb1, piece, nh);
         const int nseg = (jb1 - jb0 + kseg - 1) / kseg;
+        const int mma_n = nh ? 128 : 256;
 #pragma unroll 1
         for (int u = 0; u < NACC * nseg; ++u, ++unit) {
           const int j = u / nseg, kb0 = jb0 + (u % nseg) * kseg;
           const int kb1 = min(jb1, kb0 + kseg);
           const int t0 = P.acc_begin[j], nt = P.acc_begin[j + 1] - t0;
-          const uint32_t id0 = ptx::idesc_i8(256, 256, P.terms[t0].a_signed != 0, P.terms[t0].b_signed != 0);
-          const uint32_t id1 = nt > 1 ? ptx::idesc_i8(256, 256, P.terms[t0 + 1].a_signed != 0,
+          const uint32_t id0 = ptx::idesc_i8(256, mma_n, P.terms[t0].a_signed != 0, P.terms[t0].b_signed != 0);
+          const uint32_t id1 = nt > 1 ? ptx::idesc_i8(256, mma_n, P.terms[t0 + 1].a_signed != 0,
                                                       P.terms[t0 + 1].b_signed != 0) : id0;
           const uint32_t slot = unit & 1, use = unit >> 1;
           long long c0 = prof ? clock64() : 0;
@@ -303,13 +317,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (ADJ_EPI_WARPS 
     const uint32_t empty_remote1 = ptx::mapa(ptx::smem_u32(&slot_empty[1]), 0);
     uint32_t unit = 0;
     for (int t = cid; t < P.n_tiles; t += ncl) {
-      int q, I, J, jb0, jb1, piece;
+      int q, I, J, jb0, jb1, piece, nh;
       const uint2 job = P.tiles[t];
       decode_tile(job.x, q, I, J);
       const LeafProduct &pr = P.prod[q];
-      decode_range(job.y, pr.kblocks, jb0, jb1, piece);
+      decode_range(job.y, pr.kblocks, jb0, jb1, piece, nh);
       const int64_t row = (int64_t)I * Cfg::TILE + rank * 128 + lrow;
-      const int64_t col0 = (int64_t)J * Cfg::TILE + h0 * 128;
+      // N = 128 half jobs: TMEM columns 0..127 hold output columns (nh-1)*128..; only h0 = 0 warps work
+      const int64_t col0 = (int64_t)J * Cfg::TILE + (nh ? (nh - 1) * 128 : h0 * 128);
+      const int nch = (nh && h0 != 0) ? 0 : nchunks;
       // tail piece: residue partial of this CTA's 128 x 256 half-tile into the fixup slot
       const size_t fxo = (size_t)(piece - 1) * 65536 + (rank * 128 + lrow) * 256 + h0 * 128;
       uint16_t *fx = (piece && !P.fixup32) ? static_cast<uint16_t *>(P.fixup) + fxo : nullptr;
@@ -323,7 +339,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (ADJ_EPI_WARPS 
         ptx::mbar_wait(&slot_full[slot], use & 1);
         ptx::tc_fence_after();
 #pragma unroll 1
-        for (int c = 0; c < nchunks; ++c) {
+        for (int c = 0; c < nch; ++c) {
           uint32_t v[32];
           if (dbg_noldtm) {
 #pragma unroll

@@ -127,12 +127,23 @@ static void append_tiles(Plan &P) {
 // last wave holds n mod ncl tiles while the other clusters idle.  Those tail tiles are split
 // along K into ~ncl / rem pieces each; every piece writes its residue partial to a fixup slot
 // and fixup_kernel sums the pieces mod p (exact: < pieces * p < 2^32).
+// When the last wave fills between a half and a quarter of the clusters, its tiles are split
+// into two N = 128 column halves instead (no fixup: each half is written directly).
 static void split_tail(Plan &P, int ncl) {
   P.fixups.clear();
   P.n_pieces = 0;
   const int64_t n = (int64_t)P.tiles.size() / 2;
   const int64_t rem = n % ncl;
   if (n == 0 || rem == 0 || rem * 2 > ncl) return;
+  static const bool nsplit = !(getenv("ADJ_TAIL_KSPLIT") && atoi(getenv("ADJ_TAIL_KSPLIT")));   // diagnostics
+  if (rem * 4 > ncl && nsplit) {
+    for (int64_t t = n - rem; t < n; ++t) {
+      P.tiles[2 * t + 1] = 0x00FFFFFFu;                  // column half 0 (kb0 = kb1 = 4095: no K piece)
+      P.tiles.push_back(P.tiles[2 * t]);
+      P.tiles.push_back(0x01FFFFFFu);                    // column half 1
+    }
+    return;
+  }
   const int pieces = (int)(ncl / rem);
   std::vector<uint32_t> out(P.tiles.begin(), P.tiles.begin() + 2 * (n - rem));
   for (int64_t t = n - rem; t < n; ++t) {

@@ -40,10 +40,12 @@ struct LeafTerm {        // one tcgen05.mma operand pair accumulated into accumu
 
 struct LeafParams {
   CUtensorMap maps[kMaxMaps];
+  CUtensorMap maps_half[kMaxMaps];   // the same arenas with 64-row boxes: B operand of N = 128 tail jobs
   LeafProduct prod[kMaxProducts];
   // jobs: .x = product << 24 | I << 12 | J (longest-K products first);
-  //       .y = 0 for a whole tile, else kb0 | kb1 << 12 | piece << 24: a K-range piece of a tail
-  //       tile whose residue partial goes to fixup slot piece-1 (summed by the fixup kernel)
+  //       .y = 0 for a whole tile; kb0 | kb1 << 12 | piece << 24: a K-range piece of a tail
+  //       tile whose residue partial goes to fixup slot piece-1 (summed by the fixup kernel);
+  //       h << 24 | 0xFFFFFF: column half h (N = 128, whole K) of a tail tile, written directly
   const uint2 *tiles;
   int32_t n_tiles;
   void *fixup;             // 256 x 256 residue partials (u16, or u32 if fixup32), one slot per tail piece

@@ -408,3 +408,20 @@ def test_dist_tiles_single_rank(adj):
         assert np.array_equal(low(to_host(C)), oracle.syrk_t(A, p))
     finally:
         adj.adj_comm_destroy(comm)
+
+
+@pytest.mark.parametrize("p", [97, 8191, 65521, 131071])
+def test_tail_column_half_jobs(adj, p):
+    """Last-wave tiles split into two N = 128 column halves (74 clusters, 19..37 tail tiles):
+    gemm 2560^2 (100 tiles, tail 26) and a depth-0 SYRK of m = 4608 (171 lower tiles, tail 23)."""
+    A = uniform_matrix(2560, 300, seed=3, p=p)
+    B = uniform_matrix(2560, 300, seed=4, p=p)
+    C = adj.gemm(to_dev(A), to_dev(B), p)
+    assert np.array_equal(to_host(C), oracle.gemm_nt(A, B, p))
+    A = uniform_matrix(4608, 200, seed=5, p=p)
+    C = to_host(adj.adjprod(to_dev(A), p, depth=0))
+    rows = [0, 1, 2047, 2048, 4350, 4607]
+    ref = oracle.syrk_t(A, p)
+    for r in rows:
+        assert np.array_equal(C[r, : r + 1], ref[r, : r + 1]), r
+    assert np.array_equal(low(C), ref)
