@@ -38,6 +38,10 @@ CONFIGS = {
                workload="c4: A 16384x131072 over GF(8191), C = Low(A A^T) mod 8191 (16384^2)"),
     "x16k": dict(m=16384, k=16384, p=8191, phi="T", depth=None,
                  workload="x16k (dev): A 16384x16384 over GF(8191)"),
+    "x131071": dict(m=8192, k=8192, p=131071, phi="T", depth=None,
+                    workload="x131071 (dev): A 8192x8192 over GF(131071), the paper's modulus (PAPER.md:2237)"),
+    "x65521": dict(m=8192, k=8192, p=65521, phi="T", depth=None,
+                   workload="x65521 (dev): A 8192x8192 over GF(65521)"),
     "x251": dict(m=8192, k=8192, p=251, phi="T", depth=None,
                  workload="x251 (dev): A 8192x8192 over GF(251), one int8 limb"),
     "c5": dict(m=8192, k=8192, p=8191, phi="H", depth=None,

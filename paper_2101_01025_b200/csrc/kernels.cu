@@ -809,6 +809,32 @@ __device__ __forceinline__ void preadd_row(const PreParams &P, const PreNode &N,
 #pragma unroll
         for (int e = 0; e < 4; ++e) (*dst[a][b])[e] = addmod(re[e], im[e], m);
       }
+  } else if (fast && T == IN_U32) {
+    // all 32 loads first; one check that they are canonical (the usual case) skips the 32
+    // Barrett reductions, non-canonical input takes the reducing path (inputs are read mod p)
+    const uint32_t *src = static_cast<const uint32_t *>(v.ptr);
+    const int64_t o1 = r * v.ld, o2 = (P.mh + r) * v.ld;
+    const int64_t offs[8] = {o1 + c, o1 + c + h2, o1 + P.kh + c, o1 + P.kh + c + h2,
+                             o2 + c, o2 + c + h2, o2 + P.kh + c, o2 + P.kh + c + h2};
+    uint32_t(*dst[8])[4] = {&x11a, &x11b, &x12a, &x12b, &x21a, &x21b, &x22a, &x22b};
+    uint4 q[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) q[i] = __ldg(reinterpret_cast<const uint4 *>(src + offs[i]));
+    uint32_t mx = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) mx = max(mx, max(max(q[i].x, q[i].y), max(q[i].z, q[i].w)));
+    if (mx < m.p) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        (*dst[i])[0] = q[i].x; (*dst[i])[1] = q[i].y; (*dst[i])[2] = q[i].z; (*dst[i])[3] = q[i].w;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        (*dst[i])[0] = mod_u32(q[i].x, m); (*dst[i])[1] = mod_u32(q[i].y, m);
+        (*dst[i])[2] = mod_u32(q[i].z, m); (*dst[i])[3] = mod_u32(q[i].w, m);
+      }
+    }
   } else if (fast) {
     const int64_t o1 = r * v.ld, o2 = (P.mh + r) * v.ld;
     load4_fast<T>(v.ptr, o1 + c, m, x11a);
@@ -1081,8 +1107,23 @@ __global__ void __launch_bounds__(256) split_plain_kernel(const __grid_constant_
     const bool fast = vv.vec_ok && vv.type == IN_U32 && r < vv.rows_valid && c0 + 15 < vv.cols_valid && c0 + 15 < P.cols;
     uint32_t x[4][4];
     if (fast) {
+      uint4 q[4];
 #pragma unroll
-      for (int h = 0; h < 4; ++h) load4_fast<IN_U32>(v.ptr, r * v.ld + c0 + 4 * h, P.mod, x[h]);
+      for (int h = 0; h < 4; ++h)
+        q[h] = __ldg(reinterpret_cast<const uint4 *>(static_cast<const uint32_t *>(v.ptr) + r * v.ld + c0 + 4 * h));
+      uint32_t mx = 0;
+#pragma unroll
+      for (int h = 0; h < 4; ++h) mx = max(mx, max(max(q[h].x, q[h].y), max(q[h].z, q[h].w)));
+      if (mx < P.mod.p) {   // canonical input (the usual case) needs no reduction
+#pragma unroll
+        for (int h = 0; h < 4; ++h) { x[h][0] = q[h].x; x[h][1] = q[h].y; x[h][2] = q[h].z; x[h][3] = q[h].w; }
+      } else {
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          x[h][0] = mod_u32(q[h].x, P.mod); x[h][1] = mod_u32(q[h].y, P.mod);
+          x[h][2] = mod_u32(q[h].z, P.mod); x[h][3] = mod_u32(q[h].w, P.mod);
+        }
+      }
     } else {
 #pragma unroll
       for (int h = 0; h < 4; ++h) {
