@@ -33,7 +33,8 @@ def _nccl_include():
 
 def _flags():
     return ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
-                   "-I", CSRC, "-I", os.path.join(ROOT, "include"), "-I", _nccl_include()]
+                   "-I", CSRC, "-I", os.path.join(ROOT, "include"), "-I", _nccl_include()] + \
+        os.environ.get("ADJ_NVCC_EXTRA", "").split()   # dev experiments only (e.g. -DADJ_EPI_WARPS=4)
 
 
 def _newest(paths):
