@@ -203,8 +203,8 @@ def load_traffic(config: str, depth: int):
     path = os.path.join(ROOT, "profiles", "leaf_traffic.json")
     try:
         with open(path) as f:
-            d = json.load(f).get(config)
-        return d["dram_bytes_per_launch"] if d and d.get("depth") == depth else None
+            d = (json.load(f).get(config) or {}).get(str(depth))
+        return d["dram_bytes_per_launch"] if d else None
     except Exception:
         return None
 
@@ -298,7 +298,11 @@ def run_gpu(args, cfg, rank, world, local_rank):
                                                        else (1 if alg1 else adj.adjprod_modp_auto_depth(m, k, p, phi)))
     # N > 1: output-tile sharding for square phi = T problems (depth <= 1), split-K otherwise
     dist_mode = args.dist if args.dist != "auto" else ("tiles" if cfg["phi"] == "T" and k <= 2 * m else "splitk")
-    dist_flags = adj.ADJ_DIST_TILES if (world > 1 and dist_mode == "tiles") else 0
+    dist_flags = 0
+    if world > 1 and dist_mode == "tiles":
+        dist_flags = adj.ADJ_DIST_TILES
+    elif world > 1 and dist_mode == "p2p":
+        dist_flags = adj.ADJ_DIST_P2P
     if dist_flags:
         depth = min(depth, 1)
     A = torch.empty((m, k * w), dtype=torch.int32, device=dev)
@@ -512,8 +516,10 @@ def run_gpu(args, cfg, rank, world, local_rank):
                        "m": m, "k": k, "p": p, "phi": cfg["phi"], "depth": depth,
                        "seed": 1, "l2": "flushed before every timed step (256 MiB write, outside step events)",
                        "parallelism": ("1 GPU" if world == 1 else
-                                       (f"output tiles x{world} (NCCL send/recv gather of result tiles)" if dist_flags
-                                        else f"split-K x{world} (NCCL reduce)")),
+                                       (f"output tiles x{world} (NCCL send/recv gather of result tiles)"
+                                        if dist_mode == "tiles" else
+                                        f"split-K x{world} (partials stored into the root over NVLink)"
+                                        if dist_mode == "p2p" else f"split-K x{world} (NCCL reduce)")),
                        "fraction_of_int8_peak_effective": value / (peak * 1e12 / 2),
                        "ring_macs_per_step": mh, "limb_mmas_per_ring_mac": limb_mmas(p)},
             "roofline": roof,
@@ -542,8 +548,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-check", action="store_true", help="skip the sampled parity check")
     ap.add_argument("--no-compare", action="store_true", help="skip the depth-0 / cuBLASLt comparators")
-    ap.add_argument("--dist", default="auto", choices=["auto", "splitk", "tiles"],
-                    help="N > 1: split-K (NCCL reduce) or output-tile sharding (gather of result tiles)")
+    ap.add_argument("--dist", default="auto", choices=["auto", "splitk", "tiles", "p2p"],
+                    help="N > 1: split-K (NCCL reduce), output-tile sharding (gather of result tiles) or "
+                         "split-K with the exchange fused into the final kernel (peer stores over NVLink)")
     ap.add_argument("--herk", default="2m", choices=["2m", "alg1"],
                     help="phi = H: 2M reduction (default) or one level of Alg. 1 over GF(p^2)")
     args = ap.parse_args()

@@ -81,8 +81,12 @@ typedef enum {
  *                    to GF(p) (Alg. alg:2M).  Its Hermitian leaves P1, P2, P5 use 2M, its
  *                    general leaves P3, P4 use 3M.  Requires depth 1 (or -1); the result is the
  *                    same Low(C).  Ignored for phi = ADJ_PHI_T.
- *   ADJ_DIST_TILES : adjprod_modp_dist only -- output-tile sharding instead of split-K. */
-enum { ADJ_FILL_UPPER = 1u, ADJ_HERK_ALG1 = 2u, ADJ_DIST_TILES = 4u };
+ *   ADJ_DIST_TILES : adjprod_modp_dist only -- output-tile sharding instead of split-K.
+ *   ADJ_DIST_P2P   : adjprod_modp_dist only, phi = ADJ_PHI_T -- split-K with the exchange fused
+ *                    into the final kernel: each rank stores its partial (narrow residues)
+ *                    straight into the root's window over NVLink (CUDA IPC peer memory), the root
+ *                    sums exactly (adj_sum_partials); no NCCL data movement. */
+enum { ADJ_FILL_UPPER = 1u, ADJ_HERK_ALG1 = 2u, ADJ_DIST_TILES = 4u, ADJ_DIST_P2P = 8u };
 
 typedef struct {
   int depth;              /* recursion levels of Alg. alg:MIAHMM; -1 = automatic; 0 = classical */
@@ -191,6 +195,25 @@ adj_status_t adj_dist_kslice(int64_t k, int nranks, int rank, int64_t *k0, int64
 adj_status_t adjprod_modp_shard(int64_t m, int64_t k, uint32_t p, adj_phi_t phi,
                                 const uint32_t *A, int64_t lda, uint32_t *C, int64_t ldc,
                                 int rank, int nranks, const adj_opts_t *opts, adj_stream_t stream);
+
+/*
+ * adjprod_modp_partial -- Low(A A^T) mod p (phi = ADJ_PHI_T) written as canonical residues in
+ *   the narrowest width: uint16 for p < 2^16, uint32 otherwise.  R is m x m with leading
+ *   dimension ldr ELEMENTS of that width (device, caller-owned; may be peer memory over
+ *   NVLink).  The building block of the split-K exchange: partials of column slices are summed
+ *   exactly by adj_sum_partials (2 bytes per residue moved instead of 4).
+ */
+adj_status_t adjprod_modp_partial(int64_t m, int64_t k, uint32_t p, adj_phi_t phi,
+                                  const uint32_t *A, int64_t lda, void *R, int64_t ldr,
+                                  const adj_opts_t *opts, adj_stream_t stream);
+
+/*
+ * adj_sum_partials -- Low(C) = (sum_{r < n} Low(R_r)) mod p, R_r = R + r * stride elements,
+ *   elements uint16 for p < 2^16 else uint32 (as adjprod_modp_partial writes them), each a
+ *   residue < p; exact while n (p - 1) < 2^32.  Device pointers, async on `stream`.
+ */
+adj_status_t adj_sum_partials(int64_t m, uint32_t p, const void *R, int64_t ldr, int64_t stride, int n,
+                              uint32_t *C, int64_t ldc, adj_stream_t stream);
 
 /*
  * adj_shard_layout -- (host, no GPU) the regions of C that `rank` of `nranks` writes in

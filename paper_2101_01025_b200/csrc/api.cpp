@@ -225,6 +225,7 @@ struct Ptrs {
   const uint32_t *B = nullptr; int64_t ldb = 0;
   uint32_t *C = nullptr; int64_t ldc = 0;
   uint8_t *ws = nullptr;
+  bool res16 = false;   // write the final Low(C) as uint16 residues (adjprod_modp_partial, p < 2^16)
 };
 
 void *pbuf(const Plan &P, uint8_t *ws, int l, int n, int idx) {
@@ -262,7 +263,8 @@ adj_status_t launch_leaf_all(const Plan &P, const Ptrs &x, cudaStream_t s) {
       case OUT_C:
         L.prod[q].out = x.C;
         L.prod[q].ldo = x.ldc;
-        L.prod[q].vec_ok = ((uintptr_t)x.C % 16 == 0) && (x.ldc % 4 == 0);
+        L.prod[q].vec_ok = ((uintptr_t)x.C % 16 == 0) && (x.ldc % (x.res16 ? 8 : 4) == 0);
+        if (x.res16) L.prod[q].out_u32 = 0;
         L.prod[q].alpha = x.alpha;
         L.prod[q].beta = x.beta;
         L.prod[q].axpby = x.axpby;
@@ -405,7 +407,7 @@ adj_status_t run_syrk(const Plan &P, const Ptrs &x, adj_phi_t phi, uint32_t flag
       if (st) return st;
       st = launch_leaf_all(P, x, s);
       if (st) return st;
-      st = run_combine(P, x, x.C, x.ldc, true, s);
+      st = run_combine(P, x, x.C, x.ldc, !x.res16, s);
       if (st) return st;
     }
   } else {
@@ -728,6 +730,62 @@ adj_status_t adjprod_modp_shard(int64_t m, int64_t k, uint32_t p, adj_phi_t phi,
     if (st == ADJ_OK && e != cudaSuccess) return fail(ADJ_ERR_CUDA, "cudaFreeAsync: %s", cudaGetErrorString(e));
   }
   return st;
+}
+
+adj_status_t adjprod_modp_partial(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, const uint32_t *A, int64_t lda,
+                                  void *R, int64_t ldr, const adj_opts_t *opts, adj_stream_t stream) {
+  adj_status_t st = validate_syrk(m, k, p, phi, A, lda, static_cast<const uint32_t *>(R), ldr);
+  if (st != ADJ_OK) return st;
+  if (phi != ADJ_PHI_T) return fail(ADJ_ERR_INVALID_VALUE, "adjprod_modp_partial supports phi = ADJ_PHI_T");
+  if (m == 0) return ADJ_OK;
+  if (p > 65535) {   // residues need 32 bits: the ordinary call writes them
+    adj_opts_t o = opts ? *opts : adj_opts_t{-1, 0, nullptr, 0};
+    o.flags &= ~ADJ_FILL_UPPER;
+    return adjprod_modp_ex(m, k, p, phi, A, lda, static_cast<uint32_t *>(R), ldr, &o, stream);
+  }
+  int dev, sms;
+  if ((st = check_device(&dev, &sms)) != ADJ_OK) return st;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  uint16_t *R16 = static_cast<uint16_t *>(R);
+  if (k == 0) {
+    for (int64_t i = 0; i < m; ++i) CUDA_TRY(cudaMemsetAsync(R16 + i * ldr, 0, (size_t)(i + 1) * 2, s));
+    return ADJ_OK;
+  }
+  const int depth = (opts && opts->depth >= 0) ? opts->depth : auto_depth(m, k, p, 0);
+  if (depth > 3) return fail(ADJ_ERR_INVALID_VALUE, "depth %d > 3 unsupported", depth);
+  Plan *P = nullptr;
+  if ((st = get_plan(&P, PLAN_SYRK_T, m, m, k, p, 0, depth, dev, sms)) != ADJ_OK) return st;
+  Ptrs x;
+  x.A = A; x.lda = lda;
+  x.C = static_cast<uint32_t *>(R); x.ldc = ldr;
+  x.res16 = true;
+  void *ws = opts ? opts->workspace : nullptr;
+  bool own = false;
+  if (ws == nullptr) {
+    CUDA_TRY(cudaMallocAsync(&ws, P->ws_bytes, s));
+    own = true;
+  } else if (opts->workspace_bytes < P->ws_bytes) {
+    return fail(ADJ_ERR_WORKSPACE, "workspace %zu bytes < required %zu", opts->workspace_bytes, P->ws_bytes);
+  }
+  x.ws = static_cast<uint8_t *>(ws);
+  st = run_syrk(*P, x, phi, 0, s);
+  if (own) {
+    cudaError_t e = cudaFreeAsync(ws, s);
+    if (st == ADJ_OK && e != cudaSuccess) return fail(ADJ_ERR_CUDA, "cudaFreeAsync: %s", cudaGetErrorString(e));
+  }
+  return st;
+}
+
+adj_status_t adj_sum_partials(int64_t m, uint32_t p, const void *R, int64_t ldr, int64_t stride, int n, uint32_t *C,
+                              int64_t ldc, adj_stream_t stream) {
+  if (m < 0 || n < 0 || ldr < m || ldc < m || stride < 0) return fail(ADJ_ERR_INVALID_VALUE, "bad arguments");
+  if (!valid_modulus(p)) return fail(ADJ_ERR_UNSUPPORTED_MODULUS, "p=%u is not an odd prime in [3, 262139]", p);
+  if (m == 0) return ADJ_OK;
+  if (!C || (n > 0 && !R)) return fail(ADJ_ERR_INVALID_VALUE, "null pointer");
+  if ((uint64_t)n * (p - 1) >= (1ull << 32)) return fail(ADJ_ERR_INVALID_VALUE, "too many partials for exact uint32 sums");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  LAUNCH(launch_sum_partials(m, R, ldr, stride, n, p > 65535 ? 4 : 2, C, ldc, make_modp(p), s));
+  return ADJ_OK;
 }
 
 adj_status_t adj_shard_layout(int64_t m, int64_t k, uint32_t p, int depth, int rank, int nranks, int64_t *rects,

@@ -19,6 +19,13 @@
 struct adj_comm_s {
   ncclComm_t comm;
   int nranks, rank;
+  // ADJ_DIST_P2P exchange window: the root's G partial slots; the other ranks map it with CUDA
+  // IPC (peer memory over NVLink) and write their partials into it from the final kernel
+  void *win = nullptr;
+  size_t win_bytes = 0;
+  int win_root = -1;
+  bool win_owned = false;        // root: cudaMalloc'ed; others: IPC-mapped
+  void *d_scratch = nullptr;     // 64-byte device buffer: IPC handle broadcast and barrier token
 };
 
 namespace {
@@ -32,6 +39,9 @@ struct NcclApi {
                          cudaStream_t) = nullptr;
   ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void *, void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   const char *(*GetErrorString)(ncclResult_t) = nullptr;
@@ -56,6 +66,8 @@ bool load_nccl() {
   SYM("ncclSend", Send)
   SYM("ncclRecv", Recv)
   SYM("ncclGroupStart", GroupStart)
+  SYM("ncclBroadcast", Broadcast)
+  SYM("ncclAllReduce", AllReduce)
   SYM("ncclGroupEnd", GroupEnd)
   SYM("ncclGetErrorString", GetErrorString)
 #undef SYM
@@ -151,6 +163,68 @@ adj_status_t dist_tiles(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, const u
   for (void *ptr : allocs) cudaFreeAsync(ptr, s);
   return st;
 }
+
+// the root's exchange window (G slots of m x m narrow residues), mapped on every rank
+adj_status_t setup_window(adj_comm_t comm, int root, size_t bytes, cudaStream_t s) {
+  if (comm->win && comm->win_root == root && comm->win_bytes >= bytes) return ADJ_OK;
+  if (comm->win) {
+    if (comm->win_owned) cudaFree(comm->win);
+    else cudaIpcCloseMemHandle(comm->win);
+    comm->win = nullptr;
+  }
+  if (!comm->d_scratch && cudaMalloc(&comm->d_scratch, 64) != cudaSuccess) return ADJ_ERR_CUDA;
+  cudaIpcMemHandle_t h;
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  if (comm->rank == root) {
+    if (cudaMalloc(&comm->win, bytes) != cudaSuccess) return ADJ_ERR_CUDA;
+    comm->win_owned = true;
+    if (cudaIpcGetMemHandle(&h, comm->win) != cudaSuccess) return ADJ_ERR_CUDA;
+    if (cudaMemcpyAsync(comm->d_scratch, &h, 64, cudaMemcpyHostToDevice, s) != cudaSuccess) return ADJ_ERR_CUDA;
+  }
+  if (g_nccl.Broadcast(comm->d_scratch, comm->d_scratch, 64, ncclUint8, root, comm->comm, s) != ncclSuccess)
+    return ADJ_ERR_NCCL;
+  if (cudaStreamSynchronize(s) != cudaSuccess) return ADJ_ERR_CUDA;
+  if (comm->rank != root) {
+    if (cudaMemcpy(&h, comm->d_scratch, 64, cudaMemcpyDeviceToHost) != cudaSuccess) return ADJ_ERR_CUDA;
+    if (cudaIpcOpenMemHandle(&comm->win, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) return ADJ_ERR_CUDA;
+    comm->win_owned = false;
+  }
+  comm->win_root = root;
+  comm->win_bytes = bytes;
+  return ADJ_OK;
+}
+
+// split-K with the exchange fused into the compute (ADJ_DIST_P2P): every rank's final kernel
+// (leaf epilogue at depth 0, K4 otherwise) stores its Low(A_r A_r^T) residues, 2 bytes each for
+// p < 2^16, straight into slot r of the root's window over NVLink (adjprod_modp_partial with a
+// peer pointer); two NCCL barriers order the window's reuse and the root's exact sum
+// (adj_sum_partials).  NVLink carries m^2/2 narrow residues per rank instead of the m^2 uint32
+// words of the reduce.
+adj_status_t dist_p2p(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, const uint32_t *A, int64_t lda, uint32_t *C,
+                      int64_t ldc, int root, adj_comm_t comm, const adj_opts_t *opts, adj_stream_t stream) {
+  if (!load_nccl()) return ADJ_ERR_NCCL;
+  const int G = comm->nranks, r = comm->rank;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const size_t esize = p < 65536 ? 2 : 4;
+  const size_t slot = (size_t)m * (size_t)m;
+  adj_status_t st = setup_window(comm, root, slot * esize * (size_t)G, s);
+  if (st != ADJ_OK) return st;
+  // barrier 1: the root has finished reading the window of the previous call
+  if (g_nccl.AllReduce(comm->d_scratch, comm->d_scratch, 1, ncclInt32, ncclSum, comm->comm, s) != ncclSuccess)
+    return ADJ_ERR_NCCL;
+  int64_t k0 = 0, k1 = 0;
+  adj_dist_kslice(k, G, r, &k0, &k1);
+  void *mine = static_cast<uint8_t *>(comm->win) + (size_t)r * slot * esize;
+  adj_opts_t o = opts ? *opts : adj_opts_t{-1, 0, nullptr, 0};
+  o.flags = 0;
+  st = adjprod_modp_partial(m, k1 - k0, p, phi, A ? A + k0 : nullptr, lda, mine, m, &o, stream);
+  if (st != ADJ_OK) return st;
+  // barrier 2: every rank's partial kernels (and their peer stores) have completed
+  if (g_nccl.AllReduce(comm->d_scratch, comm->d_scratch, 1, ncclInt32, ncclSum, comm->comm, s) != ncclSuccess)
+    return ADJ_ERR_NCCL;
+  if (r == root) st = adj_sum_partials(m, p, comm->win, m, (int64_t)slot, G, C, ldc, stream);
+  return st;
+}
 }  // namespace
 
 extern "C" {
@@ -173,12 +247,21 @@ adj_status_t adj_comm_init(int nranks, const uint8_t id[128], int rank, adj_comm
   ncclComm_t c;
   ncclResult_t r = g_nccl.CommInitRank(&c, nranks, u, rank);
   if (r != ncclSuccess) return ADJ_ERR_NCCL;
-  *comm = new adj_comm_s{c, nranks, rank};
+  adj_comm_s *cm = new adj_comm_s;
+  cm->comm = c;
+  cm->nranks = nranks;
+  cm->rank = rank;
+  *comm = cm;
   return ADJ_OK;
 }
 
 adj_status_t adj_comm_destroy(adj_comm_t comm) {
   if (!comm) return ADJ_ERR_INVALID_VALUE;
+  if (comm->win) {
+    if (comm->win_owned) cudaFree(comm->win);
+    else cudaIpcCloseMemHandle(comm->win);
+  }
+  if (comm->d_scratch) cudaFree(comm->d_scratch);
   if (g_nccl.loaded) g_nccl.CommDestroy(comm->comm);
   delete comm;
   return ADJ_OK;
@@ -200,6 +283,8 @@ adj_status_t adjprod_modp_dist(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, 
   if (m == 0) return ADJ_OK;
   const int G = comm->nranks, r = comm->rank;
   if (opts && (opts->flags & ADJ_DIST_TILES)) return dist_tiles(m, k, p, phi, A, lda, C, ldc, root, comm, opts, stream);
+  if (opts && (opts->flags & ADJ_DIST_P2P) && phi == ADJ_PHI_T && G > 1)
+    return dist_p2p(m, k, p, phi, A, lda, C, ldc, root, comm, opts, stream);
   const int w = adj_phi_width(phi);
   int64_t k0 = 0, k1 = 0;
   adj_dist_kslice(k, G, r, &k0, &k1);

@@ -1883,6 +1883,31 @@ cudaError_t launch_rect_copy(const RectDev *rects, int n, int max_rows, uint32_t
   return cudaGetLastError();
 }
 
+// exact residue sum of n partials (each < p, n (p - 1) < 2^32) then mod p, on Low; one block per row
+template <typename T>
+__global__ void __launch_bounds__(256) sum_partials_kernel(int64_t m, const T *R, int64_t ldr, int64_t stride, int n,
+                                                           uint32_t *C, int64_t ldc, ModP mod) {
+  const int64_t i = blockIdx.x;
+  if (i >= m) return;
+  for (int64_t j = threadIdx.x; j <= i; j += blockDim.x) {
+    uint32_t acc = 0;
+    for (int r = 0; r < n; ++r) acc += (uint32_t)R[(int64_t)r * stride + i * ldr + j];
+    C[i * ldc + j] = mod_u32(acc, mod);
+  }
+}
+
+cudaError_t launch_sum_partials(int64_t m, const void *R, int64_t ldr, int64_t stride, int n, int esize, uint32_t *C,
+                                int64_t ldc, const ModP &mod, cudaStream_t s) {
+  if (m == 0) return cudaSuccess;
+  if (esize == 2)
+    sum_partials_kernel<uint16_t><<<(unsigned)m, 256, 0, s>>>(m, static_cast<const uint16_t *>(R), ldr, stride, n, C,
+                                                               ldc, mod);
+  else
+    sum_partials_kernel<uint32_t><<<(unsigned)m, 256, 0, s>>>(m, static_cast<const uint32_t *>(R), ldr, stride, n, C,
+                                                               ldc, mod);
+  return cudaGetLastError();
+}
+
 __global__ void __launch_bounds__(256) fill_upper_kernel(int64_t m, int w, uint32_t *C, int64_t ldc, ModP mod) {
   const int ti = blockIdx.y, tj = blockIdx.x;
   if (ti < tj) return;

@@ -425,3 +425,28 @@ def test_tail_column_half_jobs(adj, p):
     for r in rows:
         assert np.array_equal(C[r, : r + 1], ref[r, : r + 1]), r
     assert np.array_equal(low(C), ref)
+
+
+# ---------------------------------------------------------------- split-K building blocks
+@pytest.mark.parametrize("p", [97, 8191, 65521, 131071])
+@pytest.mark.parametrize("depth", [0, 1])
+@pytest.mark.parametrize("G", [1, 2, 3, 5])
+def test_partials_of_column_slices_sum_to_low_c(adj, p, depth, G):
+    """adjprod_modp_partial on every rank's column slice (adj_dist_kslice) into G narrow residue
+    buffers, then adj_sum_partials: the split-K exchange path of adjprod_modp_dist, ranks run one
+    after the other on this device."""
+    import torch
+    m, k = 300, 700
+    A = uniform_matrix(m, k, seed=G * 7 + depth, p=p)
+    dA = to_dev(A)
+    dt = torch.int16 if p < 65536 else torch.int32
+    R = torch.zeros((G, m, m), dtype=dt, device="cuda")
+    for r in range(G):
+        k0, k1 = adj.adj_dist_kslice(k, G, r)
+        adj.adjprod_modp_partial(m, k1 - k0, p, 0, dA[:, k0:], k, R[r], m, depth=depth)
+    C = torch.full((m, m), -1, dtype=torch.int32, device="cuda")
+    adj.adj_sum_partials(m, p, R, m, m * m, G, C, m)
+    got = to_host(C)
+    lo = np.tril(np.ones((m, m), dtype=bool))
+    assert np.array_equal(got[lo], oracle.syrk_t(A, p)[lo])
+    assert (got[~lo] == 0xFFFFFFFF).all()
