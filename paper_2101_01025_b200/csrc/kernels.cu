@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdint>
 #include <cstdio>
 
@@ -23,6 +24,20 @@
 namespace adj {
 
 __host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device): the attribute is
+// per device, `done` is a per-kernel bitmask of device ordinals (thread-safe)
+template <typename K>
+static cudaError_t ensure_smem(K kernel, int bytes, std::atomic<uint64_t> &done) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
+}
 
 // ============================================================================ leaf kernel
 __device__ __forceinline__ void decode_tile(uint32_t packed, int &q, int &I, int &J) {
@@ -449,13 +464,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (ADJ_EPI_WARPS 
 template <int NACC, bool PART, bool WIDE>
 static cudaError_t launch_leaf2_t(const LeafParams &p, int grid, cudaStream_t s) {
   using Cfg = Leaf2Cfg<NACC, PART, WIDE>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(leaf2_kernel<NACC, PART, WIDE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         Cfg::SMEM);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  static std::atomic<uint64_t> done{0};
+  cudaError_t e = ensure_smem(leaf2_kernel<NACC, PART, WIDE>, Cfg::SMEM, done);
+  if (e != cudaSuccess) return e;
   leaf2_kernel<NACC, PART, WIDE><<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(p);
   return cudaGetLastError();
 }
@@ -1591,20 +1602,14 @@ cudaError_t launch_herk_combine(const HerkCombParams &p, cudaStream_t s) {
   const dim3 grid(nt * (nt + 1) / 2);
   const int smem = 4 * 64 * 65 * 4;
   if (p.in32) {
-    static bool set32 = false;
-    if (!set32) {
-      cudaError_t e = cudaFuncSetAttribute(herk_combine_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      if (e != cudaSuccess) return e;
-      set32 = true;
-    }
+    static std::atomic<uint64_t> set32{0};
+    cudaError_t e = ensure_smem(herk_combine_kernel<uint32_t>, smem, set32);
+    if (e != cudaSuccess) return e;
     herk_combine_kernel<uint32_t><<<grid, 256, smem, s>>>(p);
   } else {
-    static bool set16 = false;
-    if (!set16) {
-      cudaError_t e = cudaFuncSetAttribute(herk_combine_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      if (e != cudaSuccess) return e;
-      set16 = true;
-    }
+    static std::atomic<uint64_t> set16{0};
+    cudaError_t e = ensure_smem(herk_combine_kernel<uint16_t>, smem, set16);
+    if (e != cudaSuccess) return e;
     herk_combine_kernel<uint16_t><<<grid, 256, smem, s>>>(p);
   }
   return cudaGetLastError();
@@ -1711,20 +1716,14 @@ cudaError_t launch_quat_combine(const QuatCombParams &p, cudaStream_t s) {
   const dim3 grid(nt * (nt + 1) / 2);
   const int smem = 4 * 64 * 65 * 4;
   if (p.in32) {
-    static bool set32 = false;
-    if (!set32) {
-      cudaError_t e = cudaFuncSetAttribute(quat_combine_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      if (e != cudaSuccess) return e;
-      set32 = true;
-    }
+    static std::atomic<uint64_t> set32{0};
+    cudaError_t e = ensure_smem(quat_combine_kernel<uint32_t>, smem, set32);
+    if (e != cudaSuccess) return e;
     quat_combine_kernel<uint32_t><<<grid, 256, smem, s>>>(p);
   } else {
-    static bool set16 = false;
-    if (!set16) {
-      cudaError_t e = cudaFuncSetAttribute(quat_combine_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      if (e != cudaSuccess) return e;
-      set16 = true;
-    }
+    static std::atomic<uint64_t> set16{0};
+    cudaError_t e = ensure_smem(quat_combine_kernel<uint16_t>, smem, set16);
+    if (e != cudaSuccess) return e;
     quat_combine_kernel<uint16_t><<<grid, 256, smem, s>>>(p);
   }
   return cudaGetLastError();

@@ -106,7 +106,7 @@ static void append_tiles(Plan &P) {
   std::stable_sort(P.prods.begin(), P.prods.end(),
                    [](const ProductPlan &a, const ProductPlan &b) { return a.lp.kblocks > b.lp.kblocks; });
   P.tiles.clear();
-  const int band = 8;
+  static const int band = getenv("ADJ_BAND") ? std::max(1, atoi(getenv("ADJ_BAND"))) : 8;   // diagnostics
   for (size_t q = 0; q < P.prods.size(); ++q) {
     const LeafProduct &lp = P.prods[q].lp;
     const int64_t tm = cdiv(lp.out_rows, P.tile_m);

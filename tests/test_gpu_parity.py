@@ -450,3 +450,29 @@ def test_partials_of_column_slices_sum_to_low_c(adj, p, depth, G):
     lo = np.tril(np.ones((m, m), dtype=bool))
     assert np.array_equal(got[lo], oracle.syrk_t(A, p)[lo])
     assert (got[~lo] == 0xFFFFFFFF).all()
+
+
+@pytest.mark.parametrize("depth", [0, 1, 2])
+def test_cuda_graph_capture_and_replay(adj, depth):
+    """One call is a fixed stream-ordered launch sequence with no host synchronisation: it can be
+    captured into a CUDA graph (after a first call builds the cached plan) and replayed."""
+    import torch
+    p, m, k = 8191, 600, 520
+    A = uniform_matrix(m, k, seed=21, p=p)
+    dA = to_dev(A)
+    ws_bytes = adj.adjprod_modp_workspace_size(m, k, p, 0, depth)
+    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device="cuda")
+    C = torch.zeros((m, m), dtype=torch.int32, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        adj.adjprod_modp_ex(m, k, p, 0, dA, k, C, m, depth=depth, workspace=ws, workspace_bytes=ws_bytes, stream=s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        adj.adjprod_modp_ex(m, k, p, 0, dA, k, C, m, depth=depth, workspace=ws, workspace_bytes=ws_bytes, stream=s)
+    ref = oracle.syrk_t(A, p)
+    for _ in range(3):
+        C.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert np.array_equal(low(to_host(C)), ref)
