@@ -155,7 +155,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (ADJ_EPI_WARPS 
 
   uint64_t g_enter = 0;
   long long c_enter = clock64();
-  if (P.debug & 128) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_enter));
+  if (P.debug & (128 | 16384)) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_enter));
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t rank = ptx::cluster_ctarank();
@@ -449,7 +449,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (ADJ_EPI_WARPS 
     ptx::tc_fence_after();
     ptx::tmem_dealloc_2sm(tmem_base, 512);
   }
-  if ((P.debug & 128) && threadIdx.x == 0 && rank == 0) {
+  if ((P.debug & (128 | 16384)) && threadIdx.x == 0 && rank == 0) {   // 16384: exit times only
     uint64_t g_exit;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_exit));
     uint32_t smid;
