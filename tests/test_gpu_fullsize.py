@@ -151,3 +151,24 @@ def test_c2_output_tile_shards(env, depth):
         ref = oracle.syrk_t(Ah, p, rows=(r, r + 1))
         assert np.array_equal(Ch[r, : r + 1], ref[r, : r + 1]), r
     assert _freivalds(Ah, Ch, p)
+
+
+@pytest.mark.parametrize("m,k,p,depth", [(5001, 4099, 8191, 2), (3001, 70001, 65521, -1), (2999, 3001, 131071, 1),
+                                         (4097, 257, 97, 3)])
+def test_ragged_medium_sampled_rows(env, m, k, p, depth):
+    """Ragged shapes well past one tile wave at several depths, including a k past the int32
+    accumulation bound of the 65521 scheme (K segments) and the wide scheme: sampled rows plus
+    Freivalds over the whole lower triangle."""
+    torch, adj, bench = env
+    from inputs.gpu import uniform_residues_cuda
+    A = torch.empty((m, k), dtype=torch.int32, device="cuda")
+    uniform_residues_cuda(A, seed=m + k, p=p)
+    C = torch.zeros((m, m), dtype=torch.int32, device="cuda")
+    adj.adjprod_modp_ex(m, k, p, 0, A, k, C, m, depth=depth)
+    torch.cuda.synchronize()
+    Ah = A.cpu().numpy().view(np.uint32)
+    Ch = C.cpu().numpy().view(np.uint32)
+    for r in sorted({0, 1, m // 3, m // 2, m // 2 + 1, m - 2, m - 1}):
+        ref = oracle.syrk_t(Ah, p, rows=(r, r + 1))
+        assert np.array_equal(Ch[r, : r + 1], ref[r, : r + 1]), (m, k, p, depth, r)
+    assert _freivalds(Ah, Ch, p)
