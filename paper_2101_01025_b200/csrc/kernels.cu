@@ -131,7 +131,7 @@ struct Leaf2Cfg {
   static constexpr int PART_BYTES = PART ? 128 * PART_STRIDE * 4 : 0;
   static constexpr int BAR_BYTES = 8 * (2 * STAGES + 2 * SLOTS) + 16;
   static constexpr int SMEM = STAGES * STAGE_BYTES + PART_BYTES + 1024 + BAR_BYTES;
-  static constexpr int EPI_WARPS = ADJ_EPI_WARPS;       // 8: two warps per TMEM lane quadrant; 4: one
+  static constexpr int EPI_WARPS = ADJ_EPI_WARPS;       // 4, 8 or 16: 1, 2 or 4 warps per TMEM lane quadrant
   static constexpr int THREADS = 32 * (EPI_WARPS + 3);   // + TMEM allocator, MMA issuer, TMA producer
 };
 
@@ -320,8 +320,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (ADJ_EPI_WARPS 
   } else if (warp < EW) {
     // ------------------------------------------------------------ epilogue (8 warps per CTA)
     const int q4 = warp & 3;               // TMEM lane quadrant this warp may access
-    const int h0 = EW == 8 ? (warp >> 2) : 0;  // first column half of the 256-wide tile
-    constexpr int NCH = EW == 8 ? 4 : 8;       // 32-column chunks per warp and unit
+    constexpr int CPW = 1024 / EW;             // tile columns per warp (EW / 4 warps per TMEM lane quadrant)
+    const int h0 = warp >> 2;                  // which CPW-column part of the 256-wide tile
+    constexpr int NCH = CPW / 32;              // 32-column chunks per warp and unit
     const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
     const int lrow = q4 * 32 + lane;
     uint32_t *prow0 = part_s + lrow * Cfg::PART_STRIDE;
@@ -339,10 +340,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (ADJ_EPI_WARPS 
       decode_range(job.y, pr.kblocks, jb0, jb1, piece, nh);
       const int64_t row = (int64_t)I * Cfg::TILE + rank * 128 + lrow;
       // N = 128 half jobs: TMEM columns 0..127 hold output columns (nh-1)*128..; only h0 = 0 warps work
-      const int64_t col0 = (int64_t)J * Cfg::TILE + (nh ? (nh - 1) * 128 : h0 * 128);
-      const int nch = (nh && h0 != 0) ? 0 : nchunks;
+      const int64_t col0 = (int64_t)J * Cfg::TILE + (nh ? (nh - 1) * 128 : 0) + h0 * CPW;
+      const int nch = (nh && h0 * CPW >= 128) ? 0 : nchunks;
       // tail piece: residue partial of this CTA's 128 x 256 half-tile into the fixup slot
-      const size_t fxo = (size_t)(piece - 1) * 65536 + (rank * 128 + lrow) * 256 + h0 * 128;
+      const size_t fxo = (size_t)(piece - 1) * 65536 + (rank * 128 + lrow) * 256 + h0 * CPW;
       uint16_t *fx = (piece && !P.fixup32) ? static_cast<uint16_t *>(P.fixup) + fxo : nullptr;
       uint32_t *fx32 = (piece && P.fixup32) ? static_cast<uint32_t *>(P.fixup) + fxo : nullptr;
       const int nseg = (jb1 - jb0 + pr.kseg - 1) / pr.kseg;
@@ -360,7 +361,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (ADJ_EPI_WARPS 
 #pragma unroll
             for (int e = 0; e < 32; ++e) v[e] = (uint32_t)(e * 977 + c + u) ^ (uint32_t)lrow;
           } else {
-            ptx::tmem_ld32(tmem_base + lane_off + slot * Cfg::TILE + h0 * 128 + c * 32, v);
+            ptx::tmem_ld32(tmem_base + lane_off + slot * Cfg::TILE + h0 * CPW + c * 32, v);
             ptx::tmem_wait_ld();
           }
           if (dbg_nomath) {
@@ -371,7 +372,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (ADJ_EPI_WARPS 
           const int32_t wc = P.wshoup[j].wc, wq = P.wshoup[j].wq;
           const uint32_t pm = mod.p;
           if constexpr (PART && !WIDE) {
-            uint2 *pc = reinterpret_cast<uint2 *>(prow0 + h0 * 64 + c * 16);
+            uint2 *pc = reinterpret_cast<uint2 *>(prow0 + h0 * (CPW / 2) + c * 16);
             if (u > 0) {
 #pragma unroll
               for (int e = 0; e < 8; ++e) {
@@ -392,7 +393,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (ADJ_EPI_WARPS 
               continue;
             }
           } else if constexpr (PART && WIDE) {
-            uint32_t *pc = prow0 + h0 * 96 + c * 24;     // 32 residues of 24 bits = 24 words
+            uint32_t *pc = prow0 + h0 * (CPW * 3 / 4) + c * 24;     // 32 residues of 24 bits = 24 words
             if (u > 0) {
 #pragma unroll
               for (int g = 0; g < 8; ++g) {
