@@ -1182,9 +1182,9 @@ __device__ __forceinline__ void axpby_n(const uint32_t *o, int64_t ncols_ok, uin
 template <typename OutT>
 __device__ __forceinline__ void store8(OutT *o, int64_t ncols_ok, const uint32_t (&v)[8]) {
   if (ncols_ok >= 8 && (reinterpret_cast<uintptr_t>(o) % (8 * sizeof(OutT)) == 0)) {
-    if constexpr (sizeof(OutT) == 4) {
-      reinterpret_cast<uint4 *>(o)[0] = make_uint4(v[0], v[1], v[2], v[3]);
-      reinterpret_cast<uint4 *>(o)[1] = make_uint4(v[4], v[5], v[6], v[7]);
+    if constexpr (sizeof(OutT) == 4) {   // final C: streaming stores (not re-read by this call)
+      __stcs(reinterpret_cast<uint4 *>(o), make_uint4(v[0], v[1], v[2], v[3]));
+      __stcs(reinterpret_cast<uint4 *>(o) + 1, make_uint4(v[4], v[5], v[6], v[7]));
     } else {
       *reinterpret_cast<uint4 *>(o) = make_uint4(v[0] | (v[1] << 16), v[2] | (v[3] << 16), v[4] | (v[5] << 16),
                                                  v[6] | (v[7] << 16));
@@ -1791,7 +1791,7 @@ __global__ void __launch_bounds__(256) twom_kernel(int64_t m, const InT *G, int6
     if (n == 8 && (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
 #pragma unroll
       for (int e = 0; e < 4; ++e)
-        reinterpret_cast<uint4 *>(o)[e] = make_uint4(re[2 * e], im[2 * e], re[2 * e + 1], im[2 * e + 1]);
+        __stcs(reinterpret_cast<uint4 *>(o) + e, make_uint4(re[2 * e], im[2 * e], re[2 * e + 1], im[2 * e + 1]));
     } else {
 #pragma unroll
       for (int e = 0; e < 8; ++e)
