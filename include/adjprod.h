@@ -92,7 +92,8 @@ typedef struct {
   int depth;              /* recursion levels of Alg. alg:MIAHMM; -1 = automatic; 0 = classical */
   uint32_t flags;         /* ADJ_FILL_UPPER | ADJ_HERK_ALG1 */
   void *workspace;        /* device memory of >= workspace_bytes, or NULL (library allocates
-                             stream-ordered with cudaMallocAsync/cudaFreeAsync) */
+                             stream-ordered from a per-device pool that retains its memory
+                             between calls, cudaMallocFromPoolAsync / cudaFreeAsync) */
   size_t workspace_bytes;
 } adj_opts_t;
 

@@ -114,6 +114,41 @@ adj_status_t check_device(int *dev_out, int *sms_out) {
   return ADJ_OK;
 }
 
+// ------------------------------------------------------------------ workspace pool
+// Calls without a caller workspace allocate it stream-ordered from a per-device pool that keeps
+// its memory between calls (release threshold = max): the default pool returns freed memory at
+// every synchronisation, which made each multi-GB workspace a fresh mapping (measured: a 32768^2
+// call took several times its compute time).
+std::mutex g_pool_mu;
+std::map<int, cudaMemPool_t> g_pools;
+
+}  // namespace
+cudaError_t adj_pool_alloc(void **ptr, size_t bytes, cudaStream_t s) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  cudaMemPool_t pool;
+  {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    auto it = g_pools.find(dev);
+    if (it == g_pools.end()) {
+      cudaMemPoolProps props = {};
+      props.allocType = cudaMemAllocationTypePinned;
+      props.handleTypes = cudaMemHandleTypeNone;
+      props.location.type = cudaMemLocationTypeDevice;
+      props.location.id = dev;
+      if ((e = cudaMemPoolCreate(&pool, &props)) != cudaSuccess) return e;
+      uint64_t thr = ~0ull;
+      if ((e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr)) != cudaSuccess) return e;
+      g_pools.emplace(dev, pool);
+    } else {
+      pool = it->second;
+    }
+  }
+  return cudaMallocFromPoolAsync(ptr, bytes, pool, s);
+}
+namespace {
+
 // ------------------------------------------------------------------ TMA descriptor encoding
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 
@@ -661,7 +696,7 @@ static adj_status_t adjprod_impl(int64_t m, int64_t k, uint32_t p, adj_phi_t phi
   void *ws = opts ? opts->workspace : nullptr;
   bool own = false;
   if (ws == nullptr) {
-    CUDA_TRY(cudaMallocAsync(&ws, P->ws_bytes, s));
+    CUDA_TRY(adj_pool_alloc(&ws, P->ws_bytes, s));
     own = true;
   } else if (opts->workspace_bytes < P->ws_bytes) {
     return fail(ADJ_ERR_WORKSPACE, "workspace %zu bytes < required %zu", opts->workspace_bytes, P->ws_bytes);
@@ -718,7 +753,7 @@ adj_status_t adjprod_modp_shard(int64_t m, int64_t k, uint32_t p, adj_phi_t phi,
   void *ws = opts ? opts->workspace : nullptr;
   bool own = false;
   if (ws == nullptr) {
-    CUDA_TRY(cudaMallocAsync(&ws, P->ws_bytes, s));
+    CUDA_TRY(adj_pool_alloc(&ws, P->ws_bytes, s));
     own = true;
   } else if (opts->workspace_bytes < P->ws_bytes) {
     return fail(ADJ_ERR_WORKSPACE, "workspace %zu bytes < required %zu", opts->workspace_bytes, P->ws_bytes);
@@ -762,7 +797,7 @@ adj_status_t adjprod_modp_partial(int64_t m, int64_t k, uint32_t p, adj_phi_t ph
   void *ws = opts ? opts->workspace : nullptr;
   bool own = false;
   if (ws == nullptr) {
-    CUDA_TRY(cudaMallocAsync(&ws, P->ws_bytes, s));
+    CUDA_TRY(adj_pool_alloc(&ws, P->ws_bytes, s));
     own = true;
   } else if (opts->workspace_bytes < P->ws_bytes) {
     return fail(ADJ_ERR_WORKSPACE, "workspace %zu bytes < required %zu", opts->workspace_bytes, P->ws_bytes);
@@ -852,7 +887,7 @@ adj_status_t gemm_modp(int64_t m, int64_t n, int64_t k, uint32_t p, const uint32
   Plan *P = nullptr;
   if ((st = get_plan(&P, PLAN_GEMM, m, n, k, p, 0, 0, dev, sms)) != ADJ_OK) return st;
   void *ws = nullptr;
-  CUDA_TRY(cudaMallocAsync(&ws, P->ws_bytes, s));
+  CUDA_TRY(adj_pool_alloc(&ws, P->ws_bytes, s));
   Ptrs x;
   x.A = A; x.lda = lda; x.B = B; x.ldb = ldb; x.C = C; x.ldc = ldc;
   x.ws = static_cast<uint8_t *>(ws);

@@ -77,7 +77,8 @@ bool load_nccl() {
 
 }  // namespace
 
-int adj_phi_width(adj_phi_t phi);   // api.cpp
+int adj_phi_width(adj_phi_t phi);                                    // api.cpp
+cudaError_t adj_pool_alloc(void **ptr, size_t bytes, cudaStream_t s);   // api.cpp: retained workspace pool
 
 namespace {
 // the packed regions (RectDev, buffer offsets) of `rank` for this problem
@@ -125,7 +126,7 @@ adj_status_t dist_tiles(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, const u
   std::vector<void *> allocs;
   auto dalloc = [&](size_t bytes) -> void * {
     void *ptr = nullptr;
-    if (bytes && cudaMallocAsync(&ptr, bytes, s) == cudaSuccess) allocs.push_back(ptr);
+    if (bytes && adj_pool_alloc(&ptr, bytes, s) == cudaSuccess) allocs.push_back(ptr);
     return ptr;
   };
   std::vector<adj::RectDev *> drects((size_t)G, nullptr);
@@ -295,7 +296,7 @@ adj_status_t adjprod_modp_dist(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, 
   // partial Low(A_r phi(A_r)) in a dense m x m buffer (the caller's Up(C) stays untouched)
   uint32_t *W = nullptr;
   const size_t count = (size_t)m * m * w;
-  if (cudaMallocAsync(reinterpret_cast<void **>(&W), count * 4, s) != cudaSuccess) return ADJ_ERR_CUDA;
+  if (adj_pool_alloc(reinterpret_cast<void **>(&W), count * 4, s) != cudaSuccess) return ADJ_ERR_CUDA;
   adj_status_t st = adjprod_modp_ex(m, k1 - k0, p, phi, Ar, lda, W, m, opts, stream);
   if (st == ADJ_OK) {
     // exact: each entry is a sum of G residues < G p < 2^32
