@@ -227,6 +227,16 @@ adj_status_t adj_shard_layout(int64_t m, int64_t k, uint32_t p, int depth, int r
                               int64_t *rects, int64_t max_rects, int64_t *n_rects, int64_t *n_elems);
 
 /*
+ * adj_shard_pack -- pack (unpack = 0) the regions of C that `rank` of `nranks` owns
+ *   (adj_shard_layout, region by region, row by row) into the contiguous buffer `buf`, as uint16
+ *   residues for p < 2^16 and uint32 otherwise, or unpack them back into C (unpack = 1; only the
+ *   elements col <= row of "lower" regions).  buf holds n_elems of adj_shard_layout.  Device
+ *   pointers, async on `stream`.  The gather step of ADJ_DIST_TILES.
+ */
+adj_status_t adj_shard_pack(int64_t m, int64_t k, uint32_t p, int depth, int rank, int nranks,
+                            uint32_t *C, int64_t ldc, void *buf, int unpack, adj_stream_t stream);
+
+/*
  * adjprod_modp_dist -- collective; every rank of `comm` calls it with the same m, k, p, phi,
  *   root.  Default: split-K sharding: rank r computes Low(A_r phi(A_r)) on its
  *   column slice A_r = A[:, k_r0 : k_r1] (k_r0 = r*ceil(k/G) rounded to a multiple of 8) with

@@ -24,7 +24,7 @@ STATUS = {0: "ADJ_OK", 1: "ADJ_ERR_INVALID_VALUE", 2: "ADJ_ERR_UNSUPPORTED_MODUL
 # every symbol include/adjprod.h declares (checked by tests/test_abi.py)
 EXPORTS = ["adjprod_modp", "adjprod_modp_ex", "adjprod_modp_syrk", "adjprod_modp_workspace_size", "adjprod_modp_auto_depth",
            "gemm_modp", "adj_skew_unitary", "adj_sos", "adj_mod_lower", "adj_comm_get_unique_id",
-           "adj_comm_init", "adj_comm_destroy", "adjprod_modp_dist", "adj_dist_kslice", "adjprod_modp_shard", "adj_shard_layout", "adjprod_modp_partial", "adj_sum_partials", "adj_status_string", "adj_last_error",
+           "adj_comm_init", "adj_comm_destroy", "adjprod_modp_dist", "adj_dist_kslice", "adjprod_modp_shard", "adj_shard_layout", "adjprod_modp_partial", "adj_sum_partials", "adj_shard_pack", "adj_status_string", "adj_last_error",
            "adj_launch_count", "adj_launch_count_reset", "adj_profile_enable", "adj_profile_read"]
 
 
@@ -68,6 +68,7 @@ def lib() -> ctypes.CDLL:
             "adjprod_modp_shard": [i64, i64, u32, ci, vp, i64, vp, i64, ci, ci, ctypes.POINTER(adj_opts_t), vp],
             "adjprod_modp_partial": [i64, i64, u32, ci, vp, i64, vp, i64, ctypes.POINTER(adj_opts_t), vp],
             "adj_sum_partials": [i64, u32, vp, i64, i64, ci, vp, i64, vp],
+            "adj_shard_pack": [i64, i64, u32, ci, ci, ci, vp, i64, vp, ci, vp],
             "adj_shard_layout": [i64, i64, u32, ci, ci, ci, ctypes.POINTER(i64), i64, ctypes.POINTER(i64),
                                  ctypes.POINTER(i64)],
         }
@@ -203,6 +204,11 @@ def adjprod_modp_partial(m, k, p, phi, A, lda, R, ldr, depth=-1, stream=None):
 
 def adj_sum_partials(m, p, R, ldr, stride, n, C, ldc, stream=None):
     _check(lib().adj_sum_partials(m, p, _ptr(R), ldr, stride, n, _ptr(C), ldc, _stream(stream)), "adj_sum_partials")
+
+
+def adj_shard_pack(m, k, p, rank, nranks, C, ldc, buf, unpack=False, depth=-1, stream=None):
+    _check(lib().adj_shard_pack(m, k, p, depth, rank, nranks, _ptr(C), ldc, _ptr(buf), 1 if unpack else 0,
+                                _stream(stream)), "adj_shard_pack")
 
 
 def adj_shard_layout(m, k, p, rank, nranks, depth=-1):

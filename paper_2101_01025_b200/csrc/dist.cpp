@@ -130,27 +130,30 @@ adj_status_t dist_tiles(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, const u
     return ptr;
   };
   std::vector<adj::RectDev *> drects((size_t)G, nullptr);
-  std::vector<uint32_t *> bufs((size_t)G, nullptr);
+  std::vector<void *> bufs((size_t)G, nullptr);
+  const int esize = p < 65536 ? 2 : 4;   // residues travel as uint16 when they fit
   for (int q = 0; q < G; ++q) {
     if (rects[(size_t)q].empty() || q == root) continue;
     drects[(size_t)q] = static_cast<adj::RectDev *>(dalloc(rects[(size_t)q].size() * sizeof(adj::RectDev)));
-    bufs[(size_t)q] = static_cast<uint32_t *>(dalloc((size_t)elems[(size_t)q] * 4));
+    bufs[(size_t)q] = dalloc((size_t)elems[(size_t)q] * esize);
     if (!drects[(size_t)q] || !bufs[(size_t)q]) st = ADJ_ERR_CUDA;
     else if (cudaMemcpyAsync(drects[(size_t)q], rects[(size_t)q].data(), rects[(size_t)q].size() * sizeof(adj::RectDev),
                              cudaMemcpyHostToDevice, s) != cudaSuccess) st = ADJ_ERR_CUDA;
   }
   if (st == ADJ_OK && r != root && bufs[(size_t)r] &&
-      adj::launch_rect_copy(drects[(size_t)r], (int)rects[(size_t)r].size(), max_rows[(size_t)r], C, ldc, bufs[(size_t)r], 1,
-                            s) != cudaSuccess)
+      adj::launch_rect_copy(drects[(size_t)r], (int)rects[(size_t)r].size(), max_rows[(size_t)r], C, ldc, bufs[(size_t)r],
+                            esize, 1, s) != cudaSuccess)
     st = ADJ_ERR_CUDA;
   if (st == ADJ_OK) {
     g_nccl.GroupStart();
     for (int q = 0; q < G; ++q) {
       if (q == root || !bufs[(size_t)q]) continue;
       if (r == root) {
-        if (g_nccl.Recv(bufs[(size_t)q], (size_t)elems[(size_t)q], ncclUint32, q, comm->comm, s) != ncclSuccess) st = ADJ_ERR_NCCL;
+        if (g_nccl.Recv(bufs[(size_t)q], (size_t)elems[(size_t)q] * esize, ncclUint8, q, comm->comm, s) != ncclSuccess)
+          st = ADJ_ERR_NCCL;
       } else if (q == r) {
-        if (g_nccl.Send(bufs[(size_t)q], (size_t)elems[(size_t)q], ncclUint32, root, comm->comm, s) != ncclSuccess) st = ADJ_ERR_NCCL;
+        if (g_nccl.Send(bufs[(size_t)q], (size_t)elems[(size_t)q] * esize, ncclUint8, root, comm->comm, s) != ncclSuccess)
+          st = ADJ_ERR_NCCL;
       }
     }
     if (g_nccl.GroupEnd() != ncclSuccess) st = ADJ_ERR_NCCL;
@@ -159,7 +162,7 @@ adj_status_t dist_tiles(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, const u
     for (int q = 0; q < G; ++q)
       if (q != root && bufs[(size_t)q] &&
           adj::launch_rect_copy(drects[(size_t)q], (int)rects[(size_t)q].size(), max_rows[(size_t)q], C, ldc,
-                                bufs[(size_t)q], 0, s) != cudaSuccess)
+                                bufs[(size_t)q], esize, 0, s) != cudaSuccess)
         st = ADJ_ERR_CUDA;
   for (void *ptr : allocs) cudaFreeAsync(ptr, s);
   return st;
@@ -306,6 +309,27 @@ adj_status_t adjprod_modp_dist(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, 
     if (adj::launch_mod_lower(m, w, W, m, C, ldc, adj::make_modp(p), s) != cudaSuccess) st = ADJ_ERR_CUDA;
   }
   cudaFreeAsync(W, s);
+  return st;
+}
+
+adj_status_t adj_shard_pack(int64_t m, int64_t k, uint32_t p, int depth, int rank, int nranks, uint32_t *C,
+                            int64_t ldc, void *buf, int unpack, adj_stream_t stream) {
+  if (m < 0 || ldc < m || !C || !buf) return ADJ_ERR_INVALID_VALUE;
+  if (m == 0) return ADJ_OK;
+  std::vector<adj::RectDev> rects;
+  int64_t elems = 0;
+  int max_rows = 0;
+  adj_status_t st = rank_rects(m, k, p, depth, rank, nranks, rects, &elems, &max_rows);
+  if (st != ADJ_OK || rects.empty()) return st;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  void *d = nullptr;
+  if (adj_pool_alloc(&d, rects.size() * sizeof(adj::RectDev), s) != cudaSuccess) return ADJ_ERR_CUDA;
+  if (cudaMemcpyAsync(d, rects.data(), rects.size() * sizeof(adj::RectDev), cudaMemcpyHostToDevice, s) != cudaSuccess)
+    st = ADJ_ERR_CUDA;
+  if (st == ADJ_OK && adj::launch_rect_copy(static_cast<adj::RectDev *>(d), (int)rects.size(), max_rows, C, ldc, buf,
+                                            p < 65536 ? 2 : 4, unpack ? 0 : 1, s) != cudaSuccess)
+    st = ADJ_ERR_CUDA;
+  cudaFreeAsync(d, s);
   return st;
 }
 

@@ -1861,25 +1861,29 @@ cudaError_t launch_scale_lower(int64_t m, int w, uint32_t *X, int64_t ldx, uint3
 }
 
 // Up(C) = phi(Low(C)) (Lemma lem:uplow): C[j][i] = C[i][j] (conjugated for phi = H), i > j
-// one block per (region row, region); threads over the columns
-__global__ void __launch_bounds__(256) rect_copy_kernel(const RectDev *rects, uint32_t *C, int64_t ldc, uint32_t *buf,
+// one block per (region row, region); threads over the columns.  The packed buffer holds
+// uint16 residues when p < 2^16 (half the bytes on the wire), uint32 otherwise.
+template <typename BT>
+__global__ void __launch_bounds__(256) rect_copy_kernel(const RectDev *rects, uint32_t *C, int64_t ldc, BT *buf,
                                                         int to_buf) {
   const RectDev R = rects[blockIdx.y];
   const int64_t i = blockIdx.x;
   if (i >= R.rows) return;
   uint32_t *c = C + (R.r0 + i) * ldc + R.c0;
-  uint32_t *b = buf + R.off + i * R.cols;
+  BT *b = buf + R.off + i * R.cols;
   const int64_t ncol = R.lower ? min64(R.cols, R.r0 + i - R.c0 + 1) : R.cols;
   for (int64_t j = threadIdx.x; j < ncol; j += blockDim.x) {
-    if (to_buf) b[j] = c[j];
+    if (to_buf) b[j] = (BT)c[j];
     else c[j] = b[j];
   }
 }
 
-cudaError_t launch_rect_copy(const RectDev *rects, int n, int max_rows, uint32_t *C, int64_t ldc, uint32_t *buf,
-                             int to_buf, cudaStream_t s) {
+cudaError_t launch_rect_copy(const RectDev *rects, int n, int max_rows, uint32_t *C, int64_t ldc, void *buf,
+                             int esize, int to_buf, cudaStream_t s) {
   if (n == 0 || max_rows == 0) return cudaSuccess;
-  rect_copy_kernel<<<dim3((unsigned)max_rows, (unsigned)n), 256, 0, s>>>(rects, C, ldc, buf, to_buf);
+  const dim3 grid((unsigned)max_rows, (unsigned)n);
+  if (esize == 2) rect_copy_kernel<uint16_t><<<grid, 256, 0, s>>>(rects, C, ldc, static_cast<uint16_t *>(buf), to_buf);
+  else rect_copy_kernel<uint32_t><<<grid, 256, 0, s>>>(rects, C, ldc, static_cast<uint32_t *>(buf), to_buf);
   return cudaGetLastError();
 }
 

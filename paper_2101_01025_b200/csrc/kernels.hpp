@@ -22,8 +22,9 @@ cudaError_t launch_scale_lower(int64_t m, int w, uint32_t *X, int64_t ldx, uint3
 cudaError_t launch_mod_lower(int64_t m, int w, const uint32_t *src, int64_t lds, uint32_t *dst, int64_t ldd,
                              const ModP &mod, cudaStream_t s);
 // pack (to_buf = 1) / unpack (to_buf = 0) the listed regions of C into / from a contiguous buffer
-cudaError_t launch_rect_copy(const RectDev *rects, int n, int max_rows, uint32_t *C, int64_t ldc, uint32_t *buf,
-                             int to_buf, cudaStream_t s);
+// of esize-byte residues (2: uint16 for p < 2^16)
+cudaError_t launch_rect_copy(const RectDev *rects, int n, int max_rows, uint32_t *C, int64_t ldc, void *buf,
+                             int esize, int to_buf, cudaStream_t s);
 // C[i][j] = (sum_r R_r[i][j]) mod p on Low, R_r = R + r * stride (elements of `esize` bytes)
 cudaError_t launch_sum_partials(int64_t m, const void *R, int64_t ldr, int64_t stride, int n, int esize, uint32_t *C,
                                 int64_t ldc, const ModP &mod, cudaStream_t s);

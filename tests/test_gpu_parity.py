@@ -476,3 +476,29 @@ def test_cuda_graph_capture_and_replay(adj, depth):
         g.replay()
         torch.cuda.synchronize()
         assert np.array_equal(low(to_host(C)), ref)
+
+
+@pytest.mark.parametrize("p", [8191, 131071])
+@pytest.mark.parametrize("depth", [0, 1])
+def test_shard_pack_unpack_round_trip(adj, p, depth):
+    """The gather step of ADJ_DIST_TILES on one device: each rank's regions packed from C into a
+    contiguous buffer (uint16 residues for p < 2^16) and unpacked into a fresh C land exactly on
+    that rank's regions."""
+    import torch
+    m, k, G = 1030, 300, 3
+    A = uniform_matrix(m, k, seed=4, p=p)
+    C = to_dev(oracle.syrk_t(A, p))
+    for r in range(G):
+        rects = adj.adj_shard_layout(m, k, p, r, G, depth=depth)
+        n = sum(rows * cols for (_, _, rows, cols, _) in rects)
+        buf = torch.empty(max(n, 1), dtype=torch.int16 if p < 65536 else torch.int32, device="cuda")
+        adj.adj_shard_pack(m, k, p, r, G, C, m, buf, unpack=False, depth=depth)
+        C2 = torch.full((m, m), -1, dtype=torch.int32, device="cuda")
+        adj.adj_shard_pack(m, k, p, r, G, C2, m, buf, unpack=True, depth=depth)
+        got, ref = to_host(C2), to_host(C)
+        mine = np.zeros((m, m), dtype=bool)
+        for (r0, c0, rows, cols, lower) in rects:
+            ii, jj = np.meshgrid(np.arange(rows) + r0, np.arange(cols) + c0, indexing="ij")
+            mine[r0:r0 + rows, c0:c0 + cols] = (jj <= ii) if lower else True
+        assert np.array_equal(got[mine], ref[mine])
+        assert (got[~mine] == 0xFFFFFFFF).all()
