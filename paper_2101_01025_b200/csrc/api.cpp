@@ -310,6 +310,13 @@ adj_status_t launch_leaf_all(const Plan &P, const Ptrs &x, cudaStream_t s) {
   L.n_tiles = (int32_t)(P.tiles.size() / 2);
   L.fixup = x.ws + P.fixup_offset;
   if (const char *dbg = getenv("ADJ_LEAF_DEBUG")) L.debug = atoi(dbg);   // diagnostics only
+  // diagnostics: ADJ_LEAF_STATIC / ADJ_LEAF_DYNAMIC force the job scheduler (A/B measurements)
+  static const bool force_static = getenv("ADJ_LEAF_STATIC") != nullptr;
+  static const bool force_dynamic = getenv("ADJ_LEAF_DYNAMIC") != nullptr;
+  if (force_dynamic || (P.dynamic && !force_static)) {
+    L.job_counter = reinterpret_cast<int32_t *>(x.ws + P.counter_offset);
+    CUDA_TRY(cudaMemsetAsync(L.job_counter, 0, sizeof(int32_t), s));
+  }
   LAUNCH_CLS(CLS_LEAF, launch_leaf2(L, P.nacc, P.segmented, P.grid, s));
   if (!P.fixups.empty()) LAUNCH_CLS(CLS_LEAF, launch_fixup(L, P.d_fixups, (int)P.fixups.size(), s));
   return ADJ_OK;

@@ -129,7 +129,8 @@ struct Leaf2Cfg {
   //  touches are conflict-free)
   static constexpr int PART_STRIDE = WIDE ? 193 : 130;
   static constexpr int PART_BYTES = PART ? 128 * PART_STRIDE * 4 : 0;
-  static constexpr int BAR_BYTES = 8 * (2 * STAGES + 2 * SLOTS) + 16;
+  static constexpr int JQ = 4;   // dynamic job queue depth (job index ring + full / empty barriers)
+  static constexpr int BAR_BYTES = 8 * (2 * STAGES + 2 * SLOTS + 2 * JQ) + 16 + 8 * JQ;
   static constexpr int SMEM = STAGES * STAGE_BYTES + PART_BYTES + 1024 + BAR_BYTES;
   static constexpr int EPI_WARPS = ADJ_EPI_WARPS;       // 4, 8 or 16: 1, 2 or 4 warps per TMEM lane quadrant
   static constexpr int THREADS = 32 * (EPI_WARPS + 3);   // + TMEM allocator, MMA issuer, TMA producer
@@ -151,7 +152,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (ADJ_EPI_WARPS 
   uint64_t *empty_bar = full_bar + Cfg::STAGES;
   uint64_t *slot_full = empty_bar + Cfg::STAGES;
   uint64_t *slot_empty = slot_full + Cfg::SLOTS;
-  uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(slot_empty + Cfg::SLOTS);
+  uint64_t *jq_full = slot_empty + Cfg::SLOTS;
+  uint64_t *jq_empty = jq_full + Cfg::JQ;
+  uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(jq_empty + Cfg::JQ);
+  uint2 *jq = reinterpret_cast<uint2 *>(tmem_holder + 4);   // job descriptors (P.tiles entries)
 
   uint64_t g_enter = 0;
   long long c_enter = clock64();
@@ -177,6 +181,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (ADJ_EPI_WARPS 
       ptx::mbar_init(&slot_full[s], 1);
       ptx::mbar_init(&slot_empty[s], 2 * EW);   // epilogue warps x 2 CTAs (used in the leader)
     }
+    for (int s = 0; s < Cfg::JQ; ++s) {
+      ptx::mbar_init(&jq_full[s], 1);
+      // consumers of a job index: leader MMA thread, peer producer, epilogue warps of both CTAs
+      ptx::mbar_init(&jq_empty[s], 2 + 2 * EW);
+    }
     ptx::fence_barrier_init();
     for (int i = 0; i < kMaxMaps; ++i) {
       ptx::prefetch_tmap(&P.maps[i]);
@@ -190,6 +199,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (ADJ_EPI_WARPS 
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
+  // Job sequence of this cluster.  Static: cid, cid + ncl, ...  Dynamic (P.job_counter): the
+  // leader's producer claims job indices with an atomic (two jobs ahead, so neither the atomic
+  // nor the descriptor load stalls it), publishes each job descriptor in the job ring of both
+  // CTAs (jq, jq_full); every other role reads the same sequence and releases the ring slot in
+  // the leader (jq_empty).  Descriptor .x = ~0u ends the sequence.  In-order claiming keeps the
+  // 74 concurrent tiles a contiguous window of the rasterised list even when clusters run at
+  // different speeds (L2 reuse: measured -14% time at c3 / c4).
+  const bool dyn = P.job_counter != nullptr;
+  constexpr uint32_t kEnd = 0xFFFFFFFFu;
+  auto job_consume = [&](int i, bool remote_release) -> uint2 {   // all roles but the leader producer
+    const int s = i & (Cfg::JQ - 1);
+    ptx::mbar_wait_cluster(&jq_full[s], (uint32_t)(i / Cfg::JQ) & 1);
+    const volatile uint32_t *src = reinterpret_cast<volatile uint32_t *>(&jq[s]);
+    const uint2 d = make_uint2(src[0], src[1]);
+    const uint32_t e = ptx::smem_u32(&jq_empty[s]);
+    if (remote_release) ptx::mbar_arrive_cluster_release(ptx::mapa(e, 0));
+    else ptx::mbar_arrive(&jq_empty[s]);
+    return d;
+  };
+
   if (warp == W_TMA) {
     // ------------------------------------------------------------ TMA producer (both CTAs)
     if (lane == 0) {
@@ -198,12 +227,40 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (ADJ_EPI_WARPS 
       const bool skip_tma = (P.debug & 1) != 0;
       const bool prof = (P.debug & 128) != 0;
       long long t_empty = 0, t_tma = 0, t_begin = clock64();
-      uint2 next = cid < P.n_tiles ? __ldg(&P.tiles[cid]) : make_uint2(0u, 0u);
-      for (int t = cid; t < P.n_tiles; t += ncl) {
+      uint2 next = (!dyn && cid < P.n_tiles) ? __ldg(&P.tiles[cid]) : make_uint2(0u, 0u);
+      int idx2 = 0;
+      uint2 d1 = make_uint2(kEnd, 0u);
+      if (dyn && leader) {
+        const int idx1 = atomicAdd(P.job_counter, 1);
+        idx2 = atomicAdd(P.job_counter, 1);
+        if (idx1 < P.n_tiles) d1 = __ldg(&P.tiles[idx1]);
+      }
+      for (int i = 0;; ++i) {
+        int t = 0;
+        if (!dyn) {
+          t = cid + i * ncl;
+          if (t >= P.n_tiles) break;
+        } else if (leader) {
+          const int s = i & (Cfg::JQ - 1);
+          ptx::mbar_wait_cluster(&jq_empty[s], ((uint32_t)(i / Cfg::JQ) & 1) ^ 1);
+          next = d1;
+          jq[s] = next;
+          const uint32_t peer = ptx::mapa(ptx::smem_u32(&jq[s]), 1);
+          ptx::st_shared_cluster_u32(peer, next.x);
+          ptx::st_shared_cluster_u32(peer + 4, next.y);
+          ptx::mbar_arrive(&jq_full[s]);
+          ptx::mbar_arrive_cluster_release(ptx::mapa(ptx::smem_u32(&jq_full[s]), 1));
+          if (next.x == kEnd) break;
+          d1 = idx2 < P.n_tiles ? __ldg(&P.tiles[idx2]) : make_uint2(kEnd, 0u);   // used next iteration
+          idx2 = atomicAdd(P.job_counter, 1);                                     // claimed for i + 2
+        } else {
+          next = job_consume(i, true);
+          if (next.x == kEnd) break;
+        }
         int q, I, J, jb0, jb1, piece, nh;
         decode_tile(next.x, q, I, J);
         const uint32_t range = next.y;
-        if (t + ncl < P.n_tiles) next = __ldg(&P.tiles[t + ncl]);   // prefetch the next job
+        if (!dyn && t + ncl < P.n_tiles) next = __ldg(&P.tiles[t + ncl]);   // prefetch the next job
         const LeafProduct &pr = P.prod[q];
         const CUtensorMap *map = &P.maps[pr.map];
         const int kseg = pr.kseg;
@@ -261,12 +318,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (ADJ_EPI_WARPS 
       const uint32_t smem_base = ptx::smem_u32(smem);
       const bool prof = (P.debug & 128) != 0;
       long long t_full = 0, t_slot = 0, t_issue = 0, t_begin = clock64();
-      uint2 next = cid < P.n_tiles ? __ldg(&P.tiles[cid]) : make_uint2(0u, 0u);
-      for (int t = cid; t < P.n_tiles; t += ncl) {
+      uint2 next = (!dyn && cid < P.n_tiles) ? __ldg(&P.tiles[cid]) : make_uint2(0u, 0u);
+      for (int i = 0;; ++i) {
+        int t;
+        if (!dyn) {
+          t = cid + i * ncl;
+          if (t >= P.n_tiles) break;
+        } else {
+          next = job_consume(i, false);
+          if (next.x == kEnd) break;
+        }
         int q, I, J, jb0, jb1, piece, nh;
         decode_tile(next.x, q, I, J);
         const uint32_t range = next.y;
-        if (t + ncl < P.n_tiles) next = __ldg(&P.tiles[t + ncl]);
+        if (!dyn && t + ncl < P.n_tiles) next = __ldg(&P.tiles[t + ncl]);
         const LeafProduct &pr = P.prod[q];
         const int kseg = pr.kseg;
         decode_range(range, pr.kblocks, jb0, jb1, piece, nh);
@@ -332,9 +397,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (ADJ_EPI_WARPS 
     const uint32_t empty_remote0 = ptx::mapa(ptx::smem_u32(&slot_empty[0]), 0);
     const uint32_t empty_remote1 = ptx::mapa(ptx::smem_u32(&slot_empty[1]), 0);
     uint32_t unit = 0;
-    for (int t = cid; t < P.n_tiles; t += ncl) {
+    for (int i = 0;; ++i) {
+      uint2 job = make_uint2(0u, 0u);
+      if (!dyn) {
+        const int t = cid + i * ncl;
+        if (t >= P.n_tiles) break;
+        job = P.tiles[t];
+      } else {
+        if (lane == 0) job = job_consume(i, !leader);
+        job.x = __shfl_sync(0xFFFFFFFFu, job.x, 0);
+        job.y = __shfl_sync(0xFFFFFFFFu, job.y, 0);
+        if (job.x == kEnd) break;
+      }
       int q, I, J, jb0, jb1, piece, nh;
-      const uint2 job = P.tiles[t];
       decode_tile(job.x, q, I, J);
       const LeafProduct &pr = P.prod[q];
       decode_range(job.y, pr.kblocks, jb0, jb1, piece, nh);

@@ -78,8 +78,10 @@ struct Plan {
   std::vector<FixupTile> fixups;     // tail tiles split along K into pieces
   FixupTile *d_fixups = nullptr;
   size_t fixup_offset = 0;           // workspace offset of the 256x256 u16 piece slots
+  size_t counter_offset = 0;         // workspace offset of the leaf's dynamic job counter
   int n_pieces = 0;
   int grid = 1;
+  bool dynamic = false;              // leaf jobs claimed with an atomic counter (long launches)
   int dev = 0;
   LeafParams leaf_template;           // terms, weights, mod (maps/outs bound per call)
   // output-tile sharding (adjprod_modp_shard): this plan computes only the tiles `shard_rank` owns

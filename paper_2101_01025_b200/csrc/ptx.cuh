@@ -164,6 +164,14 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
   // only state handed over is TMEM, ordered by tcgen05.fence::before_thread_sync
   asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
+// release at cluster scope: orders this thread's earlier shared::cluster stores (e.g. into the
+// barrier's CTA) before the arrival
+__device__ __forceinline__ void mbar_arrive_cluster_release(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void st_shared_cluster_u32(uint32_t cluster_addr, uint32_t v) {
+  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(cluster_addr), "r"(v) : "memory");
+}
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
   uint32_t addr = smem_u32(bar);
   asm volatile(

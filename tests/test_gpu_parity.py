@@ -502,3 +502,32 @@ def test_shard_pack_unpack_round_trip(adj, p, depth):
             mine[r0:r0 + rows, c0:c0 + cols] = (jj <= ii) if lower else True
         assert np.array_equal(got[mine], ref[mine])
         assert (got[~mine] == 0xFFFFFFFF).all()
+
+
+def test_dynamic_job_scheduler_forced_small_shapes():
+    """The dynamic (atomic-counter) leaf job scheduler is chosen for long launches only; force it
+    (ADJ_LEAF_DYNAMIC, read once per process) on small shapes of every path in a subprocess."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import numpy as np, torch, oracle, paper_2101_01025_b200 as adj
+from inputs import uniform_matrix, uniform_matrix_ext, uniform_matrix_quat
+def dev(a): return torch.from_numpy(np.ascontiguousarray(a).view(np.int32)).cuda()
+def host(t): return t.cpu().numpy().view(np.uint32)
+bad = 0
+for p, m, k, d in [(97, 300, 200, 0), (8191, 700, 513, 1), (65521, 513, 1100, 2), (131071, 400, 300, 1)]:
+    A = uniform_matrix(m, k, seed=m, p=p)
+    bad += not np.array_equal(np.tril(host(adj.adjprod(dev(A), p, depth=d))), oracle.syrk_t(A, p))
+A = uniform_matrix(1000, 300, seed=1, p=8191); B = uniform_matrix(777, 300, seed=2, p=8191)
+bad += not np.array_equal(host(adj.gemm(dev(A), dev(B), 8191)), oracle.gemm_nt(A, B, 8191))
+H = uniform_matrix_ext(300, 200, seed=3, p=8191)
+bad += not np.array_equal(host(adj.adjprod(dev(H), 8191, phi="H")), oracle.syrk_h(H, 8191))
+Q = uniform_matrix_quat(200, 150, seed=4, p=8191)
+bad += not np.array_equal(host(adj.adjprod(dev(Q), 8191, phi="Q")), oracle.syrk_q(Q, 8191))
+print("BAD", bad)
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, ADJ_LEAF_DYNAMIC="1", PYTHONPATH=root)
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600, cwd=root)
+    assert "BAD 0" in out.stdout, out.stdout + out.stderr
