@@ -1,4 +1,4 @@
-// Host-callable launchers of the sm_100a kernels (kernels.cu).
+// Host-callable launchers of the sm_100a kernels (leaf.cu, preadd.cu, combine.cu, misc.cu).
 #pragma once
 #include <cuda_runtime.h>
 

@@ -1,0 +1,574 @@
+// K2/K3 leaf kernel: grouped persistent tcgen05 int8 GEMM /
+// lower-triangle SYRK on CTA pairs, int32 TMEM accumulators, mod-p limb-recombination epilogue
+// (P1..P5 of Alg. alg:MIAHMM), and the tail fixup kernel.
+#include <algorithm>
+#include <cstdio>
+
+#include "kernel_util.cuh"
+
+namespace adj {
+
+// ============================================================================ leaf kernel
+__device__ __forceinline__ void decode_tile(uint32_t packed, int &q, int &I, int &J) {
+  q = (int)(packed >> 24);
+  I = (int)((packed >> 12) & 0xFFF);
+  J = (int)(packed & 0xFFF);
+}
+
+// k-block range, fixup piece and column half of a job (whole tile: [0, kblocks), piece 0,
+// nhalf 0; nhalf 1 / 2: columns 0..127 / 128..255 of the tile with an N = 128 MMA)
+__device__ __forceinline__ void decode_range(uint32_t y, int kblocks, int &kb0, int &kb1, int &piece, int &nhalf) {
+  nhalf = 0;
+  if (y == 0 || (y & 0xFFFFFFu) == 0xFFFFFFu) {   // whole tile, or column half (empty range sentinel)
+    kb0 = 0; kb1 = kblocks; piece = 0;
+    if (y != 0) nhalf = 1 + (int)(y >> 24);
+    return;
+  }
+  kb0 = (int)(y & 0xFFF);
+  kb1 = (int)((y >> 12) & 0xFFF);
+  piece = (int)(y >> 24);
+}
+
+// store 32 consecutive residues r[0..31] of output row `row`, columns col..col+31
+__device__ __forceinline__ void store_chunk(const LeafProduct &pr, int64_t row, int64_t col,
+                                            const uint32_t (&r)[32], const ModP &m) {
+  if (row >= pr.out_rows || col >= pr.out_cols) return;
+  if (pr.sym && col > row) return;
+  const bool full = (col + 32 <= pr.out_cols) && (!pr.sym || col + 31 <= row) && pr.vec_ok;
+  if (pr.out_u32) {
+    uint32_t *o = reinterpret_cast<uint32_t *>(pr.out) + row * pr.ldo + col;
+    if (pr.axpby) {   // SYRK form: out <- alpha v + beta out_old (scalar path, final output only)
+#pragma unroll
+      for (int e = 0; e < 32; ++e)
+        if (col + e < pr.out_cols && (!pr.sym || col + e <= row))
+          o[e] = addmod(mulmod_any(pr.alpha, r[e], m), mulmod_any(pr.beta, mod_u32(o[e], m), m), m);
+      return;
+    }
+    if (full) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        reinterpret_cast<uint4 *>(o)[i] = make_uint4(r[4 * i], r[4 * i + 1], r[4 * i + 2], r[4 * i + 3]);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 32; ++e)
+        if (col + e < pr.out_cols && (!pr.sym || col + e <= row)) o[e] = r[e];
+    }
+  } else {
+    uint16_t *o = reinterpret_cast<uint16_t *>(pr.out) + row * pr.ldo + col;
+    if (full) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        uint4 v;
+        v.x = r[8 * i + 0] | (r[8 * i + 1] << 16);
+        v.y = r[8 * i + 2] | (r[8 * i + 3] << 16);
+        v.z = r[8 * i + 4] | (r[8 * i + 5] << 16);
+        v.w = r[8 * i + 6] | (r[8 * i + 7] << 16);
+        reinterpret_cast<uint4 *>(o)[i] = v;
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 32; ++e)
+        if (col + e < pr.out_cols && (!pr.sym || col + e <= row)) o[e] = (uint16_t)r[e];
+    }
+  }
+}
+
+// ============================================================================ leaf kernel, CTA pair
+// cta_group::2 version: a cluster of 2 CTAs (one TPC) computes a 256 x 256 tile with
+// tcgen05.mma.cta_group::2 M=256 N=256 K=32 (int8).  CTA r holds rows r*128.. of the A tile and
+// rows r*128.. of the B tile in its shared memory, and accumulator rows r*128.. in its TMEM.
+// Per SM this halves shared-memory traffic versus the 1-CTA M=128 N=128 tile (TMA writes 64 B/clk
+// + MMA operand reads 64 B/clk at full tensor rate).  TMEM holds 2 slots of 256 columns; the NACC
+// limb accumulators of a tile run one after the other (acc-major), the epilogue folds each into
+// a weighted mod-p partial sum kept in registers (8 warps x 128 columns).
+#ifndef ADJ_EPI_WARPS
+#define ADJ_EPI_WARPS 8
+#endif
+template <int NACC, bool PART, bool WIDE = false>
+struct Leaf2Cfg {
+  static constexpr int STAGES = PART ? (WIDE ? 4 : 5) : 6;
+  static constexpr int TILE = 256;
+  static constexpr int A_BYTES = 128 * kBK;
+  static constexpr int B_BYTES = 128 * kBK;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int SLOTS = 2;
+  // weighted mod-p partial sums of the limb accumulators: 128 rows x 128 words (u16 pairs)
+  // WIDE (p > 2^16): residues < 2^18 packed 24-bit (4 values in 3 words): 192 words + 1 pad per row
+  // (non-WIDE: stride 130 words = 65 8-byte granules, so 64-bit accesses of the 32 rows a warp
+  //  touches are conflict-free)
+  static constexpr int PART_STRIDE = WIDE ? 193 : 130;
+  static constexpr int PART_BYTES = PART ? 128 * PART_STRIDE * 4 : 0;
+  static constexpr int JQ = 4;   // dynamic job queue depth (job index ring + full / empty barriers)
+  static constexpr int BAR_BYTES = 8 * (2 * STAGES + 2 * SLOTS + 2 * JQ) + 16 + 8 * JQ;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + PART_BYTES + 1024 + BAR_BYTES;
+  static constexpr int EPI_WARPS = ADJ_EPI_WARPS;       // 4, 8 or 16: 1, 2 or 4 warps per TMEM lane quadrant
+  static constexpr int THREADS = 32 * (EPI_WARPS + 3);   // + TMEM allocator, MMA issuer, TMA producer
+};
+
+// NACC limb accumulators per tile; each may be split into K segments of at most pr.kseg k-blocks
+// (int32 bound).  A (accumulator, segment) pair is one TMEM unit; PART = the
+// epilogue folds units into the shared-memory partial sum (needed when a tile has > 1 unit).
+template <int NACC, bool PART, bool WIDE>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (ADJ_EPI_WARPS + 3), 1)
+    leaf2_kernel(const __grid_constant__ LeafParams P) {
+  using Cfg = Leaf2Cfg<NACC, PART, WIDE>;
+  extern __shared__ uint8_t smem_raw[];
+  // 1024-byte alignment (128B swizzle atoms) by pointer arithmetic on the __shared__ array, so
+  // that the compiler keeps the shared state space (LDS/STS, not generic LD/ST)
+  uint8_t *smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint32_t *part_s = reinterpret_cast<uint32_t *>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+  uint64_t *full_bar = reinterpret_cast<uint64_t *>(smem + Cfg::STAGES * Cfg::STAGE_BYTES + Cfg::PART_BYTES);
+  uint64_t *empty_bar = full_bar + Cfg::STAGES;
+  uint64_t *slot_full = empty_bar + Cfg::STAGES;
+  uint64_t *slot_empty = slot_full + Cfg::SLOTS;
+  uint64_t *jq_full = slot_empty + Cfg::SLOTS;
+  uint64_t *jq_empty = jq_full + Cfg::JQ;
+  uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(jq_empty + Cfg::JQ);
+  uint2 *jq = reinterpret_cast<uint2 *>(tmem_holder + 4);   // job descriptors (P.tiles entries)
+
+  uint64_t g_enter = 0;
+  long long c_enter = clock64();
+  if (P.debug & (128 | 16384)) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_enter));
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = ptx::cluster_ctarank();
+  const bool leader = rank == 0;
+  const int cid = (int)ptx::cluster_id_x();
+  const int ncl = (int)ptx::num_clusters_x();
+
+  // warp roles: 0..7 epilogue, 8 TMEM allocator, 9 MMA issuer, 10 TMA producer.  The issue
+  // arbiter favours the highest warp id, so the two latency-critical single-thread loops win
+  // their sub-partition against the ALU-heavy epilogue warps.
+  constexpr int EW = Cfg::EPI_WARPS;
+  constexpr int W_ALLOC = EW, W_MMA = EW + 1, W_TMA = EW + 2;
+  if (warp == W_TMA && lane == 0) {
+    for (int s = 0; s < Cfg::STAGES; ++s) {
+      ptx::mbar_init(&full_bar[s], 1);
+      ptx::mbar_init(&empty_bar[s], 1);
+    }
+    for (int s = 0; s < Cfg::SLOTS; ++s) {
+      ptx::mbar_init(&slot_full[s], 1);
+      ptx::mbar_init(&slot_empty[s], 2 * EW);   // epilogue warps x 2 CTAs (used in the leader)
+    }
+    for (int s = 0; s < Cfg::JQ; ++s) {
+      ptx::mbar_init(&jq_full[s], 1);
+      // consumers of a job index: leader MMA thread, peer producer, epilogue warps of both CTAs
+      ptx::mbar_init(&jq_empty[s], 2 + 2 * EW);
+    }
+    ptx::fence_barrier_init();
+    for (int i = 0; i < kMaxMaps; ++i) {
+      ptx::prefetch_tmap(&P.maps[i]);
+      ptx::prefetch_tmap(&P.maps_half[i]);
+    }
+  }
+  if (warp == W_ALLOC) ptx::tmem_alloc_2sm(tmem_holder, 512);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::cluster_sync();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  // Job sequence of this cluster.  Static: cid, cid + ncl, ...  Dynamic (P.job_counter): the
+  // leader's producer claims job indices with an atomic (two jobs ahead, so neither the atomic
+  // nor the descriptor load stalls it), publishes each job descriptor in the job ring of both
+  // CTAs (jq, jq_full); every other role reads the same sequence and releases the ring slot in
+  // the leader (jq_empty).  Descriptor .x = ~0u ends the sequence.  In-order claiming keeps the
+  // 74 concurrent tiles a contiguous window of the rasterised list even when clusters run at
+  // different speeds (L2 reuse: measured -14% time at c3 / c4).
+  const bool dyn = P.job_counter != nullptr;
+  constexpr uint32_t kEnd = 0xFFFFFFFFu;
+  auto job_consume = [&](int i, bool remote_release) -> uint2 {   // all roles but the leader producer
+    const int s = i & (Cfg::JQ - 1);
+    ptx::mbar_wait_cluster(&jq_full[s], (uint32_t)(i / Cfg::JQ) & 1);
+    const volatile uint32_t *src = reinterpret_cast<volatile uint32_t *>(&jq[s]);
+    const uint2 d = make_uint2(src[0], src[1]);
+    const uint32_t e = ptx::smem_u32(&jq_empty[s]);
+    if (remote_release) ptx::mbar_arrive_cluster_release(ptx::mapa(e, 0));
+    else ptx::mbar_arrive(&jq_empty[s]);
+    return d;
+  };
+
+  if (warp == W_TMA) {
+    // ------------------------------------------------------------ TMA producer (both CTAs)
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      const bool skip_tma = (P.debug & 1) != 0;
+      const bool prof = (P.debug & 128) != 0;
+      long long t_empty = 0, t_tma = 0, t_begin = clock64();
+      uint2 next = (!dyn && cid < P.n_tiles) ? __ldg(&P.tiles[cid]) : make_uint2(0u, 0u);
+      int idx2 = 0;
+      uint2 d1 = make_uint2(kEnd, 0u);
+      if (dyn && leader) {
+        const int idx1 = atomicAdd(P.job_counter, 1);
+        idx2 = atomicAdd(P.job_counter, 1);
+        if (idx1 < P.n_tiles) d1 = __ldg(&P.tiles[idx1]);
+      }
+      for (int i = 0;; ++i) {
+        int t = 0;
+        if (!dyn) {
+          t = cid + i * ncl;
+          if (t >= P.n_tiles) break;
+        } else if (leader) {
+          const int s = i & (Cfg::JQ - 1);
+          ptx::mbar_wait_cluster(&jq_empty[s], ((uint32_t)(i / Cfg::JQ) & 1) ^ 1);
+          next = d1;
+          jq[s] = next;
+          const uint32_t peer = ptx::mapa(ptx::smem_u32(&jq[s]), 1);
+          ptx::st_shared_cluster_u32(peer, next.x);
+          ptx::st_shared_cluster_u32(peer + 4, next.y);
+          ptx::mbar_arrive(&jq_full[s]);
+          ptx::mbar_arrive_cluster_release(ptx::mapa(ptx::smem_u32(&jq_full[s]), 1));
+          if (next.x == kEnd) break;
+          d1 = idx2 < P.n_tiles ? __ldg(&P.tiles[idx2]) : make_uint2(kEnd, 0u);   // used next iteration
+          idx2 = atomicAdd(P.job_counter, 1);                                     // claimed for i + 2
+        } else {
+          next = job_consume(i, true);
+          if (next.x == kEnd) break;
+        }
+        int q, I, J, jb0, jb1, piece, nh;
+        decode_tile(next.x, q, I, J);
+        const uint32_t range = next.y;
+        if (!dyn && t + ncl < P.n_tiles) next = __ldg(&P.tiles[t + ncl]);   // prefetch the next job
+        const LeafProduct &pr = P.prod[q];
+        const CUtensorMap *map = &P.maps[pr.map];
+        const int kseg = pr.kseg;
+        decode_range(range, pr.kblocks, jb0, jb1, piece, nh);
+        const CUtensorMap *bmap = nh ? &P.maps_half[pr.map] : map;
+        const int a_pr = pr.a_plane_rows, b_pr = pr.b_plane_rows;
+        const int arow = pr.a_row0 + I * Cfg::TILE + (int)rank * 128;
+        // N = 128 half jobs: this CTA's 64 rows of the B column half
+        const int brow = nh ? pr.b_row0 + J * Cfg::TILE + (nh - 1) * 128 + (int)rank * 64
+                            : pr.b_row0 + J * Cfg::TILE + (int)rank * 128;
+        const uint32_t stage_tx = nh ? 2 * (Cfg::A_BYTES + Cfg::B_BYTES / 2) : 2 * Cfg::STAGE_BYTES;
+        const int nseg = (jb1 - jb0 + kseg - 1) / kseg;
+#pragma unroll 1
+        for (int u = 0; u < NACC * nseg; ++u) {
+          const int j = u / nseg, kb0 = jb0 + (u % nseg) * kseg;
+          const int kb1 = min(jb1, kb0 + kseg);
+          // the (at most 2) operand-plane pairs accumulated into accumulator j, hoisted out of the K loop
+          const int t0 = P.acc_begin[j], nt = P.acc_begin[j + 1] - t0;
+          const int ar0 = arow + P.terms[t0].a_plane * a_pr, br0 = brow + P.terms[t0].b_plane * b_pr;
+          const int ar1 = nt > 1 ? arow + P.terms[t0 + 1].a_plane * a_pr : ar0;
+          const int br1 = nt > 1 ? brow + P.terms[t0 + 1].b_plane * b_pr : br0;
+#pragma unroll 1
+          for (int kb = kb0; kb < kb1; ++kb) {
+#pragma unroll 1
+            for (int tt = 0; tt < nt; ++tt) {
+              long long c0 = prof ? clock64() : 0;
+              ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
+              long long c1 = prof ? clock64() : 0;
+              if (prof) t_empty += c1 - c0;
+              if (skip_tma) {
+                if (leader) ptx::mbar_arrive(&full_bar[stage]);
+              } else {
+                const bool skip_b = (P.debug & 256) != 0;   // diagnostics: A operand only (L2-bound test)
+                if (leader) ptx::mbar_expect_tx(&full_bar[stage], skip_b ? 2 * Cfg::A_BYTES : stage_tx);
+                uint8_t *sa = smem + stage * Cfg::STAGE_BYTES;
+                ptx::tma_load_2d_2sm(sa, map, kb * kBK, tt ? ar1 : ar0, &full_bar[stage]);
+                if (!skip_b) ptx::tma_load_2d_2sm(sa + Cfg::A_BYTES, bmap, kb * kBK, tt ? br1 : br0, &full_bar[stage]);
+              }
+              if (prof) t_tma += clock64() - c1;
+              if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
+            }
+          }
+        }
+      }
+      if (prof && (cid == 0 || cid == ncl / 2))
+        printf("[leaf prof] cluster %d rank %u producer: total %lld cyc, empty-wait %lld, tma-issue %lld\n", cid,
+               rank, clock64() - t_begin, t_empty, t_tma);
+    }
+  } else if (warp == W_MMA) {
+    // ------------------------------------------------------------ MMA issuer (leader CTA, one thread)
+    if (leader && lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      uint32_t unit = 0;
+      const uint32_t smem_base = ptx::smem_u32(smem);
+      const bool prof = (P.debug & 128) != 0;
+      long long t_full = 0, t_slot = 0, t_issue = 0, t_begin = clock64();
+      uint2 next = (!dyn && cid < P.n_tiles) ? __ldg(&P.tiles[cid]) : make_uint2(0u, 0u);
+      for (int i = 0;; ++i) {
+        int t;
+        if (!dyn) {
+          t = cid + i * ncl;
+          if (t >= P.n_tiles) break;
+        } else {
+          next = job_consume(i, false);
+          if (next.x == kEnd) break;
+        }
+        int q, I, J, jb0, jb1, piece, nh;
+        decode_tile(next.x, q, I, J);
+        const uint32_t range = next.y;
+        if (!dyn && t + ncl < P.n_tiles) next = __ldg(&P.tiles[t + ncl]);
+        const LeafProduct &pr = P.prod[q];
+        const int kseg = pr.kseg;
+        decode_range(range, pr.kblocks, jb0, jb1, piece, nh);
+        const int nseg = (jb1 - jb0 + kseg - 1) / kseg;
+        const int mma_n = nh ? 128 : 256;
+#pragma unroll 1
+        for (int u = 0; u < NACC * nseg; ++u, ++unit) {
+          const int j = u / nseg, kb0 = jb0 + (u % nseg) * kseg;
+          const int kb1 = min(jb1, kb0 + kseg);
+          const int t0 = P.acc_begin[j], nt = P.acc_begin[j + 1] - t0;
+          const uint32_t id0 = ptx::idesc_i8(256, mma_n, P.terms[t0].a_signed != 0, P.terms[t0].b_signed != 0);
+          const uint32_t id1 = nt > 1 ? ptx::idesc_i8(256, mma_n, P.terms[t0 + 1].a_signed != 0,
+                                                      P.terms[t0 + 1].b_signed != 0) : id0;
+          const uint32_t slot = unit & 1, use = unit >> 1;
+          long long c0 = prof ? clock64() : 0;
+          if (!(P.debug & 64)) ptx::mbar_wait_cluster(&slot_empty[slot], (use & 1) ^ 1);   // 64: timing only
+          if (prof) t_slot += clock64() - c0;
+          ptx::tc_fence_after();
+          const uint32_t d_tmem = tmem_base + slot * Cfg::TILE;
+          uint32_t accumulate = 0;
+#pragma unroll 1
+          for (int kb = kb0; kb < kb1; ++kb) {
+#pragma unroll 1
+            for (int tt = 0; tt < nt; ++tt) {
+              long long c1 = prof ? clock64() : 0;
+              ptx::mbar_wait(&full_bar[stage], phase);
+              long long c2 = prof ? clock64() : 0;
+              if (prof) t_full += c2 - c1;
+              ptx::tc_fence_after();
+              const uint32_t sa = smem_base + stage * Cfg::STAGE_BYTES;
+              const uint64_t adesc = ptx::smem_desc_sw128(sa);
+              const uint64_t bdesc = ptx::smem_desc_sw128(sa + Cfg::A_BYTES);
+              const uint32_t idesc = tt ? id1 : id0;
+#pragma unroll
+              for (int kk = 0; kk < kBK / 32; ++kk) {
+                ptx::mma_i8_2sm(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, idesc, accumulate);
+                accumulate = 1;
+              }
+              ptx::mma_commit_2sm(&empty_bar[stage], 0x3);
+              if (prof) t_issue += clock64() - c2;
+              if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
+            }
+          }
+          ptx::mma_commit_2sm(&slot_full[slot], 0x3);
+        }
+      }
+      if (prof && (cid == 0 || cid == ncl / 2))
+        printf("[leaf prof] cluster %d MMA thread: total %lld cyc, full-wait %lld, slot-wait %lld, issue %lld\n", cid,
+               clock64() - t_begin, t_full, t_slot, t_issue);
+    }
+  } else if (warp < EW) {
+    // ------------------------------------------------------------ epilogue (8 warps per CTA)
+    const int q4 = warp & 3;               // TMEM lane quadrant this warp may access
+    constexpr int CPW = 1024 / EW;             // tile columns per warp (EW / 4 warps per TMEM lane quadrant)
+    const int h0 = warp >> 2;                  // which CPW-column part of the 256-wide tile
+    constexpr int NCH = CPW / 32;              // 32-column chunks per warp and unit
+    const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
+    const int lrow = q4 * 32 + lane;
+    uint32_t *prow0 = part_s + lrow * Cfg::PART_STRIDE;
+    const ModP mod = P.mod;
+    const int nchunks = (P.debug & 2) ? 0 : NCH;
+    const bool dbg_noldtm = (P.debug & 16) != 0, dbg_nomath = (P.debug & 8) != 0, dbg_nostore = (P.debug & 32) != 0;
+    const uint32_t empty_remote0 = ptx::mapa(ptx::smem_u32(&slot_empty[0]), 0);
+    const uint32_t empty_remote1 = ptx::mapa(ptx::smem_u32(&slot_empty[1]), 0);
+    uint32_t unit = 0;
+    for (int i = 0;; ++i) {
+      uint2 job = make_uint2(0u, 0u);
+      if (!dyn) {
+        const int t = cid + i * ncl;
+        if (t >= P.n_tiles) break;
+        job = P.tiles[t];
+      } else {
+        if (lane == 0) job = job_consume(i, !leader);
+        job.x = __shfl_sync(0xFFFFFFFFu, job.x, 0);
+        job.y = __shfl_sync(0xFFFFFFFFu, job.y, 0);
+        if (job.x == kEnd) break;
+      }
+      int q, I, J, jb0, jb1, piece, nh;
+      decode_tile(job.x, q, I, J);
+      const LeafProduct &pr = P.prod[q];
+      decode_range(job.y, pr.kblocks, jb0, jb1, piece, nh);
+      const int64_t row = (int64_t)I * Cfg::TILE + rank * 128 + lrow;
+      // N = 128 half jobs: TMEM columns 0..127 hold output columns (nh-1)*128..; only h0 = 0 warps work
+      const int64_t col0 = (int64_t)J * Cfg::TILE + (nh ? (nh - 1) * 128 : 0) + h0 * CPW;
+      const int nch = (nh && h0 * CPW >= 128) ? 0 : nchunks;
+      // tail piece: residue partial of this CTA's 128 x 256 half-tile into the fixup slot
+      const size_t fxo = (size_t)(piece - 1) * 65536 + (rank * 128 + lrow) * 256 + h0 * CPW;
+      uint16_t *fx = (piece && !P.fixup32) ? static_cast<uint16_t *>(P.fixup) + fxo : nullptr;
+      uint32_t *fx32 = (piece && P.fixup32) ? static_cast<uint32_t *>(P.fixup) + fxo : nullptr;
+      const int nseg = (jb1 - jb0 + pr.kseg - 1) / pr.kseg;
+      const int nunits = NACC * nseg;
+#pragma unroll 1
+      for (int u = 0; u < nunits; ++u, ++unit) {
+        const int j = u / nseg;
+        const uint32_t slot = unit & 1, use = unit >> 1;
+        ptx::mbar_wait(&slot_full[slot], use & 1);
+        ptx::tc_fence_after();
+#pragma unroll 1
+        for (int c = 0; c < nch; ++c) {
+          uint32_t v[32];
+          if (dbg_noldtm) {
+#pragma unroll
+            for (int e = 0; e < 32; ++e) v[e] = (uint32_t)(e * 977 + c + u) ^ (uint32_t)lrow;
+          } else {
+            ptx::tmem_ld32(tmem_base + lane_off + slot * Cfg::TILE + h0 * CPW + c * 32, v);
+            ptx::tmem_wait_ld();
+          }
+          if (dbg_nomath) {
+            if (v[0] == 0xFFFFFFFFu && v[31] == 0x12345u) prow0[0] = v[1];   // keep the loads alive
+            continue;
+          }
+          // (partial + acc_j * weight_j) mod p per element, Shoup-fused (modp.cuh: acc_mulred)
+          const int32_t wc = P.wshoup[j].wc, wq = P.wshoup[j].wq;
+          const uint32_t pm = mod.p;
+          if constexpr (PART && !WIDE) {
+            uint2 *pc = reinterpret_cast<uint2 *>(prow0 + h0 * (CPW / 2) + c * 16);
+            if (u > 0) {
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                const uint2 wd = pc[e];
+                v[4 * e] = acc_mulred((int32_t)v[4 * e], wc, wq, wd.x & 0xFFFF, pm);
+                v[4 * e + 1] = acc_mulred((int32_t)v[4 * e + 1], wc, wq, wd.x >> 16, pm);
+                v[4 * e + 2] = acc_mulred((int32_t)v[4 * e + 2], wc, wq, wd.y & 0xFFFF, pm);
+                v[4 * e + 3] = acc_mulred((int32_t)v[4 * e + 3], wc, wq, wd.y >> 16, pm);
+              }
+            } else {
+#pragma unroll
+              for (int e = 0; e < 32; ++e) v[e] = acc_mulred((int32_t)v[e], wc, wq, 0u, pm);
+            }
+            if (u < nunits - 1) {
+#pragma unroll
+              for (int e = 0; e < 8; ++e)
+                pc[e] = make_uint2(v[4 * e] | (v[4 * e + 1] << 16), v[4 * e + 2] | (v[4 * e + 3] << 16));
+              continue;
+            }
+          } else if constexpr (PART && WIDE) {
+            uint32_t *pc = prow0 + h0 * (CPW * 3 / 4) + c * 24;     // 32 residues of 24 bits = 24 words
+            if (u > 0) {
+#pragma unroll
+              for (int g = 0; g < 8; ++g) {
+                const uint32_t w0 = pc[3 * g], w1 = pc[3 * g + 1], w2 = pc[3 * g + 2];
+                v[4 * g] = acc_mulred((int32_t)v[4 * g], wc, wq, w0 & 0xFFFFFF, pm);
+                v[4 * g + 1] = acc_mulred((int32_t)v[4 * g + 1], wc, wq, (w0 >> 24) | ((w1 & 0xFFFF) << 8), pm);
+                v[4 * g + 2] = acc_mulred((int32_t)v[4 * g + 2], wc, wq, (w1 >> 16) | ((w2 & 0xFF) << 16), pm);
+                v[4 * g + 3] = acc_mulred((int32_t)v[4 * g + 3], wc, wq, w2 >> 8, pm);
+              }
+            } else {
+#pragma unroll
+              for (int e = 0; e < 32; ++e) v[e] = acc_mulred((int32_t)v[e], wc, wq, 0u, pm);
+            }
+            if (u < nunits - 1) {
+#pragma unroll
+              for (int g = 0; g < 8; ++g) {
+                pc[3 * g] = v[4 * g] | (v[4 * g + 1] << 24);
+                pc[3 * g + 1] = (v[4 * g + 1] >> 8) | (v[4 * g + 2] << 16);
+                pc[3 * g + 2] = (v[4 * g + 2] >> 16) | (v[4 * g + 3] << 8);
+              }
+              continue;
+            }
+          } else {
+#pragma unroll
+            for (int e = 0; e < 32; ++e) v[e] = acc_mulred((int32_t)v[e], wc, wq, 0u, pm);
+          }
+          if (fx32) {
+            uint4 *d = reinterpret_cast<uint4 *>(fx32 + c * 32);
+#pragma unroll
+            for (int i4 = 0; i4 < 8; ++i4) d[i4] = make_uint4(v[4 * i4], v[4 * i4 + 1], v[4 * i4 + 2], v[4 * i4 + 3]);
+          } else if (fx) {
+            uint4 *d = reinterpret_cast<uint4 *>(fx + c * 32);
+#pragma unroll
+            for (int i4 = 0; i4 < 4; ++i4)
+              d[i4] = make_uint4(v[8 * i4] | (v[8 * i4 + 1] << 16), v[8 * i4 + 2] | (v[8 * i4 + 3] << 16),
+                                 v[8 * i4 + 4] | (v[8 * i4 + 5] << 16), v[8 * i4 + 6] | (v[8 * i4 + 7] << 16));
+          } else if (!dbg_nostore) {
+            store_chunk(pr, row, col0 + c * 32, v, mod);
+          } else if (v[0] == 0xFFFFFFFFu && v[31] == 0x12345u) {
+            prow0[0] = v[1];
+          }
+        }
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_cluster(slot ? empty_remote1 : empty_remote0);
+      }
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::cluster_sync();
+  if (warp == W_ALLOC) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc_2sm(tmem_base, 512);
+  }
+  if ((P.debug & (128 | 16384)) && threadIdx.x == 0 && rank == 0) {   // 16384: exit times only
+    uint64_t g_exit;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_exit));
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    const long long c_exit = clock64();
+    printf("[leaf time] cluster %d sm %u enter %llu exit %llu cycles %lld eff_mhz %.1f\n", cid, smid,
+           (unsigned long long)g_enter, (unsigned long long)g_exit, c_exit - c_enter,
+           1e3 * (double)(c_exit - c_enter) / (double)(g_exit - g_enter));
+  }
+}
+
+template <int NACC, bool PART, bool WIDE>
+static cudaError_t launch_leaf2_t(const LeafParams &p, int grid, cudaStream_t s) {
+  using Cfg = Leaf2Cfg<NACC, PART, WIDE>;
+  static std::atomic<uint64_t> done{0};
+  cudaError_t e = ensure_smem(leaf2_kernel<NACC, PART, WIDE>, Cfg::SMEM, done);
+  if (e != cudaSuccess) return e;
+  leaf2_kernel<NACC, PART, WIDE><<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_leaf2(const LeafParams &p, int nacc, bool segmented, int grid, cudaStream_t s) {
+  if (p.n_tiles == 0) return cudaSuccess;
+  if (grid % 2) return cudaErrorInvalidValue;
+  if (nacc == 1)
+    return segmented ? launch_leaf2_t<1, true, false>(p, grid, s) : launch_leaf2_t<1, false, false>(p, grid, s);
+  if (nacc == 3) return launch_leaf2_t<3, true, false>(p, grid, s);
+  if (nacc == 6) return launch_leaf2_t<6, true, true>(p, grid, s);
+  return cudaErrorInvalidValue;
+}
+
+// ============================================================================ tail fixup
+// out(tile) = sum over its K pieces of the residue partials, mod p; same masking as the leaf
+// epilogue (store_chunk).  One thread per (row, 32-column chunk) of a 256 x 256 tile.
+__global__ void __launch_bounds__(256) fixup_kernel(const __grid_constant__ LeafParams P, const FixupTile *tiles) {
+  const FixupTile ft = tiles[blockIdx.y];
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;   // 0 .. 256*8-1
+  const int lr = idx >> 3, c = idx & 7;
+  const LeafProduct &pr = P.prod[ft.q];
+  uint32_t acc[32];
+#pragma unroll
+  for (int e = 0; e < 32; ++e) acc[e] = 0;
+  for (int pc = 0; pc < ft.npieces; ++pc) {
+    const size_t off = (size_t)(ft.slot0 + pc) * 65536 + lr * 256 + c * 32;
+    if (P.fixup32) {
+      const uint4 *src = reinterpret_cast<const uint4 *>(static_cast<const uint32_t *>(P.fixup) + off);
+#pragma unroll
+      for (int i4 = 0; i4 < 8; ++i4) {
+        const uint4 w = src[i4];
+        acc[4 * i4] += w.x; acc[4 * i4 + 1] += w.y; acc[4 * i4 + 2] += w.z; acc[4 * i4 + 3] += w.w;
+      }
+      continue;
+    }
+    const uint4 *src = reinterpret_cast<const uint4 *>(static_cast<const uint16_t *>(P.fixup) + off);
+#pragma unroll
+    for (int i4 = 0; i4 < 4; ++i4) {
+      const uint4 w = src[i4];
+      const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        acc[8 * i4 + 2 * e] += ws[e] & 0xFFFF;
+        acc[8 * i4 + 2 * e + 1] += ws[e] >> 16;
+      }
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < 32; ++e) acc[e] = mod_u32(acc[e], P.mod);   // < npieces * p < 2^32
+  store_chunk(pr, (int64_t)ft.I * 256 + lr, (int64_t)ft.J * 256 + c * 32, acc, P.mod);
+}
+
+cudaError_t launch_fixup(const LeafParams &p, const FixupTile *tiles, int n, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  fixup_kernel<<<dim3(8, n), 256, 0, s>>>(p, tiles);
+  return cudaGetLastError();
+}
+
+}  // namespace adj

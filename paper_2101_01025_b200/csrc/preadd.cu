@@ -1,0 +1,726 @@
+// K1: pre-addition S1=(A21-A11)Y, S2=A22-A21 Y, S3=S1-A22, S4=S3+A12 (mod p)
+// fused with the centered int8 limb split of every leaf operand (Alg. alg:MIAHMM,
+// PAPER.md:303-307); the plain / 2M / quaternion limb splits (depth 0, gemm_modp, 2M's X / Y,
+// 6M's A..W); the GF(p^2) pre-addition of ADJ_HERK_ALG1.
+#include <algorithm>
+#include <cstdio>
+
+#include "kernel_util.cuh"
+
+namespace adj {
+
+// ============================================================================ input loads
+// 4 consecutive logical elements (R, C..C+3) of a view; zero outside the valid region.
+__device__ __forceinline__ void load4(const InView &v, int64_t R, int64_t C, const ModP &m,
+                                      uint32_t (&x)[4]) {
+#pragma unroll
+  for (int e = 0; e < 4; ++e) x[e] = 0;
+  if (R >= v.rows_valid || C >= v.cols_valid) return;
+  const bool all = (C + 3 < v.cols_valid) && v.vec_ok;
+  if (v.type == IN_U32) {
+    const uint32_t *p = static_cast<const uint32_t *>(v.ptr) + R * v.ld + C;
+    if (all) {
+      uint4 q = __ldg(reinterpret_cast<const uint4 *>(p));
+      x[0] = q.x; x[1] = q.y; x[2] = q.z; x[3] = q.w;
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) if (C + e < v.cols_valid) x[e] = __ldg(p + e);
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) x[e] = mod_u32(x[e], m);
+  } else if (v.type == IN_U16) {
+    const uint16_t *p = static_cast<const uint16_t *>(v.ptr) + R * v.ld + C;
+    if (all) {
+      uint2 q = __ldg(reinterpret_cast<const uint2 *>(p));
+      x[0] = q.x & 0xFFFF; x[1] = q.x >> 16; x[2] = q.y & 0xFFFF; x[3] = q.y >> 16;
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) if (C + e < v.cols_valid) x[e] = __ldg(p + e);
+    }
+  } else if (v.type == IN_QUAD_SUM) {
+    const uint32_t *p = static_cast<const uint32_t *>(v.ptr) + 4 * (R * v.ld + C);
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      if (C + e < v.cols_valid) {
+        uint4 q = all ? __ldg(reinterpret_cast<const uint4 *>(p) + e)
+                      : make_uint4(__ldg(p + 4 * e), __ldg(p + 4 * e + 1), __ldg(p + 4 * e + 2), __ldg(p + 4 * e + 3));
+        x[e] = addmod(addmod(mod_u32(q.x, m), mod_u32(q.y, m), m), addmod(mod_u32(q.z, m), mod_u32(q.w, m), m), m);
+      }
+  } else {
+    const uint32_t *p = static_cast<const uint32_t *>(v.ptr) + 2 * (R * v.ld + C);
+    uint32_t re[4] = {0, 0, 0, 0}, im[4] = {0, 0, 0, 0};
+    if (all) {
+      uint4 a = __ldg(reinterpret_cast<const uint4 *>(p));
+      uint4 b = __ldg(reinterpret_cast<const uint4 *>(p) + 1);
+      re[0] = a.x; im[0] = a.y; re[1] = a.z; im[1] = a.w;
+      re[2] = b.x; im[2] = b.y; re[3] = b.z; im[3] = b.w;
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (C + e < v.cols_valid) { re[e] = __ldg(p + 2 * e); im[e] = __ldg(p + 2 * e + 1); }
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      uint32_t a = mod_u32(re[e], m), b = mod_u32(im[e], m);
+      x[e] = v.type == IN_PAIR_SUM ? addmod(a, b, m) : (v.type == IN_PAIR_RE ? a : b);
+    }
+  }
+}
+
+// ============================================================================ K1 pre-addition
+// Scheme-specialised limb split of 4 residues into packed int8 plane words (one u32 per plane).
+template <int SCHEME>
+__device__ __forceinline__ void limbs4(const uint32_t (&x)[4], const ModP &m, uint32_t (&w)[3]) {
+  int32_t c[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) c[e] = centered(x[e], m);
+  if constexpr (SCHEME == 0) {
+    w[0] = __byte_perm(__byte_perm(c[0], c[1], 0x40), __byte_perm(c[2], c[3], 0x40), 0x5410);
+  } else if constexpr (SCHEME == 1) {
+    int32_t hi[4], lo[4], mid[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      hi[e] = (c[e] + 64) >> 7;
+      lo[e] = c[e] - (hi[e] << 7);
+      mid[e] = hi[e] + lo[e];
+    }
+    w[0] = __byte_perm(__byte_perm(hi[0], hi[1], 0x40), __byte_perm(hi[2], hi[3], 0x40), 0x5410);
+    w[1] = __byte_perm(__byte_perm(lo[0], lo[1], 0x40), __byte_perm(lo[2], lo[3], 0x40), 0x5410);
+    w[2] = __byte_perm(__byte_perm(mid[0], mid[1], 0x40), __byte_perm(mid[2], mid[3], 0x40), 0x5410);
+  } else {
+    int32_t hi[4], lo[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      hi[e] = c[e] >> 8;
+      lo[e] = c[e] - (hi[e] << 8);
+    }
+    w[0] = __byte_perm(__byte_perm(hi[0], hi[1], 0x40), __byte_perm(hi[2], hi[3], 0x40), 0x5410);
+    w[1] = __byte_perm(__byte_perm(lo[0], lo[1], 0x40), __byte_perm(lo[2], lo[3], 0x40), 0x5410);
+  }
+}
+
+// K7 limbs of 4 already-centered values c in [-(p-1)/2, (p-1)/2]
+__device__ __forceinline__ void put_limbs4_k7c(int8_t *base, int64_t plane_stride, const int32_t (&c)[4]) {
+  int32_t hi[4], lo[4], mid[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    hi[e] = (c[e] + 64) >> 7;
+    lo[e] = c[e] - (hi[e] << 7);
+    mid[e] = hi[e] + lo[e];
+  }
+  *reinterpret_cast<uint32_t *>(base) =
+      __byte_perm(__byte_perm(hi[0], hi[1], 0x40), __byte_perm(hi[2], hi[3], 0x40), 0x5410);
+  *reinterpret_cast<uint32_t *>(base + plane_stride) =
+      __byte_perm(__byte_perm(lo[0], lo[1], 0x40), __byte_perm(lo[2], lo[3], 0x40), 0x5410);
+  *reinterpret_cast<uint32_t *>(base + 2 * plane_stride) =
+      __byte_perm(__byte_perm(mid[0], mid[1], 0x40), __byte_perm(mid[2], mid[3], 0x40), 0x5410);
+}
+
+// centered residue of a signed v with |v| < 2^30, 257 <= p <= 16763: float quotient estimate
+// (error < 0.2) then one fix in each direction
+__device__ __forceinline__ int32_t center_lazy(int32_t v, float invp, int32_t p, int32_t h) {
+  const int32_t q = __float2int_rn(__int2float_rn(v) * invp);
+  int32_t r = v - q * p;
+  r = r > h ? r - p : r;
+  r = r < -h ? r + p : r;
+  return r;
+}
+
+// wide scheme: three balanced base-64 digits d2, d1, d0 in [-32, 32] of the centered residue
+// and the pair sums d2+d1, d1+d0, d2+d0 (6 s8 planes, 3-way Karatsuba)
+__device__ __forceinline__ void put_limbs4_t6(int8_t *base, int64_t plane_stride, const uint32_t (&x)[4],
+                                              const ModP &m) {
+  int32_t d[6][4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const int32_t c = centered(x[e], m);
+    const int32_t d0 = ((c + 32) & 63) - 32;
+    const int32_t c1 = (c - d0) >> 6;
+    const int32_t d1 = ((c1 + 32) & 63) - 32;
+    const int32_t d2 = (c1 - d1) >> 6;
+    d[0][e] = d2; d[1][e] = d1; d[2][e] = d0;
+    d[3][e] = d2 + d1; d[4][e] = d1 + d0; d[5][e] = d2 + d0;
+  }
+#pragma unroll
+  for (int pl = 0; pl < 6; ++pl)
+    *reinterpret_cast<uint32_t *>(base + pl * plane_stride) =
+        __byte_perm(__byte_perm(d[pl][0], d[pl][1], 0x40), __byte_perm(d[pl][2], d[pl][3], 0x40), 0x5410);
+}
+
+template <int SCHEME>
+__device__ __forceinline__ void put_limbs4(int8_t *base, int64_t plane_stride, const uint32_t (&x)[4],
+                                           const ModP &m) {
+  if constexpr (SCHEME == 3) {
+    put_limbs4_t6(base, plane_stride, x, m);
+    return;
+  }
+  constexpr int NP = SCHEME == 0 ? 1 : (SCHEME == 1 ? 3 : 2);
+  uint32_t w[3];
+  limbs4<SCHEME>(x, m, w);
+#pragma unroll
+  for (int pl = 0; pl < NP; ++pl) *reinterpret_cast<uint32_t *>(base + pl * plane_stride) = w[pl];
+}
+
+// limb planes of 8 consecutive residues (two 4-groups), one 8-byte store per plane
+template <int SCHEME>
+__device__ __forceinline__ void put_limbs8(int8_t *base, int64_t plane_stride, const uint32_t (&x0)[4],
+                                           const uint32_t (&x1)[4], const ModP &m) {
+  if constexpr (SCHEME == 3) {
+    put_limbs4_t6(base, plane_stride, x0, m);
+    put_limbs4_t6(base + 4, plane_stride, x1, m);
+    return;
+  }
+  constexpr int NP = SCHEME == 0 ? 1 : (SCHEME == 1 ? 3 : 2);
+  uint32_t w0[3], w1[3];
+  limbs4<SCHEME>(x0, m, w0);
+  limbs4<SCHEME>(x1, m, w1);
+#pragma unroll
+  for (int pl = 0; pl < NP; ++pl) *reinterpret_cast<uint2 *>(base + pl * plane_stride) = make_uint2(w0[pl], w1[pl]);
+}
+
+// limb planes of 16 consecutive residues (four 4-groups), one 16-byte store per plane
+template <int SCHEME>
+__device__ __forceinline__ void put_limbs16(int8_t *base, int64_t plane_stride, const uint32_t (&x)[4][4],
+                                            const ModP &m) {
+  if constexpr (SCHEME == 3) {
+#pragma unroll
+    for (int g = 0; g < 4; ++g) put_limbs4_t6(base + 4 * g, plane_stride, x[g], m);
+    return;
+  }
+  constexpr int NP = SCHEME == 0 ? 1 : (SCHEME == 1 ? 3 : 2);
+  uint32_t w[4][3];
+#pragma unroll
+  for (int g = 0; g < 4; ++g) limbs4<SCHEME>(x[g], m, w[g]);
+#pragma unroll
+  for (int pl = 0; pl < NP; ++pl)
+    *reinterpret_cast<uint4 *>(base + pl * plane_stride) = make_uint4(w[0][pl], w[1][pl], w[2][pl], w[3][pl]);
+}
+
+template <int YK, bool WIDE = false>
+__device__ __forceinline__ void apply_Y4(const uint32_t (&a)[4], const uint32_t (&b)[4], uint32_t (&oa)[4],
+                                         uint32_t (&ob)[4], uint32_t ya, uint32_t yb, const ModP &m) {
+  if constexpr (WIDE) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      if constexpr (YK == 0) {
+        oa[e] = mulmod_w(ya, a[e], m);
+        ob[e] = mulmod_w(ya, b[e], m);
+      } else {
+        oa[e] = submod(mulmod_w(ya, a[e], m), mulmod_w(yb, b[e], m), m);
+        ob[e] = addmod(mulmod_w(yb, a[e], m), mulmod_w(ya, b[e], m), m);
+      }
+    }
+    return;
+  }
+  // X Y on the column pair (c, c + kh/2): Y = i I -> (i a, i b);
+  // Y = [[ya, yb], [-yb, ya]] (x) I -> [X1 X2] Y = [ya X1 - yb X2, yb X1 + ya X2]
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    if constexpr (YK == 0) {
+      oa[e] = mulmod(ya, a[e], m);
+      ob[e] = mulmod(ya, b[e], m);
+    } else {
+      oa[e] = submod(mulmod(ya, a[e], m), mulmod(yb, b[e], m), m);
+      ob[e] = addmod(mulmod(yb, a[e], m), mulmod(ya, b[e], m), m);
+    }
+  }
+}
+
+// fast 4-element load of a fully valid, vector-aligned position (type known by the caller)
+template <int T>
+__device__ __forceinline__ void load4_fast(const void *ptr, int64_t off, const ModP &m, uint32_t (&x)[4]) {
+  if constexpr (T == IN_U32) {
+    uint4 q = __ldg(reinterpret_cast<const uint4 *>(static_cast<const uint32_t *>(ptr) + off));
+    x[0] = mod_u32(q.x, m); x[1] = mod_u32(q.y, m); x[2] = mod_u32(q.z, m); x[3] = mod_u32(q.w, m);
+  } else if constexpr (T == IN_U16) {
+    uint2 q = __ldg(reinterpret_cast<const uint2 *>(static_cast<const uint16_t *>(ptr) + off));
+    x[0] = q.x & 0xFFFF; x[1] = q.x >> 16; x[2] = q.y & 0xFFFF; x[3] = q.y >> 16;
+  } else if constexpr (T == IN_QUAD_SUM) {
+    const uint4 *p = reinterpret_cast<const uint4 *>(static_cast<const uint32_t *>(ptr) + 4 * off);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const uint4 q = __ldg(p + e);
+      x[e] = addmod(addmod(mod_u32(q.x, m), mod_u32(q.y, m), m), addmod(mod_u32(q.z, m), mod_u32(q.w, m), m), m);
+    }
+  } else {
+    const uint4 *p = reinterpret_cast<const uint4 *>(static_cast<const uint32_t *>(ptr) + 2 * off);
+    uint4 a = __ldg(p), b = __ldg(p + 1);
+    x[0] = addmod(mod_u32(a.x, m), mod_u32(a.y, m), m);
+    x[1] = addmod(mod_u32(a.z, m), mod_u32(a.w, m), m);
+    x[2] = addmod(mod_u32(b.x, m), mod_u32(b.y, m), m);
+    x[3] = addmod(mod_u32(b.z, m), mod_u32(b.w, m), m);
+  }
+}
+
+// re / im of 4 consecutive GF(p^2) elements (interleaved pairs), reduced mod p
+__device__ __forceinline__ void load4_pair(const InView &v, int64_t R, int64_t C, bool fast, const ModP &m,
+                                           uint32_t (&re)[4], uint32_t (&im)[4]) {
+  if (fast) {
+    const uint4 *p = reinterpret_cast<const uint4 *>(static_cast<const uint32_t *>(v.ptr) + 2 * (R * v.ld + C));
+    uint4 a = __ldg(p), b = __ldg(p + 1);
+    re[0] = mod_u32(a.x, m); im[0] = mod_u32(a.y, m); re[1] = mod_u32(a.z, m); im[1] = mod_u32(a.w, m);
+    re[2] = mod_u32(b.x, m); im[2] = mod_u32(b.y, m); re[3] = mod_u32(b.z, m); im[3] = mod_u32(b.w, m);
+  } else {
+    InView vr = v, vi = v;
+    vr.type = IN_PAIR_RE;
+    vi.type = IN_PAIR_IM;
+    load4(vr, R, C, m, re);
+    load4(vi, R, C, m, im);
+  }
+}
+
+template <int SCHEME>
+__device__ __forceinline__ void put_side(const PreNode &N, int64_t R, int64_t C, const uint32_t (&re)[4],
+                                         const uint32_t (&im)[4], const ModP &m) {
+  const int64_t ps = N.side_rows_pad * N.side_kpad;
+  put_limbs4<SCHEME>(N.side + (N.side_x_row + R) * N.side_kpad + C, ps, re, m);
+  put_limbs4<SCHEME>(N.side + (N.side_y_row + R) * N.side_kpad + C, ps, im, m);
+}
+
+template <int SCHEME, int YK, int T>
+__device__ __forceinline__ void preadd_row(const PreParams &P, const PreNode &N, int64_t r, int64_t c) {
+  const ModP &m = P.mod;
+  const int64_t h2 = P.kh / 2;
+  const InView &v = N.in;
+  uint32_t x11a[4], x11b[4], x12a[4], x12b[4], x21a[4], x21b[4], x22a[4], x22b[4];
+  const bool top_ok = r < P.mh && r < v.rows_valid;
+  const bool bot_ok = r < P.mh && P.mh + r < v.rows_valid;
+  const bool fast = v.vec_ok && top_ok && bot_ok && P.kh + c + h2 + 3 < v.cols_valid;
+  if (T == IN_PAIR_SUM && N.side != nullptr) {
+    // 2M root: T = Re(A) + Im(A) for the pre-addition, and the limb planes of Re(A), Im(A) for H
+    InView vv = v;
+    if (r >= P.mh) vv.rows_valid = 0;
+    const int64_t R[2] = {r, P.mh + r};
+    const int64_t Cc[4] = {c, c + h2, P.kh + c, P.kh + c + h2};
+    uint32_t(*dst[2][4])[4] = {{&x11a, &x11b, &x12a, &x12b}, {&x21a, &x21b, &x22a, &x22b}};
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        uint32_t re[4], im[4];
+        load4_pair(vv, R[a], Cc[b], fast, m, re, im);
+        if (r < P.mh) put_side<SCHEME>(N, R[a], Cc[b], re, im, m);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) (*dst[a][b])[e] = addmod(re[e], im[e], m);
+      }
+  } else if (fast && T == IN_U32) {
+    // all 32 loads first; one check that they are canonical (the usual case) skips the 32
+    // Barrett reductions, non-canonical input takes the reducing path (inputs are read mod p)
+    const uint32_t *src = static_cast<const uint32_t *>(v.ptr);
+    const int64_t o1 = r * v.ld, o2 = (P.mh + r) * v.ld;
+    const int64_t offs[8] = {o1 + c, o1 + c + h2, o1 + P.kh + c, o1 + P.kh + c + h2,
+                             o2 + c, o2 + c + h2, o2 + P.kh + c, o2 + P.kh + c + h2};
+    uint32_t(*dst[8])[4] = {&x11a, &x11b, &x12a, &x12b, &x21a, &x21b, &x22a, &x22b};
+    uint4 q[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) q[i] = __ldg(reinterpret_cast<const uint4 *>(src + offs[i]));
+    uint32_t mx = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) mx = max(mx, max(max(q[i].x, q[i].y), max(q[i].z, q[i].w)));
+    if (mx < m.p) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        (*dst[i])[0] = q[i].x; (*dst[i])[1] = q[i].y; (*dst[i])[2] = q[i].z; (*dst[i])[3] = q[i].w;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        (*dst[i])[0] = mod_u32(q[i].x, m); (*dst[i])[1] = mod_u32(q[i].y, m);
+        (*dst[i])[2] = mod_u32(q[i].z, m); (*dst[i])[3] = mod_u32(q[i].w, m);
+      }
+    }
+  } else if (fast) {
+    const int64_t o1 = r * v.ld, o2 = (P.mh + r) * v.ld;
+    load4_fast<T>(v.ptr, o1 + c, m, x11a);
+    load4_fast<T>(v.ptr, o1 + c + h2, m, x11b);
+    load4_fast<T>(v.ptr, o1 + P.kh + c, m, x12a);
+    load4_fast<T>(v.ptr, o1 + P.kh + c + h2, m, x12b);
+    load4_fast<T>(v.ptr, o2 + c, m, x21a);
+    load4_fast<T>(v.ptr, o2 + c + h2, m, x21b);
+    load4_fast<T>(v.ptr, o2 + P.kh + c, m, x22a);
+    load4_fast<T>(v.ptr, o2 + P.kh + c + h2, m, x22b);
+  } else {
+    InView vv = v;
+    if (r >= P.mh) vv.rows_valid = 0;             // rows of the zero padding up to rows_pad
+    load4(vv, r, c, m, x11a);
+    load4(vv, r, c + h2, m, x11b);
+    load4(vv, r, P.kh + c, m, x12a);
+    load4(vv, r, P.kh + c + h2, m, x12b);
+    load4(vv, P.mh + r, c, m, x21a);
+    load4(vv, P.mh + r, c + h2, m, x21b);
+    load4(vv, P.mh + r, P.kh + c, m, x22a);
+    load4(vv, P.mh + r, P.kh + c + h2, m, x22b);
+  }
+  if constexpr (SCHEME == 1) {
+    // Lazy reduction (p <= 16763 so 2 p^2 < 2^31): Y products in raw int32, one centered
+    // reduction per S output; X outputs and S3/S4 need one conditional correction each.
+    const int32_t p = (int32_t)m.p, h = (int32_t)m.half;
+    const float invp = 1.0f / (float)m.p;
+    const int32_t ya = (int32_t)P.ya, yb = (int32_t)P.yb;
+    int32_t c1a[4], c1b[4], c2a[4], c2b[4], c3a[4], c3b[4], c4a[4], c4b[4];
+    int32_t c11a[4], c11b[4], c12a[4], c12b[4], c22a[4], c22b[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int32_t d1 = (int32_t)x21a[e] - (int32_t)x11a[e], d2 = (int32_t)x21b[e] - (int32_t)x11b[e];
+      int32_t s1r_a, s1r_b, tr_a, tr_b;
+      if constexpr (YK == 0) {
+        s1r_a = ya * d1; s1r_b = ya * d2;
+        tr_a = ya * (int32_t)x21a[e]; tr_b = ya * (int32_t)x21b[e];
+      } else {
+        s1r_a = ya * d1 - yb * d2; s1r_b = yb * d1 + ya * d2;                         // (A21 - A11) Y
+        tr_a = ya * (int32_t)x21a[e] - yb * (int32_t)x21b[e];                          // A21 Y
+        tr_b = yb * (int32_t)x21a[e] + ya * (int32_t)x21b[e];
+      }
+      c1a[e] = center_lazy(s1r_a, invp, p, h); c1b[e] = center_lazy(s1r_b, invp, p, h);               // S1
+      c2a[e] = center_lazy((int32_t)x22a[e] - tr_a, invp, p, h);                                        // S2
+      c2b[e] = center_lazy((int32_t)x22b[e] - tr_b, invp, p, h);
+      c3a[e] = c1a[e] - (int32_t)x22a[e]; c3a[e] = c3a[e] < -h ? c3a[e] + p : c3a[e];                 // S3
+      c3b[e] = c1b[e] - (int32_t)x22b[e]; c3b[e] = c3b[e] < -h ? c3b[e] + p : c3b[e];
+      c4a[e] = c3a[e] + (int32_t)x12a[e]; c4a[e] = c4a[e] > h ? c4a[e] - p : c4a[e];                  // S4
+      c4b[e] = c3b[e] + (int32_t)x12b[e]; c4b[e] = c4b[e] > h ? c4b[e] - p : c4b[e];
+      c11a[e] = (int32_t)x11a[e] > h ? (int32_t)x11a[e] - p : (int32_t)x11a[e];
+      c11b[e] = (int32_t)x11b[e] > h ? (int32_t)x11b[e] - p : (int32_t)x11b[e];
+      c12a[e] = (int32_t)x12a[e] > h ? (int32_t)x12a[e] - p : (int32_t)x12a[e];
+      c12b[e] = (int32_t)x12b[e] > h ? (int32_t)x12b[e] - p : (int32_t)x12b[e];
+      c22a[e] = (int32_t)x22a[e] > h ? (int32_t)x22a[e] - p : (int32_t)x22a[e];
+      c22b[e] = (int32_t)x22b[e] > h ? (int32_t)x22b[e] - p : (int32_t)x22b[e];
+    }
+    const int64_t ps = P.rows_pad * P.kpad;
+#define PUTC(o, A, B)                                                                  \
+  if (N.op_row[o] >= 0) {                                                              \
+    int8_t *b = P.arena + (N.op_row[o] + r) * P.kpad;                                  \
+    put_limbs4_k7c(b + c, ps, A);                                                      \
+    put_limbs4_k7c(b + c + h2, ps, B);                                                 \
+  }
+    PUTC(OUT_S1, c1a, c1b)
+    PUTC(OUT_S2, c2a, c2b)
+    PUTC(OUT_S4, c4a, c4b)
+    PUTC(OUT_X22, c22a, c22b)
+    PUTC(OUT_X11, c11a, c11b)
+    PUTC(OUT_X12, c12a, c12b)
+    PUTC(OUT_S3, c3a, c3b)
+#undef PUTC
+    if (N.s3 != nullptr && r < P.mh) {
+      uint16_t *d = static_cast<uint16_t *>(N.s3) + r * N.s3_ld;
+      uint32_t u[8];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        u[e] = (uint32_t)(c3a[e] < 0 ? c3a[e] + p : c3a[e]);
+        u[4 + e] = (uint32_t)(c3b[e] < 0 ? c3b[e] + p : c3b[e]);
+      }
+      *reinterpret_cast<uint2 *>(d + c) = make_uint2(u[0] | (u[1] << 16), u[2] | (u[3] << 16));
+      *reinterpret_cast<uint2 *>(d + c + h2) = make_uint2(u[4] | (u[5] << 16), u[6] | (u[7] << 16));
+    }
+    return;
+  }
+  uint32_t da[4], db[4], s1a[4], s1b[4], ta[4], tb[4], s2a[4], s2b[4], s3a[4], s3b[4], s4a[4], s4b[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) { da[e] = submod(x21a[e], x11a[e], m); db[e] = submod(x21b[e], x11b[e], m); }
+  apply_Y4<YK, SCHEME == 3>(da, db, s1a, s1b, P.ya, P.yb, m);   // S1 = (A21 - A11) Y
+  apply_Y4<YK, SCHEME == 3>(x21a, x21b, ta, tb, P.ya, P.yb, m); // A21 Y
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    s2a[e] = submod(x22a[e], ta[e], m); s2b[e] = submod(x22b[e], tb[e], m);   // S2 = A22 - A21 Y
+    s3a[e] = submod(s1a[e], x22a[e], m); s3b[e] = submod(s1b[e], x22b[e], m); // S3 = S1 - A22
+    s4a[e] = addmod(s3a[e], x12a[e], m); s4b[e] = addmod(s3b[e], x12b[e], m); // S4 = S3 + A12
+  }
+  const int64_t ps = P.rows_pad * P.kpad;
+#define PUT(o, A, B)                                                                   \
+  if (N.op_row[o] >= 0) {                                                              \
+    int8_t *b = P.arena + (N.op_row[o] + r) * P.kpad;                                  \
+    put_limbs4<SCHEME>(b + c, ps, A, m);                                               \
+    put_limbs4<SCHEME>(b + c + h2, ps, B, m);                                          \
+  }
+  PUT(OUT_S1, s1a, s1b)
+  PUT(OUT_S2, s2a, s2b)
+  PUT(OUT_S4, s4a, s4b)
+  PUT(OUT_X22, x22a, x22b)
+  PUT(OUT_X11, x11a, x11b)
+  PUT(OUT_X12, x12a, x12b)
+  PUT(OUT_S3, s3a, s3b)
+#undef PUT
+  if (N.s3 != nullptr && r < P.mh && P.res32) {
+    uint32_t *d = static_cast<uint32_t *>(N.s3) + r * N.s3_ld;
+    *reinterpret_cast<uint4 *>(d + c) = make_uint4(s3a[0], s3a[1], s3a[2], s3a[3]);
+    *reinterpret_cast<uint4 *>(d + c + h2) = make_uint4(s3b[0], s3b[1], s3b[2], s3b[3]);
+  } else if (N.s3 != nullptr && r < P.mh) {
+    uint16_t *d = static_cast<uint16_t *>(N.s3) + r * N.s3_ld;
+    uint2 va, vb;
+    va.x = s3a[0] | (s3a[1] << 16); va.y = s3a[2] | (s3a[3] << 16);
+    vb.x = s3b[0] | (s3b[1] << 16); vb.y = s3b[2] | (s3b[3] << 16);
+    *reinterpret_cast<uint2 *>(d + c) = va;
+    *reinterpret_cast<uint2 *>(d + c + h2) = vb;
+  }
+}
+
+template <int SCHEME, int YK>
+__global__ void __launch_bounds__(256) preadd_kernel(const __grid_constant__ PreParams P) {
+  constexpr int NP = SCHEME == 0 ? 1 : (SCHEME == 1 ? 3 : (SCHEME == 2 ? 2 : 6));
+  const PreNode &N = P.nodes[blockIdx.z];
+  const int64_t g_main = P.kh / 8;               // 4-column groups of the first half
+  const int64_t g_pad = (P.kpad - P.kh) / 4;     // zero padding columns [kh, kpad)
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= g_main + g_pad) return;
+  const int type = N.in.type;
+  for (int64_t r = blockIdx.y; r < P.rows_pad; r += gridDim.y) {
+    if (g >= g_main) {
+      const int64_t col = P.kh + (g - g_main) * 4;
+#pragma unroll
+      for (int o = 0; o < OUT_N; ++o)
+        if (N.op_row[o] >= 0)
+#pragma unroll
+          for (int pl = 0; pl < NP; ++pl)
+            *reinterpret_cast<uint32_t *>(P.arena + (N.op_row[o] + r + pl * P.rows_pad) * P.kpad + col) = 0u;
+      continue;
+    }
+    const int64_t c = g * 4;
+    if (type == IN_U32) preadd_row<SCHEME, YK, IN_U32>(P, N, r, c);
+    else if (type == IN_U16) preadd_row<SCHEME, YK, IN_U16>(P, N, r, c);
+    else if (type == IN_QUAD_SUM) preadd_row<SCHEME, YK, IN_QUAD_SUM>(P, N, r, c);
+    else preadd_row<SCHEME, YK, IN_PAIR_SUM>(P, N, r, c);
+  }
+}
+
+cudaError_t launch_preadd(const PreParams &p, cudaStream_t s) {
+  if (p.n_nodes == 0) return cudaSuccess;
+  const int64_t groups = p.kh / 8 + (p.kpad - p.kh) / 4;
+  dim3 block(256);
+  dim3 grid((unsigned)((groups + 255) / 256), (unsigned)(p.rows_pad < 65535 ? p.rows_pad : 65535),
+            (unsigned)p.n_nodes);
+#define PRE(S, Y) preadd_kernel<S, Y><<<grid, block, 0, s>>>(p)
+  if (p.scheme == 0) { if (p.ykind == 0) PRE(0, 0); else PRE(0, 1); }
+  else if (p.scheme == 1) { if (p.ykind == 0) PRE(1, 0); else PRE(1, 1); }
+  else if (p.scheme == 2) { if (p.ykind == 0) PRE(2, 0); else PRE(2, 1); }
+  else { if (p.ykind == 0) PRE(3, 0); else PRE(3, 1); }
+#undef PRE
+  return cudaGetLastError();
+}
+
+// ============================================================================ plain split
+// One thread per (row, 8 columns): both 4-column groups are loaded before any limb store so
+// that each thread keeps 32-64 bytes of loads in flight.
+template <int SCHEME>
+__global__ void __launch_bounds__(256) split_kernel(const __grid_constant__ SplitParams P) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= P.kpad / 8) return;
+  const int64_t c0 = g * 8;
+  const int64_t ps = P.rows_pad * P.kpad;
+  const InView &v = P.in;
+  for (int64_t r = blockIdx.y; r < P.rows_pad; r += gridDim.y) {
+    InView vv = v;
+    if (r >= P.rows) vv.rows_valid = 0;
+    const bool fast = vv.vec_ok && r < vv.rows_valid && c0 + 7 < vv.cols_valid && c0 + 7 < P.cols;
+    if (P.mode == 2) {
+      // quaternion M = A + B i + C j + D k: the operands of Alg. alg:2M3M
+      // A, B, C, D, U1 = A + B, U2 = C + D and (depth 0) W = U1 + U2, from one read of M
+      uint32_t q[2][4][4];   // [half][component][element]
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t c = c0 + 4 * h;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          uint4 w4 = make_uint4(0u, 0u, 0u, 0u);
+          if (r < vv.rows_valid && c + e < vv.cols_valid && c + e < P.cols) {
+            const uint32_t *src = static_cast<const uint32_t *>(v.ptr) + 4 * (r * v.ld + c + e);
+            w4 = vv.vec_ok ? __ldg(reinterpret_cast<const uint4 *>(src))
+                           : make_uint4(__ldg(src), __ldg(src + 1), __ldg(src + 2), __ldg(src + 3));
+          }
+          q[h][0][e] = mod_u32(w4.x, P.mod); q[h][1][e] = mod_u32(w4.y, P.mod);
+          q[h][2][e] = mod_u32(w4.z, P.mod); q[h][3][e] = mod_u32(w4.w, P.mod);
+        }
+      }
+#pragma unroll
+      for (int o = 0; o < 4; ++o)
+        put_limbs8<SCHEME>(P.arena + (P.qrow[o] + r) * P.kpad + c0, ps, q[0][o], q[1][o], P.mod);
+      uint32_t u1[2][4], u2[2][4];
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          u1[h][e] = addmod(q[h][0][e], q[h][1][e], P.mod);
+          u2[h][e] = addmod(q[h][2][e], q[h][3][e], P.mod);
+        }
+      put_limbs8<SCHEME>(P.arena + (P.qrow[4] + r) * P.kpad + c0, ps, u1[0], u1[1], P.mod);
+      put_limbs8<SCHEME>(P.arena + (P.qrow[5] + r) * P.kpad + c0, ps, u2[0], u2[1], P.mod);
+      if (P.qrow[6] >= 0) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) u1[h][e] = addmod(u1[h][e], u2[h][e], P.mod);
+        put_limbs8<SCHEME>(P.arena + (P.qrow[6] + r) * P.kpad + c0, ps, u1[0], u1[1], P.mod);
+      }
+      continue;
+    }
+    if (P.mode == 1) {
+      // 2M at depth 0: one read of the interleaved A gives X = Re, Y = Im and T = X + Y
+      uint32_t re[2][4], im[2][4];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        InView vh = vv;
+        if (c0 + 4 * h >= P.cols) vh.cols_valid = 0;
+        load4_pair(vh, r, c0 + 4 * h, fast, P.mod, re[h], im[h]);
+      }
+      uint32_t x[2][4];
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) x[h][e] = addmod(re[h][e], im[h][e], P.mod);
+      put_limbs8<SCHEME>(P.arena + (P.op_row + r) * P.kpad + c0, ps, re[0], re[1], P.mod);
+      put_limbs8<SCHEME>(P.arena + (P.op_row2 + r) * P.kpad + c0, ps, im[0], im[1], P.mod);
+      put_limbs8<SCHEME>(P.arena + (P.op_row3 + r) * P.kpad + c0, ps, x[0], x[1], P.mod);
+      continue;
+    }
+    uint32_t x[2][4];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t c = c0 + 4 * h;
+      if (fast && v.type == IN_U32) {
+        load4_fast<IN_U32>(v.ptr, r * v.ld + c, P.mod, x[h]);
+      } else {
+        InView vh = vv;
+        if (c >= P.cols) vh.cols_valid = 0;
+        load4(vh, r, c, P.mod, x[h]);
+      }
+    }
+    put_limbs8<SCHEME>(P.arena + (P.op_row + r) * P.kpad + c0, ps, x[0], x[1], P.mod);
+  }
+}
+
+// Plain split (mode 0): one thread per (row, 16 columns), four 16-byte loads in flight before
+// the 16-byte limb-plane stores.
+template <int SCHEME>
+__global__ void __launch_bounds__(256) split_plain_kernel(const __grid_constant__ SplitParams P) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= P.kpad / 16) return;
+  const int64_t c0 = g * 16;
+  const int64_t ps = P.rows_pad * P.kpad;
+  const InView &v = P.in;
+  for (int64_t r = blockIdx.y; r < P.rows_pad; r += gridDim.y) {
+    InView vv = v;
+    if (r >= P.rows) vv.rows_valid = 0;
+    const bool fast = vv.vec_ok && vv.type == IN_U32 && r < vv.rows_valid && c0 + 15 < vv.cols_valid && c0 + 15 < P.cols;
+    uint32_t x[4][4];
+    if (fast) {
+      uint4 q[4];
+#pragma unroll
+      for (int h = 0; h < 4; ++h)
+        q[h] = __ldg(reinterpret_cast<const uint4 *>(static_cast<const uint32_t *>(v.ptr) + r * v.ld + c0 + 4 * h));
+      uint32_t mx = 0;
+#pragma unroll
+      for (int h = 0; h < 4; ++h) mx = max(mx, max(max(q[h].x, q[h].y), max(q[h].z, q[h].w)));
+      if (mx < P.mod.p) {   // canonical input (the usual case) needs no reduction
+#pragma unroll
+        for (int h = 0; h < 4; ++h) { x[h][0] = q[h].x; x[h][1] = q[h].y; x[h][2] = q[h].z; x[h][3] = q[h].w; }
+      } else {
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          x[h][0] = mod_u32(q[h].x, P.mod); x[h][1] = mod_u32(q[h].y, P.mod);
+          x[h][2] = mod_u32(q[h].z, P.mod); x[h][3] = mod_u32(q[h].w, P.mod);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        InView vh = vv;
+        if (c0 + 4 * h >= P.cols) vh.cols_valid = 0;
+        load4(vh, r, c0 + 4 * h, P.mod, x[h]);
+      }
+    }
+    put_limbs16<SCHEME>(P.arena + (P.op_row + r) * P.kpad + c0, ps, x, P.mod);
+  }
+}
+
+cudaError_t launch_split(const SplitParams &p, cudaStream_t s) {
+  if (p.mode == 0) {
+    dim3 g16((unsigned)((p.kpad / 16 + 255) / 256), (unsigned)(p.rows_pad < 65535 ? p.rows_pad : 65535));
+    if (p.scheme == 0) split_plain_kernel<0><<<g16, 256, 0, s>>>(p);
+    else if (p.scheme == 1) split_plain_kernel<1><<<g16, 256, 0, s>>>(p);
+    else if (p.scheme == 2) split_plain_kernel<2><<<g16, 256, 0, s>>>(p);
+    else split_plain_kernel<3><<<g16, 256, 0, s>>>(p);
+    return cudaGetLastError();
+  }
+  dim3 grid((unsigned)((p.kpad / 8 + 255) / 256), (unsigned)(p.rows_pad < 65535 ? p.rows_pad : 65535));
+  if (p.scheme == 0) split_kernel<0><<<grid, 256, 0, s>>>(p);
+  else if (p.scheme == 1) split_kernel<1><<<grid, 256, 0, s>>>(p);
+  else if (p.scheme == 2) split_kernel<2><<<grid, 256, 0, s>>>(p);
+  else split_kernel<3><<<grid, 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+
+// ============================================================================ GF(p^2) Alg. 1 (PLAN_HERK1)
+// K1 over GF(p^2) with the scalar skew-unitary Y = y I, y = ya + i yb, y conj(y) = -1
+// (PAPER.md:750-758): S1 = y (A21 - A11), S2 = A22 - y A21, S3 = S1 - A22, S4 = S3 + A12
+// (Alg. alg:MIAHMM), then the 21 real limb operands of the leaves:
+//   2M for P1, P2, P5 (T = re + im, X = re, Y = im of A11, A12, S3),
+//   3M for P3 = A22 S4^H and P4 = S1 S2^H (re, im and re + im of the left factor, re, im and
+//   re - im of the right factor).
+// One thread per (row, 4 consecutive columns) of the (mh x kh) quadrants.
+template <int SCHEME>
+__global__ void __launch_bounds__(256) herk_preadd_kernel(const __grid_constant__ HerkPreParams P) {
+  constexpr int NP = SCHEME == 0 ? 1 : (SCHEME == 1 ? 3 : (SCHEME == 2 ? 2 : 6));
+  constexpr bool WIDE = SCHEME == 3;
+  const int64_t g_main = P.kh / 4;
+  const int64_t g_pad = (P.kpad - P.kh) / 4;
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= g_main + g_pad) return;
+  const ModP &m = P.mod;
+  const int64_t ps = P.rows_pad * P.kpad;
+  auto out = [&](int o, int64_t r, int64_t c) { return P.arena + ((int64_t)o * P.planes * P.rows_pad + r) * P.kpad + c; };
+  for (int64_t r = blockIdx.y; r < P.rows_pad; r += gridDim.y) {
+    if (g >= g_main) {
+      const int64_t col = P.kh + (g - g_main) * 4;
+#pragma unroll 1
+      for (int o = 0; o < HO_N; ++o)
+#pragma unroll
+        for (int pl = 0; pl < NP; ++pl) *reinterpret_cast<uint32_t *>(out(o, r, col) + pl * ps) = 0u;
+      continue;
+    }
+    const int64_t c = g * 4;
+    InView v = P.in;
+    if (r >= P.mh) v.rows_valid = 0;    // zero padding rows [mh, rows_pad)
+    const bool fast = v.vec_ok && r < P.mh && P.mh + r < v.rows_valid && P.kh + c + 3 < v.cols_valid;
+    uint32_t a11r[4], a11i[4], a12r[4], a12i[4], a21r[4], a21i[4], a22r[4], a22i[4];
+    load4_pair(v, r, c, fast, m, a11r, a11i);
+    load4_pair(v, r, P.kh + c, fast, m, a12r, a12i);
+    load4_pair(v, P.mh + r, c, fast, m, a21r, a21i);
+    load4_pair(v, P.mh + r, P.kh + c, fast, m, a22r, a22i);
+    uint32_t dr[4], di[4], s1r[4], s1i[4], tr[4], ti[4], s2r[4], s2i[4], s3r[4], s3i[4], s4r[4], s4i[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) { dr[e] = submod(a21r[e], a11r[e], m); di[e] = submod(a21i[e], a11i[e], m); }
+    apply_Y4<1, WIDE>(dr, di, s1r, s1i, P.ya, P.yb, m);        // S1 = y (A21 - A11)
+    apply_Y4<1, WIDE>(a21r, a21i, tr, ti, P.ya, P.yb, m);      // y A21
+    uint32_t w[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      s2r[e] = submod(a22r[e], tr[e], m); s2i[e] = submod(a22i[e], ti[e], m);     // S2 = A22 - y A21
+      s3r[e] = submod(s1r[e], a22r[e], m); s3i[e] = submod(s1i[e], a22i[e], m);   // S3 = S1 - A22
+      s4r[e] = addmod(s3r[e], a12r[e], m); s4i[e] = addmod(s3i[e], a12i[e], m);   // S4 = S3 + A12
+    }
+#define HPUT(o, X) put_limbs4<SCHEME>(out(o, r, c), ps, X, m)
+#define HSUM(X, Y) for (int e = 0; e < 4; ++e) w[e] = addmod(X[e], Y[e], m)
+#define HDIF(X, Y) for (int e = 0; e < 4; ++e) w[e] = submod(X[e], Y[e], m)
+    HSUM(a11r, a11i); HPUT(HO_T11, w); HPUT(HO_X11, a11r); HPUT(HO_Y11, a11i);
+    HSUM(a12r, a12i); HPUT(HO_T12, w); HPUT(HO_X12, a12r); HPUT(HO_Y12, a12i);
+    HSUM(s3r, s3i);   HPUT(HO_T3, w);  HPUT(HO_X3, s3r);   HPUT(HO_Y3, s3i);
+    HSUM(a22r, a22i); HPUT(HO_Z22, w); HPUT(HO_X22, a22r); HPUT(HO_Y22, a22i);
+    HDIF(s4r, s4i);   HPUT(HO_W4, w);  HPUT(HO_X4, s4r);   HPUT(HO_Y4, s4i);
+    HSUM(s1r, s1i);   HPUT(HO_Z1, w);  HPUT(HO_X1, s1r);   HPUT(HO_Y1, s1i);
+    HDIF(s2r, s2i);   HPUT(HO_W2, w);  HPUT(HO_X2, s2r);   HPUT(HO_Y2, s2i);
+#undef HPUT
+#undef HSUM
+#undef HDIF
+  }
+}
+
+cudaError_t launch_herk_preadd(const HerkPreParams &p, cudaStream_t s) {
+  const int64_t groups = p.kh / 4 + (p.kpad - p.kh) / 4;
+  dim3 grid((unsigned)((groups + 255) / 256), (unsigned)(p.rows_pad < 65535 ? p.rows_pad : 65535));
+  if (p.scheme == 0) herk_preadd_kernel<0><<<grid, 256, 0, s>>>(p);
+  else if (p.scheme == 1) herk_preadd_kernel<1><<<grid, 256, 0, s>>>(p);
+  else if (p.scheme == 2) herk_preadd_kernel<2><<<grid, 256, 0, s>>>(p);
+  else herk_preadd_kernel<3><<<grid, 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace adj
