@@ -366,22 +366,26 @@ def run_gpu(args, cfg, rank, world, local_rank):
     # A stream of problems: step i copies its A (H2D), runs the C-ABI call, and reads back its
     # Low(C) row blocks (D2H); three streams, double buffers, so step i's H2D overlaps step
     # i-1's compute and step i-2's D2H.
-    e2e = None
-    if world == 1:
+    def run_e2e(es, eflags):
+        """es = bytes per host/device element: 4 (uint32 residues, the headline) or 2 (ADJ_IN_U16 |
+        ADJ_OUT_U16, phi = T with p < 2^16: half the PCIe bytes each way)."""
         e2e_steps = max(4, min(args.steps, 12))
-        hA = torch.empty((m, k * w), dtype=torch.int32, pin_memory=True)
-        hA.copy_(A)
-        hC = [torch.empty((m, m * w), dtype=torch.int32, pin_memory=True) for _ in range(2)]
-        dA = [torch.empty_like(A) for _ in range(2)]
-        dC = [torch.empty_like(C) for _ in range(2)]
+        dt = torch.int32 if es == 4 else torch.int16
+        hA = torch.empty((m, k * w), dtype=dt, pin_memory=True)
+        hA.copy_(A)                                 # residues < 2^16 survive the int16 bit pattern
+        hC = [torch.empty((m, m * w), dtype=dt, pin_memory=True) for _ in range(2)]
+        dA = [torch.empty((m, k * w), dtype=dt, device=dev) for _ in range(2)]
+        dC = [torch.empty((m, m * w), dtype=dt, device=dev) for _ in range(2)]
         s_in, s_cmp, s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
         nb = 16                                     # Low(C) read back as nb trapezoidal row blocks
         blocks = [(m * b // nb, m * (b + 1) // nb) for b in range(nb)]
-        d2h_bytes = sum((r1 - r0) * r1 * w * 4 for r0, r1 in blocks)
+        d2h_bytes = sum((r1 - r0) * r1 * w * es for r0, r1 in blocks)
         ev_in = [torch.cuda.Event() for _ in range(e2e_steps)]
         ev_cmp = [torch.cuda.Event() for _ in range(e2e_steps)]
         ev_out = [torch.cuda.Event() for _ in range(e2e_steps)]
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        wsz = adj.adjprod_modp_workspace_size(m, k, p, phi, depth, flags | eflags)
+        wse = ws if wsz <= ws_bytes else torch.empty(wsz, dtype=torch.uint8, device=dev)
         torch.cuda.synchronize()
         t0.record(s_in)
         for i in range(e2e_steps):
@@ -395,24 +399,34 @@ def run_gpu(args, cfg, rank, world, local_rank):
                 s_cmp.wait_event(ev_in[i])
                 if i >= 2:
                     s_cmp.wait_event(ev_out[i - 2])
-                adj.adjprod_modp_ex(m, k, p, phi, dA[b], k, dC[b], m, depth=depth, flags=flags, workspace=ws,
-                                    workspace_bytes=ws_bytes, stream=s_cmp)
+                adj.adjprod_modp_ex(m, k, p, phi, dA[b], k, dC[b], m, depth=depth, flags=flags | eflags,
+                                    workspace=wse, workspace_bytes=max(wsz, ws_bytes), stream=s_cmp)
                 ev_cmp[i].record(s_cmp)
             with torch.cuda.stream(s_out):
                 s_out.wait_event(ev_cmp[i])
                 for r0, r1 in blocks:   # rows [r0, r1) of Low(C) need columns [0, r1) only
-                    memcpy2d_d2h(hC[b].data_ptr() + r0 * m * w * 4, m * w * 4, dC[b].data_ptr() + r0 * m * w * 4,
-                                 m * w * 4, r1 * w * 4, r1 - r0, s_out.cuda_stream)
+                    memcpy2d_d2h(hC[b].data_ptr() + r0 * m * w * es, m * w * es,
+                                 dC[b].data_ptr() + r0 * m * w * es, m * w * es, r1 * w * es, r1 - r0,
+                                 s_out.cuda_stream)
                 ev_out[i].record(s_out)
         s_in.wait_stream(s_out)
         t1.record(s_in)
         torch.cuda.synchronize()
         e2e_ms = t0.elapsed_time(t1) / e2e_steps
-        ok = bool(np.array_equal(hC[(e2e_steps - 1) % 2][m - 1, : m * w].numpy(), C[m - 1, : m * w].cpu().numpy()))
-        e2e = {"value": m * m * k / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms,
-               "h2d_bytes_per_step": hA.numel() * 4, "d2h_bytes_per_step": d2h_bytes,
-               "steps": e2e_steps, "pipelined": "3 streams (H2D | C-ABI call | D2H of Low(C) row blocks), 2 buffers",
-               "last_row_matches_device_result": ok}
+        last = hC[(e2e_steps - 1) % 2][m - 1, : m * w].numpy()
+        last = last.view(np.uint16).astype(np.int64) if es == 2 else last.astype(np.int64)
+        ok = bool(np.array_equal(last, C[m - 1, : m * w].cpu().numpy().astype(np.int64)))
+        return {"value": m * m * k / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": hA.numel() * es, "d2h_bytes_per_step": d2h_bytes,
+                "steps": e2e_steps, "pipelined": "3 streams (H2D | C-ABI call | D2H of Low(C) row blocks), 2 buffers",
+                "last_row_matches_device_result": ok}
+
+    e2e = e2e_compact = None
+    if world == 1:
+        e2e = run_e2e(4, 0)
+        if phi == adj.ADJ_PHI_T and p < 65536:
+            e2e_compact = run_e2e(2, adj.ADJ_IN_U16 | adj.ADJ_OUT_U16)
+            e2e_compact["io"] = "uint16 residues both ways (ADJ_IN_U16 | ADJ_OUT_U16)"
 
     # ---------------- comparators on the same box (context, not the metric): our own depth-0 path
     # (classical int8 SYRK, no Alg. 1 -- the on-box analogue of the paper's classical route,
@@ -543,6 +557,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "e2e_compact": e2e_compact,
             "gpu_launches": launches,
             "kernel_time_share": share,
             "hbm_kernels": hbm,

@@ -222,9 +222,9 @@ bool overlap(const void *a, size_t abytes, const void *b, size_t bbytes) {
   return abytes && bbytes && a0 < b1 && b0 < a1;
 }
 
-size_t span_bytes(int64_t rows, int64_t cols, int64_t ld, int w) {
+size_t span_bytes(int64_t rows, int64_t cols, int64_t ld, int elem_bytes) {
   if (rows <= 0 || cols <= 0) return 0;
-  return (size_t)(((rows - 1) * ld + cols) * w) * 4;
+  return (size_t)((rows - 1) * ld + cols) * elem_bytes;
 }
 
 InView make_view(const void *ptr, int64_t ld, int64_t rows, int64_t cols, int type) {
@@ -235,7 +235,7 @@ InView make_view(const void *ptr, int64_t ld, int64_t rows, int64_t cols, int ty
   v.cols_valid = cols;
   v.type = type;
   uintptr_t a = (uintptr_t)ptr;
-  if (type == IN_U16) v.vec_ok = (a % 8 == 0) && (ld % 4 == 0);
+  if (type == IN_U16 || type == IN_U16R) v.vec_ok = (a % 8 == 0) && (ld % 4 == 0);
   else if (type == IN_U32) v.vec_ok = (a % 16 == 0) && (ld % 4 == 0);
   else v.vec_ok = (a % 16 == 0) && (ld % 2 == 0);
   return v;
@@ -246,7 +246,7 @@ InView child_view(const InView &pv, int c, const LevelPlan &Lp, void *s3, int64_
   if (c == 2) return make_view(s3, s3_ld, Lp.mh, Lp.kh, res32 ? IN_U32 : IN_U16);
   const int64_t rows = std::min(pv.rows_valid, Lp.mh);
   if (c == 0) return make_view(pv.ptr, pv.ld, rows, std::min(pv.cols_valid, Lp.kh), pv.type);
-  const int esz = pv.type == IN_U16 ? 2 : (pv.type == IN_U32 ? 4 : (pv.type == IN_QUAD_SUM ? 16 : 8));
+  const int esz = (pv.type == IN_U16 || pv.type == IN_U16R) ? 2 : (pv.type == IN_U32 ? 4 : (pv.type == IN_QUAD_SUM ? 16 : 8));
   const void *ptr = static_cast<const uint8_t *>(pv.ptr) + (size_t)Lp.kh * esz;
   int64_t cols = std::max<int64_t>(0, std::min(pv.cols_valid - Lp.kh, Lp.kh));
   return make_view(ptr, pv.ld, rows, cols, pv.type);
@@ -260,7 +260,8 @@ struct Ptrs {
   const uint32_t *B = nullptr; int64_t ldb = 0;
   uint32_t *C = nullptr; int64_t ldc = 0;
   uint8_t *ws = nullptr;
-  bool res16 = false;   // write the final Low(C) as uint16 residues (adjprod_modp_partial, p < 2^16)
+  bool res16 = false;   // write the final Low(C) as uint16 residues (adjprod_modp_partial, ADJ_OUT_U16)
+  bool in16 = false;    // A holds uint16 values (ADJ_IN_U16)
 };
 
 void *pbuf(const Plan &P, uint8_t *ws, int l, int n, int idx) {
@@ -438,7 +439,7 @@ adj_status_t run_syrk(const Plan &P, const Ptrs &x, adj_phi_t phi, uint32_t flag
   adj_status_t st;
   const int64_t m = P.m, k = P.k;
   if (phi == ADJ_PHI_T) {
-    InView root = make_view(x.A, x.lda, m, k, IN_U32);
+    InView root = make_view(x.A, x.lda, m, k, x.in16 ? IN_U16R : IN_U32);
     if (P.depth == 0) {
       st = run_split(P, root, m, k, P.rows_pad0, P.op0_row[0], x.ws + P.arenas[0].offset, s);
       if (st) return st;
@@ -566,7 +567,7 @@ adj_status_t run_herk1(const Plan &P, const Ptrs &x, uint32_t flags, cudaStream_
 }
 
 adj_status_t validate_syrk(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, const uint32_t *A, int64_t lda,
-                           const uint32_t *C, int64_t ldc) {
+                           const uint32_t *C, int64_t ldc, uint32_t flags = 0) {
   if (m < 0 || k < 0) return fail(ADJ_ERR_INVALID_VALUE, "negative dimension (m=%lld, k=%lld)", (long long)m, (long long)k);
   if (phi != ADJ_PHI_T && phi != ADJ_PHI_H && phi != ADJ_PHI_Q)
     return fail(ADJ_ERR_INVALID_VALUE, "phi must be ADJ_PHI_T, ADJ_PHI_H or ADJ_PHI_Q");
@@ -579,7 +580,8 @@ adj_status_t validate_syrk(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, cons
   if (lda < k || (lda < 1 && k > 0)) return fail(ADJ_ERR_INVALID_VALUE, "lda=%lld < k=%lld", (long long)lda, (long long)k);
   if (ldc < m) return fail(ADJ_ERR_INVALID_VALUE, "ldc=%lld < m=%lld", (long long)ldc, (long long)m);
   const int w = adj_phi_width(phi);
-  if (overlap(A, span_bytes(m, k, lda, w), C, span_bytes(m, m, ldc, w)))
+  const int ea = (flags & ADJ_IN_U16) ? 2 : 4 * w, ec = (flags & ADJ_OUT_U16) ? 2 : 4 * w;
+  if (overlap(A, span_bytes(m, k, lda, ea), C, span_bytes(m, m, ldc, ec)))
     return fail(ADJ_ERR_INVALID_VALUE, "A and C overlap");
   return ADJ_OK;
 }
@@ -672,16 +674,27 @@ adj_status_t adjprod_modp_workspace_size(int64_t m, int64_t k, uint32_t p, adj_p
 static adj_status_t adjprod_impl(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, uint32_t alpha, const uint32_t *A,
                                  int64_t lda, uint32_t beta, uint32_t *C, int64_t ldc, const adj_opts_t *opts,
                                  cudaStream_t s) {
-  adj_status_t st = validate_syrk(m, k, p, phi, A, lda, C, ldc);
-  if (st != ADJ_OK || m == 0) return st;
-  int dev, sms;
-  if ((st = check_device(&dev, &sms)) != ADJ_OK) return st;
-  const int w = adj_phi_width(phi);
   const uint32_t flags = opts ? opts->flags : 0;
+  adj_status_t st = validate_syrk(m, k, p, phi, A, lda, C, ldc, flags);
+  if (st != ADJ_OK) return st;
   alpha %= p;
   beta %= p;
   const int axpby = !(alpha == 1 && beta == 0);
+  const bool in16 = flags & ADJ_IN_U16, out16 = flags & ADJ_OUT_U16;
+  if ((in16 || out16) && (phi != ADJ_PHI_T || p > 65535))
+    return fail(ADJ_ERR_INVALID_VALUE, "ADJ_IN_U16 / ADJ_OUT_U16 need phi = ADJ_PHI_T and p < 2^16");
+  if (out16 && (axpby || (flags & ADJ_FILL_UPPER)))
+    return fail(ADJ_ERR_INVALID_VALUE, "ADJ_OUT_U16 is the plain form: no alpha / beta, no ADJ_FILL_UPPER");
+  if (m == 0) return ADJ_OK;
+  int dev, sms;
+  if ((st = check_device(&dev, &sms)) != ADJ_OK) return st;
+  const int w = adj_phi_width(phi);
   if (k == 0 || alpha == 0) {  // Low(C) = beta Low(C)
+    if (out16) {
+      uint16_t *C16 = reinterpret_cast<uint16_t *>(C);
+      for (int64_t i = 0; i < m; ++i) CUDA_TRY(cudaMemsetAsync(C16 + i * ldc, 0, (size_t)(i + 1) * 2, s));
+      return ADJ_OK;
+    }
     if (beta == 0) {
       for (int64_t i = 0; i < m; ++i) CUDA_TRY(cudaMemsetAsync(C + i * ldc * w, 0, (size_t)(i + 1) * w * 4, s));
     } else {
@@ -700,6 +713,8 @@ static adj_status_t adjprod_impl(int64_t m, int64_t k, uint32_t p, adj_phi_t phi
   Ptrs x;
   x.A = A; x.lda = lda; x.C = C; x.ldc = ldc;
   x.alpha = alpha; x.beta = beta; x.axpby = axpby;
+  x.in16 = in16;
+  x.res16 = out16;
   void *ws = opts ? opts->workspace : nullptr;
   bool own = false;
   if (ws == nullptr) {
@@ -734,6 +749,8 @@ adj_status_t adjprod_modp_shard(int64_t m, int64_t k, uint32_t p, adj_phi_t phi,
   if (phi != ADJ_PHI_T) return fail(ADJ_ERR_INVALID_VALUE, "output-tile sharding supports phi = ADJ_PHI_T");
   if (nranks < 1 || rank < 0 || rank >= nranks) return fail(ADJ_ERR_INVALID_VALUE, "rank %d of %d", rank, nranks);
   if (opts && (opts->flags & ADJ_FILL_UPPER)) return fail(ADJ_ERR_INVALID_VALUE, "ADJ_FILL_UPPER with sharding");
+  if (opts && (opts->flags & (ADJ_IN_U16 | ADJ_OUT_U16)))
+    return fail(ADJ_ERR_INVALID_VALUE, "ADJ_IN_U16 / ADJ_OUT_U16 are adjprod_modp_ex flags");
   if (m == 0) return ADJ_OK;
   const int depth = shard_depth(m, k, p, opts);
   if (depth > 1) return fail(ADJ_ERR_INVALID_VALUE, "output-tile sharding runs at depth 0 or 1 (got %d)", depth);
@@ -779,6 +796,8 @@ adj_status_t adjprod_modp_partial(int64_t m, int64_t k, uint32_t p, adj_phi_t ph
   adj_status_t st = validate_syrk(m, k, p, phi, A, lda, static_cast<const uint32_t *>(R), ldr);
   if (st != ADJ_OK) return st;
   if (phi != ADJ_PHI_T) return fail(ADJ_ERR_INVALID_VALUE, "adjprod_modp_partial supports phi = ADJ_PHI_T");
+  if (opts && (opts->flags & (ADJ_IN_U16 | ADJ_OUT_U16)))
+    return fail(ADJ_ERR_INVALID_VALUE, "ADJ_IN_U16 / ADJ_OUT_U16 are adjprod_modp_ex flags");
   if (m == 0) return ADJ_OK;
   if (p > 65535) {   // residues need 32 bits: the ordinary call writes them
     adj_opts_t o = opts ? *opts : adj_opts_t{-1, 0, nullptr, 0};
@@ -880,8 +899,8 @@ adj_status_t gemm_modp(int64_t m, int64_t n, int64_t k, uint32_t p, const uint32
   if (m == 0 || n == 0) return ADJ_OK;
   if (!C || (k > 0 && (!A || !B))) return fail(ADJ_ERR_INVALID_VALUE, "null pointer");
   if (lda < k || ldb < k || ldc < n) return fail(ADJ_ERR_INVALID_VALUE, "leading dimension too small");
-  if (overlap(A, span_bytes(m, k, lda, 1), C, span_bytes(m, n, ldc, 1)) ||
-      overlap(B, span_bytes(n, k, ldb, 1), C, span_bytes(m, n, ldc, 1)))
+  if (overlap(A, span_bytes(m, k, lda, 4), C, span_bytes(m, n, ldc, 4)) ||
+      overlap(B, span_bytes(n, k, ldb, 4), C, span_bytes(m, n, ldc, 4)))
     return fail(ADJ_ERR_INVALID_VALUE, "C overlaps an input");
   adj_status_t st;
   int dev, sms;

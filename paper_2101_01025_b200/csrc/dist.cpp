@@ -284,6 +284,7 @@ adj_status_t adjprod_modp_dist(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, 
                                adj_stream_t stream) {
   if (!comm || root < 0 || root >= comm->nranks) return ADJ_ERR_INVALID_VALUE;
   if (m < 0 || k < 0) return ADJ_ERR_INVALID_VALUE;
+  if (opts && (opts->flags & (ADJ_IN_U16 | ADJ_OUT_U16))) return ADJ_ERR_INVALID_VALUE;
   if (m == 0) return ADJ_OK;
   const int G = comm->nranks, r = comm->rank;
   if (opts && (opts->flags & ADJ_DIST_TILES)) return dist_tiles(m, k, p, phi, A, lda, C, ldc, root, comm, opts, stream);

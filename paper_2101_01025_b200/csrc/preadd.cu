@@ -28,7 +28,7 @@ __device__ __forceinline__ void load4(const InView &v, int64_t R, int64_t C, con
     }
 #pragma unroll
     for (int e = 0; e < 4; ++e) x[e] = mod_u32(x[e], m);
-  } else if (v.type == IN_U16) {
+  } else if (v.type == IN_U16 || v.type == IN_U16R) {
     const uint16_t *p = static_cast<const uint16_t *>(v.ptr) + R * v.ld + C;
     if (all) {
       uint2 q = __ldg(reinterpret_cast<const uint2 *>(p));
@@ -36,6 +36,10 @@ __device__ __forceinline__ void load4(const InView &v, int64_t R, int64_t C, con
     } else {
 #pragma unroll
       for (int e = 0; e < 4; ++e) if (C + e < v.cols_valid) x[e] = __ldg(p + e);
+    }
+    if (v.type == IN_U16R) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) x[e] = mod_u32(x[e], m);
     }
   } else if (v.type == IN_QUAD_SUM) {
     const uint32_t *p = static_cast<const uint32_t *>(v.ptr) + 4 * (R * v.ld + C);
@@ -232,9 +236,12 @@ __device__ __forceinline__ void load4_fast(const void *ptr, int64_t off, const M
   if constexpr (T == IN_U32) {
     uint4 q = __ldg(reinterpret_cast<const uint4 *>(static_cast<const uint32_t *>(ptr) + off));
     x[0] = mod_u32(q.x, m); x[1] = mod_u32(q.y, m); x[2] = mod_u32(q.z, m); x[3] = mod_u32(q.w, m);
-  } else if constexpr (T == IN_U16) {
+  } else if constexpr (T == IN_U16 || T == IN_U16R) {
     uint2 q = __ldg(reinterpret_cast<const uint2 *>(static_cast<const uint16_t *>(ptr) + off));
     x[0] = q.x & 0xFFFF; x[1] = q.x >> 16; x[2] = q.y & 0xFFFF; x[3] = q.y >> 16;
+    if constexpr (T == IN_U16R) {
+      x[0] = mod_u32(x[0], m); x[1] = mod_u32(x[1], m); x[2] = mod_u32(x[2], m); x[3] = mod_u32(x[3], m);
+    }
   } else if constexpr (T == IN_QUAD_SUM) {
     const uint4 *p = reinterpret_cast<const uint4 *>(static_cast<const uint32_t *>(ptr) + 4 * off);
 #pragma unroll
@@ -476,6 +483,7 @@ __global__ void __launch_bounds__(256) preadd_kernel(const __grid_constant__ Pre
     const int64_t c = g * 4;
     if (type == IN_U32) preadd_row<SCHEME, YK, IN_U32>(P, N, r, c);
     else if (type == IN_U16) preadd_row<SCHEME, YK, IN_U16>(P, N, r, c);
+    else if (type == IN_U16R) preadd_row<SCHEME, YK, IN_U16R>(P, N, r, c);
     else if (type == IN_QUAD_SUM) preadd_row<SCHEME, YK, IN_QUAD_SUM>(P, N, r, c);
     else preadd_row<SCHEME, YK, IN_PAIR_SUM>(P, N, r, c);
   }

@@ -68,7 +68,8 @@ struct FixupTile {
 
 // ---------------------------------------------------------------- K1 pre-addition
 enum InType : int32_t { IN_U32 = 0, IN_U16 = 1, IN_PAIR_SUM = 2, IN_PAIR_RE = 3, IN_PAIR_IM = 4,
-                        IN_QUAD_SUM = 5 /* quaternion x1 + x2 + x3 + x4 (Q6's W = U1 + U2, Alg. alg:2M3M) */ };
+                        IN_QUAD_SUM = 5 /* quaternion x1 + x2 + x3 + x4 (Q6's W = U1 + U2, Alg. alg:2M3M) */,
+                        IN_U16R = 6     /* caller's uint16 input (ADJ_IN_U16): reduced mod p like IN_U32 */ };
 
 struct InView {          // a (possibly padded) view of a node's input matrix
   const void *ptr;

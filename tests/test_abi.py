@@ -77,6 +77,35 @@ def test_validation_is_synchronous_and_needs_no_gpu():
     adj.adjprod_modp(0, 4, 97, 0, 0, 4, 0, 0, stream=0)      # m = 0 is a no-op
 
 
+def test_header_flag_values_match_binding():
+    import re
+    text = open(os.path.join(ROOT, "include", "adjprod.h")).read()
+    for name in ("ADJ_FILL_UPPER", "ADJ_HERK_ALG1", "ADJ_DIST_TILES", "ADJ_DIST_P2P", "ADJ_IN_U16", "ADJ_OUT_U16"):
+        mt = re.search(name + r" = (\d+)u", text)
+        assert mt and int(mt.group(1)) == getattr(adj, name), name
+
+
+def test_compact_io_validation_needs_no_gpu():
+    I16, O16 = adj.ADJ_IN_U16, adj.ADJ_OUT_U16
+    for args, flags in [((4, 4, 131071, 0), I16),                 # p > 2^16: residues need 32 bits
+                        ((4, 4, 8191, 0), O16 | adj.ADJ_FILL_UPPER),
+                        ((4, 4, 8191, 1), I16),                   # phi = H
+                        ((4, 4, 8191, 2), O16)]:                  # phi = Q
+        with pytest.raises(adj.AdjError) as e:
+            adj.adjprod_modp_ex(*args, 4096, 4, 8192, 4, flags=flags, stream=0)
+        assert e.value.status == 1, (args, flags)
+    with pytest.raises(adj.AdjError) as e:                        # SYRK form into a uint16 Low(C)
+        adj.adjprod_modp_syrk(4, 4, 8191, 0, 3, 4096, 4, 1, 8192, 4, flags=O16, stream=0)
+    assert e.value.status == 1
+    # the overlap check counts 2-byte elements: A (16 uint16) ends where C starts
+    with pytest.raises(adj.AdjError) as e:
+        adj.adjprod_modp_ex(4, 4, 8191, 0, 4096, 4, 4096 + 32, 4, flags=I16 | O16, stream=0)
+    assert e.value.status != 1                                     # passes validation, then no device
+    with pytest.raises(adj.AdjError) as e:
+        adj.adjprod_modp_ex(4, 4, 8191, 0, 4096, 4, 4096 + 32, 4, stream=0)
+    assert e.value.status == 1                                     # 4-byte A overlaps
+
+
 def test_workspace_and_depth_planning():
     assert adj.adjprod_modp_auto_depth(64, 64, 97, 0) == 0
     # measured B200 crossovers (R13): recurse while (m/2)^2 (k/2) >= 2^38 per level

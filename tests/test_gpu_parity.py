@@ -531,3 +531,56 @@ print("BAD", bad)
     env = dict(os.environ, ADJ_LEAF_DYNAMIC="1", PYTHONPATH=root)
     out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600, cwd=root)
     assert "BAD 0" in out.stdout, out.stdout + out.stderr
+
+
+@pytest.mark.parametrize("p", [3, 251, 257, 8191, 16763, 16787, 65521])
+@pytest.mark.parametrize("depth", [0, 1, 2])
+@pytest.mark.parametrize("m,k", [(1, 3), (129, 200), (300, 300), (513, 1100)])
+def test_adjprod_T_compact_io(adj, p, depth, m, k):
+    """ADJ_IN_U16 / ADJ_OUT_U16: uint16 A (any value 0..65535, read mod p) and uint16 Low(C),
+    every combination, against the oracle on A mod p."""
+    import torch
+    rng = np.random.default_rng(m * 7 + k + p)
+    A16 = rng.integers(0, 1 << 16, size=(m, k), dtype=np.uint16)
+    A16[0, 0] = 65535
+    ref = oracle.syrk_t((A16.astype(np.uint32) % p).astype(np.uint32), p)
+    dA16 = torch.from_numpy(A16.view(np.int16)).cuda()
+    dA32 = to_dev((A16.astype(np.uint32) % p).astype(np.uint32))
+    for dA in (dA16, dA32):
+        for out16 in (False, True):
+            C = adj.adjprod(dA, p, depth=depth, out16=out16)
+            torch.cuda.synchronize()
+            got = C.cpu().numpy().view(np.uint16 if out16 else np.uint32).astype(np.uint32)
+            assert np.array_equal(got, ref), (p, depth, m, k, dA.element_size(), out16)
+
+
+def test_adjprod_T_compact_io_strided_and_errors(adj):
+    import torch
+    p, m, k = 8191, 300, 260
+    rng = np.random.default_rng(5)
+    A16 = rng.integers(0, 1 << 16, size=(m, k + 12), dtype=np.uint16)
+    ref = oracle.syrk_t((A16[:, :k].astype(np.uint32) % p).astype(np.uint32), p)
+    dA = torch.from_numpy(A16.view(np.int16)).cuda()
+    out = torch.full((m, m + 20), -1, dtype=torch.int16, device="cuda")
+    adj.adjprod_modp_ex(m, k, p, adj.ADJ_PHI_T, dA, k + 12, out, m + 20, depth=1,
+                        flags=adj.ADJ_IN_U16 | adj.ADJ_OUT_U16)
+    torch.cuda.synchronize()
+    got = out.cpu().numpy().view(np.uint16)
+    assert np.array_equal(low(got[:, :m].astype(np.uint32)), ref)
+    assert np.all(np.triu(got[:, :m], 1)[np.triu_indices(m, 1)] == 0xFFFF)   # Up(C) untouched
+    assert np.all(got[:, m:] == 0xFFFF)
+    # k = 0: Low(C) = 0 in uint16
+    out0 = torch.full((4, 4), -1, dtype=torch.int16, device="cuda")
+    adj.adjprod_modp_ex(4, 0, p, adj.ADJ_PHI_T, dA, 1, out0, 4, flags=adj.ADJ_OUT_U16)
+    torch.cuda.synchronize()
+    g0 = out0.cpu().numpy().view(np.uint16)
+    assert np.all(g0[np.tril_indices(4)] == 0) and np.all(g0[np.triu_indices(4, 1)] == 0xFFFF)
+    C32 = torch.zeros((m, m), dtype=torch.int32, device="cuda")
+    bad = [dict(p=131071, flags=adj.ADJ_IN_U16), dict(p=8191, flags=adj.ADJ_OUT_U16 | adj.ADJ_FILL_UPPER)]
+    for b in bad:
+        with pytest.raises(adj.AdjError):
+            adj.adjprod_modp_ex(m, k, b["p"], adj.ADJ_PHI_T, dA, k + 12, C32, m, flags=b["flags"])
+    with pytest.raises(adj.AdjError):   # phi = H
+        adj.adjprod_modp_ex(m, k // 2, p, adj.ADJ_PHI_H, dA, (k + 12) // 2, C32, m // 2, flags=adj.ADJ_IN_U16)
+    with pytest.raises(adj.AdjError):   # SYRK form with a uint16 Low(C)
+        adj.adjprod_modp_syrk(m, k, p, adj.ADJ_PHI_T, 3, dA, k + 12, 1, out, m + 20, flags=adj.ADJ_OUT_U16)
