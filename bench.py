@@ -421,12 +421,17 @@ def run_gpu(args, cfg, rank, world, local_rank):
                 "steps": e2e_steps, "pipelined": "3 streams (H2D | C-ABI call | D2H of Low(C) row blocks), 2 buffers",
                 "last_row_matches_device_result": ok}
 
-    e2e = e2e_compact = None
+    # The headline e2e moves residues in the narrowest format the public API accepts for this
+    # field: uint16 both ways when phi = T and p < 2^16 (the transfer is PCIe-bound, so this
+    # halves it); the uint32 leg is reported beside it as e2e_u32.
+    e2e = e2e_u32 = None
     if world == 1:
-        e2e = run_e2e(4, 0)
+        e2e_u32 = run_e2e(4, 0)
+        e2e_u32["io"] = "uint32 residues both ways"
+        e2e = e2e_u32
         if phi == adj.ADJ_PHI_T and p < 65536:
-            e2e_compact = run_e2e(2, adj.ADJ_IN_U16 | adj.ADJ_OUT_U16)
-            e2e_compact["io"] = "uint16 residues both ways (ADJ_IN_U16 | ADJ_OUT_U16)"
+            e2e = run_e2e(2, adj.ADJ_IN_U16 | adj.ADJ_OUT_U16)
+            e2e["io"] = "uint16 residues both ways (ADJ_IN_U16 | ADJ_OUT_U16)"
 
     # ---------------- comparators on the same box (context, not the metric): our own depth-0 path
     # (classical int8 SYRK, no Alg. 1 -- the on-box analogue of the paper's classical route,
@@ -557,7 +562,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "e2e_compact": e2e_compact,
+            "e2e_u32": e2e_u32 if e2e is not e2e_u32 else None,
             "gpu_launches": launches,
             "kernel_time_share": share,
             "hbm_kernels": hbm,
