@@ -89,21 +89,22 @@ def leaf_int8_ops(cfg, depth, herk="2m") -> float:
     return 2.0 * macs * limb_mmas(p)
 
 
-def hbm_bytes(cfg, depth, herk="2m"):
+def hbm_bytes(cfg, depth, herk="2m", res_bytes=4):
     """Algorithmic HBM bytes per step of the HBM-bound classes (K1 pre-addition / split and the
     recombination), for the layouts DESIGN.md §4 describes: read each input once, write each
-    limb plane / residue once.  None where not derived (depth >= 2, phi = H via ADJ_HERK_ALG1)."""
+    limb plane / residue once.  None where not derived (depth >= 2, phi = H via ADJ_HERK_ALG1).
+    res_bytes: bytes per caller residue of A and Low(C) (4, or 2 with ADJ_IN_U16 | ADJ_OUT_U16)."""
     m, k, p = cfg["m"], cfg["k"], cfg["p"]
     w = {"T": 1, "H": 2, "Q": 4}[cfg["phi"]]
     planes = {1: 1, 3: 3, 4: 2, 6: 6}[limb_mmas(p)]
     rp = lambda x: -(-x // 128) * 128
     res = 4 if p > 65535 else 2
-    out_c = m * (m + 1) // 2 * 4 * w                      # Low(C), uint32 words
+    out_c = m * (m + 1) // 2 * res_bytes * w              # Low(C), uint32 (or uint16) words
     if cfg["phi"] == "H" and herk == "alg1":
         return None
     if depth == 0:
         nops = {1: 1, 2: 3, 4: 7}[w]                       # A | X, Y, T | A, B, C, D, U1, U2, W
-        pre = 4 * w * m * k + nops * planes * rp(m) * rp(k)
+        pre = res_bytes * w * m * k + nops * planes * rp(m) * rp(k)
         if w == 1:
             comb = None                                    # the leaf epilogue writes C directly
         else:
@@ -112,7 +113,7 @@ def hbm_bytes(cfg, depth, herk="2m"):
         return {"preadd": pre, "combine": comb}
     if depth == 1 and w == 1:
         mh, kh = -(-m // 2), 8 * -(-k // 16)
-        pre = 4 * m * k + 7 * planes * rp(mh) * max(128, -(-kh // 128) * 128)
+        pre = res_bytes * m * k + 7 * planes * rp(mh) * max(128, -(-kh // 128) * 128)
         comb = (3 * mh * (mh + 1) // 2 + 2 * mh * mh) * res + out_c
         return {"preadd": pre, "combine": comb}
     return None
@@ -305,9 +306,20 @@ def run_gpu(args, cfg, rank, world, local_rank):
         dist_flags = adj.ADJ_DIST_P2P
     if dist_flags:
         depth = min(depth, 1)
-    A = torch.empty((m, k * w), dtype=torch.int32, device=dev)
-    uniform_residues_cuda(A, seed=1, p=p)
-    C = torch.zeros((m, m * w), dtype=torch.int32, device=dev)
+    # residues of A and Low(C) live in HBM as uint16 when phi = T and p < 2^16 (ADJ_IN_U16 |
+    # ADJ_OUT_U16; exact, the same arithmetic), else uint32.  --io u32 forces uint32.
+    io16 = (args.io == "u16" or (args.io == "auto" and cfg["phi"] == "T" and p < 65536 and world == 1))
+    if io16:
+        flags |= adj.ADJ_IN_U16 | adj.ADJ_OUT_U16
+    A32 = torch.empty((m, k * w), dtype=torch.int32, device=dev)
+    uniform_residues_cuda(A32, seed=1, p=p)
+    A = A32.to(torch.int16) if io16 else A32
+    del A32
+    C = torch.zeros((m, m * w), dtype=torch.int16 if io16 else torch.int32, device=dev)
+
+    def u32(t):
+        """the residues of a device tensor as an int32 tensor (uint16 storage zero-extended)"""
+        return (t.to(torch.int32) & 0xFFFF) if t.element_size() == 2 else t
     comm = None
     if world > 1:
         uid = adj.adj_comm_get_unique_id() if rank == 0 else bytes(128)
@@ -372,7 +384,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
         e2e_steps = max(4, min(args.steps, 12))
         dt = torch.int32 if es == 4 else torch.int16
         hA = torch.empty((m, k * w), dtype=dt, pin_memory=True)
-        hA.copy_(A)                                 # residues < 2^16 survive the int16 bit pattern
+        hA.copy_(A if A.element_size() == es else u32(A))   # residues < 2^16 survive int16 bits
         hC = [torch.empty((m, m * w), dtype=dt, pin_memory=True) for _ in range(2)]
         dA = [torch.empty((m, k * w), dtype=dt, device=dev) for _ in range(2)]
         dC = [torch.empty((m, m * w), dtype=dt, device=dev) for _ in range(2)]
@@ -384,7 +396,8 @@ def run_gpu(args, cfg, rank, world, local_rank):
         ev_cmp = [torch.cuda.Event() for _ in range(e2e_steps)]
         ev_out = [torch.cuda.Event() for _ in range(e2e_steps)]
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        wsz = adj.adjprod_modp_workspace_size(m, k, p, phi, depth, flags | eflags)
+        eflags |= flags & ~(adj.ADJ_IN_U16 | adj.ADJ_OUT_U16)
+        wsz = adj.adjprod_modp_workspace_size(m, k, p, phi, depth, eflags)
         wse = ws if wsz <= ws_bytes else torch.empty(wsz, dtype=torch.uint8, device=dev)
         torch.cuda.synchronize()
         t0.record(s_in)
@@ -399,7 +412,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
                 s_cmp.wait_event(ev_in[i])
                 if i >= 2:
                     s_cmp.wait_event(ev_out[i - 2])
-                adj.adjprod_modp_ex(m, k, p, phi, dA[b], k, dC[b], m, depth=depth, flags=flags | eflags,
+                adj.adjprod_modp_ex(m, k, p, phi, dA[b], k, dC[b], m, depth=depth, flags=eflags,
                                     workspace=wse, workspace_bytes=max(wsz, ws_bytes), stream=s_cmp)
                 ev_cmp[i].record(s_cmp)
             with torch.cuda.stream(s_out):
@@ -415,7 +428,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
         e2e_ms = t0.elapsed_time(t1) / e2e_steps
         last = hC[(e2e_steps - 1) % 2][m - 1, : m * w].numpy()
         last = last.view(np.uint16).astype(np.int64) if es == 2 else last.astype(np.int64)
-        ok = bool(np.array_equal(last, C[m - 1, : m * w].cpu().numpy().astype(np.int64)))
+        ok = bool(np.array_equal(last, u32(C[m - 1, : m * w]).cpu().numpy().astype(np.int64)))
         return {"value": m * m * k / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": hA.numel() * es, "d2h_bytes_per_step": d2h_bytes,
                 "steps": e2e_steps, "pipelined": "3 streams (H2D | C-ABI call | D2H of Low(C) row blocks), 2 buffers",
@@ -458,10 +471,31 @@ def run_gpu(args, cfg, rank, world, local_rank):
                 ts.append(a0.elapsed_time(b0))
             ms0 = statistics.median(ts)
             comparators["depth0_classical"] = {"ms_per_step": ms0, "value": m * m * k / (ms0 * 1e-3), "unit": UNIT,
-                                               "same_result": bool(torch.equal(torch.tril(C0.view(m, -1)),
-                                                                               torch.tril(C.view(m, -1))))
+                                               "same_result": bool(torch.equal(torch.tril(u32(C0).view(m, -1)),
+                                                                               torch.tril(u32(C).view(m, -1))))
                                                if w == 1 else None}
             del w0, C0
+        if io16:   # the same step with uint32 residues in HBM
+            A4, C4 = u32(A), torch.zeros((m, m * w), dtype=torch.int32, device=dev)
+            f4 = flags & ~(adj.ADJ_IN_U16 | adj.ADJ_OUT_U16)
+            for _ in range(3):
+                adj.adjprod_modp_ex(m, k, p, phi, A4, k, C4, m, depth=depth, flags=f4, workspace=ws,
+                                    workspace_bytes=ws_bytes, stream=stream)
+            ts = []
+            for _ in range(max(3, min(args.steps, 10))):
+                flush.zero_()
+                a0, b0 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a0.record(stream)
+                adj.adjprod_modp_ex(m, k, p, phi, A4, k, C4, m, depth=depth, flags=f4, workspace=ws,
+                                    workspace_bytes=ws_bytes, stream=stream)
+                b0.record(stream)
+                torch.cuda.synchronize()
+                ts.append(a0.elapsed_time(b0))
+            ms4 = statistics.median(ts)
+            comparators["uint32_residues"] = {"ms_per_step": ms4, "value": m * m * k / (ms4 * 1e-3), "unit": UNIT,
+                                              "same_result": bool(torch.equal(torch.tril(C4.view(m, -1)),
+                                                                              torch.tril(u32(C).view(m, -1))))}
+            del A4, C4
         try:
             n = 8192
             xa = torch.randint(-128, 128, (n, n), dtype=torch.int8, device=dev)
@@ -486,8 +520,8 @@ def run_gpu(args, cfg, rank, world, local_rank):
     parity = None
     if rank == 0 and not args.no_check:
         rows = (m - 2, m) if m >= 2 else (0, m)
-        Ah = A.cpu().numpy().view(np.uint32).reshape((m, k, w) if w > 1 else (m, k)).astype(np.int64) % p
-        got = C.cpu().numpy().view(np.uint32).reshape((m, m, w) if w > 1 else (m, m))
+        Ah = u32(A).cpu().numpy().view(np.uint32).reshape((m, k, w) if w > 1 else (m, k)).astype(np.int64) % p
+        got = u32(C).cpu().numpy().view(np.uint32).reshape((m, m, w) if w > 1 else (m, m))
         ok = True
         for i in range(*rows):
             X, Xi = Ah[: i + 1], Ah[i]
@@ -524,7 +558,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
             "leaf_launches_per_step": leaf_n / args.steps}
     share = {c: round(v[0] / max(1e-9, sum(x[0] for x in prof.values())), 4) for c, v in prof.items()}
     # achieved HBM bandwidth of the HBM-bound kernels (algorithmic bytes / device time per step)
-    hb = hbm_bytes(cfg, depth, args.herk)
+    hb = hbm_bytes(cfg, depth, args.herk, 2 if io16 else 4)
     hbm = None
     if hb is not None:
         hbm = {}
@@ -538,7 +572,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        Ah = A.cpu().numpy().view(np.uint32).reshape((m, k, w) if w > 1 else (m, k))
+        Ah = u32(A).cpu().numpy().view(np.uint32).reshape((m, k, w) if w > 1 else (m, k))
         eff, t, cores, desc, _ = oracle_sample(cfg, Ah, float(os.environ.get("ADJ_CPU_BUDGET_S", "12")))
         cpu = {"value": eff, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
 
@@ -552,6 +586,8 @@ def run_gpu(args, cfg, rank, world, local_rank):
             "config": {"workload": cfg["workload"] + (" via Alg. 1 over GF(p^2) (ADJ_HERK_ALG1)" if alg1 else ""),
                        "m": m, "k": k, "p": p, "phi": cfg["phi"], "depth": depth,
                        "seed": 1, "l2": "flushed before every timed step (256 MiB write, outside step events)",
+                       "residues": ("uint16 A and Low(C) in HBM (ADJ_IN_U16 | ADJ_OUT_U16)" if io16
+                                    else "uint32 A and Low(C) in HBM"),
                        "parallelism": ("1 GPU" if world == 1 else
                                        (f"output tiles x{world} (NCCL send/recv gather of result tiles)"
                                         if dist_mode == "tiles" else
@@ -584,6 +620,8 @@ def main():
     ap.add_argument("--depth", type=int, default=None)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--io", default="auto", choices=["auto", "u16", "u32"],
+                    help="storage of the residues of A and Low(C): auto = uint16 when phi = T, p < 2^16, N = 1")
     ap.add_argument("--no-check", action="store_true", help="skip the sampled parity check")
     ap.add_argument("--no-compare", action="store_true", help="skip the depth-0 / cuBLASLt comparators")
     ap.add_argument("--dist", default="auto", choices=["auto", "splitk", "tiles", "p2p"],

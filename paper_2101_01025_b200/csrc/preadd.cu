@@ -103,21 +103,21 @@ __device__ __forceinline__ void limbs4(const uint32_t (&x)[4], const ModP &m, ui
   }
 }
 
-// K7 limbs of 4 already-centered values c in [-(p-1)/2, (p-1)/2]
+// K7 limbs of 4 already-centered values c in [-(p-1)/2, (p-1)/2] (p <= 16763: |c| <= 8381):
+// hi = floor((c + 64) / 128), lo = c - 128 hi, mid = hi + lo.  Two values per register in
+// 16-bit lanes: v = c + 64 + 128 * 66 lies in [131, 16893], so hi = (v >> 7) - 66 and
+// lo = (v & 127) - 64 per lane; the int8 bytes are the low bytes of the lanes after adding
+// 256 - 66 and 256 - 64 (all lane values stay below 2^16, no carries between lanes).
 __device__ __forceinline__ void put_limbs4_k7c(int8_t *base, int64_t plane_stride, const int32_t (&c)[4]) {
-  int32_t hi[4], lo[4], mid[4];
-#pragma unroll
-  for (int e = 0; e < 4; ++e) {
-    hi[e] = (c[e] + 64) >> 7;
-    lo[e] = c[e] - (hi[e] << 7);
-    mid[e] = hi[e] + lo[e];
-  }
-  *reinterpret_cast<uint32_t *>(base) =
-      __byte_perm(__byte_perm(hi[0], hi[1], 0x40), __byte_perm(hi[2], hi[3], 0x40), 0x5410);
-  *reinterpret_cast<uint32_t *>(base + plane_stride) =
-      __byte_perm(__byte_perm(lo[0], lo[1], 0x40), __byte_perm(lo[2], lo[3], 0x40), 0x5410);
-  *reinterpret_cast<uint32_t *>(base + 2 * plane_stride) =
-      __byte_perm(__byte_perm(mid[0], mid[1], 0x40), __byte_perm(mid[2], mid[3], 0x40), 0x5410);
+  constexpr uint32_t kOff = (64u + 128u * 66u) * 0x10001u;
+  constexpr uint32_t kHi = 190u * 0x10001u, kLo = 192u * 0x10001u;
+  const uint32_t v01 = (uint32_t)c[0] + ((uint32_t)c[1] << 16) + kOff;
+  const uint32_t v23 = (uint32_t)c[2] + ((uint32_t)c[3] << 16) + kOff;
+  const uint32_t h01 = ((v01 >> 7) & 0x01FF01FFu) + kHi, h23 = ((v23 >> 7) & 0x01FF01FFu) + kHi;
+  const uint32_t l01 = (v01 & 0x007F007Fu) + kLo, l23 = (v23 & 0x007F007Fu) + kLo;
+  *reinterpret_cast<uint32_t *>(base) = __byte_perm(h01, h23, 0x6420);
+  *reinterpret_cast<uint32_t *>(base + plane_stride) = __byte_perm(l01, l23, 0x6420);
+  *reinterpret_cast<uint32_t *>(base + 2 * plane_stride) = __byte_perm(h01 + l01, h23 + l23, 0x6420);
 }
 
 // centered residue of a signed v with |v| < 2^30, 257 <= p <= 16763: float quotient estimate
@@ -336,6 +336,29 @@ __device__ __forceinline__ void preadd_row(const PreParams &P, const PreNode &N,
         (*dst[i])[2] = mod_u32(q[i].z, m); (*dst[i])[3] = mod_u32(q[i].w, m);
       }
     }
+  } else if (fast && T == IN_U16R) {
+    // the same for uint16 input (ADJ_IN_U16): 8 x 8-byte loads first, one canonical check
+    const uint16_t *src = static_cast<const uint16_t *>(v.ptr);
+    const int64_t o1 = r * v.ld, o2 = (P.mh + r) * v.ld;
+    const int64_t offs[8] = {o1 + c, o1 + c + h2, o1 + P.kh + c, o1 + P.kh + c + h2,
+                             o2 + c, o2 + c + h2, o2 + P.kh + c, o2 + P.kh + c + h2};
+    uint32_t(*dst[8])[4] = {&x11a, &x11b, &x12a, &x12b, &x21a, &x21b, &x22a, &x22b};
+    uint2 q[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) q[i] = __ldg(reinterpret_cast<const uint2 *>(src + offs[i]));
+    uint32_t mx = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      (*dst[i])[0] = q[i].x & 0xFFFF; (*dst[i])[1] = q[i].x >> 16;
+      (*dst[i])[2] = q[i].y & 0xFFFF; (*dst[i])[3] = q[i].y >> 16;
+      mx = max(mx, max(max((*dst[i])[0], (*dst[i])[1]), max((*dst[i])[2], (*dst[i])[3])));
+    }
+    if (mx >= m.p) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) (*dst[i])[e] = mod_u32((*dst[i])[e], m);
+    }
   } else if (fast) {
     const int64_t o1 = r * v.ld, o2 = (P.mh + r) * v.ld;
     load4_fast<T>(v.ptr, o1 + c, m, x11a);
@@ -461,7 +484,7 @@ __device__ __forceinline__ void preadd_row(const PreParams &P, const PreNode &N,
 }
 
 template <int SCHEME, int YK>
-__global__ void __launch_bounds__(256) preadd_kernel(const __grid_constant__ PreParams P) {
+__global__ void __launch_bounds__(256, 4) preadd_kernel(const __grid_constant__ PreParams P) {
   constexpr int NP = SCHEME == 0 ? 1 : (SCHEME == 1 ? 3 : (SCHEME == 2 ? 2 : 6));
   const PreNode &N = P.nodes[blockIdx.z];
   const int64_t g_main = P.kh / 8;               // 4-column groups of the first half
@@ -606,9 +629,27 @@ __global__ void __launch_bounds__(256) split_plain_kernel(const __grid_constant_
   for (int64_t r = blockIdx.y; r < P.rows_pad; r += gridDim.y) {
     InView vv = v;
     if (r >= P.rows) vv.rows_valid = 0;
-    const bool fast = vv.vec_ok && vv.type == IN_U32 && r < vv.rows_valid && c0 + 15 < vv.cols_valid && c0 + 15 < P.cols;
+    const bool fast = vv.vec_ok && r < vv.rows_valid && c0 + 15 < vv.cols_valid && c0 + 15 < P.cols;
     uint32_t x[4][4];
-    if (fast) {
+    if (fast && vv.type == IN_U16R && ((uintptr_t)v.ptr % 16 == 0) && (v.ld % 8 == 0)) {
+      // ADJ_IN_U16: two 16-byte loads of 8 uint16 each
+      const uint4 *src = reinterpret_cast<const uint4 *>(static_cast<const uint16_t *>(v.ptr) + r * v.ld + c0);
+      const uint4 q0 = __ldg(src), q1 = __ldg(src + 1);
+      const uint32_t w[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+      uint32_t mx = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        x[i >> 1][(i & 1) * 2] = w[i] & 0xFFFF;
+        x[i >> 1][(i & 1) * 2 + 1] = w[i] >> 16;
+        mx = max(mx, max(w[i] & 0xFFFF, w[i] >> 16));
+      }
+      if (mx >= P.mod.p) {
+#pragma unroll
+        for (int h = 0; h < 4; ++h)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) x[h][e] = mod_u32(x[h][e], P.mod);
+      }
+    } else if (fast && vv.type == IN_U32) {
       uint4 q[4];
 #pragma unroll
       for (int h = 0; h < 4; ++h)

@@ -16,6 +16,7 @@ ap.add_argument("--config", default="c2")
 ap.add_argument("--depth", type=int, default=None)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--gemm", action="store_true", help="run gemm_modp m x m x k instead")
+ap.add_argument("--io16", action="store_true", help="uint16 A and Low(C) (ADJ_IN_U16 | ADJ_OUT_U16)")
 a = ap.parse_args()
 cfg = CONFIGS[a.config]
 m, k, p = cfg["m"], cfg["k"], cfg["p"]
@@ -24,11 +25,15 @@ phi = 1 if w == 2 else 0
 A = torch.empty((m, k * w), dtype=torch.int32, device="cuda")
 uniform_residues_cuda(A, 1, p)
 C = torch.zeros((m, m * w), dtype=torch.int32, device="cuda")
+flags = 0
+if a.io16:
+    A, C = A.to(torch.int16), C.to(torch.int16)
+    flags = adj.ADJ_IN_U16 | adj.ADJ_OUT_U16
 d = a.depth if a.depth is not None else (cfg["depth"] if cfg["depth"] is not None else adj.adjprod_modp_auto_depth(m, k, p, phi))
 for _ in range(a.reps):
     if a.gemm:
         adj.gemm_modp(m, m, k, p, A, k, A, k, C, m)
     else:
-        adj.adjprod_modp_ex(m, k, p, phi, A, k, C, m, depth=d)
+        adj.adjprod_modp_ex(m, k, p, phi, A, k, C, m, depth=d, flags=flags)
 torch.cuda.synchronize()
 print("ok", a.config, "depth", d)
