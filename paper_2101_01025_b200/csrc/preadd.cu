@@ -71,6 +71,31 @@ __device__ __forceinline__ void load4(const InView &v, int64_t R, int64_t C, con
   }
 }
 
+// K7 limbs of 4 already-centered values c in [-(p-1)/2, (p-1)/2] (p <= 16763: |c| <= 8381):
+// hi = floor((c + 64) / 128), lo = c - 128 hi, mid = hi + lo.  Two values per register in
+// 16-bit lanes: v = c + 64 + 128 * 66 lies in [131, 16893], so hi = (v >> 7) - 66 and
+// lo = (v & 127) - 64 per lane; the int8 bytes are the low bytes of the lanes after adding
+// 256 - 66 and 256 - 64 (all lane values stay below 2^16, no carries between lanes).
+__device__ __forceinline__ void k7c_words(const int32_t (&c)[4], uint32_t (&w)[3]) {
+  constexpr uint32_t kOff = (64u + 128u * 66u) * 0x10001u;
+  constexpr uint32_t kHi = 190u * 0x10001u, kLo = 192u * 0x10001u;
+  const uint32_t v01 = (uint32_t)c[0] + ((uint32_t)c[1] << 16) + kOff;
+  const uint32_t v23 = (uint32_t)c[2] + ((uint32_t)c[3] << 16) + kOff;
+  const uint32_t h01 = ((v01 >> 7) & 0x01FF01FFu) + kHi, h23 = ((v23 >> 7) & 0x01FF01FFu) + kHi;
+  const uint32_t l01 = (v01 & 0x007F007Fu) + kLo, l23 = (v23 & 0x007F007Fu) + kLo;
+  w[0] = __byte_perm(h01, h23, 0x6420);
+  w[1] = __byte_perm(l01, l23, 0x6420);
+  w[2] = __byte_perm(h01 + l01, h23 + l23, 0x6420);
+}
+
+__device__ __forceinline__ void put_limbs4_k7c(int8_t *base, int64_t plane_stride, const int32_t (&c)[4]) {
+  uint32_t w[3];
+  k7c_words(c, w);
+  *reinterpret_cast<uint32_t *>(base) = w[0];
+  *reinterpret_cast<uint32_t *>(base + plane_stride) = w[1];
+  *reinterpret_cast<uint32_t *>(base + 2 * plane_stride) = w[2];
+}
+
 // ============================================================================ K1 pre-addition
 // Scheme-specialised limb split of 4 residues into packed int8 plane words (one u32 per plane).
 template <int SCHEME>
@@ -81,43 +106,13 @@ __device__ __forceinline__ void limbs4(const uint32_t (&x)[4], const ModP &m, ui
   if constexpr (SCHEME == 0) {
     w[0] = __byte_perm(__byte_perm(c[0], c[1], 0x40), __byte_perm(c[2], c[3], 0x40), 0x5410);
   } else if constexpr (SCHEME == 1) {
-    int32_t hi[4], lo[4], mid[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      hi[e] = (c[e] + 64) >> 7;
-      lo[e] = c[e] - (hi[e] << 7);
-      mid[e] = hi[e] + lo[e];
-    }
-    w[0] = __byte_perm(__byte_perm(hi[0], hi[1], 0x40), __byte_perm(hi[2], hi[3], 0x40), 0x5410);
-    w[1] = __byte_perm(__byte_perm(lo[0], lo[1], 0x40), __byte_perm(lo[2], lo[3], 0x40), 0x5410);
-    w[2] = __byte_perm(__byte_perm(mid[0], mid[1], 0x40), __byte_perm(mid[2], mid[3], 0x40), 0x5410);
+    // hi = floor((c + 64) / 128), lo = c - 128 hi, mid = hi + lo (SWAR, k7c_words above)
+    k7c_words(c, w);
   } else {
-    int32_t hi[4], lo[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      hi[e] = c[e] >> 8;
-      lo[e] = c[e] - (hi[e] << 8);
-    }
-    w[0] = __byte_perm(__byte_perm(hi[0], hi[1], 0x40), __byte_perm(hi[2], hi[3], 0x40), 0x5410);
-    w[1] = __byte_perm(__byte_perm(lo[0], lo[1], 0x40), __byte_perm(lo[2], lo[3], 0x40), 0x5410);
+    // s8 hi = c >> 8 and u8 lo = c & 255 are bytes 1 and 0 of the two's-complement c
+    w[0] = __byte_perm(__byte_perm(c[0], c[1], 0x51), __byte_perm(c[2], c[3], 0x51), 0x5410);
+    w[1] = __byte_perm(__byte_perm(c[0], c[1], 0x40), __byte_perm(c[2], c[3], 0x40), 0x5410);
   }
-}
-
-// K7 limbs of 4 already-centered values c in [-(p-1)/2, (p-1)/2] (p <= 16763: |c| <= 8381):
-// hi = floor((c + 64) / 128), lo = c - 128 hi, mid = hi + lo.  Two values per register in
-// 16-bit lanes: v = c + 64 + 128 * 66 lies in [131, 16893], so hi = (v >> 7) - 66 and
-// lo = (v & 127) - 64 per lane; the int8 bytes are the low bytes of the lanes after adding
-// 256 - 66 and 256 - 64 (all lane values stay below 2^16, no carries between lanes).
-__device__ __forceinline__ void put_limbs4_k7c(int8_t *base, int64_t plane_stride, const int32_t (&c)[4]) {
-  constexpr uint32_t kOff = (64u + 128u * 66u) * 0x10001u;
-  constexpr uint32_t kHi = 190u * 0x10001u, kLo = 192u * 0x10001u;
-  const uint32_t v01 = (uint32_t)c[0] + ((uint32_t)c[1] << 16) + kOff;
-  const uint32_t v23 = (uint32_t)c[2] + ((uint32_t)c[3] << 16) + kOff;
-  const uint32_t h01 = ((v01 >> 7) & 0x01FF01FFu) + kHi, h23 = ((v23 >> 7) & 0x01FF01FFu) + kHi;
-  const uint32_t l01 = (v01 & 0x007F007Fu) + kLo, l23 = (v23 & 0x007F007Fu) + kLo;
-  *reinterpret_cast<uint32_t *>(base) = __byte_perm(h01, h23, 0x6420);
-  *reinterpret_cast<uint32_t *>(base + plane_stride) = __byte_perm(l01, l23, 0x6420);
-  *reinterpret_cast<uint32_t *>(base + 2 * plane_stride) = __byte_perm(h01 + l01, h23 + l23, 0x6420);
 }
 
 // centered residue of a signed v with |v| < 2^30, 257 <= p <= 16763: float quotient estimate

@@ -569,6 +569,24 @@ def test_adjprod_T_compact_io_strided_and_errors(adj):
     assert np.array_equal(low(got[:, :m].astype(np.uint32)), ref)
     assert np.all(np.triu(got[:, :m], 1)[np.triu_indices(m, 1)] == 0xFFFF)   # Up(C) untouched
     assert np.all(got[:, m:] == 0xFFFF)
+    # a 2-byte-aligned view with an odd leading dimension: the scalar-load paths, every depth
+    for depth in (0, 1, 2):
+        for mm, kk in ((1, 3), (129, 200), (513, 1100)):
+            B16 = rng.integers(0, 1 << 16, size=(mm, kk + 3), dtype=np.uint16)
+            dB = torch.from_numpy(B16.view(np.int16)).cuda()[:, 1:kk + 1]
+            refb = oracle.syrk_t((B16[:, 1:kk + 1].astype(np.uint32) % p).astype(np.uint32), p)
+            Cb = adj.adjprod(dB, p, depth=depth, out16=True)
+            torch.cuda.synchronize()
+            assert np.array_equal(Cb.cpu().numpy().view(np.uint16).astype(np.uint32), refb), (depth, mm, kk)
+    # odd ldc and a 2-byte-offset output: the scalar-store paths
+    for depth in (0, 1):
+        big = torch.full((m, m + 4), -1, dtype=torch.int16, device="cuda")
+        adj.adjprod_modp_ex(m, k, p, adj.ADJ_PHI_T, dA, k + 12, big[:, 1:], m + 4, depth=depth,
+                            flags=adj.ADJ_IN_U16 | adj.ADJ_OUT_U16)
+        torch.cuda.synchronize()
+        g2 = big.cpu().numpy().view(np.uint16)[:, 1:m + 1].astype(np.uint32)
+        assert np.array_equal(low(g2), ref), depth
+        assert np.all(big.cpu().numpy()[:, 0] == -1)
     # k = 0: Low(C) = 0 in uint16
     out0 = torch.full((4, 4), -1, dtype=torch.int16, device="cuda")
     adj.adjprod_modp_ex(4, 0, p, adj.ADJ_PHI_T, dA, 1, out0, 4, flags=adj.ADJ_OUT_U16)
