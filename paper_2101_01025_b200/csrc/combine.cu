@@ -10,12 +10,12 @@
 namespace adj {
 
 // ============================================================================ K4 recombination
-// One block per lower pair {L = (ti, tj), U = (tj, ti)}, ti >= tj, of 64 x 64 tiles of the
-// (mh x mh) product grid, so that every product tile is read once:
+// One block per lower pair {L = (ti, tj), U = (tj, ti)}, ti >= tj, of T x T tiles (T = 32; 64
+// for a sharded pair list) of the (mh x mh) product grid, so that every product tile is read once:
 //   L: U1 = P1 + P5, C21 = U1 + P4 + P3, C22 = Low(U1 + P4 + P4^T), C11 = Low(P1 + P2)
 //   U (ti > tj): C21 = Up(U1) + P4 + P3 with Up(U1) = Low(U1)^T
 // P4(U) and U1(L) are staged in shared memory for the two transposed uses.  Thread (tx, ty) of
-// 8 x 32 owns 8 consecutive columns (16-byte u16 loads) of rows ty and ty + 32.
+// T/8 x T/2 owns 8 consecutive columns (16-byte u16 loads) of rows ty and ty + T/2.
 // SYRK form on the final output: v <- alpha v + beta old (mod p)
 __device__ __forceinline__ void axpby_n(const uint32_t *o, int64_t ncols_ok, uint32_t *v, int n, uint32_t alpha,
                                         uint32_t beta, const ModP &m) {
@@ -60,8 +60,9 @@ template <> struct Pk8<uint32_t> {
   }
 };
 
-template <typename InT, typename OutT>
-__global__ void __launch_bounds__(256) combine_kernel(const __grid_constant__ CombParams P) {
+template <typename InT, typename OutT, int T>
+__global__ void __launch_bounds__(T * T / 16) combine_kernel(const __grid_constant__ CombParams P) {
+  constexpr int TX = T / 8, H = T / 2;   // TX threads of 8 columns per row; rows ty and ty + H
   const CombNode &N = P.nodes[blockIdx.y];
   // lower pair index -> (ti, tj), ti >= tj (or the sharded pair list)
   const int x = (int)blockIdx.x;
@@ -76,21 +77,21 @@ __global__ void __launch_bounds__(256) combine_kernel(const __grid_constant__ Co
     tj = x - ti * (ti + 1) / 2;
   }
   const bool diag = ti == tj;
-  const int tx = threadIdx.x & 7, ty = threadIdx.x >> 3;   // 8 x 32
+  const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
   const int64_t mh = P.mh, ldp = P.ldp;                     // ldp multiple of 128 -> aligned 16-byte loads
-  const int64_t i0 = (int64_t)ti * 64, j0 = (int64_t)tj * 64;
+  const int64_t i0 = (int64_t)ti * T, j0 = (int64_t)tj * T;
   const ModP &m = P.mod;
   const InT *P1 = static_cast<const InT *>(N.P[0]), *P2 = static_cast<const InT *>(N.P[1]);
   const InT *P3 = static_cast<const InT *>(N.P[2]), *P4 = static_cast<const InT *>(N.P[3]);
   const InT *P5 = static_cast<const InT *>(N.P[4]);
-  __shared__ uint32_t sU[64][65];   // U1 on L (Low part; on a diagonal tile the full tile is filled)
-  __shared__ uint32_t sQ[64][65];   // P4 on U (rows j0.., cols i0..)
+  __shared__ uint32_t sU[T][T + 1];   // U1 on L (Low part; on a diagonal tile the full tile is filled)
+  __shared__ uint32_t sQ[T][T + 1];   // P4 on U (rows j0.., cols i0..)
   const int cx = tx * 8;
   // every load of the block up front (buffers are rows_pad x rows_pad: always in range)
   Pk8<InT> l1[2], l5[2], l2[2], l3[2], l4[2], u4[2], u3[2];
 #pragma unroll
   for (int rr = 0; rr < 2; ++rr) {
-    const int y = ty + 32 * rr;
+    const int y = ty + H * rr;
     const int64_t oL = (i0 + y) * ldp + j0 + cx, oU = (j0 + y) * ldp + i0 + cx;
     l1[rr].load(P1 + oL);
     l5[rr].load(P5 + oL);
@@ -103,7 +104,7 @@ __global__ void __launch_bounds__(256) combine_kernel(const __grid_constant__ Co
   uint32_t u1[2][8];
 #pragma unroll
   for (int rr = 0; rr < 2; ++rr) {
-    const int y = ty + 32 * rr;
+    const int y = ty + H * rr;
     uint32_t a[8], b[8], q[8];
     l1[rr].get(a);
     l5[rr].get(b);
@@ -122,7 +123,7 @@ __global__ void __launch_bounds__(256) combine_kernel(const __grid_constant__ Co
   // ---- tile L (and, on the diagonal, its upper part of C21)
 #pragma unroll
   for (int rr = 0; rr < 2; ++rr) {
-    const int y = ty + 32 * rr;
+    const int y = ty + H * rr;
     const int64_t i = i0 + y, j = j0 + cx;
     if (i >= mh || j >= mh) continue;
     uint32_t p4[8], p3[8], c21[8], u[8];
@@ -164,7 +165,7 @@ __global__ void __launch_bounds__(256) combine_kernel(const __grid_constant__ Co
   // ---- tile U = (tj, ti): C21 = Up(U1) + P4 + P3 (rows j0.., cols i0..)
 #pragma unroll
   for (int rr = 0; rr < 2; ++rr) {
-    const int y = ty + 32 * rr;
+    const int y = ty + H * rr;
     const int64_t r = j0 + y, c = i0 + cx;
     if (r >= mh || c >= mh) continue;
     uint32_t p3[8], q4[8], c21[8];
@@ -182,12 +183,20 @@ __global__ void __launch_bounds__(256) combine_kernel(const __grid_constant__ Co
 
 cudaError_t launch_combine(const CombParams &p, cudaStream_t s) {
   if (p.n_nodes == 0) return cudaSuccess;
-  const unsigned nt = (unsigned)((p.mh + 63) / 64);
-  dim3 grid(p.pairs ? (unsigned)p.n_pairs : nt * (nt + 1) / 2, (unsigned)p.n_nodes), block(256);
+  // 32 x 32 tile pairs of 64 threads: ~4x as many blocks as 64 x 64 ones (the 64-tile grid of an
+  // 8192^2 depth-1 call is 7.03 waves of 296 blocks, a near-empty last wave); the sharded pair
+  // list (P.pairs) is in 64-tile units
+  const int T = p.pairs ? 64 : 32;
+  const unsigned nt = (unsigned)((p.mh + T - 1) / T);
+  dim3 grid(p.pairs ? (unsigned)p.n_pairs : nt * (nt + 1) / 2, (unsigned)p.n_nodes), block(T * T / 16);
   if (grid.x == 0) return cudaSuccess;
-  if (p.in32) combine_kernel<uint32_t, uint32_t><<<grid, block, 0, s>>>(p);
-  else if (p.out_u32) combine_kernel<uint16_t, uint32_t><<<grid, block, 0, s>>>(p);
-  else combine_kernel<uint16_t, uint16_t><<<grid, block, 0, s>>>(p);
+#define COMB(I, O)                                                        \
+  if (T == 64) combine_kernel<I, O, 64><<<grid, block, 0, s>>>(p);       \
+  else combine_kernel<I, O, 32><<<grid, block, 0, s>>>(p)
+  if (p.in32) COMB(uint32_t, uint32_t);
+  else if (p.out_u32) COMB(uint16_t, uint32_t);
+  else COMB(uint16_t, uint16_t);
+#undef COMB
   return cudaGetLastError();
 }
 
