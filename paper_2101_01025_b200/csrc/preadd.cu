@@ -125,25 +125,38 @@ __device__ __forceinline__ int32_t center_lazy(int32_t v, float invp, int32_t p,
   return r;
 }
 
-// wide scheme: three balanced base-64 digits d2, d1, d0 in [-32, 32] of the centered residue
-// and the pair sums d2+d1, d1+d0, d2+d0 (6 s8 planes, 3-way Karatsuba)
-__device__ __forceinline__ void put_limbs4_t6(int8_t *base, int64_t plane_stride, const uint32_t (&x)[4],
-                                              const ModP &m) {
-  int32_t d[6][4];
+// wide scheme: three balanced base-64 digits d2, d1, d0 of the centered residue c (|c| <= 131069;
+// d1, d0 in [-32, 31], d2 in [-32, 32]) and the pair sums d2+d1, d1+d0, d2+d0 (6 s8 planes,
+// 3-way Karatsuba).  v = c + 32 (1 + 64 + 4096) = (d0 + 32) + 64 (d1 + 32) + 4096 (d2 + 32) is
+// non-negative, so the digits are its bit fields e0, e1, e2 minus 32.  The fields are packed as
+// bytes; d = e - 32 is the byte (e + 96) ^ 128 and d + d' = e + e' - 64 the byte
+// (e + e' + 64) ^ 128 (no byte exceeds 255, so the packed adds carry nothing between bytes).
+__device__ __forceinline__ void t6_words(const uint32_t (&x)[4], const ModP &m, uint32_t (&w)[6]) {
+  uint32_t e0[4], e1[4], e2[4];
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
-    const int32_t c = centered(x[e], m);
-    const int32_t d0 = ((c + 32) & 63) - 32;
-    const int32_t c1 = (c - d0) >> 6;
-    const int32_t d1 = ((c1 + 32) & 63) - 32;
-    const int32_t d2 = (c1 - d1) >> 6;
-    d[0][e] = d2; d[1][e] = d1; d[2][e] = d0;
-    d[3][e] = d2 + d1; d[4][e] = d1 + d0; d[5][e] = d2 + d0;
+    const uint32_t v = (uint32_t)(centered(x[e], m) + 133152);
+    e0[e] = v & 63u;
+    e1[e] = (v >> 6) & 63u;
+    e2[e] = v >> 12;
   }
+  const uint32_t E0 = __byte_perm(__byte_perm(e0[0], e0[1], 0x40), __byte_perm(e0[2], e0[3], 0x40), 0x5410);
+  const uint32_t E1 = __byte_perm(__byte_perm(e1[0], e1[1], 0x40), __byte_perm(e1[2], e1[3], 0x40), 0x5410);
+  const uint32_t E2 = __byte_perm(__byte_perm(e2[0], e2[1], 0x40), __byte_perm(e2[2], e2[3], 0x40), 0x5410);
+  w[0] = (E2 + 0x60606060u) ^ 0x80808080u;        // d2
+  w[1] = (E1 + 0x60606060u) ^ 0x80808080u;        // d1
+  w[2] = (E0 + 0x60606060u) ^ 0x80808080u;        // d0
+  w[3] = (E2 + E1 + 0x40404040u) ^ 0x80808080u;   // d2 + d1
+  w[4] = (E1 + E0 + 0x40404040u) ^ 0x80808080u;   // d1 + d0
+  w[5] = (E2 + E0 + 0x40404040u) ^ 0x80808080u;   // d2 + d0
+}
+
+__device__ __forceinline__ void put_limbs4_t6(int8_t *base, int64_t plane_stride, const uint32_t (&x)[4],
+                                              const ModP &m) {
+  uint32_t w[6];
+  t6_words(x, m, w);
 #pragma unroll
-  for (int pl = 0; pl < 6; ++pl)
-    *reinterpret_cast<uint32_t *>(base + pl * plane_stride) =
-        __byte_perm(__byte_perm(d[pl][0], d[pl][1], 0x40), __byte_perm(d[pl][2], d[pl][3], 0x40), 0x5410);
+  for (int pl = 0; pl < 6; ++pl) *reinterpret_cast<uint32_t *>(base + pl * plane_stride) = w[pl];
 }
 
 template <int SCHEME>
@@ -165,8 +178,11 @@ template <int SCHEME>
 __device__ __forceinline__ void put_limbs8(int8_t *base, int64_t plane_stride, const uint32_t (&x0)[4],
                                            const uint32_t (&x1)[4], const ModP &m) {
   if constexpr (SCHEME == 3) {
-    put_limbs4_t6(base, plane_stride, x0, m);
-    put_limbs4_t6(base + 4, plane_stride, x1, m);
+    uint32_t w0[6], w1[6];
+    t6_words(x0, m, w0);
+    t6_words(x1, m, w1);
+#pragma unroll
+    for (int pl = 0; pl < 6; ++pl) *reinterpret_cast<uint2 *>(base + pl * plane_stride) = make_uint2(w0[pl], w1[pl]);
     return;
   }
   constexpr int NP = SCHEME == 0 ? 1 : (SCHEME == 1 ? 3 : 2);
@@ -182,8 +198,12 @@ template <int SCHEME>
 __device__ __forceinline__ void put_limbs16(int8_t *base, int64_t plane_stride, const uint32_t (&x)[4][4],
                                             const ModP &m) {
   if constexpr (SCHEME == 3) {
+    uint32_t w[4][6];
 #pragma unroll
-    for (int g = 0; g < 4; ++g) put_limbs4_t6(base + 4 * g, plane_stride, x[g], m);
+    for (int g = 0; g < 4; ++g) t6_words(x[g], m, w[g]);
+#pragma unroll
+    for (int pl = 0; pl < 6; ++pl)
+      *reinterpret_cast<uint4 *>(base + pl * plane_stride) = make_uint4(w[0][pl], w[1][pl], w[2][pl], w[3][pl]);
     return;
   }
   constexpr int NP = SCHEME == 0 ? 1 : (SCHEME == 1 ? 3 : 2);
