@@ -227,17 +227,25 @@ def oracle_sample(cfg, A_host, budget_s: float):
     t_cal = time.perf_counter() - t0
     macs_cal = sum(i + 1 for i in range(m - r, m)) * k
     rate = macs_cal / max(t_cal, 1e-6)
-    target = budget_s * rate
-    rows = 1
-    macs = 0
-    while rows < m and macs < target:
-        macs += (m - rows + 1) * k
-        rows += 1
-    rows = max(1, rows - 1)
-    t0 = time.perf_counter()
-    f(A_host, p, rows=(m - rows, m))
-    t = time.perf_counter() - t0
-    sample_macs = sum(i + 1 for i in range(m - rows, m)) * k
+
+    def rows_for(target):
+        rows, macs = 1, 0
+        while rows < m and macs < target:
+            macs += (m - rows + 1) * k
+            rows += 1
+        return max(1, rows - 1)
+
+    # a tiny slab underestimates the multi-threaded rate: re-size until the slab takes at least
+    # half the budget (or covers the whole triangle)
+    rows = rows_for(budget_s * rate)
+    for _ in range(4):
+        t0 = time.perf_counter()
+        f(A_host, p, rows=(m - rows, m))
+        t = time.perf_counter() - t0
+        sample_macs = sum(i + 1 for i in range(m - rows, m)) * k
+        if t >= 0.5 * budget_s or rows >= m:
+            break
+        rows = rows_for(budget_s * sample_macs / max(t, 1e-6))
     full_lower = m * (m + 1) / 2 * k
     t_full = t * full_lower / sample_macs
     eff = m * m * k / t_full
@@ -573,7 +581,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         Ah = u32(A).cpu().numpy().view(np.uint32).reshape((m, k, w) if w > 1 else (m, k))
-        eff, t, cores, desc, _ = oracle_sample(cfg, Ah, float(os.environ.get("ADJ_CPU_BUDGET_S", "12")))
+        eff, t, cores, desc, _ = oracle_sample(cfg, Ah, float(os.environ.get("ADJ_CPU_BUDGET_S", "10")))
         cpu = {"value": eff, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
 
     if rank == 0:
