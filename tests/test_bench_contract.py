@@ -1,0 +1,78 @@
+"""bench.py's driver contract on the host: the reference arm (the CPU oracle timed as it stands,
+DESIGN.md §7) prints one JSON line with the contract's keys, and the bench's own bookkeeping
+(ring MAC counts, algorithmic bytes) follows the closed forms of Alg. alg:MIAHMM."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402
+
+
+def test_reference_arm_json_line():
+    env = dict(os.environ, ADJ_REF_STEP_S="0.05")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "c1",
+                          "--steps", "2", "--warmup", "1"], capture_output=True, text=True, env=env, timeout=300,
+                         cwd=ROOT, check=True).stdout
+    lines = [ln for ln in out.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for key in ("impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+                "scaling", "vs_baseline", "dtype", "data", "config", "cpu_baseline", "e2e"):
+        assert key in d, key
+    assert d["impl"] == "reference" and d["metric"] == bench.METRIC and d["unit"] == bench.UNIT
+    assert d["value"] > 0 and d["higher_is_better"] is True and d["steps"] == 2
+    assert d["config"]["workload"] == bench.CONFIGS["c1"]["workload"]
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] == d["value"]
+    assert d["cpu_baseline"]["cores"] >= 1 and d["cpu_baseline"]["sample"]
+    assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+
+
+def test_ring_macs_leading_ratios():
+    """R_d / R_0 -> (7/8)^... : one level of Alg. 1 does 3 half-size SYRKs and 2 half-size
+    general products, 7/8 of the classical lower-triangle MACs as m, k grow;
+    two levels 53/64."""
+    m = k = 1 << 20
+    r0 = bench.ring_macs(m, k, 0)
+    assert abs(bench.ring_macs(m, k, 1) / r0 - 7 / 8) < 1e-5
+    assert abs(bench.ring_macs(m, k, 2) / r0 - 53 / 64) < 1e-5
+    # exact small case: m = k = 2, one level = 3 (1x1 SYRK, k = 1) + 2 (1x1x1) = 5 MACs
+    assert bench.ring_macs(2, 2, 1) == 5
+
+
+@pytest.mark.parametrize("res_bytes", [2, 4])
+def test_hbm_bytes_c2(res_bytes):
+    """K1 at c2 depth 1: A read once, 7 operands x 3 limb planes of (m/2) x (k/2) int8 written;
+    K4: P1, P2, P5 lower + P3, P4 full uint16 read once, Low(C) written once."""
+    cfg = bench.CONFIGS["c2"]
+    m, k = cfg["m"], cfg["k"]
+    hb = bench.hbm_bytes(cfg, 1, res_bytes=res_bytes)
+    mh, kh = m // 2, k // 2
+    assert hb["preadd"] == res_bytes * m * k + 7 * 3 * mh * kh
+    assert hb["combine"] == (3 * mh * (mh + 1) // 2 + 2 * mh * mh) * 2 + m * (m + 1) // 2 * res_bytes
+
+
+@pytest.mark.gpu
+def test_gpu_arm_json_line():
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", "c1", "--steps", "3",
+                          "--warmup", "3", "--no-cpu", "--no-compare"], capture_output=True, text=True, timeout=600,
+                         cwd=ROOT, check=True).stdout
+    lines = [ln for ln in out.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+                "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "gpu_launches", "clocks"):
+        assert key in d, key
+    assert d["metric"] == bench.METRIC and d["n_gpus"] == 1 and d["steps"] == 3 and d["warmup"] >= 3
+    assert d["value"] > 0 and d["gpu_launches"] > 0
+    r = d["roofline"]
+    assert r["bound"] == "tensor" and r["unit"] == "TFLOP/s" and abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
+    e = d["e2e"]
+    assert e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0 and e["last_row_matches_device_result"]
+    assert d["parity"]["bit_exact"]
+    assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
