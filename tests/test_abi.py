@@ -179,3 +179,18 @@ def test_shard_layout_balanced():
                 rects = adj.adj_shard_layout(m, k, 8191, r, n, depth=depth)
                 sizes.append(sum(rows * cols for (_, _, rows, cols, _) in rects))
             assert max(sizes) - min(sizes) <= 4 * 256 * 256, (depth, n, sizes)
+
+
+def test_maximum_sizes_are_planned_or_refused():
+    """The packed tile descriptor holds 12-bit tile indices: a leaf operand of 4096 x 256 rows or
+    more is refused with ADJ_ERR_INVALID_VALUE at planning time (never a silent wrap); one level
+    of Alg. 1 halves it back into range."""
+    m = 4096 * 256
+    with pytest.raises(adj.AdjError) as e:
+        adj.adjprod_modp_workspace_size(m, 256, 8191, 0, 0)
+    assert e.value.status == 1
+    with pytest.raises(adj.AdjError) as e:
+        adj.adjprod_modp_workspace_size(m + 1000, 64, 97, 0, 0)
+    assert e.value.status == 1
+    # largest single-tile-index-range leaf still planned (m = 4095 x 256 at depth 0)
+    assert adj.adjprod_modp_workspace_size(4095 * 256, 32, 97, 0, 0) > 0
