@@ -22,20 +22,32 @@ def env():
     return torch, adj, bench
 
 
-def _run(env, cfg, A_dev):
+def _run(env, cfg, A_dev, io16=None):
+    """The bench's launch: its depth, and (io16=None) its residue storage -- uint16 A and Low(C)
+    (ADJ_IN_U16 | ADJ_OUT_U16) for phi = T, p < 2^16, else uint32.  Returns Low(C) as uint32."""
     torch, adj, bench = env
     m, k, p = cfg["m"], cfg["k"], cfg["p"]
     phi = adj.ADJ_PHI_H if cfg["phi"] == "H" else adj.ADJ_PHI_T
     depth = cfg["depth"] if cfg["depth"] is not None else adj.adjprod_modp_auto_depth(m, k, p, phi)
     w = 2 if phi else 1
+    if io16 is None:
+        io16 = cfg["phi"] == "T" and p < 65536
+    if io16:
+        A16 = A_dev.to(torch.int16)
+        C = torch.zeros((m, m), dtype=torch.int16, device="cuda")
+        adj.adjprod_modp_ex(m, k, p, phi, A16, k, C, m, depth=depth, flags=adj.ADJ_IN_U16 | adj.ADJ_OUT_U16)
+        del A16
+        torch.cuda.synchronize()
+        return C.to(torch.int32) & 0xFFFF, depth
     C = torch.zeros((m, m * w), dtype=torch.int32, device="cuda")
     adj.adjprod_modp_ex(m, k, p, phi, A_dev, k, C, m, depth=depth)
     torch.cuda.synchronize()
     return C, depth
 
 
-@pytest.mark.parametrize("name", ["c1", "c2", "c5", "c4", "c3"])
-def test_config_sampled_rows_and_freivalds(env, name):
+@pytest.mark.parametrize("name,io16", [("c1", None), ("c2", None), ("c2", False), ("c5", None), ("c4", None),
+                                       ("c3", None)])
+def test_config_sampled_rows_and_freivalds(env, name, io16):
     torch, adj, bench = env
     from inputs.gpu import uniform_residues_cuda
     cfg = bench.CONFIGS[name]
@@ -43,7 +55,7 @@ def test_config_sampled_rows_and_freivalds(env, name):
     w = 2 if cfg["phi"] == "H" else 1
     A = torch.empty((m, k * w), dtype=torch.int32, device="cuda")
     uniform_residues_cuda(A, seed=1, p=p)
-    C, depth = _run(env, cfg, A)
+    C, depth = _run(env, cfg, A, io16)
     Ah = A.cpu().numpy().view(np.uint32).reshape((m, k, 2) if w == 2 else (m, k))
     Ch = C.cpu().numpy().view(np.uint32).reshape((m, m, 2) if w == 2 else (m, m))
     del C
