@@ -9,7 +9,7 @@ import ctypes
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libadjprod.so")
+LIB_PATH = os.environ.get("ADJ_LIB_PATH") or os.path.join(_PKG, "libadjprod.so")   # override: dev A/B only
 
 ADJ_PHI_T = 0
 ADJ_PHI_H = 1

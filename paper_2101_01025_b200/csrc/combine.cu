@@ -411,7 +411,7 @@ __device__ __forceinline__ void store_q8(uint32_t *o, int64_t n, uint32_t (&h)[4
   }
   if (n == 8 && (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
 #pragma unroll
-    for (int e = 0; e < 8; ++e) reinterpret_cast<uint4 *>(o)[e] = make_uint4(h[0][e], h[1][e], h[2][e], h[3][e]);
+    for (int e = 0; e < 8; ++e) __stcs(reinterpret_cast<uint4 *>(o) + e, make_uint4(h[0][e], h[1][e], h[2][e], h[3][e]));
   } else {
 #pragma unroll
     for (int e = 0; e < 8; ++e)
