@@ -467,6 +467,8 @@ def run_gpu(args, cfg, rank, world, local_rank):
         ok = bool(np.array_equal(last, u32(C[m - 1, : m * w]).cpu().numpy().astype(np.int64)))
         return {"value": m * m * k / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": hA.numel() * es, "d2h_bytes_per_step": d2h_bytes,
+                "h2d_gbs_per_step_time": hA.numel() * es / (e2e_ms * 1e6),   # PCIe-bound: the copy rate
+                "d2h_gbs_per_step_time": d2h_bytes / (e2e_ms * 1e6),
                 "steps": e2e_steps, "pipelined": "3 streams (H2D | C-ABI call | D2H of Low(C) row blocks), 2 buffers",
                 "last_row_matches_device_result": ok}
 
