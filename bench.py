@@ -483,6 +483,45 @@ def run_gpu(args, cfg, rank, world, local_rank):
         if phi == adj.ADJ_PHI_T and p < 65536:
             e2e = run_e2e(2, adj.ADJ_IN_U16 | adj.ADJ_OUT_U16)
             e2e["io"] = "uint16 residues both ways (ADJ_IN_U16 | ADJ_OUT_U16)"
+    else:
+        # N > 1, "A on rank 0": per step rank 0 copies A from pinned host memory,
+        # broadcasts it over NCCL, every rank runs adjprod_modp_dist, rank 0 reads Low(C) back;
+        # device time per rank, max over ranks
+        try:
+            e2e_steps = max(3, min(args.steps, 8))
+            hA = torch.empty((m, k * w), dtype=torch.int32, pin_memory=True) if rank == 0 else None
+            if rank == 0:
+                hA.copy_(A)
+            hC = torch.empty((m, m * w), dtype=torch.int32, pin_memory=True) if rank == 0 else None
+            dA = torch.empty_like(A)
+            nb = 16
+            blocks = [(m * b // nb, m * (b + 1) // nb) for b in range(nb)]
+            d2h_bytes = sum((r1 - r0) * r1 * w * 4 for r0, r1 in blocks)
+            t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            dist.barrier()
+            torch.cuda.synchronize()
+            t0.record(stream)
+            for _ in range(e2e_steps):
+                if rank == 0:
+                    dA.copy_(hA, non_blocking=True)
+                dist.broadcast(dA, src=0)
+                adj.adjprod_modp_dist(m, k, p, phi, dA, k, C, m, 0, comm, depth=depth, flags=dist_flags,
+                                      stream=stream)
+                if rank == 0:
+                    for r0, r1 in blocks:
+                        memcpy2d_d2h(hC.data_ptr() + r0 * m * w * 4, m * w * 4, C.data_ptr() + r0 * m * w * 4,
+                                     m * w * 4, r1 * w * 4, r1 - r0, stream.cuda_stream)
+            t1.record(stream)
+            torch.cuda.synchronize()
+            t = torch.tensor([t0.elapsed_time(t1) / e2e_steps], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+            e2e = {"value": m * m * k / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms,
+                   "h2d_bytes_per_step": m * k * w * 4, "d2h_bytes_per_step": d2h_bytes, "steps": e2e_steps,
+                   "io": "uint32 residues; A from pinned host memory on rank 0, NCCL broadcast, Low(C) read "
+                         "back on rank 0 (SURVEY.md §8(e) 'A on rank 0')"}
+        except Exception as ex:  # noqa: BLE001 -- the device-resident line above stands without it
+            e2e = {"error": f"{type(ex).__name__}: {ex}"}
 
     # ---------------- comparators on the same box (context, not the metric): our own depth-0 path
     # (classical int8 SYRK, no Alg. 1 -- the on-box analogue of the paper's classical route,
