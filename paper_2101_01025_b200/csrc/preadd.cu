@@ -76,11 +76,13 @@ __device__ __forceinline__ void load4(const InView &v, int64_t R, int64_t C, con
 // 16-bit lanes: v = c + 64 + 128 * 66 lies in [131, 16893], so hi = (v >> 7) - 66 and
 // lo = (v & 127) - 64 per lane; the int8 bytes are the low bytes of the lanes after adding
 // 256 - 66 and 256 - 64 (all lane values stay below 2^16, no carries between lanes).
-__device__ __forceinline__ void k7c_words(const int32_t (&c)[4], uint32_t (&w)[3]) {
-  constexpr uint32_t kOff = (64u + 128u * 66u) * 0x10001u;
+// a[] are the lane values v - off of the K7 words above: v = a + off (off = 64 + 128 * 66 for
+// centered c, or 64 + 128 * 66 - (p - 1) / 2 for the offset residues c + (p - 1) / 2 of K1)
+__device__ __forceinline__ void k7_words(const uint32_t (&a)[4], uint32_t off, uint32_t (&w)[3]) {
   constexpr uint32_t kHi = 190u * 0x10001u, kLo = 192u * 0x10001u;
-  const uint32_t v01 = (uint32_t)c[0] + ((uint32_t)c[1] << 16) + kOff;
-  const uint32_t v23 = (uint32_t)c[2] + ((uint32_t)c[3] << 16) + kOff;
+  const uint32_t off2 = off * 0x10001u;
+  const uint32_t v01 = a[0] + (a[1] << 16) + off2;
+  const uint32_t v23 = a[2] + (a[3] << 16) + off2;
   const uint32_t h01 = ((v01 >> 7) & 0x01FF01FFu) + kHi, h23 = ((v23 >> 7) & 0x01FF01FFu) + kHi;
   const uint32_t l01 = (v01 & 0x007F007Fu) + kLo, l23 = (v23 & 0x007F007Fu) + kLo;
   w[0] = __byte_perm(h01, h23, 0x6420);
@@ -88,9 +90,16 @@ __device__ __forceinline__ void k7c_words(const int32_t (&c)[4], uint32_t (&w)[3
   w[2] = __byte_perm(h01 + l01, h23 + l23, 0x6420);
 }
 
-__device__ __forceinline__ void put_limbs4_k7c(int8_t *base, int64_t plane_stride, const int32_t (&c)[4]) {
+__device__ __forceinline__ void k7c_words(const int32_t (&c)[4], uint32_t (&w)[3]) {
+  const uint32_t a[4] = {(uint32_t)c[0], (uint32_t)c[1], (uint32_t)c[2], (uint32_t)c[3]};
+  k7_words(a, 64u + 128u * 66u, w);
+}
+
+// K7 limb planes of 4 offset residues u = c + (p - 1) / 2 (off = 64 + 128 * 66 - (p - 1) / 2)
+__device__ __forceinline__ void put_limbs4_k7u(int8_t *base, int64_t plane_stride, const uint32_t (&u)[4],
+                                               uint32_t off) {
   uint32_t w[3];
-  k7c_words(c, w);
+  k7_words(u, off, w);
   *reinterpret_cast<uint32_t *>(base) = w[0];
   *reinterpret_cast<uint32_t *>(base + plane_stride) = w[1];
   *reinterpret_cast<uint32_t *>(base + 2 * plane_stride) = w[2];
@@ -113,16 +122,6 @@ __device__ __forceinline__ void limbs4(const uint32_t (&x)[4], const ModP &m, ui
     w[0] = __byte_perm(__byte_perm(c[0], c[1], 0x51), __byte_perm(c[2], c[3], 0x51), 0x5410);
     w[1] = __byte_perm(__byte_perm(c[0], c[1], 0x40), __byte_perm(c[2], c[3], 0x40), 0x5410);
   }
-}
-
-// centered residue of a signed v with |v| < 2^30, 257 <= p <= 16763: float quotient estimate
-// (error < 0.2) then one fix in each direction
-__device__ __forceinline__ int32_t center_lazy(int32_t v, float invp, int32_t p, int32_t h) {
-  const int32_t q = __float2int_rn(__int2float_rn(v) * invp);
-  int32_t r = v - q * p;
-  r = r > h ? r - p : r;
-  r = r < -h ? r + p : r;
-  return r;
 }
 
 // wide scheme: three balanced base-64 digits d2, d1, d0 of the centered residue c (|c| <= 131069;
@@ -397,13 +396,23 @@ __device__ __forceinline__ void preadd_row(const PreParams &P, const PreNode &N,
     load4(vv, P.mh + r, P.kh + c + h2, m, x22b);
   }
   if constexpr (SCHEME == 1) {
-    // Lazy reduction (p <= 16763 so 2 p^2 < 2^31): Y products in raw int32, one centered
-    // reduction per S output; X outputs and S3/S4 need one conditional correction each.
+    // Lazy reduction (p <= 16763 so 2 p^2 < 2^31): Y products in raw int32, one reduction per S
+    // output.  Residues are carried as offset values u = c + h in [0, p) of the centered c
+    // (h = (p - 1) / 2), so every correction is an unsigned min of u, u - p, u + p.
     const int32_t p = (int32_t)m.p, h = (int32_t)m.half;
+    const uint32_t up = m.p;
     const float invp = 1.0f / (float)m.p;
     const int32_t ya = (int32_t)P.ya, yb = (int32_t)P.yb;
-    int32_t c1a[4], c1b[4], c2a[4], c2b[4], c3a[4], c3b[4], c4a[4], c4b[4];
-    int32_t c11a[4], c11b[4], c12a[4], c12b[4], c22a[4], c22b[4];
+    // v + h - q p with the float quotient estimate q (error < 0.2): in [-0.2 p, 1.2 p)
+    auto off_lazy = [&](int32_t v) -> uint32_t {
+      const int32_t q = __float2int_rn(__int2float_rn(v) * invp);
+      const uint32_t u = (uint32_t)(v + h - q * p);
+      return umin32(umin32(u, u - up), u + up);
+    };
+    auto wrap_lo = [&](uint32_t u) { return umin32(u, u + up); };   // u in (-p, p)
+    auto wrap_hi = [&](uint32_t u) { return umin32(u, u - up); };   // u in [0, 2p)
+    uint32_t u1a[4], u1b[4], u2a[4], u2b[4], u3a[4], u3b[4], u4a[4], u4b[4];
+    uint32_t u11a[4], u11b[4], u12a[4], u12b[4], u22a[4], u22b[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const int32_t d1 = (int32_t)x21a[e] - (int32_t)x11a[e], d2 = (int32_t)x21b[e] - (int32_t)x11b[e];
@@ -416,45 +425,40 @@ __device__ __forceinline__ void preadd_row(const PreParams &P, const PreNode &N,
         tr_a = ya * (int32_t)x21a[e] - yb * (int32_t)x21b[e];                          // A21 Y
         tr_b = yb * (int32_t)x21a[e] + ya * (int32_t)x21b[e];
       }
-      c1a[e] = center_lazy(s1r_a, invp, p, h); c1b[e] = center_lazy(s1r_b, invp, p, h);               // S1
-      c2a[e] = center_lazy((int32_t)x22a[e] - tr_a, invp, p, h);                                        // S2
-      c2b[e] = center_lazy((int32_t)x22b[e] - tr_b, invp, p, h);
-      c3a[e] = c1a[e] - (int32_t)x22a[e]; c3a[e] = c3a[e] < -h ? c3a[e] + p : c3a[e];                 // S3
-      c3b[e] = c1b[e] - (int32_t)x22b[e]; c3b[e] = c3b[e] < -h ? c3b[e] + p : c3b[e];
-      c4a[e] = c3a[e] + (int32_t)x12a[e]; c4a[e] = c4a[e] > h ? c4a[e] - p : c4a[e];                  // S4
-      c4b[e] = c3b[e] + (int32_t)x12b[e]; c4b[e] = c4b[e] > h ? c4b[e] - p : c4b[e];
-      c11a[e] = (int32_t)x11a[e] > h ? (int32_t)x11a[e] - p : (int32_t)x11a[e];
-      c11b[e] = (int32_t)x11b[e] > h ? (int32_t)x11b[e] - p : (int32_t)x11b[e];
-      c12a[e] = (int32_t)x12a[e] > h ? (int32_t)x12a[e] - p : (int32_t)x12a[e];
-      c12b[e] = (int32_t)x12b[e] > h ? (int32_t)x12b[e] - p : (int32_t)x12b[e];
-      c22a[e] = (int32_t)x22a[e] > h ? (int32_t)x22a[e] - p : (int32_t)x22a[e];
-      c22b[e] = (int32_t)x22b[e] > h ? (int32_t)x22b[e] - p : (int32_t)x22b[e];
+      u1a[e] = off_lazy(s1r_a); u1b[e] = off_lazy(s1r_b);                                           // S1
+      u2a[e] = off_lazy((int32_t)x22a[e] - tr_a); u2b[e] = off_lazy((int32_t)x22b[e] - tr_b);       // S2
+      u3a[e] = wrap_lo(u1a[e] - x22a[e]); u3b[e] = wrap_lo(u1b[e] - x22b[e]);                       // S3
+      u4a[e] = wrap_hi(u3a[e] + x12a[e]); u4b[e] = wrap_hi(u3b[e] + x12b[e]);                       // S4
+      u11a[e] = wrap_hi(x11a[e] + h); u11b[e] = wrap_hi(x11b[e] + h);
+      u12a[e] = wrap_hi(x12a[e] + h); u12b[e] = wrap_hi(x12b[e] + h);
+      u22a[e] = wrap_hi(x22a[e] + h); u22b[e] = wrap_hi(x22b[e] + h);
     }
     const int64_t ps = P.rows_pad * P.kpad;
+    const uint32_t koff = 64u + 128u * 66u - (uint32_t)h;
 #define PUTC(o, A, B)                                                                  \
   if (N.op_row[o] >= 0) {                                                              \
     int8_t *b = P.arena + (N.op_row[o] + r) * P.kpad;                                  \
-    put_limbs4_k7c(b + c, ps, A);                                                      \
-    put_limbs4_k7c(b + c + h2, ps, B);                                                 \
+    put_limbs4_k7u(b + c, ps, A, koff);                                                \
+    put_limbs4_k7u(b + c + h2, ps, B, koff);                                           \
   }
-    PUTC(OUT_S1, c1a, c1b)
-    PUTC(OUT_S2, c2a, c2b)
-    PUTC(OUT_S4, c4a, c4b)
-    PUTC(OUT_X22, c22a, c22b)
-    PUTC(OUT_X11, c11a, c11b)
-    PUTC(OUT_X12, c12a, c12b)
-    PUTC(OUT_S3, c3a, c3b)
+    PUTC(OUT_S1, u1a, u1b)
+    PUTC(OUT_S2, u2a, u2b)
+    PUTC(OUT_S4, u4a, u4b)
+    PUTC(OUT_X22, u22a, u22b)
+    PUTC(OUT_X11, u11a, u11b)
+    PUTC(OUT_X12, u12a, u12b)
+    PUTC(OUT_S3, u3a, u3b)
 #undef PUTC
-    if (N.s3 != nullptr && r < P.mh) {
+    if (N.s3 != nullptr && r < P.mh) {   // canonical S3 = (u3 - h) mod p for the next level
       uint16_t *d = static_cast<uint16_t *>(N.s3) + r * N.s3_ld;
-      uint32_t u[8];
+      uint32_t v[8];
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        u[e] = (uint32_t)(c3a[e] < 0 ? c3a[e] + p : c3a[e]);
-        u[4 + e] = (uint32_t)(c3b[e] < 0 ? c3b[e] + p : c3b[e]);
+        v[e] = wrap_lo(u3a[e] - (uint32_t)h);
+        v[4 + e] = wrap_lo(u3b[e] - (uint32_t)h);
       }
-      *reinterpret_cast<uint2 *>(d + c) = make_uint2(u[0] | (u[1] << 16), u[2] | (u[3] << 16));
-      *reinterpret_cast<uint2 *>(d + c + h2) = make_uint2(u[4] | (u[5] << 16), u[6] | (u[7] << 16));
+      *reinterpret_cast<uint2 *>(d + c) = make_uint2(v[0] | (v[1] << 16), v[2] | (v[3] << 16));
+      *reinterpret_cast<uint2 *>(d + c + h2) = make_uint2(v[4] | (v[5] << 16), v[6] | (v[7] << 16));
     }
     return;
   }
