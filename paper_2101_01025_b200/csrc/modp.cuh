@@ -31,6 +31,7 @@ inline ModP make_modp(uint32_t p) {
   return m;
 }
 
+__host__ __device__ __forceinline__ uint32_t umin32(uint32_t a, uint32_t b) { return a < b ? a : b; }
 // x mod p for any 32-bit x: q = umulhi(x, mu) underestimates floor(x/p) by at most 1.
 __host__ __device__ __forceinline__ uint32_t mod_u32(uint32_t x, const ModP &m) {
 #ifdef __CUDA_ARCH__
@@ -39,7 +40,7 @@ __host__ __device__ __forceinline__ uint32_t mod_u32(uint32_t x, const ModP &m) 
   uint32_t q = (uint32_t)(((uint64_t)x * m.mu) >> 32);
 #endif
   uint32_t r = x - q * m.p;
-  return r >= m.p ? r - m.p : r;
+  return umin32(r, r - m.p);   // r < 2p: r - p wraps above r unless r >= p
 }
 // signed 32-bit -> [0, p): reduce the two's-complement bits, then remove 2^32 if x < 0
 __host__ __device__ __forceinline__ uint32_t mod_s32(int32_t x, const ModP &m) {
@@ -65,12 +66,14 @@ __host__ __device__ __forceinline__ uint32_t mulmod_w(uint32_t a, uint32_t b, co
 __host__ __device__ __forceinline__ uint32_t mulmod_any(uint32_t a, uint32_t b, const ModP &m) {
   return m.p > 65535u ? mulmod_w(a, b, m) : mulmod(a, b, m);
 }
+// (unsigned-min forms: one VIMNMX instead of a compare and a select)
 __host__ __device__ __forceinline__ uint32_t addmod(uint32_t a, uint32_t b, const ModP &m) {
-  uint32_t s = a + b;
-  return s >= m.p ? s - m.p : s;
+  const uint32_t s = a + b;
+  return umin32(s, s - m.p);
 }
 __host__ __device__ __forceinline__ uint32_t submod(uint32_t a, uint32_t b, const ModP &m) {
-  return a >= b ? a - b : a + m.p - b;
+  const uint32_t d = a - b;
+  return umin32(d, d + m.p);
 }
 // centered representative in [-(p-1)/2, (p-1)/2]
 __host__ __device__ __forceinline__ int32_t centered(uint32_t x, const ModP &m) {
@@ -96,7 +99,6 @@ inline ShoupW make_shoup(uint32_t w, uint32_t p) {
   s.wq = (int32_t)q;
   return s;
 }
-__host__ __device__ __forceinline__ uint32_t umin32(uint32_t a, uint32_t b) { return a < b ? a : b; }
 __host__ __device__ __forceinline__ uint32_t acc_mulred(int32_t x, int32_t wc, int32_t wq, uint32_t part, uint32_t p) {
 #ifdef __CUDA_ARCH__
   const int32_t q = __mulhi(x, wq);

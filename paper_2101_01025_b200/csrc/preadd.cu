@@ -639,7 +639,7 @@ __global__ void __launch_bounds__(256) split_kernel(const __grid_constant__ Spli
 // Plain split (mode 0): one thread per (row, 16 columns), four 16-byte loads in flight before
 // the 16-byte limb-plane stores.
 template <int SCHEME>
-__global__ void __launch_bounds__(256) split_plain_kernel(const __grid_constant__ SplitParams P) {
+__global__ void __launch_bounds__(256, 6) split_plain_kernel(const __grid_constant__ SplitParams P) {
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= P.kpad / 16) return;
   const int64_t c0 = g * 16;

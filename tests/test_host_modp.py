@@ -53,3 +53,38 @@ def test_acc_mulred_exact(prog):
     assert len(out) == len(cases)
     for (p, w, x, part), got in zip(cases, out):
         assert int(got) == (part + x * w) % p, (p, w, x, part, got)
+
+
+PROG2 = r"""
+#include <cstdio>
+#include "modp.cuh"
+using namespace adj;
+int main() {
+  unsigned p, a, b, x;
+  while (scanf("%u %u %u %u", &p, &a, &b, &x) == 4) {
+    ModP m = make_modp(p);
+    printf("%u %u %u %u\n", addmod(a, b, m), submod(a, b, m), mod_u32(x, m), mulmod_any(a, b, m));
+  }
+  return 0;
+}
+"""
+
+
+def test_add_sub_mod_exact(tmp_path):
+    """addmod / submod / mod_u32 / mulmod_any (unsigned-min forms) against exact integers: residue
+    extremes, every 32-bit extreme for the reduction, random values, at the limb-scheme primes."""
+    src, exe = tmp_path / "t2.cpp", tmp_path / "t2"
+    src.write_text(PROG2)
+    subprocess.run(["g++", "-O2", "-std=c++17", "-I", CSRC, str(src), "-o", str(exe)], check=True)
+    rng = random.Random(11)
+    cases = []
+    for p in PRIMES:
+        res = sorted({0, 1, p - 1, p - 2, (p - 1) // 2, (p + 1) // 2} | {rng.randrange(p) for _ in range(12)})
+        xs = [0, 1, p - 1, p, p + 1, 2 * p - 1, 2 * p, 2**32 - 1, 2**32 - p, 2**31] + [rng.randrange(2**32) for _ in range(8)]
+        for a in res:
+            for b in res:
+                cases.append((p, a, b, xs[(a + b) % len(xs)]))
+    inp = "".join(f"{p} {a} {b} {x}\n" for p, a, b, x in cases)
+    out = subprocess.run([str(exe)], input=inp, capture_output=True, text=True, check=True).stdout.split("\n")
+    for (p, a, b, x), line in zip(cases, out):
+        assert list(map(int, line.split())) == [(a + b) % p, (a - b) % p, x % p, a * b % p], (p, a, b, x, line)
