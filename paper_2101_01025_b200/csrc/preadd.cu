@@ -725,7 +725,7 @@ cudaError_t launch_split(const SplitParams &p, cudaStream_t s) {
 //   re - im of the right factor).
 // One thread per (row, 4 consecutive columns) of the (mh x kh) quadrants.
 template <int SCHEME>
-__global__ void __launch_bounds__(256) herk_preadd_kernel(const __grid_constant__ HerkPreParams P) {
+__global__ void __launch_bounds__(256, 4) herk_preadd_kernel(const __grid_constant__ HerkPreParams P) {
   constexpr int NP = SCHEME == 0 ? 1 : (SCHEME == 1 ? 3 : (SCHEME == 2 ? 2 : 6));
   constexpr bool WIDE = SCHEME == 3;
   const int64_t g_main = P.kh / 4;
