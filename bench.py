@@ -316,7 +316,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
         depth = min(depth, 1)
     # residues of A and Low(C) live in HBM as uint16 when phi = T and p < 2^16 (ADJ_IN_U16 |
     # ADJ_OUT_U16; exact, the same arithmetic), else uint32.  --io u32 forces uint32.
-    io16 = (args.io == "u16" or (args.io == "auto" and cfg["phi"] == "T" and p < 65536 and world == 1))
+    io16 = (world == 1 and cfg["phi"] == "T" and p < 65536 and args.io in ("auto", "u16"))   # N > 1: uint32
     if io16:
         flags |= adj.ADJ_IN_U16 | adj.ADJ_OUT_U16
     A32 = torch.empty((m, k * w), dtype=torch.int32, device=dev)
