@@ -316,14 +316,17 @@ def run_gpu(args, cfg, rank, world, local_rank):
         depth = min(depth, 1)
     # residues of A and Low(C) live in HBM as uint16 when phi = T and p < 2^16 (ADJ_IN_U16 |
     # ADJ_OUT_U16; exact, the same arithmetic), else uint32.  --io u32 forces uint32.
-    io16 = (world == 1 and cfg["phi"] == "T" and p < 65536 and args.io in ("auto", "u16"))   # N > 1: uint32
-    if io16:
+    # (N > 1: uint16 A, uint32 Low(C) on the root -- the distributed entry point reads ADJ_IN_U16)
+    io16 = cfg["phi"] == "T" and p < 65536 and args.io in ("auto", "u16")
+    if io16 and world == 1:
         flags |= adj.ADJ_IN_U16 | adj.ADJ_OUT_U16
+    elif io16:
+        dist_flags |= adj.ADJ_IN_U16
     A32 = torch.empty((m, k * w), dtype=torch.int32, device=dev)
     uniform_residues_cuda(A32, seed=1, p=p)
     A = A32.to(torch.int16) if io16 else A32
     del A32
-    C = torch.zeros((m, m * w), dtype=torch.int16 if io16 else torch.int32, device=dev)
+    C = torch.zeros((m, m * w), dtype=torch.int16 if io16 and world == 1 else torch.int32, device=dev)
 
     def u32(t):
         """the residues of a device tensor as an int32 tensor (uint16 storage zero-extended)"""
@@ -489,7 +492,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
         # device time per rank, max over ranks
         try:
             e2e_steps = max(3, min(args.steps, 8))
-            hA = torch.empty((m, k * w), dtype=torch.int32, pin_memory=True) if rank == 0 else None
+            hA = torch.empty((m, k * w), dtype=A.dtype, pin_memory=True) if rank == 0 else None
             if rank == 0:
                 hA.copy_(A)
             hC = torch.empty((m, m * w), dtype=torch.int32, pin_memory=True) if rank == 0 else None
@@ -517,9 +520,10 @@ def run_gpu(args, cfg, rank, world, local_rank):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_ms = float(t.item())
             e2e = {"value": m * m * k / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms,
-                   "h2d_bytes_per_step": m * k * w * 4, "d2h_bytes_per_step": d2h_bytes, "steps": e2e_steps,
-                   "io": "uint32 residues; A from pinned host memory on rank 0, NCCL broadcast, Low(C) read "
-                         "back on rank 0 (SURVEY.md §8(e) 'A on rank 0')"}
+                   "h2d_bytes_per_step": m * k * w * A.element_size(), "d2h_bytes_per_step": d2h_bytes,
+                   "steps": e2e_steps,
+                   "io": f"A as {'uint16' if A.element_size() == 2 else 'uint32'} from pinned host memory on rank 0, "
+                         "NCCL broadcast, uint32 Low(C) read back on rank 0 (SURVEY.md §8(e) 'A on rank 0')"}
         except Exception as ex:  # noqa: BLE001 -- the device-resident line above stands without it
             e2e = {"error": f"{type(ex).__name__}: {ex}"}
 
@@ -635,7 +639,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
             "leaf_launches_per_step": leaf_n / args.steps}
     share = {c: round(v[0] / max(1e-9, sum(x[0] for x in prof.values())), 4) for c, v in prof.items()}
     # achieved HBM bandwidth of the HBM-bound kernels (algorithmic bytes / device time per step)
-    hb = hbm_bytes(cfg, depth, args.herk, 2 if io16 else 4)
+    hb = hbm_bytes(cfg, depth, args.herk, 2 if io16 and world == 1 else 4)
     hbm = None
     if hb is not None:
         hbm = {}
@@ -663,7 +667,8 @@ def run_gpu(args, cfg, rank, world, local_rank):
             "config": {"workload": cfg["workload"] + (" via Alg. 1 over GF(p^2) (ADJ_HERK_ALG1)" if alg1 else ""),
                        "m": m, "k": k, "p": p, "phi": cfg["phi"], "depth": depth,
                        "seed": 1, "l2": "flushed before every timed step (256 MiB write, outside step events)",
-                       "residues": ("uint16 A and Low(C) in HBM (ADJ_IN_U16 | ADJ_OUT_U16)" if io16
+                       "residues": ("uint16 A and Low(C) in HBM (ADJ_IN_U16 | ADJ_OUT_U16)" if io16 and world == 1
+                                    else "uint16 A (ADJ_IN_U16), uint32 Low(C) on the root" if io16
                                     else "uint32 A and Low(C) in HBM"),
                        "parallelism": ("1 GPU" if world == 1 else
                                        (f"output tiles x{world} (NCCL send/recv gather of result tiles)"

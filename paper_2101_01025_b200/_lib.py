@@ -192,14 +192,14 @@ def adjprod_modp_dist(m, k, p, phi, A, lda, C, ldc, root, comm, depth=-1, flags=
 
 
 def adjprod_modp_shard(m, k, p, phi, A, lda, C, ldc, rank, nranks, depth=-1, workspace=None, workspace_bytes=0,
-                       stream=None):
-    o = _opts(depth, 0, workspace, workspace_bytes)
+                       stream=None, flags=0):
+    o = _opts(depth, flags, workspace, workspace_bytes)
     _check(lib().adjprod_modp_shard(m, k, p, phi, _ptr(A), lda, _ptr(C), ldc, rank, nranks, ctypes.byref(o),
                                     _stream(stream)), "adjprod_modp_shard")
 
 
-def adjprod_modp_partial(m, k, p, phi, A, lda, R, ldr, depth=-1, stream=None):
-    o = _opts(depth)
+def adjprod_modp_partial(m, k, p, phi, A, lda, R, ldr, depth=-1, stream=None, flags=0):
+    o = _opts(depth, flags)
     _check(lib().adjprod_modp_partial(m, k, p, phi, _ptr(A), lda, _ptr(R), ldr, ctypes.byref(o), _stream(stream)),
            "adjprod_modp_partial")
 

@@ -744,13 +744,14 @@ static int shard_depth(int64_t m, int64_t k, uint32_t p, const adj_opts_t *opts)
 adj_status_t adjprod_modp_shard(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, const uint32_t *A, int64_t lda,
                                 uint32_t *C, int64_t ldc, int rank, int nranks, const adj_opts_t *opts,
                                 adj_stream_t stream) {
-  adj_status_t st = validate_syrk(m, k, p, phi, A, lda, C, ldc);
+  const uint32_t flags = opts ? opts->flags : 0;
+  adj_status_t st = validate_syrk(m, k, p, phi, A, lda, C, ldc, flags & ADJ_IN_U16);
   if (st != ADJ_OK) return st;
   if (phi != ADJ_PHI_T) return fail(ADJ_ERR_INVALID_VALUE, "output-tile sharding supports phi = ADJ_PHI_T");
   if (nranks < 1 || rank < 0 || rank >= nranks) return fail(ADJ_ERR_INVALID_VALUE, "rank %d of %d", rank, nranks);
-  if (opts && (opts->flags & ADJ_FILL_UPPER)) return fail(ADJ_ERR_INVALID_VALUE, "ADJ_FILL_UPPER with sharding");
-  if (opts && (opts->flags & (ADJ_IN_U16 | ADJ_OUT_U16)))
-    return fail(ADJ_ERR_INVALID_VALUE, "ADJ_IN_U16 / ADJ_OUT_U16 are adjprod_modp_ex flags");
+  if (flags & ADJ_FILL_UPPER) return fail(ADJ_ERR_INVALID_VALUE, "ADJ_FILL_UPPER with sharding");
+  if (flags & ADJ_OUT_U16) return fail(ADJ_ERR_INVALID_VALUE, "ADJ_OUT_U16 is an adjprod_modp_ex flag");
+  if ((flags & ADJ_IN_U16) && p > 65535) return fail(ADJ_ERR_INVALID_VALUE, "ADJ_IN_U16 needs p < 2^16");
   if (m == 0) return ADJ_OK;
   const int depth = shard_depth(m, k, p, opts);
   if (depth > 1) return fail(ADJ_ERR_INVALID_VALUE, "output-tile sharding runs at depth 0 or 1 (got %d)", depth);
@@ -774,6 +775,7 @@ adj_status_t adjprod_modp_shard(int64_t m, int64_t k, uint32_t p, adj_phi_t phi,
   }
   Ptrs x;
   x.A = A; x.lda = lda; x.C = C; x.ldc = ldc;
+  x.in16 = (flags & ADJ_IN_U16) != 0;
   void *ws = opts ? opts->workspace : nullptr;
   bool own = false;
   if (ws == nullptr) {
@@ -793,11 +795,12 @@ adj_status_t adjprod_modp_shard(int64_t m, int64_t k, uint32_t p, adj_phi_t phi,
 
 adj_status_t adjprod_modp_partial(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, const uint32_t *A, int64_t lda,
                                   void *R, int64_t ldr, const adj_opts_t *opts, adj_stream_t stream) {
-  adj_status_t st = validate_syrk(m, k, p, phi, A, lda, static_cast<const uint32_t *>(R), ldr);
+  const uint32_t flags = opts ? opts->flags : 0;
+  adj_status_t st = validate_syrk(m, k, p, phi, A, lda, static_cast<const uint32_t *>(R), ldr, flags & ADJ_IN_U16);
   if (st != ADJ_OK) return st;
   if (phi != ADJ_PHI_T) return fail(ADJ_ERR_INVALID_VALUE, "adjprod_modp_partial supports phi = ADJ_PHI_T");
-  if (opts && (opts->flags & (ADJ_IN_U16 | ADJ_OUT_U16)))
-    return fail(ADJ_ERR_INVALID_VALUE, "ADJ_IN_U16 / ADJ_OUT_U16 are adjprod_modp_ex flags");
+  if (flags & ADJ_OUT_U16) return fail(ADJ_ERR_INVALID_VALUE, "ADJ_OUT_U16 is an adjprod_modp_ex flag");
+  if ((flags & ADJ_IN_U16) && p > 65535) return fail(ADJ_ERR_INVALID_VALUE, "ADJ_IN_U16 needs p < 2^16");
   if (m == 0) return ADJ_OK;
   if (p > 65535) {   // residues need 32 bits: the ordinary call writes them
     adj_opts_t o = opts ? *opts : adj_opts_t{-1, 0, nullptr, 0};
@@ -820,6 +823,7 @@ adj_status_t adjprod_modp_partial(int64_t m, int64_t k, uint32_t p, adj_phi_t ph
   x.A = A; x.lda = lda;
   x.C = static_cast<uint32_t *>(R); x.ldc = ldr;
   x.res16 = true;
+  x.in16 = (flags & ADJ_IN_U16) != 0;
   void *ws = opts ? opts->workspace : nullptr;
   bool own = false;
   if (ws == nullptr) {

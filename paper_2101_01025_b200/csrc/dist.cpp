@@ -220,8 +220,10 @@ adj_status_t dist_p2p(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, const uin
   adj_dist_kslice(k, G, r, &k0, &k1);
   void *mine = static_cast<uint8_t *>(comm->win) + (size_t)r * slot * esize;
   adj_opts_t o = opts ? *opts : adj_opts_t{-1, 0, nullptr, 0};
-  o.flags = 0;
-  st = adjprod_modp_partial(m, k1 - k0, p, phi, A ? A + k0 : nullptr, lda, mine, m, &o, stream);
+  o.flags &= ADJ_IN_U16;
+  const size_t ea = (o.flags & ADJ_IN_U16) ? 2 : 4;   // bytes per element of A
+  const uint32_t *Ar = A ? reinterpret_cast<const uint32_t *>(reinterpret_cast<const uint8_t *>(A) + k0 * ea) : nullptr;
+  st = adjprod_modp_partial(m, k1 - k0, p, phi, Ar, lda, mine, m, &o, stream);
   if (st != ADJ_OK) return st;
   // barrier 2: every rank's partial kernels (and their peer stores) have completed
   if (g_nccl.AllReduce(comm->d_scratch, comm->d_scratch, 1, ncclInt32, ncclSum, comm->comm, s) != ncclSuccess)
@@ -284,7 +286,7 @@ adj_status_t adjprod_modp_dist(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, 
                                adj_stream_t stream) {
   if (!comm || root < 0 || root >= comm->nranks) return ADJ_ERR_INVALID_VALUE;
   if (m < 0 || k < 0) return ADJ_ERR_INVALID_VALUE;
-  if (opts && (opts->flags & (ADJ_IN_U16 | ADJ_OUT_U16))) return ADJ_ERR_INVALID_VALUE;
+  if (opts && (opts->flags & ADJ_OUT_U16)) return ADJ_ERR_INVALID_VALUE;   // Low(C) on the root is uint32
   if (m == 0) return ADJ_OK;
   const int G = comm->nranks, r = comm->rank;
   if (opts && (opts->flags & ADJ_DIST_TILES)) return dist_tiles(m, k, p, phi, A, lda, C, ldc, root, comm, opts, stream);
@@ -293,7 +295,8 @@ adj_status_t adjprod_modp_dist(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, 
   const int w = adj_phi_width(phi);
   int64_t k0 = 0, k1 = 0;
   adj_dist_kslice(k, G, r, &k0, &k1);
-  const uint32_t *Ar = A ? A + k0 * w : nullptr;
+  const size_t ea = (opts && (opts->flags & ADJ_IN_U16)) ? 2 : 4 * (size_t)w;   // bytes per element of A
+  const uint32_t *Ar = A ? reinterpret_cast<const uint32_t *>(reinterpret_cast<const uint8_t *>(A) + k0 * ea) : nullptr;
   if (G == 1) return adjprod_modp_ex(m, k1 - k0, p, phi, Ar, lda, C, ldc, opts, stream);
   if (!load_nccl()) return ADJ_ERR_NCCL;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);

@@ -602,3 +602,50 @@ def test_adjprod_T_compact_io_strided_and_errors(adj):
         adj.adjprod_modp_ex(m, k // 2, p, adj.ADJ_PHI_H, dA, (k + 12) // 2, C32, m // 2, flags=adj.ADJ_IN_U16)
     with pytest.raises(adj.AdjError):   # SYRK form with a uint16 Low(C)
         adj.adjprod_modp_syrk(m, k, p, adj.ADJ_PHI_T, 3, dA, k + 12, 1, out, m + 20, flags=adj.ADJ_OUT_U16)
+
+
+# ---------------------------------------------------------------- ADJ_IN_U16 on the multi-GPU paths
+@pytest.mark.parametrize("p", [251, 8191, 65521])
+@pytest.mark.parametrize("depth", [0, 1])
+def test_compact_input_shards_and_partials(adj, p, depth):
+    """uint16 A (any value, read mod p) through adjprod_modp_shard (3 ranks' shares into one C)
+    and adjprod_modp_partial on the k-slices (+ adj_sum_partials), each rank after the other."""
+    import torch
+    m, k = 700, 900
+    rng = np.random.default_rng(p + depth)
+    A16 = rng.integers(0, 1 << 16, size=(m, k), dtype=np.uint16)
+    ref = oracle.syrk_t((A16.astype(np.uint32) % p).astype(np.uint32), p)
+    dA = torch.from_numpy(A16.view(np.int16)).cuda()
+    C = torch.zeros((m, m), dtype=torch.int32, device="cuda")
+    for r in range(3):
+        adj.adjprod_modp_shard(m, k, p, 0, dA, k, C, m, r, 3, depth=depth, flags=adj.ADJ_IN_U16)
+    assert np.array_equal(low(to_host(C)), ref)
+    G = 3
+    R = torch.zeros((G, m, m), dtype=torch.int16, device="cuda")
+    for r in range(G):
+        k0, k1 = adj.adj_dist_kslice(k, G, r)
+        adj.adjprod_modp_partial(m, k1 - k0, p, 0, dA[:, k0:], k, R[r], m, depth=depth, flags=adj.ADJ_IN_U16)
+    C2 = torch.zeros((m, m), dtype=torch.int32, device="cuda")
+    adj.adj_sum_partials(m, p, R, m, m * m, G, C2, m)
+    assert np.array_equal(low(to_host(C2)), ref)
+
+
+@pytest.mark.parametrize("flags_name", ["", "ADJ_DIST_TILES", "ADJ_DIST_P2P"])
+def test_compact_input_dist_single_rank(adj, flags_name):
+    import torch
+    p, m, k = 8191, 600, 500
+    rng = np.random.default_rng(3)
+    A16 = rng.integers(0, 1 << 16, size=(m, k), dtype=np.uint16)
+    ref = oracle.syrk_t((A16.astype(np.uint32) % p).astype(np.uint32), p)
+    comm = adj.adj_comm_init(1, adj.adj_comm_get_unique_id(), 0)
+    try:
+        C = torch.zeros((m, m), dtype=torch.int32, device="cuda")
+        flags = adj.ADJ_IN_U16 | (getattr(adj, flags_name) if flags_name else 0)
+        adj.adjprod_modp_dist(m, k, p, 0, torch.from_numpy(A16.view(np.int16)).cuda(), k, C, m, 0, comm,
+                              depth=1, flags=flags)
+        assert np.array_equal(low(to_host(C)), ref)
+        with pytest.raises(adj.AdjError):
+            adj.adjprod_modp_dist(m, k, p, 0, torch.from_numpy(A16.view(np.int16)).cuda(), k, C, m, 0, comm,
+                                  depth=1, flags=adj.ADJ_OUT_U16)
+    finally:
+        adj.adj_comm_destroy(comm)
