@@ -40,6 +40,8 @@ CONFIGS = {
                  workload="x16k (dev): A 16384x16384 over GF(8191)"),
     "x131071": dict(m=8192, k=8192, p=131071, phi="T", depth=None,
                     workload="x131071 (dev): A 8192x8192 over GF(131071), the paper's modulus (PAPER.md:2237)"),
+    "x131071_32k": dict(m=32768, k=32768, p=131071, phi="T", depth=None,
+                        workload="x131071_32k (dev): A 32768x32768 over GF(131071), the paper's modulus at c3 size"),
     "x65521": dict(m=8192, k=8192, p=65521, phi="T", depth=None,
                    workload="x65521 (dev): A 8192x8192 over GF(65521)"),
     "x251": dict(m=8192, k=8192, p=251, phi="T", depth=None,
