@@ -130,11 +130,11 @@ __device__ __forceinline__ void limbs4(const uint32_t (&x)[4], const ModP &m, ui
 // non-negative, so the digits are its bit fields e0, e1, e2 minus 32.  The fields are packed as
 // bytes; d = e - 32 is the byte (e + 96) ^ 128 and d + d' = e + e' - 64 the byte
 // (e + e' + 64) ^ 128 (no byte exceeds 255, so the packed adds carry nothing between bytes).
-__device__ __forceinline__ void t6_words(const uint32_t (&x)[4], const ModP &m, uint32_t (&w)[6]) {
+__device__ __forceinline__ void t6_words_v(const uint32_t (&vv)[4], uint32_t (&w)[6]) {
   uint32_t e0[4], e1[4], e2[4];
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
-    const uint32_t v = (uint32_t)(centered(x[e], m) + 133152);
+    const uint32_t v = vv[e];
     e0[e] = v & 63u;
     e1[e] = (v >> 6) & 63u;
     e2[e] = v >> 12;
@@ -148,6 +148,22 @@ __device__ __forceinline__ void t6_words(const uint32_t (&x)[4], const ModP &m, 
   w[3] = (E2 + E1 + 0x40404040u) ^ 0x80808080u;   // d2 + d1
   w[4] = (E1 + E0 + 0x40404040u) ^ 0x80808080u;   // d1 + d0
   w[5] = (E2 + E0 + 0x40404040u) ^ 0x80808080u;   // d2 + d0
+}
+
+__device__ __forceinline__ void t6_words(const uint32_t (&x)[4], const ModP &m, uint32_t (&w)[6]) {
+  const uint32_t v[4] = {(uint32_t)(centered(x[0], m) + 133152), (uint32_t)(centered(x[1], m) + 133152),
+                         (uint32_t)(centered(x[2], m) + 133152), (uint32_t)(centered(x[3], m) + 133152)};
+  t6_words_v(v, w);
+}
+
+// the six planes of 4 offset residues u = c + (p - 1) / 2: v = u + off, off = 133152 - (p - 1) / 2
+__device__ __forceinline__ void put_limbs4_t6u(int8_t *base, int64_t plane_stride, const uint32_t (&u)[4],
+                                               uint32_t off) {
+  const uint32_t v[4] = {u[0] + off, u[1] + off, u[2] + off, u[3] + off};
+  uint32_t w[6];
+  t6_words_v(v, w);
+#pragma unroll
+  for (int pl = 0; pl < 6; ++pl) *reinterpret_cast<uint32_t *>(base + pl * plane_stride) = w[pl];
 }
 
 __device__ __forceinline__ void put_limbs4_t6(int8_t *base, int64_t plane_stride, const uint32_t (&x)[4],
@@ -395,20 +411,26 @@ __device__ __forceinline__ void preadd_row(const PreParams &P, const PreNode &N,
     load4(vv, P.mh + r, P.kh + c, m, x22a);
     load4(vv, P.mh + r, P.kh + c + h2, m, x22b);
   }
-  if constexpr (SCHEME == 1) {
-    // Lazy reduction (p <= 16763 so 2 p^2 < 2^31): Y products in raw int32, one reduction per S
-    // output.  Residues are carried as offset values u = c + h in [0, p) of the centered c
-    // (h = (p - 1) / 2), so every correction is an unsigned min of u, u - p, u + p.
+  if constexpr (SCHEME == 1 || SCHEME == 3) {
+    // Lazy reduction: Y products unreduced, one reduction per S output.  Residues are carried as
+    // offset values u = c + h in [0, p) of the centered c (h = (p - 1) / 2), so every correction
+    // is an unsigned min of u, u - p, u + p.  SCHEME 1 (p <= 16763, 2 p^2 < 2^31): exact int32
+    // products.  SCHEME 3 (p < 2^18): the products' sum v (|v| < 2^37) is known exactly mod 2^32
+    // and to ~2^13 in float; the float quotient estimate is within 0.63 of v / p, so the remainder
+    // v - q p, a value below 2^19 in magnitude, is exact in wrapping 32-bit arithmetic.
     const int32_t p = (int32_t)m.p, h = (int32_t)m.half;
     const uint32_t up = m.p;
     const float invp = 1.0f / (float)m.p;
     const int32_t ya = (int32_t)P.ya, yb = (int32_t)P.yb;
-    // v + h - q p with the float quotient estimate q (error < 0.2): in [-0.2 p, 1.2 p)
-    auto off_lazy = [&](int32_t v) -> uint32_t {
-      const int32_t q = __float2int_rn(__int2float_rn(v) * invp);
-      const uint32_t u = (uint32_t)(v + h - q * p);
+    // v + h - q p with the float quotient estimate q of v / p (v exact mod 2^32, vf its float
+    // value): in [-0.63 p, 1.63 p)
+    auto off_lazy2 = [&](int32_t v, float vf) -> uint32_t {
+      const int32_t q = __float2int_rn(vf * invp);
+      const uint32_t u = (uint32_t)v + (uint32_t)h - (uint32_t)q * up;
       return umin32(umin32(u, u - up), u + up);
     };
+    auto off_lazy = [&](int32_t v) -> uint32_t { return off_lazy2(v, __int2float_rn(v)); };
+    const float yaf = (float)ya, ybf = (float)yb;
     auto wrap_lo = [&](uint32_t u) { return umin32(u, u + up); };   // u in (-p, p)
     auto wrap_hi = [&](uint32_t u) { return umin32(u, u - up); };   // u in [0, 2p)
     uint32_t u1a[4], u1b[4], u2a[4], u2b[4], u3a[4], u3b[4], u4a[4], u4b[4];
@@ -416,17 +438,33 @@ __device__ __forceinline__ void preadd_row(const PreParams &P, const PreNode &N,
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const int32_t d1 = (int32_t)x21a[e] - (int32_t)x11a[e], d2 = (int32_t)x21b[e] - (int32_t)x11b[e];
+      // unsigned (wrapping) arithmetic: SCHEME 1 values fit int32, SCHEME 3 uses them mod 2^32
+      const uint32_t uya = (uint32_t)ya, uyb = (uint32_t)yb, ud1 = (uint32_t)d1, ud2 = (uint32_t)d2;
       int32_t s1r_a, s1r_b, tr_a, tr_b;
       if constexpr (YK == 0) {
-        s1r_a = ya * d1; s1r_b = ya * d2;
-        tr_a = ya * (int32_t)x21a[e]; tr_b = ya * (int32_t)x21b[e];
+        s1r_a = (int32_t)(uya * ud1); s1r_b = (int32_t)(uya * ud2);
+        tr_a = (int32_t)(uya * x21a[e]); tr_b = (int32_t)(uya * x21b[e]);
       } else {
-        s1r_a = ya * d1 - yb * d2; s1r_b = yb * d1 + ya * d2;                         // (A21 - A11) Y
-        tr_a = ya * (int32_t)x21a[e] - yb * (int32_t)x21b[e];                          // A21 Y
-        tr_b = yb * (int32_t)x21a[e] + ya * (int32_t)x21b[e];
+        s1r_a = (int32_t)(uya * ud1 - uyb * ud2); s1r_b = (int32_t)(uyb * ud1 + uya * ud2);   // (A21 - A11) Y
+        tr_a = (int32_t)(uya * x21a[e] - uyb * x21b[e]);                                     // A21 Y
+        tr_b = (int32_t)(uyb * x21a[e] + uya * x21b[e]);
       }
-      u1a[e] = off_lazy(s1r_a); u1b[e] = off_lazy(s1r_b);                                           // S1
-      u2a[e] = off_lazy((int32_t)x22a[e] - tr_a); u2b[e] = off_lazy((int32_t)x22b[e] - tr_b);       // S2
+      if constexpr (SCHEME == 1) {
+        u1a[e] = off_lazy(s1r_a); u1b[e] = off_lazy(s1r_b);                                         // S1
+        u2a[e] = off_lazy((int32_t)x22a[e] - tr_a); u2b[e] = off_lazy((int32_t)x22b[e] - tr_b);     // S2
+      } else {
+        const float d1f = (float)d1, d2f = (float)d2, x21af = (float)x21a[e], x21bf = (float)x21b[e];
+        float s1f_a, s1f_b, trf_a, trf_b;
+        if constexpr (YK == 0) {
+          s1f_a = yaf * d1f; s1f_b = yaf * d2f; trf_a = yaf * x21af; trf_b = yaf * x21bf;
+        } else {
+          s1f_a = fmaf(yaf, d1f, -(ybf * d2f)); s1f_b = fmaf(ybf, d1f, yaf * d2f);
+          trf_a = fmaf(yaf, x21af, -(ybf * x21bf)); trf_b = fmaf(ybf, x21af, yaf * x21bf);
+        }
+        u1a[e] = off_lazy2(s1r_a, s1f_a); u1b[e] = off_lazy2(s1r_b, s1f_b);                         // S1
+        u2a[e] = off_lazy2((int32_t)(x22a[e] - (uint32_t)tr_a), (float)x22a[e] - trf_a);             // S2
+        u2b[e] = off_lazy2((int32_t)(x22b[e] - (uint32_t)tr_b), (float)x22b[e] - trf_b);
+      }
       u3a[e] = wrap_lo(u1a[e] - x22a[e]); u3b[e] = wrap_lo(u1b[e] - x22b[e]);                       // S3
       u4a[e] = wrap_hi(u3a[e] + x12a[e]); u4b[e] = wrap_hi(u3b[e] + x12b[e]);                       // S4
       u11a[e] = wrap_hi(x11a[e] + h); u11b[e] = wrap_hi(x11b[e] + h);
@@ -434,12 +472,17 @@ __device__ __forceinline__ void preadd_row(const PreParams &P, const PreNode &N,
       u22a[e] = wrap_hi(x22a[e] + h); u22b[e] = wrap_hi(x22b[e] + h);
     }
     const int64_t ps = P.rows_pad * P.kpad;
-    const uint32_t koff = 64u + 128u * 66u - (uint32_t)h;
+    const uint32_t koff = SCHEME == 1 ? 64u + 128u * 66u - (uint32_t)h : 133152u - (uint32_t)h;
 #define PUTC(o, A, B)                                                                  \
   if (N.op_row[o] >= 0) {                                                              \
     int8_t *b = P.arena + (N.op_row[o] + r) * P.kpad;                                  \
-    put_limbs4_k7u(b + c, ps, A, koff);                                                \
-    put_limbs4_k7u(b + c + h2, ps, B, koff);                                           \
+    if constexpr (SCHEME == 1) {                                                       \
+      put_limbs4_k7u(b + c, ps, A, koff);                                              \
+      put_limbs4_k7u(b + c + h2, ps, B, koff);                                         \
+    } else {                                                                           \
+      put_limbs4_t6u(b + c, ps, A, koff);                                              \
+      put_limbs4_t6u(b + c + h2, ps, B, koff);                                         \
+    }                                                                                  \
   }
     PUTC(OUT_S1, u1a, u1b)
     PUTC(OUT_S2, u2a, u2b)
@@ -449,7 +492,13 @@ __device__ __forceinline__ void preadd_row(const PreParams &P, const PreNode &N,
     PUTC(OUT_X12, u12a, u12b)
     PUTC(OUT_S3, u3a, u3b)
 #undef PUTC
-    if (N.s3 != nullptr && r < P.mh) {   // canonical S3 = (u3 - h) mod p for the next level
+    if (SCHEME == 3 && N.s3 != nullptr && r < P.mh) {   // canonical uint32 S3 for the next level
+      uint32_t *d = static_cast<uint32_t *>(N.s3) + r * N.s3_ld;
+      *reinterpret_cast<uint4 *>(d + c) = make_uint4(wrap_lo(u3a[0] - (uint32_t)h), wrap_lo(u3a[1] - (uint32_t)h),
+                                                     wrap_lo(u3a[2] - (uint32_t)h), wrap_lo(u3a[3] - (uint32_t)h));
+      *reinterpret_cast<uint4 *>(d + c + h2) = make_uint4(wrap_lo(u3b[0] - (uint32_t)h), wrap_lo(u3b[1] - (uint32_t)h),
+                                                          wrap_lo(u3b[2] - (uint32_t)h), wrap_lo(u3b[3] - (uint32_t)h));
+    } else if (N.s3 != nullptr && r < P.mh) {   // canonical S3 = (u3 - h) mod p for the next level
       uint16_t *d = static_cast<uint16_t *>(N.s3) + r * N.s3_ld;
       uint32_t v[8];
 #pragma unroll
