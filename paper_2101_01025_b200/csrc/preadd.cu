@@ -156,6 +156,15 @@ __device__ __forceinline__ void t6_words(const uint32_t (&x)[4], const ModP &m, 
   t6_words_v(v, w);
 }
 
+// s8 hi / u8 lo planes of 4 offset residues u = c + (p - 1) / 2 (bytes 1 and 0 of c = u - h)
+__device__ __forceinline__ void put_limbs4_s8u8u(int8_t *base, int64_t plane_stride, const uint32_t (&u)[4],
+                                                 uint32_t h) {
+  const uint32_t c0 = u[0] - h, c1 = u[1] - h, c2 = u[2] - h, c3 = u[3] - h;
+  *reinterpret_cast<uint32_t *>(base) = __byte_perm(__byte_perm(c0, c1, 0x51), __byte_perm(c2, c3, 0x51), 0x5410);
+  *reinterpret_cast<uint32_t *>(base + plane_stride) =
+      __byte_perm(__byte_perm(c0, c1, 0x40), __byte_perm(c2, c3, 0x40), 0x5410);
+}
+
 // the six planes of 4 offset residues u = c + (p - 1) / 2: v = u + off, off = 133152 - (p - 1) / 2
 __device__ __forceinline__ void put_limbs4_t6u(int8_t *base, int64_t plane_stride, const uint32_t (&u)[4],
                                                uint32_t off) {
@@ -411,11 +420,11 @@ __device__ __forceinline__ void preadd_row(const PreParams &P, const PreNode &N,
     load4(vv, P.mh + r, P.kh + c, m, x22a);
     load4(vv, P.mh + r, P.kh + c + h2, m, x22b);
   }
-  if constexpr (SCHEME == 1 || SCHEME == 3) {
+  if constexpr (SCHEME == 1 || SCHEME == 2 || SCHEME == 3) {
     // Lazy reduction: Y products unreduced, one reduction per S output.  Residues are carried as
     // offset values u = c + h in [0, p) of the centered c (h = (p - 1) / 2), so every correction
     // is an unsigned min of u, u - p, u + p.  SCHEME 1 (p <= 16763, 2 p^2 < 2^31): exact int32
-    // products.  SCHEME 3 (p < 2^18): the products' sum v (|v| < 2^37) is known exactly mod 2^32
+    // products.  SCHEMES 2 / 3 (p < 2^18): the products' sum v (|v| < 2^37) is known exactly mod 2^32
     // and to ~2^13 in float; the float quotient estimate is within 0.63 of v / p, so the remainder
     // v - q p, a value below 2^19 in magnitude, is exact in wrapping 32-bit arithmetic.
     const int32_t p = (int32_t)m.p, h = (int32_t)m.half;
@@ -472,13 +481,17 @@ __device__ __forceinline__ void preadd_row(const PreParams &P, const PreNode &N,
       u22a[e] = wrap_hi(x22a[e] + h); u22b[e] = wrap_hi(x22b[e] + h);
     }
     const int64_t ps = P.rows_pad * P.kpad;
-    const uint32_t koff = SCHEME == 1 ? 64u + 128u * 66u - (uint32_t)h : 133152u - (uint32_t)h;
+    const uint32_t koff = SCHEME == 1 ? 64u + 128u * 66u - (uint32_t)h
+                          : (SCHEME == 3 ? 133152u - (uint32_t)h : (uint32_t)h);
 #define PUTC(o, A, B)                                                                  \
   if (N.op_row[o] >= 0) {                                                              \
     int8_t *b = P.arena + (N.op_row[o] + r) * P.kpad;                                  \
     if constexpr (SCHEME == 1) {                                                       \
       put_limbs4_k7u(b + c, ps, A, koff);                                              \
       put_limbs4_k7u(b + c + h2, ps, B, koff);                                         \
+    } else if constexpr (SCHEME == 2) {                                                \
+      put_limbs4_s8u8u(b + c, ps, A, koff);                                            \
+      put_limbs4_s8u8u(b + c + h2, ps, B, koff);                                       \
     } else {                                                                           \
       put_limbs4_t6u(b + c, ps, A, koff);                                              \
       put_limbs4_t6u(b + c + h2, ps, B, koff);                                         \
