@@ -156,6 +156,12 @@ __device__ __forceinline__ void t6_words(const uint32_t (&x)[4], const ModP &m, 
   t6_words_v(v, w);
 }
 
+// the single s8 plane of 4 offset residues u = c + (p - 1) / 2 (p <= 255: byte 0 of c = u - h)
+__device__ __forceinline__ void put_limbs4_s8u(int8_t *base, const uint32_t (&u)[4], uint32_t h) {
+  *reinterpret_cast<uint32_t *>(base) =
+      __byte_perm(__byte_perm(u[0] - h, u[1] - h, 0x40), __byte_perm(u[2] - h, u[3] - h, 0x40), 0x5410);
+}
+
 // s8 hi / u8 lo planes of 4 offset residues u = c + (p - 1) / 2 (bytes 1 and 0 of c = u - h)
 __device__ __forceinline__ void put_limbs4_s8u8u(int8_t *base, int64_t plane_stride, const uint32_t (&u)[4],
                                                  uint32_t h) {
@@ -420,11 +426,11 @@ __device__ __forceinline__ void preadd_row(const PreParams &P, const PreNode &N,
     load4(vv, P.mh + r, P.kh + c, m, x22a);
     load4(vv, P.mh + r, P.kh + c + h2, m, x22b);
   }
-  if constexpr (SCHEME == 1 || SCHEME == 2 || SCHEME == 3) {
+  {
     // Lazy reduction: Y products unreduced, one reduction per S output.  Residues are carried as
     // offset values u = c + h in [0, p) of the centered c (h = (p - 1) / 2), so every correction
-    // is an unsigned min of u, u - p, u + p.  SCHEME 1 (p <= 16763, 2 p^2 < 2^31): exact int32
-    // products.  SCHEMES 2 / 3 (p < 2^18): the products' sum v (|v| < 2^37) is known exactly mod 2^32
+    // is an unsigned min of u, u - p, u + p.  SCHEMES 0 / 1 (p <= 16763, 2 p^2 < 2^31): exact
+    // int32 products.  SCHEMES 2 / 3 (p < 2^18): the products' sum v (|v| < 2^37) is known exactly mod 2^32
     // and to ~2^13 in float; the float quotient estimate is within 0.63 of v / p, so the remainder
     // v - q p, a value below 2^19 in magnitude, is exact in wrapping 32-bit arithmetic.
     const int32_t p = (int32_t)m.p, h = (int32_t)m.half;
@@ -458,7 +464,7 @@ __device__ __forceinline__ void preadd_row(const PreParams &P, const PreNode &N,
         tr_a = (int32_t)(uya * x21a[e] - uyb * x21b[e]);                                     // A21 Y
         tr_b = (int32_t)(uyb * x21a[e] + uya * x21b[e]);
       }
-      if constexpr (SCHEME == 1) {
+      if constexpr (SCHEME <= 1) {
         u1a[e] = off_lazy(s1r_a); u1b[e] = off_lazy(s1r_b);                                         // S1
         u2a[e] = off_lazy((int32_t)x22a[e] - tr_a); u2b[e] = off_lazy((int32_t)x22b[e] - tr_b);     // S2
       } else {
@@ -482,11 +488,14 @@ __device__ __forceinline__ void preadd_row(const PreParams &P, const PreNode &N,
     }
     const int64_t ps = P.rows_pad * P.kpad;
     const uint32_t koff = SCHEME == 1 ? 64u + 128u * 66u - (uint32_t)h
-                          : (SCHEME == 3 ? 133152u - (uint32_t)h : (uint32_t)h);
+                          : (SCHEME == 3 ? 133152u - (uint32_t)h : (uint32_t)h);   // (0, 2: h)
 #define PUTC(o, A, B)                                                                  \
   if (N.op_row[o] >= 0) {                                                              \
     int8_t *b = P.arena + (N.op_row[o] + r) * P.kpad;                                  \
-    if constexpr (SCHEME == 1) {                                                       \
+    if constexpr (SCHEME == 0) {                                                       \
+      put_limbs4_s8u(b + c, A, koff);                                                  \
+      put_limbs4_s8u(b + c + h2, B, koff);                                             \
+    } else if constexpr (SCHEME == 1) {                                                \
       put_limbs4_k7u(b + c, ps, A, koff);                                              \
       put_limbs4_k7u(b + c + h2, ps, B, koff);                                         \
     } else if constexpr (SCHEME == 2) {                                                \
@@ -522,45 +531,6 @@ __device__ __forceinline__ void preadd_row(const PreParams &P, const PreNode &N,
       *reinterpret_cast<uint2 *>(d + c) = make_uint2(v[0] | (v[1] << 16), v[2] | (v[3] << 16));
       *reinterpret_cast<uint2 *>(d + c + h2) = make_uint2(v[4] | (v[5] << 16), v[6] | (v[7] << 16));
     }
-    return;
-  }
-  uint32_t da[4], db[4], s1a[4], s1b[4], ta[4], tb[4], s2a[4], s2b[4], s3a[4], s3b[4], s4a[4], s4b[4];
-#pragma unroll
-  for (int e = 0; e < 4; ++e) { da[e] = submod(x21a[e], x11a[e], m); db[e] = submod(x21b[e], x11b[e], m); }
-  apply_Y4<YK, SCHEME == 3>(da, db, s1a, s1b, P.ya, P.yb, m);   // S1 = (A21 - A11) Y
-  apply_Y4<YK, SCHEME == 3>(x21a, x21b, ta, tb, P.ya, P.yb, m); // A21 Y
-#pragma unroll
-  for (int e = 0; e < 4; ++e) {
-    s2a[e] = submod(x22a[e], ta[e], m); s2b[e] = submod(x22b[e], tb[e], m);   // S2 = A22 - A21 Y
-    s3a[e] = submod(s1a[e], x22a[e], m); s3b[e] = submod(s1b[e], x22b[e], m); // S3 = S1 - A22
-    s4a[e] = addmod(s3a[e], x12a[e], m); s4b[e] = addmod(s3b[e], x12b[e], m); // S4 = S3 + A12
-  }
-  const int64_t ps = P.rows_pad * P.kpad;
-#define PUT(o, A, B)                                                                   \
-  if (N.op_row[o] >= 0) {                                                              \
-    int8_t *b = P.arena + (N.op_row[o] + r) * P.kpad;                                  \
-    put_limbs4<SCHEME>(b + c, ps, A, m);                                               \
-    put_limbs4<SCHEME>(b + c + h2, ps, B, m);                                          \
-  }
-  PUT(OUT_S1, s1a, s1b)
-  PUT(OUT_S2, s2a, s2b)
-  PUT(OUT_S4, s4a, s4b)
-  PUT(OUT_X22, x22a, x22b)
-  PUT(OUT_X11, x11a, x11b)
-  PUT(OUT_X12, x12a, x12b)
-  PUT(OUT_S3, s3a, s3b)
-#undef PUT
-  if (N.s3 != nullptr && r < P.mh && P.res32) {
-    uint32_t *d = static_cast<uint32_t *>(N.s3) + r * N.s3_ld;
-    *reinterpret_cast<uint4 *>(d + c) = make_uint4(s3a[0], s3a[1], s3a[2], s3a[3]);
-    *reinterpret_cast<uint4 *>(d + c + h2) = make_uint4(s3b[0], s3b[1], s3b[2], s3b[3]);
-  } else if (N.s3 != nullptr && r < P.mh) {
-    uint16_t *d = static_cast<uint16_t *>(N.s3) + r * N.s3_ld;
-    uint2 va, vb;
-    va.x = s3a[0] | (s3a[1] << 16); va.y = s3a[2] | (s3a[3] << 16);
-    vb.x = s3b[0] | (s3b[1] << 16); vb.y = s3b[2] | (s3b[3] << 16);
-    *reinterpret_cast<uint2 *>(d + c) = va;
-    *reinterpret_cast<uint2 *>(d + c + h2) = vb;
   }
 }
 
