@@ -359,32 +359,40 @@ def run_gpu(args, cfg, rank, world, local_rank):
         step()
     torch.cuda.synchronize()
 
-    # ---------------- timed region: device time per step, L2 flushed before each step
-    adj.adj_launch_count_reset()
-    adj.adj_profile_enable(True)
-    adj.adj_profile_read()
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local_rank) as clk:
-        for i in range(args.steps):
-            flush.zero_()
-            evs[i][0].record(stream)
-            step()
-            evs[i][1].record(stream)
+    # ---------------- timed region: device time per step, L2 flushed before each step.  The
+    # library's per-kernel events (adj_profile_*) cost ~3% of a c2 step, so the headline pass runs
+    # without them; a second pass of the same K steps (same flushes) records them for the roofline
+    # of the leaf kernel and the HBM fractions.
+    def timed_pass(profile):
+        adj.adj_launch_count_reset()
+        adj.adj_profile_enable(profile)
+        adj.adj_profile_read()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        if world > 1:
+            dist.barrier()
         torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    launches = adj.adj_launch_count()
-    prof = adj.adj_profile_read()
-    adj.adj_profile_enable(False)
-    step_ms = [a.elapsed_time(b) for a, b in evs]
-    ms = sum(step_ms) / len(step_ms)
-    if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        with ClockSampler(local_rank) as clk:
+            for i in range(args.steps):
+                flush.zero_()
+                evs[i][0].record(stream)
+                step()
+                evs[i][1].record(stream)
+            torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        launches = adj.adj_launch_count()
+        prof = adj.adj_profile_read()
+        adj.adj_profile_enable(False)
+        step_ms = [a.elapsed_time(b) for a, b in evs]
+        ms = sum(step_ms) / len(step_ms)
+        if world > 1:
+            t = torch.tensor([ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms, launches, prof, clk
+
+    ms, launches, _, clk = timed_pass(False)
+    ms_prof, _, prof, clk_prof = timed_pass(True)
     value = m * m * k / (ms * 1e-3)
 
     # ---------------- sustained: the same steps back to back for ~--sustain-s seconds (the board
@@ -638,7 +646,11 @@ def run_gpu(args, cfg, rank, world, local_rank):
             "kernel": "leaf_kernel (grouped tcgen05 kind::i8 GEMM/SYRK + mod-p epilogue)",
             "peak_source": f"{src}: 2 x bf16_tflops ({peaks['bf16_tflops']}) burst, int8 = 2x bf16 nominal",
             "algorithmic_ops_per_launch": ops, "leaf_ms_per_launch": leaf_avg_ms,
-            "leaf_launches_per_step": leaf_n / args.steps}
+            "leaf_launches_per_step": leaf_n / args.steps,
+            "measured": (f"library CUDA events around each leaf launch on the launch stream, over a second "
+                         f"pass of the {args.steps} timed steps (same flushes; with these events a step "
+                         f"takes {ms_prof:.4f} ms, without them {ms:.4f} ms)"),
+            "clocks_during": clk_prof.summary()}
     share = {c: round(v[0] / max(1e-9, sum(x[0] for x in prof.values())), 4) for c, v in prof.items()}
     # achieved HBM bandwidth of the HBM-bound kernels (algorithmic bytes / device time per step)
     hb = hbm_bytes(cfg, depth, args.herk, 2 if io16 and world == 1 else 4)
