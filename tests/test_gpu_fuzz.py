@@ -64,3 +64,60 @@ def test_fuzz_phi_t(adj, case):
     got = C.cpu().numpy().view(np.uint32)
     assert np.array_equal(got[:, :m], exp), (p, m, k, depth, mode, in16)
     assert np.array_equal(got[:, m:], C0[:, m:]), (p, m, k, depth, mode)   # columns past m untouched
+
+
+PRIMES_3MOD4 = [3, 251, 8191, 16763, 16787, 65519, 131071, 262139]
+
+
+@pytest.mark.parametrize("case", range(40))
+def test_fuzz_phi_h_and_q(adj, case):
+    """phi = H (2M, or one level of Alg. 1 over GF(p^2)) and phi = Q (6M): random ragged shapes,
+    depths, strides, plain / FILL_UPPER."""
+    import torch
+    rng = np.random.default_rng(5000 + case)
+    phi = "H" if case % 2 == 0 else "Q"
+    p = int(rng.choice(PRIMES_3MOD4)) if phi == "H" else int(rng.choice(PRIMES))
+    w = 2 if phi == "H" else 4
+    m, k = int(rng.integers(1, 300)), int(rng.integers(1, 300))
+    depth = int(rng.integers(0, 3))
+    lda, ldc = k + int(rng.integers(0, 5)), m + int(rng.integers(0, 5))
+    Araw = rng.integers(0, 1 << 32, size=(m, lda, w), dtype=np.uint64).astype(np.uint32)
+    A = (Araw[:, :k] % p).astype(np.uint32)
+    dA = torch.from_numpy(Araw.reshape(m, lda * w).view(np.int32)).cuda()
+    ref = oracle.syrk_h(A, p) if phi == "H" else oracle.syrk_q(A, p)
+    C0 = rng.integers(0, 1 << 32, size=(m, ldc, w), dtype=np.uint64).astype(np.uint32)
+    C = torch.from_numpy(C0.reshape(m, ldc * w).view(np.int32).copy()).cuda()
+    alg1 = phi == "H" and rng.random() < 0.5
+    fill = rng.random() < 0.3
+    flags = (adj.ADJ_HERK_ALG1 if alg1 else 0) | (adj.ADJ_FILL_UPPER if fill else 0)
+    adj.adjprod_modp_ex(m, k, p, adj.ADJ_PHI_H if phi == "H" else adj.ADJ_PHI_Q, dA, lda, C, ldc,
+                        depth=1 if alg1 else depth, flags=flags)
+    torch.cuda.synchronize()
+    got = C.cpu().numpy().view(np.uint32).reshape(m, ldc, w)
+    lo = np.tril(np.ones((m, m), dtype=bool))
+    assert np.array_equal(got[:, :m][lo], ref[lo]), (phi, p, m, k, depth, alg1)
+    if fill:   # Up(C) = phi(Low(C)): conjugation negates the imaginary components
+        up = ~lo
+        conj = ref.transpose(1, 0, 2).astype(np.int64)
+        conj[..., 1:] = (-conj[..., 1:]) % p
+        assert np.array_equal(got[:, :m][up], conj.astype(np.uint32)[up]), (phi, p, m, k, depth)
+    else:
+        assert np.array_equal(got[:, :m][~lo], C0[:, :m][~lo])
+    assert np.array_equal(got[:, m:], C0[:, m:])
+
+
+@pytest.mark.parametrize("case", range(40))
+def test_fuzz_gemm(adj, case):
+    import torch
+    rng = np.random.default_rng(9000 + case)
+    p = int(rng.choice(PRIMES))
+    m, n, k = (int(x) for x in rng.integers(1, 600, size=3))
+    lda, ldb, ldc = k + int(rng.integers(0, 5)), k + int(rng.integers(0, 5)), n + int(rng.integers(0, 5))
+    Ar = rng.integers(0, 1 << 32, size=(m, lda), dtype=np.uint64).astype(np.uint32)
+    Br = rng.integers(0, 1 << 32, size=(n, ldb), dtype=np.uint64).astype(np.uint32)
+    C = torch.zeros((m, ldc), dtype=torch.int32, device="cuda")
+    adj.gemm_modp(m, n, k, p, torch.from_numpy(Ar.view(np.int32)).cuda(), lda,
+                  torch.from_numpy(Br.view(np.int32)).cuda(), ldb, C, ldc)
+    torch.cuda.synchronize()
+    ref = oracle.gemm_nt((Ar[:, :k] % p).astype(np.uint32), (Br[:, :k] % p).astype(np.uint32), p)
+    assert np.array_equal(C.cpu().numpy().view(np.uint32)[:, :n], ref), (p, m, n, k)
