@@ -96,7 +96,7 @@ enum { ADJ_FILL_UPPER = 1u, ADJ_HERK_ALG1 = 2u, ADJ_DIST_TILES = 4u, ADJ_DIST_P2
 
 typedef struct {
   int depth;              /* recursion levels of Alg. alg:MIAHMM; -1 = automatic; 0 = classical */
-  uint32_t flags;         /* ADJ_FILL_UPPER | ADJ_HERK_ALG1 */
+  uint32_t flags;         /* ADJ_* option flags above, or-ed */
   void *workspace;        /* device memory of >= workspace_bytes, or NULL (library allocates
                              stream-ordered from a per-device pool that retains its memory
                              between calls, cudaMallocFromPoolAsync / cudaFreeAsync) */
