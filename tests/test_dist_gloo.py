@@ -49,7 +49,7 @@ def _worker(rank, world, port, cases, out_q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 4])
 def test_split_k_reduce_gloo(world):
     cases = [(37, 100, 8191, "T"), (64, 7, 65521, "T"), (20, 33, 8191, "H"), (5, 1, 97, "T")]
     ctx = mp.get_context("spawn")
@@ -119,7 +119,7 @@ def _tiles_worker(rank, world, port, cases, out_q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 4])
 def test_tile_sharding_gather_gloo(world):
     cases = [(300, 40, 8191, 0), (700, 33, 97, 1), (5, 3, 65521, 0), (1030, 16, 8191, 1)]
     ctx = mp.get_context("spawn")
