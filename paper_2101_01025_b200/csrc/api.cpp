@@ -227,16 +227,19 @@ size_t span_bytes(int64_t rows, int64_t cols, int64_t ld, int elem_bytes) {
   return (size_t)((rows - 1) * ld + cols) * elem_bytes;
 }
 
-InView make_view(const void *ptr, int64_t ld, int64_t rows, int64_t cols, int type) {
+InView make_view(const void *ptr, int64_t ld, int64_t rows, int64_t cols, int type, bool e16 = false) {
   InView v;
+  std::memset(&v, 0, sizeof(v));
   v.ptr = ptr;
   v.ld = ld;
   v.rows_valid = rows;
   v.cols_valid = cols;
   v.type = type;
+  v.e16 = e16 ? 1 : 0;   // pair types only: (re, im) uint16 pairs
   uintptr_t a = (uintptr_t)ptr;
   if (type == IN_U16 || type == IN_U16R) v.vec_ok = (a % 8 == 0) && (ld % 4 == 0);
   else if (type == IN_U32) v.vec_ok = (a % 16 == 0) && (ld % 4 == 0);
+  else if (e16) v.vec_ok = (a % 16 == 0) && (ld % 4 == 0);
   else v.vec_ok = (a % 16 == 0) && (ld % 2 == 0);
   return v;
 }
@@ -245,11 +248,12 @@ InView child_view(const InView &pv, int c, const LevelPlan &Lp, void *s3, int64_
   // children of a node at level l-1 (half sizes Lp.mh, Lp.kh): 0 = X11, 1 = X12, 2 = S3
   if (c == 2) return make_view(s3, s3_ld, Lp.mh, Lp.kh, res32 ? IN_U32 : IN_U16);
   const int64_t rows = std::min(pv.rows_valid, Lp.mh);
-  if (c == 0) return make_view(pv.ptr, pv.ld, rows, std::min(pv.cols_valid, Lp.kh), pv.type);
-  const int esz = (pv.type == IN_U16 || pv.type == IN_U16R) ? 2 : (pv.type == IN_U32 ? 4 : (pv.type == IN_QUAD_SUM ? 16 : 8));
+  if (c == 0) return make_view(pv.ptr, pv.ld, rows, std::min(pv.cols_valid, Lp.kh), pv.type, pv.e16);
+  const int esz = (pv.type == IN_U16 || pv.type == IN_U16R) ? 2
+                  : (pv.type == IN_U32 ? 4 : (pv.type == IN_QUAD_SUM ? 16 : (pv.e16 ? 4 : 8)));
   const void *ptr = static_cast<const uint8_t *>(pv.ptr) + (size_t)Lp.kh * esz;
   int64_t cols = std::max<int64_t>(0, std::min(pv.cols_valid - Lp.kh, Lp.kh));
-  return make_view(ptr, pv.ld, rows, cols, pv.type);
+  return make_view(ptr, pv.ld, rows, cols, pv.type, pv.e16);
 }
 
 // ------------------------------------------------------------------ launch schedule
@@ -458,7 +462,7 @@ adj_status_t run_syrk(const Plan &P, const Ptrs &x, adj_phi_t phi, uint32_t flag
     // X / Y limb planes come from the same pass over A as T (split mode 1 at depth 0, the
     // root pre-addition's side output at depth >= 1).
     uint8_t *arena0 = x.ws + P.arenas[0].offset;
-    InView troot = make_view(x.A, x.lda, m, k, IN_PAIR_SUM);
+    InView troot = make_view(x.A, x.lda, m, k, IN_PAIR_SUM, x.in16);
     void *G = x.ws + P.g_offset;
     void *H = x.ws + P.h_offset;
     if (P.depth == 0) {
@@ -490,7 +494,7 @@ adj_status_t run_syrk(const Plan &P, const Ptrs &x, adj_phi_t phi, uint32_t flag
       if (st) return st;
     }
     LAUNCH_CLS(CLS_COMB, launch_twom(m, G, P.rows_pad0, H, P.rows_pad0, P.res32 ? 1 : 0, x.C, x.ldc, P.mod, x.alpha,
-                                     x.beta, x.axpby, s));
+                                     x.beta, x.axpby, x.res16 ? 1 : 0, s));
   }
   if (flags & ADJ_FILL_UPPER) LAUNCH(launch_fill_upper(m, adj_phi_width(phi), x.C, x.ldc, P.mod, s));
   return ADJ_OK;
@@ -543,7 +547,7 @@ adj_status_t run_herk1(const Plan &P, const Ptrs &x, uint32_t flags, cudaStream_
   const LevelPlan &L = P.lv[1];
   HerkPreParams hp;
   std::memset(&hp, 0, sizeof(hp));
-  hp.in = make_view(x.A, x.lda, P.m, P.k, IN_PAIR_RE);
+  hp.in = make_view(x.A, x.lda, P.m, P.k, IN_PAIR_RE, x.in16);
   hp.mh = L.mh; hp.kh = L.kh;
   hp.rows_pad = L.rows_pad; hp.kpad = L.kpad;
   hp.arena = reinterpret_cast<int8_t *>(x.ws + P.arenas[0].offset);
@@ -580,7 +584,7 @@ adj_status_t validate_syrk(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, cons
   if (lda < k || (lda < 1 && k > 0)) return fail(ADJ_ERR_INVALID_VALUE, "lda=%lld < k=%lld", (long long)lda, (long long)k);
   if (ldc < m) return fail(ADJ_ERR_INVALID_VALUE, "ldc=%lld < m=%lld", (long long)ldc, (long long)m);
   const int w = adj_phi_width(phi);
-  const int ea = (flags & ADJ_IN_U16) ? 2 : 4 * w, ec = (flags & ADJ_OUT_U16) ? 2 : 4 * w;
+  const int ea = (flags & ADJ_IN_U16) ? 2 * w : 4 * w, ec = (flags & ADJ_OUT_U16) ? 2 * w : 4 * w;
   if (overlap(A, span_bytes(m, k, lda, ea), C, span_bytes(m, m, ldc, ec)))
     return fail(ADJ_ERR_INVALID_VALUE, "A and C overlap");
   return ADJ_OK;
@@ -681,10 +685,10 @@ static adj_status_t adjprod_impl(int64_t m, int64_t k, uint32_t p, adj_phi_t phi
   beta %= p;
   const int axpby = !(alpha == 1 && beta == 0);
   const bool in16 = flags & ADJ_IN_U16, out16 = flags & ADJ_OUT_U16;
-  if ((in16 || out16) && (phi != ADJ_PHI_T || p > 65535))
-    return fail(ADJ_ERR_INVALID_VALUE, "ADJ_IN_U16 / ADJ_OUT_U16 need phi = ADJ_PHI_T and p < 2^16");
-  if (out16 && (axpby || (flags & ADJ_FILL_UPPER)))
-    return fail(ADJ_ERR_INVALID_VALUE, "ADJ_OUT_U16 is the plain form: no alpha / beta, no ADJ_FILL_UPPER");
+  if ((in16 || out16) && (phi == ADJ_PHI_Q || p > 65535))
+    return fail(ADJ_ERR_INVALID_VALUE, "ADJ_IN_U16 / ADJ_OUT_U16 need phi = ADJ_PHI_T or ADJ_PHI_H and p < 2^16");
+  if (out16 && (axpby || (flags & (ADJ_FILL_UPPER | ADJ_HERK_ALG1))))
+    return fail(ADJ_ERR_INVALID_VALUE, "ADJ_OUT_U16 is the plain form: no alpha / beta, ADJ_FILL_UPPER or ADJ_HERK_ALG1");
   if (m == 0) return ADJ_OK;
   int dev, sms;
   if ((st = check_device(&dev, &sms)) != ADJ_OK) return st;
@@ -692,7 +696,7 @@ static adj_status_t adjprod_impl(int64_t m, int64_t k, uint32_t p, adj_phi_t phi
   if (k == 0 || alpha == 0) {  // Low(C) = beta Low(C)
     if (out16) {
       uint16_t *C16 = reinterpret_cast<uint16_t *>(C);
-      for (int64_t i = 0; i < m; ++i) CUDA_TRY(cudaMemsetAsync(C16 + i * ldc, 0, (size_t)(i + 1) * 2, s));
+      for (int64_t i = 0; i < m; ++i) CUDA_TRY(cudaMemsetAsync(C16 + i * ldc * w, 0, (size_t)(i + 1) * 2 * w, s));
       return ADJ_OK;
     }
     if (beta == 0) {

@@ -515,11 +515,12 @@ cudaError_t launch_quat_combine(const QuatCombParams &p, cudaStream_t s) {
 // One block per lower 64 x 64 tile (grid over lower tile pairs as K4); G, H are rows_pad x
 // rows_pad (multiple of 128, ld a multiple of 8) so every 16-byte tile load is in range.  The
 // mirrored H tile is staged in shared memory; C pairs are stored as 16-byte (re, im, re, im).
-template <typename InT>
+template <typename InT, bool O16>
 __global__ void __launch_bounds__(256) twom_kernel(int64_t m, const InT *G, int64_t ldg,
-                                                   const InT *H, int64_t ldh, uint32_t *C,
+                                                   const InT *H, int64_t ldh, void *Cv,
                                                    int64_t ldc, ModP mod, uint32_t alpha, uint32_t beta,
                                                    int axpby) {
+  uint32_t *C = static_cast<uint32_t *>(Cv);   // (re, im) uint32 pairs, or uint16 pairs when O16
   const int x = (int)blockIdx.x;
   int ti = (int)((sqrtf(8.0f * (float)x + 1.0f) - 1.0f) * 0.5f);
   while ((ti + 1) * (ti + 2) / 2 <= x) ++ti;
@@ -560,6 +561,20 @@ __global__ void __launch_bounds__(256) twom_kernel(int64_t m, const InT *G, int6
       im[e] = submod(ht, hv[e], mod);                                     // H^T - H
     }
     const int64_t n = min64(8, min64(i - j + 1, m - j));
+    if constexpr (O16) {   // ADJ_OUT_U16: one 32-bit word (re | im << 16) per element
+      uint32_t *o = C + (i * ldc + j);
+      if (n == 8 && (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
+        __stcs(reinterpret_cast<uint4 *>(o), make_uint4(re[0] | (im[0] << 16), re[1] | (im[1] << 16),
+                                                        re[2] | (im[2] << 16), re[3] | (im[3] << 16)));
+        __stcs(reinterpret_cast<uint4 *>(o) + 1, make_uint4(re[4] | (im[4] << 16), re[5] | (im[5] << 16),
+                                                            re[6] | (im[6] << 16), re[7] | (im[7] << 16)));
+      } else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          if (e < n) o[e] = re[e] | (im[e] << 16);
+      }
+      continue;
+    }
     uint32_t *o = C + 2 * (i * ldc + j);
     if (axpby) {
       for (int e = 0; e < n; ++e) {
@@ -580,17 +595,23 @@ __global__ void __launch_bounds__(256) twom_kernel(int64_t m, const InT *G, int6
 }
 
 cudaError_t launch_twom(int64_t m, const void *G, int64_t ldg, const void *H, int64_t ldh, int in32,
-                        uint32_t *C, int64_t ldc, const ModP &mod, uint32_t alpha, uint32_t beta, int axpby,
-                        cudaStream_t s) {
+                        void *C, int64_t ldc, const ModP &mod, uint32_t alpha, uint32_t beta, int axpby,
+                        int out16, cudaStream_t s) {
   if (m == 0) return cudaSuccess;
   const unsigned nt = (unsigned)((m + 63) / 64);
   const dim3 grid(nt * (nt + 1) / 2);
   if (in32)
-    twom_kernel<uint32_t><<<grid, 256, 0, s>>>(m, static_cast<const uint32_t *>(G), ldg,
-                                               static_cast<const uint32_t *>(H), ldh, C, ldc, mod, alpha, beta, axpby);
+    twom_kernel<uint32_t, false><<<grid, 256, 0, s>>>(m, static_cast<const uint32_t *>(G), ldg,
+                                                      static_cast<const uint32_t *>(H), ldh, C, ldc, mod, alpha,
+                                                      beta, axpby);
+  else if (out16)
+    twom_kernel<uint16_t, true><<<grid, 256, 0, s>>>(m, static_cast<const uint16_t *>(G), ldg,
+                                                     static_cast<const uint16_t *>(H), ldh, C, ldc, mod, alpha,
+                                                     beta, axpby);
   else
-    twom_kernel<uint16_t><<<grid, 256, 0, s>>>(m, static_cast<const uint16_t *>(G), ldg,
-                                               static_cast<const uint16_t *>(H), ldh, C, ldc, mod, alpha, beta, axpby);
+    twom_kernel<uint16_t, false><<<grid, 256, 0, s>>>(m, static_cast<const uint16_t *>(G), ldg,
+                                                      static_cast<const uint16_t *>(H), ldh, C, ldc, mod, alpha,
+                                                      beta, axpby);
   return cudaGetLastError();
 }
 

@@ -15,8 +15,8 @@ cudaError_t launch_herk_preadd(const HerkPreParams &p, cudaStream_t s);
 cudaError_t launch_herk_combine(const HerkCombParams &p, cudaStream_t s);
 cudaError_t launch_quat_combine(const QuatCombParams &p, cudaStream_t s);
 cudaError_t launch_twom(int64_t m, const void *G, int64_t ldg, const void *H, int64_t ldh, int in32,
-                        uint32_t *C, int64_t ldc, const ModP &mod, uint32_t alpha, uint32_t beta, int axpby,
-                        cudaStream_t s);
+                        void *C, int64_t ldc, const ModP &mod, uint32_t alpha, uint32_t beta, int axpby,
+                        int out16, cudaStream_t s);
 cudaError_t launch_scale_lower(int64_t m, int w, uint32_t *X, int64_t ldx, uint32_t beta, const ModP &mod,
                                cudaStream_t s);
 cudaError_t launch_mod_lower(int64_t m, int w, const uint32_t *src, int64_t lds, uint32_t *dst, int64_t ldd,

@@ -51,17 +51,30 @@ __device__ __forceinline__ void load4(const InView &v, int64_t R, int64_t C, con
         x[e] = addmod(addmod(mod_u32(q.x, m), mod_u32(q.y, m), m), addmod(mod_u32(q.z, m), mod_u32(q.w, m), m), m);
       }
   } else {
-    const uint32_t *p = static_cast<const uint32_t *>(v.ptr) + 2 * (R * v.ld + C);
     uint32_t re[4] = {0, 0, 0, 0}, im[4] = {0, 0, 0, 0};
-    if (all) {
-      uint4 a = __ldg(reinterpret_cast<const uint4 *>(p));
-      uint4 b = __ldg(reinterpret_cast<const uint4 *>(p) + 1);
-      re[0] = a.x; im[0] = a.y; re[1] = a.z; im[1] = a.w;
-      re[2] = b.x; im[2] = b.y; re[3] = b.z; im[3] = b.w;
-    } else {
+    if (v.e16) {   // (re, im) uint16 pairs (ADJ_IN_U16)
+      const uint16_t *p = static_cast<const uint16_t *>(v.ptr) + 2 * (R * v.ld + C);
+      if (all) {
+        const uint4 q = __ldg(reinterpret_cast<const uint4 *>(p));
+        re[0] = q.x & 0xFFFF; im[0] = q.x >> 16; re[1] = q.y & 0xFFFF; im[1] = q.y >> 16;
+        re[2] = q.z & 0xFFFF; im[2] = q.z >> 16; re[3] = q.w & 0xFFFF; im[3] = q.w >> 16;
+      } else {
 #pragma unroll
-      for (int e = 0; e < 4; ++e)
-        if (C + e < v.cols_valid) { re[e] = __ldg(p + 2 * e); im[e] = __ldg(p + 2 * e + 1); }
+        for (int e = 0; e < 4; ++e)
+          if (C + e < v.cols_valid) { re[e] = __ldg(p + 2 * e); im[e] = __ldg(p + 2 * e + 1); }
+      }
+    } else {
+      const uint32_t *p = static_cast<const uint32_t *>(v.ptr) + 2 * (R * v.ld + C);
+      if (all) {
+        uint4 a = __ldg(reinterpret_cast<const uint4 *>(p));
+        uint4 b = __ldg(reinterpret_cast<const uint4 *>(p) + 1);
+        re[0] = a.x; im[0] = a.y; re[1] = a.z; im[1] = a.w;
+        re[2] = b.x; im[2] = b.y; re[3] = b.z; im[3] = b.w;
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (C + e < v.cols_valid) { re[e] = __ldg(p + 2 * e); im[e] = __ldg(p + 2 * e + 1); }
+      }
     }
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
@@ -307,7 +320,12 @@ __device__ __forceinline__ void load4_fast(const void *ptr, int64_t off, const M
 // re / im of 4 consecutive GF(p^2) elements (interleaved pairs), reduced mod p
 __device__ __forceinline__ void load4_pair(const InView &v, int64_t R, int64_t C, bool fast, const ModP &m,
                                            uint32_t (&re)[4], uint32_t (&im)[4]) {
-  if (fast) {
+  if (fast && v.e16) {
+    const uint4 q = __ldg(reinterpret_cast<const uint4 *>(static_cast<const uint16_t *>(v.ptr) + 2 * (R * v.ld + C)));
+    re[0] = mod_u32(q.x & 0xFFFF, m); im[0] = mod_u32(q.x >> 16, m); re[1] = mod_u32(q.y & 0xFFFF, m);
+    im[1] = mod_u32(q.y >> 16, m); re[2] = mod_u32(q.z & 0xFFFF, m); im[2] = mod_u32(q.z >> 16, m);
+    re[3] = mod_u32(q.w & 0xFFFF, m); im[3] = mod_u32(q.w >> 16, m);
+  } else if (fast) {
     const uint4 *p = reinterpret_cast<const uint4 *>(static_cast<const uint32_t *>(v.ptr) + 2 * (R * v.ld + C));
     uint4 a = __ldg(p), b = __ldg(p + 1);
     re[0] = mod_u32(a.x, m); im[0] = mod_u32(a.y, m); re[1] = mod_u32(a.z, m); im[1] = mod_u32(a.w, m);
@@ -404,7 +422,7 @@ __device__ __forceinline__ void preadd_row(const PreParams &P, const PreNode &N,
 #pragma unroll
         for (int e = 0; e < 4; ++e) (*dst[i])[e] = mod_u32((*dst[i])[e], m);
     }
-  } else if (fast) {
+  } else if (fast && !v.e16) {
     const int64_t o1 = r * v.ld, o2 = (P.mh + r) * v.ld;
     load4_fast<T>(v.ptr, o1 + c, m, x11a);
     load4_fast<T>(v.ptr, o1 + c + h2, m, x11b);

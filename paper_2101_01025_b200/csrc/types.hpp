@@ -77,6 +77,8 @@ struct InView {          // a (possibly padded) view of a node's input matrix
   int64_t rows_valid, cols_valid;
   int32_t type;
   int32_t vec_ok;        // 16-byte aligned rows -> vector loads allowed
+  int32_t e16;           // IN_PAIR_*: (re, im) pairs of uint16 (ADJ_IN_U16) instead of uint32
+  int32_t pad_;
 };
 
 // S1, S2, S4, X22 (GEMM operands), X11, X12, S3 (SYRK leaves when the level is the last)

@@ -598,8 +598,8 @@ def test_adjprod_T_compact_io_strided_and_errors(adj):
     for b in bad:
         with pytest.raises(adj.AdjError):
             adj.adjprod_modp_ex(m, k, b["p"], adj.ADJ_PHI_T, dA, k + 12, C32, m, flags=b["flags"])
-    with pytest.raises(adj.AdjError):   # phi = H
-        adj.adjprod_modp_ex(m, k // 2, p, adj.ADJ_PHI_H, dA, (k + 12) // 2, C32, m // 2, flags=adj.ADJ_IN_U16)
+    with pytest.raises(adj.AdjError):   # phi = Q
+        adj.adjprod_modp_ex(m // 2, k // 4, p, adj.ADJ_PHI_Q, dA, (k + 12) // 4, C32, m // 4, flags=adj.ADJ_IN_U16)
     with pytest.raises(adj.AdjError):   # SYRK form with a uint16 Low(C)
         adj.adjprod_modp_syrk(m, k, p, adj.ADJ_PHI_T, 3, dA, k + 12, 1, out, m + 20, flags=adj.ADJ_OUT_U16)
 
@@ -649,3 +649,35 @@ def test_compact_input_dist_single_rank(adj, flags_name):
                                   depth=1, flags=adj.ADJ_OUT_U16)
     finally:
         adj.adj_comm_destroy(comm)
+
+
+@pytest.mark.parametrize("p", [251, 8191, 16763, 65519])
+@pytest.mark.parametrize("depth", [0, 1, 2])
+@pytest.mark.parametrize("m,k", [(1, 3), (129, 200), (300, 257)])
+def test_adjprod_H_compact_io(adj, p, depth, m, k):
+    """ADJ_IN_U16 / ADJ_OUT_U16 for phi = H (2M): (re, im) uint16 pairs in (any value, read mod
+    p) and out, every combination, strided; one level of Alg. 1 over GF(p^2) reads uint16 too."""
+    import torch
+    rng = np.random.default_rng(m * 5 + k + p + depth)
+    lda = k + 3
+    A16 = rng.integers(0, 1 << 16, size=(m, lda, 2), dtype=np.uint16)
+    Ared = (A16[:, :k].astype(np.uint32) % p).astype(np.uint32)
+    ref = oracle.syrk_h(Ared, p)
+    dA16 = torch.from_numpy(A16.reshape(m, lda * 2).view(np.int16)).cuda()
+    dA32 = torch.from_numpy(np.ascontiguousarray(Ared).reshape(m, k * 2).view(np.int32)).cuda()
+    lo = np.tril(np.ones((m, m), dtype=bool))
+    for dA, ld in ((dA16, lda), (dA32, k)):
+        for out16 in (False, True):
+            C = torch.zeros((m, m * 2), dtype=torch.int16 if out16 else torch.int32, device="cuda")
+            flags = (adj.ADJ_IN_U16 if dA.element_size() == 2 else 0) | (adj.ADJ_OUT_U16 if out16 else 0)
+            adj.adjprod_modp_ex(m, k, p, adj.ADJ_PHI_H, dA, ld, C, m, depth=depth, flags=flags)
+            torch.cuda.synchronize()
+            got = C.cpu().numpy().view(np.uint16 if out16 else np.uint32).astype(np.uint32).reshape(m, m, 2)
+            assert np.array_equal(got[lo], ref[lo]), (p, depth, m, k, dA.element_size(), out16)
+    if depth == 1:   # Alg. 1 over GF(p^2) with uint16 input
+        C = torch.zeros((m, m * 2), dtype=torch.int32, device="cuda")
+        adj.adjprod_modp_ex(m, k, p, adj.ADJ_PHI_H, dA16, lda, C, m, depth=1,
+                            flags=adj.ADJ_IN_U16 | adj.ADJ_HERK_ALG1)
+        torch.cuda.synchronize()
+        got = C.cpu().numpy().view(np.uint32).reshape(m, m, 2)
+        assert np.array_equal(got[lo], ref[lo]), (p, m, k, "alg1")
