@@ -319,7 +319,10 @@ def run_gpu(args, cfg, rank, world, local_rank):
     # residues of A and Low(C) live in HBM as uint16 when phi = T and p < 2^16 (ADJ_IN_U16 |
     # ADJ_OUT_U16; exact, the same arithmetic), else uint32.  --io u32 forces uint32.
     # (N > 1: uint16 A, uint32 Low(C) on the root -- the distributed entry point reads ADJ_IN_U16)
-    io16 = cfg["phi"] == "T" and p < 65536 and args.io in ("auto", "u16")
+    # phi = H: (re, im) uint16 pairs; Alg. 1 over GF(p^2) reads them but writes uint32 (and the
+    # distributed path takes phi = T only), so those runs keep uint32 residues throughout
+    io16 = ((cfg["phi"] == "T" or (cfg["phi"] == "H" and not alg1 and world == 1)) and p < 65536
+            and args.io in ("auto", "u16"))
     if io16 and world == 1:
         flags |= adj.ADJ_IN_U16 | adj.ADJ_OUT_U16
     elif io16:
@@ -497,7 +500,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
         e2e_u32 = run_e2e(4, 0)
         e2e_u32["io"] = "uint32 residues both ways"
         e2e = e2e_u32
-        if phi == adj.ADJ_PHI_T and p < 65536:
+        if io16:
             e2e = run_e2e(2, adj.ADJ_IN_U16 | adj.ADJ_OUT_U16)
             e2e["io"] = "uint16 residues both ways (ADJ_IN_U16 | ADJ_OUT_U16)"
     else:
