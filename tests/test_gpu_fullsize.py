@@ -31,10 +31,10 @@ def _run(env, cfg, A_dev, io16=None):
     depth = cfg["depth"] if cfg["depth"] is not None else adj.adjprod_modp_auto_depth(m, k, p, phi)
     w = 2 if phi else 1
     if io16 is None:
-        io16 = cfg["phi"] == "T" and p < 65536
+        io16 = cfg["phi"] in ("T", "H") and p < 65536
     if io16:
         A16 = A_dev.to(torch.int16)
-        C = torch.zeros((m, m), dtype=torch.int16, device="cuda")
+        C = torch.zeros((m, m * w), dtype=torch.int16, device="cuda")
         adj.adjprod_modp_ex(m, k, p, phi, A16, k, C, m, depth=depth, flags=adj.ADJ_IN_U16 | adj.ADJ_OUT_U16)
         del A16
         torch.cuda.synchronize()
