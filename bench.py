@@ -321,7 +321,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
     # (N > 1: uint16 A, uint32 Low(C) on the root -- the distributed entry point reads ADJ_IN_U16)
     # phi = H: (re, im) uint16 pairs; Alg. 1 over GF(p^2) reads them but writes uint32 (and the
     # distributed path takes phi = T only), so those runs keep uint32 residues throughout
-    io16 = ((cfg["phi"] == "T" or (cfg["phi"] == "H" and not alg1 and world == 1)) and p < 65536
+    io16 = ((cfg["phi"] == "T" or (cfg["phi"] in ("H", "Q") and not alg1 and world == 1)) and p < 65536
             and args.io in ("auto", "u16"))
     if io16 and world == 1:
         flags |= adj.ADJ_IN_U16 | adj.ADJ_OUT_U16

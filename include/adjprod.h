@@ -86,13 +86,13 @@ typedef enum {
  *                    into the final kernel: each rank stores its partial (narrow residues)
  *                    straight into the root's window over NVLink (CUDA IPC peer memory), the root
  *                    sums exactly (adj_sum_partials); no NCCL data movement.
- *   ADJ_IN_U16     : phi = ADJ_PHI_T or ADJ_PHI_H, p < 2^16 -- A holds uint16 values (phi = H:
- *                    interleaved uint16 (re, im) pairs), read mod p; lda counts elements as
+ *   ADJ_IN_U16     : p < 2^16 -- A holds uint16 values (phi = H: interleaved uint16 (re, im)
+ *                    pairs; phi = Q: 4 uint16 components), read mod p; lda counts elements as
  *                    before: half the bytes to read and to ship over PCIe.  phi = T also through
  *                    adjprod_modp_shard, adjprod_modp_partial and adjprod_modp_dist.
- *   ADJ_OUT_U16    : phi = ADJ_PHI_T or ADJ_PHI_H (2M), p < 2^16 -- Low(C) written as uint16
- *                    residues (pairs for phi = H); the plain form only (no alpha / beta, no
- *                    ADJ_FILL_UPPER, not with ADJ_HERK_ALG1). */
+ *   ADJ_OUT_U16    : p < 2^16 -- Low(C) written as uint16 residues (pairs / quadruples for
+ *                    phi = H / Q); the plain form only (no alpha / beta, no ADJ_FILL_UPPER, not
+ *                    with ADJ_HERK_ALG1). */
 enum { ADJ_FILL_UPPER = 1u, ADJ_HERK_ALG1 = 2u, ADJ_DIST_TILES = 4u, ADJ_DIST_P2P = 8u, ADJ_IN_U16 = 16u,
        ADJ_OUT_U16 = 32u };
 

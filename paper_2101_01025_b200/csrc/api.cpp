@@ -250,7 +250,7 @@ InView child_view(const InView &pv, int c, const LevelPlan &Lp, void *s3, int64_
   const int64_t rows = std::min(pv.rows_valid, Lp.mh);
   if (c == 0) return make_view(pv.ptr, pv.ld, rows, std::min(pv.cols_valid, Lp.kh), pv.type, pv.e16);
   const int esz = (pv.type == IN_U16 || pv.type == IN_U16R) ? 2
-                  : (pv.type == IN_U32 ? 4 : (pv.type == IN_QUAD_SUM ? 16 : (pv.e16 ? 4 : 8)));
+                  : (pv.type == IN_U32 ? 4 : (pv.type == IN_QUAD_SUM ? (pv.e16 ? 8 : 16) : (pv.e16 ? 4 : 8)));
   const void *ptr = static_cast<const uint8_t *>(pv.ptr) + (size_t)Lp.kh * esz;
   int64_t cols = std::max<int64_t>(0, std::min(pv.cols_valid - Lp.kh, Lp.kh));
   return make_view(ptr, pv.ld, rows, cols, pv.type, pv.e16);
@@ -508,7 +508,7 @@ adj_status_t run_quat(const Plan &P, const Ptrs &x, uint32_t flags, cudaStream_t
   const int64_t m = P.m, k = P.k;
   SplitParams sp;
   std::memset(&sp, 0, sizeof(sp));
-  sp.in = make_view(x.A, x.lda, m, k, IN_QUAD_SUM);
+  sp.in = make_view(x.A, x.lda, m, k, IN_QUAD_SUM, x.in16);
   sp.rows = m; sp.cols = k;
   sp.rows_pad = P.rows_pad0; sp.kpad = P.kpad0;
   sp.arena = reinterpret_cast<int8_t *>(x.ws + P.arenas[0].offset);
@@ -518,7 +518,7 @@ adj_status_t run_quat(const Plan &P, const Ptrs &x, uint32_t flags, cudaStream_t
   adj_status_t st;
   void *G = x.ws + P.g_offset;
   if (P.depth >= 1) {
-    st = run_tree(P, make_view(x.A, x.lda, m, k, IN_QUAD_SUM), x, s);
+    st = run_tree(P, make_view(x.A, x.lda, m, k, IN_QUAD_SUM, x.in16), x, s);
     if (st) return st;
   }
   st = launch_leaf_all(P, x, s);
@@ -536,6 +536,7 @@ adj_status_t run_quat(const Plan &P, const Ptrs &x, uint32_t flags, cudaStream_t
   qp.mod = P.mod;
   qp.alpha = x.alpha; qp.beta = x.beta; qp.axpby = x.axpby;
   qp.in32 = P.res32 ? 1 : 0;
+  qp.out16 = x.res16 ? 1 : 0;
   LAUNCH_CLS(CLS_COMB, launch_quat_combine(qp, s));
   if (flags & ADJ_FILL_UPPER) LAUNCH(launch_fill_upper(m, 4, x.C, x.ldc, P.mod, s));
   return ADJ_OK;
@@ -685,8 +686,8 @@ static adj_status_t adjprod_impl(int64_t m, int64_t k, uint32_t p, adj_phi_t phi
   beta %= p;
   const int axpby = !(alpha == 1 && beta == 0);
   const bool in16 = flags & ADJ_IN_U16, out16 = flags & ADJ_OUT_U16;
-  if ((in16 || out16) && (phi == ADJ_PHI_Q || p > 65535))
-    return fail(ADJ_ERR_INVALID_VALUE, "ADJ_IN_U16 / ADJ_OUT_U16 need phi = ADJ_PHI_T or ADJ_PHI_H and p < 2^16");
+  if ((in16 || out16) && p > 65535)
+    return fail(ADJ_ERR_INVALID_VALUE, "ADJ_IN_U16 / ADJ_OUT_U16 need p < 2^16");
   if (out16 && (axpby || (flags & (ADJ_FILL_UPPER | ADJ_HERK_ALG1))))
     return fail(ADJ_ERR_INVALID_VALUE, "ADJ_OUT_U16 is the plain form: no alpha / beta, ADJ_FILL_UPPER or ADJ_HERK_ALG1");
   if (m == 0) return ADJ_OK;

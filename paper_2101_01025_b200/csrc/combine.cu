@@ -486,7 +486,25 @@ __global__ void __launch_bounds__(256) quat_combine_kernel(const __grid_constant
       h[2][e] = submod(t1, t1t, md);                                                       // H3
       h[3][e] = submod(t3t, t3, md);                                                       // H4
     }
-    store_q8(P.C + 4 * (i * P.ldc + j), min64(8, min64(i - j + 1, m - j)), h, P);
+    const int64_t nq = min64(8, min64(i - j + 1, m - j));
+    if (P.out16) {   // ADJ_OUT_U16: 4 uint16 components per quaternion (plain form only)
+      uint16_t *o = reinterpret_cast<uint16_t *>(P.C) + 4 * (i * P.ldc + j);
+      if (nq == 8 && (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          __stcs(reinterpret_cast<uint4 *>(o) + e,
+                 make_uint4(h[0][2 * e] | (h[1][2 * e] << 16), h[2][2 * e] | (h[3][2 * e] << 16),
+                            h[0][2 * e + 1] | (h[1][2 * e + 1] << 16), h[2][2 * e + 1] | (h[3][2 * e + 1] << 16)));
+      } else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          if (e < nq)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) o[4 * e + c] = (uint16_t)h[c][e];
+      }
+      continue;
+    }
+    store_q8(P.C + 4 * (i * P.ldc + j), nq, h, P);
   }
 }
 

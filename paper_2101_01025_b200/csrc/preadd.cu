@@ -41,6 +41,17 @@ __device__ __forceinline__ void load4(const InView &v, int64_t R, int64_t C, con
 #pragma unroll
       for (int e = 0; e < 4; ++e) x[e] = mod_u32(x[e], m);
     }
+  } else if (v.type == IN_QUAD_SUM && v.e16) {   // 4 uint16 components per quaternion (ADJ_IN_U16)
+    const uint16_t *p = static_cast<const uint16_t *>(v.ptr) + 4 * (R * v.ld + C);
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      if (C + e < v.cols_valid) {
+        uint2 q = all ? __ldg(reinterpret_cast<const uint2 *>(p) + e)
+                      : make_uint2((uint32_t)__ldg(p + 4 * e) | ((uint32_t)__ldg(p + 4 * e + 1) << 16),
+                                   (uint32_t)__ldg(p + 4 * e + 2) | ((uint32_t)__ldg(p + 4 * e + 3) << 16));
+        x[e] = addmod(addmod(mod_u32(q.x & 0xFFFF, m), mod_u32(q.x >> 16, m), m),
+                      addmod(mod_u32(q.y & 0xFFFF, m), mod_u32(q.y >> 16, m), m), m);
+      }
   } else if (v.type == IN_QUAD_SUM) {
     const uint32_t *p = static_cast<const uint32_t *>(v.ptr) + 4 * (R * v.ld + C);
 #pragma unroll
@@ -621,9 +632,17 @@ __global__ void __launch_bounds__(256) split_kernel(const __grid_constant__ Spli
         for (int e = 0; e < 4; ++e) {
           uint4 w4 = make_uint4(0u, 0u, 0u, 0u);
           if (r < vv.rows_valid && c + e < vv.cols_valid && c + e < P.cols) {
-            const uint32_t *src = static_cast<const uint32_t *>(v.ptr) + 4 * (r * v.ld + c + e);
-            w4 = vv.vec_ok ? __ldg(reinterpret_cast<const uint4 *>(src))
-                           : make_uint4(__ldg(src), __ldg(src + 1), __ldg(src + 2), __ldg(src + 3));
+            if (v.e16) {   // 4 uint16 components (ADJ_IN_U16)
+              const uint16_t *src = static_cast<const uint16_t *>(v.ptr) + 4 * (r * v.ld + c + e);
+              const uint2 h2 = vv.vec_ok ? __ldg(reinterpret_cast<const uint2 *>(src))
+                                         : make_uint2((uint32_t)__ldg(src) | ((uint32_t)__ldg(src + 1) << 16),
+                                                      (uint32_t)__ldg(src + 2) | ((uint32_t)__ldg(src + 3) << 16));
+              w4 = make_uint4(h2.x & 0xFFFF, h2.x >> 16, h2.y & 0xFFFF, h2.y >> 16);
+            } else {
+              const uint32_t *src = static_cast<const uint32_t *>(v.ptr) + 4 * (r * v.ld + c + e);
+              w4 = vv.vec_ok ? __ldg(reinterpret_cast<const uint4 *>(src))
+                             : make_uint4(__ldg(src), __ldg(src + 1), __ldg(src + 2), __ldg(src + 3));
+            }
           }
           q[h][0][e] = mod_u32(w4.x, P.mod); q[h][1][e] = mod_u32(w4.y, P.mod);
           q[h][2][e] = mod_u32(w4.z, P.mod); q[h][3][e] = mod_u32(w4.w, P.mod);

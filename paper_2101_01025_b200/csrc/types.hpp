@@ -189,6 +189,7 @@ struct QuatCombParams {
   ModP mod;
   uint32_t alpha, beta;
   int32_t axpby, in32;
+  int32_t out16, pad_;     // ADJ_OUT_U16: C holds 4 uint16 components per quaternion
 };
 
 // ---------------------------------------------------------------- output-tile sharding: pack / unpack

@@ -90,7 +90,7 @@ def test_compact_io_validation_needs_no_gpu():
     for args, flags in [((4, 4, 131071, 0), I16),                 # p > 2^16: residues need 32 bits
                         ((4, 4, 8191, 0), O16 | adj.ADJ_FILL_UPPER),
                         ((4, 4, 8191, 1), O16 | adj.ADJ_HERK_ALG1),   # phi = H: 2M output only
-                        ((4, 4, 8191, 2), O16)]:                  # phi = Q
+                        ((4, 4, 65537, 2), I16)]:                 # phi = Q, p > 2^16
         with pytest.raises(adj.AdjError) as e:
             adj.adjprod_modp_ex(*args, 4096, 4, 8192, 4, flags=flags, stream=0)
         assert e.value.status == 1, (args, flags)

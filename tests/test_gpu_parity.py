@@ -598,8 +598,8 @@ def test_adjprod_T_compact_io_strided_and_errors(adj):
     for b in bad:
         with pytest.raises(adj.AdjError):
             adj.adjprod_modp_ex(m, k, b["p"], adj.ADJ_PHI_T, dA, k + 12, C32, m, flags=b["flags"])
-    with pytest.raises(adj.AdjError):   # phi = Q
-        adj.adjprod_modp_ex(m // 2, k // 4, p, adj.ADJ_PHI_Q, dA, (k + 12) // 4, C32, m // 4, flags=adj.ADJ_IN_U16)
+    with pytest.raises(adj.AdjError):   # phi = Q with p > 2^16
+        adj.adjprod_modp_ex(m // 2, k // 4, 65537, adj.ADJ_PHI_Q, dA, (k + 12) // 4, C32, m // 4, flags=adj.ADJ_IN_U16)
     with pytest.raises(adj.AdjError):   # SYRK form with a uint16 Low(C)
         adj.adjprod_modp_syrk(m, k, p, adj.ADJ_PHI_T, 3, dA, k + 12, 1, out, m + 20, flags=adj.ADJ_OUT_U16)
 
@@ -681,3 +681,28 @@ def test_adjprod_H_compact_io(adj, p, depth, m, k):
         torch.cuda.synchronize()
         got = C.cpu().numpy().view(np.uint32).reshape(m, m, 2)
         assert np.array_equal(got[lo], ref[lo]), (p, m, k, "alg1")
+
+
+@pytest.mark.parametrize("p", [251, 8191, 65521])
+@pytest.mark.parametrize("depth", [0, 1])
+@pytest.mark.parametrize("m,k", [(1, 3), (129, 200), (260, 131)])
+def test_adjprod_Q_compact_io(adj, p, depth, m, k):
+    """ADJ_IN_U16 / ADJ_OUT_U16 for phi = Q (6M): 4 uint16 components in (any value, read mod p)
+    and out, every combination, strided."""
+    import torch
+    rng = np.random.default_rng(m * 3 + k + p + depth)
+    lda = k + 2
+    M16 = rng.integers(0, 1 << 16, size=(m, lda, 4), dtype=np.uint16)
+    Mred = (M16[:, :k].astype(np.uint32) % p).astype(np.uint32)
+    ref = oracle.syrk_q(Mred, p)
+    dM16 = torch.from_numpy(M16.reshape(m, lda * 4).view(np.int16)).cuda()
+    dM32 = torch.from_numpy(np.ascontiguousarray(Mred).reshape(m, k * 4).view(np.int32)).cuda()
+    lo = np.tril(np.ones((m, m), dtype=bool))
+    for dM, ld in ((dM16, lda), (dM32, k)):
+        for out16 in (False, True):
+            C = torch.zeros((m, m * 4), dtype=torch.int16 if out16 else torch.int32, device="cuda")
+            flags = (adj.ADJ_IN_U16 if dM.element_size() == 2 else 0) | (adj.ADJ_OUT_U16 if out16 else 0)
+            adj.adjprod_modp_ex(m, k, p, adj.ADJ_PHI_Q, dM, ld, C, m, depth=depth, flags=flags)
+            torch.cuda.synchronize()
+            got = C.cpu().numpy().view(np.uint16 if out16 else np.uint32).astype(np.uint32).reshape(m, m, 4)
+            assert np.array_equal(got[lo], ref[lo]), (p, depth, m, k, dM.element_size(), out16)
