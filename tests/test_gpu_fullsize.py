@@ -107,16 +107,25 @@ def test_c5_vandermonde_hermitian(env):
             np.array_equal(Ch[r, : r + 1, 1].astype(np.int64), im), r
 
 
-def test_q5_quaternion_sampled_rows(env):
-    """SURVEY §8(f)-4 at the bench's q5 size (8192^2 over H_GF(8191), Alg. 2M3M)."""
+@pytest.mark.parametrize("io16", [True, False])
+def test_q5_quaternion_sampled_rows(env, io16):
+    """SURVEY §8(f)-4 at the bench's q5 size (8192^2 over H_GF(8191), Alg. 2M3M), in the bench's
+    uint16 storage and in uint32."""
     torch, adj, bench = env
     from inputs.gpu import uniform_residues_cuda
     cfg = bench.CONFIGS["q5"]
     m, k, p = cfg["m"], cfg["k"], cfg["p"]
     A = torch.empty((m, k * 4), dtype=torch.int32, device="cuda")
     uniform_residues_cuda(A, seed=1, p=p)
-    C = torch.zeros((m, m * 4), dtype=torch.int32, device="cuda")
-    adj.adjprod_modp_ex(m, k, p, adj.ADJ_PHI_Q, A, k, C, m)
+    if io16:
+        C16 = torch.zeros((m, m * 4), dtype=torch.int16, device="cuda")
+        adj.adjprod_modp_ex(m, k, p, adj.ADJ_PHI_Q, A.to(torch.int16), k, C16, m,
+                            flags=adj.ADJ_IN_U16 | adj.ADJ_OUT_U16)
+        C = C16.to(torch.int32) & 0xFFFF
+        del C16
+    else:
+        C = torch.zeros((m, m * 4), dtype=torch.int32, device="cuda")
+        adj.adjprod_modp_ex(m, k, p, adj.ADJ_PHI_Q, A, k, C, m)
     torch.cuda.synchronize()
     Ah = A.cpu().numpy().view(np.uint32).reshape(m, k, 4)
     Ch = C.cpu().numpy().view(np.uint32).reshape(m, m, 4)
