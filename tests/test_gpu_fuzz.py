@@ -69,7 +69,7 @@ def test_fuzz_phi_t(adj, case):
 PRIMES_3MOD4 = [3, 251, 8191, 16763, 16787, 65519, 131071, 262139]
 
 
-@pytest.mark.parametrize("case", range(40))
+@pytest.mark.parametrize("case", range(80))
 def test_fuzz_phi_h_and_q(adj, case):
     """phi = H (2M, or one level of Alg. 1 over GF(p^2)) and phi = Q (6M): random ragged shapes,
     depths, strides, plain / FILL_UPPER."""
@@ -81,19 +81,30 @@ def test_fuzz_phi_h_and_q(adj, case):
     m, k = int(rng.integers(1, 300)), int(rng.integers(1, 300))
     depth = int(rng.integers(0, 3))
     lda, ldc = k + int(rng.integers(0, 5)), m + int(rng.integers(0, 5))
-    Araw = rng.integers(0, 1 << 32, size=(m, lda, w), dtype=np.uint64).astype(np.uint32)
-    A = (Araw[:, :k] % p).astype(np.uint32)
-    dA = torch.from_numpy(Araw.reshape(m, lda * w).view(np.int32)).cuda()
-    ref = oracle.syrk_h(A, p) if phi == "H" else oracle.syrk_q(A, p)
-    C0 = rng.integers(0, 1 << 32, size=(m, ldc, w), dtype=np.uint64).astype(np.uint32)
-    C = torch.from_numpy(C0.reshape(m, ldc * w).view(np.int32).copy()).cuda()
     alg1 = phi == "H" and rng.random() < 0.5
     fill = rng.random() < 0.3
-    flags = (adj.ADJ_HERK_ALG1 if alg1 else 0) | (adj.ADJ_FILL_UPPER if fill else 0)
+    in16 = p < 65536 and rng.random() < 0.4
+    out16 = in16 and not (alg1 or fill) and rng.random() < 0.7
+    if in16:
+        Araw = rng.integers(0, 1 << 16, size=(m, lda, w), dtype=np.uint16)
+        dA = torch.from_numpy(Araw.reshape(m, lda * w).view(np.int16)).cuda()
+    else:
+        Araw = rng.integers(0, 1 << 32, size=(m, lda, w), dtype=np.uint64).astype(np.uint32)
+        dA = torch.from_numpy(Araw.reshape(m, lda * w).view(np.int32)).cuda()
+    A = (Araw[:, :k].astype(np.uint32) % p).astype(np.uint32)
+    ref = oracle.syrk_h(A, p) if phi == "H" else oracle.syrk_q(A, p)
+    if out16:
+        C0 = rng.integers(0, 1 << 16, size=(m, ldc, w), dtype=np.uint64).astype(np.uint32)
+        C = torch.from_numpy(C0.astype(np.uint16).reshape(m, ldc * w).view(np.int16).copy()).cuda()
+    else:
+        C0 = rng.integers(0, 1 << 32, size=(m, ldc, w), dtype=np.uint64).astype(np.uint32)
+        C = torch.from_numpy(C0.reshape(m, ldc * w).view(np.int32).copy()).cuda()
+    flags = ((adj.ADJ_HERK_ALG1 if alg1 else 0) | (adj.ADJ_FILL_UPPER if fill else 0)
+             | (adj.ADJ_IN_U16 if in16 else 0) | (adj.ADJ_OUT_U16 if out16 else 0))
     adj.adjprod_modp_ex(m, k, p, adj.ADJ_PHI_H if phi == "H" else adj.ADJ_PHI_Q, dA, lda, C, ldc,
                         depth=1 if alg1 else depth, flags=flags)
     torch.cuda.synchronize()
-    got = C.cpu().numpy().view(np.uint32).reshape(m, ldc, w)
+    got = C.cpu().numpy().view(np.uint16 if out16 else np.uint32).astype(np.uint32).reshape(m, ldc, w)
     lo = np.tril(np.ones((m, m), dtype=bool))
     assert np.array_equal(got[:, :m][lo], ref[lo]), (phi, p, m, k, depth, alg1)
     if fill:   # Up(C) = phi(Low(C)): conjugation negates the imaginary components
