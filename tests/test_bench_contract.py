@@ -76,3 +76,23 @@ def test_gpu_arm_json_line():
     assert e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0 and e["last_row_matches_device_result"]
     assert d["parity"]["bit_exact"]
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
+
+
+def test_hbm_bytes_compact_halves_the_residue_terms():
+    """Only the caller-residue terms (reading A, writing Low(C)) shrink with uint16 storage; the
+    limb planes and the narrow product buffers do not."""
+    for name, depth in (("c2", 0), ("c2", 1), ("c5", 0), ("q5", 0)):
+        cfg = bench.CONFIGS[name]
+        m, k = cfg["m"], cfg["k"]
+        w = {"T": 1, "H": 2, "Q": 4}[cfg["phi"]]
+        b4, b2 = bench.hbm_bytes(cfg, depth, res_bytes=4), bench.hbm_bytes(cfg, depth, res_bytes=2)
+        assert b4["preadd"] - b2["preadd"] == 2 * w * m * k
+        if b4["combine"] is not None:
+            assert b4["combine"] - b2["combine"] == 2 * w * m * (m + 1) // 2
+
+
+def test_bench_help():
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--help"], capture_output=True, text=True,
+                         cwd=ROOT, timeout=120, check=True).stdout
+    for flag in ("--gpus", "--steps", "--warmup", "--config", "--impl", "--io", "--dist", "--sustain-s"):
+        assert flag in out
