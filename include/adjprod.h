@@ -183,12 +183,21 @@ adj_status_t adj_mod_lower(int64_t m, uint32_t p, adj_phi_t phi, uint32_t *X, in
 /* rank 0 creates an id (host buffer of 128 bytes); ship it to the other ranks out of band */
 adj_status_t adj_comm_get_unique_id(uint8_t id[128]);
 adj_status_t adj_comm_init(int nranks, const uint8_t id[128], int rank, adj_comm_t *comm);
+/* adj_comm_destroy -- releases the communicator.  Collective (every rank calls it) once an
+ *   ADJ_DIST_P2P call has set up the exchange window: importers unmap it, a barrier follows, then
+ *   the root frees it (CUDA IPC requires importers to close before the exporter frees). */
 adj_status_t adj_comm_destroy(adj_comm_t comm);
 
 /* adj_dist_kslice -- the column slice [k0, k1) of A that rank `rank` of `nranks` owns in
  *   adjprod_modp_dist (host, no GPU): per = ceil(k / nranks) rounded up to a multiple of 8,
  *   k0 = min(k, rank * per), k1 = min(k, k0 + per).  Slices are disjoint and cover [0, k). */
 adj_status_t adj_dist_kslice(int64_t k, int nranks, int rank, int64_t *k0, int64_t *k1);
+
+/* adj_elem_bytes -- bytes of one element of A as the entry points read it (host, no GPU):
+ *   (2 with ADJ_IN_U16 in `flags`, else 4) x the words per element of phi (T 1, H 2, Q 4).
+ *   Rank r's k-slice of a row-major A starts at byte offset k0 * adj_elem_bytes(...) of each row
+ *   (adjprod_modp_dist, split-K).  INVALID_VALUE for a null output or an unknown phi. */
+adj_status_t adj_elem_bytes(adj_phi_t phi, uint32_t flags, int64_t *bytes);
 
 /*
  * adjprod_modp_shard -- output-tile sharding, phi = ADJ_PHI_T, depth 0 or 1

@@ -9,7 +9,7 @@ import ctypes
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("ADJ_LIB_PATH") or os.path.join(_PKG, "libadjprod.so")   # override: dev A/B only
+LIB_PATH = os.path.join(_PKG, "libadjprod.so")
 
 ADJ_PHI_T = 0
 ADJ_PHI_H = 1
@@ -26,7 +26,7 @@ STATUS = {0: "ADJ_OK", 1: "ADJ_ERR_INVALID_VALUE", 2: "ADJ_ERR_UNSUPPORTED_MODUL
 # every symbol include/adjprod.h declares (checked by tests/test_abi.py)
 EXPORTS = ["adjprod_modp", "adjprod_modp_ex", "adjprod_modp_syrk", "adjprod_modp_workspace_size", "adjprod_modp_auto_depth",
            "gemm_modp", "adj_skew_unitary", "adj_sos", "adj_mod_lower", "adj_comm_get_unique_id",
-           "adj_comm_init", "adj_comm_destroy", "adjprod_modp_dist", "adj_dist_kslice", "adjprod_modp_shard", "adj_shard_layout", "adjprod_modp_partial", "adj_sum_partials", "adj_shard_pack", "adj_status_string", "adj_last_error",
+           "adj_comm_init", "adj_comm_destroy", "adjprod_modp_dist", "adj_dist_kslice", "adj_elem_bytes", "adjprod_modp_shard", "adj_shard_layout", "adjprod_modp_partial", "adj_sum_partials", "adj_shard_pack", "adj_status_string", "adj_last_error",
            "adj_launch_count", "adj_launch_count_reset", "adj_profile_enable", "adj_profile_read"]
 
 
@@ -67,6 +67,7 @@ def lib() -> ctypes.CDLL:
             "adj_comm_destroy": [vp],
             "adjprod_modp_dist": [i64, i64, u32, ci, vp, i64, vp, i64, ci, vp, ctypes.POINTER(adj_opts_t), vp],
             "adj_dist_kslice": [i64, ci, ci, ctypes.POINTER(i64), ctypes.POINTER(i64)],
+            "adj_elem_bytes": [ci, u32, ctypes.POINTER(i64)],
             "adjprod_modp_shard": [i64, i64, u32, ci, vp, i64, vp, i64, ci, ci, ctypes.POINTER(adj_opts_t), vp],
             "adjprod_modp_partial": [i64, i64, u32, ci, vp, i64, vp, i64, ctypes.POINTER(adj_opts_t), vp],
             "adj_sum_partials": [i64, u32, vp, i64, i64, ci, vp, i64, vp],
@@ -228,6 +229,13 @@ def adj_dist_kslice(k, nranks, rank):
     k0, k1 = ctypes.c_int64(0), ctypes.c_int64(0)
     _check(lib().adj_dist_kslice(k, nranks, rank, ctypes.byref(k0), ctypes.byref(k1)), "adj_dist_kslice")
     return k0.value, k1.value
+
+
+def adj_elem_bytes(phi, flags=0) -> int:
+    """bytes of one element of A as the entry points read it (rank r's k-slice offset = k0 x this)"""
+    b = ctypes.c_int64(0)
+    _check(lib().adj_elem_bytes(phi, flags, ctypes.byref(b)), "adj_elem_bytes")
+    return b.value
 
 
 def adj_launch_count() -> int:

@@ -174,17 +174,64 @@ adj_status_t encode_arena(CUtensorMap *map, void *base, int64_t kpad, int64_t ro
   return ADJ_OK;
 }
 
+// SM count of the current device for host-only queries (workspace size, shard layout); 148
+// (B200) when no device is visible -- the plan's only SM dependence is the tail split and its
+// fixup slots, which are sized for num_sms / 2 pieces
+int query_sms() {
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess &&
+      sms > 0)
+    return sms;
+  cudaGetLastError();
+  return 148;
+}
+
 // ------------------------------------------------------------------ plan cache
-// dev, kind, m, n, k, p, phi, depth, shard rank, shard count
+// dev, kind, m, n, k, p, phi, depth, shard rank, shard count.  Bounded (LRU): an evicted plan's
+// device tile arrays are released with cudaFree, which waits for the launches that read them.
 using Key = std::tuple<int, int, int64_t, int64_t, int64_t, uint32_t, int, int, int, int>;
-std::map<Key, std::unique_ptr<Plan>> g_plans;
+struct CachedPlan {
+  std::unique_ptr<Plan> plan;
+  uint64_t last_use = 0;
+};
+std::map<Key, CachedPlan> g_plans;
+uint64_t g_plan_clock = 0;
+constexpr size_t kMaxCachedPlans = 64;
+
+void free_plan_device(Plan &P) {
+  if (P.d_tiles) cudaFree(P.d_tiles);
+  if (P.d_comb_pairs) cudaFree(P.d_comb_pairs);
+  if (P.d_fixups) cudaFree(P.d_fixups);
+  P.d_tiles = nullptr;
+  P.d_comb_pairs = nullptr;
+  P.d_fixups = nullptr;
+}
+
+void evict_plans() {   // caller holds g_mu
+  while (g_plans.size() >= kMaxCachedPlans) {
+    auto lru = g_plans.begin();
+    for (auto it = g_plans.begin(); it != g_plans.end(); ++it)
+      if (it->second.last_use < lru->second.last_use) lru = it;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(lru->second.plan->dev);
+    free_plan_device(*lru->second.plan);
+    cudaSetDevice(cur);
+    g_plans.erase(lru);
+  }
+}
 
 adj_status_t get_plan(Plan **out, int kind, int64_t m, int64_t n, int64_t k, uint32_t p, int phi, int depth, int dev,
                       int sms, int shard_rank = -1, int shard_n = 0) {
   std::lock_guard<std::mutex> lk(g_mu);
   Key key{dev, kind, m, n, k, p, phi, depth, shard_rank, shard_n};
   auto it = g_plans.find(key);
-  if (it != g_plans.end()) { *out = it->second.get(); return ADJ_OK; }
+  if (it != g_plans.end()) {
+    it->second.last_use = ++g_plan_clock;
+    *out = it->second.plan.get();
+    return ADJ_OK;
+  }
+  evict_plans();
   auto P = std::make_unique<Plan>();
   const char *err = nullptr;
   bool ok = kind == PLAN_GEMM    ? build_gemm_plan(*P, m, n, k, p, sms, &err)
@@ -192,21 +239,25 @@ adj_status_t get_plan(Plan **out, int kind, int64_t m, int64_t n, int64_t k, uin
                                  : build_syrk_plan(*P, m, k, p, phi, depth, sms, &err, shard_rank, shard_n);
   if (!ok) return fail(ADJ_ERR_INVALID_VALUE, "plan: %s", err ? err : "unsupported");
   P->dev = dev;
-  if (!P->tiles.empty()) {
-    CUDA_TRY(cudaMalloc(&P->d_tiles, P->tiles.size() * sizeof(uint32_t)));
-    CUDA_TRY(cudaMemcpy(P->d_tiles, P->tiles.data(), P->tiles.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
-  }
-  if (!P->comb_pairs.empty()) {
-    CUDA_TRY(cudaMalloc(&P->d_comb_pairs, P->comb_pairs.size() * sizeof(uint32_t)));
-    CUDA_TRY(cudaMemcpy(P->d_comb_pairs, P->comb_pairs.data(), P->comb_pairs.size() * sizeof(uint32_t),
-                        cudaMemcpyHostToDevice));
-  }
-  if (!P->fixups.empty()) {
-    CUDA_TRY(cudaMalloc(&P->d_fixups, P->fixups.size() * sizeof(FixupTile)));
-    CUDA_TRY(cudaMemcpy(P->d_fixups, P->fixups.data(), P->fixups.size() * sizeof(FixupTile), cudaMemcpyHostToDevice));
+  auto upload = [&](void **dst, const void *src, size_t bytes) -> cudaError_t {
+    if (bytes == 0) return cudaSuccess;
+    cudaError_t e = cudaMalloc(dst, bytes);
+    return e != cudaSuccess ? e : cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice);
+  };
+  cudaError_t e = upload(reinterpret_cast<void **>(&P->d_tiles), P->tiles.data(), P->tiles.size() * sizeof(uint32_t));
+  if (e == cudaSuccess)
+    e = upload(reinterpret_cast<void **>(&P->d_comb_pairs), P->comb_pairs.data(), P->comb_pairs.size() * sizeof(uint32_t));
+  if (e == cudaSuccess)
+    e = upload(reinterpret_cast<void **>(&P->d_fixups), P->fixups.data(), P->fixups.size() * sizeof(FixupTile));
+  if (e != cudaSuccess) {
+    free_plan_device(*P);
+    return fail(ADJ_ERR_CUDA, "plan upload: %s", cudaGetErrorString(e));
   }
   *out = P.get();
-  g_plans.emplace(key, std::move(P));
+  CachedPlan cp;
+  cp.plan = std::move(P);
+  cp.last_use = ++g_plan_clock;
+  g_plans.emplace(key, std::move(cp));
   return ADJ_OK;
 }
 
@@ -670,7 +721,8 @@ adj_status_t adjprod_modp_workspace_size(int64_t m, int64_t k, uint32_t p, adj_p
   if (herk1 && depth != 1) return fail(ADJ_ERR_INVALID_VALUE, "ADJ_HERK_ALG1 runs exactly one level (depth 1 or -1)");
   Plan P;
   const char *err = nullptr;
-  if (!(herk1 ? build_herk1_plan(P, m, k, p, 148, &err) : build_syrk_plan(P, m, k, p, (int)phi, depth, 148, &err)))
+  const int sms = query_sms();
+  if (!(herk1 ? build_herk1_plan(P, m, k, p, sms, &err) : build_syrk_plan(P, m, k, p, (int)phi, depth, sms, &err)))
     return fail(ADJ_ERR_INVALID_VALUE, "plan: %s", err ? err : "unsupported");
   *bytes = P.ws_bytes;
   return ADJ_OK;
@@ -696,12 +748,11 @@ static adj_status_t adjprod_impl(int64_t m, int64_t k, uint32_t p, adj_phi_t phi
   const int w = adj_phi_width(phi);
   if (k == 0 || alpha == 0) {  // Low(C) = beta Low(C)
     if (out16) {
-      uint16_t *C16 = reinterpret_cast<uint16_t *>(C);
-      for (int64_t i = 0; i < m; ++i) CUDA_TRY(cudaMemsetAsync(C16 + i * ldc * w, 0, (size_t)(i + 1) * 2 * w, s));
+      LAUNCH(launch_zero_lower(m, C, ldc * w * 2, 2 * w, s));
       return ADJ_OK;
     }
     if (beta == 0) {
-      for (int64_t i = 0; i < m; ++i) CUDA_TRY(cudaMemsetAsync(C + i * ldc * w, 0, (size_t)(i + 1) * w * 4, s));
+      LAUNCH(launch_zero_lower(m, C, ldc * w * 4, 4 * w, s));
     } else {
       LAUNCH(launch_scale_lower(m, w, C, ldc, beta, make_modp(p), s));
     }
@@ -765,17 +816,21 @@ adj_status_t adjprod_modp_shard(int64_t m, int64_t k, uint32_t p, adj_phi_t phi,
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   Plan *P = nullptr;
   if ((st = shard_plan(&P, m, k, p, depth, rank, nranks, dev, sms)) != ADJ_OK) return st;
-  if (k == 0) {   // Low(C) = 0 on the owned regions
-    for (const ShardRect &R : P->shard_rects) {
-      if (!R.lower) {
-        CUDA_TRY(cudaMemset2DAsync(C + R.r0 * ldc + R.c0, (size_t)ldc * 4, 0, (size_t)R.cols * 4, (size_t)R.rows, s));
-      } else {
-        for (int64_t i = 0; i < R.rows; ++i) {
-          const int64_t n = std::min(R.cols, R.r0 + i - R.c0 + 1);
-          if (n > 0) CUDA_TRY(cudaMemsetAsync(C + (R.r0 + i) * ldc + R.c0, 0, (size_t)n * 4, s));
-        }
-      }
+  if (k == 0) {   // Low(C) = 0 on the owned regions: one launch over the region list
+    if (P->shard_rects.empty()) return ADJ_OK;
+    std::vector<RectDev> rd(P->shard_rects.size());
+    int max_rows = 0;
+    for (size_t i = 0; i < rd.size(); ++i) {
+      const ShardRect &R = P->shard_rects[i];
+      rd[i].r0 = R.r0; rd[i].c0 = R.c0; rd[i].rows = R.rows; rd[i].cols = R.cols;
+      rd[i].lower = R.lower ? 1 : 0; rd[i].pad_ = 0; rd[i].off = 0;
+      max_rows = std::max<int>(max_rows, (int)R.rows);
     }
+    void *d = nullptr;
+    CUDA_TRY(adj_pool_alloc(&d, rd.size() * sizeof(RectDev), s));
+    CUDA_TRY(cudaMemcpyAsync(d, rd.data(), rd.size() * sizeof(RectDev), cudaMemcpyHostToDevice, s));
+    LAUNCH(launch_rect_copy(static_cast<RectDev *>(d), (int)rd.size(), max_rows, C, ldc, d, 4, 2, s));
+    CUDA_TRY(cudaFreeAsync(d, s));
     return ADJ_OK;
   }
   Ptrs x;
@@ -801,7 +856,9 @@ adj_status_t adjprod_modp_shard(int64_t m, int64_t k, uint32_t p, adj_phi_t phi,
 adj_status_t adjprod_modp_partial(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, const uint32_t *A, int64_t lda,
                                   void *R, int64_t ldr, const adj_opts_t *opts, adj_stream_t stream) {
   const uint32_t flags = opts ? opts->flags : 0;
-  adj_status_t st = validate_syrk(m, k, p, phi, A, lda, static_cast<const uint32_t *>(R), ldr, flags & ADJ_IN_U16);
+  // R holds uint16 residues for p < 2^16 (ADJ_OUT_U16's width for the overlap check), uint32 otherwise
+  adj_status_t st = validate_syrk(m, k, p, phi, A, lda, static_cast<const uint32_t *>(R), ldr,
+                                  (flags & ADJ_IN_U16) | (p < 65536 ? ADJ_OUT_U16 : 0u));
   if (st != ADJ_OK) return st;
   if (phi != ADJ_PHI_T) return fail(ADJ_ERR_INVALID_VALUE, "adjprod_modp_partial supports phi = ADJ_PHI_T");
   if (flags & ADJ_OUT_U16) return fail(ADJ_ERR_INVALID_VALUE, "ADJ_OUT_U16 is an adjprod_modp_ex flag");
@@ -817,7 +874,7 @@ adj_status_t adjprod_modp_partial(int64_t m, int64_t k, uint32_t p, adj_phi_t ph
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   uint16_t *R16 = static_cast<uint16_t *>(R);
   if (k == 0) {
-    for (int64_t i = 0; i < m; ++i) CUDA_TRY(cudaMemsetAsync(R16 + i * ldr, 0, (size_t)(i + 1) * 2, s));
+    LAUNCH(launch_zero_lower(m, R16, ldr * 2, 2, s));
     return ADJ_OK;
   }
   const int depth = (opts && opts->depth >= 0) ? opts->depth : auto_depth(m, k, p, 0);
@@ -871,7 +928,7 @@ adj_status_t adj_shard_layout(int64_t m, int64_t k, uint32_t p, int depth, int r
   if (d > 1) return fail(ADJ_ERR_INVALID_VALUE, "output-tile sharding runs at depth 0 or 1 (got %d)", d);
   Plan P;
   const char *err = nullptr;
-  if (!build_syrk_plan(P, m, std::max<int64_t>(k, 1), p, 0, d, 148, &err, rank, nranks))
+  if (!build_syrk_plan(P, m, std::max<int64_t>(k, 1), p, 0, d, query_sms(), &err, rank, nranks))
     return fail(ADJ_ERR_INVALID_VALUE, "plan: %s", err ? err : "unsupported");
   *n_rects = (int64_t)P.shard_rects.size();
   for (size_t i = 0; i < P.shard_rects.size(); ++i) {

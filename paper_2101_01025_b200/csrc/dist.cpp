@@ -77,10 +77,61 @@ bool load_nccl() {
 
 }  // namespace
 
+namespace {
+adj_status_t ensure_scratch(adj_comm_t comm) {
+  if (!comm->d_scratch && cudaMalloc(&comm->d_scratch, 64) != cudaSuccess) return ADJ_ERR_CUDA;
+  return ADJ_OK;
+}
+
+// every rank's status -> the worst one, on every rank (a 4-byte NCCL max all-reduce and a stream
+// synchronisation), so that no rank enters a collective its peers skipped after a local failure
+adj_status_t agree_status(adj_comm_t comm, adj_status_t st, cudaStream_t s) {
+  if (comm->nranks == 1) return st;
+  if (ensure_scratch(comm) != ADJ_OK) return ADJ_ERR_CUDA;   // (a peer then fails its all-reduce: NCCL error)
+  int32_t v = (int32_t)st;
+  if (cudaMemcpyAsync(comm->d_scratch, &v, 4, cudaMemcpyHostToDevice, s) != cudaSuccess) return ADJ_ERR_CUDA;
+  if (g_nccl.AllReduce(comm->d_scratch, comm->d_scratch, 1, ncclInt32, ncclMax, comm->comm, s) != ncclSuccess)
+    return ADJ_ERR_NCCL;
+  if (cudaMemcpyAsync(&v, comm->d_scratch, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess) return ADJ_ERR_CUDA;
+  if (cudaStreamSynchronize(s) != cudaSuccess) return ADJ_ERR_CUDA;
+  return (adj_status_t)v;
+}
+
+// a barrier over the communicator (4-byte all-reduce, then the stream is synchronised)
+adj_status_t host_barrier(adj_comm_t comm, cudaStream_t s) {
+  if (ensure_scratch(comm) != ADJ_OK) return ADJ_ERR_CUDA;
+  if (g_nccl.AllReduce(comm->d_scratch, comm->d_scratch, 1, ncclInt32, ncclSum, comm->comm, s) != ncclSuccess)
+    return ADJ_ERR_NCCL;
+  return cudaStreamSynchronize(s) == cudaSuccess ? ADJ_OK : ADJ_ERR_CUDA;
+}
+
+// releases the exchange window in the order CUDA IPC requires: importers close their mappings,
+// a barrier, then the root frees the exported allocation
+adj_status_t release_window(adj_comm_t comm, cudaStream_t s) {
+  if (!comm->win) return ADJ_OK;
+  if (!comm->win_owned) cudaIpcCloseMemHandle(comm->win);
+  adj_status_t st = comm->nranks > 1 ? host_barrier(comm, s) : ADJ_OK;
+  if (comm->win_owned) cudaFree(comm->win);
+  comm->win = nullptr;
+  comm->win_bytes = 0;
+  comm->win_root = -1;
+  return st;
+}
+
+}  // namespace
+
 int adj_phi_width(adj_phi_t phi);                                    // api.cpp
 cudaError_t adj_pool_alloc(void **ptr, size_t bytes, cudaStream_t s);   // api.cpp: retained workspace pool
 
 namespace {
+// rank r's column slice of A starts k0 elements into each row: k0 x (uint16 | uint32 words) x
+// phi's width bytes (adj_elem_bytes)
+const uint32_t *kslice_ptr(const uint32_t *A, adj_phi_t phi, uint32_t flags, int64_t k0) {
+  int64_t ea = 0;
+  if (!A || adj_elem_bytes(phi, flags, &ea) != ADJ_OK) return A;
+  return reinterpret_cast<const uint32_t *>(reinterpret_cast<const uint8_t *>(A) + k0 * ea);
+}
+
 // the packed regions (RectDev, buffer offsets) of `rank` for this problem
 adj_status_t rank_rects(int64_t m, int64_t k, uint32_t p, int depth, int rank, int G, std::vector<adj::RectDev> &out,
                         int64_t *elems, int *max_rows) {
@@ -110,9 +161,10 @@ adj_status_t dist_tiles(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, const u
                         int64_t ldc, int root, adj_comm_t comm, const adj_opts_t *opts, adj_stream_t stream) {
   const int G = comm->nranks, r = comm->rank;
   adj_status_t st = adjprod_modp_shard(m, k, p, phi, A, lda, C, ldc, r, G, opts, stream);
-  if (st != ADJ_OK || G == 1) return st;
+  if (G == 1) return st;
   if (!load_nccl()) return ADJ_ERR_NCCL;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if ((st = agree_status(comm, st, s)) != ADJ_OK) return st;
   const int depth = opts ? opts->depth : -1;
   std::vector<std::vector<adj::RectDev>> rects((size_t)G);
   std::vector<int64_t> elems((size_t)G, 0);
@@ -144,6 +196,9 @@ adj_status_t dist_tiles(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, const u
       adj::launch_rect_copy(drects[(size_t)r], (int)rects[(size_t)r].size(), max_rows[(size_t)r], C, ldc, bufs[(size_t)r],
                             esize, 1, s) != cudaSuccess)
     st = ADJ_ERR_CUDA;
+  // a local failure (allocation, launch) on one rank must not leave its peers blocked in the
+  // send / recv group: agree on the status first
+  st = agree_status(comm, st, s);
   if (st == ADJ_OK) {
     g_nccl.GroupStart();
     for (int q = 0; q < G; ++q) {
@@ -169,22 +224,30 @@ adj_status_t dist_tiles(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, const u
 }
 
 // the root's exchange window (G slots of m x m narrow residues), mapped on every rank
+// (collective: every rank calls it with the same root and size, so all take the same branch)
 adj_status_t setup_window(adj_comm_t comm, int root, size_t bytes, cudaStream_t s) {
   if (comm->win && comm->win_root == root && comm->win_bytes >= bytes) return ADJ_OK;
-  if (comm->win) {
-    if (comm->win_owned) cudaFree(comm->win);
-    else cudaIpcCloseMemHandle(comm->win);
-    comm->win = nullptr;
-  }
-  if (!comm->d_scratch && cudaMalloc(&comm->d_scratch, 64) != cudaSuccess) return ADJ_ERR_CUDA;
+  adj_status_t st = release_window(comm, s);
+  if (st != ADJ_OK) return st;
+  if (ensure_scratch(comm) != ADJ_OK) return ADJ_ERR_CUDA;
   cudaIpcMemHandle_t h;
   static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  st = ADJ_OK;
   if (comm->rank == root) {
-    if (cudaMalloc(&comm->win, bytes) != cudaSuccess) return ADJ_ERR_CUDA;
-    comm->win_owned = true;
-    if (cudaIpcGetMemHandle(&h, comm->win) != cudaSuccess) return ADJ_ERR_CUDA;
-    if (cudaMemcpyAsync(comm->d_scratch, &h, 64, cudaMemcpyHostToDevice, s) != cudaSuccess) return ADJ_ERR_CUDA;
+    if (cudaMalloc(&comm->win, bytes) != cudaSuccess) { comm->win = nullptr; st = ADJ_ERR_CUDA; }
+    else {
+      comm->win_owned = true;
+      if (cudaIpcGetMemHandle(&h, comm->win) != cudaSuccess) st = ADJ_ERR_CUDA;
+    }
   }
+  // the root's allocation failing must not leave the other ranks waiting in the broadcast
+  if ((st = agree_status(comm, st, s)) != ADJ_OK) {
+    if (comm->win && comm->win_owned) cudaFree(comm->win);
+    comm->win = nullptr;
+    return st;
+  }
+  if (comm->rank == root &&
+      cudaMemcpyAsync(comm->d_scratch, &h, 64, cudaMemcpyHostToDevice, s) != cudaSuccess) return ADJ_ERR_CUDA;
   if (g_nccl.Broadcast(comm->d_scratch, comm->d_scratch, 64, ncclUint8, root, comm->comm, s) != ncclSuccess)
     return ADJ_ERR_NCCL;
   if (cudaStreamSynchronize(s) != cudaSuccess) return ADJ_ERR_CUDA;
@@ -221,8 +284,7 @@ adj_status_t dist_p2p(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, const uin
   void *mine = static_cast<uint8_t *>(comm->win) + (size_t)r * slot * esize;
   adj_opts_t o = opts ? *opts : adj_opts_t{-1, 0, nullptr, 0};
   o.flags &= ADJ_IN_U16;
-  const size_t ea = (o.flags & ADJ_IN_U16) ? 2 : 4;   // bytes per element of A
-  const uint32_t *Ar = A ? reinterpret_cast<const uint32_t *>(reinterpret_cast<const uint8_t *>(A) + k0 * ea) : nullptr;
+  const uint32_t *Ar = kslice_ptr(A, phi, o.flags, k0);
   st = adjprod_modp_partial(m, k1 - k0, p, phi, Ar, lda, mine, m, &o, stream);
   if (st != ADJ_OK) return st;
   // barrier 2: every rank's partial kernels (and their peer stores) have completed
@@ -263,9 +325,11 @@ adj_status_t adj_comm_init(int nranks, const uint8_t id[128], int rank, adj_comm
 
 adj_status_t adj_comm_destroy(adj_comm_t comm) {
   if (!comm) return ADJ_ERR_INVALID_VALUE;
-  if (comm->win) {
-    if (comm->win_owned) cudaFree(comm->win);
-    else cudaIpcCloseMemHandle(comm->win);
+  if (comm->win) {   // collective when a P2P window exists: importers close, barrier, the root frees
+    cudaStream_t s = nullptr;
+    cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    release_window(comm, s);
+    if (s) cudaStreamDestroy(s);
   }
   if (comm->d_scratch) cudaFree(comm->d_scratch);
   if (g_nccl.loaded) g_nccl.CommDestroy(comm->comm);
@@ -278,6 +342,12 @@ adj_status_t adj_dist_kslice(int64_t k, int nranks, int rank, int64_t *k0, int64
   const int64_t per = ((k + nranks - 1) / nranks + 7) / 8 * 8;
   *k0 = std::min<int64_t>(k, (int64_t)rank * per);
   *k1 = std::min<int64_t>(k, *k0 + per);
+  return ADJ_OK;
+}
+
+adj_status_t adj_elem_bytes(adj_phi_t phi, uint32_t flags, int64_t *bytes) {
+  if (!bytes || (phi != ADJ_PHI_T && phi != ADJ_PHI_H && phi != ADJ_PHI_Q)) return ADJ_ERR_INVALID_VALUE;
+  *bytes = (int64_t)((flags & ADJ_IN_U16) ? 2 : 4) * adj_phi_width(phi);
   return ADJ_OK;
 }
 
@@ -295,8 +365,7 @@ adj_status_t adjprod_modp_dist(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, 
   const int w = adj_phi_width(phi);
   int64_t k0 = 0, k1 = 0;
   adj_dist_kslice(k, G, r, &k0, &k1);
-  const size_t ea = (opts && (opts->flags & ADJ_IN_U16)) ? 2 : 4 * (size_t)w;   // bytes per element of A
-  const uint32_t *Ar = A ? reinterpret_cast<const uint32_t *>(reinterpret_cast<const uint8_t *>(A) + k0 * ea) : nullptr;
+  const uint32_t *Ar = kslice_ptr(A, phi, opts ? opts->flags : 0, k0);
   if (G == 1) return adjprod_modp_ex(m, k1 - k0, p, phi, Ar, lda, C, ldc, opts, stream);
   if (!load_nccl()) return ADJ_ERR_NCCL;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);

@@ -21,7 +21,9 @@ cudaError_t launch_scale_lower(int64_t m, int w, uint32_t *X, int64_t ldx, uint3
                                cudaStream_t s);
 cudaError_t launch_mod_lower(int64_t m, int w, const uint32_t *src, int64_t lds, uint32_t *dst, int64_t ldd,
                              const ModP &mod, cudaStream_t s);
-// pack (to_buf = 1) / unpack (to_buf = 0) the listed regions of C into / from a contiguous buffer
+// Low(X) <- 0, elements of esz bytes (even), one launch
+cudaError_t launch_zero_lower(int64_t m, void *X, int64_t ld_bytes, int esz, cudaStream_t s);
+// pack (to_buf = 1) / unpack (to_buf = 0) / zero (to_buf = 2) the listed regions of C into / from a contiguous buffer
 // of esize-byte residues (2: uint16 for p < 2^16)
 cudaError_t launch_rect_copy(const RectDev *rects, int n, int max_rows, uint32_t *C, int64_t ldc, void *buf,
                              int esize, int to_buf, cudaStream_t s);

@@ -52,8 +52,29 @@ cudaError_t launch_scale_lower(int64_t m, int w, uint32_t *X, int64_t ldx, uint3
   return cudaGetLastError();
 }
 
-// Up(C) = phi(Low(C)) (Lemma lem:uplow): C[j][i] = C[i][j] (conjugated for phi = H), i > j
-// one block per (region row, region); threads over the columns.  The packed buffer holds
+// Low(X) <- 0 for esz-byte elements (esz even: uint16 / uint32 residues x phi's width); one launch
+// for the whole triangle (k = 0 or alpha = 0), written as uint16 words
+__global__ void zero_lower_kernel(int64_t row0, void *X, int64_t ld_bytes, int esz) {
+  const int64_t i = row0 + blockIdx.y;
+  uint16_t *row = reinterpret_cast<uint16_t *>(static_cast<uint8_t *>(X) + i * ld_bytes);
+  const int64_t n = (i + 1) * (esz / 2);
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+    row[j] = 0;
+}
+
+cudaError_t launch_zero_lower(int64_t m, void *X, int64_t ld_bytes, int esz, cudaStream_t s) {
+  if (m == 0) return cudaSuccess;
+  const int64_t per_row = (m * (esz / 2) + 255) / 256;
+  for (int64_t r0 = 0; r0 < m; r0 += 65535) {
+    const int64_t rows = (m - r0) < 65535 ? (m - r0) : 65535;
+    zero_lower_kernel<<<dim3((unsigned)(per_row < 64 ? per_row : 64), (unsigned)rows), 256, 0, s>>>(r0, X, ld_bytes,
+                                                                                                     esz);
+  }
+  return cudaGetLastError();
+}
+
+// pack / unpack / zero (to_buf = 2) the listed regions of C: one block per (region row, region);
+// threads over the columns.  The packed buffer holds
 // uint16 residues when p < 2^16 (half the bytes on the wire), uint32 otherwise.
 template <typename BT>
 __global__ void __launch_bounds__(256) rect_copy_kernel(const RectDev *rects, uint32_t *C, int64_t ldc, BT *buf,
@@ -65,8 +86,9 @@ __global__ void __launch_bounds__(256) rect_copy_kernel(const RectDev *rects, ui
   BT *b = buf + R.off + i * R.cols;
   const int64_t ncol = R.lower ? min64(R.cols, R.r0 + i - R.c0 + 1) : R.cols;
   for (int64_t j = threadIdx.x; j < ncol; j += blockDim.x) {
-    if (to_buf) b[j] = (BT)c[j];
-    else c[j] = b[j];
+    if (to_buf == 1) b[j] = (BT)c[j];
+    else if (to_buf == 0) c[j] = b[j];
+    else c[j] = 0;
   }
 }
 
@@ -104,6 +126,7 @@ cudaError_t launch_sum_partials(int64_t m, const void *R, int64_t ldr, int64_t s
   return cudaGetLastError();
 }
 
+// Up(C) = phi(Low(C)) (Lemma lem:uplow): C[j][i] = C[i][j] (conjugated for phi = H), i > j
 __global__ void __launch_bounds__(256) fill_upper_kernel(int64_t m, int w, uint32_t *C, int64_t ldc, ModP mod) {
   const int ti = blockIdx.y, tj = blockIdx.x;
   if (ti < tj) return;

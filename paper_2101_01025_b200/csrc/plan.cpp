@@ -169,7 +169,10 @@ static void split_tail(Plan &P, int ncl) {
 static void set_grid(Plan &P, int num_sms) {
   split_tail(P, num_sms / 2);
   P.fixup_offset = P.ws_bytes;
-  P.ws_bytes += (size_t)P.n_pieces * 256 * 256 * P.res_bytes();
+  // the tail never has more pieces than clusters (pieces = ncl / rem per tail tile): reserve the
+  // worst case, so the size does not depend on the tile list (a shard's filtered list fits the
+  // full plan's workspace)
+  P.ws_bytes += (size_t)std::max(P.n_pieces, num_sms / 2) * 256 * 256 * P.res_bytes();
   P.ws_bytes = (P.ws_bytes + 255) / 256 * 256;
   P.counter_offset = P.ws_bytes;            // dynamic job counter of the leaf launch
   P.ws_bytes += 256;

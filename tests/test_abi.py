@@ -121,18 +121,20 @@ def test_workspace_and_depth_planning():
     w1 = adj.adjprod_modp_workspace_size(8192, 8192, 8191, 0, depth=1)
     w2 = adj.adjprod_modp_workspace_size(8192, 8192, 8191, 0, depth=2)
     # depth 0: 3 int8 planes of 8192 x 8192; depth 1: 7 operands x 3 planes at 4096^2 + 5 P buffers;
-    # plus 256x256 u16 fixup slots for the K-split tail tiles (<= one per cluster pair: 74) and the
-    # 256-byte job counter of the dynamic scheduler (after rounding to 256 bytes)
+    # plus 256x256 u16 fixup slots for the K-split tail tiles, reserved for the worst case (one per
+    # cluster pair: 148 / 2 = 74, independent of the tile list) and the 256-byte job counter of the
+    # dynamic scheduler (after rounding to 256 bytes)
     def tail(w, base):
         extra = w - base - 256
         slot = 256 * 256 * 2
-        return extra >= 0 and extra % slot < 256 and extra // slot <= 74
+        return extra >= 0 and extra % slot < 256 and extra // slot == 74
     assert tail(w0, 3 * 8192 * 8192)
-    assert (w0 - 3 * 8192 * 8192 - 256) // (256 * 256 * 2) == 70   # 528 tiles = 7 x 74 + 10: 10 tail tiles x 7 pieces
     assert tail(w1, 7 * 3 * 4096 * 4096 + 5 * 4096 * 4096 * 2)
     assert w2 > 0
     # k above the int32 bound of the limb scheme is handled by K segmentation (no error)
     assert tail(adj.adjprod_modp_workspace_size(256, 40000, 65521, 0, depth=0), 2 * 256 * 40064)
+    # a shard's plan (filtered tile list) fits the same workspace as the full plan
+    assert adj.adjprod_modp_workspace_size(8192, 8192, 8191, 0, depth=1) == w1
 
 
 def test_herk_alg1_workspace_planning():
