@@ -2,13 +2,15 @@
 """Benchmark of the hot path C = Low(A phi(A)) mod p (BASELINE.json metric: effective m^2 k
 modular MAC/s).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--depth D] [--impl reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--depth D] [--impl reference]
 
-One step = one adjprod_modp call (every §8(a) row: pre-additions, grouped tcgen05 leaves,
-recombination, 2M combine for phi = H) on a seeded uniform-residue A already resident in HBM.
-L2 is flushed (256 MiB write) before every timed step, outside the step's CUDA events.
-Rank 0 prints ONE JSON line.  N > 1 (torchrun): split-K over NCCL (adjprod_modp_dist), strong
-scaling, time = max over ranks.  --impl reference times the CPU oracle (oracle/) on host cores.
+Default workload: c3 = BASELINE.json configs[2] (A 32768 x 32768 over GF(65521)), the config the
+metric is quoted on at 1/2/4/8 B200.  One step = one adjprod_modp call (every §8(a) row:
+pre-additions, grouped tcgen05 leaves, recombination, 2M combine for phi = H) on a seeded
+uniform-residue A already resident in HBM.  L2 is flushed (256 MiB write) before every timed
+step, outside the step's CUDA events.  Rank 0 prints ONE JSON line.  N > 1 (torchrun, or
+`--gpus N` alone, which starts N ranks itself): adjprod_modp_dist over NCCL, strong scaling,
+time = max over ranks.  --impl reference times the CPU oracle (oracle/) on host cores.
 """
 from __future__ import annotations
 
@@ -52,9 +54,25 @@ CONFIGS = {
                workload="q5 (SURVEY 8(f)-4): M 8192x8192 over the quaternions H_GF(8191), C = Low(M M^H) via "
                         "Alg. 2M3M (6M)"),
 }
-DEFAULT_CONFIG = "c2"   # BASELINE.json configs[1]
-METRIC = "effective m^2 k modular MAC/s for C=A*A^T mod p (1 GPU: BASELINE configs[1])"
+# N = 1 headline: BASELINE.json configs[2] (c3), the configuration its metric is quoted on at
+# 1/2/4/8 B200 (c4 is the other one; c1, c2, c5 are parity cases and --config options)
+DEFAULT_CONFIG = "c3"
+BASELINE_INDEX = {"c1": 0, "c2": 1, "c3": 2, "c4": 3, "c5": 4}
 UNIT = "MAC/s"
+
+
+def metric_label(name: str) -> str:
+    """BASELINE.json's metric, labelled with the config it is measured on."""
+    where = (f"BASELINE configs[{BASELINE_INDEX[name]}]" if name in BASELINE_INDEX
+             else "SURVEY 8(f) / dev config")
+    return f"effective m^2 k modular MAC/s for C=A*A^T mod p at N B200 ({name}: {where})"
+
+
+def config_dict(name: str, cfg) -> dict:
+    """The workload, identical on both arms (--impl ours / reference): what is computed, not how."""
+    return {"workload": cfg["workload"], "id": name, "m": cfg["m"], "k": cfg["k"], "p": cfg["p"], "phi": cfg["phi"],
+            "seed": 1, "inputs": "uniform residues in [0, p) (inputs/: splitmix64 counter generator)",
+            "l2": "inputs larger than L2 and a 256 MiB L2 flush before every timed step (outside step events)"}
 
 
 def limb_mmas(p: int) -> int:
@@ -93,32 +111,59 @@ def leaf_int8_ops(cfg, depth, herk="2m") -> float:
 
 def hbm_bytes(cfg, depth, herk="2m", res_bytes=4):
     """Algorithmic HBM bytes per step of the HBM-bound classes (K1 pre-addition / split and the
-    recombination), for the layouts DESIGN.md §4 describes: read each input once, write each
-    limb plane / residue once.  None where not derived (depth >= 2, phi = H via ADJ_HERK_ALG1).
+    recombination K4 / 2M / 6M combine), for the layouts DESIGN.md §4 describes: read each input
+    once, write each limb plane (padded arena rows) / residue once.  Any depth for phi = T; depth 0
+    for phi = H / Q; None for phi = H via ADJ_HERK_ALG1.
     res_bytes: bytes per caller residue of A and Low(C) (4, or 2 with ADJ_IN_U16 | ADJ_OUT_U16)."""
     m, k, p = cfg["m"], cfg["k"], cfg["p"]
     w = {"T": 1, "H": 2, "Q": 4}[cfg["phi"]]
     planes = {1: 1, 3: 3, 4: 2, 6: 6}[limb_mmas(p)]
     rp = lambda x: -(-x // 128) * 128
-    res = 4 if p > 65535 else 2
-    out_c = m * (m + 1) // 2 * res_bytes * w              # Low(C), uint32 (or uint16) words
+    res = 4 if p > 65535 else 2                             # workspace residues (S3, P buffers)
+    out_c = m * (m + 1) // 2 * res_bytes * w                # Low(C), uint32 (or uint16) words
     if cfg["phi"] == "H" and herk == "alg1":
         return None
     if depth == 0:
         nops = {1: 1, 2: 3, 4: 7}[w]                       # A | X, Y, T | A, B, C, D, U1, U2, W
-        pre = res_bytes * w * m * k + nops * planes * rp(m) * rp(k)
+        pre = res_bytes * w * m * k + nops * planes * rp(m) * max(128, rp(k))
         if w == 1:
             comb = None                                    # the leaf epilogue writes C directly
         else:
             nbuf = {2: (1, 1), 4: (5, 1)}[w]               # full buffers read (H | Q1..Q5), lower ones (G | Q6)
             comb = (nbuf[0] * m * m + nbuf[1] * m * (m + 1) // 2) * res + out_c
         return {"preadd": pre, "combine": comb}
-    if depth == 1 and w == 1:
-        mh, kh = -(-m // 2), 8 * -(-k // 16)
-        pre = res_bytes * m * k + 7 * planes * rp(mh) * max(128, -(-kh // 128) * 128)
-        comb = (3 * mh * (mh + 1) // 2 + 2 * mh * mh) * res + out_c
-        return {"preadd": pre, "combine": comb}
-    return None
+    if w != 1:
+        return None
+    # phi = T, depth >= 1: walk the recursion tree (api.cpp run_tree / run_combine).  Level l has
+    # 3^(l-1) nodes of half sizes mh_l = ceil(mh_{l-1} / 2), kh_l = 8 ceil(kh_{l-1} / 16); K1 of a
+    # node reads the valid part of its input (A's elements at the root and in the X11 / X12 views,
+    # workspace residues in S3) and writes n_ops limb operands of planes x rows_pad x kpad bytes
+    # (4 operands S1, S2, S4, X22 above the last level, 7 at it) plus its S3 residues above the
+    # last level; K4 of a node reads P1, P2, P5 (lower) and P3, P4 (full) and writes Low of its
+    # output (Low(C) at the root, the parent's P slot below it).
+    mh, kh = [m], [k]
+    for _ in range(depth):
+        mh.append(-(-mh[-1] // 2))
+        kh.append(8 * -(-kh[-1] // 16))
+    pre = comb = 0
+
+    def node(level, rows, cols, esz):
+        nonlocal pre, comb
+        pre_read = rows * cols * esz
+        nops = 7 if level == depth else 4
+        pre_write = nops * planes * rp(mh[level]) * max(128, rp(kh[level]))
+        if level < depth:
+            pre_write += mh[level] * kh[level] * res       # S3, the third child's input
+        pre += pre_read + pre_write
+        m_l = mh[level]
+        comb += (3 * m_l * (m_l + 1) // 2 + 2 * m_l * m_l) * res
+        comb += out_c if level == 1 else mh[level - 1] * (mh[level - 1] + 1) // 2 * res
+        if level < depth:
+            node(level + 1, min(rows, m_l), min(cols, kh[level]), esz)                        # X11
+            node(level + 1, min(rows, m_l), max(0, min(cols - kh[level], kh[level])), esz)   # X12
+            node(level + 1, m_l, kh[level], res)                                            # S3
+    node(1, m, k, res_bytes)
+    return {"preadd": pre, "combine": comb}
 
 
 def load_peaks():
@@ -259,8 +304,10 @@ def oracle_sample(cfg, A_host, budget_s: float):
 
 
 def run_reference(args, cfg, rank, world):
-    """--impl reference: the CPU oracle as it stands, on host cores, rank 0 only."""
-    import numpy as np
+    """--impl reference: the CPU oracle as it stands, on host cores, rank 0 only.  One step = the
+    oracle on one bounded slab of the workload (the last rows of Low(C), the longest ones), sized
+    to ~ADJ_REF_STEP_S seconds; ms_per_step is that measured slab time, value its effective
+    m^2 k MAC/s (slab ring MACs scaled by m^2 k / full lower-triangle MACs)."""
     from inputs import uniform_matrix, uniform_matrix_ext, uniform_matrix_quat
     if rank != 0:
         return
@@ -278,12 +325,14 @@ def run_reference(args, cfg, rank, world):
         tfull.append(t_full)
     value = statistics.median(vals)
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(tfull),
-        "higher_is_better": True, "scaling": "strong" if args.gpus > 1 else "weak", "vs_baseline": None,
+        "impl": "reference", "metric": metric_label(args.config), "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(secs),
+        "ms_per_step_is": "measured: the oracle on one bounded slab of the workload per step (see cpu_baseline.sample)",
+        "extrapolated_full_problem_ms": 1e3 * statistics.median(tfull),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "uint64", "data": "synthetic",
-        "config": {"workload": cfg["workload"], "m": m, "k": k, "p": p, "phi": cfg["phi"], "seed": 1,
-                   "sample_s_per_step": statistics.median(secs), "ms_per_step_is": "extrapolated full problem"},
+        "config": config_dict(args.config, cfg),
+        "parallelism": f"CPU oracle, {cores} host threads (OpenMP)",
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -331,6 +380,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
     uniform_residues_cuda(A32, seed=1, p=p)
     A = A32.to(torch.int16) if io16 else A32
     del A32
+    A_bytes = A.numel() * A.element_size()
     C = torch.zeros((m, m * w), dtype=torch.int16 if io16 and world == 1 else torch.int32, device=dev)
 
     def u32(t):
@@ -497,9 +547,11 @@ def run_gpu(args, cfg, rank, world, local_rank):
     # halves it); the uint32 leg is reported beside it as e2e_u32.
     e2e = e2e_u32 = None
     if world == 1:
-        e2e_u32 = run_e2e(4, 0)
-        e2e_u32["io"] = "uint32 residues both ways"
-        e2e = e2e_u32
+        # the uint32 leg (context) only where its pinned host buffers stay small (<= 2^27 elements)
+        if not io16 or m * k * w <= (1 << 27):
+            e2e_u32 = run_e2e(4, 0)
+            e2e_u32["io"] = "uint32 residues both ways"
+            e2e = e2e_u32
         if io16:
             e2e = run_e2e(2, adj.ADJ_IN_U16 | adj.ADJ_OUT_U16)
             e2e["io"] = "uint16 residues both ways (ADJ_IN_U16 | ADJ_OUT_U16)"
@@ -681,28 +733,31 @@ def run_gpu(args, cfg, rank, world, local_rank):
     if rank == 0:
         mh = herk_alg1_macs(m, k) if alg1 else ring_macs(m, k, depth) + {1: 0, 2: 1, 4: 5}[w] * m * m * k
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "metric": metric_label(args.config), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "int8",
             "data": "synthetic",
-            "config": {"workload": cfg["workload"] + (" via Alg. 1 over GF(p^2) (ADJ_HERK_ALG1)" if alg1 else ""),
-                       "m": m, "k": k, "p": p, "phi": cfg["phi"], "depth": depth,
-                       "seed": 1, "l2": "flushed before every timed step (256 MiB write, outside step events)",
+            "config": config_dict(args.config, cfg),
+            "method": {"depth": depth, "route": ("Alg. 1 over GF(p^2) (ADJ_HERK_ALG1)" if alg1 else
+                                                 {"T": "Alg. alg:MIAHMM", "H": "Alg. alg:2M (G through Alg. alg:MIAHMM)",
+                                                  "Q": "Alg. alg:2M3M (6M)"}[cfg["phi"]]),
                        "residues": ("uint16 A and Low(C) in HBM (ADJ_IN_U16 | ADJ_OUT_U16)" if io16 and world == 1
                                     else "uint16 A (ADJ_IN_U16), uint32 Low(C) on the root" if io16
                                     else "uint32 A and Low(C) in HBM"),
-                       "parallelism": ("1 GPU" if world == 1 else
-                                       (f"output tiles x{world} (NCCL send/recv gather of result tiles)"
-                                        if dist_mode == "tiles" else
-                                        f"split-K x{world} (partials stored into the root over NVLink)"
-                                        if dist_mode == "p2p" else f"split-K x{world} (NCCL reduce)")),
-                       "fraction_of_int8_peak_effective": value / (peak * 1e12 / 2),
-                       "ring_macs_per_step": mh, "limb_mmas_per_ring_mac": limb_mmas(p)},
+                       "ring_macs_per_step": mh, "limb_mmas_per_ring_mac": limb_mmas(p),
+                       "workspace_bytes": ws_bytes if world == 1 else None,
+                       "workspace_over_A_bytes": (ws_bytes / A_bytes) if world == 1 else None},
+            "parallelism": ("1 GPU" if world == 1 else
+                            (f"output tiles x{world} (NCCL send/recv gather of result tiles)"
+                             if dist_mode == "tiles" else
+                             f"split-K x{world} (partials stored into the root over NVLink)"
+                             if dist_mode == "p2p" else f"split-K x{world} (NCCL reduce)")),
+            "fraction_of_int8_peak_effective": value / (world * peak * 1e12 / 2),
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "sustained": sustained,
-            "e2e_u32": e2e_u32 if e2e is not e2e_u32 else None,
+            "e2e_u32": e2e_u32 if (e2e_u32 is not None and e2e is not e2e_u32) else None,
             "gpu_launches": launches,
             "kernel_time_share": share,
             "hbm_kernels": hbm,
@@ -713,6 +768,19 @@ def run_gpu(args, cfg, rank, world, local_rank):
         print(json.dumps(line), flush=True)
     if comm is not None:
         adj.adj_comm_destroy(comm)
+
+
+def relaunch_torchrun(n: int) -> int:
+    """`python bench.py --gpus N` outside torchrun: start N ranks (one process per GPU) through
+    torch.distributed.run on 127.0.0.1 with the same arguments; rank 0 prints the JSON line."""
+    import socket
+    import subprocess
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -737,6 +805,8 @@ def main():
                     help="phi = H: 2M reduction (default) or one level of Alg. 1 over GF(p^2)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        sys.exit(relaunch_torchrun(args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))

@@ -125,13 +125,14 @@ def num_threads() -> int:
 def syrk_update(A: np.ndarray, C: np.ndarray, p: int, alpha: int, beta: int, phi: str = "T") -> np.ndarray:
     """SYRK / HERK form (Table tab:schedule:AATpC): returns C' with
     Low(C') = alpha Low(A phi(A)) + beta Low(C) mod p and Up(C') = Up(C) (old values kept).
-    Composed from the O1 definition; alpha, beta in GF(p) scale re and im alike for phi = H."""
-    base = syrk_t(A, p) if phi == "T" else syrk_h(A, p)
+    Composed from the O1 definition; alpha, beta in GF(p) scale every component alike for
+    phi = H (re, im) and phi = Q (the four quaternion components)."""
+    base = {"T": syrk_t, "H": syrk_h, "Q": syrk_q}[phi](A, p)
     out = C.copy()
     m = C.shape[0]
     mask = np.tril(np.ones((m, m), dtype=bool))
     if C.ndim == 3:
-        mask = mask[:, :, None] & np.ones((1, 1, 2), dtype=bool)
+        mask = mask[:, :, None] & np.ones((1, 1, C.shape[2]), dtype=bool)
     new = (int(alpha) % p * base.astype(np.int64) + int(beta) % p * (C.astype(np.int64) % p)) % p
     out[mask] = new[mask].astype(np.uint32)
     return out

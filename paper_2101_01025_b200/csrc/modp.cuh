@@ -1,6 +1,7 @@
 // Modular arithmetic and int8 limb splitting shared by the host planner and the kernels of
 // the CUDA path (not shared with oracle/).
 #pragma once
+#include <cmath>
 #include <cstdint>
 
 #ifndef __CUDACC__
@@ -109,6 +110,52 @@ __host__ __device__ __forceinline__ uint32_t acc_mulred(int32_t x, int32_t wc, i
   uint32_t s = part + r + p;
   s = umin32(s, s - 2 * p);
   return umin32(s, s - p);
+}
+
+// ---- K1's lazy reduction of the Y products for p > 16763 (preadd.cu) ----------
+// The products' sum v (|v| < 2 p^2 < 2^37 for p < 2^18) is carried exactly mod 2^32 (wrapping
+// uint32 arithmetic) and approximately in float (vf, relative error a few 2^-24).  The float
+// quotient estimate q = rn(vf / p) is then within ~0.6 of v / p, so u = v + h - q p, a value in
+// (-p, 2p), is exact in wrapping 32-bit arithmetic and two unsigned mins give the offset residue
+// (v + h) mod p in [0, p) (h = (p - 1) / 2: u - h is the centered residue of v).  Host-checked over
+// extreme and random inputs of every scheme above 16763 (tests/test_host_modp.py).
+__host__ __device__ __forceinline__ int32_t f2i_rn(float x) {
+#ifdef __CUDA_ARCH__
+  return __float2int_rn(x);
+#else
+  return (int32_t)std::nearbyintf(x);   // round half to even in the default FP environment
+#endif
+}
+__host__ __device__ __forceinline__ float lazy_invp(uint32_t p) { return 1.0f / (float)p; }
+__host__ __device__ __forceinline__ uint32_t lazy_off(uint32_t v_bits, float vf, float invp, uint32_t p, uint32_t h) {
+  const int32_t q = f2i_rn(vf * invp);
+  const uint32_t u = v_bits + h - (uint32_t)q * p;
+  return umin32(umin32(u, u - p), u + p);
+}
+// S1 = (A21 - A11) Y and S2 = A22 - A21 Y as offset residues, for canonical
+// inputs x < p: YK = 0, Y = i I (scalar ya, the two lanes a / b independent); YK = 1, Y = Rot2(a, b)
+// acting on the column pair (j, j + k/4): [X1 X2] Y = [a X1 - b X2, b X1 + a X2].
+template <int YK>
+__host__ __device__ __forceinline__ void lazy_s1_s2(uint32_t x11a, uint32_t x11b, uint32_t x21a, uint32_t x21b,
+                                                    uint32_t x22a, uint32_t x22b, uint32_t ya, uint32_t yb, float invp,
+                                                    uint32_t p, uint32_t h, uint32_t &s1a, uint32_t &s1b,
+                                                    uint32_t &s2a, uint32_t &s2b) {
+  const int32_t d1 = (int32_t)x21a - (int32_t)x11a, d2 = (int32_t)x21b - (int32_t)x11b;
+  const uint32_t ud1 = (uint32_t)d1, ud2 = (uint32_t)d2;
+  const float yaf = (float)ya, ybf = (float)yb, d1f = (float)d1, d2f = (float)d2;
+  const float x21af = (float)x21a, x21bf = (float)x21b, x22af = (float)x22a, x22bf = (float)x22b;
+  if (YK == 0) {
+    s1a = lazy_off(ya * ud1, yaf * d1f, invp, p, h);
+    s1b = lazy_off(ya * ud2, yaf * d2f, invp, p, h);
+    s2a = lazy_off(x22a - ya * x21a, fmaf(-yaf, x21af, x22af), invp, p, h);
+    s2b = lazy_off(x22b - ya * x21b, fmaf(-yaf, x21bf, x22bf), invp, p, h);
+  } else {
+    s1a = lazy_off(ya * ud1 - yb * ud2, fmaf(yaf, d1f, -(ybf * d2f)), invp, p, h);
+    s1b = lazy_off(yb * ud1 + ya * ud2, fmaf(ybf, d1f, yaf * d2f), invp, p, h);
+    const float trfa = fmaf(yaf, x21af, -(ybf * x21bf)), trfb = fmaf(ybf, x21af, yaf * x21bf);
+    s2a = lazy_off(x22a - (ya * x21a - yb * x21b), x22af - trfa, invp, p, h);
+    s2b = lazy_off(x22b - (yb * x21a + ya * x21b), x22bf - trfb, invp, p, h);
+  }
 }
 
 // int8 limb split of a canonical residue:

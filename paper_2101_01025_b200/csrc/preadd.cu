@@ -459,12 +459,11 @@ __device__ __forceinline__ void preadd_row(const PreParams &P, const PreNode &N,
     // Lazy reduction: Y products unreduced, one reduction per S output.  Residues are carried as
     // offset values u = c + h in [0, p) of the centered c (h = (p - 1) / 2), so every correction
     // is an unsigned min of u, u - p, u + p.  SCHEMES 0 / 1 (p <= 16763, 2 p^2 < 2^31): exact
-    // int32 products.  SCHEMES 2 / 3 (p < 2^18): the products' sum v (|v| < 2^37) is known exactly mod 2^32
-    // and to ~2^13 in float; the float quotient estimate is within 0.63 of v / p, so the remainder
-    // v - q p, a value below 2^19 in magnitude, is exact in wrapping 32-bit arithmetic.
+    // int32 products.  SCHEMES 2 / 3 (p < 2^18): modp.cuh lazy_s1_s2 (exact mod 2^32 plus a float
+    // quotient estimate; host-checked in tests/test_host_modp.py).
     const int32_t p = (int32_t)m.p, h = (int32_t)m.half;
     const uint32_t up = m.p;
-    const float invp = 1.0f / (float)m.p;
+    const float invp = lazy_invp(m.p);
     const int32_t ya = (int32_t)P.ya, yb = (int32_t)P.yb;
     // v + h - q p with the float quotient estimate q of v / p (v exact mod 2^32, vf its float
     // value): in [-0.63 p, 1.63 p)
@@ -496,18 +495,8 @@ __device__ __forceinline__ void preadd_row(const PreParams &P, const PreNode &N,
       if constexpr (SCHEME <= 1) {
         u1a[e] = off_lazy(s1r_a); u1b[e] = off_lazy(s1r_b);                                         // S1
         u2a[e] = off_lazy((int32_t)x22a[e] - tr_a); u2b[e] = off_lazy((int32_t)x22b[e] - tr_b);     // S2
-      } else {
-        const float d1f = (float)d1, d2f = (float)d2, x21af = (float)x21a[e], x21bf = (float)x21b[e];
-        float s1f_a, s1f_b, trf_a, trf_b;
-        if constexpr (YK == 0) {
-          s1f_a = yaf * d1f; s1f_b = yaf * d2f; trf_a = yaf * x21af; trf_b = yaf * x21bf;
-        } else {
-          s1f_a = fmaf(yaf, d1f, -(ybf * d2f)); s1f_b = fmaf(ybf, d1f, yaf * d2f);
-          trf_a = fmaf(yaf, x21af, -(ybf * x21bf)); trf_b = fmaf(ybf, x21af, yaf * x21bf);
-        }
-        u1a[e] = off_lazy2(s1r_a, s1f_a); u1b[e] = off_lazy2(s1r_b, s1f_b);                         // S1
-        u2a[e] = off_lazy2((int32_t)(x22a[e] - (uint32_t)tr_a), (float)x22a[e] - trf_a);             // S2
-        u2b[e] = off_lazy2((int32_t)(x22b[e] - (uint32_t)tr_b), (float)x22b[e] - trf_b);
+      } else {   // S1, S2 by the host-checked helper (modp.cuh: lazy_s1_s2)
+        lazy_s1_s2<YK>(x11a[e], x11b[e], x21a[e], x21b[e], x22a[e], x22b[e], (uint32_t)ya, (uint32_t)yb, invp, up, (uint32_t)h, u1a[e], u1b[e], u2a[e], u2b[e]);
       }
       u3a[e] = wrap_lo(u1a[e] - x22a[e]); u3b[e] = wrap_lo(u1b[e] - x22b[e]);                       // S3
       u4a[e] = wrap_hi(u3a[e] + x12a[e]); u4b[e] = wrap_hi(u3b[e] + x12b[e]);                       // S4

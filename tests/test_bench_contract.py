@@ -25,9 +25,13 @@ def test_reference_arm_json_line():
     for key in ("impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
                 "scaling", "vs_baseline", "dtype", "data", "config", "cpu_baseline", "e2e"):
         assert key in d, key
-    assert d["impl"] == "reference" and d["metric"] == bench.METRIC and d["unit"] == bench.UNIT
+    assert d["impl"] == "reference" and d["metric"] == bench.metric_label("c1") and d["unit"] == bench.UNIT
     assert d["value"] > 0 and d["higher_is_better"] is True and d["steps"] == 2
+    # the same config dict the GPU arm prints (what is computed, not how)
+    assert d["config"] == bench.config_dict("c1", bench.CONFIGS["c1"])
     assert d["config"]["workload"] == bench.CONFIGS["c1"]["workload"]
+    # ms_per_step is the measured slab time; the extrapolation to the full problem is reported apart
+    assert 0 < d["ms_per_step"] <= d["extrapolated_full_problem_ms"] * 1.0001
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] == d["value"]
     assert d["cpu_baseline"]["cores"] >= 1 and d["cpu_baseline"]["sample"]
     assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
@@ -68,7 +72,8 @@ def test_gpu_arm_json_line():
     for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
                 "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "gpu_launches", "clocks"):
         assert key in d, key
-    assert d["metric"] == bench.METRIC and d["n_gpus"] == 1 and d["steps"] == 3 and d["warmup"] >= 3
+    assert d["metric"] == bench.metric_label("c1") and d["n_gpus"] == 1
+    assert d["config"] == bench.config_dict("c1", bench.CONFIGS["c1"]) and d["steps"] == 3 and d["warmup"] >= 3
     assert d["value"] > 0 and d["gpu_launches"] > 0
     r = d["roofline"]
     assert r["bound"] == "tensor" and r["unit"] == "TFLOP/s" and abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
@@ -76,6 +81,30 @@ def test_gpu_arm_json_line():
     assert e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0 and e["last_row_matches_device_result"]
     assert d["parity"]["bit_exact"]
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
+
+
+def test_hbm_bytes_c3_depth2():
+    """K1 / K4 algorithmic bytes at c3 depth 2 (the N = 1 headline) written out level by level:
+    level 1 reads A once and writes 4 operands (S1, S2, S4, X22) x 2 planes plus S3 (uint16);
+    level 2 has 3 nodes (A11, A12 views of A and S3) each writing 7 operands x 2 planes; K4 reads
+    3 lower + 2 full product buffers per node and writes Low of its output."""
+    cfg = bench.CONFIGS["c3"]
+    n = cfg["m"]
+    assert cfg["k"] == n
+    h1, h2 = n // 2, n // 4
+    for rb in (2, 4):
+        hb = bench.hbm_bytes(cfg, 2, res_bytes=rb)
+        pre = (rb * n * n + 4 * 2 * h1 * h1 + 2 * h1 * h1               # level 1
+               + 2 * h1 * h1 * rb + h1 * h1 * 2 + 3 * 7 * 2 * h2 * h2)    # level 2: reads, writes
+        comb = (3 * ((3 * h2 * (h2 + 1) // 2 + 2 * h2 * h2) * 2 + h1 * (h1 + 1) // 2 * 2)
+                + (3 * h1 * (h1 + 1) // 2 + 2 * h1 * h1) * 2 + n * (n + 1) // 2 * rb)
+        assert hb == {"preadd": pre, "combine": comb}
+
+
+def test_metric_label_names_the_config():
+    assert bench.DEFAULT_CONFIG == "c3"
+    assert "c3: BASELINE configs[2]" in bench.metric_label("c3")
+    assert "c4: BASELINE configs[3]" in bench.metric_label("c4")
 
 
 def test_hbm_bytes_compact_halves_the_residue_terms():

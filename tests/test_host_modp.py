@@ -88,3 +88,83 @@ def test_add_sub_mod_exact(tmp_path):
     out = subprocess.run([str(exe)], input=inp, capture_output=True, text=True, check=True).stdout.split("\n")
     for (p, a, b, x), line in zip(cases, out):
         assert list(map(int, line.split())) == [(a + b) % p, (a - b) % p, x % p, a * b % p], (p, a, b, x, line)
+
+
+PROG3 = r"""
+#include <cstdio>
+#include <vector>
+#include "modp.cuh"
+using namespace adj;
+// stdin: records of 11 uint32 (p, yk, x11a, x11b, x21a, x21b, x22a, x22b, ya, yb, pad)
+// stdout: 4 uint32 per record (S1a, S1b, S2a, S2b offset residues)
+int main() {
+  uint32_t r[11];
+  std::vector<uint32_t> out;
+  while (fread(r, 4, 11, stdin) == 11) {
+    const uint32_t p = r[0], h = (p - 1) / 2;
+    uint32_t s[4];
+    if (r[1] == 0) lazy_s1_s2<0>(r[2], r[3], r[4], r[5], r[6], r[7], r[8], r[9], lazy_invp(p), p, h, s[0], s[1], s[2], s[3]);
+    else lazy_s1_s2<1>(r[2], r[3], r[4], r[5], r[6], r[7], r[8], r[9], lazy_invp(p), p, h, s[0], s[1], s[2], s[3]);
+    out.insert(out.end(), s, s + 4);
+  }
+  fwrite(out.data(), 4, out.size(), stdout);
+  return 0;
+}
+"""
+
+LAZY_PRIMES = [16787, 32749, 65519, 65521, 65537, 131041, 131071, 199999, 262139]
+
+
+def test_k1_lazy_float_quotient_reduction(tmp_path):
+    """K1's lazy reduction of the Y products for p > 16763 (modp.cuh lazy_s1_s2, used by
+    preadd.cu): S1 = (A21 - A11) Y and S2 = A22 - A21 Y for Y = i I and
+    Y = Rot2(a, b), as offset residues (v + (p-1)/2) mod p, against exact integers.
+    Every combination of extreme residues {0, 1, h, h+1, p-2, p-1} of the six inputs, with extreme
+    and actual skew-unitary Y coefficients, plus random inputs, at primes across both schemes
+    above 16763 (s8/u8 up to 65521, 6-plane up to 262139).  The float quotient estimate must stay
+    within the window the two unsigned mins correct."""
+    import itertools
+    import numpy as np
+    src, exe = tmp_path / "t3.cpp", tmp_path / "t3"
+    src.write_text(PROG3)
+    subprocess.run(["g++", "-O2", "-std=c++17", "-ffp-contract=off", "-I", CSRC, str(src), "-o", str(exe)], check=True)
+    import oracle.field as of
+    recs = []
+    rng = np.random.default_rng(5)
+    for p in LAZY_PRIMES:
+        h = (p - 1) // 2
+        ext = np.array([0, 1, h, h + 1, p - 2, p - 1], dtype=np.uint64)
+        xs = np.array(list(itertools.product(range(6), repeat=6)), dtype=np.int64)
+        X = ext[xs]                                                     # (46656, 6)
+        if p % 4 == 1:
+            yset = [(of.mod_sqrt(p - 1, p), 0)]
+        else:
+            yset = [tuple(of.sos(p - 1, p))]
+        yset += [(p - 1, p - 1), (p - 1, 1), (h, h + 1), (1, p - 1)]
+        for yk in (0, 1):
+            for ya, yb in yset:
+                n = X.shape[0]
+                R = np.zeros((n, 11), dtype=np.uint64)
+                R[:, 0], R[:, 1], R[:, 2:8], R[:, 8], R[:, 9] = p, yk, X, ya, yb
+                recs.append(R)
+            n = 60000
+            R = np.zeros((n, 11), dtype=np.uint64)
+            R[:, 0], R[:, 1] = p, yk
+            R[:, 2:10] = rng.integers(0, p, size=(n, 8))
+            recs.append(R)
+    R = np.concatenate(recs).astype(np.uint32)
+    out = subprocess.run([str(exe)], input=R.tobytes(), capture_output=True, check=True).stdout
+    got = np.frombuffer(out, dtype=np.uint32).reshape(-1, 4).astype(np.int64)
+    assert got.shape[0] == R.shape[0]
+    Ri = R.astype(np.int64)
+    p, yk = Ri[:, 0], Ri[:, 1]
+    x11a, x11b, x21a, x21b, x22a, x22b, ya, yb = (Ri[:, c] for c in range(2, 10))
+    h = (p - 1) // 2
+    d1, d2 = x21a - x11a, x21b - x11b
+    s1a = np.where(yk == 0, ya * d1, ya * d1 - yb * d2)
+    s1b = np.where(yk == 0, ya * d2, yb * d1 + ya * d2)
+    s2a = np.where(yk == 0, x22a - ya * x21a, x22a - (ya * x21a - yb * x21b))
+    s2b = np.where(yk == 0, x22b - ya * x21b, x22b - (yb * x21a + ya * x21b))
+    want = np.stack([(v + h) % p for v in (s1a, s1b, s2a, s2b)], axis=1)
+    bad = np.nonzero((got != want).any(axis=1))[0]
+    assert bad.size == 0, (bad.size, R[bad[:5]].tolist(), got[bad[:5]].tolist(), want[bad[:5]].tolist())

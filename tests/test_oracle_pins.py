@@ -214,3 +214,57 @@ def test_syrk_update_special_cases(golden):
     assert np.array_equal(np.triu(both, 1), np.triu(C, 1))
     ref = (3 * brute_syrk(A.tolist(), p).astype(np.int64) + 5 * (C.astype(np.int64) % p)) % p
     assert np.array_equal(np.tril(both), np.tril(ref).astype(np.uint32))
+
+
+@pytest.mark.parametrize("alpha,beta", [(1, 0), (0, 1), (3, 5), (10, 10)])
+def test_syrk_update_hermitian_branch(alpha, beta):
+    """The phi = H branch of syrk_update (HERK form, Table tab:schedule:AATpC)
+    against pure-Python brute force over GF(11)[i]/(i^2+1): Low(C') = alpha Low(A A^H) +
+    beta Low(C) with alpha, beta in GF(p) scaling re and im alike, on both components of the
+    lower triangle (diagonal included), and Up(C') = Up(C) untouched in both components."""
+    p = 11
+    rng = np.random.default_rng(alpha * 7 + beta)
+    m, k = 6, 5
+    A = rng.integers(0, p, size=(m, k, 2)).astype(np.uint32)
+    C = rng.integers(0, 3 * p, size=(m, m, 2)).astype(np.uint32)     # non-canonical old values too
+    got = oracle.syrk_update(A, C, p, alpha, beta, phi="H")
+    herk = brute_herk(A, p)
+    for i in range(m):
+        for j in range(m):
+            for q in range(2):
+                if j <= i:
+                    want = (alpha * int(herk[i, j, q]) + beta * (int(C[i, j, q]) % p)) % p
+                else:
+                    want = int(C[i, j, q])
+                assert int(got[i, j, q]) == want, (i, j, q)
+
+
+@pytest.mark.parametrize("alpha,beta", [(1, 0), (0, 1), (4, 9)])
+def test_syrk_update_quaternion_branch(alpha, beta):
+    """The phi = Q branch of syrk_update against pure-Python quaternion arithmetic over GF(7):
+    C_ij = sum_t M_it conj(M_jt) with the table i^2 = j^2 = k^2 = ijk = -1,
+    written out per component; Low scaled, Up untouched."""
+    p = 7
+    rng = np.random.default_rng(alpha + 10 * beta)
+    m, k = 5, 4
+    M = rng.integers(0, p, size=(m, k, 4)).astype(np.uint32)
+    C = rng.integers(0, 3 * p, size=(m, m, 4)).astype(np.uint32)
+    got = oracle.syrk_update(M, C, p, alpha, beta, phi="Q")
+
+    def qmul(x, y):
+        a, b, c, d = x
+        e, f, g, h = y
+        return (a * e - b * f - c * g - d * h, a * f + b * e + c * h - d * g,
+                a * g - b * h + c * e + d * f, a * h + b * g - c * f + d * e)
+    for i in range(m):
+        for j in range(m):
+            if j <= i:
+                acc = [0, 0, 0, 0]
+                for t in range(k):
+                    x = [int(v) for v in M[i, t]]
+                    y = [int(M[j, t, 0])] + [-int(v) for v in M[j, t, 1:]]
+                    acc = [u + v for u, v in zip(acc, qmul(x, y))]
+                want = [(alpha * acc[q] + beta * (int(C[i, j, q]) % p)) % p for q in range(4)]
+            else:
+                want = [int(v) for v in C[i, j]]
+            assert [int(v) for v in got[i, j]] == want, (i, j)
