@@ -203,12 +203,15 @@ adj_status_t adj_elem_bytes(adj_phi_t phi, uint32_t flags, int64_t *bytes);
  * adjprod_modp_shard -- output-tile sharding, phi = ADJ_PHI_T, depth 0 or 1
  *   (-1: the automatic depth capped at 1).  The top-level product grid of Alg. alg:MIAHMM (the
  *   (m/2) grid of P1..P5 at depth 1; the grid of C at depth 0) is cut into 256 x 256 tiles;
- *   pairs {(I, J), (J, I)}, I >= J, are dealt to `nranks` owners (largest cost first to the
- *   least loaded, deterministic).  This call writes exactly the regions of Low(C) that `rank`
- *   owns (adj_shard_layout) and nothing else: the pre-addition is computed in full (A is read
- *   whole), the grouped leaf launch runs only the owned tiles of P1..P5 and the recombination
- *   only the owned tile pairs.  Running every rank's share, on one device or on several,
- *   writes all of Low(C).  ADJ_FILL_UPPER is not supported here (INVALID_VALUE).
+ *   pairs {(I, J), (J, I)}, I >= J, are dealt to `nranks` owners in blocks of band groups (a
+ *   pair reads the operand rows of tile bands I and J only; the blocks keep each rank's bands
+ *   few; deterministic).  This call writes exactly the regions of Low(C) that `rank` owns
+ *   (adj_shard_layout) and nothing else: the top-level pre-addition (or the depth-0 split) covers
+ *   only the rows of the bands the rank's tiles read (adj_shard_rows), the grouped leaf launch
+ *   runs only the owned tiles of P1..P5 and the recombination only the owned tile pairs.
+ *   Running every rank's share, on one device or on several, writes all of Low(C).  A caller
+ *   workspace of adjprod_modp_workspace_size(m, k, p, ADJ_PHI_T, depth) bytes (the same depth)
+ *   suffices.  ADJ_FILL_UPPER is not supported here (INVALID_VALUE).
  */
 adj_status_t adjprod_modp_shard(int64_t m, int64_t k, uint32_t p, adj_phi_t phi,
                                 const uint32_t *A, int64_t lda, uint32_t *C, int64_t ldc,
@@ -244,6 +247,14 @@ adj_status_t adj_shard_layout(int64_t m, int64_t k, uint32_t p, int depth, int r
                               int64_t *rects, int64_t max_rects, int64_t *n_rects, int64_t *n_elems);
 
 /*
+ * adj_shard_rows -- (host, no GPU) the row ranges [lo, hi) of the top-level operands that `rank`
+ *   pre-adds in adjprod_modp_shard (rows of the (m/2) quadrants at depth 1, of A at depth 0):
+ *   *n_ranges ranges stored as ranges[2*i], ranges[2*i+1] for i < max_ranges (ranges may be NULL).
+ */
+adj_status_t adj_shard_rows(int64_t m, int64_t k, uint32_t p, int depth, int rank, int nranks,
+                            int64_t *ranges, int64_t max_ranges, int64_t *n_ranges);
+
+/*
  * adj_shard_pack -- pack (unpack = 0) the regions of C that `rank` of `nranks` owns
  *   (adj_shard_layout, region by region, row by row) into the contiguous buffer `buf`, as uint16
  *   residues for p < 2^16 and uint32 otherwise, or unpack them back into C (unpack = 1; only the
@@ -257,8 +268,9 @@ adj_status_t adj_shard_pack(int64_t m, int64_t k, uint32_t p, int depth, int ran
  * adjprod_modp_dist -- collective; every rank of `comm` calls it with the same m, k, p, phi,
  *   root.  Default: split-K sharding: rank r computes Low(A_r phi(A_r)) on its
  *   column slice A_r = A[:, k_r0 : k_r1] (k_r0 = r*ceil(k/G) rounded to a multiple of 8) with
- *   the single-GPU path, then the residue partials are summed exactly with an NCCL uint32
- *   reduce to `root` (sum < G p < 2^32) and reduced mod p there.
+ *   the single-GPU path (adjprod_modp_dist_partial), packs the lower triangle (m (m+1) / 2
+ *   elements, row by row) as uint32 words, the packed partials are summed exactly with an NCCL
+ *   uint32 reduce to `root` (sum < G p < 2^32) and reduced mod p into Low(C) there.
  *   A: the full m x k matrix on every rank (only the rank's slice is read).  C: m x m on every
  *   rank; Low(C) is the result on `root` only.
  *   With opts->flags & ADJ_DIST_TILES (phi = ADJ_PHI_T): output-tile sharding instead -- every
@@ -269,6 +281,18 @@ adj_status_t adjprod_modp_dist(int64_t m, int64_t k, uint32_t p, adj_phi_t phi,
                                const uint32_t *A, int64_t lda, uint32_t *C, int64_t ldc,
                                int root, adj_comm_t comm, const adj_opts_t *opts,
                                adj_stream_t stream);
+
+/*
+ * adjprod_modp_dist_partial -- rank `rank`'s share of the split-K sharding of adjprod_modp_dist:
+ *   Low(A_r phi(A_r)) mod p of its column slice A_r = A[:, k0:k1) (adj_dist_kslice), read at byte
+ *   offset k0 * adj_elem_bytes(phi, flags) of each row of A, written to R (m x m, leading
+ *   dimension ldr, uint32 or, with ADJ_OUT_U16, uint16 words x phi's width).  Not collective:
+ *   the partials of all ranks summed mod p give Low(A phi(A)).  Device pointers, async.
+ */
+adj_status_t adjprod_modp_dist_partial(int64_t m, int64_t k, uint32_t p, adj_phi_t phi,
+                                       const uint32_t *A, int64_t lda, uint32_t *R, int64_t ldr,
+                                       int rank, int nranks, const adj_opts_t *opts,
+                                       adj_stream_t stream);
 
 /* ---------------- diagnostics ---------------- */
 const char *adj_status_string(adj_status_t status);

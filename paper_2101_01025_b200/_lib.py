@@ -26,7 +26,7 @@ STATUS = {0: "ADJ_OK", 1: "ADJ_ERR_INVALID_VALUE", 2: "ADJ_ERR_UNSUPPORTED_MODUL
 # every symbol include/adjprod.h declares (checked by tests/test_abi.py)
 EXPORTS = ["adjprod_modp", "adjprod_modp_ex", "adjprod_modp_syrk", "adjprod_modp_workspace_size", "adjprod_modp_auto_depth",
            "gemm_modp", "adj_skew_unitary", "adj_sos", "adj_mod_lower", "adj_comm_get_unique_id",
-           "adj_comm_init", "adj_comm_destroy", "adjprod_modp_dist", "adj_dist_kslice", "adj_elem_bytes", "adjprod_modp_shard", "adj_shard_layout", "adjprod_modp_partial", "adj_sum_partials", "adj_shard_pack", "adj_status_string", "adj_last_error",
+           "adj_comm_init", "adj_comm_destroy", "adjprod_modp_dist", "adj_dist_kslice", "adj_elem_bytes", "adjprod_modp_dist_partial", "adjprod_modp_shard", "adj_shard_layout", "adj_shard_rows", "adjprod_modp_partial", "adj_sum_partials", "adj_shard_pack", "adj_status_string", "adj_last_error",
            "adj_launch_count", "adj_launch_count_reset", "adj_profile_enable", "adj_profile_read"]
 
 
@@ -68,6 +68,8 @@ def lib() -> ctypes.CDLL:
             "adjprod_modp_dist": [i64, i64, u32, ci, vp, i64, vp, i64, ci, vp, ctypes.POINTER(adj_opts_t), vp],
             "adj_dist_kslice": [i64, ci, ci, ctypes.POINTER(i64), ctypes.POINTER(i64)],
             "adj_elem_bytes": [ci, u32, ctypes.POINTER(i64)],
+            "adjprod_modp_dist_partial": [i64, i64, u32, ci, vp, i64, vp, i64, ci, ci, ctypes.POINTER(adj_opts_t), vp],
+            "adj_shard_rows": [i64, i64, u32, ci, ci, ci, ctypes.POINTER(i64), i64, ctypes.POINTER(i64)],
             "adjprod_modp_shard": [i64, i64, u32, ci, vp, i64, vp, i64, ci, ci, ctypes.POINTER(adj_opts_t), vp],
             "adjprod_modp_partial": [i64, i64, u32, ci, vp, i64, vp, i64, ctypes.POINTER(adj_opts_t), vp],
             "adj_sum_partials": [i64, u32, vp, i64, i64, ci, vp, i64, vp],
@@ -223,6 +225,21 @@ def adj_shard_layout(m, k, p, rank, nranks, depth=-1):
     _check(lib().adj_shard_layout(m, k, p, depth, rank, nranks, buf, n.value, ctypes.byref(n), ctypes.byref(e)),
            "adj_shard_layout")
     return [tuple(buf[5 * i: 5 * i + 5]) for i in range(n.value)]
+
+
+def adj_shard_rows(m, k, p, rank, nranks, depth=-1):
+    """[(lo, hi), ...] rows of the top-level operands `rank` pre-adds in adjprod_modp_shard (host)."""
+    n = ctypes.c_int64(0)
+    _check(lib().adj_shard_rows(m, k, p, depth, rank, nranks, None, 0, ctypes.byref(n)), "adj_shard_rows")
+    buf = (ctypes.c_int64 * max(1, 2 * n.value))()
+    _check(lib().adj_shard_rows(m, k, p, depth, rank, nranks, buf, n.value, ctypes.byref(n)), "adj_shard_rows")
+    return [(buf[2 * i], buf[2 * i + 1]) for i in range(n.value)]
+
+
+def adjprod_modp_dist_partial(m, k, p, phi, A, lda, R, ldr, rank, nranks, depth=-1, flags=0, stream=None):
+    o = _opts(depth, flags)
+    _check(lib().adjprod_modp_dist_partial(m, k, p, phi, _ptr(A), lda, _ptr(R), ldr, rank, nranks, ctypes.byref(o),
+                                           _stream(stream)), "adjprod_modp_dist_partial")
 
 
 def adj_dist_kslice(k, nranks, rank):

@@ -378,6 +378,18 @@ adj_status_t launch_leaf_all(const Plan &P, const Ptrs &x, cudaStream_t s) {
   return ADJ_OK;
 }
 
+// output-tile sharding: the top level's pre-addition / split covers only the rows of the tile
+// bands this rank's tiles read (plan.cpp apply_shard); otherwise every row
+void set_shard_rows(const Plan &P, RowRanges &R) {
+  std::memset(&R, 0, sizeof(R));
+  if (P.shard_n <= 0) return;
+  R.n = (int32_t)P.shard_rows.size();
+  for (int i = 0; i < R.n; ++i) {
+    R.lo[i] = P.shard_rows[(size_t)i].first;
+    R.hi[i] = P.shard_rows[(size_t)i].second;
+  }
+}
+
 adj_status_t run_split(const Plan &P, const InView &v, int64_t rows, int64_t cols, int64_t rows_pad, int64_t op_row,
                        uint8_t *arena, cudaStream_t s) {
   SplitParams sp;
@@ -392,6 +404,7 @@ adj_status_t run_split(const Plan &P, const InView &v, int64_t rows, int64_t col
   sp.scheme = P.scheme;
   sp.planes = P.planes;
   sp.mod = P.mod;
+  set_shard_rows(P, sp.row_ranges);
   LAUNCH_CLS(CLS_PRE, launch_split(sp, s));
   return ADJ_OK;
 }
@@ -427,6 +440,7 @@ adj_status_t run_tree(const Plan &P, const InView &root, const Ptrs &x, cudaStre
     pp.arena = reinterpret_cast<int8_t *>(x.ws + P.arenas[L.arena].offset);
     pp.res32 = P.res32 ? 1 : 0;
     pp.mod = P.mod;
+    if (l == 1) set_shard_rows(P, pp.rows);
     for (int n = 0; n < L.n_nodes; ++n) {
       PreNode &N = pp.nodes[n];
       N.in = views[l][n];
@@ -939,6 +953,29 @@ adj_status_t adj_shard_layout(int64_t m, int64_t k, uint32_t p, int depth, int r
       rects[5 * i + 4] = R.lower;
     }
   }
+  return ADJ_OK;
+}
+
+adj_status_t adj_shard_rows(int64_t m, int64_t k, uint32_t p, int depth, int rank, int nranks, int64_t *ranges,
+                            int64_t max_ranges, int64_t *n_ranges) {
+  if (!n_ranges) return fail(ADJ_ERR_INVALID_VALUE, "null output");
+  if (m < 0 || k < 0 || nranks < 1 || rank < 0 || rank >= nranks) return fail(ADJ_ERR_INVALID_VALUE, "bad arguments");
+  if (!valid_modulus(p)) return fail(ADJ_ERR_UNSUPPORTED_MODULUS, "p=%u is not an odd prime in [3, 262139]", p);
+  *n_ranges = 0;
+  if (m == 0) return ADJ_OK;
+  adj_opts_t o{depth, 0, nullptr, 0};
+  const int d = shard_depth(m, k, p, &o);
+  if (d > 1) return fail(ADJ_ERR_INVALID_VALUE, "output-tile sharding runs at depth 0 or 1 (got %d)", d);
+  Plan P;
+  const char *err = nullptr;
+  if (!build_syrk_plan(P, m, std::max<int64_t>(k, 1), p, 0, d, query_sms(), &err, rank, nranks))
+    return fail(ADJ_ERR_INVALID_VALUE, "plan: %s", err ? err : "unsupported");
+  *n_ranges = (int64_t)P.shard_rows.size();
+  for (size_t i = 0; i < P.shard_rows.size(); ++i)
+    if (ranges && (int64_t)i < max_ranges) {
+      ranges[2 * i] = P.shard_rows[i].first;
+      ranges[2 * i + 1] = P.shard_rows[i].second;
+    }
   return ADJ_OK;
 }
 

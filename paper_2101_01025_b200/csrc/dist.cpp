@@ -351,6 +351,15 @@ adj_status_t adj_elem_bytes(adj_phi_t phi, uint32_t flags, int64_t *bytes) {
   return ADJ_OK;
 }
 
+adj_status_t adjprod_modp_dist_partial(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, const uint32_t *A, int64_t lda,
+                                       uint32_t *R, int64_t ldr, int rank, int nranks, const adj_opts_t *opts,
+                                       adj_stream_t stream) {
+  if (m < 0 || k < 0 || nranks < 1 || rank < 0 || rank >= nranks) return ADJ_ERR_INVALID_VALUE;
+  int64_t k0 = 0, k1 = 0;
+  adj_dist_kslice(k, nranks, rank, &k0, &k1);
+  return adjprod_modp_ex(m, k1 - k0, p, phi, kslice_ptr(A, phi, opts ? opts->flags : 0, k0), lda, R, ldr, opts, stream);
+}
+
 adj_status_t adjprod_modp_dist(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, const uint32_t *A, int64_t lda,
                                uint32_t *C, int64_t ldc, int root, adj_comm_t comm, const adj_opts_t *opts,
                                adj_stream_t stream) {
@@ -362,26 +371,41 @@ adj_status_t adjprod_modp_dist(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, 
   if (opts && (opts->flags & ADJ_DIST_TILES)) return dist_tiles(m, k, p, phi, A, lda, C, ldc, root, comm, opts, stream);
   if (opts && (opts->flags & ADJ_DIST_P2P) && phi == ADJ_PHI_T && G > 1)
     return dist_p2p(m, k, p, phi, A, lda, C, ldc, root, comm, opts, stream);
-  const int w = adj_phi_width(phi);
-  int64_t k0 = 0, k1 = 0;
-  adj_dist_kslice(k, G, r, &k0, &k1);
-  const uint32_t *Ar = kslice_ptr(A, phi, opts ? opts->flags : 0, k0);
-  if (G == 1) return adjprod_modp_ex(m, k1 - k0, p, phi, Ar, lda, C, ldc, opts, stream);
+  if (G == 1) return adjprod_modp_dist_partial(m, k, p, phi, A, lda, C, ldc, 0, 1, opts, stream);
   if (!load_nccl()) return ADJ_ERR_NCCL;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  // partial Low(A_r phi(A_r)) in a dense m x m buffer (the caller's Up(C) stays untouched)
-  uint32_t *W = nullptr;
-  const size_t count = (size_t)m * m * w;
-  if (adj_pool_alloc(reinterpret_cast<void **>(&W), count * 4, s) != cudaSuccess) return ADJ_ERR_CUDA;
-  adj_status_t st = adjprod_modp_ex(m, k1 - k0, p, phi, Ar, lda, W, m, opts, stream);
+  const int w = adj_phi_width(phi);
+  const uint32_t flags = opts ? opts->flags : 0;
+  // the rank's partial Low(A_r phi(A_r)) in a dense m x m buffer (the caller's Up(C) stays
+  // untouched): uint16 words when the residues fit (ADJ_OUT_U16), then its lower triangle packed
+  // as uint32 words -- the reduce moves m (m + 1) / 2 words per element instead of m^2
+  const bool narrow = p < 65536 && !(flags & (ADJ_HERK_ALG1 | ADJ_FILL_UPPER));
+  adj_opts_t o = opts ? *opts : adj_opts_t{-1, 0, nullptr, 0};
+  o.flags &= ~(ADJ_FILL_UPPER | ADJ_DIST_TILES | ADJ_DIST_P2P);
+  if (narrow) o.flags |= ADJ_OUT_U16;
+  const size_t dense = (size_t)m * (size_t)m * (size_t)w * (narrow ? 2 : 4);
+  const size_t packed = (size_t)(m * (m + 1) / 2) * (size_t)w;
+  void *W = nullptr, *Pk = nullptr;
+  adj_status_t st = ADJ_OK;
+  if (adj_pool_alloc(&W, dense, s) != cudaSuccess || adj_pool_alloc(&Pk, packed * 4, s) != cudaSuccess) st = ADJ_ERR_CUDA;
+  if (st == ADJ_OK) st = adjprod_modp_dist_partial(m, k, p, phi, A, lda, static_cast<uint32_t *>(W), m, r, G, &o, stream);
+  if (st == ADJ_OK &&
+      adj::launch_pack_lower(m, w, W, m, narrow ? 2 : 4, static_cast<uint32_t *>(Pk), s) != cudaSuccess)
+    st = ADJ_ERR_CUDA;
+  // a local failure must not leave the peers blocked in the reduce
+  st = agree_status(comm, st, s);
   if (st == ADJ_OK) {
-    // exact: each entry is a sum of G residues < G p < 2^32
-    if (g_nccl.Reduce(W, W, count, ncclUint32, ncclSum, root, comm->comm, s) != ncclSuccess) st = ADJ_ERR_NCCL;
+    // exact: each word is a sum of G residues < G p < 2^32
+    if (g_nccl.Reduce(Pk, Pk, packed, ncclUint32, ncclSum, root, comm->comm, s) != ncclSuccess) st = ADJ_ERR_NCCL;
   }
   if (st == ADJ_OK && r == root) {
-    if (adj::launch_mod_lower(m, w, W, m, C, ldc, adj::make_modp(p), s) != cudaSuccess) st = ADJ_ERR_CUDA;
+    if (adj::launch_unpack_mod_lower(m, w, static_cast<uint32_t *>(Pk), C, ldc, adj::make_modp(p), s) != cudaSuccess)
+      st = ADJ_ERR_CUDA;
+    else if ((flags & ADJ_FILL_UPPER) && adj::launch_fill_upper(m, w, C, ldc, adj::make_modp(p), s) != cudaSuccess)
+      st = ADJ_ERR_CUDA;
   }
-  cudaFreeAsync(W, s);
+  if (W) cudaFreeAsync(W, s);
+  if (Pk) cudaFreeAsync(Pk, s);
   return st;
 }
 

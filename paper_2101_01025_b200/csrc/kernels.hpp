@@ -21,6 +21,11 @@ cudaError_t launch_scale_lower(int64_t m, int w, uint32_t *X, int64_t ldx, uint3
                                cudaStream_t s);
 cudaError_t launch_mod_lower(int64_t m, int w, const uint32_t *src, int64_t lds, uint32_t *dst, int64_t ldd,
                              const ModP &mod, cudaStream_t s);
+// split-K exchange: Low(src) (uint16 / uint32 words, esz 2 / 4, w per element) packed row by row
+// into uint32 words (element offset i (i + 1) / 2 for row i), and the packed sum back into Low(C) mod p
+cudaError_t launch_pack_lower(int64_t m, int w, const void *src, int64_t lds, int esz, uint32_t *dst, cudaStream_t s);
+cudaError_t launch_unpack_mod_lower(int64_t m, int w, const uint32_t *src, uint32_t *C, int64_t ldc, const ModP &mod,
+                                    cudaStream_t s);
 // Low(X) <- 0, elements of esz bytes (even), one launch
 cudaError_t launch_zero_lower(int64_t m, void *X, int64_t ld_bytes, int esz, cudaStream_t s);
 // pack (to_buf = 1) / unpack (to_buf = 0) / zero (to_buf = 2) the listed regions of C into / from a contiguous buffer

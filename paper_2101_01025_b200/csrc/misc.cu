@@ -31,6 +31,49 @@ cudaError_t launch_mod_lower(int64_t m, int w, const uint32_t *src, int64_t lds,
   return cudaGetLastError();
 }
 
+// split-K exchange: Low(src) packed row by row (row i holds i + 1 elements of w words at
+// element offset i (i + 1) / 2) as uint32 words; src words are uint16 (esz 2) or uint32
+template <typename T>
+__global__ void pack_lower_kernel(int64_t row0, int w, const T *src, int64_t lds, uint32_t *dst) {
+  const int64_t i = row0 + blockIdx.y;
+  const T *a = src + i * lds * w;
+  uint32_t *b = dst + (i * (i + 1) / 2) * w;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < (i + 1) * w; j += (int64_t)gridDim.x * blockDim.x)
+    b[j] = (uint32_t)a[j];
+}
+// and back: C = packed mod p on Low(C)
+__global__ void unpack_mod_lower_kernel(int64_t row0, int w, const uint32_t *src, uint32_t *C, int64_t ldc, ModP mod) {
+  const int64_t i = row0 + blockIdx.y;
+  const uint32_t *a = src + (i * (i + 1) / 2) * w;
+  uint32_t *b = C + i * ldc * w;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < (i + 1) * w; j += (int64_t)gridDim.x * blockDim.x)
+    b[j] = mod_u32(a[j], mod);
+}
+
+cudaError_t launch_pack_lower(int64_t m, int w, const void *src, int64_t lds, int esz, uint32_t *dst, cudaStream_t s) {
+  if (m == 0) return cudaSuccess;
+  const int64_t per_row = (m * w + 255) / 256;
+  for (int64_t r0 = 0; r0 < m; r0 += 65535) {
+    const int64_t rows = (m - r0) < 65535 ? (m - r0) : 65535;
+    const dim3 grid((unsigned)(per_row < 64 ? per_row : 64), (unsigned)rows);
+    if (esz == 2) pack_lower_kernel<uint16_t><<<grid, 256, 0, s>>>(r0, w, static_cast<const uint16_t *>(src), lds, dst);
+    else pack_lower_kernel<uint32_t><<<grid, 256, 0, s>>>(r0, w, static_cast<const uint32_t *>(src), lds, dst);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_unpack_mod_lower(int64_t m, int w, const uint32_t *src, uint32_t *C, int64_t ldc, const ModP &mod,
+                                    cudaStream_t s) {
+  if (m == 0) return cudaSuccess;
+  const int64_t per_row = (m * w + 255) / 256;
+  for (int64_t r0 = 0; r0 < m; r0 += 65535) {
+    const int64_t rows = (m - r0) < 65535 ? (m - r0) : 65535;
+    unpack_mod_lower_kernel<<<dim3((unsigned)(per_row < 64 ? per_row : 64), (unsigned)rows), 256, 0, s>>>(
+        r0, w, src, C, ldc, mod);
+  }
+  return cudaGetLastError();
+}
+
 // Low(X) <- beta Low(X) (SYRK form with k = 0)
 __global__ void scale_lower_kernel(int64_t row0, int w, uint32_t *X, int64_t ldx, uint32_t beta, ModP mod) {
   const int64_t i = row0 + blockIdx.y;

@@ -213,27 +213,72 @@ int auto_depth(int64_t m, int64_t k, uint32_t p, int phi) {
 // Ownership unit: a pair {(I, J), (J, I)}, I >= J, of 256 x 256 tiles of the top-level product
 // grid (depth 1: the (m/2) grid of P1..P5; depth 0: the grid of C).  Cost in leaf-tile units: a
 // diagonal pair has its SYRK tile(s) and, at depth 1, the P3 / P4 tiles (I, I); an off-diagonal
-// pair twice the GEMM tiles.  Pairs go, largest first, to the least loaded rank (deterministic).
+// pair twice the GEMM tiles.
+// A pair (I, J) reads the operand rows of tile bands I and J only, so a rank whose pairs touch
+// few bands pre-adds (K1) only those rows.  The bands are cut into g contiguous groups and the
+// triangle into the g (g + 1) / 2 blocks of group pairs (gi >= gj); whole blocks are dealt,
+// largest first, to the least loaded rank (ties: the rank that already touches the block's
+// groups).  g is chosen per (T, nranks) to minimise the modelled per-rank time
+//   load_r / total + kK1Share * bands_r / T
+// (kK1Share: K1's measured share of a depth-1 step); g = T degenerates to dealing
+// single pairs.  Deterministic: every rank computes the same table.
+static constexpr double kK1Share = 0.06;
+
 std::vector<int> shard_owners(int64_t T, int depth, int nranks) {
-  std::vector<int> owner((size_t)(T * (T + 1) / 2), 0);
-  std::vector<std::pair<int, int64_t>> order;   // (cost, pair index)
-  for (int64_t I = 0; I < T; ++I)
-    for (int64_t J = 0; J <= I; ++J) {
-      const int cost = depth == 0 ? 1 : (I == J ? 5 : 7);
-      order.push_back({cost, I * (I + 1) / 2 + J});
+  const int64_t npairs = T * (T + 1) / 2;
+  auto cost = [&](int64_t I, int64_t J) -> int64_t { return depth == 0 ? 1 : (I == J ? 5 : 7); };
+  std::vector<int> best_owner;
+  double best_score = 1e30;
+  std::vector<int64_t> cand;
+  for (int64_t g = 1; g <= std::min<int64_t>(T, 24); ++g) cand.push_back(g);
+  if (T > 24) cand.push_back(T);
+  for (int64_t g : cand) {
+    std::vector<int64_t> gb((size_t)g + 1);
+    for (int64_t i = 0; i <= g; ++i) gb[(size_t)i] = T * i / g;
+    struct Blk { int64_t gi, gj, cost; };
+    std::vector<Blk> blks;
+    for (int64_t gi = 0; gi < g; ++gi)
+      for (int64_t gj = 0; gj <= gi; ++gj) {
+        int64_t c = 0;
+        for (int64_t I = gb[gi]; I < gb[gi + 1]; ++I)
+          for (int64_t J = gb[gj]; J < std::min(gb[gj + 1], I + 1); ++J) c += cost(I, J);
+        if (c > 0) blks.push_back({gi, gj, c});
+      }
+    if ((int64_t)blks.size() < nranks && g < T) continue;
+    std::stable_sort(blks.begin(), blks.end(), [](const Blk &a, const Blk &b) { return a.cost > b.cost; });
+    std::vector<int64_t> load((size_t)nranks, 0);
+    std::vector<std::vector<char>> touch((size_t)nranks, std::vector<char>((size_t)g, 0));
+    std::vector<int> blk_owner(blks.size(), 0);
+    for (size_t b = 0; b < blks.size(); ++b) {
+      int bestr = 0;
+      int64_t bl = -1;
+      int bn = 3;
+      for (int r = 0; r < nranks; ++r) {
+        const int fresh = (touch[r][(size_t)blks[b].gi] ? 0 : 1) + (blks[b].gi != blks[b].gj && !touch[r][(size_t)blks[b].gj] ? 1 : 0);
+        if (bl < 0 || load[r] < bl || (load[r] == bl && fresh < bn)) { bestr = r; bl = load[r]; bn = fresh; }
+      }
+      blk_owner[b] = bestr;
+      load[bestr] += blks[b].cost;
+      touch[bestr][(size_t)blks[b].gi] = touch[bestr][(size_t)blks[b].gj] = 1;
     }
-  std::stable_sort(order.begin(), order.end(), [](const std::pair<int, int64_t> &a, const std::pair<int, int64_t> &b) {
-    return a.first > b.first;
-  });
-  std::vector<int64_t> load((size_t)nranks, 0);
-  for (const auto &o : order) {
-    int best = 0;
-    for (int r = 1; r < nranks; ++r)
-      if (load[r] < load[best]) best = r;
-    owner[(size_t)o.second] = best;
-    load[best] += o.first;
+    int64_t total = 0;
+    for (int64_t l : load) total += l;
+    double score = 0;
+    for (int r = 0; r < nranks; ++r) {
+      int64_t bands = 0;
+      for (int64_t q = 0; q < g; ++q) if (touch[r][(size_t)q]) bands += gb[q + 1] - gb[q];
+      score = std::max(score, (double)load[r] / (double)std::max<int64_t>(1, total) + kK1Share * (double)bands / (double)T);
+    }
+    if (score < best_score - 1e-12) {
+      best_score = score;
+      best_owner.assign((size_t)npairs, 0);
+      for (size_t b = 0; b < blks.size(); ++b)
+        for (int64_t I = gb[blks[b].gi]; I < gb[blks[b].gi + 1]; ++I)
+          for (int64_t J = gb[blks[b].gj]; J < std::min(gb[blks[b].gj + 1], I + 1); ++J)
+            best_owner[(size_t)(I * (I + 1) / 2 + J)] = blk_owner[b];
+    }
   }
-  return owner;
+  return best_owner;
 }
 
 bool apply_shard(Plan &P, int rank, int nranks, const char **err) {
@@ -253,6 +298,21 @@ bool apply_shard(Plan &P, int rank, int nranks, const char **err) {
     if (owns((x >> 12) & 0xFFF, x & 0xFFF)) { kept.push_back(x); kept.push_back(P.tiles[t + 1]); }
   }
   P.tiles.swap(kept);
+  // the tile bands this rank's pairs read: K1 (or the depth-0 split) pre-adds only their rows
+  {
+    std::vector<char> band((size_t)T, 0);
+    for (int64_t I = 0; I < T; ++I)
+      for (int64_t J = 0; J <= I; ++J)
+        if (owns(I, J)) band[(size_t)I] = band[(size_t)J] = 1;
+    P.shard_rows.clear();
+    for (int64_t I = 0; I < T; ++I) {
+      if (!band[(size_t)I]) continue;
+      const int64_t r0 = 256 * I, r1 = std::min<int64_t>(256 * (I + 1), grid_rows);
+      if (!P.shard_rows.empty() && P.shard_rows.back().second == r0) P.shard_rows.back().second = r1;
+      else P.shard_rows.push_back({r0, r1});
+    }
+    if ((int)P.shard_rows.size() > kMaxRowRanges) P.shard_rows.assign(1, {0, grid_rows});   // too fragmented: all rows
+  }
   // C regions this rank writes (for packing / gathering) and, at depth 1, the 64 x 64 lower tile
   // pairs of the K4 combine inside the owned 256-pairs
   P.shard_rects.clear();

@@ -6,6 +6,7 @@
 #pragma once
 #include <cstddef>
 #include <cstdint>
+#include <utility>
 #include <vector>
 
 #include "field.hpp"
@@ -87,6 +88,7 @@ struct Plan {
   // output-tile sharding (adjprod_modp_shard): this plan computes only the tiles `shard_rank` owns
   int shard_rank = -1, shard_n = 0;
   std::vector<ShardRect> shard_rects;  // the regions of C it writes (Low part when `lower`)
+  std::vector<std::pair<int64_t, int64_t>> shard_rows;   // [r0, r1) rows of the top level's operands its tiles read
   std::vector<uint32_t> comb_pairs;    // depth 1: K4 64 x 64 lower tile pairs (ti << 16 | tj)
   uint32_t *d_comb_pairs = nullptr;
 };

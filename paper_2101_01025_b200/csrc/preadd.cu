@@ -561,7 +561,9 @@ __global__ void __launch_bounds__(256, 4) preadd_kernel(const __grid_constant__ 
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= g_main + g_pad) return;
   const int type = N.in.type;
-  for (int64_t r = blockIdx.y; r < P.rows_pad; r += gridDim.y) {
+  const int64_t nrows = range_rows(P.rows, P.rows_pad);
+  for (int64_t j = blockIdx.y; j < nrows; j += gridDim.y) {
+    const int64_t r = range_row(P.rows, j);
     if (g >= g_main) {
       const int64_t col = P.kh + (g - g_main) * 4;
 #pragma unroll
@@ -585,8 +587,8 @@ cudaError_t launch_preadd(const PreParams &p, cudaStream_t s) {
   if (p.n_nodes == 0) return cudaSuccess;
   const int64_t groups = p.kh / 8 + (p.kpad - p.kh) / 4;
   dim3 block(256);
-  dim3 grid((unsigned)((groups + 255) / 256), (unsigned)(p.rows_pad < 65535 ? p.rows_pad : 65535),
-            (unsigned)p.n_nodes);
+  const int64_t nrows = range_rows(p.rows, p.rows_pad);
+  dim3 grid((unsigned)((groups + 255) / 256), (unsigned)(nrows < 65535 ? nrows : 65535), (unsigned)p.n_nodes);
 #define PRE(S, Y) preadd_kernel<S, Y><<<grid, block, 0, s>>>(p)
   if (p.scheme == 0) { if (p.ykind == 0) PRE(0, 0); else PRE(0, 1); }
   else if (p.scheme == 1) { if (p.ykind == 0) PRE(1, 0); else PRE(1, 1); }
@@ -606,7 +608,9 @@ __global__ void __launch_bounds__(256) split_kernel(const __grid_constant__ Spli
   const int64_t c0 = g * 8;
   const int64_t ps = P.rows_pad * P.kpad;
   const InView &v = P.in;
-  for (int64_t r = blockIdx.y; r < P.rows_pad; r += gridDim.y) {
+  const int64_t nrows = range_rows(P.row_ranges, P.rows_pad);
+  for (int64_t j = blockIdx.y; j < nrows; j += gridDim.y) {
+    const int64_t r = range_row(P.row_ranges, j);
     InView vv = v;
     if (r >= P.rows) vv.rows_valid = 0;
     const bool fast = vv.vec_ok && r < vv.rows_valid && c0 + 7 < vv.cols_valid && c0 + 7 < P.cols;
@@ -703,7 +707,9 @@ __global__ void __launch_bounds__(256, 6) split_plain_kernel(const __grid_consta
   const int64_t c0 = g * 16;
   const int64_t ps = P.rows_pad * P.kpad;
   const InView &v = P.in;
-  for (int64_t r = blockIdx.y; r < P.rows_pad; r += gridDim.y) {
+  const int64_t nrows = range_rows(P.row_ranges, P.rows_pad);
+  for (int64_t j = blockIdx.y; j < nrows; j += gridDim.y) {
+    const int64_t r = range_row(P.row_ranges, j);
     InView vv = v;
     if (r >= P.rows) vv.rows_valid = 0;
     const bool fast = vv.vec_ok && r < vv.rows_valid && c0 + 15 < vv.cols_valid && c0 + 15 < P.cols;
@@ -757,15 +763,17 @@ __global__ void __launch_bounds__(256, 6) split_plain_kernel(const __grid_consta
 }
 
 cudaError_t launch_split(const SplitParams &p, cudaStream_t s) {
+  const int64_t nrows = range_rows(p.row_ranges, p.rows_pad);
+  const unsigned gy = (unsigned)(nrows < 65535 ? nrows : 65535);
   if (p.mode == 0) {
-    dim3 g16((unsigned)((p.kpad / 16 + 255) / 256), (unsigned)(p.rows_pad < 65535 ? p.rows_pad : 65535));
+    dim3 g16((unsigned)((p.kpad / 16 + 255) / 256), gy);
     if (p.scheme == 0) split_plain_kernel<0><<<g16, 256, 0, s>>>(p);
     else if (p.scheme == 1) split_plain_kernel<1><<<g16, 256, 0, s>>>(p);
     else if (p.scheme == 2) split_plain_kernel<2><<<g16, 256, 0, s>>>(p);
     else split_plain_kernel<3><<<g16, 256, 0, s>>>(p);
     return cudaGetLastError();
   }
-  dim3 grid((unsigned)((p.kpad / 8 + 255) / 256), (unsigned)(p.rows_pad < 65535 ? p.rows_pad : 65535));
+  dim3 grid((unsigned)((p.kpad / 8 + 255) / 256), gy);
   if (p.scheme == 0) split_kernel<0><<<grid, 256, 0, s>>>(p);
   else if (p.scheme == 1) split_kernel<1><<<grid, 256, 0, s>>>(p);
   else if (p.scheme == 2) split_kernel<2><<<grid, 256, 0, s>>>(p);

@@ -11,6 +11,7 @@ namespace adj {
 constexpr int kMaxMaps = 4;        // one TMA map per operand arena (levels 0..3)
 constexpr int kMaxProducts = 64;   // leaf products in one grouped launch (depth <= 3)
 constexpr int kMaxNodes = 32;      // recursion nodes per level in one batched launch
+constexpr int kMaxRowRanges = 8;   // output-tile sharding: row ranges a rank's K1 / split covers
 constexpr int kBM = 128;           // UMMA M / tile rows
 constexpr int kBK = 128;           // bytes of K per pipeline stage (one 128B swizzle atom)
 
@@ -95,8 +96,15 @@ struct PreNode {
   int64_t side_kpad, side_rows_pad, side_x_row, side_y_row;
 };
 
+// rows [0, rows_pad) of the arena (n = 0) or only the listed ranges (output-tile sharding)
+struct RowRanges {
+  int32_t n, pad_;
+  int64_t lo[kMaxRowRanges], hi[kMaxRowRanges];
+};
+
 struct PreParams {
   PreNode nodes[kMaxNodes];
+  RowRanges rows;
   int32_t n_nodes;
   int32_t scheme, planes;
   int32_t ykind;           // 0: Y = i I ; 1: Y = [[a,b],[-b,a]] (x) I
@@ -113,6 +121,7 @@ struct PreParams {
 // plain limb split of a view into arena planes (depth 0, gemm_modp, 2M's X / Y)
 struct SplitParams {
   InView in;
+  RowRanges row_ranges;
   int64_t rows, cols;      // logical size (>= valid); padding written as zero
   int64_t rows_pad, kpad;
   int64_t op_row;

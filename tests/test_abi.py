@@ -4,6 +4,7 @@ import ctypes
 import os
 import re
 
+import numpy as np
 import pytest
 
 import paper_2101_01025_b200 as adj
@@ -172,15 +173,41 @@ def test_shard_layout_partitions_low_c(m, k, depth, nranks):
 
 
 def test_shard_layout_balanced():
-    """The deterministic greedy deal keeps the ranks' shares within one 256-tile pair."""
-    m, k = 8192, 8192
-    for depth in (0, 1):
-        for n in (2, 4, 8):
-            sizes = []
-            for r in range(n):
-                rects = adj.adj_shard_layout(m, k, 8191, r, n, depth=depth)
-                sizes.append(sum(rows * cols for (_, _, rows, cols, _) in rects))
-            assert max(sizes) - min(sizes) <= 4 * 256 * 256, (depth, n, sizes)
+    """The deterministic block deal keeps the ranks' shares of Low(C) within 10% of the mean
+    (whole blocks of band groups are dealt; the planner trades a few % of leaf balance for
+    pre-adding only the rows a rank reads)."""
+    for m in (8192, 32768):
+        for depth in (0, 1):
+            for n in (2, 4, 8):
+                sizes = []
+                for r in range(n):
+                    rects = adj.adj_shard_layout(m, m, 8191, r, n, depth=depth)
+                    sizes.append(sum(rows * cols for (_, _, rows, cols, _) in rects))
+                assert max(sizes) <= 1.10 * (sum(sizes) / n), (m, depth, n, sizes)
+
+
+@pytest.mark.parametrize("m,depth,nranks", [(32768, 1, 8), (32768, 1, 4), (32768, 1, 3), (8192, 1, 8), (8192, 0, 8),
+                                            (1030, 1, 3), (700, 0, 2), (32768, 1, 1)])
+def test_shard_rows_cover_every_band_the_tiles_read(m, depth, nranks):
+    """A rank's pre-addition rows (adj_shard_rows) cover the operand rows of every tile pair it
+    owns -- bands I and J of each owned pair (I, J), read off its C11 regions (depth 1) or its C
+    regions (depth 0) -- and, at 8 ranks of c3, only half of all rows (the blocked deal)."""
+    mh = -(-m // 2) if depth == 1 else m
+    rows_pad = -(-mh // 128) * 128
+    total = []
+    for r in range(nranks):
+        ranges = adj.adj_shard_rows(m, m, 8191, r, nranks, depth=depth)
+        covered = np.zeros(rows_pad + 256, dtype=bool)
+        for lo, hi in ranges:
+            assert 0 <= lo < hi <= rows_pad
+            covered[lo:hi] = True
+        for (r0, c0, rows, cols, _) in adj.adj_shard_layout(m, m, 8191, r, nranks, depth=depth):
+            if r0 < mh and c0 < mh:     # C11 (depth 1) / C (depth 0): tile pair (r0 / 256, c0 / 256)
+                for b in (r0 // 256, c0 // 256):
+                    assert covered[256 * b: min(256 * b + 256, rows_pad)].all(), (r, b)
+        total.append(int(covered.sum()))
+    if (m, depth, nranks) == (32768, 1, 8):
+        assert max(total) <= rows_pad // 2, total
 
 
 def test_maximum_sizes_are_planned_or_refused():

@@ -701,3 +701,57 @@ def test_adjprod_Q_compact_io(adj, p, depth, m, k):
             torch.cuda.synchronize()
             got = C.cpu().numpy().view(np.uint16 if out16 else np.uint32).astype(np.uint32).reshape(m, m, 4)
             assert np.array_equal(got[lo], ref[lo]), (p, depth, m, k, dM.element_size(), out16)
+
+
+# ---------------------------------------------------------------- multi-GPU building blocks, round 2
+@pytest.mark.parametrize("p", [8191, 65521])
+@pytest.mark.parametrize("depth,m,k", [(1, 3000, 700), (0, 4100, 300), (1, 1030, 520)])
+@pytest.mark.parametrize("nranks", [3, 8])
+def test_shard_rank_local_preadd_with_garbage_workspace(adj, p, depth, m, k, nranks):
+    """Each rank's share pre-adds only the rows of the tile bands its tiles read (adj_shard_rows);
+    with a caller workspace filled with garbage before every rank's call, no rank may read a row
+    it did not write: all shares into one C give Low(C) bit-exactly, Up(C) untouched."""
+    import torch
+    A = uniform_matrix(m, k, seed=m + nranks + depth, p=p)
+    dA = to_dev(A)
+    ws_bytes = adj.adjprod_modp_workspace_size(m, k, p, 0, depth)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
+    C = torch.full((m, m), -1, dtype=torch.int32, device="cuda")
+    for r in range(nranks):
+        ws.fill_(0x5A + 13 * r)
+        adj.adjprod_modp_shard(m, k, p, 0, dA, k, C, m, r, nranks, depth=depth, workspace=ws, workspace_bytes=ws_bytes)
+    got = to_host(C)
+    lo = np.tril(np.ones((m, m), dtype=bool))
+    assert np.array_equal(got[lo], oracle.syrk_t(A, p)[lo])
+    assert (got[~lo] == 0xFFFFFFFF).all()
+
+
+@pytest.mark.parametrize("phi", ["T", "H", "Q"])
+@pytest.mark.parametrize("in16", [False, True])
+@pytest.mark.parametrize("G", [2, 3, 8])
+def test_dist_partial_pointer_per_rank(adj, phi, in16, G):
+    """adjprod_modp_dist_partial -- the per-rank computation of the split-K path, with the exact
+    k-slice pointer adjprod_modp_dist builds (k0 x adj_elem_bytes(phi, flags) bytes into each
+    row) -- for phi = T / H / Q and uint16 / uint32 input: the ranks' partials summed mod p give
+    the oracle's Low(C)."""
+    import torch
+    from inputs import uniform_matrix_quat
+    p, m, k = 8191, 130, 333
+    w = {"T": 1, "H": 2, "Q": 4}[phi]
+    gen = {"T": uniform_matrix, "H": uniform_matrix_ext, "Q": uniform_matrix_quat}[phi]
+    ref = {"T": oracle.syrk_t, "H": oracle.syrk_h, "Q": oracle.syrk_q}[phi]
+    A = gen(m, k, G + 5, p)
+    want = ref(A, p).reshape(m, m, w).astype(np.int64)
+    code = {"T": adj.ADJ_PHI_T, "H": adj.ADJ_PHI_H, "Q": adj.ADJ_PHI_Q}[phi]
+    flags = adj.ADJ_IN_U16 if in16 else 0
+    assert adj.adj_elem_bytes(code, flags) == (2 if in16 else 4) * w
+    dA = torch.from_numpy(A.reshape(m, k * w).astype(np.uint16).view(np.int16)).cuda() if in16 else to_dev(A.reshape(m, k * w))
+    acc = np.zeros((m, m, w), dtype=np.int64)
+    for r in range(G):
+        R = torch.full((m, m * w), -1, dtype=torch.int32, device="cuda")
+        adj.adjprod_modp_dist_partial(m, k, p, code, dA, k, R, m, r, G, flags=flags)
+        part = to_host(R).reshape(m, m, w)
+        acc += np.where(np.tril(np.ones((m, m), dtype=bool))[:, :, None], part, 0)
+        assert (part[~np.tril(np.ones((m, m), dtype=bool))] == 0xFFFFFFFF).all()
+    lo = np.tril(np.ones((m, m), dtype=bool))
+    assert np.array_equal((acc % p)[lo], want[lo])
