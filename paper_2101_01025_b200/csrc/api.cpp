@@ -830,6 +830,7 @@ adj_status_t adjprod_modp_shard(int64_t m, int64_t k, uint32_t p, adj_phi_t phi,
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   Plan *P = nullptr;
   if ((st = shard_plan(&P, m, k, p, depth, rank, nranks, dev, sms)) != ADJ_OK) return st;
+  if (P->shard_rects.empty()) return ADJ_OK;   // more ranks than tile pairs: this rank owns nothing
   if (k == 0) {   // Low(C) = 0 on the owned regions: one launch over the region list
     if (P->shard_rects.empty()) return ADJ_OK;
     std::vector<RectDev> rd(P->shard_rects.size());
