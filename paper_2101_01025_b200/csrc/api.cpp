@@ -440,6 +440,7 @@ adj_status_t run_tree(const Plan &P, const InView &root, const Ptrs &x, cudaStre
     pp.arena = reinterpret_cast<int8_t *>(x.ws + P.arenas[L.arena].offset);
     pp.res32 = P.res32 ? 1 : 0;
     pp.mod = P.mod;
+    pp.kc = make_k1const(P.p, P.Y.a, P.Y.b);
     if (l == 1) set_shard_rows(P, pp.rows);
     for (int n = 0; n < L.n_nodes; ++n) {
       PreNode &N = pp.nodes[n];

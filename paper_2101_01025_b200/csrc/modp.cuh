@@ -132,24 +132,64 @@ __host__ __device__ __forceinline__ uint32_t lazy_off(uint32_t v_bits, float vf,
   const uint32_t u = v_bits + h - (uint32_t)q * p;
   return umin32(umin32(u, u - p), u + p);
 }
-// S1 = (A21 - A11) Y and S2 = A22 - A21 Y as offset residues, for canonical
-// inputs x < p: YK = 0, Y = i I (scalar ya, the two lanes a / b independent); YK = 1, Y = Rot2(a, b)
-// acting on the column pair (j, j + k/4): [X1 X2] Y = [a X1 - b X2, b X1 + a X2].
-template <int YK>
-__host__ __device__ __forceinline__ void lazy_s1_s2(uint32_t x11a, uint32_t x11b, uint32_t x21a, uint32_t x21b,
-                                                    uint32_t x22a, uint32_t x22b, uint32_t ya, uint32_t yb, float invp,
-                                                    uint32_t p, uint32_t h, uint32_t &s1a, uint32_t &s1b,
-                                                    uint32_t &s2a, uint32_t &s2b) {
+// K1 constants of one prime and skew-unitary Y (host-made, passed to the kernel)
+struct K1Const {
+  ModP mod;
+  uint32_t ya, yb;     // Y = ya I (YK = 0) or Rot2(ya, yb) (YK = 1)
+  uint32_t bias;       // p <= 16763: h + p (2p + 1) -- makes every exact int32 v of S1 / S2 non-negative
+  float invp;          // p > 16763, Rot2: float quotient estimate
+  ShoupW ya_w, nya_w;  // p > 16763, Y = ya I: Shoup weights of ya and -ya
+};
+inline K1Const make_k1const(uint32_t p, uint32_t ya, uint32_t yb) {
+  K1Const k;
+  k.mod = make_modp(p);
+  k.ya = ya;
+  k.yb = yb;
+  k.bias = (uint32_t)((p - 1) / 2 + (uint64_t)p * (2ull * p + 1));
+  k.invp = lazy_invp(p);
+  k.ya_w = make_shoup(ya, p);
+  k.nya_w = make_shoup((p - ya % p) % p, p);
+  return k;
+}
+
+// S1 = (A21 - A11) Y and S2 = A22 - A21 Y as offset residues (v + h) mod p,
+// h = (p - 1) / 2, for canonical inputs x < p: YK = 0, Y = ya I (the two lanes a / b
+// independent); YK = 1, Y = Rot2(ya, yb) on the column pair (j, j + k/4): [X1 X2] Y =
+// [a X1 - b X2, b X1 + a X2].  Three reductions, by prime range:
+//   WIDE = false (p <= 16763, 2 p^2 + p < 2^30): v exact in int32, (v + bias) mod p by mod_u32
+//     (bias = h + p (2p + 1) keeps v + bias in [0, 2^31));
+//   WIDE, YK = 0: one Shoup step per output (acc_mulred: (part + x w) mod p for any int32 x);
+//   WIDE, YK = 1: v exact mod 2^32 plus the float quotient estimate (lazy_off).
+// Host-checked over extreme and random inputs (tests/test_host_modp.py).
+template <bool WIDE, int YK>
+__host__ __device__ __forceinline__ void k1_s1_s2(uint32_t x11a, uint32_t x11b, uint32_t x21a, uint32_t x21b,
+                                                  uint32_t x22a, uint32_t x22b, const K1Const &kc, uint32_t &s1a,
+                                                  uint32_t &s1b, uint32_t &s2a, uint32_t &s2b) {
+  const uint32_t p = kc.mod.p, h = kc.mod.half, ya = kc.ya, yb = kc.yb;
   const int32_t d1 = (int32_t)x21a - (int32_t)x11a, d2 = (int32_t)x21b - (int32_t)x11b;
   const uint32_t ud1 = (uint32_t)d1, ud2 = (uint32_t)d2;
-  const float yaf = (float)ya, ybf = (float)yb, d1f = (float)d1, d2f = (float)d2;
-  const float x21af = (float)x21a, x21bf = (float)x21b, x22af = (float)x22a, x22bf = (float)x22b;
-  if (YK == 0) {
-    s1a = lazy_off(ya * ud1, yaf * d1f, invp, p, h);
-    s1b = lazy_off(ya * ud2, yaf * d2f, invp, p, h);
-    s2a = lazy_off(x22a - ya * x21a, fmaf(-yaf, x21af, x22af), invp, p, h);
-    s2b = lazy_off(x22b - ya * x21b, fmaf(-yaf, x21bf, x22bf), invp, p, h);
+  if (!WIDE) {
+    if (YK == 0) {
+      s1a = mod_u32(ya * ud1 + kc.bias, kc.mod);
+      s1b = mod_u32(ya * ud2 + kc.bias, kc.mod);
+      s2a = mod_u32(x22a - ya * x21a + kc.bias, kc.mod);
+      s2b = mod_u32(x22b - ya * x21b + kc.bias, kc.mod);
+    } else {
+      s1a = mod_u32(ya * ud1 - yb * ud2 + kc.bias, kc.mod);
+      s1b = mod_u32(yb * ud1 + ya * ud2 + kc.bias, kc.mod);
+      s2a = mod_u32(x22a - (ya * x21a - yb * x21b) + kc.bias, kc.mod);
+      s2b = mod_u32(x22b - (yb * x21a + ya * x21b) + kc.bias, kc.mod);
+    }
+  } else if (YK == 0) {
+    const uint32_t u22a = umin32(x22a + h, x22a + h - p), u22b = umin32(x22b + h, x22b + h - p);
+    s1a = acc_mulred(d1, kc.ya_w.wc, kc.ya_w.wq, h, p);
+    s1b = acc_mulred(d2, kc.ya_w.wc, kc.ya_w.wq, h, p);
+    s2a = acc_mulred((int32_t)x21a, kc.nya_w.wc, kc.nya_w.wq, u22a, p);
+    s2b = acc_mulred((int32_t)x21b, kc.nya_w.wc, kc.nya_w.wq, u22b, p);
   } else {
+    const float invp = kc.invp;
+    const float yaf = (float)ya, ybf = (float)yb, d1f = (float)d1, d2f = (float)d2;
+    const float x21af = (float)x21a, x21bf = (float)x21b, x22af = (float)x22a, x22bf = (float)x22b;
     s1a = lazy_off(ya * ud1 - yb * ud2, fmaf(yaf, d1f, -(ybf * d2f)), invp, p, h);
     s1b = lazy_off(yb * ud1 + ya * ud2, fmaf(ybf, d1f, yaf * d2f), invp, p, h);
     const float trfa = fmaf(yaf, x21af, -(ybf * x21bf)), trfb = fmaf(ybf, x21af, yaf * x21bf);

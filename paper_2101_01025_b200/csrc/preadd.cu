@@ -456,48 +456,20 @@ __device__ __forceinline__ void preadd_row(const PreParams &P, const PreNode &N,
     load4(vv, P.mh + r, P.kh + c + h2, m, x22b);
   }
   {
-    // Lazy reduction: Y products unreduced, one reduction per S output.  Residues are carried as
-    // offset values u = c + h in [0, p) of the centered c (h = (p - 1) / 2), so every correction
-    // is an unsigned min of u, u - p, u + p.  SCHEMES 0 / 1 (p <= 16763, 2 p^2 < 2^31): exact
-    // int32 products.  SCHEMES 2 / 3 (p < 2^18): modp.cuh lazy_s1_s2 (exact mod 2^32 plus a float
-    // quotient estimate; host-checked in tests/test_host_modp.py).
-    const int32_t p = (int32_t)m.p, h = (int32_t)m.half;
+    // One reduction per S output (modp.cuh k1_s1_s2).  Residues are carried as offset values
+    // u = c + h in [0, p) of the centered c (h = (p - 1) / 2), so every correction is an unsigned
+    // min of u, u - p, u + p.
+    const int32_t h = (int32_t)m.half;
     const uint32_t up = m.p;
-    const float invp = lazy_invp(m.p);
-    const int32_t ya = (int32_t)P.ya, yb = (int32_t)P.yb;
-    // v + h - q p with the float quotient estimate q of v / p (v exact mod 2^32, vf its float
-    // value): in [-0.63 p, 1.63 p)
-    auto off_lazy2 = [&](int32_t v, float vf) -> uint32_t {
-      const int32_t q = __float2int_rn(vf * invp);
-      const uint32_t u = (uint32_t)v + (uint32_t)h - (uint32_t)q * up;
-      return umin32(umin32(u, u - up), u + up);
-    };
-    auto off_lazy = [&](int32_t v) -> uint32_t { return off_lazy2(v, __int2float_rn(v)); };
-    const float yaf = (float)ya, ybf = (float)yb;
     auto wrap_lo = [&](uint32_t u) { return umin32(u, u + up); };   // u in (-p, p)
     auto wrap_hi = [&](uint32_t u) { return umin32(u, u - up); };   // u in [0, 2p)
     uint32_t u1a[4], u1b[4], u2a[4], u2b[4], u3a[4], u3b[4], u4a[4], u4b[4];
     uint32_t u11a[4], u11b[4], u12a[4], u12b[4], u22a[4], u22b[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const int32_t d1 = (int32_t)x21a[e] - (int32_t)x11a[e], d2 = (int32_t)x21b[e] - (int32_t)x11b[e];
-      // unsigned (wrapping) arithmetic: SCHEME 1 values fit int32, SCHEME 3 uses them mod 2^32
-      const uint32_t uya = (uint32_t)ya, uyb = (uint32_t)yb, ud1 = (uint32_t)d1, ud2 = (uint32_t)d2;
-      int32_t s1r_a, s1r_b, tr_a, tr_b;
-      if constexpr (YK == 0) {
-        s1r_a = (int32_t)(uya * ud1); s1r_b = (int32_t)(uya * ud2);
-        tr_a = (int32_t)(uya * x21a[e]); tr_b = (int32_t)(uya * x21b[e]);
-      } else {
-        s1r_a = (int32_t)(uya * ud1 - uyb * ud2); s1r_b = (int32_t)(uyb * ud1 + uya * ud2);   // (A21 - A11) Y
-        tr_a = (int32_t)(uya * x21a[e] - uyb * x21b[e]);                                     // A21 Y
-        tr_b = (int32_t)(uyb * x21a[e] + uya * x21b[e]);
-      }
-      if constexpr (SCHEME <= 1) {
-        u1a[e] = off_lazy(s1r_a); u1b[e] = off_lazy(s1r_b);                                         // S1
-        u2a[e] = off_lazy((int32_t)x22a[e] - tr_a); u2b[e] = off_lazy((int32_t)x22b[e] - tr_b);     // S2
-      } else {   // S1, S2 by the host-checked helper (modp.cuh: lazy_s1_s2)
-        lazy_s1_s2<YK>(x11a[e], x11b[e], x21a[e], x21b[e], x22a[e], x22b[e], (uint32_t)ya, (uint32_t)yb, invp, up, (uint32_t)h, u1a[e], u1b[e], u2a[e], u2b[e]);
-      }
+      // S1, S2 by the host-checked helper (modp.cuh: k1_s1_s2)
+      k1_s1_s2<(SCHEME >= 2), YK>(x11a[e], x11b[e], x21a[e], x21b[e], x22a[e], x22b[e], P.kc, u1a[e], u1b[e], u2a[e],
+                                  u2b[e]);
       u3a[e] = wrap_lo(u1a[e] - x22a[e]); u3b[e] = wrap_lo(u1b[e] - x22b[e]);                       // S3
       u4a[e] = wrap_hi(u3a[e] + x12a[e]); u4b[e] = wrap_hi(u3b[e] + x12b[e]);                       // S4
       u11a[e] = wrap_hi(x11a[e] + h); u11b[e] = wrap_hi(x11b[e] + h);
@@ -552,7 +524,10 @@ __device__ __forceinline__ void preadd_row(const PreParams &P, const PreNode &N,
   }
 }
 
-template <int SCHEME, int YK>
+// TSEL: 0 = any input type (runtime switch per node), 1 = every node reads uint16 (caller
+// ADJ_IN_U16 or workspace residues), 2 = every node reads uint32 -- the specialised instances
+// carry only their own load path (less register pressure in the hot loop)
+template <int SCHEME, int YK, int TSEL>
 __global__ void __launch_bounds__(256, 4) preadd_kernel(const __grid_constant__ PreParams P) {
   constexpr int NP = SCHEME == 0 ? 1 : (SCHEME == 1 ? 3 : (SCHEME == 2 ? 2 : 6));
   const PreNode &N = P.nodes[blockIdx.z];
@@ -575,11 +550,17 @@ __global__ void __launch_bounds__(256, 4) preadd_kernel(const __grid_constant__ 
       continue;
     }
     const int64_t c = g * 4;
-    if (type == IN_U32) preadd_row<SCHEME, YK, IN_U32>(P, N, r, c);
-    else if (type == IN_U16) preadd_row<SCHEME, YK, IN_U16>(P, N, r, c);
-    else if (type == IN_U16R) preadd_row<SCHEME, YK, IN_U16R>(P, N, r, c);
-    else if (type == IN_QUAD_SUM) preadd_row<SCHEME, YK, IN_QUAD_SUM>(P, N, r, c);
-    else preadd_row<SCHEME, YK, IN_PAIR_SUM>(P, N, r, c);
+    if constexpr (TSEL == 1) {
+      preadd_row<SCHEME, YK, IN_U16R>(P, N, r, c);   // canonical workspace residues pass its check
+    } else if constexpr (TSEL == 2) {
+      preadd_row<SCHEME, YK, IN_U32>(P, N, r, c);
+    } else {
+      if (type == IN_U32) preadd_row<SCHEME, YK, IN_U32>(P, N, r, c);
+      else if (type == IN_U16) preadd_row<SCHEME, YK, IN_U16>(P, N, r, c);
+      else if (type == IN_U16R) preadd_row<SCHEME, YK, IN_U16R>(P, N, r, c);
+      else if (type == IN_QUAD_SUM) preadd_row<SCHEME, YK, IN_QUAD_SUM>(P, N, r, c);
+      else preadd_row<SCHEME, YK, IN_PAIR_SUM>(P, N, r, c);
+    }
   }
 }
 
@@ -589,7 +570,20 @@ cudaError_t launch_preadd(const PreParams &p, cudaStream_t s) {
   dim3 block(256);
   const int64_t nrows = range_rows(p.rows, p.rows_pad);
   dim3 grid((unsigned)((groups + 255) / 256), (unsigned)(nrows < 65535 ? nrows : 65535), (unsigned)p.n_nodes);
-#define PRE(S, Y) preadd_kernel<S, Y><<<grid, block, 0, s>>>(p)
+  // the specialised instance when every node of the launch reads the same storage
+  bool all16 = true, all32 = true;
+  for (int n = 0; n < p.n_nodes; ++n) {
+    const InView &v = p.nodes[n].in;
+    all16 = all16 && (v.type == IN_U16 || v.type == IN_U16R) && p.nodes[n].side == nullptr;
+    all32 = all32 && v.type == IN_U32 && p.nodes[n].side == nullptr;
+  }
+  const int tsel = all16 ? 1 : (all32 ? 2 : 0);
+#define PRE(S, Y)                                                   \
+  do {                                                              \
+    if (tsel == 1) preadd_kernel<S, Y, 1><<<grid, block, 0, s>>>(p); \
+    else if (tsel == 2) preadd_kernel<S, Y, 2><<<grid, block, 0, s>>>(p); \
+    else preadd_kernel<S, Y, 0><<<grid, block, 0, s>>>(p);          \
+  } while (0)
   if (p.scheme == 0) { if (p.ykind == 0) PRE(0, 0); else PRE(0, 1); }
   else if (p.scheme == 1) { if (p.ykind == 0) PRE(1, 0); else PRE(1, 1); }
   else if (p.scheme == 2) { if (p.ykind == 0) PRE(2, 0); else PRE(2, 1); }

@@ -116,6 +116,7 @@ struct PreParams {
   int32_t res32;           // workspace residues are uint32 (p > 2^16)
   int32_t pad_;
   ModP mod;
+  K1Const kc;              // S1 / S2 reduction constants (modp.cuh k1_s1_s2)
 };
 
 // plain limb split of a view into arena planes (depth 0, gemm_modp, 2M's X / Y)

@@ -101,10 +101,17 @@ int main() {
   uint32_t r[11];
   std::vector<uint32_t> out;
   while (fread(r, 4, 11, stdin) == 11) {
-    const uint32_t p = r[0], h = (p - 1) / 2;
+    const uint32_t p = r[0];
     uint32_t s[4];
-    if (r[1] == 0) lazy_s1_s2<0>(r[2], r[3], r[4], r[5], r[6], r[7], r[8], r[9], lazy_invp(p), p, h, s[0], s[1], s[2], s[3]);
-    else lazy_s1_s2<1>(r[2], r[3], r[4], r[5], r[6], r[7], r[8], r[9], lazy_invp(p), p, h, s[0], s[1], s[2], s[3]);
+    const K1Const kc = make_k1const(p, r[8], r[9]);
+    const bool wide = p > 16763;
+    if (r[1] == 0) {
+      if (wide) k1_s1_s2<true, 0>(r[2], r[3], r[4], r[5], r[6], r[7], kc, s[0], s[1], s[2], s[3]);
+      else k1_s1_s2<false, 0>(r[2], r[3], r[4], r[5], r[6], r[7], kc, s[0], s[1], s[2], s[3]);
+    } else {
+      if (wide) k1_s1_s2<true, 1>(r[2], r[3], r[4], r[5], r[6], r[7], kc, s[0], s[1], s[2], s[3]);
+      else k1_s1_s2<false, 1>(r[2], r[3], r[4], r[5], r[6], r[7], kc, s[0], s[1], s[2], s[3]);
+    }
     out.insert(out.end(), s, s + 4);
   }
   fwrite(out.data(), 4, out.size(), stdout);
@@ -112,17 +119,17 @@ int main() {
 }
 """
 
-LAZY_PRIMES = [16787, 32749, 65519, 65521, 65537, 131041, 131071, 199999, 262139]
+LAZY_PRIMES = [3, 5, 97, 251, 257, 8191, 16763, 16787, 32749, 65519, 65521, 65537, 131041, 131071, 199999, 262139]
 
 
-def test_k1_lazy_float_quotient_reduction(tmp_path):
-    """K1's lazy reduction of the Y products for p > 16763 (modp.cuh lazy_s1_s2, used by
-    preadd.cu): S1 = (A21 - A11) Y and S2 = A22 - A21 Y for Y = i I and
-    Y = Rot2(a, b), as offset residues (v + (p-1)/2) mod p, against exact integers.
-    Every combination of extreme residues {0, 1, h, h+1, p-2, p-1} of the six inputs, with extreme
-    and actual skew-unitary Y coefficients, plus random inputs, at primes across both schemes
-    above 16763 (s8/u8 up to 65521, 6-plane up to 262139).  The float quotient estimate must stay
-    within the window the two unsigned mins correct."""
+def test_k1_s1_s2_reductions(tmp_path):
+    """K1's reduction of the Y products (modp.cuh k1_s1_s2, used by preadd.cu): S1 = (A21 - A11) Y
+    and S2 = A22 - A21 Y for Y = i I and Y = Rot2(a, b), as
+    offset residues (v + (p-1)/2) mod p, against exact integers -- the exact int32 + Barrett
+    path (p <= 16763), the Shoup path (p > 16763, Y = i I) and the float quotient estimate
+    (p > 16763, Rot2).  Every combination of extreme residues {0, 1, h, h+1, p-2, p-1} of the six
+    inputs, with extreme and actual skew-unitary Y coefficients, plus random inputs, at primes
+    of every limb scheme (1 plane, K7, s8/u8, 6-plane)."""
     import itertools
     import numpy as np
     src, exe = tmp_path / "t3.cpp", tmp_path / "t3"
@@ -138,8 +145,10 @@ def test_k1_lazy_float_quotient_reduction(tmp_path):
         X = ext[xs]                                                     # (46656, 6)
         if p % 4 == 1:
             yset = [(of.mod_sqrt(p - 1, p), 0)]
-        else:
+        elif p > 3:
             yset = [tuple(of.sos(p - 1, p))]
+        else:
+            yset = [(1, 1)]
         yset += [(p - 1, p - 1), (p - 1, 1), (h, h + 1), (1, p - 1)]
         for yk in (0, 1):
             for ya, yb in yset:
