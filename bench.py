@@ -602,29 +602,36 @@ def run_gpu(args, cfg, rank, world, local_rank):
     comparators = None
     if world == 1 and not args.no_compare:
         comparators = {}
-        if depth != 0 and not alg1:
-            ws0 = adj.adjprod_modp_workspace_size(m, k, p, phi, 0, flags)
-            w0 = torch.empty(max(ws0, 1), dtype=torch.uint8, device=dev)
-            C0 = torch.zeros_like(C)
+
+        def other_depth(d):
+            """the same step at depth d (median of flushed steps) and whether Low(C) is identical"""
+            wsd = adj.adjprod_modp_workspace_size(m, k, p, phi, d, flags)
+            wd = torch.empty(max(wsd, 1), dtype=torch.uint8, device=dev)
+            Cd = torch.zeros_like(C)
             for _ in range(3):
-                adj.adjprod_modp_ex(m, k, p, phi, A, k, C0, m, depth=0, flags=flags, workspace=w0, workspace_bytes=ws0,
+                adj.adjprod_modp_ex(m, k, p, phi, A, k, Cd, m, depth=d, flags=flags, workspace=wd, workspace_bytes=wsd,
                                     stream=stream)
             ts = []
             for _ in range(max(3, min(args.steps, 10))):
                 flush.zero_()
                 a0, b0 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a0.record(stream)
-                adj.adjprod_modp_ex(m, k, p, phi, A, k, C0, m, depth=0, flags=flags, workspace=w0, workspace_bytes=ws0,
+                adj.adjprod_modp_ex(m, k, p, phi, A, k, Cd, m, depth=d, flags=flags, workspace=wd, workspace_bytes=wsd,
                                     stream=stream)
                 b0.record(stream)
                 torch.cuda.synchronize()
                 ts.append(a0.elapsed_time(b0))
-            ms0 = statistics.median(ts)
-            comparators["depth0_classical"] = {"ms_per_step": ms0, "value": m * m * k / (ms0 * 1e-3), "unit": UNIT,
-                                               "same_result": bool(torch.equal(torch.tril(u32(C0).view(m, -1)),
-                                                                               torch.tril(u32(C).view(m, -1))))
-                                               if w == 1 else None}
-            del w0, C0
+            msd = statistics.median(ts)
+            lo = torch.tril(torch.ones(m, m, dtype=torch.bool, device=dev))
+            same = bool(torch.equal(u32(Cd).view(m, m, w)[lo], u32(C).view(m, m, w)[lo]))
+            return {"depth": d, "ms_per_step": msd, "value": m * m * k / (msd * 1e-3), "unit": UNIT,
+                    "same_result": same, "workspace_bytes": wsd}
+        if depth != 0 and not alg1:
+            # the classical route (no Alg. 1 level): the on-box analogue of the paper's comparator
+            comparators["depth0_classical"] = other_depth(0)
+        elif depth == 0 and not alg1 and cfg["phi"] in ("T", "H"):
+            # one level of Alg. 1 (inside 2M's G for phi = H) where the automatic depth is 0
+            comparators["depth1_alg1"] = other_depth(1)
         if io16:   # the same step with uint32 residues in HBM
             A4, C4 = u32(A), torch.zeros((m, m * w), dtype=torch.int32, device=dev)
             f4 = flags & ~(adj.ADJ_IN_U16 | adj.ADJ_OUT_U16)
