@@ -92,9 +92,23 @@ typedef enum {
  *                    adjprod_modp_shard, adjprod_modp_partial and adjprod_modp_dist.
  *   ADJ_OUT_U16    : p < 2^16 -- Low(C) written as uint16 residues (pairs / quadruples for
  *                    phi = H / Q); the plain form only (no alpha / beta, no ADJ_FILL_UPPER, not
- *                    with ADJ_HERK_ALG1). */
+ *                    with ADJ_HERK_ALG1).
+ *   ADJ_LOW_MEM    : phi = ADJ_PHI_T, depth >= 1, m a multiple of 64, plain form (alpha = 1,
+ *                    beta = 0) -- the low-memory temporary schedule (the GPU counterpart of the
+ *                    in-place schedules of Table tab:schedule:AAT): the root
+ *                    level's products P1, P3, P5 are formed in C's own blocks C11, C21, C22 and
+ *                    only P2, P4 and S3 live in the workspace; the root's operand arena is
+ *                    reused by its three children (ordinary calls one level shallower), and the
+ *                    root recombination runs in place.  Same Low(C); Up(C) untouched.  Requires
+ *                    C 16-byte aligned and ldc a multiple of 8 (INVALID_VALUE otherwise).
+ *                    Ignored where it does not apply (other phi, depth 0, m % 64 != 0, SYRK
+ *                    form); adjprod_modp_workspace_size honours it the same way.  Without the
+ *                    flag a call falls back to this schedule by itself where it applies and C is
+ *                    so aligned, when the caller's workspace is smaller than the grouped
+ *                    schedule's size but not than this one's, or when the library's workspace
+ *                    allocation fails. */
 enum { ADJ_FILL_UPPER = 1u, ADJ_HERK_ALG1 = 2u, ADJ_DIST_TILES = 4u, ADJ_DIST_P2P = 8u, ADJ_IN_U16 = 16u,
-       ADJ_OUT_U16 = 32u };
+       ADJ_OUT_U16 = 32u, ADJ_LOW_MEM = 64u };
 
 typedef struct {
   int depth;              /* recursion levels of Alg. alg:MIAHMM; -1 = automatic; 0 = classical */

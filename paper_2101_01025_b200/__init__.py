@@ -7,19 +7,19 @@ without an sm_100 GPU every call raises.
 """
 from __future__ import annotations
 
-from ._lib import (ADJ_IN_U16, ADJ_OUT_U16, ADJ_DIST_P2P, ADJ_DIST_TILES, ADJ_FILL_UPPER, ADJ_HERK_ALG1, ADJ_PHI_H, ADJ_PHI_Q, ADJ_PHI_T, AdjError, adj_comm_destroy, adj_comm_get_unique_id,
+from ._lib import (ADJ_IN_U16, ADJ_OUT_U16, ADJ_LOW_MEM, ADJ_DIST_P2P, ADJ_DIST_TILES, ADJ_FILL_UPPER, ADJ_HERK_ALG1, ADJ_PHI_H, ADJ_PHI_Q, ADJ_PHI_T, AdjError, adj_comm_destroy, adj_comm_get_unique_id,
                    adj_comm_init, adj_launch_count, adj_launch_count_reset, adj_mod_lower, adj_profile_enable, adj_profile_read, adj_skew_unitary, adj_sos,
                    adj_dist_kslice, adj_elem_bytes, adj_shard_layout, adj_shard_rows, adjprod_modp_dist_partial, adj_shard_pack, adj_sum_partials, adjprod_modp, adjprod_modp_partial, adjprod_modp_shard, adjprod_modp_auto_depth, adjprod_modp_dist, adjprod_modp_ex, adjprod_modp_syrk,
                    adjprod_modp_workspace_size, gemm_modp, lib)
 
-__all__ = ["ADJ_IN_U16", "ADJ_OUT_U16", "adj_shard_pack", "ADJ_DIST_P2P", "adjprod_modp_partial", "adj_sum_partials", "ADJ_DIST_TILES", "adjprod_modp_shard", "adj_shard_layout", "ADJ_PHI_T", "ADJ_PHI_H", "ADJ_PHI_Q", "ADJ_FILL_UPPER", "ADJ_HERK_ALG1", "AdjError", "adjprod_modp", "adjprod_modp_ex", "adjprod_modp_syrk",
+__all__ = ["ADJ_IN_U16", "ADJ_OUT_U16", "ADJ_LOW_MEM", "adj_shard_pack", "ADJ_DIST_P2P", "adjprod_modp_partial", "adj_sum_partials", "ADJ_DIST_TILES", "adjprod_modp_shard", "adj_shard_layout", "ADJ_PHI_T", "ADJ_PHI_H", "ADJ_PHI_Q", "ADJ_FILL_UPPER", "ADJ_HERK_ALG1", "AdjError", "adjprod_modp", "adjprod_modp_ex", "adjprod_modp_syrk",
            "adjprod_modp_workspace_size", "adjprod_modp_auto_depth", "gemm_modp", "adj_skew_unitary", "adj_sos",
            "adj_mod_lower", "adj_dist_kslice", "adj_elem_bytes", "adj_shard_rows", "adjprod_modp_dist_partial", "adj_comm_get_unique_id", "adj_comm_init", "adj_comm_destroy", "adjprod_modp_dist",
            "adj_launch_count", "adj_launch_count_reset", "adj_profile_enable", "adj_profile_read", "lib", "adjprod", "gemm"]
 
 
 def adjprod(A, p: int, phi: str = "T", depth: int = -1, fill_upper: bool = False, out=None, workspace=None,
-            stream=None, herk: str = "2m", out16: bool = False):
+            stream=None, herk: str = "2m", out16: bool = False, low_mem: bool = False):
     """Low(A phi(A)) mod p for a CUDA int32/uint32 tensor A (m x k; m x k x 2 for phi='H', GF(p^2);
     m x k x 4 for phi='Q', quaternions over GF(p)).
 
@@ -27,7 +27,8 @@ def adjprod(A, p: int, phi: str = "T", depth: int = -1, fill_upper: bool = False
     whatever `out` held (zeros for a fresh output) unless fill_upper.  For phi='H', herk='alg1'
     selects one level of Alg. alg:MIAHMM directly over GF(p^2) (ADJ_HERK_ALG1) instead of 2M.
     Compact residues (phi='T', p < 2^16): a 2-byte A (int16/uint16 tensor) is read as uint16
-    (ADJ_IN_U16); out16 (or a 2-byte `out`) writes Low(C) as uint16 (ADJ_OUT_U16)."""
+    (ADJ_IN_U16); out16 (or a 2-byte `out`) writes Low(C) as uint16 (ADJ_OUT_U16).  low_mem
+    selects the low-memory temporary schedule where it applies (ADJ_LOW_MEM)."""
     import torch
     assert A.is_cuda and A.element_size() in (2, 4)
     ph = {"T": ADJ_PHI_T, "H": ADJ_PHI_H, "Q": ADJ_PHI_Q}[phi.upper()]
@@ -41,7 +42,8 @@ def adjprod(A, p: int, phi: str = "T", depth: int = -1, fill_upper: bool = False
     ldc = out.stride(0) // w
     nbytes = workspace.numel() * workspace.element_size() if workspace is not None else 0
     flags = ((ADJ_FILL_UPPER if fill_upper else 0) | (ADJ_HERK_ALG1 if herk == "alg1" else 0)
-             | (ADJ_IN_U16 if A.element_size() == 2 else 0) | (ADJ_OUT_U16 if out16 else 0))
+             | (ADJ_IN_U16 if A.element_size() == 2 else 0) | (ADJ_OUT_U16 if out16 else 0)
+             | (ADJ_LOW_MEM if low_mem else 0))
     adjprod_modp_ex(m, k, p, ph, A, lda, out, ldc, depth=depth, flags=flags,
                     workspace=workspace, workspace_bytes=nbytes, stream=stream)
     return out

@@ -20,6 +20,7 @@ ADJ_DIST_TILES = 4
 ADJ_DIST_P2P = 8
 ADJ_IN_U16 = 16
 ADJ_OUT_U16 = 32
+ADJ_LOW_MEM = 64
 STATUS = {0: "ADJ_OK", 1: "ADJ_ERR_INVALID_VALUE", 2: "ADJ_ERR_UNSUPPORTED_MODULUS", 3: "ADJ_ERR_WORKSPACE",
           4: "ADJ_ERR_CUDA", 5: "ADJ_ERR_NCCL", 6: "ADJ_ERR_ARCH"}
 

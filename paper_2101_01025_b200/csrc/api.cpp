@@ -234,9 +234,10 @@ adj_status_t get_plan(Plan **out, int kind, int64_t m, int64_t n, int64_t k, uin
   evict_plans();
   auto P = std::make_unique<Plan>();
   const char *err = nullptr;
-  bool ok = kind == PLAN_GEMM    ? build_gemm_plan(*P, m, n, k, p, sms, &err)
-            : kind == PLAN_HERK1 ? build_herk1_plan(*P, m, k, p, sms, &err)
-                                 : build_syrk_plan(*P, m, k, p, phi, depth, sms, &err, shard_rank, shard_n);
+  bool ok = kind == PLAN_GEMM     ? build_gemm_plan(*P, m, n, k, p, sms, &err)
+            : kind == PLAN_HERK1  ? build_herk1_plan(*P, m, k, p, sms, &err)
+            : kind == PLAN_LOWMEM ? build_lowmem_plan(*P, m, k, p, depth, sms, &err)
+                                  : build_syrk_plan(*P, m, k, p, phi, depth, sms, &err, shard_rank, shard_n);
   if (!ok) return fail(ADJ_ERR_INVALID_VALUE, "plan: %s", err ? err : "unsupported");
   P->dev = dev;
   auto upload = [&](void **dst, const void *src, size_t bytes) -> cudaError_t {
@@ -351,6 +352,15 @@ adj_status_t launch_leaf_all(const Plan &P, const Ptrs &x, cudaStream_t s) {
       case OUT_HBUF: L.prod[q].out = x.ws + P.h_offset; break;
       case OUT_GBUF: L.prod[q].out = x.ws + P.g_offset; break;
       case OUT_QBUF: L.prod[q].out = x.ws + P.q_offset + (size_t)pp.idx * P.q_bytes; break;
+      case OUT_LMP4: L.prod[q].out = x.ws + P.lm_p4_off; break;
+      case OUT_C21: {   // low-memory root: P3 into C's C21 block, in C's element type
+        const size_t eb = (x.res16 && !P.res32) ? 2 : 4;
+        L.prod[q].out = reinterpret_cast<uint8_t *>(x.C) + (size_t)P.lv[1].mh * (size_t)x.ldc * eb;
+        L.prod[q].ldo = x.ldc;
+        L.prod[q].out_u32 = eb == 4 ? 1 : 0;
+        L.prod[q].vec_ok = ((uintptr_t)L.prod[q].out % 16 == 0) && (x.ldc % (eb == 2 ? 8 : 4) == 0);
+        break;
+      }
       case OUT_C:
         L.prod[q].out = x.C;
         L.prod[q].ldo = x.ldc;
@@ -447,7 +457,7 @@ adj_status_t run_tree(const Plan &P, const InView &root, const Ptrs &x, cudaStre
       N.in = views[l][n];
       for (int o = 0; o < OUT_N; ++o)
         N.op_row[o] = o < L.n_ops ? ((int64_t)n * L.n_ops + o) * P.planes * L.rows_pad : -1;
-      if (l < P.depth) {
+      if (l < P.depth || P.kind == PLAN_LOWMEM) {
         N.s3 = s3buf(P, x.ws, l, n);
         N.s3_ld = L.kh;
       }
@@ -462,6 +472,13 @@ adj_status_t run_tree(const Plan &P, const InView &root, const Ptrs &x, cudaStre
     LAUNCH_CLS(CLS_PRE, launch_preadd(pp, s));
   }
   return ADJ_OK;
+}
+
+// K1 of every level, then the grouped leaf launch
+adj_status_t run_tree_leaf(const Plan &P, const InView &root, const Ptrs &x, cudaStream_t s,
+                           uint8_t *side_arena = nullptr) {
+  adj_status_t st = run_tree(P, root, x, s, side_arena);
+  return st != ADJ_OK ? st : launch_leaf_all(P, x, s);
 }
 
 adj_status_t run_combine(const Plan &P, const Ptrs &x, void *final_out, int64_t final_ld, bool final_u32,
@@ -505,24 +522,78 @@ adj_status_t run_combine(const Plan &P, const Ptrs &x, void *final_out, int64_t 
   return ADJ_OK;
 }
 
-adj_status_t run_syrk(const Plan &P, const Ptrs &x, adj_phi_t phi, uint32_t flags, cudaStream_t s) {
+// phi = T through the grouped schedule: Low(x.C) = Low(V V^T) for the view `root` (m x k valid)
+adj_status_t run_syrk_t(const Plan &P, const InView &root, const Ptrs &x, cudaStream_t s) {
+  adj_status_t st;
+  if (P.depth == 0) {
+    st = run_split(P, root, P.m, P.k, P.rows_pad0, P.op0_row[0], x.ws + P.arenas[0].offset, s);
+    if (st) return st;
+    return launch_leaf_all(P, x, s);
+  }
+  st = run_tree_leaf(P, root, x, s);
+  if (st) return st;
+  return run_combine(P, x, x.C, x.ldc, !x.res16, s);
+}
+
+// Low-memory schedule (ADJ_LOW_MEM; plan.hpp PLAN_LOWMEM).  R is the root plan.
+adj_status_t run_lowmem(const Plan &R, const InView &root, const Ptrs &x, int dev, int sms, cudaStream_t s) {
+  adj_status_t st;
+  const LevelPlan &L = R.lv[1];
+  // K1 of the root: S1, S2, S4, A22 limb planes and S3
+  if ((st = run_tree(R, root, x, s)) != ADJ_OK) return st;
+  // P3 -> C21, P4 -> buffer (one grouped launch)
+  if ((st = launch_leaf_all(R, x, s)) != ADJ_OK) return st;
+  // the three recursive products, each an ordinary call one level shallower
+  // whose workspace reuses the root's arena region: P1 = X11 X11^T -> C11, P2 = X12 X12^T ->
+  // buffer, P5 = S3 S3^T -> C22 (Low parts only)
+  Plan *Q = nullptr;
+  if ((st = get_plan(&Q, PLAN_SYRK_T, L.mh, L.mh, L.kh, R.p, 0, R.lm_depth - 1, dev, sms)) != ADJ_OK) return st;
+  if (Q->ws_bytes > R.lm_child_ws) return fail(ADJ_ERR_WORKSPACE, "low-memory child workspace");
+  const size_t eb = (x.res16 && !R.res32) ? 2 : 4;
+  for (int c = 0; c < 3; ++c) {
+    const InView v = child_view(root, c, L, c == 2 ? x.ws + L.s3_offset : nullptr, L.kh, R.res32);
+    Ptrs xc;
+    xc.ws = x.ws + R.lm_region_off;
+    if (c == 1) {
+      xc.C = reinterpret_cast<uint32_t *>(x.ws + R.lm_p2_off);
+      xc.ldc = L.rows_pad;
+      xc.res16 = !R.res32;
+    } else {
+      const size_t off = c == 0 ? 0 : ((size_t)L.mh * (size_t)x.ldc + (size_t)L.mh) * eb;
+      xc.C = reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(x.C) + off);
+      xc.ldc = x.ldc;
+      xc.res16 = x.res16;
+    }
+    if ((st = run_syrk_t(*Q, v, xc, s)) != ADJ_OK) return st;
+  }
+  // root K4 in place (U1..U5)
+  CombParams cp;
+  std::memset(&cp, 0, sizeof(cp));
+  cp.n_nodes = 1;
+  cp.mh = L.mh;
+  cp.ldp = L.rows_pad;
+  cp.mod = R.mod;
+  cp.in32 = R.res32 ? 1 : 0;
+  cp.out_u32 = eb == 4 ? 1 : 0;
+  cp.inplace = 1;
+  CombNode &N = cp.nodes[0];
+  N.P[1] = x.ws + R.lm_p2_off;
+  N.P[3] = x.ws + R.lm_p4_off;
+  N.out = x.C;
+  N.ldo = x.ldc;
+  N.out_valid = R.m;
+  LAUNCH_CLS(CLS_COMB, launch_combine(cp, s));
+  return ADJ_OK;
+}
+
+adj_status_t run_syrk(const Plan &P, const Ptrs &x, adj_phi_t phi, uint32_t flags, cudaStream_t s, int dev = 0,
+                      int sms = 0) {
   adj_status_t st;
   const int64_t m = P.m, k = P.k;
   if (phi == ADJ_PHI_T) {
     InView root = make_view(x.A, x.lda, m, k, x.in16 ? IN_U16R : IN_U32);
-    if (P.depth == 0) {
-      st = run_split(P, root, m, k, P.rows_pad0, P.op0_row[0], x.ws + P.arenas[0].offset, s);
-      if (st) return st;
-      st = launch_leaf_all(P, x, s);
-      if (st) return st;
-    } else {
-      st = run_tree(P, root, x, s);
-      if (st) return st;
-      st = launch_leaf_all(P, x, s);
-      if (st) return st;
-      st = run_combine(P, x, x.C, x.ldc, !x.res16, s);
-      if (st) return st;
-    }
+    st = P.kind == PLAN_LOWMEM ? run_lowmem(P, root, x, dev, sms, s) : run_syrk_t(P, root, x, s);
+    if (st) return st;
   } else {
     // 2M (Alg. alg:2M): A = X + iY; H = X phi(Y) = X Y^T; G = (X+Y) phi(X + eps Y), eps = 1.
     // X / Y limb planes come from the same pass over A as T (split mode 1 at depth 0, the
@@ -552,9 +623,7 @@ adj_status_t run_syrk(const Plan &P, const Ptrs &x, adj_phi_t phi, uint32_t flag
           if (2 * mh < rp0) CUDA_TRY(cudaMemsetAsync(base + (size_t)(2 * mh) * kp0, 0, (size_t)(rp0 - 2 * mh) * kp0, s));
           if (2 * kh < kp0) CUDA_TRY(cudaMemset2DAsync(base + 2 * kh, kp0, 0, kp0 - 2 * kh, 2 * mh, s));
         }
-      st = run_tree(P, troot, x, s, arena0);
-      if (st) return st;
-      st = launch_leaf_all(P, x, s);
+      st = run_tree_leaf(P, troot, x, s, arena0);
       if (st) return st;
       st = run_combine(P, x, G, P.rows_pad0, false, s);
       if (st) return st;
@@ -583,11 +652,8 @@ adj_status_t run_quat(const Plan &P, const Ptrs &x, uint32_t flags, cudaStream_t
   LAUNCH_CLS(CLS_PRE, launch_split(sp, s));
   adj_status_t st;
   void *G = x.ws + P.g_offset;
-  if (P.depth >= 1) {
-    st = run_tree(P, make_view(x.A, x.lda, m, k, IN_QUAD_SUM, x.in16), x, s);
-    if (st) return st;
-  }
-  st = launch_leaf_all(P, x, s);
+  st = P.depth >= 1 ? run_tree_leaf(P, make_view(x.A, x.lda, m, k, IN_QUAD_SUM, x.in16), x, s)
+                    : launch_leaf_all(P, x, s);
   if (st) return st;
   if (P.depth >= 1) {
     st = run_combine(P, x, G, P.rows_pad0, false, s);
@@ -737,7 +803,10 @@ adj_status_t adjprod_modp_workspace_size(int64_t m, int64_t k, uint32_t p, adj_p
   Plan P;
   const char *err = nullptr;
   const int sms = query_sms();
-  if (!(herk1 ? build_herk1_plan(P, m, k, p, sms, &err) : build_syrk_plan(P, m, k, p, (int)phi, depth, sms, &err)))
+  const bool lowmem = opts && (opts->flags & ADJ_LOW_MEM) && phi == ADJ_PHI_T && lowmem_shape_ok(m, k, depth);
+  if (!(herk1    ? build_herk1_plan(P, m, k, p, sms, &err)
+        : lowmem ? build_lowmem_plan(P, m, k, p, depth, sms, &err)
+                 : build_syrk_plan(P, m, k, p, (int)phi, depth, sms, &err)))
     return fail(ADJ_ERR_INVALID_VALUE, "plan: %s", err ? err : "unsupported");
   *bytes = P.ws_bytes;
   return ADJ_OK;
@@ -778,9 +847,21 @@ static adj_status_t adjprod_impl(int64_t m, int64_t k, uint32_t p, adj_phi_t phi
   int depth = (opts && opts->depth >= 0) ? opts->depth : (herk1 ? 1 : auto_depth(m, k, p, (int)phi));
   if (depth > 3) return fail(ADJ_ERR_INVALID_VALUE, "depth %d > 3 unsupported", depth);
   if (herk1 && depth != 1) return fail(ADJ_ERR_INVALID_VALUE, "ADJ_HERK_ALG1 runs exactly one level (depth 1 or -1)");
+  // low-memory schedule (ADJ_LOW_MEM): where it applies; the in-place K4 reads C with 16-byte loads
+  const bool lm_applies = phi == ADJ_PHI_T && !axpby && lowmem_shape_ok(m, k, depth);
+  const bool lm_aligned = (uintptr_t)C % 16 == 0 && ldc % 8 == 0;
+  const bool lowmem = (flags & ADJ_LOW_MEM) && lm_applies;
+  if (lowmem && !lm_aligned)
+    return fail(ADJ_ERR_INVALID_VALUE, "ADJ_LOW_MEM needs C 16-byte aligned and ldc %% 8 == 0");
   Plan *P = nullptr;
-  const int kind = herk1 ? PLAN_HERK1 : (phi == ADJ_PHI_T ? PLAN_SYRK_T : (phi == ADJ_PHI_H ? PLAN_SYRK_H : PLAN_QUAT));
+  const int kind = herk1 ? PLAN_HERK1
+                   : lowmem ? PLAN_LOWMEM
+                   : (phi == ADJ_PHI_T ? PLAN_SYRK_T : (phi == ADJ_PHI_H ? PLAN_SYRK_H : PLAN_QUAT));
   if ((st = get_plan(&P, kind, m, m, k, p, (int)phi, depth, dev, sms)) != ADJ_OK) return st;
+  // automatic fall-back to the low-memory schedule: a caller workspace too small for the grouped
+  // schedule but large enough for it, or a failed library workspace allocation
+  const bool lm_fallback = !lowmem && lm_applies && lm_aligned;
+  auto to_lowmem = [&]() -> adj_status_t { return get_plan(&P, PLAN_LOWMEM, m, m, k, p, (int)phi, depth, dev, sms); };
   Ptrs x;
   x.A = A; x.lda = lda; x.C = C; x.ldc = ldc;
   x.alpha = alpha; x.beta = beta; x.axpby = axpby;
@@ -789,13 +870,23 @@ static adj_status_t adjprod_impl(int64_t m, int64_t k, uint32_t p, adj_phi_t phi
   void *ws = opts ? opts->workspace : nullptr;
   bool own = false;
   if (ws == nullptr) {
-    CUDA_TRY(adj_pool_alloc(&ws, P->ws_bytes, s));
+    cudaError_t e = adj_pool_alloc(&ws, P->ws_bytes, s);
+    if (e != cudaSuccess && lm_fallback) {
+      cudaGetLastError();
+      if ((st = to_lowmem()) != ADJ_OK) return st;
+      e = adj_pool_alloc(&ws, P->ws_bytes, s);
+    }
+    if (e != cudaSuccess) return fail(ADJ_ERR_WORKSPACE, "workspace allocation of %zu bytes: %s", P->ws_bytes,
+                                      cudaGetErrorString(e));
     own = true;
   } else if (opts->workspace_bytes < P->ws_bytes) {
-    return fail(ADJ_ERR_WORKSPACE, "workspace %zu bytes < required %zu", opts->workspace_bytes, P->ws_bytes);
+    if (lm_fallback && (st = to_lowmem()) != ADJ_OK) return st;
+    if (opts->workspace_bytes < P->ws_bytes)
+      return fail(ADJ_ERR_WORKSPACE, "workspace %zu bytes < required %zu", opts->workspace_bytes, P->ws_bytes);
   }
   x.ws = static_cast<uint8_t *>(ws);
-  st = herk1 ? run_herk1(*P, x, flags, s) : (phi == ADJ_PHI_Q ? run_quat(*P, x, flags, s) : run_syrk(*P, x, phi, flags, s));
+  st = herk1 ? run_herk1(*P, x, flags, s)
+              : (phi == ADJ_PHI_Q ? run_quat(*P, x, flags, s) : run_syrk(*P, x, phi, flags, s, dev, sms));
   if (own) {
     cudaError_t e = cudaFreeAsync(ws, s);
     if (st == ADJ_OK && e != cudaSuccess) return fail(ADJ_ERR_CUDA, "cudaFreeAsync: %s", cudaGetErrorString(e));

@@ -3,6 +3,7 @@
 // phi(H), Im = H^T - H (Alg. alg:2M); the GF(p^2) and quaternion (6M,
 // PAPER.md:2016-2037) recombinations.
 #include <algorithm>
+#include <type_traits>
 #include <cstdio>
 
 #include "kernel_util.cuh"
@@ -60,7 +61,11 @@ template <> struct Pk8<uint32_t> {
   }
 };
 
-template <typename InT, typename OutT, int T>
+// INPL (low-memory schedule): P1, P3 and P5 are read from C's own C11, C21 and C22
+// blocks (OutT, leading dimension ldo), where the children and the root leaf wrote them.  Each
+// thread writes only positions it has itself read above (C11 / C21 / C22 on L over its P1 / P3 /
+// P5 loads, C21 on U over its P3 load), so the in-place update needs no extra ordering.
+template <typename InT, typename OutT, int T, bool INPL = false>
 __global__ void __launch_bounds__(T * T / 16) combine_kernel(const __grid_constant__ CombParams P) {
   constexpr int TX = T / 8, H = T / 2;   // TX threads of 8 columns per row; rows ty and ty + H
   const CombNode &N = P.nodes[blockIdx.y];
@@ -81,25 +86,30 @@ __global__ void __launch_bounds__(T * T / 16) combine_kernel(const __grid_consta
   const int64_t mh = P.mh, ldp = P.ldp;                     // ldp multiple of 128 -> aligned 16-byte loads
   const int64_t i0 = (int64_t)ti * T, j0 = (int64_t)tj * T;
   const ModP &m = P.mod;
-  const InT *P1 = static_cast<const InT *>(N.P[0]), *P2 = static_cast<const InT *>(N.P[1]);
-  const InT *P3 = static_cast<const InT *>(N.P[2]), *P4 = static_cast<const InT *>(N.P[3]);
-  const InT *P5 = static_cast<const InT *>(N.P[4]);
+  using T1 = typename std::conditional<INPL, OutT, InT>::type;   // type of P1, P3, P5
+  const int64_t ld1 = INPL ? N.ldo : ldp;
+  const T1 *P1 = INPL ? static_cast<const T1 *>(N.out) : static_cast<const T1 *>(N.P[0]);
+  const T1 *P3 = INPL ? static_cast<const T1 *>(N.out) + mh * ld1 : static_cast<const T1 *>(N.P[2]);
+  const T1 *P5 = INPL ? static_cast<const T1 *>(N.out) + mh * ld1 + mh : static_cast<const T1 *>(N.P[4]);
+  const InT *P2 = static_cast<const InT *>(N.P[1]), *P4 = static_cast<const InT *>(N.P[3]);
   __shared__ uint32_t sU[T][T + 1];   // U1 on L (Low part; on a diagonal tile the full tile is filled)
   __shared__ uint32_t sQ[T][T + 1];   // P4 on U (rows j0.., cols i0..)
   const int cx = tx * 8;
   // every load of the block up front (buffers are rows_pad x rows_pad: always in range)
-  Pk8<InT> l1[2], l5[2], l2[2], l3[2], l4[2], u4[2], u3[2];
+  Pk8<T1> l1[2], l5[2], l3[2], u3[2];
+  Pk8<InT> l2[2], l4[2], u4[2];
 #pragma unroll
   for (int rr = 0; rr < 2; ++rr) {
     const int y = ty + H * rr;
     const int64_t oL = (i0 + y) * ldp + j0 + cx, oU = (j0 + y) * ldp + i0 + cx;
-    l1[rr].load(P1 + oL);
-    l5[rr].load(P5 + oL);
+    const int64_t oL1 = (i0 + y) * ld1 + j0 + cx, oU1 = (j0 + y) * ld1 + i0 + cx;
+    l1[rr].load(P1 + oL1);
+    l5[rr].load(P5 + oL1);
     u4[rr].load(P4 + oU);
     l4[rr].load(P4 + oL);
-    l3[rr].load(P3 + oL);
+    l3[rr].load(P3 + oL1);
     l2[rr].load(P2 + oL);
-    if (!diag) u3[rr].load(P3 + oU);
+    if (!diag) u3[rr].load(P3 + oU1);
   }
   uint32_t u1[2][8];
 #pragma unroll
@@ -191,7 +201,8 @@ cudaError_t launch_combine(const CombParams &p, cudaStream_t s) {
   dim3 grid(p.pairs ? (unsigned)p.n_pairs : nt * (nt + 1) / 2, (unsigned)p.n_nodes), block(T * T / 16);
   if (grid.x == 0) return cudaSuccess;
 #define COMB(I, O)                                                        \
-  if (T == 64) combine_kernel<I, O, 64><<<grid, block, 0, s>>>(p);       \
+  if (p.inplace) combine_kernel<I, O, 32, true><<<grid, block, 0, s>>>(p); \
+  else if (T == 64) combine_kernel<I, O, 64><<<grid, block, 0, s>>>(p);  \
   else combine_kernel<I, O, 32><<<grid, block, 0, s>>>(p)
   if (p.in32) COMB(uint32_t, uint32_t);
   else if (p.out_u32) COMB(uint16_t, uint32_t);

@@ -528,6 +528,61 @@ bool build_herk1_plan(Plan &P, int64_t m, int64_t k, uint32_t p, int num_sms, co
   return true;
 }
 
+// ---------------------------------------------------------------- low-memory schedule (row N1)
+// Applies to phi = T at depth >= 1 when the root's blocks are whole 64-row multiples (m even
+// halves, 32 x 32 in-place K4 tiles stay inside C): m % 64 == 0.
+bool lowmem_shape_ok(int64_t m, int64_t k, int depth) { return depth >= 1 && m >= 128 && m % 64 == 0 && k >= 1; }
+
+bool build_lowmem_plan(Plan &P, int64_t m, int64_t k, uint32_t p, int depth, int num_sms, const char **err) {
+  if (!lowmem_shape_ok(m, k, depth)) { *err = "low-memory schedule needs depth >= 1 and m % 64 == 0"; return false; }
+  Plan child;
+  const int64_t mh = m / 2, kh = 8 * cdiv(k, 16);
+  if (!build_syrk_plan(child, mh, kh, p, 0, depth - 1, num_sms, err)) return false;
+  P = Plan();
+  P.kind = PLAN_LOWMEM;
+  P.m = m; P.n = m; P.k = k; P.depth = 1; P.lm_depth = depth;
+  fill_scheme(P, p);
+  P.lv.resize(2);
+  P.lv[0].mh = m; P.lv[0].kh = k;
+  P.lv[0].rows_pad = rup(m, kBM);
+  P.lv[0].kpad = std::max<int64_t>(kBK, rup(k, kBK));
+  LevelPlan &L = P.lv[1];
+  L.mh = mh; L.kh = kh;
+  L.rows_pad = rup(mh, kBM);
+  L.kpad = std::max<int64_t>(kBK, rup(kh, kBK));
+  L.n_nodes = 1;
+  L.n_ops = 4;                                   // S1, S2, S4, A22 (P1, P2, P5 are the children)
+  P.rows_pad0 = P.lv[0].rows_pad;
+  P.kpad0 = P.lv[0].kpad;
+  if (L.rows_pad >= (int64_t)4096 * P.tile_m) { *err = "m too large"; return false; }
+  size_t off = 0;
+  auto alloc = [&](size_t bytes) { size_t o = off; off += (size_t)rup((int64_t)bytes, 256); return o; };
+  L.s3_node_bytes = (size_t)rup(mh * kh * P.res_bytes(), 256);
+  L.s3_offset = alloc(L.s3_node_bytes);
+  const size_t pb = (size_t)L.rows_pad * L.rows_pad * P.res_bytes();
+  P.lm_p2_off = alloc(pb);
+  P.lm_p4_off = alloc(pb);
+  P.lm_region_off = off;
+  ArenaPlan a;
+  a.kpad = L.kpad;
+  a.n_rows = (int64_t)4 * P.planes * L.rows_pad;
+  a.offset = alloc(a.bytes());
+  L.arena = 0;
+  P.arenas.push_back(a);
+  P.ws_bytes = off;
+  const int64_t rp = L.rows_pad;
+  auto row = [&](int o) { return (int64_t)o * P.planes * rp; };
+  // P3 = A22 phi(S4) into C21 (m - mh = mh rows), P4 = S1 phi(S2) into its buffer
+  P.prods.push_back(make_prod(P, 0, row(OUT_X22), row(OUT_S4), rp, rp, L.kpad, false, OUT_C21, 1, 0, 2, mh, mh, true, 0));
+  P.prods.push_back(make_prod(P, 0, row(OUT_S1), row(OUT_S2), rp, rp, L.kpad, false, OUT_LMP4, 1, 0, 3, rp, rp, false, rp));
+  append_tiles(P);
+  set_grid(P, num_sms);
+  P.lm_child_ws = child.ws_bytes;
+  P.ws_bytes = std::max(P.ws_bytes, P.lm_region_off + child.ws_bytes);
+  P.ws_bytes = (P.ws_bytes + 255) / 256 * 256;
+  return true;
+}
+
 bool build_gemm_plan(Plan &P, int64_t m, int64_t n, int64_t k, uint32_t p, int num_sms, const char **err) {
   P = Plan();
   P.kind = PLAN_GEMM;

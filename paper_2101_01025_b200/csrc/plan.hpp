@@ -14,7 +14,8 @@
 
 namespace adj {
 
-enum PlanKind : int { PLAN_SYRK_T = 0, PLAN_SYRK_H = 1, PLAN_GEMM = 2, PLAN_HERK1 = 3, PLAN_QUAT = 4 };
+enum PlanKind : int { PLAN_SYRK_T = 0, PLAN_SYRK_H = 1, PLAN_GEMM = 2, PLAN_HERK1 = 3, PLAN_QUAT = 4,
+                      PLAN_LOWMEM = 5 /* root level of the low-memory schedule (phi = T, ADJ_LOW_MEM) */ };
 
 // PLAN_QUAT (phi = quaternion conjugate transpose, Alg. alg:2M3M): arena-0 operands
 enum QuatOp : int { QO_A = 0, QO_B, QO_C, QO_D, QO_U1, QO_U2, QO_W, QO_N };
@@ -42,7 +43,9 @@ struct LevelPlan {
 };
 
 // leaf product whose output pointer is resolved at bind time
-enum OutTarget : int { OUT_PBUF = 0, OUT_C = 1, OUT_HBUF = 2, OUT_GBUF = 3, OUT_QBUF = 4 };
+enum OutTarget : int { OUT_PBUF = 0, OUT_C = 1, OUT_HBUF = 2, OUT_GBUF = 3, OUT_QBUF = 4,
+                       OUT_C21 = 5 /* low-memory root: P3 into C's C21 block */,
+                       OUT_LMP4 = 6 /* low-memory root: P4 buffer */ };
 struct ProductPlan {
   LeafProduct lp;        // everything except `out` (and ldo for OUT_C)
   int target;            // OutTarget
@@ -91,6 +94,14 @@ struct Plan {
   std::vector<std::pair<int64_t, int64_t>> shard_rows;   // [r0, r1) rows of the top level's operands its tiles read
   std::vector<uint32_t> comb_pairs;    // depth 1: K4 64 x 64 lower tile pairs (ti << 16 | tj)
   uint32_t *d_comb_pairs = nullptr;
+  // PLAN_LOWMEM: the root level of Alg. alg:MIAHMM only (depth = 1 here; the call's
+  // depth is lm_depth).  K1 writes S1, S2, S4, A22 and materialises S3; one leaf launch writes
+  // P3 into C21 and P4 into a buffer; then the children X11, X12, S3 run as ordinary calls of
+  // depth lm_depth - 1 whose Low results land in C11, a P2 buffer and C22; K4 runs in place.
+  // Workspace: [S3 | P2 | P4 | region], the region holding the root's arena and then, reused,
+  // the children's workspace.
+  int lm_depth = 0;
+  size_t lm_p2_off = 0, lm_p4_off = 0, lm_region_off = 0, lm_child_ws = 0;
 };
 
 // Build (host only, no CUDA calls).  Returns false with *err set if unsupported.
@@ -99,6 +110,8 @@ bool build_syrk_plan(Plan &P, int64_t m, int64_t k, uint32_t p, int phi, int dep
 std::vector<int> shard_owners(int64_t T, int depth, int nranks);
 bool build_gemm_plan(Plan &P, int64_t m, int64_t n, int64_t k, uint32_t p, int num_sms, const char **err);
 bool build_herk1_plan(Plan &P, int64_t m, int64_t k, uint32_t p, int num_sms, const char **err);
+bool build_lowmem_plan(Plan &P, int64_t m, int64_t k, uint32_t p, int depth, int num_sms, const char **err);
+bool lowmem_shape_ok(int64_t m, int64_t k, int depth);
 int auto_depth(int64_t m, int64_t k, uint32_t p, int phi);
 
 }  // namespace adj

@@ -154,6 +154,7 @@ struct CombParams {
   int32_t in32;            // P buffers hold uint32 residues (p > 2^16)
   const uint32_t *pairs;   // output-tile sharding: the (ti << 16 | tj) lower tile pairs to do (else all)
   int32_t n_pairs;
+  int32_t inplace;         // low-memory schedule: P1, P3, P5 read from out's C11, C21, C22 blocks
 };
 
 // ---------------------------------------------------------------- GF(p^2) Alg. 1 (PLAN_HERK1)

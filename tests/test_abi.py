@@ -223,3 +223,14 @@ def test_maximum_sizes_are_planned_or_refused():
     assert e.value.status == 1
     # largest single-tile-index-range leaf still planned (m = 4095 x 256 at depth 0)
     assert adj.adjprod_modp_workspace_size(4095 * 256, 32, 97, 0, 0) > 0
+
+
+def test_lowmem_workspace_within_twice_a_at_bench_sizes():
+    """ADJ_LOW_MEM: at c3 (32768^2, depth 2) and c4 (16384 x 131072, depth
+    2) the workspace is at most twice the uint16 A, and below the grouped schedule's."""
+    import paper_2101_01025_b200 as adj
+    for m, k, p in [(32768, 32768, 65521), (16384, 131072, 8191)]:
+        w_def = adj.adjprod_modp_workspace_size(m, k, p, 0, depth=2)
+        w_lm = adj.adjprod_modp_workspace_size(m, k, p, 0, depth=2, flags=adj.ADJ_LOW_MEM)
+        a16 = 2 * m * k
+        assert w_lm <= 2 * a16 < w_def, (m, k, w_lm / a16, w_def / a16)
