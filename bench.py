@@ -109,6 +109,13 @@ def leaf_int8_ops(cfg, depth, herk="2m") -> float:
     return 2.0 * macs * limb_mmas(p)
 
 
+def k1_fused(cfg, depth, res_bytes):
+    """the library's fused K1 of levels 1 + 2 runs (api.cpp k1_fused_ok): phi = T, depth >= 2,
+    uint16 residues, m and k multiples of 512"""
+    return (cfg["phi"] == "T" and depth >= 2 and res_bytes == 2 and cfg["p"] < 65536
+            and cfg["m"] % 512 == 0 and cfg["k"] % 512 == 0)
+
+
 def hbm_bytes(cfg, depth, herk="2m", res_bytes=4):
     """Algorithmic HBM bytes per step of the HBM-bound classes (K1 pre-addition / split and the
     recombination K4 / 2M / 6M combine), for the layouts DESIGN.md §4 describes: read each input
@@ -146,13 +153,14 @@ def hbm_bytes(cfg, depth, herk="2m", res_bytes=4):
         mh.append(-(-mh[-1] // 2))
         kh.append(8 * -(-kh[-1] // 16))
     pre = comb = 0
+    fused = k1_fused(cfg, depth, res_bytes)   # levels 1 + 2 in one pass: A read once, level-1 S3 in registers
 
     def node(level, rows, cols, esz):
         nonlocal pre, comb
-        pre_read = rows * cols * esz
+        pre_read = 0 if (fused and level == 2) else rows * cols * esz   # (level 3 reads as before)
         nops = 7 if level == depth else 4
         pre_write = nops * planes * rp(mh[level]) * max(128, rp(kh[level]))
-        if level < depth:
+        if level < depth and not (fused and level == 1 and depth == 2):
             pre_write += mh[level] * kh[level] * res       # S3, the third child's input
         pre += pre_read + pre_write
         m_l = mh[level]
@@ -603,20 +611,21 @@ def run_gpu(args, cfg, rank, world, local_rank):
     if world == 1 and not args.no_compare:
         comparators = {}
 
-        def other_depth(d):
+        def other_depth(d, extra=0):
             """the same step at depth d (median of flushed steps) and whether Low(C) is identical"""
-            wsd = adj.adjprod_modp_workspace_size(m, k, p, phi, d, flags)
+            fl = flags | extra
+            wsd = adj.adjprod_modp_workspace_size(m, k, p, phi, d, fl)
             wd = torch.empty(max(wsd, 1), dtype=torch.uint8, device=dev)
             Cd = torch.zeros_like(C)
             for _ in range(3):
-                adj.adjprod_modp_ex(m, k, p, phi, A, k, Cd, m, depth=d, flags=flags, workspace=wd, workspace_bytes=wsd,
+                adj.adjprod_modp_ex(m, k, p, phi, A, k, Cd, m, depth=d, flags=fl, workspace=wd, workspace_bytes=wsd,
                                     stream=stream)
             ts = []
             for _ in range(max(3, min(args.steps, 10))):
                 flush.zero_()
                 a0, b0 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a0.record(stream)
-                adj.adjprod_modp_ex(m, k, p, phi, A, k, Cd, m, depth=d, flags=flags, workspace=wd, workspace_bytes=wsd,
+                adj.adjprod_modp_ex(m, k, p, phi, A, k, Cd, m, depth=d, flags=fl, workspace=wd, workspace_bytes=wsd,
                                     stream=stream)
                 b0.record(stream)
                 torch.cuda.synchronize()
@@ -625,13 +634,17 @@ def run_gpu(args, cfg, rank, world, local_rank):
             lo = torch.tril(torch.ones(m, m, dtype=torch.bool, device=dev))
             same = bool(torch.equal(u32(Cd).view(m, m, w)[lo], u32(C).view(m, m, w)[lo]))
             return {"depth": d, "ms_per_step": msd, "value": m * m * k / (msd * 1e-3), "unit": UNIT,
-                    "same_result": same, "workspace_bytes": wsd}
+                    "same_result": same, "workspace_bytes": wsd, "workspace_over_A_bytes": wsd / A_bytes}
         if depth != 0 and not alg1:
             # the classical route (no Alg. 1 level): the on-box analogue of the paper's comparator
             comparators["depth0_classical"] = other_depth(0)
         elif depth == 0 and not alg1 and cfg["phi"] in ("T", "H"):
             # one level of Alg. 1 (inside 2M's G for phi = H) where the automatic depth is 0
             comparators["depth1_alg1"] = other_depth(1)
+        if cfg["phi"] == "T" and depth >= 1 and m % 64 == 0:
+            # the low-memory temporary schedule (ADJ_LOW_MEM): P1 / P3 / P5 of the root
+            # in C's own blocks, the root arena reused by the children, K4 in place
+            comparators["low_mem_schedule"] = other_depth(depth, adj.ADJ_LOW_MEM)
         if io16:   # the same step with uint32 residues in HBM
             A4, C4 = u32(A), torch.zeros((m, m * w), dtype=torch.int32, device=dev)
             f4 = flags & ~(adj.ADJ_IN_U16 | adj.ADJ_OUT_U16)

@@ -419,9 +419,26 @@ adj_status_t run_split(const Plan &P, const InView &v, int64_t rows, int64_t col
   return ADJ_OK;
 }
 
+// The fused K1 of levels 1 + 2 (preadd.cu preadd2_kernel) applies: phi = T, depth >= 2, uint16
+// residues, a uint16 root view covering the whole m x k input, and both levels halve exactly
+// with no padding rows or columns (m, k multiples of 512).
+bool k1_fused_ok(const Plan &P, const InView &root, const uint8_t *side_arena) {
+  static const bool off = getenv("ADJ_K1_UNFUSED") != nullptr;   // diagnostics (A/B)
+  if (off || P.kind != PLAN_SYRK_T || P.depth < 2 || P.res32 || P.scheme > 2 ||
+      side_arena != nullptr || P.shard_n > 0)
+    return false;
+  if ((root.type != IN_U16 && root.type != IN_U16R) || !root.vec_ok || root.rows_valid != P.m || root.cols_valid != P.k)
+    return false;
+  const LevelPlan &A = P.lv[1], &B = P.lv[2];
+  return 2 * A.mh == P.m && 2 * A.kh == P.k && A.rows_pad == A.mh && A.kpad == A.kh && 2 * B.mh == A.mh &&
+         2 * B.kh == A.kh && B.rows_pad == B.mh && B.kpad == B.kh && A.kh % 16 == 0;
+}
+
 adj_status_t run_tree(const Plan &P, const InView &root, const Ptrs &x, cudaStream_t s,
                       uint8_t *side_arena = nullptr) {
   // top-down pre-additions
+  const bool fused = k1_fused_ok(P, root, side_arena);
+  PreParams pp1;
   std::vector<std::vector<InView>> views(P.depth + 1);
   views[1] = {root};
   for (int l = 1; l <= P.depth; ++l) {
@@ -457,7 +474,9 @@ adj_status_t run_tree(const Plan &P, const InView &root, const Ptrs &x, cudaStre
       N.in = views[l][n];
       for (int o = 0; o < OUT_N; ++o)
         N.op_row[o] = o < L.n_ops ? ((int64_t)n * L.n_ops + o) * P.planes * L.rows_pad : -1;
-      if (l < P.depth || P.kind == PLAN_LOWMEM) {
+      // fused levels 1 + 2 keep the level-1 S3 in registers -- unless level 3 exists: the X11 / X12
+      // views of the level-2 S3 node's children point into it
+      if ((l < P.depth || P.kind == PLAN_LOWMEM) && !(fused && l == 1 && P.depth == 2)) {
         N.s3 = s3buf(P, x.ws, l, n);
         N.s3_ld = L.kh;
       }
@@ -469,7 +488,9 @@ adj_status_t run_tree(const Plan &P, const InView &root, const Ptrs &x, cudaStre
         N.side_y_row = P.op0_row[1];
       }
     }
-    LAUNCH_CLS(CLS_PRE, launch_preadd(pp, s));
+    if (fused && l == 1) { pp1 = pp; continue; }
+    if (fused && l == 2) LAUNCH_CLS(CLS_PRE, launch_preadd2(pp1, pp, s));
+    else LAUNCH_CLS(CLS_PRE, launch_preadd(pp, s));
   }
   return ADJ_OK;
 }

@@ -358,6 +358,14 @@ __device__ __forceinline__ void put_side(const PreNode &N, int64_t R, int64_t C,
   put_limbs4<SCHEME>(N.side + (N.side_y_row + R) * N.side_kpad + C, ps, im, m);
 }
 
+template <int SCHEME, int YK>
+__device__ __forceinline__ void k1_core(const PreParams &P, const PreNode &N, int64_t r, int64_t c,
+                                        const uint32_t (&x11a)[4], const uint32_t (&x11b)[4],
+                                        const uint32_t (&x12a)[4], const uint32_t (&x12b)[4],
+                                        const uint32_t (&x21a)[4], const uint32_t (&x21b)[4],
+                                        const uint32_t (&x22a)[4], const uint32_t (&x22b)[4],
+                                        uint32_t *s3a = nullptr, uint32_t *s3b = nullptr);
+
 template <int SCHEME, int YK, int T>
 __device__ __forceinline__ void preadd_row(const PreParams &P, const PreNode &N, int64_t r, int64_t c) {
   const ModP &m = P.mod;
@@ -455,6 +463,22 @@ __device__ __forceinline__ void preadd_row(const PreParams &P, const PreNode &N,
     load4(vv, P.mh + r, P.kh + c, m, x22a);
     load4(vv, P.mh + r, P.kh + c + h2, m, x22b);
   }
+  k1_core<SCHEME, YK>(P, N, r, c, x11a, x11b, x12a, x12b, x21a, x21b, x22a, x22b);
+}
+
+// The arithmetic and stores of K1 at one position (row r, columns c..c+3 and c+h2..c+h2+3 of the
+// quadrants) from the canonical residues of the 8 quadrant quads.  Writes the node's limb
+// operands and, when N.s3 is set, its canonical S3; s3a / s3b (if given) receive the canonical
+// S3 residues (the fused two-level K1 keeps them in registers for the next level).
+template <int SCHEME, int YK>
+__device__ __forceinline__ void k1_core(const PreParams &P, const PreNode &N, int64_t r, int64_t c,
+                                        const uint32_t (&x11a)[4], const uint32_t (&x11b)[4],
+                                        const uint32_t (&x12a)[4], const uint32_t (&x12b)[4],
+                                        const uint32_t (&x21a)[4], const uint32_t (&x21b)[4],
+                                        const uint32_t (&x22a)[4], const uint32_t (&x22b)[4],
+                                        uint32_t *s3a, uint32_t *s3b) {
+  const ModP &m = P.mod;
+  const int64_t h2 = P.kh / 2;
   {
     // One reduction per S output (modp.cuh k1_s1_s2).  Residues are carried as offset values
     // u = c + h in [0, p) of the centered c (h = (p - 1) / 2), so every correction is an unsigned
@@ -520,6 +544,13 @@ __device__ __forceinline__ void preadd_row(const PreParams &P, const PreNode &N,
       }
       *reinterpret_cast<uint2 *>(d + c) = make_uint2(v[0] | (v[1] << 16), v[2] | (v[3] << 16));
       *reinterpret_cast<uint2 *>(d + c + h2) = make_uint2(v[4] | (v[5] << 16), v[6] | (v[7] << 16));
+    }
+    if (s3a != nullptr) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        s3a[e] = wrap_lo(u3a[e] - (uint32_t)h);
+        s3b[e] = wrap_lo(u3b[e] - (uint32_t)h);
+      }
     }
   }
 }
@@ -589,6 +620,114 @@ cudaError_t launch_preadd(const PreParams &p, cudaStream_t s) {
   else if (p.scheme == 2) { if (p.ykind == 0) PRE(2, 0); else PRE(2, 1); }
   else { if (p.ykind == 0) PRE(3, 0); else PRE(3, 1); }
 #undef PRE
+  return cudaGetLastError();
+}
+
+// ============================================================================ fused K1, levels 1 + 2
+// Depth >= 2, phi = T, uint16 input (ADJ_IN_U16), p < 2^16 and exact halving without padding
+// (m, k multiples of 512; api.cpp k1_fused_ok).  The quads a level-2 position (r2, c2) of the
+// three level-2 nodes reads -- X11 = A11, X12 = A12 and S3 of level 1, rows {r2, r2 + mh2},
+// columns {c2, c2 + kh2/2, c2 + kh2, c2 + 3 kh2/2} -- are exactly the level-1 quadrant positions
+// of rows {r2, r2 + mh1/2} and columns {c2 + j kh1/4} (kh2 = kh1/2, mh2 = mh1/2).  One thread
+// loads those 32 quads of A once, runs the level-1 pre-addition at its 4 positions (writing the
+// level-1 limb operands), keeps the 8 S3 quads in registers and runs the level-2 pre-addition of
+// the three nodes from registers: A is read once and, at depth 2, the level-1 S3 never goes
+// through HBM (at depth >= 3 it is still written: level 3 reads views of it) (Alg. alg:MIAHMM
+// applied twice; level 2 reads only what level 1 produced).
+struct Pre2Params {
+  PreParams l1, l2;
+};
+
+__device__ __forceinline__ void unpack4(uint2 q, uint32_t (&x)[4]) {
+  x[0] = q.x & 0xFFFF; x[1] = q.x >> 16; x[2] = q.y & 0xFFFF; x[3] = q.y >> 16;
+}
+__device__ __forceinline__ uint2 pack4(const uint32_t (&x)[4]) {
+  return make_uint2(x[0] | (x[1] << 16), x[2] | (x[3] << 16));
+}
+
+template <int SCHEME, int YK>
+__global__ void __launch_bounds__(256, 2) preadd2_kernel(const __grid_constant__ Pre2Params P) {
+  const PreParams &L1 = P.l1, &L2 = P.l2;
+  const PreNode &N1 = L1.nodes[0];
+  const int64_t kq = L1.kh / 4;               // = kh2 / 2
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (4 * g >= kq) return;
+  const int64_t c2 = 4 * g;
+  const uint16_t *src = static_cast<const uint16_t *>(N1.in.ptr);
+  const int64_t ld = N1.in.ld;
+  const ModP &m = L1.mod;
+  for (int64_t r2 = blockIdx.y; r2 < L2.mh; r2 += gridDim.y) {
+    uint2 q[4][2][4];   // quadrant (A11, A12, A21, A22) x row (r2, r2 + mh2) x column c2 + j kq
+#pragma unroll
+    for (int qd = 0; qd < 4; ++qd)
+#pragma unroll
+      for (int ri = 0; ri < 2; ++ri)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int64_t row = (qd >= 2 ? L1.mh : 0) + r2 + ri * L2.mh;
+          const int64_t col = ((qd & 1) ? L1.kh : 0) + c2 + j * kq;
+          q[qd][ri][j] = __ldg(reinterpret_cast<const uint2 *>(src + row * ld + col));
+        }
+    // inputs are read mod p: one packed max over the 128 values, the reducing path only if needed
+    uint32_t mx = 0;
+#pragma unroll
+    for (int qd = 0; qd < 4; ++qd)
+#pragma unroll
+      for (int ri = 0; ri < 2; ++ri)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) mx = __vmaxu2(mx, __vmaxu2(q[qd][ri][j].x, q[qd][ri][j].y));
+    if (max(mx & 0xFFFF, mx >> 16) >= m.p) {
+#pragma unroll
+      for (int qd = 0; qd < 4; ++qd)
+#pragma unroll
+        for (int ri = 0; ri < 2; ++ri)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            uint32_t x[4];
+            unpack4(q[qd][ri][j], x);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) x[e] = mod_u32(x[e], m);
+            q[qd][ri][j] = pack4(x);
+          }
+    }
+    // level 1 at (r2 + ri mh2, c2 + j kq), j = 0, 1 (columns j + 2 are the Y partners, + kh1/2)
+    uint2 s3[2][4];
+#pragma unroll
+    for (int ri = 0; ri < 2; ++ri)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        uint32_t x11a[4], x11b[4], x12a[4], x12b[4], x21a[4], x21b[4], x22a[4], x22b[4], sa[4], sb[4];
+        unpack4(q[0][ri][j], x11a); unpack4(q[0][ri][j + 2], x11b);
+        unpack4(q[1][ri][j], x12a); unpack4(q[1][ri][j + 2], x12b);
+        unpack4(q[2][ri][j], x21a); unpack4(q[2][ri][j + 2], x21b);
+        unpack4(q[3][ri][j], x22a); unpack4(q[3][ri][j + 2], x22b);
+        k1_core<SCHEME, YK>(L1, N1, r2 + ri * L2.mh, c2 + j * kq, x11a, x11b, x12a, x12b, x21a, x21b, x22a, x22b,
+                            sa, sb);
+        s3[ri][j] = pack4(sa);
+        s3[ri][j + 2] = pack4(sb);
+      }
+    // level 2: nodes X11 (A11), X12 (A12), S3 at (r2, c2); their quadrant quads: row ri, column j
+#pragma unroll
+    for (int n = 0; n < 3; ++n) {
+      const uint2(&t)[2][4] = n == 0 ? q[0] : (n == 1 ? q[1] : s3);
+      uint32_t x11a[4], x11b[4], x12a[4], x12b[4], x21a[4], x21b[4], x22a[4], x22b[4];
+      unpack4(t[0][0], x11a); unpack4(t[0][1], x11b); unpack4(t[0][2], x12a); unpack4(t[0][3], x12b);
+      unpack4(t[1][0], x21a); unpack4(t[1][1], x21b); unpack4(t[1][2], x22a); unpack4(t[1][3], x22b);
+      k1_core<SCHEME, YK>(L2, L2.nodes[n], r2, c2, x11a, x11b, x12a, x12b, x21a, x21b, x22a, x22b);
+    }
+  }
+}
+
+cudaError_t launch_preadd2(const PreParams &l1, const PreParams &l2, cudaStream_t s) {
+  Pre2Params p;
+  p.l1 = l1;
+  p.l2 = l2;
+  const int64_t threads = l1.kh / 16;   // kq / 4 column groups
+  dim3 grid((unsigned)((threads + 255) / 256), (unsigned)std::min<int64_t>(l2.mh, 65535), 1);
+  if (l1.scheme == 0) { if (l1.ykind == 0) preadd2_kernel<0, 0><<<grid, 256, 0, s>>>(p); else preadd2_kernel<0, 1><<<grid, 256, 0, s>>>(p); }
+  else if (l1.scheme == 1) { if (l1.ykind == 0) preadd2_kernel<1, 0><<<grid, 256, 0, s>>>(p); else preadd2_kernel<1, 1><<<grid, 256, 0, s>>>(p); }
+  else if (l1.scheme == 2) { if (l1.ykind == 0) preadd2_kernel<2, 0><<<grid, 256, 0, s>>>(p); else preadd2_kernel<2, 1><<<grid, 256, 0, s>>>(p); }
+  else return cudaErrorInvalidValue;
   return cudaGetLastError();
 }
 

@@ -87,15 +87,20 @@ def test_hbm_bytes_c3_depth2():
     """K1 / K4 algorithmic bytes at c3 depth 2 (the N = 1 headline) written out level by level:
     level 1 reads A once and writes 4 operands (S1, S2, S4, X22) x 2 planes plus S3 (uint16);
     level 2 has 3 nodes (A11, A12 views of A and S3) each writing 7 operands x 2 planes; K4 reads
-    3 lower + 2 full product buffers per node and writes Low of its output."""
+    3 lower + 2 full product buffers per node and writes Low of its output.  With uint16 residues
+    the library fuses K1 of levels 1 and 2 (one read of A, S3 kept in registers): no level-2 reads
+    and no S3 round trip."""
     cfg = bench.CONFIGS["c3"]
     n = cfg["m"]
     assert cfg["k"] == n
     h1, h2 = n // 2, n // 4
     for rb in (2, 4):
         hb = bench.hbm_bytes(cfg, 2, res_bytes=rb)
-        pre = (rb * n * n + 4 * 2 * h1 * h1 + 2 * h1 * h1               # level 1
-               + 2 * h1 * h1 * rb + h1 * h1 * 2 + 3 * 7 * 2 * h2 * h2)    # level 2: reads, writes
+        if rb == 4:
+            pre = (rb * n * n + 4 * 2 * h1 * h1 + 2 * h1 * h1               # level 1
+                   + 2 * h1 * h1 * rb + h1 * h1 * 2 + 3 * 7 * 2 * h2 * h2)    # level 2: reads, writes
+        else:
+            pre = rb * n * n + 4 * 2 * h1 * h1 + 3 * 7 * 2 * h2 * h2          # fused levels 1 + 2
         comb = (3 * ((3 * h2 * (h2 + 1) // 2 + 2 * h2 * h2) * 2 + h1 * (h1 + 1) // 2 * 2)
                 + (3 * h1 * (h1 + 1) // 2 + 2 * h1 * h1) * 2 + n * (n + 1) // 2 * rb)
         assert hb == {"preadd": pre, "combine": comb}
