@@ -464,6 +464,7 @@ adj_status_t run_tree(const Plan &P, const InView &root, const Ptrs &x, cudaStre
     pp.kh = L.kh;
     pp.rows_pad = L.rows_pad;
     pp.kpad = L.kpad;
+    pp.plane_bytes = L.rows_pad * L.kpad;
     pp.arena = reinterpret_cast<int8_t *>(x.ws + P.arenas[L.arena].offset);
     pp.res32 = P.res32 ? 1 : 0;
     pp.mod = P.mod;
@@ -472,8 +473,10 @@ adj_status_t run_tree(const Plan &P, const InView &root, const Ptrs &x, cudaStre
     for (int n = 0; n < L.n_nodes; ++n) {
       PreNode &N = pp.nodes[n];
       N.in = views[l][n];
-      for (int o = 0; o < OUT_N; ++o)
+      for (int o = 0; o < OUT_N; ++o) {
         N.op_row[o] = o < L.n_ops ? ((int64_t)n * L.n_ops + o) * P.planes * L.rows_pad : -1;
+        N.op_off[o] = N.op_row[o] >= 0 ? N.op_row[o] * L.kpad : 0;
+      }
       // fused levels 1 + 2 keep the level-1 S3 in registers -- unless level 3 exists: the X11 / X12
       // views of the level-2 S3 node's children point into it
       if ((l < P.depth || P.kind == PLAN_LOWMEM) && !(fused && l == 1 && P.depth == 2)) {

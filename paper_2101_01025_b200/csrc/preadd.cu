@@ -500,24 +500,26 @@ __device__ __forceinline__ void k1_core(const PreParams &P, const PreNode &N, in
       u12a[e] = wrap_hi(x12a[e] + h); u12b[e] = wrap_hi(x12b[e] + h);
       u22a[e] = wrap_hi(x22a[e] + h); u22b[e] = wrap_hi(x22b[e] + h);
     }
-    const int64_t ps = P.rows_pad * P.kpad;
+    const int64_t ps = P.plane_bytes;
     const uint32_t koff = SCHEME == 1 ? 64u + 128u * 66u - (uint32_t)h
                           : (SCHEME == 3 ? 133152u - (uint32_t)h : (uint32_t)h);   // (0, 2: h)
+    // one row address per call; each operand adds its host-computed byte offset
+    int8_t *const rc = P.arena + r * P.kpad + c;
 #define PUTC(o, A, B)                                                                  \
   if (N.op_row[o] >= 0) {                                                              \
-    int8_t *b = P.arena + (N.op_row[o] + r) * P.kpad;                                  \
+    int8_t *b = rc + N.op_off[o];                                                      \
     if constexpr (SCHEME == 0) {                                                       \
-      put_limbs4_s8u(b + c, A, koff);                                                  \
-      put_limbs4_s8u(b + c + h2, B, koff);                                             \
+      put_limbs4_s8u(b, A, koff);                                                      \
+      put_limbs4_s8u(b + h2, B, koff);                                                 \
     } else if constexpr (SCHEME == 1) {                                                \
-      put_limbs4_k7u(b + c, ps, A, koff);                                              \
-      put_limbs4_k7u(b + c + h2, ps, B, koff);                                         \
+      put_limbs4_k7u(b, ps, A, koff);                                                  \
+      put_limbs4_k7u(b + h2, ps, B, koff);                                             \
     } else if constexpr (SCHEME == 2) {                                                \
-      put_limbs4_s8u8u(b + c, ps, A, koff);                                            \
-      put_limbs4_s8u8u(b + c + h2, ps, B, koff);                                       \
+      put_limbs4_s8u8u(b, ps, A, koff);                                                \
+      put_limbs4_s8u8u(b + h2, ps, B, koff);                                           \
     } else {                                                                           \
-      put_limbs4_t6u(b + c, ps, A, koff);                                              \
-      put_limbs4_t6u(b + c + h2, ps, B, koff);                                         \
+      put_limbs4_t6u(b, ps, A, koff);                                                  \
+      put_limbs4_t6u(b + h2, ps, B, koff);                                             \
     }                                                                                  \
   }
     PUTC(OUT_S1, u1a, u1b)

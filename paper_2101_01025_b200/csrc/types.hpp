@@ -88,6 +88,7 @@ enum PreOut : int { OUT_S1 = 0, OUT_S2, OUT_S4, OUT_X22, OUT_X11, OUT_X12, OUT_S
 struct PreNode {
   InView in;
   int64_t op_row[OUT_N];   // arena row of plane 0 for each output operand; -1 = not produced
+  int64_t op_off[OUT_N];   // the same as a byte offset, op_row * kpad (host-computed)
   void *s3;                // materialised S3 residues (when S3 recurses), else null (u16 / u32 if res32)
   int64_t s3_ld;
   // 2M side output (root node, IN_PAIR_SUM input): limb planes of X = Re(A) and Y = Im(A) for
@@ -112,6 +113,7 @@ struct PreParams {
   int64_t mh, kh;          // half sizes (node input is 2 mh x 2 kh, zero padded)
   int64_t rows_pad;        // rows per plane in the arena (>= mh, multiple of 128)
   int64_t kpad;            // arena row length in bytes (>= kh, multiple of 128)
+  int64_t plane_bytes;     // rows_pad * kpad (host-computed)
   int8_t *arena;
   int32_t res32;           // workspace residues are uint32 (p > 2^16)
   int32_t pad_;
