@@ -266,6 +266,18 @@ def load_traffic(config: str, depth: int):
 
 
 # ------------------------------------------------------------------------------ oracle
+def cpu_model() -> str:
+    """the host CPU's model name (/proc/cpuinfo), for the cpu_baseline context"""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def oracle_sample(cfg, A_host, budget_s: float):
     """Time the oracle (as it stands) on a slab of the last rows of Low(C) -- the longest rows --
     sized to ~budget_s of CPU work; returns (effective m^2 k MAC/s extrapolated, seconds, cores, desc)."""
@@ -341,7 +353,8 @@ def run_reference(args, cfg, rank, world):
         "dtype": "uint64", "data": "synthetic",
         "config": config_dict(args.config, cfg),
         "parallelism": f"CPU oracle, {cores} host threads (OpenMP)",
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc,
+                         "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -446,14 +459,18 @@ def run_gpu(args, cfg, rank, world, local_rank):
         adj.adj_profile_enable(False)
         step_ms = [a.elapsed_time(b) for a, b in evs]
         ms = sum(step_ms) / len(step_ms)
+        stats = {"min": min(step_ms), "median": statistics.median(step_ms), "max": max(step_ms)}
         if world > 1:
-            t = torch.tensor([ms], dtype=torch.float64, device=dev)
+            t = torch.tensor([ms, stats["min"], stats["median"], stats["max"]], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
+            ms = float(t[0].item())
+            stats = {"min": float(t[1].item()), "median": float(t[2].item()), "max": float(t[3].item())}
+        timed_pass.stats = stats
         return ms, launches, prof, clk
 
     t_pass = time.perf_counter()
     ms, launches, _, clk = timed_pass(False)
+    step_stats = timed_pass.stats   # of the headline pass (max over ranks)
     # an idle gap of ~3x the pass lets the board's power average recover, so that the profiled
     # pass runs under the same clocks as the headline one
     time.sleep(min(3.0, max(0.3, 3.0 * (time.perf_counter() - t_pass))))
@@ -608,6 +625,33 @@ def run_gpu(args, cfg, rank, world, local_rank):
     # (classical int8 SYRK, no Alg. 1 -- the on-box analogue of the paper's classical route,
     # SURVEY.md §8(d)) and cuBLASLt int8 (torch._int_mm) as a library int8 throughput point
     comparators = None
+    if world > 1 and dist_mode == "tiles" and not args.no_compare:
+        # the compute-only time of the output-tile sharding -- every rank computes its
+        # own regions of Low(C) (adjprod_modp_shard) and leaves them in place, no gather to the root;
+        # max over ranks.  Context beside the headline, which includes the gather.
+        try:
+            fl = dist_flags & ~adj.ADJ_DIST_TILES
+            for _ in range(2):
+                adj.adjprod_modp_shard(m, k, p, phi, A, k, C, m, rank, world, depth=depth, flags=fl, stream=stream)
+            ts = []
+            for _ in range(max(3, min(args.steps, 10))):
+                flush.zero_()
+                dist.barrier()
+                a0, b0 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a0.record(stream)
+                adj.adjprod_modp_shard(m, k, p, phi, A, k, C, m, rank, world, depth=depth, flags=fl, stream=stream)
+                b0.record(stream)
+                torch.cuda.synchronize()
+                ts.append(a0.elapsed_time(b0))
+            t = torch.tensor([statistics.median(ts)], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            msc = float(t.item())
+            comparators = {"compute_only_sharded_output": {
+                "ms_per_step": msc, "value": m * m * k / (msc * 1e-3), "unit": UNIT,
+                "what": "each rank's owned tile regions of Low(C) computed in place (adjprod_modp_shard), no gather; "
+                        "median of flushed steps, max over ranks"}}
+        except Exception as e:  # noqa: BLE001 -- context only, never breaks the headline line
+            comparators = {"compute_only_sharded_output": f"unavailable: {type(e).__name__}: {e}"}
     if world == 1 and not args.no_compare:
         comparators = {}
 
@@ -734,6 +778,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
                             f"{'sustained: the board was at its power cap (sw_power_cap) during the timed steps' if capped else 'burst'}"
                             f", int8 = 2x bf16 nominal; of burst (2 x {peaks['bf16_tflops']}): "
                             f"{achieved / (2.0 * peaks['bf16_tflops']):.3f}"),
+            "frac_of_spec_dense_int8": achieved / 4500.0,   # B200 datasheet 4.5 POPS dense (context)
             "algorithmic_ops_per_launch": ops, "leaf_ms_per_launch": leaf_avg_ms,
             "leaf_launches_per_step": leaf_n / args.steps,
             "measured": (f"library CUDA events around each leaf launch on the launch stream, over a second "
@@ -758,13 +803,13 @@ def run_gpu(args, cfg, rank, world, local_rank):
     if rank == 0 and world == 1 and not args.no_cpu:
         Ah = u32(A).cpu().numpy().view(np.uint32).reshape((m, k, w) if w > 1 else (m, k))
         eff, t, cores, desc, _ = oracle_sample(cfg, Ah, float(os.environ.get("ADJ_CPU_BUDGET_S", "10")))
-        cpu = {"value": eff, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
+        cpu = {"value": eff, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc, "cpu_model": cpu_model()}
 
     if rank == 0:
         mh = herk_alg1_macs(m, k) if alg1 else ring_macs(m, k, depth) + {1: 0, 2: 1, 4: 5}[w] * m * m * k
         line = {
             "metric": metric_label(args.config), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms, "step_ms": step_stats, "higher_is_better": True,
             "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "int8",
             "data": "synthetic",
             "config": config_dict(args.config, cfg),
