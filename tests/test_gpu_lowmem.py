@@ -138,3 +138,34 @@ def test_small_caller_workspace_falls_back_to_lowmem(adj):
     assert np.array_equal(np.tril(to_host(C)), np.tril(oracle.syrk_t(A, p)))
     with pytest.raises(adj.AdjError):
         adj.adjprod_modp_ex(m, k, p, 0, to_dev(A), k, C, m, depth=2, workspace=ws, workspace_bytes=w_lm - 256)
+
+
+@pytest.mark.parametrize("low_mem", [False, True])
+def test_graph_capture_fused_k1_and_lowmem(adj, low_mem):
+    """The fused K1 (uint16, m, k multiples of 512, depth 2) and the low-memory schedule (its
+    child calls and in-place K4) are fixed stream-ordered launch sequences: captured into a CUDA
+    graph and replayed, they reproduce the oracle's Low(C)."""
+    import torch
+    p, m, k, depth = 65521, 1024, 1536, 2
+    A = uniform_matrix(m, k, seed=31, p=p)
+    dA = to_dev(A).to(torch.int16)
+    flags = adj.ADJ_IN_U16 | adj.ADJ_OUT_U16 | (adj.ADJ_LOW_MEM if low_mem else 0)
+    ws_bytes = adj.adjprod_modp_workspace_size(m, k, p, 0, depth, flags=flags)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
+    C = torch.zeros((m, m), dtype=torch.int16, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        adj.adjprod_modp_ex(m, k, p, 0, dA, k, C, m, depth=depth, flags=flags, workspace=ws, workspace_bytes=ws_bytes,
+                            stream=s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        adj.adjprod_modp_ex(m, k, p, 0, dA, k, C, m, depth=depth, flags=flags, workspace=ws, workspace_bytes=ws_bytes,
+                            stream=s)
+    ref = np.tril(oracle.syrk_t(A, p))
+    for _ in range(2):
+        C.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        got = C.cpu().numpy().view(np.uint16).astype(np.uint32)
+        assert np.array_equal(np.tril(got), ref)
