@@ -29,11 +29,11 @@ sys.path.insert(0, ROOT)
 CONFIGS = {
     "c1": dict(m=256, k=256, p=97, phi="T", depth=1,
                workload="c1: A 256x256 over GF(97), C = Low(A A^T) mod 97, Y = 22 I, one recursion level"),
-    # c2 runs one level of Alg. 1 (the method's full hot path: pre-add, 5 products, recombine);
-    # the library's automatic depth is 0 at this size (classical is 8% faster on B200, reported
-    # as the depth0_classical comparator)
-    "c2": dict(m=8192, k=8192, p=8191, phi="T", depth=1,
-               workload="c2: A 8192x8192 over GF(8191), C = Low(A A^T) mod 8191, Y = Rot2(2670, 5929), one level of Alg. 1"),
+    # c2 runs at the library's automatic depth, 0 at this size (classical is 5-8% faster on B200:
+    # K1 + K4 cost more than the 1/8 of the MMAs one level saves on an L2-bound leaf); one level
+    # of Alg. 1 is reported beside it (comparators.depth1_alg1)
+    "c2": dict(m=8192, k=8192, p=8191, phi="T", depth=None,
+               workload="c2: A 8192x8192 over GF(8191), C = Low(A A^T) mod 8191, Y = Rot2(2670, 5929)"),
     "c3": dict(m=32768, k=32768, p=65521, phi="T", depth=None,
                workload="c3: A 32768x32768 over GF(65521), C = Low(A A^T) mod 65521, Y = 24297 I"),
     "c4": dict(m=16384, k=131072, p=8191, phi="T", depth=None,

@@ -234,3 +234,24 @@ def test_lowmem_workspace_within_twice_a_at_bench_sizes():
         w_lm = adj.adjprod_modp_workspace_size(m, k, p, 0, depth=2, flags=adj.ADJ_LOW_MEM)
         a16 = 2 * m * k
         assert w_lm <= 2 * a16 < w_def, (m, k, w_lm / a16, w_def / a16)
+
+
+def test_lowmem_workspace_layout():
+    """The low-memory workspace is [S3 | P2 | P4 | max(root arena, child workspace)] (plan.cpp
+    build_lowmem_plan), recomputed here from the level sizes: S3 is mh x kh
+    residues, P2 / P4 rows_pad^2 residues, the root arena 4 operands x planes x rows_pad x kpad
+    int8 (plus the tail's fixup slots and the job counter), the children ordinary calls of
+    shape mh x kh one level shallower."""
+    import paper_2101_01025_b200 as adj
+    rup = lambda x, a: -(-x // a) * a
+    for m, k, p, d in [(32768, 32768, 65521, 2), (16384, 131072, 8191, 2), (2048, 3000, 8191, 2), (1024, 1001, 97, 1)]:
+        planes = 1 if p <= 255 else (3 if p <= 16763 else 2)
+        res = 2
+        mh, kh = m // 2, 8 * -(-k // 16)
+        rp, kp = rup(mh, 128), max(128, rup(kh, 128))
+        head = rup(mh * kh * res, 256) + 2 * rup(rp * rp * res, 256)
+        arena = rup(4 * planes * rp * kp, 256)
+        child = adj.adjprod_modp_workspace_size(mh, kh, p, 0, depth=d - 1)
+        w = adj.adjprod_modp_workspace_size(m, k, p, 0, depth=d, flags=adj.ADJ_LOW_MEM)
+        fixup_and_counter = 74 * 256 * 256 * res + 256   # worst-case tail slots (num_sms / 2) + job counter
+        assert w == rup(head + max(arena + fixup_and_counter, child), 256), (m, k, p, d)

@@ -33,7 +33,7 @@ def env():
     return torch, adj, bench
 
 
-def _bench_run(env, name):
+def _bench_run(env, name, depth=None):
     """The bench's launch for config `name`: its depth and residue storage (uint16 A and Low(C)
     with ADJ_IN_U16 | ADJ_OUT_U16 when p < 2^16).  Returns (A residues int32 on the device,
     Low(C) as int32 on the device (m x m x w), depth)."""
@@ -43,7 +43,8 @@ def _bench_run(env, name):
     m, k, p = cfg["m"], cfg["k"], cfg["p"]
     phi = {"T": adj.ADJ_PHI_T, "H": adj.ADJ_PHI_H, "Q": adj.ADJ_PHI_Q}[cfg["phi"]]
     w = {"T": 1, "H": 2, "Q": 4}[cfg["phi"]]
-    depth = cfg["depth"] if cfg["depth"] is not None else adj.adjprod_modp_auto_depth(m, k, p, phi)
+    if depth is None:
+        depth = cfg["depth"] if cfg["depth"] is not None else adj.adjprod_modp_auto_depth(m, k, p, phi)
     A = torch.empty((m, k * w), dtype=torch.int32, device="cuda")
     uniform_residues_cuda(A, seed=1, p=p)
     assert p < 65536
@@ -60,14 +61,16 @@ def _bench_run(env, name):
     return A.view(m, k, w), C, depth
 
 
-@pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5", "q5"])
+@pytest.mark.parametrize("name", ["c2", "c2@1", "c3", "c4", "c5", "q5"])
 def test_whole_low_c_bench_launch(env, name):
     """Every entry of Low(C) at the config, in the bench's launch configuration (depth, uint16
-    residues), against the float64 product on the GPU and by Freivalds on the host."""
+    residues), against the float64 product on the GPU and by Freivalds on the host.  c2@1: c2
+    through one level of Alg. 1 (the bench's depth1_alg1 comparator; its automatic depth is 0)."""
     torch, adj, bench = env
+    name, _, d = name.partition("@")
     cfg = bench.CONFIGS[name]
     p = cfg["p"]
-    A, C, depth = _bench_run(env, name)
+    A, C, depth = _bench_run(env, name, int(d) if d else None)
     w = A.shape[2]
     if name == "c3":
         assert depth == 2          # the depth-2 tree the N = 1 headline times
@@ -90,7 +93,7 @@ def test_c2_fill_upper_full_symmetric(env):
     A = torch.empty((m, k), dtype=torch.int32, device="cuda")
     uniform_residues_cuda(A, seed=1, p=p)
     C = torch.full((m, m), -1, dtype=torch.int32, device="cuda")
-    adj.adjprod_modp_ex(m, k, p, adj.ADJ_PHI_T, A, k, C, m, depth=cfg["depth"], flags=adj.ADJ_FILL_UPPER)
+    adj.adjprod_modp_ex(m, k, p, adj.ADJ_PHI_T, A, k, C, m, depth=1, flags=adj.ADJ_FILL_UPPER)   # through Alg. 1
     torch.cuda.synchronize()
     assert torch.equal(C, C.T)
     Af = A.to(torch.float64)

@@ -169,3 +169,17 @@ def test_graph_capture_fused_k1_and_lowmem(adj, low_mem):
         torch.cuda.synchronize()
         got = C.cpu().numpy().view(np.uint16).astype(np.uint32)
         assert np.array_equal(np.tril(got), ref)
+
+
+def test_lowmem_fill_upper(adj):
+    """ADJ_LOW_MEM with ADJ_FILL_UPPER: Up(C) = Low(C)^T is written after the in-place K4."""
+    import torch
+    m, k, p = 1024, 700, 8191
+    A = uniform_matrix(m, k, seed=41, p=p)
+    C = torch.full((m, m), -1, dtype=torch.int32, device="cuda")
+    adj.adjprod_modp_ex(m, k, p, 0, to_dev(A), k, C, m, depth=2, flags=adj.ADJ_LOW_MEM | adj.ADJ_FILL_UPPER)
+    got = to_host(C)
+    ref = oracle.syrk_t(A, p)
+    lo = np.tril(np.ones((m, m), dtype=bool))
+    assert np.array_equal(got[lo], ref[lo])
+    assert np.array_equal(got, got.T)
