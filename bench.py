@@ -377,11 +377,14 @@ def run_gpu(args, cfg, rank, world, local_rank):
     flags = adj.ADJ_HERK_ALG1 if alg1 else 0
     depth = args.depth if args.depth is not None else (cfg["depth"] if cfg["depth"] is not None
                                                        else (1 if alg1 else adj.adjprod_modp_auto_depth(m, k, p, phi)))
-    # N > 1: output-tile sharding for square phi = T problems (depth <= 1), split-K otherwise
-    dist_mode = args.dist if args.dist != "auto" else ("tiles" if cfg["phi"] == "T" and k <= 2 * m else "splitk")
+    # N > 1: output-tile sharding for square phi = T problems (depth <= 1) with each rank's final
+    # kernel storing its regions straight into rank 0's C over NVLink, split-K otherwise
+    dist_mode = args.dist if args.dist != "auto" else ("tiles-p2p" if cfg["phi"] == "T" and k <= 2 * m else "splitk")
     dist_flags = 0
     if world > 1 and dist_mode == "tiles":
         dist_flags = adj.ADJ_DIST_TILES
+    elif world > 1 and dist_mode == "tiles-p2p":
+        dist_flags = adj.ADJ_DIST_TILES | adj.ADJ_DIST_P2P
     elif world > 1 and dist_mode == "p2p":
         dist_flags = adj.ADJ_DIST_P2P
     if dist_flags:
@@ -428,6 +431,16 @@ def run_gpu(args, cfg, rank, world, local_rank):
         else:
             adj.adjprod_modp_dist(m, k, p, phi, A, k, C, m, 0, comm, depth=depth, flags=dist_flags, stream=stream)
 
+    dist_fallback = None
+    if comm is not None and dist_mode == "tiles-p2p":
+        # the fused mode needs the root's C exportable over CUDA IPC; every rank agrees on the
+        # status inside the call, so all of them fall back together to the NCCL gather
+        try:
+            step()
+            torch.cuda.synchronize()
+        except adj.AdjError as e:
+            dist_fallback = f"tiles-p2p unavailable ({e}); NCCL gather of result tiles"
+            dist_mode, dist_flags = "tiles", (dist_flags & ~adj.ADJ_DIST_P2P)
     for _ in range(max(args.warmup, 3)):
         flush.zero_()
         step()
@@ -625,12 +638,12 @@ def run_gpu(args, cfg, rank, world, local_rank):
     # (classical int8 SYRK, no Alg. 1 -- the on-box analogue of the paper's classical route,
     # SURVEY.md §8(d)) and cuBLASLt int8 (torch._int_mm) as a library int8 throughput point
     comparators = None
-    if world > 1 and dist_mode == "tiles" and not args.no_compare:
+    if world > 1 and dist_mode in ("tiles", "tiles-p2p") and not args.no_compare:
         # the compute-only time of the output-tile sharding -- every rank computes its
         # own regions of Low(C) (adjprod_modp_shard) and leaves them in place, no gather to the root;
         # max over ranks.  Context beside the headline, which includes the gather.
         try:
-            fl = dist_flags & ~adj.ADJ_DIST_TILES
+            fl = dist_flags & ~(adj.ADJ_DIST_TILES | adj.ADJ_DIST_P2P)
             for _ in range(2):
                 adj.adjprod_modp_shard(m, k, p, phi, A, k, C, m, rank, world, depth=depth, flags=fl, stream=stream)
             ts = []
@@ -650,6 +663,27 @@ def run_gpu(args, cfg, rank, world, local_rank):
                 "ms_per_step": msc, "value": m * m * k / (msc * 1e-3), "unit": UNIT,
                 "what": "each rank's owned tile regions of Low(C) computed in place (adjprod_modp_shard), no gather; "
                         "median of flushed steps, max over ranks"}}
+            if dist_mode == "tiles-p2p":
+                # the same sharding with the NCCL gather (pack, send / recv, unpack) instead of peer stores
+                fg = dist_flags & ~adj.ADJ_DIST_P2P
+                ts = []
+                for i in range(2 + max(3, min(args.steps, 10))):
+                    flush.zero_()
+                    dist.barrier()
+                    a0, b0 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a0.record(stream)
+                    adj.adjprod_modp_dist(m, k, p, phi, A, k, C, m, 0, comm, depth=depth, flags=fg, stream=stream)
+                    b0.record(stream)
+                    torch.cuda.synchronize()
+                    if i >= 2:
+                        ts.append(a0.elapsed_time(b0))
+                t = torch.tensor([statistics.median(ts)], dtype=torch.float64, device=dev)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                msg = float(t.item())
+                comparators["tiles_nccl_gather"] = {
+                    "ms_per_step": msg, "value": m * m * k / (msg * 1e-3), "unit": UNIT,
+                    "what": "the same output-tile sharding with the result tiles packed, sent to rank 0 with NCCL "
+                            "send / recv and unpacked there; median of flushed steps, max over ranks"}
         except Exception as e:  # noqa: BLE001 -- context only, never breaks the headline line
             comparators = {"compute_only_sharded_output": f"unavailable: {type(e).__name__}: {e}"}
     if world == 1 and not args.no_compare:
@@ -825,8 +859,11 @@ def run_gpu(args, cfg, rank, world, local_rank):
             "parallelism": ("1 GPU" if world == 1 else
                             (f"output tiles x{world} (NCCL send/recv gather of result tiles)"
                              if dist_mode == "tiles" else
+                             f"output tiles x{world} (each rank's final kernel stores its regions into rank 0's C "
+                             f"over NVLink)" if dist_mode == "tiles-p2p" else
                              f"split-K x{world} (partials stored into the root over NVLink)"
                              if dist_mode == "p2p" else f"split-K x{world} (NCCL reduce)")),
+            "dist_fallback": dist_fallback,
             "fraction_of_int8_peak_effective": value / (world * peak * 1e12 / 2),
             "roofline": roof,
             "cpu_baseline": cpu,
@@ -873,9 +910,11 @@ def main():
                     help="storage of the residues of A and Low(C): auto = uint16 when phi = T, p < 2^16, N = 1")
     ap.add_argument("--no-check", action="store_true", help="skip the sampled parity check")
     ap.add_argument("--no-compare", action="store_true", help="skip the depth-0 / cuBLASLt comparators")
-    ap.add_argument("--dist", default="auto", choices=["auto", "splitk", "tiles", "p2p"],
-                    help="N > 1: split-K (NCCL reduce), output-tile sharding (gather of result tiles) or "
-                         "split-K with the exchange fused into the final kernel (peer stores over NVLink)")
+    ap.add_argument("--dist", default="auto", choices=["auto", "splitk", "tiles", "tiles-p2p", "p2p"],
+                    help="N > 1: split-K (NCCL reduce), output-tile sharding (NCCL gather of result tiles), "
+                         "output-tile sharding with the gather fused into the final kernel (peer stores into the "
+                         "root's C over NVLink; auto for square phi = T) or split-K with the exchange fused into "
+                         "the final kernel (peer stores into the root's window)")
     ap.add_argument("--herk", default="2m", choices=["2m", "alg1"],
                     help="phi = H: 2M reduction (default) or one level of Alg. 1 over GF(p^2)")
     args = ap.parse_args()

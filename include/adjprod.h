@@ -86,6 +86,11 @@ typedef enum {
  *                    into the final kernel: each rank stores its partial (narrow residues)
  *                    straight into the root's window over NVLink (CUDA IPC peer memory), the root
  *                    sums exactly (adj_sum_partials); no NCCL data movement.
+ *                    With ADJ_DIST_TILES as well: output-tile sharding with the gather fused into
+ *                    the final kernel -- the root's C is mapped on every rank (adj_ipc_export /
+ *                    adj_ipc_open), and each rank's last kernel (leaf epilogue at depth 0, K4 at
+ *                    depth 1) stores its owned regions of Low(C) straight into it over NVLink;
+ *                    no pack, no NCCL data movement, no unpack.
  *   ADJ_IN_U16     : p < 2^16 -- A holds uint16 values (phi = H: interleaved uint16 (re, im)
  *                    pairs; phi = Q: 4 uint16 components), read mod p; lda counts elements as
  *                    before: half the bytes to read and to ship over PCIe.  phi = T also through
@@ -202,6 +207,22 @@ adj_status_t adj_comm_init(int nranks, const uint8_t id[128], int rank, adj_comm
  *   the root frees it (CUDA IPC requires importers to close before the exporter frees). */
 adj_status_t adj_comm_destroy(adj_comm_t comm);
 
+/* CUDA IPC of a device pointer inside an allocation (the building blocks of ADJ_DIST_TILES |
+ *   ADJ_DIST_P2P; host calls, synchronous).
+ *   adj_ipc_export -- ptr: a device pointer anywhere inside a cudaMalloc allocation (e.g. a torch
+ *     tensor's data pointer) of the current device.  Writes an ADJ_IPC_RECORD_BYTES record (the
+ *     allocation's 64-byte cudaIpcMemHandle_t, then the byte offset of ptr from its base as a
+ *     little-endian int64) to rec.  ADJ_ERR_INVALID_VALUE for a null ptr / rec, ADJ_ERR_CUDA
+ *     when the memory cannot be exported (stream-ordered pool memory, host memory).
+ *   adj_ipc_open -- maps the record's allocation in this process (another process; any device
+ *     with peer access to the owner's, or the same device) and returns base + offset in *ptr.
+ *   adj_ipc_close -- unmaps a pointer adj_ipc_open returned (after the work that uses it has
+ *     completed).  The exporter must not free the allocation before every importer closed it. */
+#define ADJ_IPC_RECORD_BYTES 72
+adj_status_t adj_ipc_export(const void *ptr, uint8_t rec[ADJ_IPC_RECORD_BYTES]);
+adj_status_t adj_ipc_open(const uint8_t rec[ADJ_IPC_RECORD_BYTES], void **ptr);
+adj_status_t adj_ipc_close(void *ptr);
+
 /* adj_dist_kslice -- the column slice [k0, k1) of A that rank `rank` of `nranks` owns in
  *   adjprod_modp_dist (host, no GPU): per = ceil(k / nranks) rounded up to a multiple of 8,
  *   k0 = min(k, rank * per), k1 = min(k, k0 + per).  Slices are disjoint and cover [0, k). */
@@ -290,6 +311,12 @@ adj_status_t adj_shard_pack(int64_t m, int64_t k, uint32_t p, int depth, int ran
  *   With opts->flags & ADJ_DIST_TILES (phi = ADJ_PHI_T): output-tile sharding instead -- every
  *   rank runs adjprod_modp_shard with the full A into its C, then the root gathers the other
  *   ranks' regions (packed, NCCL send/recv: only result tiles move).
+ *   With ADJ_DIST_TILES | ADJ_DIST_P2P: the same sharding, each rank's final kernel storing its
+ *   regions straight into the root's C over NVLink (the root exports C with adj_ipc_export and
+ *   broadcasts the record and ldc; the other ranks' C arguments are not used).  The root's C
+ *   must be cudaMalloc memory (ADJ_ERR_CUDA on every rank otherwise).  Two host-synchronised
+ *   barriers: after the compute (every peer store has landed when the call returns on the root)
+ *   and after the importers unmapped C (the caller may free C once the call returns).
  */
 adj_status_t adjprod_modp_dist(int64_t m, int64_t k, uint32_t p, adj_phi_t phi,
                                const uint32_t *A, int64_t lda, uint32_t *C, int64_t ldc,

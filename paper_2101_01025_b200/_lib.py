@@ -21,13 +21,14 @@ ADJ_DIST_P2P = 8
 ADJ_IN_U16 = 16
 ADJ_OUT_U16 = 32
 ADJ_LOW_MEM = 64
+ADJ_IPC_RECORD_BYTES = 72
 STATUS = {0: "ADJ_OK", 1: "ADJ_ERR_INVALID_VALUE", 2: "ADJ_ERR_UNSUPPORTED_MODULUS", 3: "ADJ_ERR_WORKSPACE",
           4: "ADJ_ERR_CUDA", 5: "ADJ_ERR_NCCL", 6: "ADJ_ERR_ARCH"}
 
 # every symbol include/adjprod.h declares (checked by tests/test_abi.py)
 EXPORTS = ["adjprod_modp", "adjprod_modp_ex", "adjprod_modp_syrk", "adjprod_modp_workspace_size", "adjprod_modp_auto_depth",
            "gemm_modp", "adj_skew_unitary", "adj_sos", "adj_mod_lower", "adj_comm_get_unique_id",
-           "adj_comm_init", "adj_comm_destroy", "adjprod_modp_dist", "adj_dist_kslice", "adj_elem_bytes", "adjprod_modp_dist_partial", "adjprod_modp_shard", "adj_shard_layout", "adj_shard_rows", "adjprod_modp_partial", "adj_sum_partials", "adj_shard_pack", "adj_status_string", "adj_last_error",
+           "adj_comm_init", "adj_comm_destroy", "adjprod_modp_dist", "adj_dist_kslice", "adj_elem_bytes", "adjprod_modp_dist_partial", "adjprod_modp_shard", "adj_shard_layout", "adj_shard_rows", "adjprod_modp_partial", "adj_sum_partials", "adj_shard_pack", "adj_ipc_export", "adj_ipc_open", "adj_ipc_close", "adj_status_string", "adj_last_error",
            "adj_launch_count", "adj_launch_count_reset", "adj_profile_enable", "adj_profile_read"]
 
 
@@ -75,6 +76,9 @@ def lib() -> ctypes.CDLL:
             "adjprod_modp_partial": [i64, i64, u32, ci, vp, i64, vp, i64, ctypes.POINTER(adj_opts_t), vp],
             "adj_sum_partials": [i64, u32, vp, i64, i64, ci, vp, i64, vp],
             "adj_shard_pack": [i64, i64, u32, ci, ci, ci, vp, i64, vp, ci, vp],
+            "adj_ipc_export": [vp, ctypes.c_char_p],
+            "adj_ipc_open": [ctypes.c_char_p, ctypes.POINTER(vp)],
+            "adj_ipc_close": [vp],
             "adj_shard_layout": [i64, i64, u32, ci, ci, ci, ctypes.POINTER(i64), i64, ctypes.POINTER(i64),
                                  ctypes.POINTER(i64)],
         }
@@ -187,6 +191,22 @@ def adj_comm_init(nranks: int, uid: bytes, rank: int):
 
 def adj_comm_destroy(comm):
     _check(lib().adj_comm_destroy(comm), "adj_comm_destroy")
+
+
+def adj_ipc_export(ptr) -> bytes:
+    buf = ctypes.create_string_buffer(ADJ_IPC_RECORD_BYTES)
+    _check(lib().adj_ipc_export(_ptr(ptr), buf), "adj_ipc_export")
+    return buf.raw
+
+
+def adj_ipc_open(rec: bytes) -> int:
+    out = ctypes.c_void_p(0)
+    _check(lib().adj_ipc_open(rec, ctypes.byref(out)), "adj_ipc_open")
+    return out.value
+
+
+def adj_ipc_close(ptr):
+    _check(lib().adj_ipc_close(_ptr(ptr)), "adj_ipc_close")
 
 
 def adjprod_modp_dist(m, k, p, phi, A, lda, C, ldc, root, comm, depth=-1, flags=0, stream=None):

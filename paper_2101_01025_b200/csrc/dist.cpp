@@ -2,6 +2,7 @@
 // column slice with the single-GPU path, the residue partials are summed exactly by an NCCL
 // uint32 reduce (sum < G p < 2^32) and reduced mod p on the root.  NCCL is resolved with
 // dlopen at first use (the torch-bundled libnccl.so.2 when running inside torch).
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
@@ -9,6 +10,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -25,7 +27,7 @@ struct adj_comm_s {
   size_t win_bytes = 0;
   int win_root = -1;
   bool win_owned = false;        // root: cudaMalloc'ed; others: IPC-mapped
-  void *d_scratch = nullptr;     // 64-byte device buffer: IPC handle broadcast and barrier token
+  void *d_scratch = nullptr;     // 128-byte device buffer: IPC record broadcast and barrier token
 };
 
 namespace {
@@ -79,7 +81,7 @@ bool load_nccl() {
 
 namespace {
 adj_status_t ensure_scratch(adj_comm_t comm) {
-  if (!comm->d_scratch && cudaMalloc(&comm->d_scratch, 64) != cudaSuccess) return ADJ_ERR_CUDA;
+  if (!comm->d_scratch && cudaMalloc(&comm->d_scratch, 128) != cudaSuccess) return ADJ_ERR_CUDA;
   return ADJ_OK;
 }
 
@@ -293,6 +295,54 @@ adj_status_t dist_p2p(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, const uin
   if (r == root) st = adj_sum_partials(m, p, comm->win, m, (int64_t)slot, G, C, ldc, stream);
   return st;
 }
+
+// output-tile sharding with the gather fused into the compute (ADJ_DIST_TILES | ADJ_DIST_P2P):
+// the root exports its C (adj_ipc_export), the record and ldc are broadcast, every other rank
+// maps the root's C and runs its share (adjprod_modp_shard) with the mapped pointer as its output:
+// the final kernel of the share -- the leaf epilogue at depth 0 (tile by tile, under the MMAs of
+// the following tiles), K4 at depth 1 -- stores the owned regions of Low(C) over NVLink straight
+// into their place.  No pack, no NCCL data movement, no unpack on the root.
+adj_status_t dist_tiles_p2p(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, const uint32_t *A, int64_t lda,
+                            uint32_t *C, int64_t ldc, int root, adj_comm_t comm, const adj_opts_t *opts,
+                            adj_stream_t stream) {
+  const int G = comm->nranks, r = comm->rank;
+  if (G == 1) return adjprod_modp_shard(m, k, p, phi, A, lda, C, ldc, 0, 1, opts, stream);
+  if (!load_nccl()) return ADJ_ERR_NCCL;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  constexpr size_t kRec = ADJ_IPC_RECORD_BYTES + 8;   // handle, offset, ldc
+  uint8_t rec[kRec] = {};
+  adj_status_t st = ensure_scratch(comm);
+  if (st == ADJ_OK && r == root) {
+    st = adj_ipc_export(C, rec);
+    std::memcpy(rec + ADJ_IPC_RECORD_BYTES, &ldc, 8);
+  }
+  if ((st = agree_status(comm, st, s)) != ADJ_OK) return st;
+  if (r == root && cudaMemcpyAsync(comm->d_scratch, rec, kRec, cudaMemcpyHostToDevice, s) != cudaSuccess)
+    st = ADJ_ERR_CUDA;   // (the peers then see garbage and fail to open: agreed below)
+  if (g_nccl.Broadcast(comm->d_scratch, comm->d_scratch, kRec, ncclUint8, root, comm->comm, s) != ncclSuccess)
+    return ADJ_ERR_NCCL;
+  void *dst = nullptr;
+  int64_t ldd = ldc;
+  if (r != root && st == ADJ_OK) {
+    if (cudaMemcpyAsync(rec, comm->d_scratch, kRec, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+      st = ADJ_ERR_CUDA;
+    else {
+      std::memcpy(&ldd, rec + ADJ_IPC_RECORD_BYTES, 8);
+      st = adj_ipc_open(rec, &dst);
+    }
+  }
+  // every rank has its output pointer before any store
+  if ((st = agree_status(comm, st, s)) == ADJ_OK)
+    st = adjprod_modp_shard(m, k, p, phi, A, lda, r == root ? C : static_cast<uint32_t *>(dst), r == root ? ldc : ldd,
+                            r, G, opts, stream);
+  // barrier 1 (host-synchronised): every rank's share, and so every peer store, has completed
+  st = agree_status(comm, st, s);
+  if (dst) adj_ipc_close(dst);
+  // barrier 2: the importers have unmapped C -- the root's caller may free it after the return
+  const adj_status_t b = host_barrier(comm, s);
+  return st != ADJ_OK ? st : b;
+}
 }  // namespace
 
 extern "C" {
@@ -337,6 +387,70 @@ adj_status_t adj_comm_destroy(adj_comm_t comm) {
   return ADJ_OK;
 }
 
+// ---- CUDA IPC of a pointer inside an allocation: the handle names the allocation's base, the
+// record carries the offset (cuMemGetAddressRange through the runtime's driver entry point)
+namespace {
+std::mutex g_ipc_mu;
+std::map<void *, void *> g_ipc_open;   // pointer handed out -> mapped base
+}  // namespace
+
+adj_status_t adj_ipc_export(const void *ptr, uint8_t rec[ADJ_IPC_RECORD_BYTES]) {
+  if (!ptr || !rec) return ADJ_ERR_INVALID_VALUE;
+  using range_fn = CUresult (*)(CUdeviceptr *, size_t *, CUdeviceptr);
+  static range_fn get_range = nullptr;
+  if (!get_range) {
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn ||
+        q != cudaDriverEntryPointSuccess)
+      return ADJ_ERR_CUDA;
+    get_range = reinterpret_cast<range_fn>(fn);
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (get_range(&base, &size, reinterpret_cast<CUdeviceptr>(ptr)) != CUDA_SUCCESS) return ADJ_ERR_CUDA;
+  cudaIpcMemHandle_t h;
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  if (cudaIpcGetMemHandle(&h, reinterpret_cast<void *>(base)) != cudaSuccess) {
+    cudaGetLastError();
+    return ADJ_ERR_CUDA;
+  }
+  const int64_t off = (int64_t)(reinterpret_cast<CUdeviceptr>(ptr) - base);
+  std::memcpy(rec, &h, 64);
+  std::memcpy(rec + 64, &off, 8);
+  return ADJ_OK;
+}
+
+adj_status_t adj_ipc_open(const uint8_t rec[ADJ_IPC_RECORD_BYTES], void **ptr) {
+  if (!rec || !ptr) return ADJ_ERR_INVALID_VALUE;
+  cudaIpcMemHandle_t h;
+  int64_t off = 0;
+  std::memcpy(&h, rec, 64);
+  std::memcpy(&off, rec + 64, 8);
+  if (off < 0) return ADJ_ERR_INVALID_VALUE;
+  void *base = nullptr;
+  if (cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+    cudaGetLastError();
+    return ADJ_ERR_CUDA;
+  }
+  *ptr = static_cast<uint8_t *>(base) + off;
+  std::lock_guard<std::mutex> g(g_ipc_mu);
+  g_ipc_open[*ptr] = base;
+  return ADJ_OK;
+}
+
+adj_status_t adj_ipc_close(void *ptr) {
+  void *base = nullptr;
+  {
+    std::lock_guard<std::mutex> g(g_ipc_mu);
+    auto it = g_ipc_open.find(ptr);
+    if (it == g_ipc_open.end()) return ADJ_ERR_INVALID_VALUE;
+    base = it->second;
+    g_ipc_open.erase(it);
+  }
+  return cudaIpcCloseMemHandle(base) == cudaSuccess ? ADJ_OK : ADJ_ERR_CUDA;
+}
+
 adj_status_t adj_dist_kslice(int64_t k, int nranks, int rank, int64_t *k0, int64_t *k1) {
   if (!k0 || !k1 || k < 0 || nranks < 1 || rank < 0 || rank >= nranks) return ADJ_ERR_INVALID_VALUE;
   const int64_t per = ((k + nranks - 1) / nranks + 7) / 8 * 8;
@@ -368,6 +482,8 @@ adj_status_t adjprod_modp_dist(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, 
   if (opts && (opts->flags & ADJ_OUT_U16)) return ADJ_ERR_INVALID_VALUE;   // Low(C) on the root is uint32
   if (m == 0) return ADJ_OK;
   const int G = comm->nranks, r = comm->rank;
+  if (opts && (opts->flags & ADJ_DIST_TILES) && (opts->flags & ADJ_DIST_P2P))
+    return dist_tiles_p2p(m, k, p, phi, A, lda, C, ldc, root, comm, opts, stream);
   if (opts && (opts->flags & ADJ_DIST_TILES)) return dist_tiles(m, k, p, phi, A, lda, C, ldc, root, comm, opts, stream);
   if (opts && (opts->flags & ADJ_DIST_P2P) && phi == ADJ_PHI_T && G > 1)
     return dist_p2p(m, k, p, phi, A, lda, C, ldc, root, comm, opts, stream);

@@ -255,3 +255,22 @@ def test_lowmem_workspace_layout():
         w = adj.adjprod_modp_workspace_size(m, k, p, 0, depth=d, flags=adj.ADJ_LOW_MEM)
         fixup_and_counter = 74 * 256 * 256 * res + 256   # worst-case tail slots (num_sms / 2) + job counter
         assert w == rup(head + max(arena + fixup_and_counter, child), 256), (m, k, p, d)
+
+
+def test_ipc_validation_needs_no_gpu():
+    """adj_ipc_export / adj_ipc_open / adj_ipc_close (the building blocks of ADJ_DIST_TILES |
+    ADJ_DIST_P2P) reject null pointers and unknown mappings before touching CUDA."""
+    import re
+    text = open(os.path.join(ROOT, "include", "adjprod.h")).read()
+    assert int(re.search(r"#define ADJ_IPC_RECORD_BYTES (\d+)", text).group(1)) == adj._lib.ADJ_IPC_RECORD_BYTES
+    with pytest.raises(adj.AdjError) as e:
+        adj.adj_ipc_export(0)
+    assert e.value.status == 1
+    L = adj.lib()
+    out = ctypes.c_void_p(0)
+    assert L.adj_ipc_open(None, ctypes.byref(out)) == 1
+    rec = bytes(64) + (-8).to_bytes(8, "little", signed=True)       # negative offset
+    assert L.adj_ipc_open(rec, ctypes.byref(out)) == 1
+    with pytest.raises(adj.AdjError) as e:
+        adj.adj_ipc_close(0x1000)                                     # never opened
+    assert e.value.status == 1

@@ -1,6 +1,7 @@
 """adjprod_modp_dist with N > 1 ranks, one process per GPU over NCCL: every mode
 (split-K with the packed uint32 reduce, output-tile sharding with the rank-local pre-addition and
-the gather of result tiles, split-K with peer stores into the root's window) against the oracle,
+the gather of result tiles, split-K with peer stores into the root's window, output-tile sharding with peer stores into the
+root's C) against the oracle,
 bit-exactly, on the root.  Needs N devices: skipped when fewer are visible (the round's GPU box
 has one; the driver's 8-GPU step runs it)."""
 import os
@@ -44,7 +45,8 @@ def _worker(rank, world, port, cases, q):
             gen = {"T": uniform_matrix, "H": uniform_matrix_ext, "Q": uniform_matrix_quat}[phi]
             A = gen(m, k, 17, p).reshape(m, k * w)
             code = {"T": adj.ADJ_PHI_T, "H": adj.ADJ_PHI_H, "Q": adj.ADJ_PHI_Q}[phi]
-            flags = {"splitk": 0, "tiles": adj.ADJ_DIST_TILES, "p2p": adj.ADJ_DIST_P2P}[mode]
+            flags = {"splitk": 0, "tiles": adj.ADJ_DIST_TILES, "p2p": adj.ADJ_DIST_P2P,
+                     "tiles-p2p": adj.ADJ_DIST_TILES | adj.ADJ_DIST_P2P}[mode]
             if in16:
                 flags |= adj.ADJ_IN_U16
                 dA = torch.from_numpy(A.astype(np.uint16).view(np.int16)).cuda()
@@ -74,7 +76,9 @@ def test_dist_all_modes_n_ranks(world):
     cases = [(1030, 700, 8191, "T", "splitk", -1, False), (1030, 700, 8191, "T", "tiles", 1, False),
              (1030, 700, 8191, "T", "tiles", 0, True), (1030, 700, 8191, "T", "p2p", -1, True),
              (600, 900, 65521, "T", "splitk", 2, True), (300, 257, 8191, "H", "splitk", 1, False),
-             (200, 130, 8191, "Q", "splitk", 0, True), (700, 500, 131071, "T", "tiles", 1, False)]
+             (200, 130, 8191, "Q", "splitk", 0, True), (700, 500, 131071, "T", "tiles", 1, False),
+             (1030, 700, 8191, "T", "tiles-p2p", 1, False), (1030, 700, 8191, "T", "tiles-p2p", 0, True),
+             (777, 520, 65521, "T", "tiles-p2p", 1, True), (600, 333, 131071, "T", "tiles-p2p", 1, False)]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
