@@ -489,6 +489,15 @@ def run_gpu(args, cfg, rank, world, local_rank):
     time.sleep(min(3.0, max(0.3, 3.0 * (time.perf_counter() - t_pass))))
     ms_prof, _, prof, clk_prof = timed_pass(True)
     value = m * m * k / (ms * 1e-3)
+    # N > 1: each rank runs its share of the step's leaf work (and K1 / K4 bytes); the roofline and
+    # the HBM fractions below divide the whole step's algorithmic work by the per-class device time
+    # summed over the ranks (the per-GPU average), not by rank 0's share alone
+    prof_all = prof
+    if world > 1:
+        cls = sorted(prof)
+        t = torch.tensor([prof[c][0] for c in cls], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        prof_all = {c: (float(t[i].item()) / world, prof[c][1]) for i, c in enumerate(cls)}
 
     # ---------------- sustained: the same steps back to back for ~--sustain-s seconds (the board
     # reaches its power cap on long streams; context for the burst-regime headline above, and the
@@ -792,10 +801,10 @@ def run_gpu(args, cfg, rank, world, local_rank):
 
     # ---------------- roofline of the dominant kernel (grouped tcgen05 leaf launch)
     peaks, src = load_peaks()
-    leaf_ms, leaf_n = prof["leaf"]
+    leaf_ms, leaf_n = prof_all["leaf"]
     # one grouped leaf stage per step: the tcgen05 leaf launch (+ its tail fixup launch, if any)
     leaf_avg_ms = leaf_ms / args.steps
-    ops = leaf_int8_ops(cfg, depth, args.herk)
+    ops = leaf_int8_ops(cfg, depth, args.herk) / world   # per GPU: the ranks share the step's leaf work
     achieved = ops / (leaf_avg_ms * 1e-3) / 1e12
     # int8 dense = 2 x bf16 dense (the guide's nominal ratio).  Burst figure for a leaf timed in the
     # burst regime; the sustained (power-capped) figure when the board sat at its power limit during
@@ -817,7 +826,10 @@ def run_gpu(args, cfg, rank, world, local_rank):
             "leaf_launches_per_step": leaf_n / args.steps,
             "measured": (f"library CUDA events around each leaf launch on the launch stream, over a second "
                          f"pass of the {args.steps} timed steps (same flushes; with these events a step "
-                         f"takes {ms_prof:.4f} ms, without them {ms:.4f} ms)"),
+                         f"takes {ms_prof:.4f} ms, without them {ms:.4f} ms)"
+                         + ("" if world == 1 else
+                            f"; N = {world}: 1/N of the step's leaf work over the leaf time averaged over the "
+                            f"ranks (each rank runs its share)")),
             "clocks_during": clk_prof.summary()}
     share = {c: round(v[0] / max(1e-9, sum(x[0] for x in prof.values())), 4) for c, v in prof.items()}
     # achieved HBM bandwidth of the HBM-bound kernels (algorithmic bytes / device time per step)
@@ -826,10 +838,10 @@ def run_gpu(args, cfg, rank, world, local_rank):
     if hb is not None:
         hbm = {}
         for cls, nbytes in hb.items():
-            t_ms = prof[cls][0] / args.steps
+            t_ms = prof_all[cls][0] / args.steps
             if nbytes is None or t_ms <= 0:
                 continue
-            gbs = nbytes / (t_ms * 1e-3) / 1e9
+            gbs = nbytes / world / (t_ms * 1e-3) / 1e9   # N > 1: the single-GPU bytes shared by the ranks
             hbm[cls] = {"bound": "hbm", "algorithmic_bytes": nbytes, "ms": t_ms, "achieved": gbs,
                         "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": gbs / peaks["hbm_gbs"]}
 
