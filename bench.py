@@ -265,6 +265,17 @@ def load_traffic(config: str, depth: int):
         return None
 
 
+def load_pure_mma_sustained():
+    """The pure tcgen05 kind::i8 rate with random operands back to back at the board's power cap
+    (tools/mma_peak.cu sustain, profiles/r02/int8_mma_sustained.json): the tensor datapath's own
+    ceiling under the cap, context beside the contract's 2 x bf16 sustained peak."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02", "int8_mma_sustained.json")) as f:
+            return float(json.load(f)["sustained_random_operands"]["steady_median_tops"])
+    except Exception:
+        return None
+
+
 # ------------------------------------------------------------------------------ oracle
 def cpu_model() -> str:
     """the host CPU's model name (/proc/cpuinfo), for the cpu_baseline context"""
@@ -822,6 +833,10 @@ def run_gpu(args, cfg, rank, world, local_rank):
                             f", int8 = 2x bf16 nominal; of burst (2 x {peaks['bf16_tflops']}): "
                             f"{achieved / (2.0 * peaks['bf16_tflops']):.3f}"),
             "frac_of_spec_dense_int8": achieved / 4500.0,   # B200 datasheet 4.5 POPS dense (context)
+            "frac_of_pure_mma_sustained": ((achieved / pm) if capped and (pm := load_pure_mma_sustained()) else None),
+            "pure_mma_sustained_source": ("pure tcgen05 kind::i8 issue rate with random operands resident in shared "
+                                          "memory, back to back at the power cap on this pool's B200 "
+                                          "(profiles/r02/int8_mma_sustained.json, an earlier run)" if capped else None),
             "algorithmic_ops_per_launch": ops, "leaf_ms_per_launch": leaf_avg_ms,
             "leaf_launches_per_step": leaf_n / args.steps,
             "measured": (f"library CUDA events around each leaf launch on the launch stream, over a second "

@@ -33,7 +33,7 @@ def env():
     return torch, adj, bench
 
 
-def _bench_run(env, name, depth=None):
+def _bench_run(env, name, depth=None, seed=1):
     """The bench's launch for config `name`: its depth and residue storage (uint16 A and Low(C)
     with ADJ_IN_U16 | ADJ_OUT_U16 when p < 2^16).  Returns (A residues int32 on the device,
     Low(C) as int32 on the device (m x m x w), depth)."""
@@ -46,7 +46,7 @@ def _bench_run(env, name, depth=None):
     if depth is None:
         depth = cfg["depth"] if cfg["depth"] is not None else adj.adjprod_modp_auto_depth(m, k, p, phi)
     A = torch.empty((m, k * w), dtype=torch.int32, device="cuda")
-    uniform_residues_cuda(A, seed=1, p=p)
+    uniform_residues_cuda(A, seed=seed, p=p)
     assert p < 65536
     A16 = A.to(torch.int16)
     C16 = torch.zeros((m, m * w), dtype=torch.int16, device="cuda")
@@ -80,6 +80,19 @@ def test_whole_low_c_bench_launch(env, name):
     del A, C
     torch.cuda.empty_cache()
     assert freivalds_low(Ah, Ch, p, w), (name, depth)
+
+
+@pytest.mark.parametrize("seed", [2, 3])
+@pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5", "q5"])
+def test_whole_low_c_other_seeds(env, name, seed):
+    """parity on seeds {1, 2, 3}.  Seeds 2 and 3 at every BASELINE config in the
+    bench's launch configuration: every entry of Low(C) against the float64 product on the GPU
+    (the Freivalds pass runs on seed 1 above)."""
+    torch, adj, bench = env
+    A, C, depth = _bench_run(env, name, None, seed)
+    assert exact_low_mismatches(torch, A, C, bench.CONFIGS[name]["p"], A.shape[2]) == 0, (name, seed, depth)
+    del A, C
+    torch.cuda.empty_cache()
 
 
 def test_c2_fill_upper_full_symmetric(env):

@@ -3,8 +3,11 @@
 //   mode 1: cta_group::1, M=128 N=256
 //   mode 2: cta_group::1, M=128 N=128
 // Reports int8 TOP/s (2 ops per MAC) over all SMs, timed with CUDA events.
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <string>
+#include <vector>
 #include <cuda_runtime.h>
 
 #include "../paper_2101_01025_b200/csrc/ptx.cuh"
@@ -14,7 +17,7 @@ using namespace adj;
 // VAR bits (pair mode only): 1 = tcgen05.commit after every 4 MMAs, 2 = try_wait on a completed
 // mbarrier + tcgen05.fence::after_thread_sync before every 4 MMAs, 4 = 8 MMAs per group
 template <int MODE, int VAR = 0>
-__global__ void __launch_bounds__(128, 1) mma_loop(int iters, int *sink) {
+__global__ void __launch_bounds__(128, 1) mma_loop(int iters, int *sink, int rnd = 0) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t bar, bar2, bar3;
@@ -27,7 +30,13 @@ __global__ void __launch_bounds__(128, 1) mma_loop(int iters, int *sink) {
   uint32_t rank = 0;
   if constexpr (PAIR) rank = ptx::cluster_ctarank();
   // fill operand smem (64 KB) with small values
-  for (int i = threadIdx.x; i < 65536 / 4; i += blockDim.x) reinterpret_cast<uint32_t *>(smem)[i] = 0x01010101u * (i & 3);
+  // rnd: uniformly random bytes (the leaf's limb planes of uniform residues toggle like this;
+  // tensor-core power depends on the operand bits)
+  for (int i = threadIdx.x; i < 65536 / 4; i += blockDim.x) {
+    uint32_t h = (uint32_t)i * 0x9E3779B9u + blockIdx.x * 0x85EBCA6Bu;
+    h ^= h >> 15; h *= 0x2C1B3C6Du; h ^= h >> 12; h *= 0x297A2D39u; h ^= h >> 15;
+    reinterpret_cast<uint32_t *>(smem)[i] = rnd ? h : 0x01010101u * (i & 3);
+  }
   if (threadIdx.x == 0) {
     ptx::mbar_init(&bar, 1);
     ptx::mbar_init(&bar2, 1 << 20);
@@ -135,13 +144,13 @@ double run(int sms, int iters) {
   cfg.numAttrs = 1;
   int *sink;
   cudaMalloc(&sink, sms * sizeof(int));
-  for (int w = 0; w < 2; ++w) cudaLaunchKernelEx(&cfg, k, iters, sink);
+  for (int w = 0; w < 2; ++w) cudaLaunchKernelEx(&cfg, k, iters, sink, 0);
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   cudaEventRecord(a);
   const int reps = 5;
-  for (int r = 0; r < reps; ++r) cudaLaunchKernelEx(&cfg, k, iters, sink);
+  for (int r = 0; r < reps; ++r) cudaLaunchKernelEx(&cfg, k, iters, sink, 0);
   cudaEventRecord(b);
   cudaEventSynchronize(b);
   float ms = 0;
@@ -155,9 +164,60 @@ double run(int sms, int iters) {
   return 2 * macs / (ms * 1e-3) / 1e12;
 }
 
+// back-to-back launches of the pair kernel (random operands) for `seconds`: TOP/s of every launch;
+// prints the first launch and the median of the second half (the board at its steady state)
+int sustain(int sms, int iters, double seconds) {
+  auto k = mma_loop<0, 0>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 66 * 1024 + 1024);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(sms);
+  cfg.blockDim = dim3(128);
+  cfg.dynamicSmemBytes = 66 * 1024 + 1024;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int *sink;
+  cudaMalloc(&sink, sms * sizeof(int));
+  const double macs = (sms / 2) * (double)iters * 4 * 256 * 256 * 32;
+  const int batch = 20;
+  cudaEvent_t ev[batch + 1];
+  for (int i = 0; i <= batch; ++i) cudaEventCreate(&ev[i]);
+  std::vector<double> tops;
+  double total = 0;
+  while (total < seconds * 1e3) {
+    cudaEventRecord(ev[0]);
+    for (int i = 0; i < batch; ++i) {
+      cudaLaunchKernelEx(&cfg, k, iters, sink, 1);
+      cudaEventRecord(ev[i + 1]);
+    }
+    cudaEventSynchronize(ev[batch]);
+    for (int i = 0; i < batch; ++i) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
+      total += ms;
+      tops.push_back(2 * macs / (ms * 1e-3) / 1e12);
+    }
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return 1; }
+  std::vector<double> tail(tops.begin() + tops.size() / 2, tops.end());
+  std::sort(tail.begin(), tail.end());
+  printf("{\"mode\": \"sustain\", \"operands\": \"random bytes\", \"sms\": %d, \"launches\": %zu, \"seconds\": %.2f, "
+         "\"first_launch_tops\": %.1f, \"steady_median_tops\": %.1f, \"steady_min_tops\": %.1f}\n",
+         sms, tops.size(), total * 1e-3, tops[0], tail[tail.size() / 2], tail[0]);
+  cudaFree(sink);
+  return 0;
+}
+
 int main(int argc, char **argv) {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  if (argc > 1 && std::string(argv[1]) == "sustain")
+    return sustain(sms, argc > 2 ? atoi(argv[2]) : 20000, argc > 3 ? atof(argv[3]) : 8.0);
   const int iters = argc > 1 ? atoi(argv[1]) : 20000;
   printf("{\"sms\": %d, \"iters\": %d, \"pair_256x256_tops\": %.1f, \"single_128x256_tops\": %.1f, "
          "\"single_128x128_tops\": %.1f,\n", sms, iters, run<0>(sms, iters), run<1>(sms, iters), run<2>(sms, iters));
