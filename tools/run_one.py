@@ -17,9 +17,11 @@ ap.add_argument("--depth", type=int, default=None)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--gemm", action="store_true", help="run gemm_modp m x m x k instead")
 ap.add_argument("--io16", action="store_true", help="uint16 A and Low(C) (ADJ_IN_U16 | ADJ_OUT_U16)")
+ap.add_argument("--m", type=int, default=None, help="override the config's m")
+ap.add_argument("--k", type=int, default=None, help="override the config's k")
 a = ap.parse_args()
 cfg = CONFIGS[a.config]
-m, k, p = cfg["m"], cfg["k"], cfg["p"]
+m, k, p = a.m or cfg["m"], a.k or cfg["k"], cfg["p"]
 w = 2 if cfg["phi"] == "H" else 1
 phi = 1 if w == 2 else 0
 A = torch.empty((m, k * w), dtype=torch.int32, device="cuda")
