@@ -386,7 +386,8 @@ adj_status_t launch_leaf_all(const Plan &P, const Ptrs &x, cudaStream_t s) {
   // diagnostics: ADJ_LEAF_GRID caps the persistent grid (CTAs, even; power-regime A/B)
   static const int grid_cap = getenv("ADJ_LEAF_GRID") ? atoi(getenv("ADJ_LEAF_GRID")) & ~1 : 0;
   const int grid = grid_cap > 0 ? std::min(P.grid, grid_cap) : P.grid;
-  LAUNCH_CLS(CLS_LEAF, launch_leaf2(L, P.nacc, P.segmented, grid, s));
+  if (P.wide) LAUNCH_CLS(CLS_LEAF, launch_leafw(L, P.nacc, grid, s));
+  else LAUNCH_CLS(CLS_LEAF, launch_leaf2(L, P.nacc, P.segmented, grid, s));
   if (!P.fixups.empty()) LAUNCH_CLS(CLS_LEAF, launch_fixup(L, P.d_fixups, (int)P.fixups.size(), s));
   return ADJ_OK;
 }

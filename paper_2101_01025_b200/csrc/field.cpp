@@ -91,8 +91,11 @@ LimbScheme limb_scheme(uint32_t p) {
 int limb_planes(LimbScheme s) { return s == LIMB_S8 ? 1 : (s == LIMB_K7 ? 3 : (s == LIMB_SU8 ? 2 : 6)); }
 int limb_accs(LimbScheme s) { return s == LIMB_S8 ? 1 : (s == LIMB_T6 ? 6 : 3); }
 
-int64_t limb_kmax(LimbScheme s, uint32_t p) {
-  const int64_t lim = 2147483647;
+static int64_t limb_kmax_lim(LimbScheme s, uint32_t p, int64_t lim);
+int64_t limb_kmax(LimbScheme s, uint32_t p) { return limb_kmax_lim(s, p, 2147483647); }
+int64_t limb_kmax_from_residue(LimbScheme s, uint32_t p) { return limb_kmax_lim(s, p, 2147483647 - (int64_t)p); }
+
+static int64_t limb_kmax_lim(LimbScheme s, uint32_t p, int64_t lim) {
   int64_t c = (p - 1) / 2;                       // centered |x| <= c
   if (s == LIMB_S8) return lim / (c * c);
   if (s == LIMB_K7) {

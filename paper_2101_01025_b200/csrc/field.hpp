@@ -33,5 +33,8 @@ int limb_planes(LimbScheme s);       // int8 planes per operand
 int limb_accs(LimbScheme s);         // TMEM accumulators per output tile
 // largest inner dimension one int32 accumulation segment may take without overflow
 int64_t limb_kmax(LimbScheme s, uint32_t p);
+// the same bound when every accumulation starts from a residue < p (the wide-N leaf's Horner
+// values in TMEM): k * max|term| + p <= 2^31 - 1
+int64_t limb_kmax_from_residue(LimbScheme s, uint32_t p);
 
 }  // namespace adj

@@ -8,6 +8,7 @@ namespace adj {
 
 cudaError_t launch_fixup(const LeafParams &p, const FixupTile *tiles, int n, cudaStream_t s);
 cudaError_t launch_leaf2(const LeafParams &p, int nacc, bool segmented, int grid, cudaStream_t s);  // CTA-pair, 256x256 tiles
+cudaError_t launch_leafw(const LeafParams &p, int nacc, int grid, cudaStream_t s);                  // CTA-pair, 256x512 tiles
 cudaError_t launch_preadd(const PreParams &p, cudaStream_t s);
 cudaError_t launch_preadd2(const PreParams &l1, const PreParams &l2, cudaStream_t s);   // fused K1 of levels 1 + 2
 cudaError_t launch_split(const SplitParams &p, cudaStream_t s);

@@ -506,6 +506,353 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (ADJ_EPI_WARPS 
   }
 }
 
+// ============================================================================ wide-N leaf (256 x 512)
+// The same CTA-pair tcgen05 kind::i8 leaf with 256 x 512 output tiles: each k-block stage holds the
+// A tile (128 rows per CTA) and two B tiles (the two N = 256 halves), and the MMA thread issues
+// both halves against the one A tile, so A is staged once per 2 x 256 x 256 MACs: 25% fewer
+// operand bytes per MAC through L2, the crossbar and shared memory than 256 x 256 tiles.  Under
+// the board's power cap the operand stream is about a third of the leaf's energy per MAC (DESIGN
+// §5), so the bytes buy clock.  The accumulator takes all 512 TMEM columns (two 256-column halves),
+// so the limb accumulators of a tile cannot alternate between slots; instead the recombination
+// runs Horner-style in TMEM: after unit u (accumulator j, K segment) the epilogue replaces each
+// value t by t * h_u mod p (h_u = w_j / w_{j+1}, or 1 between K segments of one accumulator) and
+// stores it back (tcgen05.st), the next unit accumulates on top of it, and the last unit's drain
+// multiplies by w_last and writes the residue:  sum_u w_u a_u = w_last (a_last + h (a_prev + ...)).
+// No shared-memory partial sums.  The MMA thread hides the drain behind the halves: the first
+// H stages of a unit run half 0 only (half 1 is still being drained), the last T stages run
+// half 0 first and commit it, so half 0's drain overlaps half 1's last MMAs.
+template <int NACC, int EW_ = 8>
+struct LeafWCfg {
+  static constexpr int STAGES = 4;
+  static constexpr int A_BYTES = 128 * kBK;
+  static constexpr int B_BYTES = 128 * kBK;          // one N = 256 half: 128 rows per CTA
+  static constexpr int STAGE_BYTES = A_BYTES + 2 * B_BYTES;
+  static constexpr int JQ = 4;
+  static constexpr int BAR_BYTES = 8 * (2 * STAGES + 4 + 2 * JQ) + 16 + 8 * JQ;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + BAR_BYTES;
+  static constexpr int EPI_WARPS = EW_;              // 4 TMEM lane quadrants x 2 column halves x EW_ / 8 column parts
+  static constexpr int THREADS = 32 * (EPI_WARPS + 3);
+  static constexpr int EDGE = STAGES - 1;            // H = T: stages run half-0-first at a unit's edges
+};
+
+template <int NACC, bool WIDE, int EWN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (EWN + 3), 1)
+    leafw_kernel(const __grid_constant__ LeafParams P) {
+  using Cfg = LeafWCfg<NACC, EWN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t *full_bar = reinterpret_cast<uint64_t *>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+  uint64_t *empty_bar = full_bar + Cfg::STAGES;
+  uint64_t *acc_full = empty_bar + Cfg::STAGES;     // [2]: MMA -> epilogue, one per N half
+  uint64_t *acc_empty = acc_full + 2;               // [2]: epilogue -> MMA (leader CTA)
+  uint64_t *jq_full = acc_empty + 2;
+  uint64_t *jq_empty = jq_full + Cfg::JQ;
+  uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(jq_empty + Cfg::JQ);
+  uint2 *jq = reinterpret_cast<uint2 *>(tmem_holder + 4);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = ptx::cluster_ctarank();
+  const bool leader = rank == 0;
+  const int cid = (int)ptx::cluster_id_x();
+  const int ncl = (int)ptx::num_clusters_x();
+  constexpr int EW = Cfg::EPI_WARPS;
+  constexpr int W_ALLOC = EW, W_MMA = EW + 1, W_TMA = EW + 2;
+  if (warp == W_TMA && lane == 0) {
+    for (int s = 0; s < Cfg::STAGES; ++s) {
+      ptx::mbar_init(&full_bar[s], 1);
+      ptx::mbar_init(&empty_bar[s], 1);
+    }
+    for (int h = 0; h < 2; ++h) {
+      ptx::mbar_init(&acc_full[h], 1);
+      ptx::mbar_init(&acc_empty[h], 2 * (EW / 2));   // the EW / 2 warps of half h in both CTAs
+    }
+    for (int s = 0; s < Cfg::JQ; ++s) {
+      ptx::mbar_init(&jq_full[s], 1);
+      ptx::mbar_init(&jq_empty[s], 2 + 2 * EW);
+    }
+    ptx::fence_barrier_init();
+    for (int i = 0; i < kMaxMaps; ++i) ptx::prefetch_tmap(&P.maps[i]);
+  }
+  if (warp == W_ALLOC) ptx::tmem_alloc_2sm(tmem_holder, 512);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::cluster_sync();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  const bool dyn = P.job_counter != nullptr;
+  constexpr uint32_t kEnd = 0xFFFFFFFFu;
+  auto job_consume = [&](int i, bool remote_release) -> uint2 {
+    const int s = i & (Cfg::JQ - 1);
+    ptx::mbar_wait_cluster(&jq_full[s], (uint32_t)(i / Cfg::JQ) & 1);
+    const volatile uint32_t *src = reinterpret_cast<volatile uint32_t *>(&jq[s]);
+    const uint2 d = make_uint2(src[0], src[1]);
+    const uint32_t e = ptx::smem_u32(&jq_empty[s]);
+    if (remote_release) ptx::mbar_arrive_cluster_release(ptx::mapa(e, 0));
+    else ptx::mbar_arrive(&jq_empty[s]);
+    return d;
+  };
+
+  if (warp == W_TMA) {
+    // ------------------------------------------------------------ TMA producer (both CTAs)
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      uint2 next = (!dyn && cid < P.n_tiles) ? __ldg(&P.tiles[cid]) : make_uint2(0u, 0u);
+      int idx2 = 0;
+      uint2 d1 = make_uint2(kEnd, 0u);
+      if (dyn && leader) {
+        const int idx1 = atomicAdd(P.job_counter, 1);
+        idx2 = atomicAdd(P.job_counter, 1);
+        if (idx1 < P.n_tiles) d1 = __ldg(&P.tiles[idx1]);
+      }
+      for (int i = 0;; ++i) {
+        int t = 0;
+        if (!dyn) {
+          t = cid + i * ncl;
+          if (t >= P.n_tiles) break;
+        } else if (leader) {
+          const int s = i & (Cfg::JQ - 1);
+          ptx::mbar_wait_cluster(&jq_empty[s], ((uint32_t)(i / Cfg::JQ) & 1) ^ 1);
+          next = d1;
+          jq[s] = next;
+          const uint32_t peer = ptx::mapa(ptx::smem_u32(&jq[s]), 1);
+          ptx::st_shared_cluster_u32(peer, next.x);
+          ptx::st_shared_cluster_u32(peer + 4, next.y);
+          ptx::mbar_arrive(&jq_full[s]);
+          ptx::mbar_arrive_cluster_release(ptx::mapa(ptx::smem_u32(&jq_full[s]), 1));
+          if (next.x == kEnd) break;
+          d1 = idx2 < P.n_tiles ? __ldg(&P.tiles[idx2]) : make_uint2(kEnd, 0u);
+          idx2 = atomicAdd(P.job_counter, 1);
+        } else {
+          next = job_consume(i, true);
+          if (next.x == kEnd) break;
+        }
+        int q, I, J;
+        decode_tile(next.x, q, I, J);
+        if (!dyn && t + ncl < P.n_tiles) next = __ldg(&P.tiles[t + ncl]);
+        const LeafProduct &pr = P.prod[q];
+        const CUtensorMap *map = &P.maps[pr.map];
+        const int kseg = pr.kseg, kblocks = pr.kblocks;
+        const int a_pr = pr.a_plane_rows, b_pr = pr.b_plane_rows;
+        const int arow = pr.a_row0 + I * 256 + (int)rank * 128;
+        const int brow = pr.b_row0 + J * 512 + (int)rank * 128;   // half h: + h * 256
+        const int nseg = (kblocks + kseg - 1) / kseg;
+#pragma unroll 1
+        for (int u = 0; u < NACC * nseg; ++u) {
+          const int j = u / nseg, kb0 = (u % nseg) * kseg;
+          const int kb1 = min(kblocks, kb0 + kseg);
+          const int t0 = P.acc_begin[j], nt = P.acc_begin[j + 1] - t0;
+          const int ar0 = arow + P.terms[t0].a_plane * a_pr, br0 = brow + P.terms[t0].b_plane * b_pr;
+          const int ar1 = nt > 1 ? arow + P.terms[t0 + 1].a_plane * a_pr : ar0;
+          const int br1 = nt > 1 ? brow + P.terms[t0 + 1].b_plane * b_pr : br0;
+#pragma unroll 1
+          for (int kb = kb0; kb < kb1; ++kb) {
+#pragma unroll 1
+            for (int tt = 0; tt < nt; ++tt) {
+              ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
+              if (leader) ptx::mbar_expect_tx(&full_bar[stage], 2 * Cfg::STAGE_BYTES);
+              uint8_t *sa = smem + stage * Cfg::STAGE_BYTES;
+              const int br = tt ? br1 : br0;
+              ptx::tma_load_2d_2sm(sa, map, kb * kBK, tt ? ar1 : ar0, &full_bar[stage]);
+              ptx::tma_load_2d_2sm(sa + Cfg::A_BYTES, map, kb * kBK, br, &full_bar[stage]);
+              ptx::tma_load_2d_2sm(sa + Cfg::A_BYTES + Cfg::B_BYTES, map, kb * kBK, br + 256, &full_bar[stage]);
+              if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == W_MMA) {
+    // ------------------------------------------------------------ MMA issuer (leader CTA, one thread)
+    if (leader && lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      uint32_t unit = 0;   // units issued so far (acc_empty / acc_full phases: both halves per unit)
+      const uint32_t smem_base = ptx::smem_u32(smem);
+      uint2 next = (!dyn && cid < P.n_tiles) ? __ldg(&P.tiles[cid]) : make_uint2(0u, 0u);
+      for (int i = 0;; ++i) {
+        int t;
+        if (!dyn) {
+          t = cid + i * ncl;
+          if (t >= P.n_tiles) break;
+        } else {
+          next = job_consume(i, false);
+          if (next.x == kEnd) break;
+        }
+        int q, I, J;
+        decode_tile(next.x, q, I, J);
+        if (!dyn && t + ncl < P.n_tiles) next = __ldg(&P.tiles[t + ncl]);
+        const LeafProduct &pr = P.prod[q];
+        const int kseg = pr.kseg, kblocks = pr.kblocks;
+        const int nseg = (kblocks + kseg - 1) / kseg;
+#pragma unroll 1
+        for (int u = 0; u < NACC * nseg; ++u, ++unit) {
+          const int j = u / nseg, kb0 = (u % nseg) * kseg;
+          const int kb1 = min(kblocks, kb0 + kseg);
+          const int t0 = P.acc_begin[j], nt = P.acc_begin[j + 1] - t0;
+          const uint32_t id0 = ptx::idesc_i8(256, 256, P.terms[t0].a_signed != 0, P.terms[t0].b_signed != 0);
+          const uint32_t id1 = nt > 1 ? ptx::idesc_i8(256, 256, P.terms[t0 + 1].a_signed != 0,
+                                                      P.terms[t0 + 1].b_signed != 0) : id0;
+          const int nst = (kb1 - kb0) * nt;                      // stages of this unit
+          const int edge = min(Cfg::EDGE, nst / 2);              // H = T
+          // the first unit of a job starts from zero; later ones accumulate onto the Horner value
+          uint32_t acc0 = u > 0 ? 1u : 0u, acc1 = acc0;
+          auto issue = [&](int h, uint32_t sa, uint32_t idesc, uint32_t &acc) {
+            const uint64_t adesc = ptx::smem_desc_sw128(sa);
+            const uint64_t bdesc = ptx::smem_desc_sw128(sa + Cfg::A_BYTES + h * Cfg::B_BYTES);
+#pragma unroll
+            for (int kk = 0; kk < kBK / 32; ++kk) {
+              ptx::mma_i8_2sm(tmem_base + h * 256, adesc + 2 * kk, bdesc + 2 * kk, idesc, acc);
+              acc = 1;
+            }
+          };
+          // head: half 0 on the first `edge` stages while half 1 of the previous unit drains
+          ptx::mbar_wait_cluster(&acc_empty[0], (unit & 1) ^ 1);
+          ptx::tc_fence_after();
+          int st = stage;
+          uint32_t ph = phase;
+          for (int x = 0; x < edge; ++x) {
+            ptx::mbar_wait(&full_bar[st], ph);
+            ptx::tc_fence_after();
+            issue(0, smem_base + st * Cfg::STAGE_BYTES, (x % nt) ? id1 : id0, acc0);
+            if (++st == Cfg::STAGES) { st = 0; ph ^= 1; }
+          }
+          ptx::mbar_wait_cluster(&acc_empty[1], (unit & 1) ^ 1);
+          ptx::tc_fence_after();
+          for (int x = 0; x < edge; ++x) {
+            issue(1, smem_base + stage * Cfg::STAGE_BYTES, (x % nt) ? id1 : id0, acc1);
+            ptx::mma_commit_2sm(&empty_bar[stage], 0x3);
+            if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
+          }
+          // body: both halves per stage
+          for (int x = edge; x < nst - edge; ++x) {
+            ptx::mbar_wait(&full_bar[stage], phase);
+            ptx::tc_fence_after();
+            const uint32_t sa = smem_base + stage * Cfg::STAGE_BYTES;
+            const uint32_t idesc = (x % nt) ? id1 : id0;
+            issue(0, sa, idesc, acc0);
+            issue(1, sa, idesc, acc1);
+            ptx::mma_commit_2sm(&empty_bar[stage], 0x3);
+            if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
+          }
+          // tail: half 0 on the last `edge` stages and its commit, then half 1
+          st = stage;
+          ph = phase;
+          for (int x = nst - edge; x < nst; ++x) {
+            ptx::mbar_wait(&full_bar[st], ph);
+            ptx::tc_fence_after();
+            issue(0, smem_base + st * Cfg::STAGE_BYTES, (x % nt) ? id1 : id0, acc0);
+            if (++st == Cfg::STAGES) { st = 0; ph ^= 1; }
+          }
+          ptx::mma_commit_2sm(&acc_full[0], 0x3);
+          for (int x = nst - edge; x < nst; ++x) {
+            issue(1, smem_base + stage * Cfg::STAGE_BYTES, (x % nt) ? id1 : id0, acc1);
+            ptx::mma_commit_2sm(&empty_bar[stage], 0x3);
+            if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
+          }
+          ptx::mma_commit_2sm(&acc_full[1], 0x3);
+        }
+      }
+    }
+  } else if (warp < EW) {
+    // ------------------------------------------------------------ epilogue (8 warps per CTA)
+    constexpr int NPART = EW / 8;     // column parts per half
+    constexpr int NCH = 8 / NPART;    // 32-column chunks per warp and unit
+    const int q4 = warp & 3;          // TMEM lane quadrant
+    const int h = (warp >> 2) & 1;    // N half: TMEM columns h * 256 .. + 255
+    const int part = warp >> 3;       // columns part * NCH * 32 .. of the half
+    const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
+    const int lrow = q4 * 32 + lane;
+    const ModP mod = P.mod;
+    const uint32_t pm = mod.p;
+    const uint32_t empty_remote = ptx::mapa(ptx::smem_u32(&acc_empty[h]), 0);
+    uint32_t unit = 0;
+    for (int i = 0;; ++i) {
+      uint2 job = make_uint2(0u, 0u);
+      if (!dyn) {
+        const int t = cid + i * ncl;
+        if (t >= P.n_tiles) break;
+        job = P.tiles[t];
+      } else {
+        if (lane == 0) job = job_consume(i, !leader);
+        job.x = __shfl_sync(0xFFFFFFFFu, job.x, 0);
+        job.y = __shfl_sync(0xFFFFFFFFu, job.y, 0);
+        if (job.x == kEnd) break;
+      }
+      int q, I, J;
+      decode_tile(job.x, q, I, J);
+      const LeafProduct &pr = P.prod[q];
+      const int64_t row = (int64_t)I * 256 + rank * 128 + lrow;
+      const int64_t col0 = (int64_t)J * 512 + h * 256 + part * NCH * 32;
+      const int nseg = (pr.kblocks + pr.kseg - 1) / pr.kseg;
+      const int nunits = NACC * nseg;
+#pragma unroll 1
+      for (int u = 0; u < nunits; ++u, ++unit) {
+        const int j = u / nseg;
+        const bool last = u == nunits - 1;
+        // Horner step: the last unit's weight, 1 between K segments, w_j / w_{j+1} between accumulators
+        const ShoupW w = last ? P.wshoup[j] : ((u + 1) % nseg ? P.one : P.hshoup[j]);
+        ptx::mbar_wait(&acc_full[h], unit & 1);
+        ptx::tc_fence_after();
+        // a diagonal SYRK tile whose columns all lie above this CTA half's rows needs no drain
+        // of its values, but its TMEM is still released below
+#pragma unroll 1
+        for (int c = 0; c < NCH; ++c) {
+          uint32_t v[32];
+          const uint32_t taddr = tmem_base + lane_off + h * 256 + (part * NCH + c) * 32;
+          ptx::tmem_ld32(taddr, v);
+          ptx::tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) v[e] = acc_mulred((int32_t)v[e], w.wc, w.wq, 0u, pm);
+          if (last) store_chunk(pr, row, col0 + c * 32, v, mod);
+          else ptx::tmem_st32(taddr, v);
+        }
+        if (!last) ptx::tmem_wait_st();
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_cluster(empty_remote);
+      }
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::cluster_sync();
+  if (warp == W_ALLOC) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc_2sm(tmem_base, 512);
+  }
+}
+
+template <int NACC, bool WIDE, int EWN>
+static cudaError_t launch_leafw_t(const LeafParams &p, int grid, cudaStream_t s) {
+  using Cfg = LeafWCfg<NACC, EWN>;
+  static std::atomic<uint64_t> done{0};
+  cudaError_t e = ensure_smem(leafw_kernel<NACC, WIDE, EWN>, Cfg::SMEM, done);
+  if (e != cudaSuccess) return e;
+  leafw_kernel<NACC, WIDE, EWN><<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_leafw(const LeafParams &p, int nacc, int grid, cudaStream_t s) {
+  if (p.n_tiles == 0) return cudaSuccess;
+  if (grid % 2) return cudaErrorInvalidValue;
+  // 8 epilogue warps (16 measured the same at c3 / c4: the drain is not the limit); ADJ_LEAFW_EPI=16 (A/B)
+  static const int ew = getenv("ADJ_LEAFW_EPI") ? atoi(getenv("ADJ_LEAFW_EPI")) : 8;
+  if (ew == 8) {
+    if (nacc == 1) return launch_leafw_t<1, false, 8>(p, grid, s);
+    if (nacc == 3) return launch_leafw_t<3, false, 8>(p, grid, s);
+    if (nacc == 6) return launch_leafw_t<6, true, 8>(p, grid, s);
+    return cudaErrorInvalidValue;
+  }
+  if (nacc == 1) return launch_leafw_t<1, false, 16>(p, grid, s);
+  if (nacc == 3) return launch_leafw_t<3, false, 16>(p, grid, s);
+  if (nacc == 6) return launch_leafw_t<6, true, 16>(p, grid, s);
+  return cudaErrorInvalidValue;
+}
+
 template <int NACC, bool PART, bool WIDE>
 static cudaError_t launch_leaf2_t(const LeafParams &p, int grid, cudaStream_t s) {
   using Cfg = Leaf2Cfg<NACC, PART, WIDE>;

@@ -166,8 +166,47 @@ static void split_tail(Plan &P, int ncl) {
   P.tiles.swap(out);
 }
 
+// Wide-N leaf (leafw_kernel: 256 x 512 tiles, 25% fewer operand bytes per MAC, the limb
+// recombination Horner-style in TMEM) for long launches (> 16 waves of wide jobs, where the
+// static tail of the last wave is small without splitting).  Needs every limb weight invertible
+// mod p (the Horner steps are w_j / w_{j+1}) and K segments bounded for accumulations that start
+// from a residue < p.  Not for shard plans (their ownership is in 256 x 256 tiles).
+static uint32_t powmod(uint64_t b, uint64_t e, uint32_t p) {
+  uint64_t r = 1;
+  b %= p;
+  for (; e; e >>= 1, b = b * b % p)
+    if (e & 1) r = r * b % p;
+  return (uint32_t)r;
+}
+static void choose_wide(Plan &P, int num_sms) {
+  P.wide = false;
+  P.tile_n = 256;
+  // ADJ_LEAF_WIDE (diagnostics, A/B): 0 off, 1 long launches (default), 2 always
+  static const int env = getenv("ADJ_LEAF_WIDE") ? atoi(getenv("ADJ_LEAF_WIDE")) : 1;
+  if (env == 0) return;
+  LeafParams &L = P.leaf_template;
+  for (int j = 0; j < P.nacc; ++j)
+    if (L.weight[j] % P.p == 0) return;
+  int64_t nt = 0;
+  for (const ProductPlan &pp : P.prods) {
+    const int64_t tm = cdiv(pp.lp.out_rows, 256), tn = cdiv(pp.lp.out_cols, 512);
+    for (int64_t I = 0; I < tm; ++I)
+      for (int64_t J = 0; J < tn; ++J)
+        if (!pp.lp.sym || J * 512 <= I * 256 + 255) ++nt;
+  }
+  if (env != 2 && nt <= 16 * (int64_t)(num_sms / 2)) return;
+  const int kseg = (int)std::max<int64_t>(1, limb_kmax_from_residue((LimbScheme)P.scheme, P.p) / kBK);
+  P.wide = true;
+  P.tile_n = 512;
+  P.kseg = kseg;
+  for (ProductPlan &pp : P.prods) pp.lp.kseg = kseg;
+  for (int j = 0; j + 1 < P.nacc; ++j)
+    L.hshoup[j] = make_shoup((uint32_t)((uint64_t)L.weight[j] * powmod(L.weight[j + 1], P.p - 2, P.p) % P.p), P.p);
+  L.one = make_shoup(1, P.p);
+}
+
 static void set_grid(Plan &P, int num_sms) {
-  split_tail(P, num_sms / 2);
+  if (!P.wide) split_tail(P, num_sms / 2);
   P.fixup_offset = P.ws_bytes;
   // the tail never has more pieces than clusters (pieces = ncl / rem per tail tile): reserve the
   // worst case, so the size does not depend on the tile list (a shard's filtered list fits the
@@ -474,6 +513,7 @@ bool build_syrk_plan(Plan &P, int64_t m, int64_t k, uint32_t p, int phi, int dep
     }
   }
   if ((int)P.prods.size() > kMaxProducts) { *err = "too many leaf products"; return false; }
+  if (shard_n == 0) choose_wide(P, num_sms);
   append_tiles(P);
   if (shard_n > 0 && !apply_shard(P, shard_rank, shard_n, err)) return false;
   set_grid(P, num_sms);

@@ -86,6 +86,7 @@ struct Plan {
   int n_pieces = 0;
   int grid = 1;
   bool dynamic = false;              // leaf jobs claimed with an atomic counter (long launches)
+  bool wide = false;                 // 256 x 512 leaf tiles (leafw_kernel, Horner recombination in TMEM)
   int dev = 0;
   LeafParams leaf_template;           // terms, weights, mod (maps/outs bound per call)
   // output-tile sharding (adjprod_modp_shard): this plan computes only the tiles `shard_rank` owns

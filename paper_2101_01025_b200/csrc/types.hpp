@@ -55,6 +55,8 @@ struct LeafParams {
   LeafTerm terms[8];
   uint32_t weight[6];      // residue weight of each accumulator in the limb recombination
   ShoupW wshoup[6];        // the same weights as Shoup pairs (centered weight, floor(w 2^32 / p))
+  ShoupW hshoup[6];        // wide-N leaf (Horner in TMEM): w_j / w_{j+1} mod p, the step to the next accumulator
+  ShoupW one;              // Shoup pair of 1 (the step between K segments of one accumulator)
   int32_t fixup32;         // fixup slots hold uint32 residues (p > 2^16) instead of uint16
   int32_t *job_counter;    // dynamic scheduling: next job index (zeroed before the launch); null = static
   int32_t debug;           // diagnostics only (ADJ_LEAF_DEBUG): 1 no TMA, 2 no epilogue, 8 no math, 16 no tcgen05.ld,
