@@ -812,6 +812,10 @@ def run_gpu(args, cfg, rank, world, local_rank):
 
     # ---------------- roofline of the dominant kernel (grouped tcgen05 leaf launch)
     peaks, src = load_peaks()
+    try:   # which leaf kernel the timed call launches (256 x 256 or the wide 256 x 512 tiles)
+        leaf_tile = adj.adjprod_modp_leaf_tile(m, k, p, phi, depth, flags) if world == 1 else 256
+    except Exception:  # noqa: BLE001 -- label only
+        leaf_tile = None
     leaf_ms, leaf_n = prof_all["leaf"]
     # one grouped leaf stage per step: the tcgen05 leaf launch (+ its tail fixup launch, if any)
     leaf_avg_ms = leaf_ms / args.steps
@@ -827,7 +831,9 @@ def run_gpu(args, cfg, rank, world, local_rank):
     peak = 2.0 * bf16
     roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
             "traffic": load_traffic(args.config, depth),
-            "kernel": "leaf_kernel (grouped tcgen05 kind::i8 GEMM/SYRK + mod-p epilogue)",
+            "kernel": ("leafw_kernel (grouped tcgen05 kind::i8 GEMM/SYRK on 256 x 512 tiles, Horner mod-p "
+                       "recombination in TMEM)" if leaf_tile == 512 else
+                       "leaf2_kernel (grouped tcgen05 kind::i8 GEMM/SYRK on 256 x 256 tiles + mod-p epilogue)"),
             "peak_source": (f"{src}: 2 x bf16_tflops{'_sustained' if capped else ''} ({bf16}) "
                             f"{'sustained: the board was at its power cap (sw_power_cap) during the timed steps' if capped else 'burst'}"
                             f", int8 = 2x bf16 nominal; of burst (2 x {peaks['bf16_tflops']}): "

@@ -165,6 +165,12 @@ adj_status_t adjprod_modp_workspace_size(int64_t m, int64_t k, uint32_t p, adj_p
 adj_status_t adjprod_modp_auto_depth(int64_t m, int64_t k, uint32_t p, adj_phi_t phi,
                                      int *depth);
 
+/* Output-tile width of the grouped leaf launch this call would use (host, no device work):
+ * 512 for the wide-N leaf (256 x 512 CTA-pair tiles, Horner recombination in TMEM; launches of
+ * more than 16 waves), 256 otherwise.  Same arguments and errors as the workspace query. */
+adj_status_t adjprod_modp_leaf_tile(int64_t m, int64_t k, uint32_t p, adj_phi_t phi,
+                                    const adj_opts_t *opts, int *tile_n);
+
 /*
  * gemm_modp -- C = A B^T mod p over GF(p), all of C (m x n).  The paper's general product
  *   A phi(B) (P3, P4 of Alg. alg:MIAHMM) exposed on its own.

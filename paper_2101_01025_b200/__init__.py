@@ -9,10 +9,10 @@ from __future__ import annotations
 
 from ._lib import (ADJ_IN_U16, ADJ_OUT_U16, ADJ_LOW_MEM, ADJ_DIST_P2P, ADJ_DIST_TILES, ADJ_FILL_UPPER, ADJ_HERK_ALG1, ADJ_PHI_H, ADJ_PHI_Q, ADJ_PHI_T, AdjError, adj_comm_destroy, adj_comm_get_unique_id,
                    adj_comm_init, adj_launch_count, adj_launch_count_reset, adj_mod_lower, adj_profile_enable, adj_profile_read, adj_skew_unitary, adj_sos,
-                   adj_dist_kslice, adj_elem_bytes, adj_shard_layout, adj_shard_rows, adjprod_modp_dist_partial, adj_shard_pack, adj_ipc_export, adj_ipc_open, adj_ipc_close, adj_sum_partials, adjprod_modp, adjprod_modp_partial, adjprod_modp_shard, adjprod_modp_auto_depth, adjprod_modp_dist, adjprod_modp_ex, adjprod_modp_syrk,
+                   adj_dist_kslice, adj_elem_bytes, adj_shard_layout, adj_shard_rows, adjprod_modp_dist_partial, adj_shard_pack, adj_ipc_export, adj_ipc_open, adj_ipc_close, adj_sum_partials, adjprod_modp, adjprod_modp_partial, adjprod_modp_shard, adjprod_modp_auto_depth, adjprod_modp_leaf_tile, adjprod_modp_dist, adjprod_modp_ex, adjprod_modp_syrk,
                    adjprod_modp_workspace_size, gemm_modp, lib)
 
-__all__ = ["ADJ_IN_U16", "ADJ_OUT_U16", "ADJ_LOW_MEM", "adj_shard_pack", "adj_ipc_export", "adj_ipc_open", "adj_ipc_close", "ADJ_DIST_P2P", "adjprod_modp_partial", "adj_sum_partials", "ADJ_DIST_TILES", "adjprod_modp_shard", "adj_shard_layout", "ADJ_PHI_T", "ADJ_PHI_H", "ADJ_PHI_Q", "ADJ_FILL_UPPER", "ADJ_HERK_ALG1", "AdjError", "adjprod_modp", "adjprod_modp_ex", "adjprod_modp_syrk",
+__all__ = ["ADJ_IN_U16", "ADJ_OUT_U16", "ADJ_LOW_MEM", "adj_shard_pack", "adj_ipc_export", "adj_ipc_open", "adj_ipc_close", "ADJ_DIST_P2P", "adjprod_modp_partial", "adj_sum_partials", "ADJ_DIST_TILES", "adjprod_modp_shard", "adj_shard_layout", "ADJ_PHI_T", "ADJ_PHI_H", "ADJ_PHI_Q", "ADJ_FILL_UPPER", "ADJ_HERK_ALG1", "AdjError", "adjprod_modp", "adjprod_modp_ex", "adjprod_modp_syrk", "adjprod_modp_leaf_tile",
            "adjprod_modp_workspace_size", "adjprod_modp_auto_depth", "gemm_modp", "adj_skew_unitary", "adj_sos",
            "adj_mod_lower", "adj_dist_kslice", "adj_elem_bytes", "adj_shard_rows", "adjprod_modp_dist_partial", "adj_comm_get_unique_id", "adj_comm_init", "adj_comm_destroy", "adjprod_modp_dist",
            "adj_launch_count", "adj_launch_count_reset", "adj_profile_enable", "adj_profile_read", "lib", "adjprod", "gemm"]

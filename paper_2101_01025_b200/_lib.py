@@ -26,7 +26,7 @@ STATUS = {0: "ADJ_OK", 1: "ADJ_ERR_INVALID_VALUE", 2: "ADJ_ERR_UNSUPPORTED_MODUL
           4: "ADJ_ERR_CUDA", 5: "ADJ_ERR_NCCL", 6: "ADJ_ERR_ARCH"}
 
 # every symbol include/adjprod.h declares (checked by tests/test_abi.py)
-EXPORTS = ["adjprod_modp", "adjprod_modp_ex", "adjprod_modp_syrk", "adjprod_modp_workspace_size", "adjprod_modp_auto_depth",
+EXPORTS = ["adjprod_modp", "adjprod_modp_ex", "adjprod_modp_syrk", "adjprod_modp_workspace_size", "adjprod_modp_auto_depth", "adjprod_modp_leaf_tile",
            "gemm_modp", "adj_skew_unitary", "adj_sos", "adj_mod_lower", "adj_comm_get_unique_id",
            "adj_comm_init", "adj_comm_destroy", "adjprod_modp_dist", "adj_dist_kslice", "adj_elem_bytes", "adjprod_modp_dist_partial", "adjprod_modp_shard", "adj_shard_layout", "adj_shard_rows", "adjprod_modp_partial", "adj_sum_partials", "adj_shard_pack", "adj_ipc_export", "adj_ipc_open", "adj_ipc_close", "adj_status_string", "adj_last_error",
            "adj_launch_count", "adj_launch_count_reset", "adj_profile_enable", "adj_profile_read"]
@@ -60,6 +60,7 @@ def lib() -> ctypes.CDLL:
             "adjprod_modp_workspace_size": [i64, i64, u32, ci, ctypes.POINTER(adj_opts_t),
                                             ctypes.POINTER(ctypes.c_size_t)],
             "adjprod_modp_auto_depth": [i64, i64, u32, ci, ctypes.POINTER(ci)],
+            "adjprod_modp_leaf_tile": [i64, i64, u32, ci, ctypes.POINTER(adj_opts_t), ctypes.POINTER(ci)],
             "gemm_modp": [i64, i64, i64, u32, vp, i64, vp, i64, vp, i64, vp],
             "adj_skew_unitary": [u32, ci, ctypes.POINTER(ci), ctypes.POINTER(u32), ctypes.POINTER(u32)],
             "adj_sos": [u32, u32, ctypes.POINTER(u32), ctypes.POINTER(u32)],
@@ -155,6 +156,13 @@ def adjprod_modp_auto_depth(m, k, p, phi) -> int:
     d = ctypes.c_int(0)
     _check(lib().adjprod_modp_auto_depth(m, k, p, phi, ctypes.byref(d)), "adjprod_modp_auto_depth")
     return d.value
+
+
+def adjprod_modp_leaf_tile(m, k, p, phi, depth=-1, flags=0) -> int:
+    o = _opts(depth, flags)
+    t = ctypes.c_int(0)
+    _check(lib().adjprod_modp_leaf_tile(m, k, p, phi, ctypes.byref(o), ctypes.byref(t)), "adjprod_modp_leaf_tile")
+    return t.value
 
 
 def gemm_modp(m, n, k, p, A, lda, B, ldb, C, ldc, stream=None):

@@ -840,6 +840,27 @@ adj_status_t adjprod_modp_workspace_size(int64_t m, int64_t k, uint32_t p, adj_p
   return ADJ_OK;
 }
 
+adj_status_t adjprod_modp_leaf_tile(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, const adj_opts_t *opts,
+                                    int *tile_n) {
+  if (!tile_n) return fail(ADJ_ERR_INVALID_VALUE, "null output");
+  if (m < 0 || k < 0) return fail(ADJ_ERR_INVALID_VALUE, "negative dimension");
+  if (!valid_modulus(p)) return fail(ADJ_ERR_UNSUPPORTED_MODULUS, "p=%u is not an odd prime in [3, 262139]", p);
+  *tile_n = 256;
+  if (m == 0 || k == 0) return ADJ_OK;
+  const bool herk1 = phi == ADJ_PHI_H && opts && (opts->flags & ADJ_HERK_ALG1);
+  const int depth = (opts && opts->depth >= 0) ? opts->depth : (herk1 ? 1 : auto_depth(m, k, p, (int)phi));
+  Plan P;
+  const char *err = nullptr;
+  const int sms = query_sms();
+  const bool lowmem = opts && (opts->flags & ADJ_LOW_MEM) && phi == ADJ_PHI_T && lowmem_shape_ok(m, k, depth);
+  if (!(herk1    ? build_herk1_plan(P, m, k, p, sms, &err)
+        : lowmem ? build_lowmem_plan(P, m, k, p, depth, sms, &err)
+                 : build_syrk_plan(P, m, k, p, (int)phi, depth, sms, &err)))
+    return fail(ADJ_ERR_INVALID_VALUE, "plan: %s", err ? err : "unsupported");
+  *tile_n = P.tile_n;
+  return ADJ_OK;
+}
+
 static adj_status_t adjprod_impl(int64_t m, int64_t k, uint32_t p, adj_phi_t phi, uint32_t alpha, const uint32_t *A,
                                  int64_t lda, uint32_t beta, uint32_t *C, int64_t ldc, const adj_opts_t *opts,
                                  cudaStream_t s) {

@@ -274,3 +274,16 @@ def test_ipc_validation_needs_no_gpu():
     with pytest.raises(adj.AdjError) as e:
         adj.adj_ipc_close(0x1000)                                     # never opened
     assert e.value.status == 1
+
+
+def test_leaf_tile_query():
+    """The wide-N leaf (256 x 512 tiles) serves long launches only: c3 / c4 (the metric's configs)
+    use it, c2 and the small configs keep 256 x 256 tiles with their tail balancing."""
+    assert adj.adjprod_modp_leaf_tile(32768, 32768, 65521, 0) == 512       # c3, depth 2
+    assert adj.adjprod_modp_leaf_tile(16384, 131072, 8191, 0) == 512      # c4, depth 2
+    assert adj.adjprod_modp_leaf_tile(8192, 8192, 8191, 0) == 256         # c2
+    assert adj.adjprod_modp_leaf_tile(256, 256, 97, 0, depth=1) == 256     # c1
+    assert adj.adjprod_modp_leaf_tile(0, 5, 97, 0) == 256
+    with pytest.raises(adj.AdjError) as e:
+        adj.adjprod_modp_leaf_tile(4, 4, 91, 0)
+    assert e.value.status == 2

@@ -74,6 +74,9 @@ def test_whole_low_c_bench_launch(env, name):
     w = A.shape[2]
     if name == "c3":
         assert depth == 2          # the depth-2 tree the N = 1 headline times
+    if name in ("c3", "c4"):       # ... on the wide-N leaf (256 x 512 tiles, Horner in TMEM)
+        assert adj.adjprod_modp_leaf_tile(A.shape[0], A.shape[1], p, 0, depth,
+                                          adj.ADJ_IN_U16 | adj.ADJ_OUT_U16) == 512
     assert exact_low_mismatches(torch, A, C, p, w) == 0, (name, depth)
     Ah = A.cpu().numpy().view(np.uint32)
     Ch = C.cpu().numpy().view(np.uint32)
