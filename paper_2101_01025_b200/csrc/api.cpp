@@ -435,7 +435,10 @@ bool k1_fused_ok(const Plan &P, const InView &root, const uint8_t *side_arena) {
     return false;
   const LevelPlan &A = P.lv[1], &B = P.lv[2];
   return 2 * A.mh == P.m && 2 * A.kh == P.k && A.rows_pad == A.mh && A.kpad == A.kh && 2 * B.mh == A.mh &&
-         2 * B.kh == A.kh && B.rows_pad == B.mh && B.kpad == B.kh && A.kh % 16 == 0;
+         2 * B.kh == A.kh && B.rows_pad == B.mh && B.kpad == B.kh && A.kh % 16 == 0 &&
+         // 32-bit thread offsets into every level's planes (preadd.cu k1_core<O32>)
+         (int64_t)P.planes * A.rows_pad * A.kpad <= (int64_t(1) << 32) &&
+         (int64_t)P.planes * B.rows_pad * B.kpad <= (int64_t(1) << 32);
 }
 
 adj_status_t run_tree(const Plan &P, const InView &root, const Ptrs &x, cudaStream_t s,

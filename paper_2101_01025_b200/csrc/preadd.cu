@@ -195,6 +195,33 @@ __device__ __forceinline__ void put_limbs4_s8u8u(int8_t *base, int64_t plane_str
       __byte_perm(__byte_perm(c0, c1, 0x40), __byte_perm(c2, c3, 0x40), 0x5410);
 }
 
+// 4-byte global store at base + off for a 32-bit off: one IMAD.WIDE.U32 forms the address
+// (a plain pointer add of a uint32 costs two or three 32-bit adds with carries)
+__device__ __forceinline__ void st_off32(const int8_t *base, uint32_t off, uint32_t v) {
+  asm volatile("{\n\t.reg .u64 a;\n\tmad.wide.u32 a, %1, 1, %0;\n\tst.global.u32 [a], %2;\n\t}" ::"l"(base), "r"(off),
+               "r"(v));
+}
+
+// packed plane words of 4 offset residues u = c + (p - 1) / 2 (koff as for put_limbs4_*):
+//   scheme 0: byte 0 of c = u - h;  scheme 1: k7_words;
+//   scheme 2: v = u - h + 2^15 = c + 2^15 lies in [0, 2^16), so two of them packed in one word add
+//   without carries between the 16-bit lanes; byte 0 of v is the u8 lo of c, byte 1 is its s8 hi
+//   + 128 (flipped back by the xor)
+template <int SCHEME>
+__device__ __forceinline__ void limb_words_u(const uint32_t (&u)[4], uint32_t koff, uint32_t (&w)[3]) {
+  if constexpr (SCHEME == 0) {
+    w[0] = __byte_perm(__byte_perm(u[0] - koff, u[1] - koff, 0x40), __byte_perm(u[2] - koff, u[3] - koff, 0x40),
+                       0x5410);
+  } else if constexpr (SCHEME == 1) {
+    k7_words(u, koff, w);
+  } else {
+    const uint32_t K = (0x8000u - koff) * 0x10001u;
+    const uint32_t v01 = (u[0] + (u[1] << 16)) + K, v23 = (u[2] + (u[3] << 16)) + K;
+    w[0] = __byte_perm(v01, v23, 0x7531) ^ 0x80808080u;
+    w[1] = __byte_perm(v01, v23, 0x6420);
+  }
+}
+
 // the six planes of 4 offset residues u = c + (p - 1) / 2: v = u + off, off = 133152 - (p - 1) / 2
 __device__ __forceinline__ void put_limbs4_t6u(int8_t *base, int64_t plane_stride, const uint32_t (&u)[4],
                                                uint32_t off) {
@@ -358,7 +385,11 @@ __device__ __forceinline__ void put_side(const PreNode &N, int64_t R, int64_t C,
   put_limbs4<SCHEME>(N.side + (N.side_y_row + R) * N.side_kpad + C, ps, im, m);
 }
 
-template <int SCHEME, int YK>
+// O32: every plane byte offset of the launch (rows_pad * kpad * planes) fits 32 bits, so each
+// store address is one uniform operand base plus a 32-bit thread offset (the fused K1)
+// NOPS > 0: the node writes exactly operands 0 .. NOPS-1 and no S3 buffer (known at compile time:
+// the fused K1 at depth 2, where level 1 writes S1, S2, S4, X22 and level 2 all seven)
+template <int SCHEME, int YK, bool O32 = false, int NOPS = 0>
 __device__ __forceinline__ void k1_core(const PreParams &P, const PreNode &N, int64_t r, int64_t c,
                                         const uint32_t (&x11a)[4], const uint32_t (&x11b)[4],
                                         const uint32_t (&x12a)[4], const uint32_t (&x12b)[4],
@@ -470,7 +501,7 @@ __device__ __forceinline__ void preadd_row(const PreParams &P, const PreNode &N,
 // quadrants) from the canonical residues of the 8 quadrant quads.  Writes the node's limb
 // operands and, when N.s3 is set, its canonical S3; s3a / s3b (if given) receive the canonical
 // S3 residues (the fused two-level K1 keeps them in registers for the next level).
-template <int SCHEME, int YK>
+template <int SCHEME, int YK, bool O32, int NOPS>
 __device__ __forceinline__ void k1_core(const PreParams &P, const PreNode &N, int64_t r, int64_t c,
                                         const uint32_t (&x11a)[4], const uint32_t (&x11b)[4],
                                         const uint32_t (&x12a)[4], const uint32_t (&x12b)[4],
@@ -505,8 +536,20 @@ __device__ __forceinline__ void k1_core(const PreParams &P, const PreNode &N, in
                           : (SCHEME == 3 ? 133152u - (uint32_t)h : (uint32_t)h);   // (0, 2: h)
     // one row address per call; each operand adds its host-computed byte offset
     int8_t *const rc = P.arena + r * P.kpad + c;
+    // O32: 32-bit thread offsets of the (a, b) column halves in planes 0..2, shared by every operand
+    const uint32_t t0 = O32 ? (uint32_t)(r * P.kpad + c) : 0u, t1 = t0 + (uint32_t)h2;
+    const uint32_t pst = (uint32_t)ps;
 #define PUTC(o, A, B)                                                                  \
-  if (N.op_row[o] >= 0) {                                                              \
+  if (O32 && SCHEME <= 2 && (NOPS > 0 ? (o) < NOPS : N.op_row[o] >= 0)) {              \
+    int8_t *const ob = P.arena + N.op_off[o];                                          \
+    uint32_t wa[3], wb[3];                                                             \
+    limb_words_u<SCHEME>(A, koff, wa);                                                 \
+    limb_words_u<SCHEME>(B, koff, wb);                                                 \
+    _Pragma("unroll") for (int pl = 0; pl < (SCHEME == 0 ? 1 : (SCHEME == 1 ? 3 : 2)); ++pl) { \
+      st_off32(ob, t0 + pl * pst, wa[pl]);                                             \
+      st_off32(ob, t1 + pl * pst, wb[pl]);                                             \
+    }                                                                                  \
+  } else if (!(O32 && SCHEME <= 2) && N.op_row[o] >= 0) {                              \
     int8_t *b = rc + N.op_off[o];                                                      \
     if constexpr (SCHEME == 0) {                                                       \
       put_limbs4_s8u(b, A, koff);                                                      \
@@ -530,7 +573,9 @@ __device__ __forceinline__ void k1_core(const PreParams &P, const PreNode &N, in
     PUTC(OUT_X12, u12a, u12b)
     PUTC(OUT_S3, u3a, u3b)
 #undef PUTC
-    if (SCHEME == 3 && N.s3 != nullptr && r < P.mh) {   // canonical uint32 S3 for the next level
+    if (NOPS > 0) {
+      // no S3 buffer
+    } else if (SCHEME == 3 && N.s3 != nullptr && r < P.mh) {   // canonical uint32 S3 for the next level
       uint32_t *d = static_cast<uint32_t *>(N.s3) + r * N.s3_ld;
       *reinterpret_cast<uint4 *>(d + c) = make_uint4(wrap_lo(u3a[0] - (uint32_t)h), wrap_lo(u3a[1] - (uint32_t)h),
                                                      wrap_lo(u3a[2] - (uint32_t)h), wrap_lo(u3a[3] - (uint32_t)h));
@@ -647,7 +692,8 @@ __device__ __forceinline__ uint2 pack4(const uint32_t (&x)[4]) {
   return make_uint2(x[0] | (x[1] << 16), x[2] | (x[3] << 16));
 }
 
-template <int SCHEME, int YK>
+// D2: depth 2 (level 1 writes S1, S2, S4, X22, level 2 every operand, no S3 buffers)
+template <int SCHEME, int YK, bool D2>
 __global__ void __launch_bounds__(256, 2) preadd2_kernel(const __grid_constant__ Pre2Params P) {
   const PreParams &L1 = P.l1, &L2 = P.l2;
   const PreNode &N1 = L1.nodes[0];
@@ -703,7 +749,7 @@ __global__ void __launch_bounds__(256, 2) preadd2_kernel(const __grid_constant__
         unpack4(q[1][ri][j], x12a); unpack4(q[1][ri][j + 2], x12b);
         unpack4(q[2][ri][j], x21a); unpack4(q[2][ri][j + 2], x21b);
         unpack4(q[3][ri][j], x22a); unpack4(q[3][ri][j + 2], x22b);
-        k1_core<SCHEME, YK>(L1, N1, r2 + ri * L2.mh, c2 + j * kq, x11a, x11b, x12a, x12b, x21a, x21b, x22a, x22b,
+        k1_core<SCHEME, YK, true, D2 ? 4 : 0>(L1, N1, r2 + ri * L2.mh, c2 + j * kq, x11a, x11b, x12a, x12b, x21a, x21b, x22a, x22b,
                             sa, sb);
         s3[ri][j] = pack4(sa);
         s3[ri][j + 2] = pack4(sb);
@@ -715,7 +761,7 @@ __global__ void __launch_bounds__(256, 2) preadd2_kernel(const __grid_constant__
       uint32_t x11a[4], x11b[4], x12a[4], x12b[4], x21a[4], x21b[4], x22a[4], x22b[4];
       unpack4(t[0][0], x11a); unpack4(t[0][1], x11b); unpack4(t[0][2], x12a); unpack4(t[0][3], x12b);
       unpack4(t[1][0], x21a); unpack4(t[1][1], x21b); unpack4(t[1][2], x22a); unpack4(t[1][3], x22b);
-      k1_core<SCHEME, YK>(L2, L2.nodes[n], r2, c2, x11a, x11b, x12a, x12b, x21a, x21b, x22a, x22b);
+      k1_core<SCHEME, YK, true, D2 ? 7 : 0>(L2, L2.nodes[n], r2, c2, x11a, x11b, x12a, x12b, x21a, x21b, x22a, x22b);
     }
   }
 }
@@ -726,10 +772,23 @@ cudaError_t launch_preadd2(const PreParams &l1, const PreParams &l2, cudaStream_
   p.l2 = l2;
   const int64_t threads = l1.kh / 16;   // kq / 4 column groups
   dim3 grid((unsigned)((threads + 255) / 256), (unsigned)std::min<int64_t>(l2.mh, 65535), 1);
-  if (l1.scheme == 0) { if (l1.ykind == 0) preadd2_kernel<0, 0><<<grid, 256, 0, s>>>(p); else preadd2_kernel<0, 1><<<grid, 256, 0, s>>>(p); }
-  else if (l1.scheme == 1) { if (l1.ykind == 0) preadd2_kernel<1, 0><<<grid, 256, 0, s>>>(p); else preadd2_kernel<1, 1><<<grid, 256, 0, s>>>(p); }
-  else if (l1.scheme == 2) { if (l1.ykind == 0) preadd2_kernel<2, 0><<<grid, 256, 0, s>>>(p); else preadd2_kernel<2, 1><<<grid, 256, 0, s>>>(p); }
+  // the depth-2 instance when the operand sets are exactly those (host-side check of the layout)
+  bool d2 = l1.n_nodes == 1 && l2.n_nodes == 3 && l1.nodes[0].s3 == nullptr;
+  for (int o = 0; o < OUT_N && d2; ++o) d2 = (l1.nodes[0].op_row[o] >= 0) == (o < 4);
+  for (int n = 0; n < l2.n_nodes && d2; ++n) {
+    d2 = l2.nodes[n].s3 == nullptr;
+    for (int o = 0; o < OUT_N && d2; ++o) d2 = l2.nodes[n].op_row[o] >= 0;
+  }
+#define P2(S, Y)                                                                   \
+  do {                                                                             \
+    if (d2) preadd2_kernel<S, Y, true><<<grid, 256, 0, s>>>(p);                    \
+    else preadd2_kernel<S, Y, false><<<grid, 256, 0, s>>>(p);                      \
+  } while (0)
+  if (l1.scheme == 0) { if (l1.ykind == 0) P2(0, 0); else P2(0, 1); }
+  else if (l1.scheme == 1) { if (l1.ykind == 0) P2(1, 0); else P2(1, 1); }
+  else if (l1.scheme == 2) { if (l1.ykind == 0) P2(2, 0); else P2(2, 1); }
   else return cudaErrorInvalidValue;
+#undef P2
   return cudaGetLastError();
 }
 
