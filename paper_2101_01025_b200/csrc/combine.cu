@@ -40,6 +40,18 @@ __device__ __forceinline__ void store8(OutT *o, int64_t ncols_ok, const uint32_t
   }
 }
 
+// store8 of 8 in-range residues at a 16-byte aligned position (the FULL instance)
+template <typename OutT>
+__device__ __forceinline__ void store8_full(OutT *o, const uint32_t (&v)[8]) {
+  if constexpr (sizeof(OutT) == 4) {
+    __stcs(reinterpret_cast<uint4 *>(o), make_uint4(v[0], v[1], v[2], v[3]));
+    __stcs(reinterpret_cast<uint4 *>(o) + 1, make_uint4(v[4], v[5], v[6], v[7]));
+  } else {
+    *reinterpret_cast<uint4 *>(o) =
+        make_uint4(v[0] | (v[1] << 16), v[2] | (v[3] << 16), v[4] | (v[5] << 16), v[6] | (v[7] << 16));
+  }
+}
+
 // 8 residues of a product buffer, kept packed until used (u16: one uint4; u32: two)
 template <typename InT> struct Pk8;
 template <> struct Pk8<uint16_t> {
@@ -65,7 +77,10 @@ template <> struct Pk8<uint32_t> {
 // blocks (OutT, leading dimension ldo), where the children and the root leaf wrote them.  Each
 // thread writes only positions it has itself read above (C11 / C21 / C22 on L over its P1 / P3 /
 // P5 loads, C21 on U over its P3 load), so the in-place update needs no extra ordering.
-template <typename InT, typename OutT, int T, bool INPL = false>
+// FULL (host-checked in launch_combine): mh a multiple of T, every node's output covers its
+// 2 mh x 2 mh positions with 16-byte aligned rows, no SYRK form: off-diagonal pairs then need no
+// bounds, masks or diagonal selects (the generic path below still runs the diagonal pairs).
+template <typename InT, typename OutT, int T, bool INPL = false, bool FULL = false>
 __global__ void __launch_bounds__(T * T / 16) combine_kernel(const __grid_constant__ CombParams P) {
   constexpr int TX = T / 8, H = T / 2;   // TX threads of 8 columns per row; rows ty and ty + H
   const CombNode &N = P.nodes[blockIdx.y];
@@ -129,6 +144,43 @@ __global__ void __launch_bounds__(T * T / 16) combine_kernel(const __grid_consta
   __syncthreads();
   OutT *O = static_cast<OutT *>(N.out);
   const int64_t ov = N.out_valid;
+  if constexpr (FULL) {
+    if (!diag) {
+      const int64_t ldo = N.ldo;
+#pragma unroll
+      for (int rr = 0; rr < 2; ++rr) {   // tile L: C21 = U1 + P4 + P3, C22 = U1 + P4 + P4^T, C11 = P1 + P2
+        const int y = ty + H * rr;
+        const int64_t i = i0 + y, j = j0 + cx;
+        uint32_t p4[8], p3[8], p1[8], p2[8], c21[8], c22[8], c11[8];
+        l4[rr].get(p4);
+        l3[rr].get(p3);
+        l1[rr].get(p1);
+        l2[rr].get(p2);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const uint32_t u2 = addmod(u1[rr][e], p4[e], m);
+          c21[e] = addmod(u2, p3[e], m);
+          c22[e] = addmod(u2, sQ[cx + e][y], m);
+          c11[e] = addmod(p1[e], p2[e], m);
+        }
+        store8_full<OutT>(O + (mh + i) * ldo + j, c21);
+        store8_full<OutT>(O + (mh + i) * ldo + mh + j, c22);
+        store8_full<OutT>(O + i * ldo + j, c11);
+      }
+#pragma unroll
+      for (int rr = 0; rr < 2; ++rr) {   // tile U: C21 = Up(U1) + P4 + P3
+        const int y = ty + H * rr;
+        const int64_t r = j0 + y, c = i0 + cx;
+        uint32_t p3[8], q4[8], c21[8];
+        u3[rr].get(p3);
+        u4[rr].get(q4);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) c21[e] = addmod(addmod(sU[cx + e][y], q4[e], m), p3[e], m);
+        store8_full<OutT>(O + (mh + r) * ldo + c, c21);
+      }
+      return;
+    }
+  }
   const bool ax = sizeof(OutT) == 4 && P.axpby;
   // ---- tile L (and, on the diagonal, its upper part of C21)
 #pragma unroll
@@ -200,9 +252,17 @@ cudaError_t launch_combine(const CombParams &p, cudaStream_t s) {
   const unsigned nt = (unsigned)((p.mh + T - 1) / T);
   dim3 grid(p.pairs ? (unsigned)p.n_pairs : nt * (nt + 1) / 2, (unsigned)p.n_nodes), block(T * T / 16);
   if (grid.x == 0) return cudaSuccess;
-#define COMB(I, O)                                                        \
-  if (p.inplace) combine_kernel<I, O, 32, true><<<grid, block, 0, s>>>(p); \
-  else if (T == 64) combine_kernel<I, O, 64><<<grid, block, 0, s>>>(p);  \
+  // FULL instance: no bounds on the off-diagonal pairs (see combine_kernel)
+  const int osz = p.out_u32 ? 4 : 2;
+  bool full = !p.inplace && !p.axpby && p.pairs == nullptr && p.mh % 32 == 0;
+  for (int n = 0; n < p.n_nodes && full; ++n) {
+    const CombNode &N = p.nodes[n];
+    full = N.out_valid >= 2 * p.mh && (N.ldo * osz) % 16 == 0 && (reinterpret_cast<uintptr_t>(N.out) & 15) == 0;
+  }
+#define COMB(I, O)                                                              \
+  if (p.inplace) combine_kernel<I, O, 32, true><<<grid, block, 0, s>>>(p);       \
+  else if (T == 64) combine_kernel<I, O, 64><<<grid, block, 0, s>>>(p);        \
+  else if (full) combine_kernel<I, O, 32, false, true><<<grid, block, 0, s>>>(p); \
   else combine_kernel<I, O, 32><<<grid, block, 0, s>>>(p)
   if (p.in32) COMB(uint32_t, uint32_t);
   else if (p.out_u32) COMB(uint16_t, uint32_t);

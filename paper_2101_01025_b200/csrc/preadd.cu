@@ -203,7 +203,7 @@ __device__ __forceinline__ void st_off32(const int8_t *base, uint32_t off, uint3
 }
 
 // packed plane words of 4 offset residues u = c + (p - 1) / 2 (koff as for put_limbs4_*):
-//   scheme 0: byte 0 of c = u - h;  scheme 1: k7_words;
+//   scheme 0: byte 0 of c = u - h;  scheme 1: as k7_words;
 //   scheme 2: v = u - h + 2^15 = c + 2^15 lies in [0, 2^16), so two of them packed in one word add
 //   without carries between the 16-bit lanes; byte 0 of v is the u8 lo of c, byte 1 is its s8 hi
 //   + 128 (flipped back by the xor)
@@ -213,7 +213,15 @@ __device__ __forceinline__ void limb_words_u(const uint32_t (&u)[4], uint32_t ko
     w[0] = __byte_perm(__byte_perm(u[0] - koff, u[1] - koff, 0x40), __byte_perm(u[2] - koff, u[3] - koff, 0x40),
                        0x5410);
   } else if constexpr (SCHEME == 1) {
-    k7_words(u, koff, w);
+    // k7_words with v = c + 64 + 2^15 (koff + 2^15 - 128 * 66): v >> 7 = hi + 256 and v & 127 =
+    // lo + 64, so the hi bytes need no constant and hi + lo stays inside its 16-bit lane
+    const uint32_t K = (koff + 32768u - 128u * 66u) * 0x10001u;
+    const uint32_t v01 = (u[0] + (u[1] << 16)) + K, v23 = (u[2] + (u[3] << 16)) + K;
+    const uint32_t h01 = (v01 >> 7) & 0x00FF00FFu, h23 = (v23 >> 7) & 0x00FF00FFu;
+    const uint32_t l01 = (v01 & 0x007F007Fu) + 0x00C000C0u, l23 = (v23 & 0x007F007Fu) + 0x00C000C0u;
+    w[0] = __byte_perm(h01, h23, 0x6420);
+    w[1] = __byte_perm(l01, l23, 0x6420);
+    w[2] = __byte_perm(h01 + l01, h23 + l23, 0x6420);
   } else {
     const uint32_t K = (0x8000u - koff) * 0x10001u;
     const uint32_t v01 = (u[0] + (u[1] << 16)) + K, v23 = (u[2] + (u[3] << 16)) + K;
