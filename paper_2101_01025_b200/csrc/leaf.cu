@@ -600,11 +600,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (EWN + 3), 1)
       int stage = 0;
       uint32_t phase = 0;
       uint2 next = (!dyn && cid < P.n_tiles) ? __ldg(&P.tiles[cid]) : make_uint2(0u, 0u);
-      int idx2 = 0;
+      int idx2 = 0, idx_d1 = 0;
       uint2 d1 = make_uint2(kEnd, 0u);
-      if (dyn && leader) {
+      // claim1: a job is claimed when its loads are about to start (claim order = start order);
+      // otherwise two ahead (claim latency hidden, claim order = start order of the previous job)
+      const bool claim1 = P.gate < 0 || P.gate > 100;
+      const int gate = claim1 ? (P.gate < 0 ? 0 : P.gate - 1000) : P.gate;
+      if (dyn && leader && !claim1) {
         const int idx1 = atomicAdd(P.job_counter, 1);
         idx2 = atomicAdd(P.job_counter, 1);
+        idx_d1 = idx1;
         if (idx1 < P.n_tiles) d1 = __ldg(&P.tiles[idx1]);
       }
       for (int i = 0;; ++i) {
@@ -615,6 +620,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (EWN + 3), 1)
         } else if (leader) {
           const int s = i & (Cfg::JQ - 1);
           ptx::mbar_wait_cluster(&jq_empty[s], ((uint32_t)(i / Cfg::JQ) & 1) ^ 1);
+          if (claim1) {
+            idx_d1 = atomicAdd(P.job_counter, 1);
+            d1 = idx_d1 < P.n_tiles ? __ldg(&P.tiles[idx_d1]) : make_uint2(kEnd, 0u);
+          }
+          if (gate > 0 && d1.x != kEnd && idx_d1 >= ncl) {
+            // claim-wave gate: every dependency is a job of a lower claim index, whose producer
+            // never waits on a higher one, so the wait always ends
+            const int w = idx_d1 / ncl;
+            const int need = min(P.n_tiles, (w - 1) * ncl + (gate * ncl + 99) / 100);
+            const volatile int32_t *done = P.job_counter + 1;
+            while (*done < need) __nanosleep(64);
+          }
           next = d1;
           jq[s] = next;
           const uint32_t peer = ptx::mapa(ptx::smem_u32(&jq[s]), 1);
@@ -623,8 +640,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (EWN + 3), 1)
           ptx::mbar_arrive(&jq_full[s]);
           ptx::mbar_arrive_cluster_release(ptx::mapa(ptx::smem_u32(&jq_full[s]), 1));
           if (next.x == kEnd) break;
-          d1 = idx2 < P.n_tiles ? __ldg(&P.tiles[idx2]) : make_uint2(kEnd, 0u);
-          idx2 = atomicAdd(P.job_counter, 1);
+          if (!claim1) {
+            d1 = idx2 < P.n_tiles ? __ldg(&P.tiles[idx2]) : make_uint2(kEnd, 0u);
+            idx_d1 = idx2;
+            idx2 = atomicAdd(P.job_counter, 1);
+          }
         } else {
           next = job_consume(i, true);
           if (next.x == kEnd) break;
@@ -662,6 +682,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (EWN + 3), 1)
             }
           }
         }
+        if (dyn && leader && P.gate != 0) atomicAdd(P.job_counter + 1, 1);   // this job's loads are issued
       }
     }
   } else if (warp == W_MMA) {

@@ -61,6 +61,11 @@ struct LeafParams {
   int32_t *job_counter;    // dynamic scheduling: next job index (zeroed before the launch); null = static
   int32_t debug;           // diagnostics only (ADJ_LEAF_DEBUG): 1 no TMA, 2 no epilogue, 8 no math, 16 no tcgen05.ld,
                            // 32 no stores, 128 per-role cycle profile, 256 A operand only, 16384 cluster exit times
+  int32_t gate;            // wide leaf, dynamic: claim-wave gate (api.cpp launch_leaf_all): 1000 + g = a job is
+                           // claimed when it starts and claim wave w starts once g % of wave w - 1 has issued
+                           // its loads (job_counter[1] counts them); 1..100 = the same with claims two ahead;
+                           // -1 = claim at start without a gate; 0 = neither
+  int32_t pad_gate;
   ModP mod;
 };
 
