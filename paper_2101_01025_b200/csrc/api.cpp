@@ -382,14 +382,14 @@ adj_status_t launch_leaf_all(const Plan &P, const Ptrs &x, cudaStream_t s) {
   if (force_dynamic || (P.dynamic && !force_static)) {
     L.job_counter = reinterpret_cast<int32_t *>(x.ws + P.counter_offset);
     CUDA_TRY(cudaMemsetAsync(L.job_counter, 0, 2 * sizeof(int32_t), s));   // claims, jobs loaded
-    // Wide leaf: claim-wave gate.  A job is claimed when its loads are about to
+    // Claim-wave gate of the dynamic leaf launch.  A job is claimed when its loads are about to
     // start, and the jobs of claim wave w (claim index / clusters) start only once every job of
     // wave w - 1 has issued its loads, so the tiles that run together walk K together and their
     // operand panels are read from DRAM about once (c3 -5.7%, c4 -11% under the power cap).
     // ADJ_LEAF_GATE (diagnostics, A/B): 0 = off (claims two ahead, no gate); 1..100 = gate % with
     // claims two ahead; 1000 + g = claim at start, gate g %; -1 = claim at start, no gate
     static const int gate = getenv("ADJ_LEAF_GATE") ? atoi(getenv("ADJ_LEAF_GATE")) : 1100;
-    L.gate = P.wide ? gate : 0;
+    L.gate = gate;
   }
   // diagnostics: ADJ_LEAF_GRID caps the persistent grid (CTAs, even; power-regime A/B)
   static const int grid_cap = getenv("ADJ_LEAF_GRID") ? atoi(getenv("ADJ_LEAF_GRID")) & ~1 : 0;

@@ -197,11 +197,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (ADJ_EPI_WARPS 
       const bool prof = (P.debug & 128) != 0;
       long long t_empty = 0, t_tma = 0, t_begin = clock64();
       uint2 next = (!dyn && cid < P.n_tiles) ? __ldg(&P.tiles[cid]) : make_uint2(0u, 0u);
-      int idx2 = 0;
+      int idx2 = 0, idx_d1 = 0;
       uint2 d1 = make_uint2(kEnd, 0u);
-      if (dyn && leader) {
+      // claim-wave gate (as in leafw_kernel; api.cpp launch_leaf_all)
+      const bool claim1 = P.gate < 0 || P.gate > 100;
+      const int gate = claim1 ? (P.gate < 0 ? 0 : P.gate - 1000) : P.gate;
+      if (dyn && leader && !claim1) {
         const int idx1 = atomicAdd(P.job_counter, 1);
         idx2 = atomicAdd(P.job_counter, 1);
+        idx_d1 = idx1;
         if (idx1 < P.n_tiles) d1 = __ldg(&P.tiles[idx1]);
       }
       for (int i = 0;; ++i) {
@@ -212,6 +216,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (ADJ_EPI_WARPS 
         } else if (leader) {
           const int s = i & (Cfg::JQ - 1);
           ptx::mbar_wait_cluster(&jq_empty[s], ((uint32_t)(i / Cfg::JQ) & 1) ^ 1);
+          if (claim1) {
+            idx_d1 = atomicAdd(P.job_counter, 1);
+            d1 = idx_d1 < P.n_tiles ? __ldg(&P.tiles[idx_d1]) : make_uint2(kEnd, 0u);
+          }
+          if (gate > 0 && d1.x != kEnd && idx_d1 >= ncl) {
+            const int w = idx_d1 / ncl;
+            const int need = min(P.n_tiles, (w - 1) * ncl + (gate * ncl + 99) / 100);
+            const volatile int32_t *done = P.job_counter + 1;
+            while (*done < need) __nanosleep(64);
+          }
           next = d1;
           jq[s] = next;
           const uint32_t peer = ptx::mapa(ptx::smem_u32(&jq[s]), 1);
@@ -220,8 +234,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (ADJ_EPI_WARPS 
           ptx::mbar_arrive(&jq_full[s]);
           ptx::mbar_arrive_cluster_release(ptx::mapa(ptx::smem_u32(&jq_full[s]), 1));
           if (next.x == kEnd) break;
-          d1 = idx2 < P.n_tiles ? __ldg(&P.tiles[idx2]) : make_uint2(kEnd, 0u);   // used next iteration
-          idx2 = atomicAdd(P.job_counter, 1);                                     // claimed for i + 2
+          if (!claim1) {
+            d1 = idx2 < P.n_tiles ? __ldg(&P.tiles[idx2]) : make_uint2(kEnd, 0u);   // used next iteration
+            idx_d1 = idx2;
+            idx2 = atomicAdd(P.job_counter, 1);                                     // claimed for i + 2
+          }
         } else {
           next = job_consume(i, true);
           if (next.x == kEnd) break;
@@ -273,6 +290,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (ADJ_EPI_WARPS 
             }
           }
         }
+        if (dyn && leader && P.gate != 0) atomicAdd(P.job_counter + 1, 1);   // this job's loads are issued
       }
       if (prof && (cid == 0 || cid == ncl / 2))
         printf("[leaf prof] cluster %d rank %u producer: total %lld cyc, empty-wait %lld, tma-issue %lld\n", cid,
