@@ -376,6 +376,11 @@ adj_status_t launch_leaf_all(const Plan &P, const Ptrs &x, cudaStream_t s) {
   L.n_tiles = (int32_t)(P.tiles.size() / 2);
   L.fixup = x.ws + P.fixup_offset;
   if (const char *dbg = getenv("ADJ_LEAF_DEBUG")) L.debug = atoi(dbg);   // diagnostics only
+  // K-direction alternation of a job's units, for the s8 / u8 scheme only, whose
+  // consecutive accumulators share operand planes (c3 -1.2%; the K7 scheme's do not: c4 +0.3%);
+  // ADJ_LEAF_KALT (diagnostics): 0 off, 2 every scheme
+  static const int kalt = getenv("ADJ_LEAF_KALT") ? atoi(getenv("ADJ_LEAF_KALT")) : 1;
+  L.kalt = (kalt == 2 || (kalt == 1 && P.scheme == LIMB_SU8)) ? 1 : 0;
   // diagnostics: ADJ_LEAF_STATIC / ADJ_LEAF_DYNAMIC force the job scheduler (A/B measurements)
   static const bool force_static = getenv("ADJ_LEAF_STATIC") != nullptr;
   static const bool force_dynamic = getenv("ADJ_LEAF_DYNAMIC") != nullptr;

@@ -268,8 +268,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (ADJ_EPI_WARPS 
           const int ar0 = arow + P.terms[t0].a_plane * a_pr, br0 = brow + P.terms[t0].b_plane * b_pr;
           const int ar1 = nt > 1 ? arow + P.terms[t0 + 1].a_plane * a_pr : ar0;
           const int br1 = nt > 1 ? brow + P.terms[t0 + 1].b_plane * b_pr : br0;
+          const bool rev = P.kalt && (u & 1);   // odd units walk K backwards (as in leafw_kernel)
 #pragma unroll 1
-          for (int kb = kb0; kb < kb1; ++kb) {
+          for (int x = 0; x < kb1 - kb0; ++x) {
+            const int kb = rev ? kb1 - 1 - x : kb0 + x;
 #pragma unroll 1
             for (int tt = 0; tt < nt; ++tt) {
               long long c0 = prof ? clock64() : 0;
@@ -685,8 +687,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (EWN + 3), 1)
           const int ar0 = arow + P.terms[t0].a_plane * a_pr, br0 = brow + P.terms[t0].b_plane * b_pr;
           const int ar1 = nt > 1 ? arow + P.terms[t0 + 1].a_plane * a_pr : ar0;
           const int br1 = nt > 1 ? brow + P.terms[t0 + 1].b_plane * b_pr : br0;
+          // odd units walk K backwards: a unit starts on the k-blocks the previous one loaded last
+          const bool rev = P.kalt && (u & 1);
 #pragma unroll 1
-          for (int kb = kb0; kb < kb1; ++kb) {
+          for (int x = 0; x < kb1 - kb0; ++x) {
+            const int kb = rev ? kb1 - 1 - x : kb0 + x;
 #pragma unroll 1
             for (int tt = 0; tt < nt; ++tt) {
               ptx::mbar_wait(&empty_bar[stage], phase ^ 1);

@@ -63,6 +63,20 @@ static void fill_scheme(Plan &P, uint32_t p) {
   } else {
     // x y = 2^16 hh + 2^8 (hl + lh) + ll ; hi signed, lo unsigned
     L.n_terms = 4;
+    // accumulator order hh, (hl + lh), ll: with the K direction alternating per unit, the mixed
+    // sweep (all four planes) starts on the hi planes hh just loaded and ll on the lo planes the
+    // mixed sweep loaded last (c3 -0.95%); ADJ_ACC_ORDER=0 (diagnostics): hh, ll, mixed
+    static const bool mixed_mid = !(getenv("ADJ_ACC_ORDER") && !atoi(getenv("ADJ_ACC_ORDER")));
+    if (mixed_mid) {
+      L.terms[0] = {0, 0, 0, 1, 1, {0, 0, 0}};   // hh  s8 x s8
+      L.terms[1] = {1, 0, 1, 1, 0, {0, 0, 0}};   // hl  s8 x u8
+      L.terms[2] = {1, 1, 0, 0, 1, {0, 0, 0}};   // lh  u8 x s8
+      L.terms[3] = {2, 1, 1, 0, 0, {0, 0, 0}};   // ll  u8 x u8
+      L.acc_begin[0] = 0; L.acc_begin[1] = 1; L.acc_begin[2] = 3; L.acc_begin[3] = 4;
+      L.weight[0] = pw(16);
+      L.weight[1] = pw(8);
+      L.weight[2] = 1 % p;
+    } else {
     L.terms[0] = {0, 0, 0, 1, 1, {0, 0, 0}};   // hh  s8 x s8
     L.terms[1] = {1, 1, 1, 0, 0, {0, 0, 0}};   // ll  u8 x u8
     L.terms[2] = {2, 0, 1, 1, 0, {0, 0, 0}};   // hl  s8 x u8
@@ -71,6 +85,7 @@ static void fill_scheme(Plan &P, uint32_t p) {
     L.weight[0] = pw(16);
     L.weight[1] = 1 % p;
     L.weight[2] = pw(8);
+    }
   }
   for (int j = 0; j < 6; ++j) L.wshoup[j] = make_shoup(L.weight[j], p);
 }

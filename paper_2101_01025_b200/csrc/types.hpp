@@ -65,7 +65,8 @@ struct LeafParams {
                            // claimed when it starts and claim wave w starts once g % of wave w - 1 has issued
                            // its loads (job_counter[1] counts them); 1..100 = the same with claims two ahead;
                            // -1 = claim at start without a gate; 0 = neither
-  int32_t pad_gate;
+  int32_t kalt;            // odd units of a job walk K backwards (a unit starts on the k-blocks the previous
+                           // one loaded last, still in L2); api.cpp launch_leaf_all
   ModP mod;
 };
 
