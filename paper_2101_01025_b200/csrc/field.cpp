@@ -93,7 +93,8 @@ int limb_accs(LimbScheme s) { return s == LIMB_S8 ? 1 : (s == LIMB_T6 ? 6 : 3); 
 
 static int64_t limb_kmax_lim(LimbScheme s, uint32_t p, int64_t lim);
 int64_t limb_kmax(LimbScheme s, uint32_t p) { return limb_kmax_lim(s, p, 2147483647); }
-int64_t limb_kmax_from_residue(LimbScheme s, uint32_t p) { return limb_kmax_lim(s, p, 2147483647 - (int64_t)p); }
+// accumulations that start from a lazy Horner value < 3p (modp.cuh mulred_lazy3)
+int64_t limb_kmax_from_residue(LimbScheme s, uint32_t p) { return limb_kmax_lim(s, p, 2147483647 - 3 * (int64_t)p); }
 
 static int64_t limb_kmax_lim(LimbScheme s, uint32_t p, int64_t lim) {
   int64_t c = (p - 1) / 2;                       // centered |x| <= c

@@ -848,10 +848,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (EWN + 3), 1)
           const uint32_t taddr = tmem_base + lane_off + h * 256 + (part * NCH + c) * 32;
           ptx::tmem_ld32(taddr, v);
           ptx::tmem_wait_ld();
+          if (last) {
 #pragma unroll
-          for (int e = 0; e < 32; ++e) v[e] = acc_mulred((int32_t)v[e], w.wc, w.wq, 0u, pm);
-          if (last) store_chunk(pr, row, col0 + c * 32, v, mod);
-          else ptx::tmem_st32(taddr, v);
+            for (int e = 0; e < 32; ++e) v[e] = acc_mulred((int32_t)v[e], w.wc, w.wq, 0u, pm);
+            store_chunk(pr, row, col0 + c * 32, v, mod);
+          } else {   // intermediate Horner step: a value < 3p stays in TMEM (modp.cuh mulred_lazy3)
+#pragma unroll
+            for (int e = 0; e < 32; ++e) v[e] = mulred_lazy3((int32_t)v[e], w.wc, w.wq, pm);
+            ptx::tmem_st32(taddr, v);
+          }
         }
         if (!last) ptx::tmem_wait_st();
         ptx::tc_fence_before();

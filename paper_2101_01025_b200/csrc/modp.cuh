@@ -112,6 +112,19 @@ __host__ __device__ __forceinline__ uint32_t acc_mulred(int32_t x, int32_t wc, i
   return umin32(s, s - p);
 }
 
+// The same Shoup step without the final corrections (part = 0): x w mod p + {0, p, 2p}, a value
+// in [0, 3p) (r = x wc - q p lies in [-p, 2p)).  The wide leaf's intermediate Horner steps keep
+// it in TMEM: the next unit accumulates on top of it (K segments bounded for a start < 3p,
+// field.cpp limb_kmax_from_residue), and only the last step of a tile reduces fully.
+__host__ __device__ __forceinline__ uint32_t mulred_lazy3(int32_t x, int32_t wc, int32_t wq, uint32_t p) {
+#ifdef __CUDA_ARCH__
+  const int32_t q = __mulhi(x, wq);
+#else
+  const int32_t q = (int32_t)(((int64_t)x * (int64_t)wq) >> 32);
+#endif
+  return (uint32_t)x * (uint32_t)wc - (uint32_t)q * p + p;
+}
+
 // ---- K1's lazy reduction of the Y products for p > 16763 (preadd.cu) ----------
 // The products' sum v (|v| < 2 p^2 < 2^37 for p < 2^18) is carried exactly mod 2^32 (wrapping
 // uint32 arithmetic) and approximately in float (vf, relative error a few 2^-24).  The float

@@ -177,3 +177,40 @@ def test_k1_s1_s2_reductions(tmp_path):
     want = np.stack([(v + h) % p for v in (s1a, s1b, s2a, s2b)], axis=1)
     bad = np.nonzero((got != want).any(axis=1))[0]
     assert bad.size == 0, (bad.size, R[bad[:5]].tolist(), got[bad[:5]].tolist(), want[bad[:5]].tolist())
+
+
+PROG_LAZY3 = r"""
+#include <cstdio>
+#include "modp.cuh"
+using namespace adj;
+int main() {
+  unsigned p, w; long long x;
+  while (scanf("%u %u %lld", &p, &w, &x) == 3) {
+    ShoupW s = make_shoup(w, p);
+    printf("%u\n", mulred_lazy3((int32_t)x, s.wc, s.wq, p));
+  }
+  return 0;
+}
+"""
+
+
+def test_mulred_lazy3_range_and_residue(tmp_path):
+    """The wide leaf's intermediate Horner step (modp.cuh mulred_lazy3): x w mod p + {0, p, 2p},
+    always in [0, 3p), for every int32 extreme and random x at the scheme boundary primes."""
+    src, exe = tmp_path / "tl.cpp", tmp_path / "tl"
+    src.write_text(PROG_LAZY3)
+    subprocess.run(["g++", "-O2", "-std=c++17", "-I", CSRC, str(src), "-o", str(exe)], check=True)
+    rng = random.Random(11)
+    cases = []
+    xs_fixed = [-2**31, -2**31 + 1, -1, 0, 1, 2**31 - 1, 2**31 - 2, -2**30, 2**30]
+    for p in PRIMES:
+        ws = sorted({0, 1, 2, p - 1, p - 2, (p - 1) // 2, (p + 1) // 2} | {rng.randrange(p) for _ in range(20)})
+        for w in ws:
+            for x in xs_fixed + [rng.randrange(-2**31, 2**31) for _ in range(30)]:
+                cases.append((p, w, x))
+    inp = "".join(f"{p} {w} {x}\n" for p, w, x in cases)
+    out = subprocess.run([str(exe)], input=inp, capture_output=True, text=True, check=True).stdout.split()
+    assert len(out) == len(cases)
+    for (p, w, x), got in zip(cases, out):
+        g = int(got)
+        assert 0 <= g < 3 * p and g % p == (x * w) % p, (p, w, x, g)
