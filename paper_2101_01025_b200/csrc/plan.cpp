@@ -202,14 +202,23 @@ static void choose_wide(Plan &P, int num_sms) {
   LeafParams &L = P.leaf_template;
   for (int j = 0; j < P.nacc; ++j)
     if (L.weight[j] % P.p == 0) return;
-  int64_t nt = 0;
+  int64_t nt = 0, nt_n = 0;   // wide (256 x 512) and 256 x 256 jobs of the launch
   for (const ProductPlan &pp : P.prods) {
-    const int64_t tm = cdiv(pp.lp.out_rows, 256), tn = cdiv(pp.lp.out_cols, 512);
-    for (int64_t I = 0; I < tm; ++I)
+    const int64_t tm = cdiv(pp.lp.out_rows, 256), tn = cdiv(pp.lp.out_cols, 512), tn2 = cdiv(pp.lp.out_cols, 256);
+    for (int64_t I = 0; I < tm; ++I) {
       for (int64_t J = 0; J < tn; ++J)
         if (!pp.lp.sym || J * 512 <= I * 256 + 255) ++nt;
+      for (int64_t J = 0; J < tn2; ++J)
+        if (!pp.lp.sym || J <= I) ++nt_n;
+    }
   }
-  if (env != 2 && nt <= 16 * (int64_t)(num_sms / 2)) return;
+  // Long launches (> 16 waves) always; shorter ones when the wide makespan -- whole waves of jobs
+  // costing 1.74 narrow jobs each (2 x the MACs at ~0.87 of the time per MAC, measured at c2) --
+  // beats the narrow one, whose K-split tail balances to nt_n / clusters (c2 -1.8%, the 6-plane
+  // x131071 -5.5%, c5 equal: profiles/r02/wide_short_launches.txt)
+  const int64_t ncl = std::max(1, num_sms / 2);
+  const bool short_ok = (double)cdiv(nt, ncl) * 1.74 < (double)nt_n / (double)ncl;
+  if (env != 2 && nt <= 16 * ncl && !short_ok) return;
   const int kseg = (int)std::max<int64_t>(1, limb_kmax_from_residue((LimbScheme)P.scheme, P.p) / kBK);
   P.wide = true;
   P.tile_n = 512;

@@ -277,11 +277,14 @@ def test_ipc_validation_needs_no_gpu():
 
 
 def test_leaf_tile_query():
-    """The wide-N leaf (256 x 512 tiles) serves long launches only: c3 / c4 (the metric's configs)
-    use it, c2 and the small configs keep 256 x 256 tiles with their tail balancing."""
+    """The wide-N leaf (256 x 512 tiles) serves long launches (c3 / c4, the metric's configs) and
+    shorter ones whose whole waves of wide jobs beat the narrow tail-balanced makespan (c2 and the
+    6-plane x131071: 4 waves x 1.74 < 7.1); the smallest configs keep 256 x 256 tiles."""
     assert adj.adjprod_modp_leaf_tile(32768, 32768, 65521, 0) == 512       # c3, depth 2
     assert adj.adjprod_modp_leaf_tile(16384, 131072, 8191, 0) == 512      # c4, depth 2
-    assert adj.adjprod_modp_leaf_tile(8192, 8192, 8191, 0) == 256         # c2
+    assert adj.adjprod_modp_leaf_tile(8192, 8192, 8191, 0) == 512         # c2
+    assert adj.adjprod_modp_leaf_tile(8192, 8192, 131071, 0) == 512       # x131071
+    assert adj.adjprod_modp_leaf_tile(2048, 2048, 8191, 0) == 256         # one short wave
     assert adj.adjprod_modp_leaf_tile(256, 256, 97, 0, depth=1) == 256     # c1
     assert adj.adjprod_modp_leaf_tile(0, 5, 97, 0) == 256
     with pytest.raises(adj.AdjError) as e:

@@ -1,0 +1,5 @@
+# Wide-leaf choice by the makespan rule: GPU suite, then same-box A/B against abtmp/libB.so on the
+# configs whose leaf changes (c2, c5, x131071) and two that do not (q5, c1)
+python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
+CFGS="c2 c5 x131071 q5 c1" LIBB=abtmp/libB.so STEPS=20 bash tools/ab_multi.sh
