@@ -145,6 +145,23 @@ def test_overflow_stress_constant(adj, p, c, k, depth):
     assert (G == exp).all()
 
 
+@pytest.mark.parametrize("c", [65521 - 32513, 32760])   # (hi, lo) = (-128, 255) and (127, 248)
+def test_overflow_stress_constant_wide_leaf(adj, c):
+    """Constant A = c on the wide-N leaf with K segmentation: 8192 x 65536 over GF(65521) at depth
+    0 is 272 wide jobs (the 256 x 512 leaf by the makespan rule) whose K = 512 k-blocks run as two
+    segments per accumulator, each starting from the lazy Horner value < 3p the previous unit left
+    in TMEM (modp.cuh mulred_lazy3, field.cpp limb_kmax_from_residue) and accumulating 32768
+    extreme products: C = k c^2 mod p everywhere (SURVEY.md §8(c) pin 4)."""
+    import torch
+    p, m, k = 65521, 8192, 65536
+    assert adj.adjprod_modp_leaf_tile(m, k, p, 0, 0, adj.ADJ_IN_U16 | adj.ADJ_OUT_U16) == 512
+    A = torch.full((m, k), c if c < 32768 else c - 65536, dtype=torch.int16, device="cuda")   # uint16 bits
+    C = adj.adjprod(A, p, depth=0, out16=True)
+    got = (C.to(torch.int32) & 0xFFFF)
+    lo = torch.tril(torch.ones((m, m), dtype=torch.bool, device="cuda"))
+    assert bool((got[lo] == k * c * c % p).all())
+
+
 def test_depth_invariance(adj):
     p = 65521
     A = uniform_matrix(1000, 1500, seed=3, p=p)
