@@ -678,6 +678,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (EWN + 3), 1)
         const int a_pr = pr.a_plane_rows, b_pr = pr.b_plane_rows;
         const int arow = pr.a_row0 + I * 256 + (int)rank * 128;
         const int brow = pr.b_row0 + J * 512 + (int)rank * 128;   // half h: + h * 256
+        // diagonal SYRK tile whose column half 1 lies wholly above its rows: half 0 only.  Dynamic
+        // (gated) launches only: there the early finish waits at the gate and saves energy; in a
+        // static short launch (c2, L2-bound at full clock) the early finishers run ahead into the
+        // next wave and the step got 1.8% slower (profiles/r02/skip_half_ab.txt)
+        const bool skip1 = dyn && pr.sym && J * 512 + 256 > I * 256 + 255;
         const int nseg = (kblocks + kseg - 1) / kseg;
 #pragma unroll 1
         for (int u = 0; u < NACC * nseg; ++u) {
@@ -695,12 +700,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (EWN + 3), 1)
 #pragma unroll 1
             for (int tt = 0; tt < nt; ++tt) {
               ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
-              if (leader) ptx::mbar_expect_tx(&full_bar[stage], 2 * Cfg::STAGE_BYTES);
+              if (leader)
+                ptx::mbar_expect_tx(&full_bar[stage], skip1 ? 2 * (Cfg::A_BYTES + Cfg::B_BYTES) : 2 * Cfg::STAGE_BYTES);
               uint8_t *sa = smem + stage * Cfg::STAGE_BYTES;
               const int br = tt ? br1 : br0;
               ptx::tma_load_2d_2sm(sa, map, kb * kBK, tt ? ar1 : ar0, &full_bar[stage]);
               ptx::tma_load_2d_2sm(sa + Cfg::A_BYTES, map, kb * kBK, br, &full_bar[stage]);
-              ptx::tma_load_2d_2sm(sa + Cfg::A_BYTES + Cfg::B_BYTES, map, kb * kBK, br + 256, &full_bar[stage]);
+              if (!skip1)
+                ptx::tma_load_2d_2sm(sa + Cfg::A_BYTES + Cfg::B_BYTES, map, kb * kBK, br + 256, &full_bar[stage]);
               if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
             }
           }
@@ -731,6 +738,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (EWN + 3), 1)
         const LeafProduct &pr = P.prod[q];
         const int kseg = pr.kseg, kblocks = pr.kblocks;
         const int nseg = (kblocks + kseg - 1) / kseg;
+        const bool skip1 = dyn && pr.sym && J * 512 + 256 > I * 256 + 255;   // half 0 only (as the producer)
 #pragma unroll 1
         for (int u = 0; u < NACC * nseg; ++u, ++unit) {
           const int j = u / nseg, kb0 = (u % nseg) * kseg;
@@ -744,6 +752,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (EWN + 3), 1)
           // the first unit of a job starts from zero; later ones accumulate onto the Horner value
           uint32_t acc0 = u > 0 ? 1u : 0u, acc1 = acc0;
           auto issue = [&](int h, uint32_t sa, uint32_t idesc, uint32_t &acc) {
+            if (h == 1 && skip1) return;
             const uint64_t adesc = ptx::smem_desc_sw128(sa);
             const uint64_t bdesc = ptx::smem_desc_sw128(sa + Cfg::A_BYTES + h * Cfg::B_BYTES);
 #pragma unroll
@@ -840,10 +849,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (EWN + 3), 1)
         const ShoupW w = last ? P.wshoup[j] : ((u + 1) % nseg ? P.one : P.hshoup[j]);
         ptx::mbar_wait(&acc_full[h], unit & 1);
         ptx::tc_fence_after();
-        // a diagonal SYRK tile whose columns all lie above this CTA half's rows needs no drain
-        // of its values, but its TMEM is still released below
+        // a diagonal SYRK tile whose column half 1 lies wholly above its rows ran no half-1 MMAs:
+        // nothing to drain there, but its TMEM is still released below
+        const bool skip = h == 1 && dyn && pr.sym && J * 512 + 256 > I * 256 + 255;
 #pragma unroll 1
-        for (int c = 0; c < NCH; ++c) {
+        for (int c = 0; c < (skip ? 0 : NCH); ++c) {
           uint32_t v[32];
           const uint32_t taddr = tmem_base + lane_off + h * 256 + (part * NCH + c) * 32;
           ptx::tmem_ld32(taddr, v);
@@ -858,7 +868,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (EWN + 3), 1)
             ptx::tmem_st32(taddr, v);
           }
         }
-        if (!last) ptx::tmem_wait_st();
+        if (!last && !skip) ptx::tmem_wait_st();
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive_cluster(empty_remote);
