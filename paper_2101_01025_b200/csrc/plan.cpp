@@ -242,9 +242,11 @@ static void set_grid(Plan &P, int num_sms) {
   const int64_t nt = std::max<int64_t>(1, (int64_t)P.tiles.size() / 2);
   P.grid = 2 * (int)std::min<int64_t>(num_sms / 2, nt);   // CTA pairs
   // dynamic job claiming pays on long launches (clusters drift apart; in-order claiming keeps the
-  // concurrent tiles a contiguous window: c3 / c4 -11..-17% time), static round-robin is ~1%
-  // faster for launches of a dozen waves (c2)
-  P.dynamic = nt > 16 * (int64_t)(num_sms / 2);
+  // concurrent tiles a contiguous window: c3 / c4 -11..-17% time); for the 256 x 256 leaf static
+  // round-robin was ~1% faster on launches of a dozen waves (c2, before the gate), and the
+  // wide launches always claim dynamically, so the claim-wave gate keeps their tiles in step
+  // (short ones too: c2 -1.2%, c5 -5.3%, x131071 -1.9% against static)
+  P.dynamic = P.wide || nt > 16 * (int64_t)(num_sms / 2);
   P.segmented = false;
   for (const ProductPlan &pp : P.prods) P.segmented |= pp.lp.kblocks > pp.lp.kseg;
 }
