@@ -2,7 +2,7 @@
 # config's bench line, the reference arm, the c3 launch list, ncu --set full of c3 / c4 / c2
 # summarised by tools/ncu_summary.py.  Every step under its own timeout.
 set -x
-OUT=gpurun_out/prof5; mkdir -p $OUT
+OUT=gpurun_out/prof6; mkdir -p $OUT
 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > $OUT/smoke.log 2>&1
 timeout 900 python bench.py > $OUT/bench_c3.log 2>&1
 for c in c4 c2 c5 q5 c1 x131071; do timeout 600 python bench.py --config $c --steps ${STEPS:-10} > $OUT/bench_$c.log 2>&1; done
@@ -12,6 +12,6 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:'lea
 python tools/ncu_summary.py /tmp/full_c3.ncu-rep > $OUT/ncu_full_c3_d2.json 2>&1
 timeout 600 ncu --set full --clock-control none -k regex:'leafw_kernel|preadd2_kernel' -c 2 -o /tmp/full_c4 -f python tools/run_one.py --config c4 --reps 1 --io16 > $OUT/ncu_full_c4.log 2>&1
 python tools/ncu_summary.py /tmp/full_c4.ncu-rep > $OUT/ncu_full_c4_d2.json 2>&1
-timeout 300 ncu --set full --clock-control none -k regex:'leaf2_kernel|split_plain_kernel' -s 2 -c 2 -o /tmp/full_c2 -f python tools/run_one.py --config c2 --depth 0 --reps 2 --io16 > $OUT/ncu_full_c2.log 2>&1
+timeout 300 ncu --set full --clock-control none -k regex:'leafw_kernel|leaf2_kernel|split_plain_kernel' -s 2 -c 2 -o /tmp/full_c2 -f python tools/run_one.py --config c2 --depth 0 --reps 2 --io16 > $OUT/ncu_full_c2.log 2>&1
 python tools/ncu_summary.py /tmp/full_c2.ncu-rep > $OUT/ncu_full_c2_d0.json 2>&1
 du -sh $OUT
