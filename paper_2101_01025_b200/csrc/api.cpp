@@ -381,6 +381,10 @@ adj_status_t launch_leaf_all(const Plan &P, const Ptrs &x, cudaStream_t s) {
   // ADJ_LEAF_KALT (diagnostics): 0 off, 2 every scheme
   static const int kalt = getenv("ADJ_LEAF_KALT") ? atoi(getenv("ADJ_LEAF_KALT")) : 1;
   L.kalt = (kalt == 2 || (kalt == 1 && P.scheme == LIMB_SU8)) ? 1 : 0;
+  // soft claim-wave gate: a gated job issues its first gate_pre stages before it waits,
+  // so its MMAs start as soon as the gate opens (2: c3 -0.7%, c4 -0.6%; ADJ_LEAF_GATE_PRE: diagnostics)
+  static const int gate_pre = getenv("ADJ_LEAF_GATE_PRE") ? atoi(getenv("ADJ_LEAF_GATE_PRE")) : 2;
+  L.gate_pre = std::max(0, gate_pre);
   // diagnostics: ADJ_LEAF_STATIC / ADJ_LEAF_DYNAMIC force the job scheduler (A/B measurements)
   static const bool force_static = getenv("ADJ_LEAF_STATIC") != nullptr;
   static const bool force_dynamic = getenv("ADJ_LEAF_DYNAMIC") != nullptr;

@@ -621,6 +621,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (EWN + 3), 1)
       uint32_t phase = 0;
       uint2 next = (!dyn && cid < P.n_tiles) ? __ldg(&P.tiles[cid]) : make_uint2(0u, 0u);
       int idx2 = 0, idx_d1 = 0;
+      int gate_need = 0;   // soft gate: the wait of the current job, after its first P.gate_pre stages
       uint2 d1 = make_uint2(kEnd, 0u);
       // claim1: a job is claimed when its loads are about to start (claim order = start order);
       // otherwise two ahead (claim latency hidden, claim order = start order of the previous job)
@@ -644,13 +645,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (EWN + 3), 1)
             idx_d1 = atomicAdd(P.job_counter, 1);
             d1 = idx_d1 < P.n_tiles ? __ldg(&P.tiles[idx_d1]) : make_uint2(kEnd, 0u);
           }
+          gate_need = 0;
           if (gate > 0 && d1.x != kEnd && idx_d1 >= ncl) {
             // claim-wave gate: every dependency is a job of a lower claim index, whose producer
             // never waits on a higher one, so the wait always ends
             const int w = idx_d1 / ncl;
             const int need = min(P.n_tiles, (w - 1) * ncl + (gate * ncl + 99) / 100);
-            const volatile int32_t *done = P.job_counter + 1;
-            while (*done < need) __nanosleep(64);
+            if (P.gate_pre > 0) {
+              gate_need = need;   // waited for inside the load loop below
+            } else {
+              const volatile int32_t *done = P.job_counter + 1;
+              while (*done < need) __nanosleep(64);
+            }
           }
           next = d1;
           jq[s] = next;
@@ -684,6 +690,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (EWN + 3), 1)
         // next wave and the step got 1.8% slower (profiles/r02/skip_half_ab.txt)
         const bool skip1 = dyn && pr.sym && J * 512 + 256 > I * 256 + 255;
         const int nseg = (kblocks + kseg - 1) / kseg;
+        int issued = 0;   // stages of this job issued so far (soft gate)
 #pragma unroll 1
         for (int u = 0; u < NACC * nseg; ++u) {
           const int j = u / nseg, kb0 = (u % nseg) * kseg;
@@ -699,6 +706,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (EWN + 3), 1)
             const int kb = rev ? kb1 - 1 - x : kb0 + x;
 #pragma unroll 1
             for (int tt = 0; tt < nt; ++tt) {
+              if (gate_need > 0 && issued++ == P.gate_pre) {   // leader only (gate_need stays 0 elsewhere)
+                const volatile int32_t *done = P.job_counter + 1;
+                while (*done < gate_need) __nanosleep(64);
+                gate_need = 0;
+              }
               ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
               if (leader)
                 ptx::mbar_expect_tx(&full_bar[stage], skip1 ? 2 * (Cfg::A_BYTES + Cfg::B_BYTES) : 2 * Cfg::STAGE_BYTES);

@@ -67,6 +67,8 @@ struct LeafParams {
                            // -1 = claim at start without a gate; 0 = neither
   int32_t kalt;            // odd units of a job walk K backwards (a unit starts on the k-blocks the previous
                            // one loaded last, still in L2); api.cpp launch_leaf_all
+  int32_t gate_pre;        // wide leaf: stages of a gated job issued before its gate wait (soft gate)
+  int32_t pad_gp;
   ModP mod;
 };
 

@@ -44,6 +44,7 @@ VARIANTS = {
     "default": {},
     "no_gate_claim_ahead": {"ADJ_LEAF_GATE": "0"},
     "claim_at_start_no_gate": {"ADJ_LEAF_GATE": "-1"},
+    "hard_gate": {"ADJ_LEAF_GATE_PRE": "0"},
     "kalt_every_scheme_other_order": {"ADJ_LEAF_KALT": "2", "ADJ_ACC_ORDER": "0"},
     "leaf2_gated": {"ADJ_LEAF_WIDE": "0"},
 }
