@@ -195,11 +195,10 @@ __device__ __forceinline__ void put_limbs4_s8u8u(int8_t *base, int64_t plane_str
       __byte_perm(__byte_perm(c0, c1, 0x40), __byte_perm(c2, c3, 0x40), 0x5410);
 }
 
-// 4-byte global store at base + off for a 32-bit off: one IMAD.WIDE.U32 forms the address
-// (a plain pointer add of a uint32 costs two or three 32-bit adds with carries)
-__device__ __forceinline__ void st_off32(const int8_t *base, uint32_t off, uint32_t v) {
-  asm volatile("{\n\t.reg .u64 a;\n\tmad.wide.u32 a, %1, 1, %0;\n\tst.global.u32 [a], %2;\n\t}" ::"l"(base), "r"(off),
-               "r"(v));
+// 8-byte global store of (v0, v1) at base + off for a 32-bit off (8-byte aligned)
+__device__ __forceinline__ void st2_off32(const int8_t *base, uint32_t off, uint32_t v0, uint32_t v1) {
+  asm volatile("{\n\t.reg .u64 a;\n\tmad.wide.u32 a, %1, 1, %0;\n\tst.global.v2.u32 [a], {%2, %3};\n\t}" ::"l"(base),
+               "r"(off), "r"(v0), "r"(v1));
 }
 
 // packed plane words of 4 offset residues u = c + (p - 1) / 2 (koff as for put_limbs4_*):
@@ -544,8 +543,11 @@ __device__ __forceinline__ void k1_core(const PreParams &P, const PreNode &N, in
                           : (SCHEME == 3 ? 133152u - (uint32_t)h : (uint32_t)h);   // (0, 2: h)
     // one row address per call; each operand adds its host-computed byte offset
     int8_t *const rc = P.arena + r * P.kpad + c;
-    // O32: 32-bit thread offsets of the (a, b) column halves in planes 0..2, shared by every operand
-    const uint32_t t0 = O32 ? (uint32_t)(r * P.kpad + c) : 0u, t1 = t0 + (uint32_t)h2;
+    // O32 (the fused K1): the (a, b) column halves c.. and c + kh/2.. of a thread are stored side by
+    // side, one 8-byte word per plane at byte 2c of the row: every limb operand of the level is
+    // written with the same permutation of its K columns (4-column groups of the two halves
+    // interleaved), and the leaf's sums over K do not depend on K order
+    const uint32_t t0 = O32 ? (uint32_t)(r * P.kpad + 2 * c) : 0u;
     const uint32_t pst = (uint32_t)ps;
 #define PUTC(o, A, B)                                                                  \
   if (O32 && SCHEME <= 2 && (NOPS > 0 ? (o) < NOPS : N.op_row[o] >= 0)) {              \
@@ -553,10 +555,8 @@ __device__ __forceinline__ void k1_core(const PreParams &P, const PreNode &N, in
     uint32_t wa[3], wb[3];                                                             \
     limb_words_u<SCHEME>(A, koff, wa);                                                 \
     limb_words_u<SCHEME>(B, koff, wb);                                                 \
-    _Pragma("unroll") for (int pl = 0; pl < (SCHEME == 0 ? 1 : (SCHEME == 1 ? 3 : 2)); ++pl) { \
-      st_off32(ob, t0 + pl * pst, wa[pl]);                                             \
-      st_off32(ob, t1 + pl * pst, wb[pl]);                                             \
-    }                                                                                  \
+    _Pragma("unroll") for (int pl = 0; pl < (SCHEME == 0 ? 1 : (SCHEME == 1 ? 3 : 2)); ++pl) \
+      st2_off32(ob, t0 + pl * pst, wa[pl], wb[pl]);                                    \
   } else if (!(O32 && SCHEME <= 2) && N.op_row[o] >= 0) {                              \
     int8_t *b = rc + N.op_off[o];                                                      \
     if constexpr (SCHEME == 0) {                                                       \
