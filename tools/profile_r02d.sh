@@ -2,8 +2,9 @@
 # config's bench line, the reference arm, the c3 launch list, ncu --set full of c3 / c4 / c2
 # summarised by tools/ncu_summary.py.  Every step under its own timeout.
 set -x
-OUT=gpurun_out/prof6; mkdir -p $OUT
+OUT=gpurun_out/prof7; mkdir -p $OUT
 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > $OUT/smoke.log 2>&1
+timeout 1500 python -m pytest tests -m gpu -x -q > $OUT/pytest_gpu.log 2>&1
 timeout 900 python bench.py > $OUT/bench_c3.log 2>&1
 for c in c4 c2 c5 q5 c1 x131071; do timeout 600 python bench.py --config $c --steps ${STEPS:-10} > $OUT/bench_$c.log 2>&1; done
 timeout 300 python bench.py --impl reference --steps 2 --warmup 1 > $OUT/bench_reference_c3.log 2>&1
