@@ -73,6 +73,23 @@ __device__ __forceinline__ void store_chunk(const LeafProduct &pr, int64_t row, 
   }
 }
 
+// Claim-wave gate wait: until `need` jobs have issued their loads.  The gate only
+// orders job starts (results never depend on it) and cannot deadlock when every CTA of the launch
+// is resident; should CTAs ever be time-sliced (another context, MPS), it gives up after 50 ms
+// instead of waiting on a CTA that is not running.
+__device__ __forceinline__ void gate_wait(const int32_t *counter, int need) {
+  const volatile int32_t *done = counter;
+  if (*done >= need) return;
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while (*done < need) {
+    __nanosleep(64);
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 50000000ull) return;
+  }
+}
+
 // ============================================================================ leaf kernel, CTA pair
 // cta_group::2 version: a cluster of 2 CTAs (one TPC) computes a 256 x 256 tile with
 // tcgen05.mma.cta_group::2 M=256 N=256 K=32 (int8).  CTA r holds rows r*128.. of the A tile and
@@ -223,8 +240,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (ADJ_EPI_WARPS 
           if (gate > 0 && d1.x != kEnd && idx_d1 >= ncl) {
             const int w = idx_d1 / ncl;
             const int need = min(P.n_tiles, (w - 1) * ncl + (gate * ncl + 99) / 100);
-            const volatile int32_t *done = P.job_counter + 1;
-            while (*done < need) __nanosleep(64);
+            gate_wait(P.job_counter + 1, need);
           }
           next = d1;
           jq[s] = next;
@@ -654,8 +670,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (EWN + 3), 1)
             if (P.gate_pre > 0) {
               gate_need = need;   // waited for inside the load loop below
             } else {
-              const volatile int32_t *done = P.job_counter + 1;
-              while (*done < need) __nanosleep(64);
+              gate_wait(P.job_counter + 1, need);
             }
           }
           next = d1;
@@ -707,8 +722,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (EWN + 3), 1)
 #pragma unroll 1
             for (int tt = 0; tt < nt; ++tt) {
               if (gate_need > 0 && issued++ == P.gate_pre) {   // leader only (gate_need stays 0 elsewhere)
-                const volatile int32_t *done = P.job_counter + 1;
-                while (*done < gate_need) __nanosleep(64);
+                gate_wait(P.job_counter + 1, gate_need);
                 gate_need = 0;
               }
               ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
