@@ -540,8 +540,12 @@ def run_gpu(args, cfg, rank, world, local_rank):
 
     # ---------------- end to end through the C ABI with host buffers (pinned), copies timed.
     # A stream of problems: step i copies its A (H2D), runs the C-ABI call, and reads back its
-    # Low(C) row blocks (D2H); three streams, double buffers, so step i's H2D overlaps step
-    # i-1's compute and step i-2's D2H.
+    # Low(C) row blocks (D2H); three streams, three A buffers and two C buffers, so step i's H2D
+    # overlaps step i-1's compute and step i-2's D2H and may start one compute early (at c3 the
+    # H2D of the uint16 A alone takes about as long as the device step; a third A buffer gives the
+    # copy slack against jitter: equal time on a steady box, profiles/r02/e2e_ab.txt).  With the
+    # steady state at max(io_only_ms, device step), the rest of e2e's step is the pipeline's fill
+    # (the first H2D) and drain (the last D2H) spread over the steps.
     def run_e2e(es, eflags):
         """es = bytes per host/device element: 4 (uint32 residues, the headline) or 2 (ADJ_IN_U16 |
         ADJ_OUT_U16, phi = T with p < 2^16: half the PCIe bytes each way)."""
@@ -550,7 +554,8 @@ def run_gpu(args, cfg, rank, world, local_rank):
         hA = torch.empty((m, k * w), dtype=dt, pin_memory=True)
         hA.copy_(A if A.element_size() == es else u32(A))   # residues < 2^16 survive int16 bits
         hC = [torch.empty((m, m * w), dtype=dt, pin_memory=True) for _ in range(2)]
-        dA = [torch.empty((m, k * w), dtype=dt, device=dev) for _ in range(2)]
+        nA = 3
+        dA = [torch.empty((m, k * w), dtype=dt, device=dev) for _ in range(nA)]
         dC = [torch.empty((m, m * w), dtype=dt, device=dev) for _ in range(2)]
         s_in, s_cmp, s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
         nb = 16                                     # Low(C) read back as nb trapezoidal row blocks
@@ -563,28 +568,47 @@ def run_gpu(args, cfg, rank, world, local_rank):
         eflags |= flags & ~(adj.ADJ_IN_U16 | adj.ADJ_OUT_U16)
         wsz = adj.adjprod_modp_workspace_size(m, k, p, phi, depth, eflags)
         wse = ws if wsz <= ws_bytes else torch.empty(wsz, dtype=torch.uint8, device=dev)
+        def d2h(b, stream):
+            for r0, r1 in blocks:   # rows [r0, r1) of Low(C) need columns [0, r1) only
+                memcpy2d_d2h(hC[b].data_ptr() + r0 * m * w * es, m * w * es,
+                             dC[b].data_ptr() + r0 * m * w * es, m * w * es, r1 * w * es, r1 - r0,
+                             stream.cuda_stream)
+
+        # the transfers alone: one step's H2D and D2H on their two streams at once, no compute (the
+        # copy engines' bound for a step; e2e cannot beat max(this, the device step))
+        io = []
+        for _ in range(3):
+            c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            c0.record(s_in)
+            s_out.wait_event(c0)
+            with torch.cuda.stream(s_in):
+                dA[0].copy_(hA, non_blocking=True)
+            d2h(0, s_out)
+            s_in.wait_stream(s_out)
+            c1.record(s_in)
+            torch.cuda.synchronize()
+            io.append(c0.elapsed_time(c1))
+        io_ms = statistics.median(io)
         torch.cuda.synchronize()
         t0.record(s_in)
         for i in range(e2e_steps):
-            b = i % 2
+            b, a = i % 2, i % nA
             with torch.cuda.stream(s_in):
-                if i >= 2:
-                    s_in.wait_event(ev_cmp[i - 2])
-                dA[b].copy_(hA, non_blocking=True)
+                if i >= nA:
+                    s_in.wait_event(ev_cmp[i - nA])
+                dA[a].copy_(hA, non_blocking=True)
                 ev_in[i].record(s_in)
             with torch.cuda.stream(s_cmp):
                 s_cmp.wait_event(ev_in[i])
                 if i >= 2:
                     s_cmp.wait_event(ev_out[i - 2])
-                adj.adjprod_modp_ex(m, k, p, phi, dA[b], k, dC[b], m, depth=depth, flags=eflags,
+                adj.adjprod_modp_ex(m, k, p, phi, dA[a], k, dC[b], m, depth=depth, flags=eflags,
                                     workspace=wse, workspace_bytes=max(wsz, ws_bytes), stream=s_cmp)
                 ev_cmp[i].record(s_cmp)
             with torch.cuda.stream(s_out):
                 s_out.wait_event(ev_cmp[i])
-                for r0, r1 in blocks:   # rows [r0, r1) of Low(C) need columns [0, r1) only
-                    memcpy2d_d2h(hC[b].data_ptr() + r0 * m * w * es, m * w * es,
-                                 dC[b].data_ptr() + r0 * m * w * es, m * w * es, r1 * w * es, r1 - r0,
-                                 s_out.cuda_stream)
+                d2h(b, s_out)
                 ev_out[i].record(s_out)
         s_in.wait_stream(s_out)
         t1.record(s_in)
@@ -597,7 +621,11 @@ def run_gpu(args, cfg, rank, world, local_rank):
                 "h2d_bytes_per_step": hA.numel() * es, "d2h_bytes_per_step": d2h_bytes,
                 "h2d_gbs_per_step_time": hA.numel() * es / (e2e_ms * 1e6),   # PCIe-bound: the copy rate
                 "d2h_gbs_per_step_time": d2h_bytes / (e2e_ms * 1e6),
-                "steps": e2e_steps, "pipelined": "3 streams (H2D | C-ABI call | D2H of Low(C) row blocks), 2 buffers",
+                "steps": e2e_steps,
+                "pipelined": "3 streams (H2D | C-ABI call | D2H of Low(C) row blocks), 3 A and 2 C buffers",
+                "io_only_ms": io_ms,
+                "io_only": "one step's H2D and D2H at once on the same streams, no compute (median of 3)",
+                "bound_ms": max(io_ms, ms), "frac_of_bound": max(io_ms, ms) / e2e_ms,
                 "last_row_matches_device_result": ok}
 
     # The headline e2e moves residues in the narrowest format the public API accepts for this
