@@ -981,6 +981,10 @@ def main():
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        import torch
+        if torch.cuda.device_count() < args.gpus:   # one process per GPU: fail before starting ranks
+            sys.exit(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, "
+                     f"{torch.cuda.device_count()} visible")
         sys.exit(relaunch_torchrun(args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
