@@ -1,0 +1,112 @@
+"""Race detection by repetition (compute-sanitizer is not available on the GPU pool): all
+arithmetic is exact mod p, so whatever order the persistent leaf claims its jobs in, whatever the
+claim-wave gate and the K4 / K5 passes overlap with, every call must return the same bits.  A
+missing barrier, a stage released too early, a job claimed twice or a read of workspace bytes no
+kernel of this call wrote shows up as a run that differs from the first one (or from the
+oracle).  Each repetition starts from a poisoned output and a poisoned caller workspace.
+
+The contract of include/adjprod.h ("concurrent calls on different streams with different
+workspaces") is exercised the same way: two problems interleaved on two streams."""
+import numpy as np
+import pytest
+
+import oracle
+from inputs import uniform_matrix, uniform_matrix_ext, uniform_matrix_quat
+from gpu_util import to_dev, to_host
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def adj():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    import paper_2101_01025_b200 as adj
+    adj.lib()
+    return adj
+
+
+def _gen(phi, m, k, seed, p):
+    return {"T": uniform_matrix, "H": uniform_matrix_ext, "Q": uniform_matrix_quat}[phi](m, k, seed=seed, p=p)
+
+
+def _oracle_rows(phi, A, p, rows):
+    return {"T": oracle.syrk_t, "H": oracle.syrk_h, "Q": oracle.syrk_q}[phi](A, p, rows=rows)
+
+
+# (phi, p, m, k, depth, repetitions, leaf tile width): launches of several waves on 74 CTA pairs,
+# a ragged one, the 3-limb scheme, 2M and 6M.  The last column is adjprod_modp_leaf_tile's answer
+# (asserted below, so the list keeps covering both leaf kernels): 512 = the wide-N leaf with
+# dynamic claiming and the claim-wave gate, 256 = the 256 x 256 leaf with its K-split tail
+CASES = [
+    ("T", 65521, 8192, 8192, 0, 12, 512),
+    ("T", 65521, 8192, 8192, 1, 12, 512),
+    ("T", 8191, 6144, 4096, 2, 12, 512),
+    ("T", 65521, 5000, 3001, 2, 12, 256),
+    ("T", 131071, 4096, 2048, 1, 8, 256),
+    ("H", 8191, 3072, 2048, 1, 8, 512),
+    ("Q", 8191, 2048, 1024, 0, 8, 256),
+]
+
+
+@pytest.mark.parametrize("phi,p,m,k,depth,reps,tile", CASES)
+def test_repeated_calls_bit_identical_poisoned_workspace(adj, phi, p, m, k, depth, reps, tile):
+    import torch
+    ph = {"T": 0, "H": 1, "Q": 2}[phi]
+    assert adj.adjprod_modp_leaf_tile(m, k, p, ph, depth) == tile
+    w = {"T": 1, "H": 2, "Q": 4}[phi]
+    A = _gen(phi, m, k, seed=7 * m + depth, p=p)
+    dA = to_dev(A)
+    ws_bytes = adj.adjprod_modp_workspace_size(m, k, p, ph, depth)
+    ws = torch.empty(max(ws_bytes, 16), dtype=torch.uint8, device="cuda")
+    shape = (m, m) if w == 1 else (m, m, w)
+    first = None
+    for r in range(reps):
+        ws.fill_((0x5A + 37 * r) & 0xFF)                     # stale products of another call
+        C = torch.full(shape, -1, dtype=torch.int32, device="cuda")
+        adj.adjprod_modp_ex(m, k, p, ph, dA, k, C, m, depth=depth, workspace=ws, workspace_bytes=ws_bytes)
+        torch.cuda.synchronize()
+        if first is None:
+            first = C
+            rows = sorted({0, 1, 255, 256, m // 2 - 1, m // 2, m // 2 + 257, m - 2, m - 1})
+            got = to_host(C)
+            for i in rows:                                   # Low(C) rows vs the oracle, Up(C) untouched
+                ref = _oracle_rows(phi, A, p, (i, i + 1))
+                assert np.array_equal(got[i, : i + 1], ref[i, : i + 1]), (phi, p, m, k, depth, i)
+                assert (got[i, i + 1:] == 0xFFFFFFFF).all(), (phi, p, m, k, depth, i)
+        else:
+            assert torch.equal(C, first), f"run {r} differs from run 0: {(C != first).sum().item()} words"
+
+
+def test_two_streams_two_workspaces_interleaved(adj):
+    """Two different problems issued alternately on two streams, each with its own workspace and
+    output (include/adjprod.h: concurrent calls on different streams with different workspaces):
+    every result equals the one the same call gives alone."""
+    import torch
+    probs = [(65521, 4096, 4096, 2), (8191, 3000, 5000, 1)]
+    state = []
+    for p, m, k, depth in probs:
+        A = uniform_matrix(m, k, seed=m + k, p=p)
+        dA = to_dev(A)
+        nb = adj.adjprod_modp_workspace_size(m, k, p, 0, depth)
+        ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+        alone = torch.zeros((m, m), dtype=torch.int32, device="cuda")
+        adj.adjprod_modp_ex(m, k, p, 0, dA, k, alone, m, depth=depth, workspace=ws, workspace_bytes=nb)
+        torch.cuda.synchronize()
+        rows = [0, 255, 256, m // 2, m - 1]
+        got = to_host(alone)
+        for i in rows:
+            ref = oracle.syrk_t(A, p, rows=(i, i + 1))
+            assert np.array_equal(got[i, : i + 1], ref[i, : i + 1])
+        state.append((p, m, k, depth, dA, ws, nb, alone, torch.cuda.Stream()))
+    outs = [[], []]
+    for r in range(6):
+        for j, (p, m, k, depth, dA, ws, nb, alone, s) in enumerate(state):
+            C = torch.zeros((m, m), dtype=torch.int32, device="cuda")
+            s.wait_stream(torch.cuda.current_stream())       # C's zero fill
+            adj.adjprod_modp_ex(m, k, p, 0, dA, k, C, m, depth=depth, workspace=ws, workspace_bytes=nb, stream=s)
+            outs[j].append(C)
+    torch.cuda.synchronize()
+    for j, st in enumerate(state):
+        for r, C in enumerate(outs[j]):
+            assert torch.equal(C, st[7]), f"problem {j}, round {r}: differs from the call run alone"
