@@ -110,3 +110,38 @@ def test_two_streams_two_workspaces_interleaved(adj):
     for j, st in enumerate(state):
         for r, C in enumerate(outs[j]):
             assert torch.equal(C, st[7]), f"problem {j}, round {r}: differs from the call run alone"
+
+
+@pytest.mark.parametrize("name,reps", [("c3", 6), ("c4", 6)])
+def test_full_size_bench_launch_repeats_bit_identical(adj, name, reps):
+    """The metric's configurations in the launch bench.py times (depth 2, uint16 residues, the
+    wide-N leaf with 1840+ jobs claimed dynamically behind the claim-wave gate, board at its power
+    cap): back-to-back calls, each from a poisoned Low(C) and a poisoned workspace, return the same
+    bits.  The first run's values are checked entry by entry in test_gpu_fullsize_exact.py."""
+    import torch
+    import bench
+    from inputs.gpu import uniform_residues_cuda
+    cfg = bench.CONFIGS[name]
+    m, k, p = cfg["m"], cfg["k"], cfg["p"]
+    fl = adj.ADJ_IN_U16 | adj.ADJ_OUT_U16
+    depth = adj.adjprod_modp_auto_depth(m, k, p, 0)
+    assert depth == 2 and adj.adjprod_modp_leaf_tile(m, k, p, 0, depth, fl) == 512
+    A = torch.empty((m, k), dtype=torch.int32, device="cuda")
+    uniform_residues_cuda(A, seed=1, p=p)
+    A16 = A.to(torch.int16)
+    del A
+    nb = adj.adjprod_modp_workspace_size(m, k, p, 0, depth, fl)
+    W = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    first = None
+    for r in range(reps):
+        W.fill_((0xC3 + 29 * r) & 0xFF)
+        C16 = torch.full((m, m), -1, dtype=torch.int16, device="cuda")
+        adj.adjprod_modp_ex(m, k, p, 0, A16, k, C16, m, depth=depth, flags=fl, workspace=W, workspace_bytes=nb)
+        if first is None:
+            first = C16
+        else:
+            assert torch.equal(C16, first), f"{name}: run {r} differs from run 0"
+    i = m - 1                                   # last row: Low(C) row complete, nothing above the diagonal
+    j = 5
+    assert (first[j, j + 1:] == -1).all()       # Up(C) untouched
+    assert int(first[i].to(torch.int32).bitwise_and(0xFFFF).max()) < p
