@@ -145,3 +145,33 @@ def test_full_size_bench_launch_repeats_bit_identical(adj, name, reps):
     j = 5
     assert (first[j, j + 1:] == -1).all()       # Up(C) untouched
     assert int(first[i].to(torch.int32).bitwise_and(0xFFFF).max()) < p
+
+
+@pytest.mark.parametrize("p,m,k,depth,io16", [(65521, 8192, 8192, 2, True), (8191, 6144, 4096, 2, False),
+                                              (65521, 4608, 3000, 3, True)])
+def test_low_memory_schedule_repeats_bit_identical(adj, p, m, k, depth, io16):
+    """ADJ_LOW_MEM: the root's products are formed in C's own blocks and K4 runs in place (every
+    thread overwrites only positions it has read itself), arenas are reused across
+    children.  Repeated from poisoned C and workspace it must return, every time, the grouped
+    schedule's Low(C) bit for bit (which the first loop of this file ties to the oracle)."""
+    import torch
+    A = uniform_matrix(m, k, seed=3 * m + depth, p=p)
+    dt = torch.int16 if io16 else torch.int32
+    dA = torch.from_numpy(A.astype(np.uint16).view(np.int16)).cuda() if io16 else to_dev(A)
+    io = (adj.ADJ_IN_U16 | adj.ADJ_OUT_U16) if io16 else 0
+    ref = torch.full((m, m), -1, dtype=dt, device="cuda")
+    adj.adjprod_modp_ex(m, k, p, 0, dA, k, ref, m, depth=depth, flags=io)
+    torch.cuda.synchronize()
+    got = ref.cpu().numpy().view(np.uint16 if io16 else np.uint32)
+    for i in (0, 255, 256, m // 2 + 1, m - 1):
+        want = oracle.syrk_t(A, p, rows=(i, i + 1))
+        assert np.array_equal(got[i, : i + 1].astype(np.uint32), want[i, : i + 1]), (p, m, k, depth, i)
+    fl = io | adj.ADJ_LOW_MEM
+    nb = adj.adjprod_modp_workspace_size(m, k, p, 0, depth, fl)
+    assert nb < adj.adjprod_modp_workspace_size(m, k, p, 0, depth, io)     # the low-memory schedule applies
+    W = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    for r in range(8):
+        W.fill_((0x3C + 41 * r) & 0xFF)
+        C = torch.full((m, m), -1, dtype=dt, device="cuda")
+        adj.adjprod_modp_ex(m, k, p, 0, dA, k, C, m, depth=depth, flags=fl, workspace=W, workspace_bytes=nb)
+        assert torch.equal(C, ref), f"low-memory run {r}: {(C != ref).sum().item()} entries differ from the grouped schedule"
