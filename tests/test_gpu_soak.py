@@ -78,12 +78,17 @@ def test_repeated_calls_bit_identical_poisoned_workspace(adj, phi, p, m, k, dept
             assert torch.equal(C, first), f"run {r} differs from run 0: {(C != first).sum().item()} words"
 
 
-def test_two_streams_two_workspaces_interleaved(adj):
+# small launches on the 256 x 256 leaf; then two long launches of the wide-N leaf, whose persistent
+# grids (one CTA pair per SM pair each) share the SMs, so the claim-wave gate of either may wait on
+# a job whose CTA is not resident: its wait is bounded and the launch degrades to ungated
+@pytest.mark.parametrize("PROBS", [[(65521, 4096, 4096, 2), (8191, 3000, 5000, 1)],
+                                   [(65521, 8192, 8192, 1), (8191, 6144, 4096, 2)]])
+def test_two_streams_two_workspaces_interleaved(adj, PROBS):
     """Two different problems issued alternately on two streams, each with its own workspace and
     output (include/adjprod.h: concurrent calls on different streams with different workspaces):
     every result equals the one the same call gives alone."""
     import torch
-    probs = [(65521, 4096, 4096, 2), (8191, 3000, 5000, 1)]
+    probs = PROBS
     state = []
     for p, m, k, depth in probs:
         A = uniform_matrix(m, k, seed=m + k, p=p)
