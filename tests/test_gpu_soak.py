@@ -180,3 +180,57 @@ def test_low_memory_schedule_repeats_bit_identical(adj, p, m, k, depth, io16):
         C = torch.full((m, m), -1, dtype=dt, device="cuda")
         adj.adjprod_modp_ex(m, k, p, 0, dA, k, C, m, depth=depth, flags=fl, workspace=W, workspace_bytes=nb)
         assert torch.equal(C, ref), f"low-memory run {r}: {(C != ref).sum().item()} entries differ from the grouped schedule"
+
+
+def test_host_threads_call_concurrently(adj):
+    """include/adjprod.h: calls may come from several host threads (different streams, different
+    workspaces); the plan cache and the workspace pool are locked.  Four threads (ctypes drops the
+    GIL inside the call), each with its own stream and two shapes of its own - so plans are built
+    and inserted while other threads launch - repeat their calls; every result equals the one the
+    same call gave alone on the main thread (tied to the oracle on sampled rows)."""
+    import threading
+    import torch
+    jobs = [(65521, 2304, 1536, 2), (8191, 2000, 3000, 1), (97, 1500, 700, 1), (131071, 1280, 1024, 1),
+            (65521, 1111, 999, 1), (8191, 2560, 2560, 2), (251, 900, 2100, 0), (16763, 1792, 512, 1)]
+    items = []
+    for p, m, k, depth in jobs:
+        A = uniform_matrix(m, k, seed=p + m, p=p)
+        dA = to_dev(A)
+        alone = torch.zeros((m, m), dtype=torch.int32, device="cuda")
+        adj.adjprod_modp_ex(m, k, p, 0, dA, k, alone, m, depth=depth)
+        got = to_host(alone)
+        for i in (0, m // 2, m - 1):
+            ref = oracle.syrk_t(A, p, rows=(i, i + 1))
+            assert np.array_equal(got[i, : i + 1], ref[i, : i + 1]), (p, m, k, depth, i)
+        items.append((p, m, k, depth, dA, alone))
+    torch.cuda.synchronize()
+    errors = []
+
+    def worker(t):
+        try:
+            torch.cuda.set_device(0)
+            s = torch.cuda.Stream()
+            mine = items[2 * t: 2 * t + 2]
+            # new shapes per thread as well: their plans are built under the lock while others launch
+            for r in range(10):
+                for p, m, k, depth, dA, alone in mine:
+                    with torch.cuda.stream(s):
+                        C = torch.zeros((m, m), dtype=torch.int32, device="cuda")
+                        adj.adjprod_modp_ex(m, k, p, 0, dA, k, C, m, depth=depth, stream=s)
+                        mm = m - 128 * (1 + (r + t) % 3)           # a shape only this thread uses
+                        C2 = torch.zeros((mm, mm), dtype=torch.int32, device="cuda")
+                        adj.adjprod_modp_ex(mm, k, p, 0, dA, k, C2, mm, depth=depth, stream=s)
+                    s.synchronize()
+                    if not torch.equal(C, alone):
+                        errors.append(f"thread {t} round {r}: {(p, m, k, depth)} differs")
+                    if not torch.equal(C2, alone[:mm, :mm]):      # leading rows of A give the leading block
+                        errors.append(f"thread {t} round {r}: {(p, mm, k, depth)} differs")
+        except Exception as e:                                     # noqa: BLE001
+            errors.append(f"thread {t}: {type(e).__name__}: {e}")
+
+    threads = [threading.Thread(target=worker, args=(t,)) for t in range(4)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    assert not errors, errors[:5]
