@@ -187,16 +187,37 @@ int query_sms() {
 }
 
 // ------------------------------------------------------------------ plan cache
-// dev, kind, m, n, k, p, phi, depth, shard rank, shard count.  Bounded (LRU): an evicted plan's
-// device tile arrays are released with cudaFree, which waits for the launches that read them.
+// dev, kind, m, n, k, p, phi, depth, shard rank, shard count.  Bounded (LRU over the plans no
+// call holds, see PlanRef): an evicted plan's device tile arrays are released with cudaFree, which
+// waits for the launches that read them.
 using Key = std::tuple<int, int, int64_t, int64_t, int64_t, uint32_t, int, int, int, int>;
 struct CachedPlan {
   std::unique_ptr<Plan> plan;
   uint64_t last_use = 0;
 };
 std::map<Key, CachedPlan> g_plans;
+std::map<const Plan *, int> g_plan_pins;   // plans some call is using right now (guarded by g_mu)
 uint64_t g_plan_clock = 0;
 constexpr size_t kMaxCachedPlans = 64;
+
+// What get_plan hands out: the plan stays pinned -- never evicted, whatever other host threads
+// insert meanwhile -- until the PlanRef goes out of scope or is given another plan.
+struct PlanRef {
+  Plan *p = nullptr;
+  PlanRef() = default;
+  PlanRef(const PlanRef &) = delete;
+  PlanRef &operator=(const PlanRef &) = delete;
+  ~PlanRef() { reset(); }
+  void reset() {
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_plan_pins.find(p);
+    if (it != g_plan_pins.end() && --it->second <= 0) g_plan_pins.erase(it);
+    p = nullptr;
+  }
+  Plan *operator->() const { return p; }
+  Plan &operator*() const { return *p; }
+};
 
 void free_plan_device(Plan &P) {
   if (P.d_tiles) cudaFree(P.d_tiles);
@@ -209,9 +230,12 @@ void free_plan_device(Plan &P) {
 
 void evict_plans() {   // caller holds g_mu
   while (g_plans.size() >= kMaxCachedPlans) {
-    auto lru = g_plans.begin();
+    auto lru = g_plans.end();
     for (auto it = g_plans.begin(); it != g_plans.end(); ++it)
-      if (it->second.last_use < lru->second.last_use) lru = it;
+      if (g_plan_pins.count(it->second.plan.get()) == 0 &&
+          (lru == g_plans.end() || it->second.last_use < lru->second.last_use))
+        lru = it;
+    if (lru == g_plans.end()) return;   // every cached plan is in use: the cache grows past its bound
     int cur = 0;
     cudaGetDevice(&cur);
     cudaSetDevice(lru->second.plan->dev);
@@ -221,14 +245,16 @@ void evict_plans() {   // caller holds g_mu
   }
 }
 
-adj_status_t get_plan(Plan **out, int kind, int64_t m, int64_t n, int64_t k, uint32_t p, int phi, int depth, int dev,
+adj_status_t get_plan(PlanRef *out, int kind, int64_t m, int64_t n, int64_t k, uint32_t p, int phi, int depth, int dev,
                       int sms, int shard_rank = -1, int shard_n = 0) {
+  out->reset();
   std::lock_guard<std::mutex> lk(g_mu);
   Key key{dev, kind, m, n, k, p, phi, depth, shard_rank, shard_n};
   auto it = g_plans.find(key);
   if (it != g_plans.end()) {
     it->second.last_use = ++g_plan_clock;
-    *out = it->second.plan.get();
+    out->p = it->second.plan.get();
+    ++g_plan_pins[out->p];
     return ADJ_OK;
   }
   evict_plans();
@@ -254,7 +280,8 @@ adj_status_t get_plan(Plan **out, int kind, int64_t m, int64_t n, int64_t k, uin
     free_plan_device(*P);
     return fail(ADJ_ERR_CUDA, "plan upload: %s", cudaGetErrorString(e));
   }
-  *out = P.get();
+  out->p = P.get();
+  ++g_plan_pins[out->p];
   CachedPlan cp;
   cp.plan = std::move(P);
   cp.last_use = ++g_plan_clock;
@@ -594,7 +621,7 @@ adj_status_t run_lowmem(const Plan &R, const InView &root, const Ptrs &x, int de
   // the three recursive products, each an ordinary call one level shallower
   // whose workspace reuses the root's arena region: P1 = X11 X11^T -> C11, P2 = X12 X12^T ->
   // buffer, P5 = S3 S3^T -> C22 (Low parts only)
-  Plan *Q = nullptr;
+  PlanRef Q;
   if ((st = get_plan(&Q, PLAN_SYRK_T, L.mh, L.mh, L.kh, R.p, 0, R.lm_depth - 1, dev, sms)) != ADJ_OK) return st;
   if (Q->ws_bytes > R.lm_child_ws) return fail(ADJ_ERR_WORKSPACE, "low-memory child workspace");
   const size_t eb = (x.res16 && !R.res32) ? 2 : 4;
@@ -922,7 +949,7 @@ static adj_status_t adjprod_impl(int64_t m, int64_t k, uint32_t p, adj_phi_t phi
   const bool lowmem = (flags & ADJ_LOW_MEM) && lm_applies;
   if (lowmem && !lm_aligned)
     return fail(ADJ_ERR_INVALID_VALUE, "ADJ_LOW_MEM needs C 16-byte aligned and ldc %% 8 == 0");
-  Plan *P = nullptr;
+  PlanRef P;
   const int kind = herk1 ? PLAN_HERK1
                    : lowmem ? PLAN_LOWMEM
                    : (phi == ADJ_PHI_T ? PLAN_SYRK_T : (phi == ADJ_PHI_H ? PLAN_SYRK_H : PLAN_QUAT));
@@ -963,7 +990,7 @@ static adj_status_t adjprod_impl(int64_t m, int64_t k, uint32_t p, adj_phi_t phi
   return st;
 }
 
-static adj_status_t shard_plan(Plan **out, int64_t m, int64_t k, uint32_t p, int depth, int rank, int nranks, int dev,
+static adj_status_t shard_plan(PlanRef *out, int64_t m, int64_t k, uint32_t p, int depth, int rank, int nranks, int dev,
                                int sms) {
   return get_plan(out, PLAN_SYRK_T, m, m, std::max<int64_t>(k, 1), p, 0, depth, dev, sms, rank, nranks);
 }
@@ -989,7 +1016,7 @@ adj_status_t adjprod_modp_shard(int64_t m, int64_t k, uint32_t p, adj_phi_t phi,
   int dev, sms;
   if ((st = check_device(&dev, &sms)) != ADJ_OK) return st;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  Plan *P = nullptr;
+  PlanRef P;
   if ((st = shard_plan(&P, m, k, p, depth, rank, nranks, dev, sms)) != ADJ_OK) return st;
   if (P->shard_rects.empty()) return ADJ_OK;   // more ranks than tile pairs: this rank owns nothing
   if (k == 0) {   // Low(C) = 0 on the owned regions: one launch over the region list
@@ -1055,7 +1082,7 @@ adj_status_t adjprod_modp_partial(int64_t m, int64_t k, uint32_t p, adj_phi_t ph
   }
   const int depth = (opts && opts->depth >= 0) ? opts->depth : auto_depth(m, k, p, 0);
   if (depth > 3) return fail(ADJ_ERR_INVALID_VALUE, "depth %d > 3 unsupported", depth);
-  Plan *P = nullptr;
+  PlanRef P;
   if ((st = get_plan(&P, PLAN_SYRK_T, m, m, k, p, 0, depth, dev, sms)) != ADJ_OK) return st;
   Ptrs x;
   x.A = A; x.lda = lda;
@@ -1175,7 +1202,7 @@ adj_status_t gemm_modp(int64_t m, int64_t n, int64_t k, uint32_t p, const uint32
     CUDA_TRY(cudaMemset2DAsync(C, (size_t)ldc * 4, 0, (size_t)n * 4, (size_t)m, s));
     return ADJ_OK;
   }
-  Plan *P = nullptr;
+  PlanRef P;
   if ((st = get_plan(&P, PLAN_GEMM, m, n, k, p, 0, 0, dev, sms)) != ADJ_OK) return st;
   void *ws = nullptr;
   CUDA_TRY(adj_pool_alloc(&ws, P->ws_bytes, s));

@@ -234,3 +234,20 @@ def test_host_threads_call_concurrently(adj):
     for th in threads:
         th.join()
     assert not errors, errors[:5]
+
+
+def test_plan_cache_eviction_over_many_shapes(adj):
+    """More distinct shapes than the plan cache holds (64, LRU over the plans no call is using):
+    plans are evicted, their device tile lists freed and rebuilt on the next use; every call,
+    before and after its plan's eviction, matches the oracle on the whole Low(C)."""
+    p = 8191
+    shapes = [(130 + 3 * i, 64 + (i % 5) * 32, i % 2) for i in range(80)]
+    As = {}
+    for rnd in range(2):
+        for m, k, depth in shapes + shapes[:10]:
+            if (m, k) not in As:
+                A = uniform_matrix(m, k, seed=m * 1000 + k, p=p)
+                As[(m, k)] = (to_dev(A), oracle.syrk_t(A, p))
+            dA, ref = As[(m, k)]
+            C = adj.adjprod(dA, p, depth=depth)
+            assert np.array_equal(to_host(C), ref), (rnd, m, k, depth)
