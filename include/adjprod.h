@@ -39,7 +39,8 @@
  *   at a later synchronisation, as in cuBLAS.  adj_last_error() gives a thread-local detail
  *   string for the last failing call on the calling thread.
  * - Thread safety: entry points may be called concurrently from several host threads on
- *   different streams with different workspaces; the internal plan cache is locked.
+ *   different streams with different workspaces; the internal plan cache is locked, bounded
+ *   (64 plans per process, least recently used first) and never evicts a plan a call is using.
  */
 #ifndef ADJPROD_H
 #define ADJPROD_H
